@@ -1,0 +1,74 @@
+/*
+ * synth_cpu.c -- host side of the synthetic-input generator (see synth_core.h).
+ * Test / bench infrastructure: produces X row ranges bit-identical to
+ * synth_gpu.cu.  Compile with -ffp-contract=off (no FMA contraction).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include "synth_core.h"
+
+/* Philox known-answer access for tests. */
+void synth_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  syn_u32x4 r = syn_philox(ctr[0], ctr[1], ctr[2], ctr[3], key[0], key[1]);
+  for (int i = 0; i < 4; ++i) out[i] = r.v[i];
+}
+
+double synth_normal(uint64_t seed, uint32_t stream, uint64_t idx) {
+  return syn_normal(seed, stream, idx);
+}
+double synth_log(double x) { return syn_log(x); }
+double synth_cos2pi(double u) { return syn_cos2pi(u); }
+
+/* Row factor rows [begin, begin+count) x k, or column factor (which=1). */
+void synth_factor(int recipe, uint64_t seed, int which, int64_t begin, int64_t count,
+                  int k, float* out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < count; ++r)
+    for (int c = 0; c < k; ++c)
+      out[r * k + c] = which == 0 ? syn_rowf(recipe, seed, (uint64_t)(begin + r), k, c)
+                                  : syn_colf(recipe, seed, (uint64_t)(begin + r), k, c);
+}
+
+/* max over all (i,j) of S_ij = A_i . B_j (IMAGE normalisation, reading R21). */
+double synth_smax(int recipe, uint64_t seed, int64_t m, int64_t n, int k) {
+  float* A = (float*)malloc(sizeof(float) * (size_t)m * k);
+  float* B = (float*)malloc(sizeof(float) * (size_t)n * k);
+  synth_factor(recipe, seed, 0, 0, m, k, A);
+  synth_factor(recipe, seed, 1, 0, n, k, B);
+  double best = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : best)
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double s = syn_dot(A + i * k, B + j * k, k);
+      if (s > best) best = s;
+    }
+  free(A);
+  free(B);
+  return best;
+}
+
+/* X rows [row_begin, row_begin+row_count) of an m x n matrix into out (ld = ldo). */
+int synth_x_rows(int recipe, uint64_t seed, int64_t m, int64_t n, int k, double noise,
+                 double smax, int64_t row_begin, int64_t row_count, float* out, int64_t ldo) {
+  if (row_begin < 0 || row_count < 0 || row_begin + row_count > m || ldo < n) return -1;
+  float* A = NULL;
+  float* B = NULL;
+  if (recipe != SYN_RATINGS) {
+    A = (float*)malloc(sizeof(float) * (size_t)(row_count > 0 ? row_count : 1) * k);
+    B = (float*)malloc(sizeof(float) * (size_t)n * k);
+    synth_factor(recipe, seed, 0, row_begin, row_count, k, A);
+    synth_factor(recipe, seed, 1, 0, n, k, B);
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < row_count; ++r) {
+    uint64_t i = (uint64_t)(row_begin + r);
+    for (int64_t j = 0; j < n; ++j) {
+      double s = recipe == SYN_RATINGS ? 0.0 : syn_dot(A + r * k, B + j * k, k);
+      out[r * ldo + j] = syn_x_from_s(recipe, seed, i, (uint64_t)j, (uint64_t)n, s, noise, smax);
+    }
+  }
+  free(A);
+  free(B);
+  return 0;
+}
