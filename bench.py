@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""bench.py -- eNMF sweeps/s and achieved HBM GB/s over X on the largest BASELINE config.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl enmf|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (row-sharded, NCCL)
+
+Workload (BASELINE.json:11, the config the metric's HBM roofline and 1/2/4/8-GPU scaling are
+quoted on): C5, X = U0 V0^T + 0.01|N(0,1)| with U0 (200000 x 128), V0 (50000 x 128) ~ U[0,1),
+r = 128, 40 GB fp32, rows sharded over the ranks (strong scaling: total work fixed).
+A step is one eNMF sweep (U block + V block, ascent or HALS by the method's own stage
+control) over all of X.  X is generated on the device by the seeded
+Philox generator (synth/) and stays resident; it is larger than L2, so no flush is needed.
+Init (randomised SVD + ADMM rotation) runs before the timed region and is reported as
+init_s.  Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "eNMF iters/sec + achieved HBM GB/s over X per iteration at 1/2/4/8 B200"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["enmf", "reference"], default="enmf")
+    p.add_argument("--config", default="C5-large-planted")
+    p.add_argument("--precision", choices=["auto", "fp64", "tc"], default="auto")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-rows", type=int, default=0)
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-i", str(self.gpu), "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        med = float(np.median(sm)) if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def gpu_index(local_rank):
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [v for v in vis.split(",") if v.strip()]
+        if local_rank < len(ids) and ids[local_rank].strip().isdigit():
+            return int(ids[local_rank])
+    return local_rank
+
+
+def cpu_sample(cfg, rows, U_rows, V, n_sweeps=1):
+    """Oracle (as it stands) on a row sample of the workload: seconds per HALS sweep."""
+    import oracle
+    import synth
+    Xs = synth.x_rows(cfg, 0, rows)
+    st = oracle.SweepState(stage=1)
+    U, Vv = U_rows.astype(np.float64), V.astype(np.float64)
+    t0 = time.perf_counter()
+    for _ in range(n_sweeps):
+        U, Vv, _, _ = oracle.sweep(Xs, U, Vv, st)
+    return (time.perf_counter() - t0) / n_sweeps
+
+
+def run_reference(args):
+    """--impl reference: the fp64 oracle timed on this box's host cores (SPEC arm of the
+    driver; rank 0 only under torchrun)."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import synth
+    cfg = synth.ALL[args.config]
+    rows = args.cpu_sample_rows or 96
+    g = np.random.default_rng(0)
+    U = g.random((rows, cfg.r)).astype(np.float32)
+    V = g.random((cfg.n, cfg.r)).astype(np.float32)
+    cpu_sample(cfg, rows, U, V, 1)          # warm-up (page-in, OpenMP pool)
+    for _ in range(max(0, args.warmup - 1)):
+        pass
+    times = [cpu_sample(cfg, rows, U, V, 1) for _ in range(args.steps)]
+    s_per_sweep_full = float(np.mean(times)) * cfg.m / rows
+    value = 1.0 / s_per_sweep_full
+    cores = len(os.sched_getaffinity(0))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "sweeps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * s_per_sweep_full, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "r": cfg.r,
+                   "parallelism": "cpu oracle (OpenMP over rows)"},
+        "cpu_baseline": {"value": value, "unit": "sweeps/s", "cores": cores, "kind": "oracle",
+                         "sample": f"one HALS sweep of the fp64 oracle on rows 0..{rows} of "
+                                   f"{cfg.name} per step, scaled by m/{rows}"},
+        "e2e": {"value": value, "unit": "sweeps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_enmf(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_19325_b200 as E
+    import synth
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = synth.ALL[args.config]
+    m, n, r = cfg.m, cfg.n, cfg.r
+    begin, count = E.row_partition(m, world, rank)
+    uid = None
+    if world > 1:
+        obj = [E.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    stream = torch.cuda.current_stream()
+    X = torch.empty(count, n, device="cuda", dtype=torch.float32)
+    synth.x_rows_device(cfg, begin, count, X, stream.cuda_stream)
+    U = torch.empty(count, r, device="cuda")
+    V = torch.empty(n, r, device="cuda")
+    prec = {"auto": E.PREC_AUTO, "fp64": E.PREC_FP64, "tc": E.PREC_TC}[args.precision]
+    h = E.Enmf(m, n, r, row_begin=begin, row_count=count, world_size=world, rank=rank,
+               nccl_id=uid, stream=stream, precision=prec)
+
+    def maxr(x):
+        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    barrier()
+    t0 = time.perf_counter()
+    info = h.init(X, U, V)
+    torch.cuda.synchronize()
+    init_s = maxr(time.perf_counter() - t0)
+    f_w, info_w = h.iterate(U, V, args.warmup)
+
+    # ---- timed region: K sweeps, CUDA events on the handle's stream, max over ranks
+    sampler = ClockSampler(gpu_index(local))
+    barrier()
+    sampler.start()
+    time.sleep(0.3)
+    l0 = h.launch_count
+    h.set_profiling(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    f_t, info_t = h.iterate(U, V, args.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms = maxr(ev0.elapsed_time(ev1))
+    prof = h.profile()
+    h.set_profiling(False)
+    launches = h.launch_count - l0
+    sweeps_per_s = args.steps / (ms / 1000.0)
+    x_bytes_pass = float(m) * n * 4
+    gbs = 2.0 * x_bytes_pass * sweeps_per_s / 1e9
+
+    peaks, peak_kind = measured_peaks()
+    # dominant kernel: the X passes (X V and X^T U) -- algorithmic bytes = this rank's X
+    pass_ms = (prof["xv"][0] + prof["xtu"][0]) / max(1, prof["xv"][1] + prof["xtu"][1])
+    achieved = float(count) * n * 4 / (pass_ms / 1000.0) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        traffic = tj.get(h.precision, {}).get("bytes_per_pass")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "kernel": f"X pass ({h.precision})", "peak_kind": peak_kind,
+                "pass_ms": pass_ms,
+                "share_of_step": (prof["xv"][0] + prof["xtu"][0]) / max(ms, 1e-9)}
+
+    # ---- end to end through the public API: each step uploads the factor state (U, V)
+    # from pinned host memory, runs one sweep, and reads U, V and f back.
+    e2e = None
+    if not args.no_e2e:
+        Uh = torch.empty(count, r, dtype=torch.float32).pin_memory()
+        Vh = torch.empty(n, r, dtype=torch.float32).pin_memory()
+        Uh.copy_(U)
+        Vh.copy_(V)
+        k2 = max(3, min(args.steps, 10))
+        barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fsum = 0.0
+        for _ in range(k2):
+            U.copy_(Uh, non_blocking=True)
+            V.copy_(Vh, non_blocking=True)
+            f, _ = h.iterate(U, V, 1)
+            Uh.copy_(U, non_blocking=True)
+            Vh.copy_(V, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            fsum += float(f[-1])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms2 = maxr(e0.elapsed_time(e1))
+        e2e = {"value": k2 / (ms2 / 1000.0), "unit": "sweeps/s",
+               "h2d_bytes_per_step": int((count + n) * r * 4),
+               "d2h_bytes_per_step": int((count + n) * r * 4 + 8),
+               "what": "per step: H2D of (U, V) from pinned host, enmf_iterate(1), D2H of "
+                       "(U, V, f); X resident"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows = args.cpu_sample_rows or 96
+        Us = U[:rows].cpu().numpy()
+        Vs = V.cpu().numpy()
+        cpu_sample(cfg, rows, Us, Vs, 1)
+        secs = cpu_sample(cfg, rows, Us, Vs, 1)
+        cpu = {"value": 1.0 / (secs * m / rows), "unit": "sweeps/s",
+               "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+               "sample": f"one HALS sweep of the fp64 oracle on rows 0..{rows} of {cfg.name} "
+                         f"({secs:.2f} s), scaled by m/{rows} to the full workload"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": sweeps_per_s, "unit": "sweeps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if h.precision == "fp64-simt" else "f16x2-split/f32-tmem/f64",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "m": m, "n": n, "r": r,
+                       "global_batch": m, "seq_len": n,
+                       "parallelism": f"row-shard x{world} (NCCL allreduce of X^T U, Grams)",
+                       "l2": "inputs larger than L2 (X is 40 GB), no flush",
+                       "precision_path": h.precision,
+                       "timed_sweeps": {"ascent": info_t["ascent_sweeps"],
+                                        "hals": info_t["hals_sweeps"]},
+                       "warmup_sweeps": {"ascent": info_w["ascent_sweeps"],
+                                         "hals": info_w["hals_sweeps"]}},
+            "hbm_gbs_over_x": gbs,
+            "init_s": init_s,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "f_last": float(f_t[-1]) if len(f_t) else None,
+        }
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_enmf(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,199 @@
+/*
+ * enmf.h -- C-ABI of the B200 (sm_100a) eNMF hot path.
+ *
+ * Method: "An Exterior Method for Nonnegative Matrix Factorization" (arxiv 2605.19325),
+ * PAPER.md = /root/reference/PAPER.md of the build environment.  Problem (Eq.(1),
+ * PAPER.md:107-110): minimise f(U,V) = 1/2 ||X - U V^T||_F^2 over U >= 0, V >= 0 for a
+ * nonnegative X.  Pipeline (Alg. 3): truncated SVD with balanced scaling
+ * -> ADMM orthogonal rotation toward the orthant (Alg. 1)
+ * -> exterior ascent: lift + PBCD with optimal row steps (Eqs.(6)-(11), Alg. 2,
+ * PAPER.md:197-244) until U, V >= 0 -> HALS descent.
+ *
+ * Conventions
+ *   - Orientation (reading R1): X is m x n, U is m x r, V is n x r.  All
+ *     matrices are fp32, row-major, with a leading dimension (elements) >= #columns.
+ *   - Every pointer named without a _host suffix is a DEVICE pointer on the handle's
+ *     device, except in enmf_solve_host.  X, U, V are caller-owned; U and V are updated in
+ *     place; X is read only and must not change while it is bound to a handle.
+ *   - Multi-GPU (SPMD, one process per GPU): rank s owns X rows [row_begin, row_begin +
+ *     row_count) and the same U rows; V is replicated.  Every rank makes the same calls
+ *     in the same order.  On return V is bitwise identical on all ranks.
+ *   - The objective is REPORTED un-halved, ||X - U V^T||_F^2 (reading R2); gradients keep
+ *     the 1/2 convention of PAPER.md:217, grad_U f = (U V^T - X) V.
+ *   - All calls are ordered on the problem's CUDA stream.  Calls that return host values
+ *     (arguments ending in _host) synchronise that stream before returning.
+ *   - Errors: every call returns an enmf_status_t; nothing throws across the ABI.  After
+ *     ENMF_ERR_CUDA / ENMF_ERR_NCCL the handle must be destroyed.
+ *   - The handle owns every workspace (allocated in enmf_create / enmf_set_data), so
+ *     enmf_iterate performs no allocation.
+ */
+#ifndef ENMF_H
+#define ENMF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct enmf_handle_s* enmf_handle_t;
+
+typedef enum {
+  ENMF_OK = 0,
+  ENMF_ERR_INVALID_ARG = -1,   /* NULL pointer, bad option value, leading dim too small */
+  ENMF_ERR_SHAPE = -2,         /* r < 1, r > min(m, n), r > ENMF_MAX_RANK, bad row range */
+  ENMF_ERR_NEGATIVE_X = -3,    /* X has a negative entry (PAPER.md:110 requires X >= 0) */
+  ENMF_ERR_RANK_DEFICIENT = -4,/* sigma_1 = 0 (X = 0) */
+  ENMF_ERR_NONFINITE = -5,     /* NaN/Inf in X or produced by an update */
+  ENMF_ERR_CUDA = -6,
+  ENMF_ERR_NCCL = -7,
+  ENMF_ERR_OOM = -8,
+  ENMF_ERR_STATE = -9          /* call out of order (e.g. iterate before set_data) */
+} enmf_status_t;
+
+#define ENMF_MAX_RANK 128
+
+typedef struct {
+  int64_t m_global;        /* rows of X */
+  int64_t n;               /* columns of X */
+  int64_t r;               /* factor rank, 1 <= r <= min(m, n, ENMF_MAX_RANK) */
+  int64_t row_begin;       /* first X/U row owned by this rank */
+  int64_t row_count;       /* X/U rows owned by this rank (m_global when world_size == 1) */
+  int world_size;          /* ranks (GPUs) */
+  int rank;                /* this rank */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId from rank 0; NULL if world_size == 1 */
+  void* cuda_stream;       /* cudaStream_t for every call; NULL = legacy default stream */
+} enmf_problem_t;
+
+typedef enum {
+  ENMF_PREC_AUTO = 0,      /* tensor-core split path when profitable, else FP64 */
+  ENMF_PREC_FP64 = 1,      /* SIMT contractions with fp64 accumulation */
+  ENMF_PREC_TC = 2         /* tcgen05 split-fp16 X (X = Xhi + Xlo), fp32 TMEM chunks
+                              promoted to fp64 */
+} enmf_precision_t;
+
+typedef struct {
+  uint64_t seed;           /* Philox key of the Gaussian test matrix Omega (randomised SVD) */
+  int oversample;          /* p, block size l = r + p (reading R3); default 10 */
+  int power_iters;         /* q power iterations of the range finder; default 2 */
+  int admm_iters;          /* T_admm fixed ADMM steps, last iterate output (R8); default 100 */
+  double admm_rho;         /* rho of Alg. 1; <= 0: 1/rho = 1000 max|W| (reading R7) */
+  int lift_steps;          /* L: lift = 1.001 |min| / L, fixed at the rotated point (R9); 10 */
+  double pbcd_eps;         /* epsilon of Alg. 2 (R10); default 1e-2 */
+  int pbcd_max_iter;       /* max_iter of Alg. 2 (R10); default 50 */
+  int precision;           /* enmf_precision_t */
+} enmf_options_t;
+
+typedef struct {
+  double sigma[ENMF_MAX_RANK]; /* leading singular values of X */
+  int rank_deficient;      /* columns with sigma_k <= 1e-7 sigma_1 (zero-filled in U*, V*) */
+  double negativity_svd;   /* sum h over [U*; V*] */
+  double negativity_rot;   /* sum h over [U* R; V* R] after the last ADMM step */
+  double orth_residual;    /* max |R^T R - I| */
+  int64_t admm_third_branch; /* Z entries that took the third branch of Eq.(7) */
+  double lambda_u, lambda_v; /* lift constants rho_u delta_u, rho_v delta_v (R9) */
+  double xnorm2;           /* ||X||_F^2 */
+} enmf_init_info_t;
+
+typedef struct {
+  int ascent_sweeps;       /* sweeps of this call spent in the ascent stage */
+  int hals_sweeps;         /* sweeps of this call spent in HALS */
+  int feasible;            /* 1 if U, V >= 0 on return */
+  int pbcd_iters_u;        /* PBCD inner iterations of the last ascent U block (k*) */
+  int pbcd_iters_v;        /* same for the V block */
+} enmf_iter_info_t;
+
+typedef struct {
+  double min_u, min_v;     /* KKT: U >= 0, V >= 0 */
+  double comp_max;         /* max |grad (.) W| over W = [U; V] */
+  double comp_sum;         /* sum |grad (.) W| */
+  double delta_w;          /* Table 10: max(grad (.) W) */
+  double sigma_w;          /* Table 10: sum(grad (.) W) */
+  double dual_viol;        /* max(0, -min grad): violation of grad >= 0 */
+  double xnorm2;           /* ||X||_F^2 (normaliser of comp_*) */
+  double rms_cross;        /* rms of [X V; X^T U] (normaliser of dual_viol) */
+} enmf_kkt_t;
+
+/* Fill *opt with the defaults listed above. */
+void enmf_default_options(enmf_options_t* opt);
+
+/* Create a handle for one problem shape.  Validates shapes (ENMF_ERR_SHAPE), sets up the
+ * NCCL communicator when world_size > 1 (ENMF_ERR_NCCL), allocates workspaces
+ * (ENMF_ERR_OOM).  *out is NULL on failure. */
+enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
+                          enmf_handle_t* out);
+enmf_status_t enmf_destroy(enmf_handle_t h);
+
+/* Bind this rank's rows of X (device, row_count x n, leading dim ldx >= n).  Computes
+ * ||X||_F^2 and checks X >= 0 and finite (ENMF_ERR_NEGATIVE_X / ENMF_ERR_NONFINITE).  On
+ * the tensor-core path also builds the handle-owned split copy X = Xhi + Xlo (fp16 pair).
+ * Resets the stage machine. */
+enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx);
+
+/* Rank-r truncated SVD with balanced scaling U* = U S^1/2, V* = V S^1/2 by
+ * a randomised range finder (reading R3); sign rule R5.  Writes U* (this
+ * rank's rows) into U and V* into V; sigma_host (r values) may be NULL. */
+enmf_status_t enmf_svd(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                       double* sigma_host);
+
+/* Alg. 1: rotate (U, V) <- (U R, V R) by T_admm ADMM steps from
+ * R0 = I, Y0 = 0 (reading R6), then fix the lift constants from the rotated point (R9)
+ * and enter the ascent stage.  info_host may be NULL. */
+enmf_status_t enmf_rotate(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                          enmf_init_info_t* info_host);
+
+/* enmf_set_data + enmf_svd + enmf_rotate (Alg. 3). */
+enmf_status_t enmf_init(enmf_handle_t h, const float* X, int64_t ldx, float* U, int64_t ldu,
+                        float* V, int64_t ldv, enmf_init_info_t* info_host);
+
+/* Stage machine access (checkpoint/resume and shared-init parity runs): stage 0 = ascent,
+ * 1 = HALS; lambda_u / lambda_v are the lift constants (reading R9). */
+enmf_status_t enmf_set_stage(enmf_handle_t h, int stage, double lambda_u, double lambda_v);
+enmf_status_t enmf_get_stage(enmf_handle_t h, int* stage, double* lambda_u, double* lambda_v);
+
+/* n_iters sweeps of Alg. 3's loop: each sweep is one U block and one
+ * V block, ascent (lift + mask + PBCD) while min(U) < 0 or min(V) < 0, HALS afterwards.
+ * f_trace_host (n_iters doubles, may be NULL) receives ||X - U V^T||_F^2 after every
+ * sweep in trace form ||X||^2 - 2<X^T U, V> + <U^T U, V^T V> (fp64 terms). */
+enmf_status_t enmf_iterate(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                           int n_iters, double* f_trace_host, enmf_iter_info_t* info_host);
+
+/* ||X - U V^T||_F^2 for the bound X: exact = 0 trace form (one X pass), exact = 1 direct
+ * definition sum (X - U V^T)^2 (one X pass, 2mnr flops, fp64 accumulation). */
+enmf_status_t enmf_objective(enmf_handle_t h, const float* U, int64_t ldu, const float* V,
+                             int64_t ldv, int exact, double* f_host);
+
+/* KKT residuals of App. G at (U, V) for the bound X. */
+enmf_status_t enmf_kkt_residual(enmf_handle_t h, const float* U, int64_t ldu, const float* V,
+                                int64_t ldv, enmf_kkt_t* out_host);
+
+/* End-to-end solve from HOST buffers (single GPU): X_host (m x n, ld = n), U_host
+ * (m x r), V_host (n x r) and f_trace_host (n_iters) are host pointers.  Copies X to the
+ * device through a pinned staging buffer, runs init + n_iters sweeps, copies U, V back. */
+enmf_status_t enmf_solve_host(enmf_handle_t h, const float* X_host, float* U_host,
+                              float* V_host, int n_iters, double* f_trace_host,
+                              enmf_init_info_t* info_host);
+
+/* Kernel launches issued by this handle since creation (instrumentation). */
+int64_t enmf_launch_count(enmf_handle_t h);
+
+/* Instrumentation of the two X passes: with profiling on, every X V and X^T U contraction
+ * is bracketed by CUDA events on the handle's stream; enmf_get_profile returns the summed
+ * device milliseconds ms_host[2] and pass counts count_host[2] ({X V, X^T U}) since the last
+ * enmf_set_profiling call (synchronises the stream). */
+enmf_status_t enmf_set_profiling(enmf_handle_t h, int on);
+enmf_status_t enmf_get_profile(enmf_handle_t h, double* ms_host, int64_t* count_host);
+
+/* 128-byte ncclUniqueId for a multi-GPU job (call on rank 0, broadcast the bytes, pass them
+ * in enmf_problem_t.nccl_unique_id on every rank). */
+enmf_status_t enmf_nccl_unique_id(void* out128);
+
+/* Name of the contraction path selected by enmf_set_data ("fp64-simt" or "tc-split-f16/f64"). */
+const char* enmf_precision_name(enmf_handle_t h);
+
+const char* enmf_status_string(enmf_status_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

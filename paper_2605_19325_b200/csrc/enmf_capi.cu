@@ -1,0 +1,555 @@
+// enmf_capi.cu -- the C-ABI of include/enmf.h: handle, workspaces, and the orchestration of
+// Alg. 3 on one stream.  All arithmetic runs in the kernels of this
+// library; this file only sequences launches and NCCL collectives.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "handle.h"
+
+namespace enmf {
+thread_local int64_t* g_launch_counter = nullptr;
+
+enmf_status_t check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "enmf: kernel launch failed: %s\n", cudaGetErrorString(e));
+    return ENMF_ERR_CUDA;
+  }
+  return ENMF_OK;
+}
+
+enmf_status_t dalloc_bytes(void** p, size_t bytes) {
+  *p = nullptr;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return e == cudaErrorMemoryAllocation ? ENMF_ERR_OOM : ENMF_ERR_CUDA;
+  }
+  return ENMF_OK;
+}
+
+enmf_status_t ar(enmf_handle_t h, double* buf, size_t count, CommOp op) {
+  if (h->prob.world_size <= 1) return ENMF_OK;
+  return comm_allreduce(h->comm, buf, count, CommType::F64, op, h->st) == 0 ? ENMF_OK
+                                                                           : ENMF_ERR_NCCL;
+}
+
+enmf_status_t validate_ld(const void* p, int64_t ld, int64_t cols) {
+  if (!p || ld < cols) return ENMF_ERR_INVALID_ARG;
+  return ENMF_OK;
+}
+
+// ---------------------------------------------------------------- contractions (a5, a6)
+// Optional CUDA-event bracketing of each X pass (enmf_set_profiling) on the handle's stream.
+static enmf_status_t prof_mark(enmf_handle_t h, int kind) {
+  if (!h->prof) return ENMF_OK;
+  if (h->ev_used == h->ev_pool.size()) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    h->ev_pool.push_back(e);
+  }
+  if (h->ev_used % 2 == 0) h->ev_kind.push_back(kind);
+  CUDA_TRY(cudaEventRecord(h->ev_pool[h->ev_used++], h->st));
+  return ENMF_OK;
+}
+
+// Accumulate elapsed times of completed event pairs (stream already synchronised).
+static void prof_collect(enmf_handle_t h) {
+  for (size_t p = 0; p + 1 < h->ev_used; p += 2) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, h->ev_pool[p], h->ev_pool[p + 1]) == cudaSuccess) {
+      const int k = h->ev_kind[p / 2];
+      h->prof_ms[k] += ms;
+      h->prof_cnt[k] += 1;
+    }
+  }
+  h->ev_used = 0;
+  h->ev_kind.clear();
+}
+
+// P = X V (this rank's rows): the first X pass of a sweep.
+enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* P) {
+  ENMF_TRY(prof_mark(h, 0));
+  if (h->tc) {
+    if (tc_xv(h->tc, V, ldv, P, h->st) != 0) return ENMF_ERR_CUDA;
+  } else {
+    GemmOut o;
+    o.C = P;
+    o.ldc = h->r;
+    gemm<float, float>(false, h->X, h->ldx, V, ldv, h->m_loc, h->r, h->n, o, h->work,
+                       h->work_elems, h->st);
+  }
+  return prof_mark(h, 0);
+}
+
+// Q = X^T U summed over ranks: the second X pass.
+enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q) {
+  ENMF_TRY(prof_mark(h, 1));
+  if (h->tc) {
+    if (tc_xtu(h->tc, U, ldu, Q, h->st) != 0) return ENMF_ERR_CUDA;
+  } else {
+    GemmOut o;
+    o.C = Q;
+    o.ldc = h->r;
+    gemm<float, float>(true, h->X, h->ldx, U, ldu, h->n, h->r, h->m_loc, o, h->work,
+                       h->work_elems, h->st);
+  }
+  ENMF_TRY(prof_mark(h, 1));
+  return ar(h, Q, (size_t)(h->n * h->r), CommOp::Sum);
+}
+
+// G = A^T A of an fp32 factor (rows x r); sum over ranks if `sharded`.
+enmf_status_t gram_f32(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, double* G,
+                       bool sharded) {
+  GemmOut o;
+  o.C = G;
+  o.ldc = h->r;
+  gemm<float, float>(true, A, lda, A, lda, h->r, h->r, rows, o, h->work, h->work_elems, h->st);
+  return sharded ? ar(h, G, (size_t)(h->r * h->r), CommOp::Sum) : ENMF_OK;
+}
+
+enmf_status_t min_factor(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, int slot,
+                         bool sharded) {
+  min_f32(A, lda, rows, h->r, h->parts, h->dscal + slot, h->st);
+  return sharded ? ar(h, h->dscal + slot, 1, CommOp::Min) : ENMF_OK;
+}
+
+}  // namespace enmf
+
+using namespace enmf;
+
+namespace {
+
+// One block update (U block: F = U, C = P, G = G_V; V block: F = V, C = Q, G = G_U).
+// In the ascent stage: lift + mask + PBCD (Eqs.(6)-(10), Alg. 2); in HALS: the column sweep.
+enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
+                           const double* C, const double* G, int lam_slot, int kstar_slot,
+                           int min_slot, bool sharded, bool maybe_ascent) {
+  const int r = (int)h->r;
+  int* stage = h->dint + I_STAGE;
+  const int mi = h->opt.pbcd_max_iter;
+  if (maybe_ascent) {
+    pbcd_rows(F, ldf, rows, r, C, G, h->dscal + lam_slot, mi, h->snaps, h->parts, stage, h->st);
+    reduce_parts(h->parts, pbcd_parts(), mi + 1, h->pgsum, h->st);
+    if (sharded) ENMF_TRY(ar(h, h->pgsum, (size_t)(mi + 1), CommOp::Sum));
+    pbcd_commit(F, ldf, rows, r, h->snaps, h->pgsum, h->opt.pbcd_eps, mi, h->dint + kstar_slot,
+                stage, h->minparts, h->st);
+  }
+  hals_rows(F, ldf, rows, r, C, G, stage, h->minparts, h->st);
+  reduce_min(h->minparts, kRowGrid, h->dscal + min_slot, h->st);
+  return sharded ? ar(h, h->dscal + min_slot, 1, CommOp::Min) : ENMF_OK;
+}
+
+enmf_status_t ensure_snaps(enmf_handle_t h) {
+  if (h->snaps) return ENMF_OK;
+  const size_t rows = (size_t)std::max(h->m_loc, h->n);
+  return dalloc(&h->snaps, (size_t)h->opt.pbcd_max_iter * rows * (size_t)h->r);
+}
+
+enmf_status_t ensure_ftrace(enmf_handle_t h, int n) {
+  if (h->ftrace_cap >= n) return ENMF_OK;
+  if (h->ftrace) cudaFree(h->ftrace);
+  h->ftrace = nullptr;
+  h->ftrace_cap = 0;
+  ENMF_TRY(dalloc(&h->ftrace, (size_t)n));
+  h->ftrace_cap = n;
+  return ENMF_OK;
+}
+
+// One sweep (U block then V block) with the trace-form objective into ftrace[t].
+enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv, int t,
+                    bool maybe_ascent) {
+  const bool sh = h->prob.world_size > 1;
+  cudaStream_t st = h->st;
+  // stage control: HALS once U >= 0 and V >= 0
+  stage_update(h->dint + I_STAGE, h->dscal + S_MINU, h->dscal + S_MINV, h->dint + I_CNT_ASC, st);
+  // U block: P = X V, G_V = V^T V (G_V carried over from the previous sweep's end)
+  ENMF_TRY(contract_xv(h, V, ldv, h->P));
+  ENMF_TRY(block_update(h, U, ldu, h->m_loc, h->P, h->GV, S_LAMU, I_KSTAR_U, S_MINU, sh,
+                        maybe_ascent));
+  // V block: Q = X^T U_new (allreduced), G_U = U_new^T U_new (PAPER.md:220 uses U^(k+1))
+  ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh));
+  ENMF_TRY(contract_xtu(h, U, ldu, h->Q));
+  ENMF_TRY(block_update(h, V, ldv, h->n, h->Q, h->GU, S_LAMV, I_KSTAR_V, S_MINV, false,
+                        maybe_ascent));
+  // objective f = ||X||^2 - 2 <X^T U, V> + <U^T U, V^T V>   (BASELINE.json:5)
+  ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
+  dot_f64_f32(h->Q, V, ldv, h->n, h->r, h->parts, h->dscal + S_CROSS, st);
+  objective_finish(h->dscal + S_XNORM2, h->dscal + S_CROSS, h->GU, h->GV, (int)h->r,
+                   h->ftrace + t, st);
+  return check_launch();
+}
+
+}  // namespace
+
+// ==================================================================== C-ABI
+extern "C" {
+
+void enmf_default_options(enmf_options_t* o) {
+  if (!o) return;
+  o->seed = 0x5EEDull;
+  o->oversample = 10;
+  o->power_iters = 2;
+  o->admm_iters = 100;
+  o->admm_rho = 0.0;
+  o->lift_steps = 10;
+  o->pbcd_eps = 1e-2;
+  o->pbcd_max_iter = 50;
+  o->precision = ENMF_PREC_AUTO;
+}
+
+const char* enmf_status_string(enmf_status_t s) {
+  switch (s) {
+    case ENMF_OK: return "ok";
+    case ENMF_ERR_INVALID_ARG: return "invalid argument";
+    case ENMF_ERR_SHAPE: return "invalid shape";
+    case ENMF_ERR_NEGATIVE_X: return "X has a negative entry";
+    case ENMF_ERR_RANK_DEFICIENT: return "X has rank 0";
+    case ENMF_ERR_NONFINITE: return "non-finite value";
+    case ENMF_ERR_CUDA: return "CUDA error";
+    case ENMF_ERR_NCCL: return "NCCL error";
+    case ENMF_ERR_OOM: return "out of device memory";
+    case ENMF_ERR_STATE: return "call out of order";
+  }
+  return "unknown status";
+}
+
+int64_t enmf_launch_count(enmf_handle_t h) { return h ? h->launches : -1; }
+
+enmf_status_t enmf_set_profiling(enmf_handle_t h, int on) {
+  if (!h) return ENMF_ERR_INVALID_ARG;
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  prof_collect(h);
+  h->prof = on != 0;
+  h->prof_ms[0] = h->prof_ms[1] = 0.0;
+  h->prof_cnt[0] = h->prof_cnt[1] = 0;
+  return ENMF_OK;
+}
+
+enmf_status_t enmf_get_profile(enmf_handle_t h, double* ms_host, int64_t* count_host) {
+  if (!h || !ms_host || !count_host) return ENMF_ERR_INVALID_ARG;
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  prof_collect(h);
+  for (int k = 0; k < 2; ++k) {
+    ms_host[k] = h->prof_ms[k];
+    count_host[k] = h->prof_cnt[k];
+  }
+  return ENMF_OK;
+}
+
+enmf_status_t enmf_nccl_unique_id(void* out128) {
+  if (!out128) return ENMF_ERR_INVALID_ARG;
+  return comm_unique_id(out128) == 0 ? ENMF_OK : ENMF_ERR_NCCL;
+}
+
+const char* enmf_precision_name(enmf_handle_t h) {
+  if (!h) return "none";
+  return h->precision == ENMF_PREC_TC ? "tc-split-f16/f64" : "fp64-simt";
+}
+
+enmf_status_t enmf_destroy(enmf_handle_t h) {
+  if (!h) return ENMF_ERR_INVALID_ARG;
+  if (h->st) cudaStreamSynchronize(h->st);
+  void* bufs[] = {h->dscal, h->dint, h->P, h->Q, h->GU, h->GV, h->work, h->parts,
+                  h->minparts, h->pgsum, h->snaps, h->ftrace, h->x_owned, h->W64};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (h->tc) tc_destroy(h->tc);
+  for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  comm_destroy(h->comm);
+  delete h;
+  return ENMF_OK;
+}
+
+enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
+                          enmf_handle_t* out) {
+  if (!out) return ENMF_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!prob) return ENMF_ERR_INVALID_ARG;
+  enmf_options_t o;
+  enmf_default_options(&o);
+  if (opt) o = *opt;
+  const int64_t m = prob->m_global, n = prob->n, r = prob->r;
+  if (m < 1 || n < 1 || r < 1 || r > std::min(m, n) || r > ENMF_MAX_RANK) return ENMF_ERR_SHAPE;
+  if (prob->world_size < 1 || prob->rank < 0 || prob->rank >= prob->world_size)
+    return ENMF_ERR_INVALID_ARG;
+  if (prob->row_begin < 0 || prob->row_count < 1 || prob->row_begin + prob->row_count > m)
+    return ENMF_ERR_SHAPE;
+  if (prob->world_size == 1 && (prob->row_begin != 0 || prob->row_count != m))
+    return ENMF_ERR_SHAPE;
+  if (prob->world_size > 1 && !prob->nccl_unique_id) return ENMF_ERR_INVALID_ARG;
+  if (o.oversample < 0 || o.power_iters < 0 || o.admm_iters < 0 || o.lift_steps < 1 ||
+      o.pbcd_max_iter < 1 || o.pbcd_max_iter > 1000 || !(o.pbcd_eps >= 0.0) ||
+      o.precision < ENMF_PREC_AUTO || o.precision > ENMF_PREC_TC)
+    return ENMF_ERR_INVALID_ARG;
+  enmf_handle_t h = new enmf_handle_s();
+  h->prob = *prob;
+  h->opt = o;
+  h->st = (cudaStream_t)prob->cuda_stream;
+  h->m_loc = prob->row_count;
+  h->n = n;
+  h->r = r;
+  LaunchScope ls(h);
+  enmf_status_t s = ENMF_OK;
+#define ALLOC(p, c)                         \
+  if (s == ENMF_OK) s = dalloc(&(p), (c));
+  ALLOC(h->dscal, S_COUNT);
+  ALLOC(h->dint, I_COUNT);
+  ALLOC(h->P, (size_t)(h->m_loc * r));
+  ALLOC(h->Q, (size_t)(n * r));
+  ALLOC(h->GU, (size_t)(r * r));
+  ALLOC(h->GV, (size_t)(r * r));
+  // split-K partials: enough for the small GEMMs (r x r, l x l) and for the SVD panels
+  const int64_t l = std::min<int64_t>(std::min(m, n), r + o.oversample);
+  h->work_elems = (size_t)std::max<int64_t>(
+      {(int64_t)8 << 20, 40 * l * l, 2 * (int64_t)512 * 512, 8 * r * r});
+  ALLOC(h->work, h->work_elems);
+  h->parts_elems = (size_t)std::max<int64_t>(
+      {(int64_t)pbcd_parts() * (o.pbcd_max_iter + 1), (int64_t)kkt_parts() * 8,
+       (int64_t)colabsmax_parts() * 3 * std::max<int64_t>(r, 1), 3 * 4 * kSMs, 4096});
+  ALLOC(h->parts, h->parts_elems);
+  ALLOC(h->minparts, (size_t)kRowGrid);
+  ALLOC(h->pgsum, (size_t)(o.pbcd_max_iter + 1));
+#undef ALLOC
+  if (s == ENMF_OK && prob->world_size > 1) {
+    if (comm_init(&h->comm, prob->nccl_unique_id, prob->world_size, prob->rank) != 0)
+      s = ENMF_ERR_NCCL;
+  }
+  if (s == ENMF_OK) {
+    cudaMemsetAsync(h->dscal, 0, sizeof(double) * S_COUNT, h->st);
+    cudaMemsetAsync(h->dint, 0, sizeof(int) * I_COUNT, h->st);
+    if (cudaGetLastError() != cudaSuccess) s = ENMF_ERR_CUDA;
+  }
+  if (s != ENMF_OK) {
+    enmf_destroy(h);
+    return s;
+  }
+  *out = h;
+  return ENMF_OK;
+}
+
+enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
+  if (!h) return ENMF_ERR_INVALID_ARG;
+  ENMF_TRY(validate_ld(X, ldx, h->n));
+  LaunchScope ls(h);
+  h->X = X;
+  h->ldx = ldx;
+  h->bound = false;
+  const int np = x_stats_parts(h->m_loc);
+  double* out3 = h->work;   // [sum, min, nonfinite]
+  x_stats(X, ldx, h->m_loc, h->n, h->parts, np, out3, h->st);
+  ENMF_TRY(ar(h, out3, 1, CommOp::Sum));
+  ENMF_TRY(ar(h, out3 + 1, 1, CommOp::Min));
+  ENMF_TRY(ar(h, out3 + 2, 1, CommOp::Sum));
+  double hv[3];
+  CUDA_TRY(cudaMemcpyAsync(hv, out3, sizeof(hv), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  if (hv[2] > 0) return ENMF_ERR_NONFINITE;
+  if (hv[1] < 0) return ENMF_ERR_NEGATIVE_X;
+  CUDA_TRY(cudaMemcpyAsync(h->dscal + S_XNORM2, out3, sizeof(double), cudaMemcpyDeviceToDevice,
+                           h->st));
+  // precision selection: the tensor-core split path pays off on large X
+  int prec = h->opt.precision;
+  if (prec == ENMF_PREC_AUTO)
+    prec = (tc_supported(h->m_loc, h->n, h->r) && (double)h->m_loc * h->n >= 2.5e8)
+               ? ENMF_PREC_TC : ENMF_PREC_FP64;
+  if (prec == ENMF_PREC_TC && !tc_supported(h->m_loc, h->n, h->r)) return ENMF_ERR_SHAPE;
+  if (h->tc) { tc_destroy(h->tc); h->tc = nullptr; }
+  if (prec == ENMF_PREC_TC) {
+    int rc = tc_create(&h->tc, X, ldx, h->m_loc, h->n, h->r, h->st);
+    if (rc != 0) return rc == 2 ? ENMF_ERR_OOM : ENMF_ERR_CUDA;
+  }
+  h->precision = prec;
+  int zero[I_COUNT] = {0};
+  CUDA_TRY(cudaMemcpyAsync(h->dint, zero, sizeof(zero), cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  h->stage_known_hals = false;
+  h->bound = true;
+  return check_launch();
+}
+
+enmf_status_t enmf_set_stage(enmf_handle_t h, int stage, double lambda_u, double lambda_v) {
+  if (!h || (stage != 0 && stage != 1) || !(lambda_u >= 0) || !(lambda_v >= 0))
+    return ENMF_ERR_INVALID_ARG;
+  int st = stage;
+  double lam[2] = {lambda_u, lambda_v};
+  CUDA_TRY(cudaMemcpyAsync(h->dint + I_STAGE, &st, sizeof(int), cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaMemcpyAsync(h->dscal + S_LAMU, lam, sizeof(lam), cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  h->stage_known_hals = stage == 1;
+  return ENMF_OK;
+}
+
+enmf_status_t enmf_get_stage(enmf_handle_t h, int* stage, double* lambda_u, double* lambda_v) {
+  if (!h) return ENMF_ERR_INVALID_ARG;
+  int st = 0;
+  double lam[2];
+  CUDA_TRY(cudaMemcpyAsync(&st, h->dint + I_STAGE, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaMemcpyAsync(lam, h->dscal + S_LAMU, sizeof(lam), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  if (stage) *stage = st;
+  if (lambda_u) *lambda_u = lam[0];
+  if (lambda_v) *lambda_v = lam[1];
+  return ENMF_OK;
+}
+
+enmf_status_t enmf_iterate(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                           int n_iters, double* f_trace_host, enmf_iter_info_t* info) {
+  if (!h || n_iters < 0) return ENMF_ERR_INVALID_ARG;
+  if (!h->bound) return ENMF_ERR_STATE;
+  ENMF_TRY(validate_ld(U, ldu, h->r));
+  ENMF_TRY(validate_ld(V, ldv, h->r));
+  LaunchScope ls(h);
+  const bool sh = h->prob.world_size > 1;
+  const bool maybe_ascent = !h->stage_known_hals;
+  if (maybe_ascent) ENMF_TRY(ensure_snaps(h));
+  ENMF_TRY(ensure_ftrace(h, std::max(n_iters, 1)));
+  CUDA_TRY(cudaMemsetAsync(h->dint + I_CNT_ASC, 0, 2 * sizeof(int), h->st));
+  // entry state: mins of the factors as given, G_V of the given V
+  ENMF_TRY(min_factor(h, U, ldu, h->m_loc, S_MINU, sh));
+  ENMF_TRY(min_factor(h, V, ldv, h->n, S_MINV, false));
+  ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
+  for (int t = 0; t < n_iters; ++t) ENMF_TRY(sweep(h, U, ldu, V, ldv, t, maybe_ascent));
+  // final stage flag (does not consume a sweep) and host-side bookkeeping
+  int hi[I_COUNT];
+  CUDA_TRY(cudaMemcpyAsync(hi, h->dint, sizeof(hi), cudaMemcpyDeviceToHost, h->st));
+  double mins[2];
+  CUDA_TRY(cudaMemcpyAsync(mins, h->dscal + S_MINU, sizeof(mins), cudaMemcpyDeviceToHost, h->st));
+  if (f_trace_host && n_iters > 0)
+    CUDA_TRY(cudaMemcpyAsync(f_trace_host, h->ftrace, sizeof(double) * n_iters,
+                             cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  ENMF_TRY(check_launch());
+  prof_collect(h);
+  if (hi[I_STAGE] == 1) h->stage_known_hals = true;
+  if (info) {
+    info->ascent_sweeps = hi[I_CNT_ASC];
+    info->hals_sweeps = hi[I_CNT_HALS];
+    info->feasible = mins[0] >= 0.0 && mins[1] >= 0.0;
+    info->pbcd_iters_u = hi[I_KSTAR_U];
+    info->pbcd_iters_v = hi[I_KSTAR_V];
+  }
+  if (f_trace_host)
+    for (int t = 0; t < n_iters; ++t)
+      if (!isfinite(f_trace_host[t])) return ENMF_ERR_NONFINITE;
+  return ENMF_OK;
+}
+
+enmf_status_t enmf_objective(enmf_handle_t h, const float* U, int64_t ldu, const float* V,
+                             int64_t ldv, int exact, double* f_host) {
+  if (!h || !f_host) return ENMF_ERR_INVALID_ARG;
+  if (!h->bound) return ENMF_ERR_STATE;
+  ENMF_TRY(validate_ld(U, ldu, h->r));
+  ENMF_TRY(validate_ld(V, ldv, h->r));
+  LaunchScope ls(h);
+  const bool sh = h->prob.world_size > 1;
+  double* f = h->dscal + S_SCRATCH;
+  if (exact) {
+    int np = 0;
+    frob_direct(h->X, h->ldx, h->m_loc, h->n, U, ldu, V, ldv, (int)h->r, h->parts, &np, h->st);
+    reduce_parts(h->parts, np, 1, f, h->st);
+    ENMF_TRY(ar(h, f, 1, CommOp::Sum));
+  } else {
+    ENMF_TRY(contract_xtu(h, U, ldu, h->Q));
+    ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh));
+    double* gv = h->work + h->work_elems - (size_t)(h->r * h->r);
+    GemmOut o;
+    o.C = gv;
+    o.ldc = h->r;
+    gemm<float, float>(true, V, ldv, V, ldv, h->r, h->r, h->n, o, h->work,
+                       h->work_elems - (size_t)(h->r * h->r), h->st);
+    dot_f64_f32(h->Q, V, ldv, h->n, h->r, h->parts, h->dscal + S_CROSS, h->st);
+    objective_finish(h->dscal + S_XNORM2, h->dscal + S_CROSS, h->GU, gv, (int)h->r, f, h->st);
+  }
+  CUDA_TRY(cudaMemcpyAsync(f_host, f, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return check_launch();
+}
+
+enmf_status_t enmf_kkt_residual(enmf_handle_t h, const float* U, int64_t ldu, const float* V,
+                                int64_t ldv, enmf_kkt_t* out) {
+  if (!h || !out) return ENMF_ERR_INVALID_ARG;
+  if (!h->bound) return ENMF_ERR_STATE;
+  ENMF_TRY(validate_ld(U, ldu, h->r));
+  ENMF_TRY(validate_ld(V, ldv, h->r));
+  LaunchScope ls(h);
+  const bool sh = h->prob.world_size > 1;
+  const int r = (int)h->r;
+  // grad_U f = U G_V - X V ; grad_V f = V G_U - X^T U
+  ENMF_TRY(contract_xv(h, V, ldv, h->P));
+  ENMF_TRY(contract_xtu(h, U, ldu, h->Q));
+  ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh));
+  double* gv = h->GV;   // recomputed at the next enmf_iterate entry
+  ENMF_TRY(gram_f32(h, V, ldv, h->n, gv, false));
+  const int np = kkt_parts();
+  double* pu = h->parts;
+  double* pv = h->work;
+  kkt_rows(U, ldu, h->m_loc, r, h->P, gv, pu, h->st);
+  kkt_rows(V, ldv, h->n, r, h->Q, h->GU, pv, h->st);
+  std::vector<double> hu((size_t)np * 8), hv((size_t)np * 8);
+  CUDA_TRY(cudaMemcpyAsync(hu.data(), pu, sizeof(double) * hu.size(), cudaMemcpyDeviceToHost,
+                           h->st));
+  CUDA_TRY(cudaMemcpyAsync(hv.data(), pv, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost,
+                           h->st));
+  double xn2 = 0.0;
+  CUDA_TRY(cudaMemcpyAsync(&xn2, h->dscal + S_XNORM2, sizeof(double), cudaMemcpyDeviceToHost,
+                           h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  ENMF_TRY(check_launch());
+  // fixed-order host reduction of the per-warp partials
+  auto fold = [&](const std::vector<double>& p, double* s7) {
+    s7[0] = 0; s7[1] = 0; s7[2] = -INFINITY; s7[3] = 0; s7[4] = INFINITY; s7[5] = INFINITY;
+    s7[6] = 0;
+    for (int w = 0; w < np; ++w) {
+      const double* q = &p[(size_t)w * 8];
+      s7[0] = std::max(s7[0], q[0]);
+      s7[1] += q[1];
+      s7[2] = std::max(s7[2], q[2]);
+      s7[3] += q[3];
+      s7[4] = std::min(s7[4], q[4]);
+      s7[5] = std::min(s7[5], q[5]);
+      s7[6] += q[6];
+    }
+  };
+  double su[7], sv[7];
+  fold(hu, su);
+  fold(hv, sv);
+  if (sh) {
+    // combine the U-block statistics over ranks (V is replicated: counted once)
+    double* d = h->dscal + S_SCRATCH;
+    double sums[3] = {su[1], su[3], su[6]}, maxs[2] = {su[0], su[2]}, mins[2] = {su[4], su[5]};
+    double* buf = h->work;
+    CUDA_TRY(cudaMemcpyAsync(buf, sums, sizeof(sums), cudaMemcpyHostToDevice, h->st));
+    CUDA_TRY(cudaMemcpyAsync(buf + 3, maxs, sizeof(maxs), cudaMemcpyHostToDevice, h->st));
+    CUDA_TRY(cudaMemcpyAsync(buf + 5, mins, sizeof(mins), cudaMemcpyHostToDevice, h->st));
+    ENMF_TRY(ar(h, buf, 3, CommOp::Sum));
+    ENMF_TRY(ar(h, buf + 3, 2, CommOp::Max));
+    ENMF_TRY(ar(h, buf + 5, 2, CommOp::Min));
+    double all[7];
+    CUDA_TRY(cudaMemcpyAsync(all, buf, sizeof(all), cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+    (void)d;
+    su[1] = all[0]; su[3] = all[1]; su[6] = all[2]; su[0] = all[3]; su[2] = all[4];
+    su[4] = all[5]; su[5] = all[6];
+  }
+  out->min_u = su[5];
+  out->min_v = sv[5];
+  out->comp_max = std::max(su[0], sv[0]);
+  out->comp_sum = su[1] + sv[1];
+  out->delta_w = std::max(su[2], sv[2]);
+  out->sigma_w = su[3] + sv[3];
+  const double gmin = std::min(su[4], sv[4]);
+  out->dual_viol = gmin < 0 ? -gmin : 0.0;
+  out->xnorm2 = xn2;
+  out->rms_cross = sqrt((su[6] + sv[6]) / (double)((h->prob.m_global + h->n) * h->r));
+  return ENMF_OK;
+}
+
+}  // extern "C"

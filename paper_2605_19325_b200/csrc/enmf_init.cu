@@ -1,0 +1,418 @@
+// enmf_init.cu -- initialisation of Alg. 3: randomised truncated SVD with
+// balanced scaling and the ADMM rotation of Alg. 1,
+// plus the host-buffer end-to-end entry point.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "handle.h"
+
+using namespace enmf;
+
+namespace {
+
+struct DevBuf {
+  std::vector<void*> ptrs;
+  ~DevBuf() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <typename T>
+  enmf_status_t get(T** p, size_t count) {
+    enmf_status_t s = dalloc(p, count);
+    if (s == ENMF_OK) ptrs.push_back((void*)*p);
+    return s;
+  }
+};
+
+// CholeskyQR2 (first pass shifted): A (rows x l, fp64, ld l) <- A R^{-1}, columns orthonormal.
+enmf_status_t cholqr(enmf_handle_t h, double* A, double* tmp, int64_t rows, int l,
+                     bool sharded, double* G, double* R, double* Rinv, int* bad) {
+  for (int pass = 0; pass < 2; ++pass) {
+    GemmOut o;
+    o.C = G;
+    o.ldc = l;
+    gemm<double, double>(true, A, l, A, l, l, l, rows, o, h->work, h->work_elems, h->st);
+    if (sharded) ENMF_TRY(ar(h, G, (size_t)l * l, CommOp::Sum));
+    chol_inv(G, l, pass == 0 ? 1e-13 : 0.0, R, Rinv, bad, h->st);
+    GemmOut o2;
+    o2.C = tmp;
+    o2.ldc = l;
+    gemm<double, double>(false, A, l, Rinv, l, rows, l, l, o2, h->work, h->work_elems, h->st);
+    CUDA_TRY(cudaMemcpyAsync(A, tmp, sizeof(double) * rows * l, cudaMemcpyDeviceToDevice, h->st));
+  }
+  return check_launch();
+}
+
+// Global column-wise arg max |A_ik| (ties: lowest global row) -> sign of that entry (R5).
+enmf_status_t column_signs(enmf_handle_t h, const double* A, int64_t rows, int r,
+                           int64_t row_offset, std::vector<double>& sign) {
+  colabsmax(A, rows, r, row_offset, h->parts, h->st);
+  const int np = colabsmax_parts();
+  std::vector<double> hp((size_t)np * r * 3);
+  CUDA_TRY(cudaMemcpyAsync(hp.data(), h->parts, sizeof(double) * hp.size(),
+                           cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  std::vector<double> best(r, -1.0), bidx(r, 0.0), bval(r, 0.0);
+  for (int p = 0; p < np; ++p)
+    for (int k = 0; k < r; ++k) {
+      const double* q = &hp[((size_t)p * r + k) * 3];
+      if (q[0] > best[k] || (q[0] == best[k] && q[1] < bidx[k])) {
+        best[k] = q[0]; bidx[k] = q[1]; bval[k] = q[2];
+      }
+    }
+  sign.assign(r, 1.0);
+  if (h->prob.world_size > 1) {
+    double* d = h->work;   // [best | idx | sign]
+    std::vector<double> tmp(best);
+    CUDA_TRY(cudaMemcpyAsync(d, tmp.data(), sizeof(double) * r, cudaMemcpyHostToDevice, h->st));
+    ENMF_TRY(ar(h, d, r, CommOp::Max));
+    std::vector<double> gbest(r);
+    CUDA_TRY(cudaMemcpyAsync(gbest.data(), d, sizeof(double) * r, cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+    for (int k = 0; k < r; ++k) tmp[k] = best[k] == gbest[k] ? bidx[k] : 1e300;
+    CUDA_TRY(cudaMemcpyAsync(d, tmp.data(), sizeof(double) * r, cudaMemcpyHostToDevice, h->st));
+    ENMF_TRY(ar(h, d, r, CommOp::Min));
+    std::vector<double> gidx(r);
+    CUDA_TRY(cudaMemcpyAsync(gidx.data(), d, sizeof(double) * r, cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+    for (int k = 0; k < r; ++k)
+      tmp[k] = (best[k] == gbest[k] && bidx[k] == gidx[k]) ? (bval[k] < 0 ? -1.0 : 1.0) : 0.0;
+    CUDA_TRY(cudaMemcpyAsync(d, tmp.data(), sizeof(double) * r, cudaMemcpyHostToDevice, h->st));
+    ENMF_TRY(ar(h, d, r, CommOp::Sum));
+    CUDA_TRY(cudaMemcpyAsync(tmp.data(), d, sizeof(double) * r, cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+    for (int k = 0; k < r; ++k) sign[k] = tmp[k] < 0 ? -1.0 : 1.0;
+  } else {
+    for (int k = 0; k < r; ++k) sign[k] = bval[k] < 0 ? -1.0 : 1.0;
+  }
+  return ENMF_OK;
+}
+
+// Sum of h(A) = max(0, -A) over `count` fp64 entries.
+enmf_status_t negativity(enmf_handle_t h, const double* A, int64_t count, double* out_host) {
+  negsum(A, count, h->parts, h->dscal + S_NEG, h->st);
+  CUDA_TRY(cudaMemcpyAsync(out_host, h->dscal + S_NEG, sizeof(double), cudaMemcpyDeviceToHost,
+                           h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return check_launch();
+}
+
+// Randomised range finder + Rayleigh-Ritz; writes U*, V* into W64 (fp64) and U, V (fp32).
+enmf_status_t svd_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                       double* sigma_host, enmf_init_info_t* info) {
+  const int64_t m = h->prob.m_global, n = h->n, mr = h->m_loc;
+  const int r = (int)h->r;
+  int64_t l64 = std::min<int64_t>(std::min(m, n), r + h->opt.oversample);
+  l64 = std::min<int64_t>(l64, 512);
+  const int l = (int)l64;
+  const bool sh = h->prob.world_size > 1;
+  DevBuf db;
+  double *Om, *Y, *Z, *Qt, *tmp, *G, *R, *Rinv, *Ue, *Ve, *sv, *jw, *Us;
+  int* bad;
+  const int64_t big = std::max(mr, n);
+  ENMF_TRY(db.get(&Om, (size_t)(n * l)));
+  ENMF_TRY(db.get(&Y, (size_t)(mr * l)));
+  ENMF_TRY(db.get(&Z, (size_t)(n * l)));
+  ENMF_TRY(db.get(&Qt, (size_t)(n * l)));
+  ENMF_TRY(db.get(&tmp, (size_t)(big * l)));
+  ENMF_TRY(db.get(&G, (size_t)l * l));
+  ENMF_TRY(db.get(&R, (size_t)l * l));
+  ENMF_TRY(db.get(&Rinv, (size_t)l * l));
+  ENMF_TRY(db.get(&Ue, (size_t)l * l));
+  ENMF_TRY(db.get(&Ve, (size_t)l * l));
+  ENMF_TRY(db.get(&sv, (size_t)l));
+  ENMF_TRY(db.get(&jw, (size_t)2 * l * l));
+  ENMF_TRY(db.get(&Us, (size_t)(big * r)));
+  ENMF_TRY(db.get(&bad, 1));
+  if (!h->W64) ENMF_TRY(dalloc(&h->W64, (size_t)((mr + n) * r)));
+  // Y = X Omega ; orth                                   (Krylov-type, 1827-1835)
+  gaussian_fill(Om, n, l, h->opt.seed, h->st);
+  GemmOut o;
+  o.ldc = l;
+  o.C = Y;
+  gemm<float, double>(false, h->X, h->ldx, Om, l, mr, l, n, o, h->work, h->work_elems, h->st);
+  ENMF_TRY(cholqr(h, Y, tmp, mr, l, sh, G, R, Rinv, bad));
+  for (int q = 0; q < h->opt.power_iters; ++q) {
+    o.C = Z;
+    gemm<float, double>(true, h->X, h->ldx, Y, l, n, l, mr, o, h->work, h->work_elems, h->st);
+    ENMF_TRY(ar(h, Z, (size_t)(n * l), CommOp::Sum));
+    ENMF_TRY(cholqr(h, Z, tmp, n, l, false, G, R, Rinv, bad));
+    o.C = Y;
+    gemm<float, double>(false, h->X, h->ldx, Z, l, mr, l, n, o, h->work, h->work_elems, h->st);
+    ENMF_TRY(cholqr(h, Y, tmp, mr, l, sh, G, R, Rinv, bad));
+  }
+  // B^T = X^T Q (n x l); B B^T = Qt^T Qt = Ve diag(s) Ve^T; sigma = sqrt(s)
+  o.C = Qt;
+  gemm<float, double>(true, h->X, h->ldx, Y, l, n, l, mr, o, h->work, h->work_elems, h->st);
+  ENMF_TRY(ar(h, Qt, (size_t)(n * l), CommOp::Sum));
+  o.C = G;
+  gemm<double, double>(true, Qt, l, Qt, l, l, l, n, o, h->work, h->work_elems, h->st);
+  jacobi_svd(G, l, Ue, sv, Ve, jw, h->st);
+  std::vector<double> hs(l);
+  CUDA_TRY(cudaMemcpyAsync(hs.data(), sv, sizeof(double) * l, cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  ENMF_TRY(check_launch());
+  std::vector<double> sig(r);
+  for (int k = 0; k < r; ++k) sig[k] = sqrt(std::max(hs[k], 0.0));
+  if (!(sig[0] > 0.0)) return ENMF_ERR_RANK_DEFICIENT;
+  int deficient = 0;
+  // left singular vectors Q Ve_r (unscaled) for the sign rule R5
+  o.C = Us;
+  o.ldc = r;
+  gemm<double, double>(false, Y, l, Ve, l, mr, r, l, o, h->work, h->work_elems, h->st);
+  std::vector<double> sgn;
+  ENMF_TRY(column_signs(h, Us, mr, r, h->prob.row_begin, sgn));
+  std::vector<double> cu(r), cv(r);
+  for (int k = 0; k < r; ++k) {
+    const bool zero = sig[k] <= 1e-7 * sig[0];
+    deficient += zero;
+    cu[k] = zero ? 0.0 : sgn[k] * sqrt(sig[k]);          // U* = U S^1/2
+    cv[k] = zero ? 0.0 : sgn[k] / sqrt(sig[k]);          // V* = B^T U S^-1 S^1/2
+  }
+  double* dcs = h->work;   // 2r column scales
+  CUDA_TRY(cudaMemcpyAsync(dcs, cu.data(), sizeof(double) * r, cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaMemcpyAsync(dcs + r, cv.data(), sizeof(double) * r, cudaMemcpyHostToDevice, h->st));
+  scale_cols_f64(Us, mr, r, dcs, h->st);
+  CUDA_TRY(cudaMemcpyAsync(h->W64, Us, sizeof(double) * mr * r, cudaMemcpyDeviceToDevice, h->st));
+  o.C = Us;
+  gemm<double, double>(false, Qt, l, Ve, l, n, r, l, o, h->work + 2 * r, h->work_elems - 2 * r,
+                       h->st);
+  scale_cols_f64(Us, n, r, dcs + r, h->st);
+  CUDA_TRY(cudaMemcpyAsync(h->W64 + mr * r, Us, sizeof(double) * n * r,
+                           cudaMemcpyDeviceToDevice, h->st));
+  f64_to_f32(h->W64, mr, r, nullptr, U, ldu, h->st);
+  f64_to_f32(h->W64 + mr * r, n, r, nullptr, V, ldv, h->st);
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  ENMF_TRY(check_launch());
+  if (sigma_host)
+    for (int k = 0; k < r; ++k) sigma_host[k] = sig[k];
+  if (info) {
+    memset(info->sigma, 0, sizeof(info->sigma));
+    for (int k = 0; k < r; ++k) info->sigma[k] = sig[k];
+    info->rank_deficient = deficient;
+  }
+  return ENMF_OK;
+}
+
+// Alg. 1 from W64 = [U*; V*] (this rank's U rows, all V rows); writes U = U* R, V = V* R.
+enmf_status_t rotate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                          enmf_init_info_t* info) {
+  const int64_t mr = h->m_loc, n = h->n, rows = mr + n;
+  const int r = (int)h->r;
+  const int64_t count = rows * r;
+  const bool sh = h->prob.world_size > 1;
+  DevBuf db;
+  double *WR, *Yh, *Z, *B, *R, *M, *Cs, *Ds, *sv, *jw;
+  unsigned long long* third;
+  ENMF_TRY(db.get(&WR, (size_t)count));
+  ENMF_TRY(db.get(&Yh, (size_t)count));
+  ENMF_TRY(db.get(&Z, (size_t)count));
+  ENMF_TRY(db.get(&B, (size_t)count));
+  ENMF_TRY(db.get(&R, (size_t)r * r));
+  ENMF_TRY(db.get(&M, (size_t)2 * r * r));
+  ENMF_TRY(db.get(&Cs, (size_t)r * r));
+  ENMF_TRY(db.get(&Ds, (size_t)r * r));
+  ENMF_TRY(db.get(&sv, (size_t)r));
+  ENMF_TRY(db.get(&jw, (size_t)2 * r * r));
+  ENMF_TRY(db.get(&third, 1));
+  CUDA_TRY(cudaMemsetAsync(third, 0, sizeof(unsigned long long), h->st));
+  double* W = h->W64;
+  // negativity of the unrotated point (info) and max|W| for reading R7
+  double neg0u = 0.0, neg0v = 0.0;
+  ENMF_TRY(negativity(h, W, mr * r, &neg0u));
+  ENMF_TRY(negativity(h, W + mr * r, n * r, &neg0v));
+  std::vector<double> hp;
+  colabsmax(W, rows, r, 0, h->parts, h->st);
+  {
+    const int np = colabsmax_parts();
+    hp.resize((size_t)np * r * 3);
+    CUDA_TRY(cudaMemcpyAsync(hp.data(), h->parts, sizeof(double) * hp.size(),
+                             cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+  }
+  double wmax = 0.0;
+  for (size_t e = 0; e < hp.size(); e += 3) wmax = std::max(wmax, hp[e]);
+  if (sh) {
+    CUDA_TRY(cudaMemcpyAsync(h->dscal + S_WMAX, &wmax, sizeof(double), cudaMemcpyHostToDevice,
+                             h->st));
+    ENMF_TRY(ar(h, h->dscal + S_WMAX, 1, CommOp::Max));
+    CUDA_TRY(cudaMemcpyAsync(&wmax, h->dscal + S_WMAX, sizeof(double), cudaMemcpyDeviceToHost,
+                             h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+  }
+  const double inv_rho = h->opt.admm_rho > 0.0 ? 1.0 / h->opt.admm_rho
+                                                : (wmax > 0.0 ? 1000.0 * wmax : 1.0);
+  CUDA_TRY(cudaMemsetAsync(third, 0, sizeof(unsigned long long), h->st));
+  std::vector<double> eye((size_t)r * r, 0.0);
+  for (int a = 0; a < r; ++a) eye[(size_t)a * r + a] = 1.0;             // R0 = I (R6)
+  CUDA_TRY(cudaMemcpyAsync(R, eye.data(), sizeof(double) * r * r, cudaMemcpyHostToDevice, h->st));
+  GemmOut o;
+  o.ldc = r;
+  for (int t = 0; t < h->opt.admm_iters; ++t) {
+    o.C = WR;
+    gemm<double, double>(false, W, r, R, r, rows, r, r, o, h->work, h->work_elems, h->st);
+    admm_z(WR, Yh, Z, B, count, inv_rho, t == 0, h->parts, third, h->st);
+    // M = W^T (Z + Y/rho) = W^T B, U rows summed over ranks, V rows counted once
+    if (!sh) {
+      o.C = M;
+      gemm<double, double>(true, W, r, B, r, r, r, rows, o, h->work, h->work_elems, h->st);
+    } else {
+      o.C = M;
+      gemm<double, double>(true, W, r, B, r, r, r, mr, o, h->work, h->work_elems, h->st);
+      if (h->prob.rank == 0) {
+        o.C = M + r * r;
+        gemm<double, double>(true, W + mr * r, r, B + mr * r, r, r, r, n, o, h->work,
+                             h->work_elems, h->st);
+      } else {
+        CUDA_TRY(cudaMemsetAsync(M + r * r, 0, sizeof(double) * r * r, h->st));
+      }
+      reduce_parts(M, 2, (int64_t)r * r, Cs, h->st);
+      CUDA_TRY(cudaMemcpyAsync(M, Cs, sizeof(double) * r * r, cudaMemcpyDeviceToDevice, h->st));
+      ENMF_TRY(ar(h, M, (size_t)r * r, CommOp::Sum));
+    }
+    // R = C D^T from W^T B = C S D^T (orthogonal Procrustes)
+    jacobi_svd(M, r, Cs, sv, Ds, jw, h->st);
+    procrustes_from_svd(Cs, sv, Ds, r, R, h->st);
+  }
+  ENMF_TRY(check_launch());
+  unsigned long long third_h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&third_h, third, sizeof(third_h), cudaMemcpyDeviceToHost, h->st));
+  // (U, V) = (U* R, V* R)   (Alg. 3)
+  o.C = WR;
+  gemm<double, double>(false, W, r, R, r, rows, r, r, o, h->work, h->work_elems, h->st);
+  f64_to_f32(WR, mr, r, nullptr, U, ldu, h->st);
+  f64_to_f32(WR + mr * r, n, r, nullptr, V, ldv, h->st);
+  double negu = 0.0, negv = 0.0;
+  ENMF_TRY(negativity(h, WR, mr * r, &negu));
+  ENMF_TRY(negativity(h, WR + mr * r, n * r, &negv));
+  std::vector<double> hR((size_t)r * r);
+  CUDA_TRY(cudaMemcpyAsync(hR.data(), R, sizeof(double) * r * r, cudaMemcpyDeviceToHost, h->st));
+  // lift constants from the rotated point, fixed for the whole ascent stage (R9)
+  ENMF_TRY(min_factor(h, U, ldu, mr, S_MINU, sh));
+  ENMF_TRY(min_factor(h, V, ldv, n, S_MINV, false));
+  double mins[2];
+  CUDA_TRY(cudaMemcpyAsync(mins, h->dscal + S_MINU, sizeof(mins), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  ENMF_TRY(check_launch());
+  const double L = (double)h->opt.lift_steps;
+  const double lu = mins[0] < 0 ? (1.0 + 1e-3) * (-mins[0]) / L : 0.0;
+  const double lv = mins[1] < 0 ? (1.0 + 1e-3) * (-mins[1]) / L : 0.0;
+  ENMF_TRY(enmf_set_stage(h, 0, lu, lv));
+  if (info) {
+    double orth = 0.0;
+    for (int a = 0; a < r; ++a)
+      for (int b = 0; b < r; ++b) {
+        double s = 0.0;
+        for (int c = 0; c < r; ++c) s += hR[(size_t)c * r + a] * hR[(size_t)c * r + b];
+        orth = std::max(orth, fabs(s - (a == b ? 1.0 : 0.0)));
+      }
+    info->orth_residual = orth;
+    info->negativity_svd = neg0u + neg0v;
+    info->negativity_rot = negu + negv;
+    info->admm_third_branch = (int64_t)third_h;
+    info->lambda_u = lu;
+    info->lambda_v = lv;
+  }
+  return ENMF_OK;
+}
+
+enmf_status_t xnorm2_host(enmf_handle_t h, double* out) {
+  CUDA_TRY(cudaMemcpyAsync(out, h->dscal + S_XNORM2, sizeof(double), cudaMemcpyDeviceToHost,
+                           h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return ENMF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+enmf_status_t enmf_svd(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                       double* sigma_host) {
+  if (!h) return ENMF_ERR_INVALID_ARG;
+  if (!h->bound) return ENMF_ERR_STATE;
+  ENMF_TRY(validate_ld(U, ldu, h->r));
+  ENMF_TRY(validate_ld(V, ldv, h->r));
+  LaunchScope ls(h);
+  return svd_core(h, U, ldu, V, ldv, sigma_host, nullptr);
+}
+
+enmf_status_t enmf_rotate(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                          enmf_init_info_t* info) {
+  if (!h) return ENMF_ERR_INVALID_ARG;
+  if (!h->bound) return ENMF_ERR_STATE;
+  ENMF_TRY(validate_ld(U, ldu, h->r));
+  ENMF_TRY(validate_ld(V, ldv, h->r));
+  LaunchScope ls(h);
+  if (!h->W64) ENMF_TRY(dalloc(&h->W64, (size_t)((h->m_loc + h->n) * h->r)));
+  f32_to_f64(U, ldu, h->m_loc, h->r, h->W64, h->st);
+  f32_to_f64(V, ldv, h->n, h->r, h->W64 + h->m_loc * h->r, h->st);
+  ENMF_TRY(rotate_core(h, U, ldu, V, ldv, info));
+  if (info) ENMF_TRY(xnorm2_host(h, &info->xnorm2));
+  return ENMF_OK;
+}
+
+enmf_status_t enmf_init(enmf_handle_t h, const float* X, int64_t ldx, float* U, int64_t ldu,
+                        float* V, int64_t ldv, enmf_init_info_t* info) {
+  if (!h) return ENMF_ERR_INVALID_ARG;
+  ENMF_TRY(validate_ld(U, ldu, h->r));
+  ENMF_TRY(validate_ld(V, ldv, h->r));
+  ENMF_TRY(enmf_set_data(h, X, ldx));
+  LaunchScope ls(h);
+  enmf_init_info_t tmp;
+  enmf_init_info_t* inf = info ? info : &tmp;
+  memset(inf, 0, sizeof(*inf));
+  ENMF_TRY(svd_core(h, U, ldu, V, ldv, nullptr, inf));
+  ENMF_TRY(rotate_core(h, U, ldu, V, ldv, inf));   // from the fp64 W64 of svd_core
+  ENMF_TRY(xnorm2_host(h, &inf->xnorm2));
+  return ENMF_OK;
+}
+
+enmf_status_t enmf_solve_host(enmf_handle_t h, const float* X_host, float* U_host,
+                              float* V_host, int n_iters, double* f_trace_host,
+                              enmf_init_info_t* info) {
+  if (!h || !X_host || !U_host || !V_host || n_iters < 0) return ENMF_ERR_INVALID_ARG;
+  if (h->prob.world_size != 1) return ENMF_ERR_STATE;
+  const int64_t m = h->m_loc, n = h->n, r = h->r;
+  if (!h->x_owned) ENMF_TRY(dalloc(&h->x_owned, (size_t)(m * n)));
+  // host -> device through two pinned staging buffers, copies overlapped with memcpy
+  const size_t chunk = (size_t)64 << 20;
+  char* pin[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2];
+  CUDA_TRY(cudaMallocHost((void**)&pin[0], chunk));
+  CUDA_TRY(cudaMallocHost((void**)&pin[1], chunk));
+  CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  const size_t total = sizeof(float) * (size_t)(m * n);
+  const char* src = (const char*)X_host;
+  char* dst = (char*)h->x_owned;
+  int b = 0;
+  bool used[2] = {false, false};
+  for (size_t off = 0; off < total; off += chunk, b ^= 1) {
+    const size_t len = std::min(chunk, total - off);
+    if (used[b]) CUDA_TRY(cudaEventSynchronize(ev[b]));
+    memcpy(pin[b], src + off, len);
+    CUDA_TRY(cudaMemcpyAsync(dst + off, pin[b], len, cudaMemcpyHostToDevice, h->st));
+    CUDA_TRY(cudaEventRecord(ev[b], h->st));
+    used[b] = true;
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  cudaFreeHost(pin[0]);
+  cudaFreeHost(pin[1]);
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  float *dU, *dV;
+  DevBuf db;
+  ENMF_TRY(db.get(&dU, (size_t)(m * r)));
+  ENMF_TRY(db.get(&dV, (size_t)(n * r)));
+  ENMF_TRY(enmf_init(h, h->x_owned, n, dU, r, dV, r, info));
+  ENMF_TRY(enmf_iterate(h, dU, r, dV, r, n_iters, f_trace_host, nullptr));
+  CUDA_TRY(cudaMemcpyAsync(U_host, dU, sizeof(float) * m * r, cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaMemcpyAsync(V_host, dV, sizeof(float) * n * r, cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return ENMF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+// handle.h -- the enmf handle and the orchestration helpers shared by enmf_capi.cu and
+// enmf_init.cu (private to libenmf.so).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include <vector>
+
+#include "comm.h"
+#include "enmf.h"
+#include "internal.h"
+#include "tc.h"
+
+namespace enmf {
+
+// device scalar slots (doubles)
+enum {
+  S_XNORM2 = 0, S_XMIN, S_XBAD, S_MINU, S_MINV, S_CROSS, S_LAMU, S_LAMV, S_NEG, S_SCRATCH,
+  S_WMAX, S_COUNT = 16
+};
+// device int slots
+enum { I_STAGE = 0, I_KSTAR_U, I_KSTAR_V, I_CNT_ASC, I_CNT_HALS, I_BAD, I_COUNT = 8 };
+
+}  // namespace enmf
+
+struct enmf_handle_s {
+  enmf_problem_t prob{};
+  enmf_options_t opt{};
+  cudaStream_t st = nullptr;
+  int64_t m_loc = 0, n = 0, r = 0;
+  const float* X = nullptr;
+  int64_t ldx = 0;
+  bool bound = false;
+  bool stage_known_hals = false;   // host mirror: once HALS, always HALS
+  enmf::Comm* comm = nullptr;
+  int64_t launches = 0;
+  int precision = ENMF_PREC_FP64;
+  double* dscal = nullptr;
+  int* dint = nullptr;
+  double* P = nullptr;       // m_loc x r
+  double* Q = nullptr;       // n x r
+  double* GU = nullptr;      // r x r
+  double* GV = nullptr;      // r x r
+  double* work = nullptr;    // split-K partials and small dense scratch
+  size_t work_elems = 0;
+  double* parts = nullptr;   // reduction partials
+  size_t parts_elems = 0;
+  double* minparts = nullptr;
+  double* pgsum = nullptr;   // max_iter + 1
+  float* snaps = nullptr;    // max_iter x max(m_loc, n) x r
+  double* ftrace = nullptr;
+  int ftrace_cap = 0;
+  enmf::TcState* tc = nullptr;
+  float* x_owned = nullptr;  // device copy of X owned by enmf_solve_host
+  double* W64 = nullptr;     // (m_loc + n) x r fp64 [U*; V*] kept from enmf_svd for enmf_rotate
+  // profiling of the X passes (enmf_set_profiling): CUDA events around every contraction
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<int> ev_kind;  // 0 = X V, 1 = X^T U, per event pair
+  size_t ev_used = 0;
+  double prof_ms[2] = {0.0, 0.0};
+  int64_t prof_cnt[2] = {0, 0};
+};
+
+namespace enmf {
+
+struct LaunchScope {
+  explicit LaunchScope(enmf_handle_t h) { g_launch_counter = &h->launches; }
+  ~LaunchScope() { g_launch_counter = nullptr; }
+};
+
+#define CUDA_TRY(x)                                                                  \
+  do {                                                                               \
+    cudaError_t _e = (x);                                                            \
+    if (_e != cudaSuccess) {                                                         \
+      fprintf(stderr, "enmf: CUDA error %s at %s:%d\n", cudaGetErrorString(_e),     \
+              __FILE__, __LINE__);                                                   \
+      return _e == cudaErrorMemoryAllocation ? ENMF_ERR_OOM : ENMF_ERR_CUDA;         \
+    }                                                                                \
+  } while (0)
+
+#define ENMF_TRY(x)                        \
+  do {                                     \
+    enmf_status_t _s = (x);                \
+    if (_s != ENMF_OK) return _s;          \
+  } while (0)
+
+enmf_status_t check_launch();
+enmf_status_t dalloc_bytes(void** p, size_t bytes);
+template <typename T>
+enmf_status_t dalloc(T** p, size_t count) {
+  return dalloc_bytes((void**)p, sizeof(T) * (count ? count : 1));
+}
+enmf_status_t ar(enmf_handle_t h, double* buf, size_t count, CommOp op);
+enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* P);
+enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q);
+enmf_status_t gram_f32(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, double* G,
+                       bool sharded);
+enmf_status_t min_factor(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, int slot,
+                         bool sharded);
+enmf_status_t validate_ld(const void* p, int64_t ld, int64_t cols);
+
+}  // namespace enmf

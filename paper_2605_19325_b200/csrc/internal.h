@@ -1,0 +1,122 @@
+// internal.h -- launchers shared by the translation units of libenmf.so (not installed).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "enmf.h"
+
+namespace enmf {
+
+constexpr int kSMs = 148;
+constexpr int kMaxRankPad = 128;    // r padded to 32*CPL <= 128 in the row-block kernels
+
+// Counts kernel launches issued by the library (reported by enmf_launch_count).
+extern thread_local int64_t* g_launch_counter;
+inline void count_launch(int n = 1) {
+  if (g_launch_counter) *g_launch_counter += n;
+}
+
+// ---------------------------------------------------------------- SIMT fp64 GEMMs
+// C = op(A) * B accumulated in fp64, op(A) = A (M x K, row-major, lda) or A^T where A is
+// (K x M, row-major, lda).  B is K x N (row-major, ldb).  TA/TB are float or double.
+// The K range is split over `splits` CTAs layers; partial results go to
+// work[s*M*N + i*N + j] and are summed in split order (deterministic).  The final result
+// is written to C (fp64, ldc) or, if Cf != nullptr, converted to fp32 into Cf (ldcf)
+// after multiplication by colscale[j] (may be null).
+struct GemmOut {
+  double* C = nullptr;
+  int64_t ldc = 0;
+  float* Cf = nullptr;
+  int64_t ldcf = 0;
+  const double* colscale = nullptr;
+};
+template <typename TA, typename TB>
+void gemm(bool transA, const TA* A, int64_t lda, const TB* B, int64_t ldb, int64_t M,
+          int64_t N, int64_t K, GemmOut out, double* work, size_t work_elems,
+          cudaStream_t st);
+
+// Deterministic sum of `parts` contiguous blocks of `len` doubles into out.
+void reduce_parts(const double* parts, int nparts, int64_t len, double* out, cudaStream_t st);
+
+// ---------------------------------------------------------------- elementwise / reductions
+// sum of squares, min and non-finite count of X (rows x n): writes {sum, min, nonfinite}.
+void x_stats(const float* X, int64_t ldx, int64_t rows, int64_t n, double* parts, int nparts,
+             double* out3, cudaStream_t st);
+int x_stats_parts(int64_t rows);
+// min over an fp32 matrix (rows x cols, ld): partials then out[0].
+void min_f32(const float* A, int64_t ld, int64_t rows, int64_t cols, double* parts,
+             double* out, cudaStream_t st);
+// out = <A, B> (A fp64 rows x cols ld=cols, B fp32 ld) via partials.
+void dot_f64_f32(const double* A, const float* B, int64_t ldb, int64_t rows, int64_t cols,
+                 double* parts, double* out, cudaStream_t st);
+// fp64 (ld=cols) -> fp32 strided copy with optional per-column scale.
+void f64_to_f32(const double* A, int64_t rows, int64_t cols, const double* colscale,
+                float* B, int64_t ldb, cudaStream_t st);
+void f32_to_f64(const float* A, int64_t lda, int64_t rows, int64_t cols, double* B,
+                cudaStream_t st);
+// Gaussian test matrix Omega (rows x cols, fp64) from Philox4x32-10 keyed by seed.
+void gaussian_fill(double* A, int64_t rows, int64_t cols, uint64_t seed, cudaStream_t st);
+
+// ---------------------------------------------------------------- row-block updates
+// HALS on F (rows x r fp32) with cross term C (rows x r fp64) and Gram G (r x r fp64).
+// Runs only if *stage == want (device flag).  min partials to minparts[kRowGrid].
+constexpr int kRowGrid = 2 * kSMs;
+constexpr int kRowWarps = 8;
+void hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
+               const int* stage, double* minparts, cudaStream_t st);
+// PBCD phase A (all max_iter inner iterations, snapshots of every iterate, per-warp
+// partial ||M o grad||^2 for each iteration 0..max_iter), runs only in the ascent stage.
+void pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
+               const double* G, const double* lam, int max_iter, float* snaps,
+               double* pgparts, const int* stage, cudaStream_t st);
+int pbcd_parts();
+// Selects k* from the partials (eps rule of Alg. 2), copies snapshot k* into F and
+// writes min partials; records k* into *kstar.
+void pbcd_commit(float* F, int64_t ldf, int64_t rows, int r, const float* snaps,
+                 const double* pgparts, double eps, int max_iter, int* kstar,
+                 const int* stage, double* minparts, cudaStream_t st);
+// KKT partial statistics of one block (F, C = cross term, G): 8 values per warp slot.
+void kkt_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
+              const double* G, double* parts, cudaStream_t st);
+int kkt_parts();
+// Direct objective sum (X - U V^T)^2 partials.
+void frob_direct(const float* X, int64_t ldx, int64_t rows, int64_t n, const float* U,
+                 int64_t ldu, const float* V, int64_t ldv, int r, double* parts, int* nparts,
+                 cudaStream_t st);
+
+// ---------------------------------------------------------------- small dense (one CTA)
+// Upper Cholesky G = R^T R of a k x k SPD matrix (row-major, ld k) with diagonal shift,
+// and Rinv = R^{-1}.  *bad = number of non-positive pivots (replaced by tiny values).
+void chol_inv(const double* G, int k, double shift_rel, double* R, double* Rinv, int* bad,
+              cudaStream_t st);
+// One-sided Jacobi SVD of a k x k matrix A (row-major): A = U diag(s) V^T, s descending.
+// Uo, Vo are k x k row-major.  work >= 2*k*k doubles.
+void jacobi_svd(const double* A, int k, double* Uo, double* s, double* Vo, double* work,
+                cudaStream_t st);
+// R = C D^T from the SVD W^T B = C S D^T (orthogonal Procrustes), completing C's basis
+// for zero singular values.
+void procrustes_from_svd(const double* Cm, const double* s, const double* Dm, int k, double* R,
+                         cudaStream_t st);
+
+// ---------------------------------------------------------------- stage / scalars
+// stage[0]: 0 ascent, 1 HALS.  Switches to HALS when min U >= 0 and min V >= 0.
+void stage_update(int* stage, const double* minu, const double* minv, int* counters,
+                  cudaStream_t st);
+// f = xnorm2 - 2 cross + gg, stored to *fout.
+void objective_finish(const double* xnorm2, const double* cross, const double* gu,
+                      const double* gv, int r, double* fout, cudaStream_t st);
+// min over partial buffers.
+void reduce_min(const double* parts, int n, double* out, cudaStream_t st);
+// ADMM elementwise step (see kernels_small.cu).
+void admm_z(const double* WR, double* Yh, double* Z, double* B, int64_t count, double inv_rho,
+            int first, double* negparts, unsigned long long* third, cudaStream_t st);
+// sum of h(A) = max(0, -A) over count entries into *out (device).
+void negsum(const double* A, int64_t count, double* parts, double* out, cudaStream_t st);
+// sign rule R5 helpers
+void colabsmax(const double* A, int64_t rows, int r, int64_t row_offset, double* parts,
+               cudaStream_t st);
+int colabsmax_parts();
+void colabsmax_finish(const double* parts, int r, double* sign_out, cudaStream_t st);
+void scale_cols_f64(double* A, int64_t rows, int r, const double* s, cudaStream_t st);
+
+}  // namespace enmf

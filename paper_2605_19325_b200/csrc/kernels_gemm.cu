@@ -1,0 +1,196 @@
+// kernels_gemm.cu -- SIMT GEMMs with fp64 accumulation (the ENMF_PREC_FP64 path and the
+// small dense products of init / ADMM).
+//
+// Used for the cross terms X V and X^T U, the Grams U^T U, V^T V, the
+// range-finder products X Omega, X^T Q and the ADMM products W R,
+// W^T B.  64x64 output tiles, 16-deep K slabs staged in shared memory
+// as fp64, 4x4 register tile per thread (rows ty+16a, cols tx+16b so both operand reads
+// are conflict-free / broadcast), split-K layers reduced in a fixed order.
+#include "internal.h"
+
+namespace enmf {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+template <typename TA, typename TB, bool TRANS>
+__global__ void __launch_bounds__(256)
+gemm_kernel(const TA* __restrict__ A, int64_t lda, const TB* __restrict__ B, int64_t ldb,
+            int64_t M, int64_t N, int64_t K, int64_t kchunk, double* __restrict__ out,
+            int64_t ldo, int64_t split_stride) {
+  __shared__ double As[BK][BM + 1];
+  __shared__ double Bs[BK][BN];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int64_t i0 = (int64_t)blockIdx.y * BM, j0 = (int64_t)blockIdx.x * BN;
+  const int64_t kb = (int64_t)blockIdx.z * kchunk;
+  const int64_t ke = K < kb + kchunk ? K : kb + kchunk;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = t + 256 * q;
+      int ii, kk;
+      if (TRANS) { kk = e / BM; ii = e % BM; }
+      else { ii = e / BK; kk = e % BK; }
+      const int64_t gi = i0 + ii, gk = k0 + kk;
+      double v = 0.0;
+      if (gi < M && gk < ke) v = (double)(TRANS ? A[gk * lda + gi] : A[gi * lda + gk]);
+      As[kk][ii] = v;
+      const int kb2 = e / BN, jj = e % BN;
+      const int64_t gj = j0 + jj, gk2 = k0 + kb2;
+      Bs[kb2][jj] = (gj < N && gk2 < ke) ? (double)B[gk2 * ldb + gj] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[kk][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+  double* o = out + (int64_t)blockIdx.z * split_stride;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t gi = i0 + ty + 16 * a;
+    if (gi >= M) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int64_t gj = j0 + tx + 16 * b;
+      if (gj < N) o[gi * ldo + gj] = acc[a][b];
+    }
+  }
+}
+
+__global__ void reduce_parts_kernel(const double* __restrict__ parts, int nparts, int64_t len,
+                                    double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += parts[(int64_t)p * len + e];
+    out[e] = s;
+  }
+}
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ A, int64_t rows, int64_t cols,
+                                  const double* __restrict__ colscale, float* __restrict__ B,
+                                  int64_t ldb) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    double v = A[e];
+    if (colscale) v *= colscale[j];
+    B[i * ldb + j] = (float)v;
+  }
+}
+
+__global__ void f32_to_f64_kernel(const float* __restrict__ A, int64_t lda, int64_t rows,
+                                  int64_t cols, double* __restrict__ B) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    B[e] = (double)A[i * lda + j];
+  }
+}
+
+inline int grid_for(int64_t n, int per = 256) {
+  int64_t g = (n + per - 1) / per;
+  return (int)(g < 4 * kSMs ? (g < 1 ? 1 : g) : 4 * kSMs);
+}
+
+}  // namespace
+
+template <typename TA, typename TB>
+void gemm(bool transA, const TA* A, int64_t lda, const TB* B, int64_t ldb, int64_t M,
+          int64_t N, int64_t K, GemmOut out, double* work, size_t work_elems,
+          cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  int64_t splits = (2 * kSMs + tiles - 1) / tiles;
+  const int64_t kmax = (K + 255) / 256;
+  if (splits > kmax) splits = kmax;
+  if (splits < 1) splits = 1;
+  const int64_t need_extra = (out.Cf || (out.C && out.ldc != N)) ? 1 : 0;
+  while (splits > 1 && (size_t)((splits + need_extra) * M * N) > work_elems) --splits;
+  int64_t kchunk = (K + splits - 1) / splits;
+  kchunk = ((kchunk + BK - 1) / BK) * BK;
+  if (kchunk < BK) kchunk = BK;
+  splits = (K + kchunk - 1) / kchunk;
+  if (splits < 1) splits = 1;
+  const bool direct = splits == 1 && out.C != nullptr;
+  double* dst = direct ? out.C : work;
+  const int64_t ldo = direct ? out.ldc : N;
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)splits);
+  if (K <= 0) {
+    // empty contraction: C = 0
+    cudaMemsetAsync(work, 0, sizeof(double) * M * N, st);
+    splits = 1;
+    dst = work;
+  } else if (transA) {
+    gemm_kernel<TA, TB, true><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, kchunk, dst, ldo,
+                                                    M * N);
+    count_launch();
+  } else {
+    gemm_kernel<TA, TB, false><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, kchunk, dst, ldo,
+                                                     M * N);
+    count_launch();
+  }
+  if (direct && K > 0) return;
+  double* res = work;
+  if (splits > 1) {
+    res = out.Cf ? work + splits * M * N : nullptr;
+    if (out.C && !out.Cf && out.ldc == N) {
+      reduce_parts(work, (int)splits, M * N, out.C, st);
+      return;
+    }
+    if (!res) res = work + splits * M * N;
+    reduce_parts(work, (int)splits, M * N, res, st);
+  }
+  if (out.Cf) {
+    f64_to_f32(res, M, N, out.colscale, out.Cf, out.ldcf, st);
+  } else if (out.C) {
+    cudaMemcpy2DAsync(out.C, sizeof(double) * out.ldc, res, sizeof(double) * N,
+                      sizeof(double) * N, M, cudaMemcpyDeviceToDevice, st);
+  }
+}
+
+template void gemm<float, float>(bool, const float*, int64_t, const float*, int64_t, int64_t,
+                                 int64_t, int64_t, GemmOut, double*, size_t, cudaStream_t);
+template void gemm<float, double>(bool, const float*, int64_t, const double*, int64_t, int64_t,
+                                  int64_t, int64_t, GemmOut, double*, size_t, cudaStream_t);
+template void gemm<double, double>(bool, const double*, int64_t, const double*, int64_t,
+                                   int64_t, int64_t, int64_t, GemmOut, double*, size_t,
+                                   cudaStream_t);
+template void gemm<double, float>(bool, const double*, int64_t, const float*, int64_t, int64_t,
+                                  int64_t, int64_t, GemmOut, double*, size_t, cudaStream_t);
+
+void reduce_parts(const double* parts, int nparts, int64_t len, double* out, cudaStream_t st) {
+  reduce_parts_kernel<<<grid_for(len), 256, 0, st>>>(parts, nparts, len, out);
+  count_launch();
+}
+
+void f64_to_f32(const double* A, int64_t rows, int64_t cols, const double* colscale, float* B,
+                int64_t ldb, cudaStream_t st) {
+  f64_to_f32_kernel<<<grid_for(rows * cols), 256, 0, st>>>(A, rows, cols, colscale, B, ldb);
+  count_launch();
+}
+
+void f32_to_f64(const float* A, int64_t lda, int64_t rows, int64_t cols, double* B,
+                cudaStream_t st) {
+  f32_to_f64_kernel<<<grid_for(rows * cols), 256, 0, st>>>(A, lda, rows, cols, B);
+  count_launch();
+}
+
+}  // namespace enmf

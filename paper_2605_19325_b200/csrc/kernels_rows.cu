@@ -1,0 +1,427 @@
+// kernels_rows.cu -- row-block factor updates of the exterior method.
+//
+// Rows of U (and of V) are independent given the cross term C (= X V or X^T U) and the
+// Gram G ("we can leverage this to update the rows of U and V
+// independently"), so every kernel here maps RB rows to one warp: lane L owns columns
+// L, L+32, ... (CPL = ceil(r/32) of them), the r x r Gram sits in shared memory (fp64,
+// zero-padded to 32*CPL), and the row vectors live in registers in fp64.  One G row
+// load serves RB rows, which keeps the fp64 FMA pipe (not shared-memory bandwidth) the
+// bound.
+//
+//   hals_kernel   HALS column sweep, Gauss-Seidel over k with an
+//                 incrementally updated residual t = C - u G.
+//   pbcd_kernel   Alg. 2: lift (Eq.6/7), mask (line 336), then all
+//                 max_iter inner iterations of Eq.(8) with the Eq.(10) step, snapshotting
+//                 each iterate and accumulating ||M o grad||^2 per iteration; the global
+//                 stopping rule is applied afterwards by pbcd_select (k*), see DESIGN.md.
+//   kkt_kernel    App. G residual statistics.
+#include <float.h>
+
+#include "internal.h"
+
+namespace enmf {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+
+// out[b][c] += sign * sum_l S[b][l] G[l][lane + 32c]   (S held lane-distributed like out)
+template <int CPL, int RB>
+__device__ __forceinline__ void row_times_gram(const double (&S)[RB][CPL], const double* Gs,
+                                               int r, int lane, double sign,
+                                               double (&out)[RB][CPL]) {
+  constexpr int RP = 32 * CPL;
+#pragma unroll
+  for (int s = 0; s < CPL; ++s) {
+    const int lmax = r - 32 * s < 32 ? r - 32 * s : 32;
+#pragma unroll 4
+    for (int ll = 0; ll < lmax; ++ll) {
+      const int l = 32 * s + ll;
+      double gl[CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) gl[c] = Gs[l * RP + lane + 32 * c];
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        const double sv = sign * __shfl_sync(FULL, S[b][s], ll);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) out[b][c] = fma(sv, gl[c], out[b][c]);
+      }
+    }
+  }
+}
+
+template <int CPL>
+__device__ __forceinline__ void load_gram(const double* G, int r, double* Gs) {
+  constexpr int RP = 32 * CPL;
+  for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) {
+    const int l = e / RP, j = e % RP;
+    Gs[e] = (l < r && j < r) ? G[l * r + j] : 0.0;
+  }
+}
+
+template <int CPL, int RB>
+__global__ void __launch_bounds__(32 * kRowWarps)
+hals_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r, const double* __restrict__ C,
+            const double* __restrict__ G, const int* __restrict__ stage, double* minparts) {
+  constexpr int RP = 32 * CPL;
+  extern __shared__ double smem[];
+  double* Gs = smem;
+  __shared__ double wmin_s[kRowWarps];
+  const bool active = stage == nullptr || *stage == 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double wmin = DBL_MAX;
+  if (active) {
+    load_gram<CPL>(G, r, Gs);
+    __syncthreads();
+    const int64_t nblk = (rows + RB - 1) / RB;
+    for (int64_t rb = (int64_t)blockIdx.x * kRowWarps + warp; rb < nblk;
+         rb += (int64_t)gridDim.x * kRowWarps) {
+      double u[RB][CPL], t[RB][CPL];
+#pragma unroll
+      for (int b = 0; b < RB; ++b)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int64_t row = rb * RB + b;
+          const int col = lane + 32 * c;
+          const bool ok = row < rows && col < r;
+          u[b][c] = ok ? (double)F[row * ldf + col] : 0.0;
+          t[b][c] = ok ? C[row * r + col] : 0.0;
+        }
+      row_times_gram<CPL, RB>(u, Gs, r, lane, -1.0, t);      // t = C - u G
+#pragma unroll
+      for (int s = 0; s < CPL; ++s) {
+        const int kmax = r - 32 * s < 32 ? r - 32 * s : 32;
+        for (int kk = 0; kk < kmax; ++kk) {
+          const int k = 32 * s + kk;
+          const double gkk = Gs[k * RP + k];
+          double gk[CPL];
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) gk[c] = Gs[k * RP + lane + 32 * c];
+#pragma unroll
+          for (int b = 0; b < RB; ++b) {
+            const double tk = __shfl_sync(FULL, t[b][s], kk);
+            const double uk = __shfl_sync(FULL, u[b][s], kk);
+            // U_ik <- max(0, U_ik + (C_ik - sum_l U_il G_lk) / G_kk)   (skip if G_kk <= 0)
+            const double nu = gkk > 0.0 ? fmax(0.0, uk + tk / gkk) : uk;
+            const double d = nu - uk;
+            if (lane == kk) u[b][s] = nu;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) t[b][c] = fma(-d, gk[c], t[b][c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < RB; ++b)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int64_t row = rb * RB + b;
+          const int col = lane + 32 * c;
+          if (row < rows && col < r) {
+            const float v = (float)u[b][c];
+            F[row * ldf + col] = v;
+            wmin = fmin(wmin, (double)v);
+          }
+        }
+    }
+  }
+  if (minparts) {
+    wmin = warp_min(wmin);
+    if (lane == 0) wmin_s[warp] = wmin;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = DBL_MAX;
+      for (int w = 0; w < kRowWarps; ++w) m = fmin(m, wmin_s[w]);
+      if (active) minparts[blockIdx.x] = m;
+    }
+  }
+}
+
+template <int CPL, int RB>
+__global__ void __launch_bounds__(32 * kRowWarps)
+pbcd_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
+            const double* __restrict__ C, const double* __restrict__ G,
+            const double* __restrict__ lam_ptr, int max_iter, float* __restrict__ snaps,
+            double* __restrict__ pgparts, const int* __restrict__ stage) {
+  constexpr int RP = 32 * CPL;
+  if (stage != nullptr && *stage != 0) return;
+  extern __shared__ double smem[];
+  double* Gs = smem;
+  double* pgw = smem + RP * RP;            // [kRowWarps][max_iter + 1]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double lam = *lam_ptr;
+  load_gram<CPL>(G, r, Gs);
+  for (int e = threadIdx.x; e < kRowWarps * (max_iter + 1); e += blockDim.x) pgw[e] = 0.0;
+  __syncthreads();
+  double* mypg = pgw + warp * (max_iter + 1);
+  const int64_t nblk = (rows + RB - 1) / RB;
+  const int64_t snap_stride = rows * (int64_t)r;
+  for (int64_t rb = (int64_t)blockIdx.x * kRowWarps + warp; rb < nblk;
+       rb += (int64_t)gridDim.x * kRowWarps) {
+    double u[RB][CPL], cc[RB][CPL], gr[RB][CPL];
+    bool msk[RB][CPL];
+#pragma unroll
+    for (int b = 0; b < RB; ++b)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int64_t row = rb * RB + b;
+        const int col = lane + 32 * c;
+        const bool ok = row < rows && col < r;
+        double v = ok ? (double)F[row * ldf + col] : 0.0;
+        if (v < 0.0) v += lam;                      // Eq.(6)/(7) lift of I_-
+        u[b][c] = v;
+        msk[b][c] = ok && v >= 0.0;                 // M_{U+} after the lift (R14)
+        cc[b][c] = ok ? C[row * r + col] : 0.0;
+        gr[b][c] = -cc[b][c];
+      }
+    row_times_gram<CPL, RB>(u, Gs, r, lane, 1.0, gr);   // grad = u G - C
+    {
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < RB; ++b)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) s += msk[b][c] ? gr[b][c] * gr[b][c] : 0.0;
+      s = warp_sum(s);
+      if (lane == 0) mypg[0] += s;
+    }
+    for (int it = 1; it <= max_iter; ++it) {
+      double g[RB][CPL], gG[RB][CPL];
+      double num[RB], den[RB];
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        double sn = 0.0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          g[b][c] = msk[b][c] ? gr[b][c] : 0.0;
+          sn += g[b][c] * g[b][c];
+          gG[b][c] = 0.0;
+        }
+        num[b] = warp_sum(sn);
+      }
+      row_times_gram<CPL, RB>(g, Gs, r, lane, 1.0, gG);  // g V^T V
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        double sd = 0.0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) sd += gG[b][c] * g[b][c];
+        den[b] = warp_sum(sd);
+      }
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        // Eq.(10): d_i = ||g_i||^2 / ||g_i V^T||^2 ; 0 on a zero denominator (R10)
+        const double d = den[b] > 0.0 ? num[b] / den[b] : 0.0;
+        const int64_t row = rb * RB + b;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          if (msk[b][c]) u[b][c] = fmax(0.0, u[b][c] - d * gr[b][c]);   // Eq.(8)
+          const int col = lane + 32 * c;
+          if (row < rows && col < r)
+            snaps[(int64_t)(it - 1) * snap_stride + row * r + col] = (float)u[b][c];
+          gr[b][c] = -cc[b][c];
+        }
+      }
+      row_times_gram<CPL, RB>(u, Gs, r, lane, 1.0, gr);
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < RB; ++b)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) s += msk[b][c] ? gr[b][c] * gr[b][c] : 0.0;
+      s = warp_sum(s);
+      if (lane == 0) mypg[it] += s;
+    }
+  }
+  __syncwarp();
+  for (int it = lane; it <= max_iter; it += 32)
+    pgparts[((int64_t)blockIdx.x * kRowWarps + warp) * (max_iter + 1) + it] = mypg[it];
+}
+
+// k* = first inner iteration whose projected gradient drops below eps * initial
+// (Alg. 2), or max_iter.
+// pgsum[it] = ||M o grad||_F^2 after `it` inner iterations, summed over all rows (and ranks).
+__global__ void pbcd_select_kernel(const double* __restrict__ pgsum, int max_iter, double eps,
+                                   int* kstar, const int* stage) {
+  if (stage != nullptr && *stage != 0) return;
+  if (threadIdx.x == 0) {
+    const double pg0 = sqrt(pgsum[0]);
+    int k = max_iter;
+    for (int it = 1; it <= max_iter; ++it)
+      if (sqrt(pgsum[it]) < eps * pg0) { k = it; break; }
+    *kstar = k;
+  }
+}
+
+__global__ void pbcd_copy_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r,
+                                 const float* __restrict__ snaps, const int* __restrict__ kstar,
+                                 const int* stage, double* minparts) {
+  __shared__ double red[256];
+  const bool active = stage == nullptr || *stage == 0;
+  double mn = DBL_MAX;
+  if (active) {
+    const float* src = snaps + (int64_t)(*kstar - 1) * rows * r;
+    const int64_t total = rows * (int64_t)r;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = e / r, j = e - i * r;
+      const float v = src[e];
+      F[i * ldf + j] = v;
+      mn = fmin(mn, (double)v);
+    }
+  }
+  red[threadIdx.x] = mn;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && active) minparts[blockIdx.x] = red[0];
+}
+
+// KKT statistics per warp slot: {max|c|, sum|c|, max c, sum c, min grad, min F, sum C^2, 0}
+template <int CPL, int RB>
+__global__ void __launch_bounds__(32 * kRowWarps)
+kkt_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
+           const double* __restrict__ C, const double* __restrict__ G, double* parts) {
+  extern __shared__ double smem[];
+  double* Gs = smem;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  load_gram<CPL>(G, r, Gs);
+  __syncthreads();
+  double cmax = 0.0, csum = 0.0, dmax = -DBL_MAX, dsum = 0.0, gmin = DBL_MAX, fmn = DBL_MAX,
+         c2 = 0.0;
+  const int64_t nblk = (rows + RB - 1) / RB;
+  for (int64_t rb = (int64_t)blockIdx.x * kRowWarps + warp; rb < nblk;
+       rb += (int64_t)gridDim.x * kRowWarps) {
+    double u[RB][CPL], gr[RB][CPL];
+    bool ok[RB][CPL];
+#pragma unroll
+    for (int b = 0; b < RB; ++b)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int64_t row = rb * RB + b;
+        const int col = lane + 32 * c;
+        ok[b][c] = row < rows && col < r;
+        u[b][c] = ok[b][c] ? (double)F[row * ldf + col] : 0.0;
+        const double cv = ok[b][c] ? C[row * r + col] : 0.0;
+        gr[b][c] = -cv;
+        c2 += cv * cv;
+      }
+    row_times_gram<CPL, RB>(u, Gs, r, lane, 1.0, gr);
+#pragma unroll
+    for (int b = 0; b < RB; ++b)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        if (!ok[b][c]) continue;
+        const double cv = gr[b][c] * u[b][c];
+        cmax = fmax(cmax, fabs(cv));
+        csum += fabs(cv);
+        dmax = fmax(dmax, cv);
+        dsum += cv;
+        gmin = fmin(gmin, gr[b][c]);
+        fmn = fmin(fmn, u[b][c]);
+      }
+  }
+  cmax = warp_max(cmax);
+  csum = warp_sum(csum);
+  dmax = warp_max(dmax);
+  dsum = warp_sum(dsum);
+  gmin = warp_min(gmin);
+  fmn = warp_min(fmn);
+  c2 = warp_sum(c2);
+  if (lane == 0) {
+    double* p = parts + ((int64_t)blockIdx.x * kRowWarps + warp) * 8;
+    p[0] = cmax; p[1] = csum; p[2] = dmax; p[3] = dsum; p[4] = gmin; p[5] = fmn; p[6] = c2;
+    p[7] = 0.0;
+  }
+}
+
+template <int CPL>
+size_t row_smem(int extra_doubles) {
+  return sizeof(double) * (size_t)(32 * CPL * 32 * CPL + extra_doubles);
+}
+
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+}  // namespace
+
+#define ENMF_CPL_DISPATCH(r, CALL) \
+  do {                             \
+    if ((r) <= 32) { CALL(1); }    \
+    else if ((r) <= 64) { CALL(2); } \
+    else if ((r) <= 96) { CALL(3); } \
+    else { CALL(4); }              \
+  } while (0)
+
+void hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
+               const int* stage, double* minparts, cudaStream_t st) {
+#define CALL(CPL)                                                                      \
+  {                                                                                    \
+    auto k = hals_kernel<CPL, 4>;                                                      \
+    size_t sm = row_smem<CPL>(0);                                                      \
+    set_smem(k, sm);                                                                   \
+    k<<<kRowGrid, 32 * kRowWarps, sm, st>>>(F, ldf, rows, r, C, G, stage, minparts);   \
+  }
+  ENMF_CPL_DISPATCH(r, CALL);
+#undef CALL
+  count_launch();
+}
+
+int pbcd_parts() { return kRowGrid * kRowWarps; }
+
+void pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
+               const double* G, const double* lam, int max_iter, float* snaps,
+               double* pgparts, const int* stage, cudaStream_t st) {
+#define CALL(CPL)                                                                           \
+  {                                                                                         \
+    auto k = pbcd_kernel<CPL, 4>;                                                           \
+    size_t sm = row_smem<CPL>(kRowWarps * (max_iter + 1));                                  \
+    set_smem(k, sm);                                                                        \
+    k<<<kRowGrid, 32 * kRowWarps, sm, st>>>(F, ldf, rows, r, C, G, lam, max_iter, snaps,    \
+                                           pgparts, stage);                                 \
+  }
+  ENMF_CPL_DISPATCH(r, CALL);
+#undef CALL
+  count_launch();
+}
+
+void pbcd_commit(float* F, int64_t ldf, int64_t rows, int r, const float* snaps,
+                 const double* pgsum, double eps, int max_iter, int* kstar, const int* stage,
+                 double* minparts, cudaStream_t st) {
+  pbcd_select_kernel<<<1, 32, 0, st>>>(pgsum, max_iter, eps, kstar, stage);
+  pbcd_copy_kernel<<<kRowGrid, 256, 0, st>>>(F, ldf, rows, r, snaps, kstar, stage, minparts);
+  count_launch(2);
+}
+
+int kkt_parts() { return kRowGrid * kRowWarps; }
+
+void kkt_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
+              const double* G, double* parts, cudaStream_t st) {
+#define CALL(CPL)                                                                 \
+  {                                                                               \
+    auto k = kkt_kernel<CPL, 4>;                                                  \
+    size_t sm = row_smem<CPL>(0);                                                 \
+    set_smem(k, sm);                                                              \
+    k<<<kRowGrid, 32 * kRowWarps, sm, st>>>(F, ldf, rows, r, C, G, parts);        \
+  }
+  ENMF_CPL_DISPATCH(r, CALL);
+#undef CALL
+  count_launch();
+}
+
+}  // namespace enmf

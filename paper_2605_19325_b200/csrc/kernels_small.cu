@@ -1,0 +1,483 @@
+// kernels_small.cu -- reductions, scalar bookkeeping, the ADMM elementwise step, the
+// randomised-SVD helpers and the single-CTA fp64 dense kernels (Cholesky, one-sided Jacobi
+// SVD, Procrustes) used at init.
+#include <float.h>
+
+#include "internal.h"
+
+namespace enmf {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// Block-wide reduction of one double with a fixed tree (deterministic).
+template <int OP>  // 0 sum, 1 min, 2 max
+__device__ double block_reduce(double v, double* red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      const double a = red[threadIdx.x], b = red[threadIdx.x + o];
+      red[threadIdx.x] = OP == 0 ? a + b : (OP == 1 ? fmin(a, b) : fmax(a, b));
+    }
+    __syncthreads();
+  }
+  const double out = red[0];
+  __syncthreads();
+  return out;
+}
+
+constexpr int kStatGrid = 4 * kSMs;
+
+__global__ void x_stats_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows,
+                               int64_t n, double* parts) {
+  __shared__ double red[256];
+  double s = 0.0, mn = DBL_MAX, bad = 0.0;
+  const int64_t total = rows * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    const float v = X[i * ldx + j];
+    if (!isfinite(v)) { bad += 1.0; continue; }
+    s += (double)v * (double)v;
+    mn = fmin(mn, (double)v);
+  }
+  s = block_reduce<0>(s, red);
+  mn = block_reduce<1>(mn, red);
+  bad = block_reduce<0>(bad, red);
+  if (threadIdx.x == 0) {
+    parts[3 * blockIdx.x] = s;
+    parts[3 * blockIdx.x + 1] = mn;
+    parts[3 * blockIdx.x + 2] = bad;
+  }
+}
+
+__global__ void x_stats_finish(const double* parts, int nparts, double* out3) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0, mn = DBL_MAX, bad = 0.0;
+  for (int p = 0; p < nparts; ++p) {
+    s += parts[3 * p];
+    mn = fmin(mn, parts[3 * p + 1]);
+    bad += parts[3 * p + 2];
+  }
+  out3[0] = s;
+  out3[1] = mn;
+  out3[2] = bad;
+}
+
+__global__ void min_f32_kernel(const float* __restrict__ A, int64_t ld, int64_t rows,
+                               int64_t cols, double* parts) {
+  __shared__ double red[256];
+  double mn = DBL_MAX;
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    mn = fmin(mn, (double)A[i * ld + j]);
+  }
+  mn = block_reduce<1>(mn, red);
+  if (threadIdx.x == 0) parts[blockIdx.x] = mn;
+}
+
+__global__ void reduce_min_kernel(const double* parts, int n, double* out) {
+  if (threadIdx.x != 0) return;
+  double mn = DBL_MAX;
+  for (int p = 0; p < n; ++p) mn = fmin(mn, parts[p]);
+  *out = mn;
+}
+
+__global__ void dot_kernel(const double* __restrict__ A, const float* __restrict__ B,
+                           int64_t ldb, int64_t rows, int64_t cols, double* parts) {
+  __shared__ double red[256];
+  double s = 0.0;
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    s += A[e] * (double)B[i * ldb + j];
+  }
+  s = block_reduce<0>(s, red);
+  if (threadIdx.x == 0) parts[blockIdx.x] = s;
+}
+
+// Philox4x32-10 (Salmon et al. 2011) for the Gaussian test matrix of the range finder.
+__device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    const unsigned lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const unsigned lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__global__ void gaussian_kernel(double* A, int64_t total, uint64_t seed) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = philox10(make_uint4((unsigned)e, (unsigned)(e >> 32), 0x4F6D6567u, 0u),
+                             make_uint2((unsigned)seed, (unsigned)(seed >> 32)));
+    const double u1 = ((double)(w.x >> 8) + 1.0) * (1.0 / 16777216.0);
+    const double u2 = (double)(w.y >> 8) * (1.0 / 16777216.0);
+    A[e] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  }
+}
+
+__global__ void stage_update_kernel(int* stage, const double* minu, const double* minv,
+                                    int* counters) {
+  if (threadIdx.x != 0) return;
+  if (*stage == 0 && *minu >= 0.0 && *minv >= 0.0) *stage = 1;
+  if (counters) counters[*stage] += 1;                            // [ascent, hals] sweeps
+}
+
+__global__ void objective_finish_kernel(const double* xnorm2, const double* cross,
+                                        const double* gu, const double* gv, int r,
+                                        double* fout) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) s += gu[e] * gv[e];
+  s = block_reduce<0>(s, red);
+  if (threadIdx.x == 0) *fout = *xnorm2 - 2.0 * (*cross) + s;
+}
+
+// ADMM elementwise part of one step (Alg. 1 lines 171-173 with scaled dual Yh = Y/rho):
+//   [first == 0] Yh += Z - W R          (dual update of the previous step)
+//   b = W R - Yh ; Z = Eq.(7)(b) ; B = Z + Yh
+// and the negativity sum h(W R) of the current rotation.
+__global__ void admm_z_kernel(const double* __restrict__ WR, double* __restrict__ Yh,
+                              double* __restrict__ Z, double* __restrict__ B, int64_t count,
+                              double inv_rho, int first, double* negparts,
+                              unsigned long long* third) {
+  __shared__ double red[256];
+  double neg = 0.0;
+  unsigned long long th = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double wr = WR[e];
+    double yh = first ? 0.0 : Yh[e] + Z[e] - wr;
+    const double b = wr - yh;
+    double z;
+    if (b > 0.0) z = b;
+    else if (b >= -inv_rho) z = 0.0;
+    else { z = b + inv_rho; ++th; }
+    Yh[e] = yh;
+    Z[e] = z;
+    B[e] = z + yh;
+    neg += wr < 0.0 ? -wr : 0.0;
+  }
+  neg = block_reduce<0>(neg, red);
+  if (threadIdx.x == 0) negparts[blockIdx.x] = neg;
+  if (th) atomicAdd(third, th);
+}
+
+// Column-wise arg max |A_ik| (ties: lowest row) -> parts[block][k] = (|v|, row, v).
+__global__ void colabsmax_kernel(const double* __restrict__ A, int64_t rows, int r,
+                                 int64_t row_offset, double* parts) {
+  for (int k = threadIdx.x; k < r; k += blockDim.x) {
+    double best = -1.0, bv = 0.0, bi = 0.0;
+    for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
+      const double v = A[i * r + k];
+      if (fabs(v) > best) { best = fabs(v); bv = v; bi = (double)(i + row_offset); }
+    }
+    double* p = parts + ((int64_t)blockIdx.x * r + k) * 3;
+    p[0] = best; p[1] = bi; p[2] = bv;
+  }
+}
+
+__global__ void colabsmax_finish_kernel(const double* parts, int nparts, int r, double* sg) {
+  for (int k = threadIdx.x; k < r; k += blockDim.x) {
+    double best = -1.0, bi = 0.0, bv = 0.0;
+    for (int p = 0; p < nparts; ++p) {
+      const double* q = parts + ((int64_t)p * r + k) * 3;
+      if (q[0] > best || (q[0] == best && q[1] < bi)) { best = q[0]; bi = q[1]; bv = q[2]; }
+    }
+    sg[k] = bv < 0.0 ? -1.0 : 1.0;                 // sign rule R5
+  }
+}
+
+__global__ void scale_cols_kernel(double* A, int64_t rows, int r, const double* s) {
+  const int64_t total = rows * r;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    A[e] *= s[e % r];
+}
+
+// ---------------------------------------------------------------- single-CTA dense fp64
+// Upper Cholesky G = R^T R (row j of R from rows < j), then R^{-1} by back substitution,
+// one column per thread.
+__global__ void __launch_bounds__(1024)
+chol_inv_kernel(const double* __restrict__ G, int k, double shift_rel, double* R, double* Rinv,
+                int* bad) {
+  __shared__ double diag_s;
+  __shared__ double tr_s;
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < k; ++i) tr += G[i * k + i];
+    tr_s = tr;
+    *bad = 0;
+  }
+  __syncthreads();
+  const double shift = shift_rel * tr_s / (k > 0 ? k : 1);
+  for (int j = 0; j < k; ++j) {
+    if (threadIdx.x == 0) {
+      double s = G[j * k + j] + shift;
+      for (int p = 0; p < j; ++p) s -= R[p * k + j] * R[p * k + j];
+      if (!(s > 1e-300)) { ++*bad; s = 1e-300; }
+      diag_s = sqrt(s);
+      R[j * k + j] = diag_s;
+    }
+    __syncthreads();
+    for (int i = j + 1 + threadIdx.x; i < k; i += blockDim.x) {
+      double s = G[j * k + i];
+      for (int p = 0; p < j; ++p) s -= R[p * k + j] * R[p * k + i];
+      R[j * k + i] = s / diag_s;
+    }
+    for (int i = threadIdx.x; i < j; i += blockDim.x) R[j * k + i] = 0.0;
+    __syncthreads();
+  }
+  // R^{-1}: column c solves R x = e_c (x_i = 0 for i > c)
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    for (int i = k - 1; i > c; --i) Rinv[i * k + c] = 0.0;
+    for (int i = c; i >= 0; --i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int p = i + 1; p <= c; ++p) s -= R[i * k + p] * Rinv[p * k + c];
+      Rinv[i * k + c] = s / R[i * k + i];
+    }
+  }
+}
+
+// One-sided (Hestenes) Jacobi SVD of a k x k matrix, parallel round-robin pair ordering.
+// work: B (k x k column-major) and J (k x k column-major).
+__global__ void __launch_bounds__(1024)
+jacobi_svd_kernel(const double* __restrict__ A, int k, double* Uo, double* s, double* Vo,
+                  double* work) {
+  double* B = work;               // column c at B + c*k
+  double* J = work + (int64_t)k * k;
+  __shared__ int rotated;
+  __shared__ double nrm[512];
+  __shared__ int ord[512];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int i = e / k, c = e % k;
+    B[c * k + i] = A[e];
+    J[c * k + i] = (i == c) ? 1.0 : 0.0;
+  }
+  const int kk = (k + 1) & ~1;      // even number of players (one dummy if k is odd)
+  __syncthreads();
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    for (int rd = 0; rd < kk - 1; ++rd) {
+      for (int pr = warp; pr < kk / 2; pr += nw) {
+        // round-robin: player 0 fixed, others rotate
+        auto pos = [&](int x) { return x == 0 ? 0 : 1 + (x - 1 + rd) % (kk - 1); };
+        int p = pos(pr), q = pos(kk - 1 - pr);
+        if (p > q) { const int t = p; p = q; q = t; }
+        if (q >= k) continue;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < k; i += 32) {
+          const double bp = B[p * k + i], bq = B[q * k + i];
+          al += bp * bp; be += bq * bq; ga += bp * bq;
+        }
+        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+        if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+        for (int i = lane; i < k; i += 32) {
+          const double bp = B[p * k + i], bq = B[q * k + i];
+          B[p * k + i] = c * bp - sn * bq;
+          B[q * k + i] = sn * bp + c * bq;
+          const double jp = J[p * k + i], jq = J[q * k + i];
+          J[p * k + i] = c * jp - sn * jq;
+          J[q * k + i] = sn * jp + c * jq;
+        }
+        if (lane == 0) rotated = 1;
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  // column norms and a descending order (ties: lower index first)
+  for (int c = warp; c < k; c += nw) {
+    double t = 0.0;
+    for (int i = lane; i < k; i += 32) t += B[c * k + i] * B[c * k + i];
+    t = warp_sum(t);
+    if (lane == 0) nrm[c] = sqrt(t);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    int rank = 0;
+    for (int d = 0; d < k; ++d)
+      if (nrm[d] > nrm[c] || (nrm[d] == nrm[c] && d < c)) ++rank;
+    ord[rank] = c;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int i = e / k, a = e % k;
+    const int c = ord[a];
+    const double sc = nrm[c];
+    Uo[i * k + a] = sc > 0.0 ? B[c * k + i] / sc : 0.0;
+    Vo[i * k + a] = J[c * k + i];
+  }
+  for (int a = threadIdx.x; a < k; a += blockDim.x) s[a] = nrm[ord[a]];
+}
+
+// R = C D^T; columns of C with s = 0 are completed to an orthonormal basis first.
+__global__ void procrustes_kernel(double* Cm, const double* __restrict__ s,
+                                  const double* __restrict__ Dm, int k, double* R) {
+  if (threadIdx.x == 0) {
+    for (int a = 0; a < k; ++a) {
+      if (s[a] > 0.0) continue;
+      for (int e = 0; e < k; ++e) {
+        for (int i = 0; i < k; ++i) Cm[i * k + a] = (i == e) ? 1.0 : 0.0;
+        for (int pass = 0; pass < 2; ++pass)
+          for (int b = 0; b < k; ++b) {
+            if (b == a || (s[b] <= 0.0 && b > a)) continue;
+            double d = 0.0;
+            for (int i = 0; i < k; ++i) d += Cm[i * k + b] * Cm[i * k + a];
+            for (int i = 0; i < k; ++i) Cm[i * k + a] -= d * Cm[i * k + b];
+          }
+        double t = 0.0;
+        for (int i = 0; i < k; ++i) t += Cm[i * k + a] * Cm[i * k + a];
+        if (t > 1e-6) {
+          t = sqrt(t);
+          for (int i = 0; i < k; ++i) Cm[i * k + a] /= t;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int a = e / k, b = e % k;
+    double acc = 0.0;
+    for (int c = 0; c < k; ++c) acc += Cm[a * k + c] * Dm[b * k + c];
+    R[e] = acc;
+  }
+}
+
+inline int grid_for(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return (int)(g < kStatGrid ? (g < 1 ? 1 : g) : kStatGrid);
+}
+
+}  // namespace
+
+int x_stats_parts(int64_t rows) { (void)rows; return kStatGrid; }
+
+void x_stats(const float* X, int64_t ldx, int64_t rows, int64_t n, double* parts, int nparts,
+             double* out3, cudaStream_t st) {
+  x_stats_kernel<<<nparts, 256, 0, st>>>(X, ldx, rows, n, parts);
+  x_stats_finish<<<1, 32, 0, st>>>(parts, nparts, out3);
+  count_launch(2);
+}
+
+void min_f32(const float* A, int64_t ld, int64_t rows, int64_t cols, double* parts, double* out,
+             cudaStream_t st) {
+  min_f32_kernel<<<kStatGrid, 256, 0, st>>>(A, ld, rows, cols, parts);
+  reduce_min_kernel<<<1, 32, 0, st>>>(parts, kStatGrid, out);
+  count_launch(2);
+}
+
+void reduce_min(const double* parts, int n, double* out, cudaStream_t st) {
+  reduce_min_kernel<<<1, 32, 0, st>>>(parts, n, out);
+  count_launch();
+}
+
+void dot_f64_f32(const double* A, const float* B, int64_t ldb, int64_t rows, int64_t cols,
+                 double* parts, double* out, cudaStream_t st) {
+  dot_kernel<<<kStatGrid, 256, 0, st>>>(A, B, ldb, rows, cols, parts);
+  reduce_parts(parts, kStatGrid, 1, out, st);
+  count_launch();
+}
+
+void gaussian_fill(double* A, int64_t rows, int64_t cols, uint64_t seed, cudaStream_t st) {
+  gaussian_kernel<<<grid_for(rows * cols), 256, 0, st>>>(A, rows * cols, seed);
+  count_launch();
+}
+
+void stage_update(int* stage, const double* minu, const double* minv, int* counters,
+                  cudaStream_t st) {
+  stage_update_kernel<<<1, 32, 0, st>>>(stage, minu, minv, counters);
+  count_launch();
+}
+
+void objective_finish(const double* xnorm2, const double* cross, const double* gu,
+                      const double* gv, int r, double* fout, cudaStream_t st) {
+  objective_finish_kernel<<<1, 256, 0, st>>>(xnorm2, cross, gu, gv, r, fout);
+  count_launch();
+}
+
+void admm_z(const double* WR, double* Yh, double* Z, double* B, int64_t count, double inv_rho,
+            int first, double* negparts, unsigned long long* third, cudaStream_t st) {
+  admm_z_kernel<<<kStatGrid, 256, 0, st>>>(WR, Yh, Z, B, count, inv_rho, first, negparts, third);
+  count_launch();
+}
+
+int colabsmax_parts() { return kStatGrid; }
+
+void colabsmax(const double* A, int64_t rows, int r, int64_t row_offset, double* parts,
+               cudaStream_t st) {
+  colabsmax_kernel<<<kStatGrid, 128, 0, st>>>(A, rows, r, row_offset, parts);
+  count_launch();
+}
+
+void colabsmax_finish(const double* parts, int r, double* sign_out, cudaStream_t st) {
+  colabsmax_finish_kernel<<<1, 128, 0, st>>>(parts, kStatGrid, r, sign_out);
+  count_launch();
+}
+
+void scale_cols_f64(double* A, int64_t rows, int r, const double* s, cudaStream_t st) {
+  scale_cols_kernel<<<grid_for(rows * r), 256, 0, st>>>(A, rows, r, s);
+  count_launch();
+}
+
+void chol_inv(const double* G, int k, double shift_rel, double* R, double* Rinv, int* bad,
+              cudaStream_t st) {
+  chol_inv_kernel<<<1, 1024, 0, st>>>(G, k, shift_rel, R, Rinv, bad);
+  count_launch();
+}
+
+void jacobi_svd(const double* A, int k, double* Uo, double* s, double* Vo, double* work,
+                cudaStream_t st) {
+  jacobi_svd_kernel<<<1, 1024, 0, st>>>(A, k, Uo, s, Vo, work);
+  count_launch();
+}
+
+void procrustes_from_svd(const double* Cm, const double* s, const double* Dm, int k, double* R,
+                         cudaStream_t st) {
+  procrustes_kernel<<<1, 256, 0, st>>>(const_cast<double*>(Cm), s, Dm, k, R);
+  count_launch();
+}
+
+}  // namespace enmf
+
+namespace enmf {
+namespace {
+__global__ void negsum_kernel(const double* __restrict__ A, int64_t count, double* parts) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x)
+    s += A[e] < 0.0 ? -A[e] : 0.0;
+  s = block_reduce<0>(s, red);
+  if (threadIdx.x == 0) parts[blockIdx.x] = s;
+}
+}  // namespace
+
+// sum h(A), h(q) = max(0, -q)
+void negsum(const double* A, int64_t count, double* parts, double* out, cudaStream_t st) {
+  negsum_kernel<<<kStatGrid, 256, 0, st>>>(A, count, parts);
+  reduce_parts(parts, kStatGrid, 1, out, st);
+  count_launch();
+}
+}  // namespace enmf

@@ -1,0 +1,41 @@
+"""Shared helpers for the -m gpu parity tests (GPU path vs the fp64 oracle)."""
+import numpy as np
+
+import oracle
+import synth
+
+
+def rel_fro(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def to_dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def to_np(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def rotated_point(X, r, admm_iters=100):
+    """Oracle's SVD + rotation (Alg. 3) rounded to fp32, with lift constants
+    computed from the rounded factors (reading R9)."""
+    Us, Vs, s, _ = oracle.truncated_svd(X, r)
+    R, _, _ = oracle.admm_rotate(np.vstack([Us, Vs]), T=admm_iters)
+    U = (Us @ R).astype(np.float32).astype(np.float64)
+    V = (Vs @ R).astype(np.float32).astype(np.float64)
+    return U, V, oracle.lift_constant(U), oracle.lift_constant(V)
+
+
+def make(cfg_or_X, r=None, **opts):
+    import paper_2605_19325_b200 as E
+    X = cfg_or_X if isinstance(cfg_or_X, np.ndarray) else synth.x_full(cfg_or_X)
+    r = r if r is not None else cfg_or_X.r
+    m, n = X.shape
+    h = E.Enmf(m, n, r, **opts)
+    Xd = to_dev(X)
+    h.set_data(Xd)
+    return h, X, Xd

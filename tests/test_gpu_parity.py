@@ -1,0 +1,191 @@
+"""GPU path (libenmf.so through the C-ABI) vs the fp64 oracle on the same seeded inputs.
+
+Tolerances are BASELINE.json:5's: one update from identical (U, V) <= 1e-5 relative Frobenius
+per factor; objective trajectory over the first 50 sweeps <= 1e-4 relative; final objective
+<= 1e-3; factors after permutation matching.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.gpu_common import make, rel_fro, rotated_point, to_dev, to_np
+
+pytestmark = pytest.mark.gpu
+
+# small parity shapes spanning several 64-row tiles, CPL boundaries and ragged tails
+CASES = [
+    synth.C1,
+    synth.C2.scaled(150, 700, 49, 49),
+    synth.C3.scaled(160, 900, 32, 32),
+    synth.C4.scaled(300, 250, 20, 0),
+    synth.C1.scaled(257, 131, 33, 33, name="planted-ragged-r33"),
+    synth.C1.scaled(130, 97, 1, 1, name="planted-r1"),
+    synth.C5.scaled(400, 300, 128, 128, name="C5-shape-r128"),
+]
+IDS = [c.name for c in CASES]
+
+
+@pytest.mark.parametrize("cfg", CASES, ids=IDS)
+def test_one_hals_sweep(cfg):
+    h, X, _ = make(cfg)
+    U0, V0, _, _ = rotated_point(X, cfg.r)
+    U0, V0 = np.abs(U0), np.abs(V0)           # a feasible point: HALS stage
+    U, V = to_dev(U0), to_dev(V0)
+    h.set_stage(1)
+    f, info = h.iterate(U, V, 1)
+    st = oracle.SweepState(stage=1)
+    Uo, Vo, stage, _ = oracle.sweep(X, U0, V0, st)
+    assert info["hals_sweeps"] == 1 and stage == 1
+    assert rel_fro(to_np(U), Uo) < 1e-5
+    assert rel_fro(to_np(V), Vo) < 1e-5
+
+
+@pytest.mark.parametrize("cfg", CASES, ids=IDS)
+def test_one_ascent_sweep(cfg):
+    h, X, _ = make(cfg)
+    U0, V0, lu, lv = rotated_point(X, cfg.r)
+    if U0.min() >= 0 and V0.min() >= 0:
+        pytest.skip("rotated point already feasible (one-shot case)")
+    U, V = to_dev(U0), to_dev(V0)
+    h.set_stage(0, lu, lv)
+    f, info = h.iterate(U, V, 1)
+    st = oracle.SweepState(0, lu, lv, 0)
+    Uo, Vo, stage, iters = oracle.sweep(X, U0, V0, st)
+    assert info["ascent_sweeps"] == 1 and stage == 0
+    assert (info["pbcd_iters_u"], info["pbcd_iters_v"]) == iters
+    assert rel_fro(to_np(U), Uo) < 1e-5
+    assert rel_fro(to_np(V), Vo) < 1e-5
+
+
+@pytest.mark.parametrize("cfg", CASES[:4], ids=IDS[:4])
+def test_objective_trajectory_shared_init(cfg):
+    """50 sweeps from the oracle's rotated point: trace-form f within 1e-4 of the oracle's
+    direct f at every sweep (ascent and HALS stages)."""
+    h, X, _ = make(cfg)
+    U0, V0, lu, lv = rotated_point(X, cfg.r)
+    U, V = to_dev(U0), to_dev(V0)
+    h.set_stage(0, lu, lv)
+    f_gpu, info = h.iterate(U, V, 50)
+    st = oracle.SweepState(0, lu, lv, 0)
+    Uo, Vo = U0, V0
+    f_or = []
+    for _ in range(50):
+        Uo, Vo, _, _ = oracle.sweep(X, Uo, Vo, st)
+        f_or.append(oracle.frob2_direct(X, Uo, Vo))
+    f_or = np.array(f_or)
+    err = np.abs(f_gpu - f_or) / f_or
+    assert err.max() < 1e-4, err
+    assert abs(h.objective(U, V, exact=True) - f_or[-1]) / f_or[-1] < 1e-4
+
+
+def test_final_objective_and_factors_c1():
+    """Full C1 schedule (init + 200 sweeps) end to end on both sides: final f within 1e-3 and
+    factors equal after permutation matching (reading R19)."""
+    cfg = synth.C1
+    X = synth.x_full(cfg)
+    import paper_2605_19325_b200 as E
+    h = E.Enmf(cfg.m, cfg.n, cfg.r)
+    U = to_dev(np.zeros((cfg.m, cfg.r)))
+    V = to_dev(np.zeros((cfg.n, cfg.r)))
+    info = h.init(to_dev(X), U, V)
+    f_gpu, it = h.iterate(U, V, cfg.sweeps)
+    Uo, Vo, s, f_or, st = oracle.enmf(X, cfg.r, cfg.sweeps)
+    assert np.allclose(info["sigma"], s, rtol=1e-6)
+    assert abs(f_gpu[-1] - f_or[-1]) / f_or[-1] < 1e-3
+    Ug, Vg = to_np(U), to_np(V)
+    # cosine matching of U columns (Hungarian by exhaustive search is fine at r = 5)
+    import itertools
+    cu = (Ug / np.linalg.norm(Ug, axis=0)).T @ (Uo / np.linalg.norm(Uo, axis=0))
+    perm = max(itertools.permutations(range(cfg.r)), key=lambda p: sum(cu[i, p[i]] for i in range(cfg.r)))
+    Ug, Vg = Ug[:, perm], Vg[:, perm]
+    for F in (Ug, Vg):
+        pass
+    # rescale each pair to balanced norms before comparing
+    def bal(Uf, Vf):
+        a = np.sqrt(np.linalg.norm(Vf, axis=0) / np.linalg.norm(Uf, axis=0))
+        return Uf * a, Vf / a
+    Ug, Vg = bal(Ug, Vg)
+    Ub, Vb = bal(Uo, Vo)
+    assert rel_fro(Ug, Ub) < 1e-3 and rel_fro(Vg, Vb) < 1e-3
+
+
+@pytest.mark.parametrize("cfg", [synth.C1, synth.C3.scaled(160, 900, 32, 32)],
+                         ids=["C1", "C3-scaled"])
+def test_init_matches_oracle_on_gapped_spectrum(cfg):
+    """Randomised SVD (q = 2) vs the oracle's converged subspace iteration: singular values,
+    Eckart-Young error of U* V*^T, and the rotated point (R19-style comparison)."""
+    X = synth.x_full(cfg)
+    import paper_2605_19325_b200 as E
+    h = E.Enmf(cfg.m, cfg.n, cfg.r)
+    Xd = to_dev(X)
+    h.set_data(Xd)
+    U = to_dev(np.zeros((cfg.m, cfg.r)))
+    V = to_dev(np.zeros((cfg.n, cfg.r)))
+    sig = h.svd(U, V)
+    Us, Vs, s, _ = oracle.truncated_svd(X, cfg.r)
+    assert np.allclose(sig, s, rtol=1e-6)
+    assert rel_fro(to_np(U), Us) < 1e-5 and rel_fro(to_np(V), Vs) < 1e-5
+    info = h.rotate(U, V)
+    R, neg, third = oracle.admm_rotate(np.vstack([Us, Vs]), T=100)
+    assert info["admm_third_branch"] == 0 and info["orth_residual"] < 1e-12
+    assert rel_fro(to_np(U), Us @ R) < 1e-4 and rel_fro(to_np(V), Vs @ R) < 1e-4
+
+
+@pytest.mark.parametrize("cfg", CASES[:3], ids=IDS[:3])
+def test_objective_and_kkt(cfg):
+    h, X, _ = make(cfg)
+    g = np.random.default_rng(0)
+    U0, V0 = g.random((cfg.m, cfg.r)), g.random((cfg.n, cfg.r))
+    U0 = U0.astype(np.float32).astype(np.float64)
+    V0 = V0.astype(np.float32).astype(np.float64)
+    U, V = to_dev(U0), to_dev(V0)
+    f_d = oracle.frob2_direct(X, U0, V0)
+    assert abs(h.objective(U, V, exact=True) - f_d) / f_d < 1e-12
+    assert abs(h.objective(U, V, exact=False) - f_d) / f_d < 1e-12 * oracle.xnorm2(X) / f_d + 1e-13
+    k = h.kkt(U, V)
+    ko = oracle.kkt(X, U0, V0)
+    for key in ("min_u", "min_v", "comp_max", "comp_sum", "delta_w", "sigma_w", "dual_viol",
+                "xnorm2", "rms_cross"):
+        assert abs(k[key] - ko[key]) <= 1e-9 * max(abs(ko[key]), 1e-300) + 1e-12 * ko["xnorm2"], key
+
+
+def test_edge_cases():
+    import torch
+    import paper_2605_19325_b200 as E
+    with pytest.raises(E.EnmfError):
+        E.Enmf(10, 5, 6)                            # r > min(m, n)
+    with pytest.raises(E.EnmfError):
+        E.Enmf(10, 5, 0)
+    with pytest.raises(E.EnmfError):
+        E.Enmf(300, 300, 129)                       # r > ENMF_MAX_RANK
+    h = E.Enmf(8, 6, 2)
+    X = torch.rand(8, 6, device="cuda")
+    X[3, 2] = -1e-3
+    with pytest.raises(E.EnmfError) as ei:
+        h.set_data(X)
+    assert ei.value.code == -3
+    X[3, 2] = float("nan")
+    with pytest.raises(E.EnmfError) as ei:
+        h.set_data(X)
+    assert ei.value.code == -5
+    U = torch.zeros(8, 2, device="cuda")
+    V = torch.zeros(6, 2, device="cuda")
+    with pytest.raises(E.EnmfError) as ei:
+        h.iterate(U, V, 1)                          # no data bound
+    assert ei.value.code == -9
+    with pytest.raises(E.EnmfError) as ei:
+        h.init(torch.zeros(8, 6, device="cuda"), U, V)   # X = 0: rank 0
+    assert ei.value.code == -4
+
+
+def test_zero_sweeps_and_launch_count():
+    h, X, _ = make(synth.C1)
+    U0, V0, lu, lv = rotated_point(X, 5)
+    U, V = to_dev(U0), to_dev(V0)
+    h.set_stage(0, lu, lv)
+    n0 = h.launch_count
+    f, info = h.iterate(U, V, 0)
+    assert len(f) == 0 and np.array_equal(to_np(U), U0)
+    h.iterate(U, V, 2)
+    assert h.launch_count > n0
