@@ -112,17 +112,25 @@ def gpu_index(local_rank):
     return local_rank
 
 
-def cpu_sample(cfg, rows, U_rows, V, n_sweeps=1):
-    """Oracle (as it stands) on a row sample of the workload: seconds per HALS sweep."""
+def cpu_sample(cfg, s_m, s_n, U, V, n_sweeps=1):
+    """Oracle (as it stands) on the block X[:s_m, :s_n] of the workload with the matching
+    factor rows: seconds per HALS sweep.  Its cost is dominated by the two X passes
+    (4 s_m s_n r flops), so the full-size rate is extrapolated by (m n) / (s_m s_n)."""
     import oracle
     import synth
-    Xs = synth.x_rows(cfg, 0, rows)
+    Xs = synth.x_block(cfg, 0, s_m, 0, s_n)
     st = oracle.SweepState(stage=1)
-    U, Vv = U_rows.astype(np.float64), V.astype(np.float64)
+    Uu = np.abs(np.asarray(U[:s_m], np.float64))
+    Vv = np.abs(np.asarray(V[:s_n], np.float64))
     t0 = time.perf_counter()
     for _ in range(n_sweeps):
-        U, Vv, _, _ = oracle.sweep(Xs, U, Vv, st)
+        Uu, Vv, _, _ = oracle.sweep(Xs, Uu, Vv, st)
     return (time.perf_counter() - t0) / n_sweeps
+
+
+def cpu_block(cfg, args):
+    s = args.cpu_sample_rows or 3000
+    return min(s, cfg.m), min(s, cfg.n)
 
 
 def run_reference(args):
@@ -133,15 +141,14 @@ def run_reference(args):
         return
     import synth
     cfg = synth.ALL[args.config]
-    rows = args.cpu_sample_rows or 96
+    s_m, s_n = cpu_block(cfg, args)
     g = np.random.default_rng(0)
-    U = g.random((rows, cfg.r)).astype(np.float32)
-    V = g.random((cfg.n, cfg.r)).astype(np.float32)
-    cpu_sample(cfg, rows, U, V, 1)          # warm-up (page-in, OpenMP pool)
-    for _ in range(max(0, args.warmup - 1)):
-        pass
-    times = [cpu_sample(cfg, rows, U, V, 1) for _ in range(args.steps)]
-    s_per_sweep_full = float(np.mean(times)) * cfg.m / rows
+    U = g.random((s_m, cfg.r)).astype(np.float32)
+    V = g.random((s_n, cfg.r)).astype(np.float32)
+    cpu_sample(cfg, s_m, s_n, U, V, 1)          # warm-up (page-in, OpenMP pool)
+    steps = max(1, min(args.steps, 5))
+    times = [cpu_sample(cfg, s_m, s_n, U, V, 1) for _ in range(steps)]
+    s_per_sweep_full = float(np.mean(times)) * (cfg.m * cfg.n) / (s_m * s_n)
     value = 1.0 / s_per_sweep_full
     cores = len(os.sched_getaffinity(0))
     line = {
@@ -152,8 +159,8 @@ def run_reference(args):
         "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "r": cfg.r,
                    "parallelism": "cpu oracle (OpenMP over rows)"},
         "cpu_baseline": {"value": value, "unit": "sweeps/s", "cores": cores, "kind": "oracle",
-                         "sample": f"one HALS sweep of the fp64 oracle on rows 0..{rows} of "
-                                   f"{cfg.name} per step, scaled by m/{rows}"},
+                         "sample": f"one HALS sweep of the fp64 oracle on X[:{s_m}, :{s_n}] of "
+                                   f"{cfg.name} per step, scaled by mn/({s_m}*{s_n})"},
         "e2e": {"value": value, "unit": "sweeps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -281,15 +288,15 @@ def run_enmf(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rows = args.cpu_sample_rows or 96
-        Us = U[:rows].cpu().numpy()
-        Vs = V.cpu().numpy()
-        cpu_sample(cfg, rows, Us, Vs, 1)
-        secs = cpu_sample(cfg, rows, Us, Vs, 1)
-        cpu = {"value": 1.0 / (secs * m / rows), "unit": "sweeps/s",
+        s_m, s_n = cpu_block(cfg, args)
+        Us = U[:s_m].cpu().numpy()
+        Vs = V[:s_n].cpu().numpy()
+        cpu_sample(cfg, min(s_m, 256), min(s_n, 256), Us, Vs, 1)      # page-in / thread pool
+        secs = cpu_sample(cfg, s_m, s_n, Us, Vs, 1)
+        cpu = {"value": 1.0 / (secs * (m * n) / (s_m * s_n)), "unit": "sweeps/s",
                "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-               "sample": f"one HALS sweep of the fp64 oracle on rows 0..{rows} of {cfg.name} "
-                         f"({secs:.2f} s), scaled by m/{rows} to the full workload"}
+               "sample": f"one HALS sweep of the fp64 oracle on X[:{s_m}, :{s_n}] of {cfg.name} "
+                         f"({secs:.2f} s), scaled by mn/({s_m}*{s_n}) to the full workload"}
 
     if rank == 0:
         line = {

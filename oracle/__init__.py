@@ -24,7 +24,8 @@ class Options(ctypes.Structure):
     _fields_ = [("r", ctypes.c_int), ("oversample", ctypes.c_int), ("svd_tol", ctypes.c_double),
                 ("svd_max_iter", ctypes.c_int), ("admm_iters", ctypes.c_int),
                 ("admm_rho", ctypes.c_double), ("lift_steps", ctypes.c_int),
-                ("pbcd_eps", ctypes.c_double), ("pbcd_max_iter", ctypes.c_int)]
+                ("pbcd_eps", ctypes.c_double), ("pbcd_max_iter", ctypes.c_int),
+                ("round_f32", ctypes.c_int)]
 
 
 class State(ctypes.Structure):
@@ -33,9 +34,11 @@ class State(ctypes.Structure):
 
 
 def options(r, oversample=10, svd_tol=1e-13, svd_max_iter=500, admm_iters=100, admm_rho=0.0,
-            lift_steps=10, pbcd_eps=1e-2, pbcd_max_iter=50):
+            lift_steps=10, pbcd_eps=1e-2, pbcd_max_iter=50, round_f32=0):
+    """round_f32=1: factor state stored in fp32 at block boundaries, as the C-ABI stores
+    U and V (reading R26); the arithmetic itself stays fp64."""
     return Options(r, oversample, svd_tol, svd_max_iter, admm_iters, admm_rho, lift_steps,
-                   pbcd_eps, pbcd_max_iter)
+                   pbcd_eps, pbcd_max_iter, round_f32)
 
 
 def lib():

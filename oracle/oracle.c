@@ -467,6 +467,12 @@ void or_hals(double* F, int64_t rows, int r, const double* C, const double* G) {
   }
 }
 
+/* Reading R26: the C-ABI keeps U and V in fp32 between block updates. */
+static void round_state(double* A, int64_t count, int on) {
+  if (!on) return;
+  for (int64_t e = 0; e < count; ++e) A[e] = (double)(float)A[e];
+}
+
 static double min_entry(const double* A, int64_t count) {
   double mn = INFINITY;
   for (int64_t e = 0; e < count; ++e) mn = A[e] < mn ? A[e] : mn;
@@ -490,20 +496,24 @@ int or_sweep(const float* X, int64_t m, int64_t n, double* U, double* V,
     or_xv(X, m, n, V, r, C);
     or_gram(V, n, r, G);
     int iu = or_pbcd(U, m, r, C, G, M, opt->pbcd_eps, opt->pbcd_max_iter, NULL, NULL);
+    round_state(U, m * r, opt->round_f32);
     /* V block with X^T and the new U (lines 338-340; Eq.(11) uses U^(k+1)) */
     or_lift(V, n * r, st->lambda_v);
     for (int64_t e = 0; e < n * r; ++e) M[e] = V[e] >= 0.0;
     or_xtu(X, m, n, U, r, C);
     or_gram(U, m, r, G);
     int iv = or_pbcd(V, n, r, C, G, M, opt->pbcd_eps, opt->pbcd_max_iter, NULL, NULL);
+    round_state(V, n * r, opt->round_f32);
     if (iters) { iters[0] = iu; iters[1] = iv; }
   } else {
     or_xv(X, m, n, V, r, C);
     or_gram(V, n, r, G);
     or_hals(U, m, r, C, G);
+    round_state(U, m * r, opt->round_f32);
     or_xtu(X, m, n, U, r, C);
     or_gram(U, m, r, G);
     or_hals(V, n, r, C, G);
+    round_state(V, n * r, opt->round_f32);
     if (iters) { iters[0] = 0; iters[1] = 0; }
   }
   st->sweeps_done += 1;
@@ -539,6 +549,8 @@ int or_enmf(const float* X, int64_t m, int64_t n, const or_options_t* opt, int n
   or_state_t st;
   st.stage = 0;
   st.sweeps_done = 0;
+  round_state(U, m * r, opt->round_f32);
+  round_state(V, n * r, opt->round_f32);
   st.lambda_u = or_lift_constant(U, m * r, opt->lift_steps);   /* reading R9 */
   st.lambda_v = or_lift_constant(V, n * r, opt->lift_steps);
   for (int t = 0; t < n_sweeps; ++t) {

@@ -81,6 +81,8 @@ typedef struct {
   int lift_steps;      /* L (reading R9), default 10 */
   double pbcd_eps;     /* default 1e-2 (R10) */
   int pbcd_max_iter;   /* default 50 (R10) */
+  int round_f32;       /* 1: the factor state is stored in fp32 at block boundaries, as the
+                          C-ABI stores U and V (reading R26); 0: fp64 state throughout */
 } or_options_t;
 
 typedef struct {

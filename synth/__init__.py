@@ -27,6 +27,9 @@ def _load_cpu():
         lib.synth_x_rows.argtypes = [ctypes.c_int, u64, i64, i64, ctypes.c_int, dbl, dbl,
                                      i64, i64, ctypes.c_void_p, i64]
         lib.synth_x_rows.restype = ctypes.c_int
+        lib.synth_x_block.argtypes = [ctypes.c_int, u64, i64, i64, ctypes.c_int, dbl, dbl,
+                                      i64, i64, i64, i64, ctypes.c_void_p, i64]
+        lib.synth_x_block.restype = ctypes.c_int
         lib.synth_smax.argtypes = [ctypes.c_int, u64, i64, i64, ctypes.c_int]
         lib.synth_smax.restype = dbl
         lib.synth_factor.argtypes = [ctypes.c_int, u64, ctypes.c_int, i64, i64, ctypes.c_int,
@@ -90,6 +93,18 @@ def x_rows(cfg: Config, row_begin=0, row_count=None, smax=None) -> np.ndarray:
                                   row_begin, row_count, out.ctypes.data, cfg.n)
     if rc != 0:
         raise ValueError("synth_x_rows: bad row range")
+    return out
+
+
+def x_block(cfg: Config, r0, rc, c0, cc, smax=None) -> np.ndarray:
+    """X[r0:r0+rc, c0:c0+cc], bit-identical to the same entries of x_full(cfg)."""
+    if smax is None:
+        smax = _smax_cpu(cfg)
+    out = np.empty((rc, cc), dtype=np.float32)
+    rc_ = _load_cpu().synth_x_block(cfg.recipe, cfg.seed, cfg.m, cfg.n, cfg.k, cfg.noise, smax,
+                                    r0, rc, c0, cc, out.ctypes.data, cc)
+    if rc_ != 0:
+        raise ValueError("synth_x_block: bad block")
     return out
 
 

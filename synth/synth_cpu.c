@@ -48,6 +48,31 @@ double synth_smax(int recipe, uint64_t seed, int64_t m, int64_t n, int k) {
   return best;
 }
 
+/* Block X[r0:r0+rc, c0:c0+cc] of an m x n matrix into out (ld = ldo). */
+int synth_x_block(int recipe, uint64_t seed, int64_t m, int64_t n, int k, double noise,
+                  double smax, int64_t r0, int64_t rc, int64_t c0, int64_t cc, float* out,
+                  int64_t ldo) {
+  if (r0 < 0 || rc < 0 || r0 + rc > m || c0 < 0 || cc < 0 || c0 + cc > n || ldo < cc) return -1;
+  float* A = NULL;
+  float* B = NULL;
+  if (recipe != SYN_RATINGS) {
+    A = (float*)malloc(sizeof(float) * (size_t)(rc > 0 ? rc : 1) * k);
+    B = (float*)malloc(sizeof(float) * (size_t)(cc > 0 ? cc : 1) * k);
+    synth_factor(recipe, seed, 0, r0, rc, k, A);
+    synth_factor(recipe, seed, 1, c0, cc, k, B);
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rc; ++r)
+    for (int64_t c = 0; c < cc; ++c) {
+      double s = recipe == SYN_RATINGS ? 0.0 : syn_dot(A + r * k, B + c * k, k);
+      out[r * ldo + c] = syn_x_from_s(recipe, seed, (uint64_t)(r0 + r), (uint64_t)(c0 + c),
+                                      (uint64_t)n, s, noise, smax);
+    }
+  free(A);
+  free(B);
+  return 0;
+}
+
 /* X rows [row_begin, row_begin+row_count) of an m x n matrix into out (ld = ldo). */
 int synth_x_rows(int recipe, uint64_t seed, int64_t m, int64_t n, int k, double noise,
                  double smax, int64_t row_begin, int64_t row_count, float* out, int64_t ldo) {

@@ -13,6 +13,14 @@ from tests.gpu_common import make, rel_fro, rotated_point, to_dev, to_np
 
 pytestmark = pytest.mark.gpu
 
+
+def F32STATE(r):
+    """Oracle options with the factor state stored in fp32 at block boundaries, as the C-ABI
+    stores U and V (reading R26): the ascent stage amplifies an fp32 rounding of the state by
+    ~1e5 (tests/test_oracle_pins.py::test_pbcd_state_rounding_sensitivity), so the comparison
+    is only well posed with both sides rounding at the same points."""
+    return oracle.options(r, round_f32=1)
+
 # small parity shapes spanning several 64-row tiles, CPL boundaries and ragged tails
 CASES = [
     synth.C1,
@@ -35,7 +43,7 @@ def test_one_hals_sweep(cfg):
     h.set_stage(1)
     f, info = h.iterate(U, V, 1)
     st = oracle.SweepState(stage=1)
-    Uo, Vo, stage, _ = oracle.sweep(X, U0, V0, st)
+    Uo, Vo, stage, _ = oracle.sweep(X, U0, V0, st, F32STATE(cfg.r))
     assert info["hals_sweeps"] == 1 and stage == 1
     assert rel_fro(to_np(U), Uo) < 1e-5
     assert rel_fro(to_np(V), Vo) < 1e-5
@@ -51,7 +59,7 @@ def test_one_ascent_sweep(cfg):
     h.set_stage(0, lu, lv)
     f, info = h.iterate(U, V, 1)
     st = oracle.SweepState(0, lu, lv, 0)
-    Uo, Vo, stage, iters = oracle.sweep(X, U0, V0, st)
+    Uo, Vo, stage, iters = oracle.sweep(X, U0, V0, st, F32STATE(cfg.r))
     assert info["ascent_sweeps"] == 1 and stage == 0
     assert (info["pbcd_iters_u"], info["pbcd_iters_v"]) == iters
     assert rel_fro(to_np(U), Uo) < 1e-5
@@ -71,7 +79,7 @@ def test_objective_trajectory_shared_init(cfg):
     Uo, Vo = U0, V0
     f_or = []
     for _ in range(50):
-        Uo, Vo, _, _ = oracle.sweep(X, Uo, Vo, st)
+        Uo, Vo, _, _ = oracle.sweep(X, Uo, Vo, st, F32STATE(cfg.r))
         f_or.append(oracle.frob2_direct(X, Uo, Vo))
     f_or = np.array(f_or)
     err = np.abs(f_gpu - f_or) / f_or
@@ -90,17 +98,16 @@ def test_final_objective_and_factors_c1():
     V = to_dev(np.zeros((cfg.n, cfg.r)))
     info = h.init(to_dev(X), U, V)
     f_gpu, it = h.iterate(U, V, cfg.sweeps)
-    Uo, Vo, s, f_or, st = oracle.enmf(X, cfg.r, cfg.sweeps)
+    Uo, Vo, s, f_or, st = oracle.enmf(X, cfg.r, cfg.sweeps, F32STATE(cfg.r))
     assert np.allclose(info["sigma"], s, rtol=1e-6)
     assert abs(f_gpu[-1] - f_or[-1]) / f_or[-1] < 1e-3
     Ug, Vg = to_np(U), to_np(V)
-    # cosine matching of U columns (Hungarian by exhaustive search is fine at r = 5)
+    # cosine matching of U columns (exhaustive assignment is fine at r = 5)
     import itertools
     cu = (Ug / np.linalg.norm(Ug, axis=0)).T @ (Uo / np.linalg.norm(Uo, axis=0))
-    perm = max(itertools.permutations(range(cfg.r)), key=lambda p: sum(cu[i, p[i]] for i in range(cfg.r)))
-    Ug, Vg = Ug[:, perm], Vg[:, perm]
-    for F in (Ug, Vg):
-        pass
+    perm = max(itertools.permutations(range(cfg.r)),
+               key=lambda p: sum(cu[p[i], i] for i in range(cfg.r)))
+    Ug, Vg = Ug[:, list(perm)], Vg[:, list(perm)]
     # rescale each pair to balanced norms before comparing
     def bal(Uf, Vf):
         a = np.sqrt(np.linalg.norm(Vf, axis=0) / np.linalg.norm(Uf, axis=0))

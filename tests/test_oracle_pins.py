@@ -258,6 +258,24 @@ def test_pbcd_gradient_literal_and_stopping_rule():
     assert (Un[M == 0] == U[M == 0]).all() and (Un[M == 1] >= 0).all()
 
 
+def test_pbcd_state_rounding_sensitivity():
+    """Why reading R26 exists: on the image-like data the ascent stage amplifies a 1e-7
+    perturbation of the factor state by >= 1e3 (projection active sets change), so the GPU
+    (fp32 state) is compared with the oracle rounding its state to fp32 at the same points."""
+    from tests.gpu_common import rotated_point, rel_fro
+    cfg = synth.C2.scaled(150, 700, 49, 49)
+    X = synth.x_full(cfg)
+    U0, V0, lu, lv = rotated_point(X, 49)
+    a = oracle.sweep(X, U0, V0, oracle.SweepState(0, lu, lv, 0))
+    g = np.random.default_rng(1)
+    b = oracle.sweep(X, U0 * (1 + 1e-7 * g.standard_normal(U0.shape)), V0,
+                     oracle.SweepState(0, lu, lv, 0))
+    assert rel_fro(b[1], a[1]) > 1e3 * 1e-7
+    c = oracle.sweep(X, U0, V0, oracle.SweepState(0, lu, lv, 0), oracle.options(49, round_f32=1))
+    assert np.array_equal(c[0], c[0].astype(np.float32).astype(np.float64))
+    assert np.array_equal(c[1], c[1].astype(np.float32).astype(np.float64))
+
+
 # ---------------------------------------------------------------- P5 HALS
 def test_hals_matches_textbook_residual_form():
     """HALS (cited Cichocki & Phan): column k is the projected
