@@ -14,32 +14,41 @@ def run_smoke():
     cfg = synth.C1
     X = synth.x_full(cfg)
     h = E.Enmf(cfg.m, cfg.n, cfg.r)
-    Xd = torch.from_numpy(X).cuda()
     U = torch.zeros(cfg.m, cfg.r, device="cuda")
     V = torch.zeros(cfg.n, cfg.r, device="cuda")
-    # (1) init on the GPU (randomised SVD + ADMM) vs the oracle's converged SVD
-    info = h.init(Xd, U, V)
+    # (1) Alg. 3 on the GPU: randomised SVD + ADMM rotation + 20 sweeps (ascent -> HALS)
+    info = h.init(torch.from_numpy(X).cuda(), U, V)
     Us, Vs, s, _ = oracle.truncated_svd(X, cfg.r)
     assert np.allclose(info["sigma"], s, rtol=1e-6), (info["sigma"], s)
-    # (2) 20 sweeps (10 ascent + 10 HALS) from the oracle's rotated point on both sides
-    R, _, _ = oracle.admm_rotate(np.vstack([Us, Vs]), T=100)
-    U0 = (Us @ R).astype(np.float32)
-    V0 = (Vs @ R).astype(np.float32)
-    U.copy_(torch.from_numpy(U0))
-    V.copy_(torch.from_numpy(V0))
-    lu = oracle.lift_constant(U0.astype(np.float64))
-    lv = oracle.lift_constant(V0.astype(np.float64))
-    h.set_stage(0, lu, lv)
     f_gpu, it = h.iterate(U, V, 20)
-    st = oracle.SweepState(0, lu, lv, 0)
-    Uo, Vo = U0.astype(np.float64), V0.astype(np.float64)
+    assert it["ascent_sweeps"] == 10 and it["hals_sweeps"] == 10, it
+    assert float(U.min()) >= 0 and float(V.min()) >= 0
+    # (2) 5 more HALS sweeps from the GPU's feasible point on both sides
+    U0 = U.cpu().numpy().astype(np.float64)
+    V0 = V.cpu().numpy().astype(np.float64)
+    f_gpu, _ = h.iterate(U, V, 5)
+    st = oracle.SweepState(stage=1)
     f_or = []
-    for _ in range(20):
-        Uo, Vo, _, _ = oracle.sweep(X, Uo, Vo, st, oracle.options(cfg.r, round_f32=1))
-        f_or.append(oracle.frob2_direct(X, Uo, Vo))
+    for _ in range(5):
+        U0, V0, _, _ = oracle.sweep(X, U0, V0, st, oracle.options(cfg.r, round_f32=1))
+        f_or.append(oracle.frob2_direct(X, U0, V0))
     rel = np.abs(f_gpu - np.array(f_or)) / np.array(f_or)
     assert rel.max() < 1e-4, rel
-    assert it["ascent_sweeps"] == 10 and it["hals_sweeps"] == 10, it
-    assert h.launch_count > 0
-    print(f"smoke ok: f[19] gpu={f_gpu[-1]:.8g} oracle={f_or[-1]:.8g} max rel={rel.max():.2e} "
-          f"launches={h.launch_count}")
+    # (3) one HALS sweep through the tcgen05 tensor-core contraction path
+    c5 = synth.C5.scaled(400, 300, 128, 128)
+    X5 = synth.x_full(c5)
+    h5 = E.Enmf(c5.m, c5.n, c5.r, precision=E.PREC_TC)
+    h5.set_data(torch.from_numpy(X5).cuda())
+    g = np.random.default_rng(0)
+    U5 = g.random((c5.m, c5.r)).astype(np.float32)
+    V5 = g.random((c5.n, c5.r)).astype(np.float32)
+    Ud, Vd = torch.from_numpy(U5).cuda(), torch.from_numpy(V5).cuda()
+    h5.set_stage(1)
+    h5.iterate(Ud, Vd, 1)
+    Uo, Vo, _, _ = oracle.sweep(X5, U5.astype(np.float64), V5.astype(np.float64),
+                                oracle.SweepState(stage=1), oracle.options(c5.r, round_f32=1))
+    eu = np.linalg.norm(Ud.cpu().numpy() - Uo) / np.linalg.norm(Uo)
+    ev = np.linalg.norm(Vd.cpu().numpy() - Vo) / np.linalg.norm(Vo)
+    assert eu < 1e-5 and ev < 1e-5, (eu, ev)
+    print(f"smoke ok: HALS f rel err {rel.max():.2e}; tc path ({h5.precision}) U {eu:.2e} "
+          f"V {ev:.2e}; launches {h.launch_count + h5.launch_count}")
