@@ -167,6 +167,12 @@ enmf_status_t enmf_objective(enmf_handle_t h, const float* U, int64_t ldu, const
 enmf_status_t enmf_kkt_residual(enmf_handle_t h, const float* U, int64_t ldu, const float* V,
                                 int64_t ldv, enmf_kkt_t* out_host);
 
+/* The two X passes of a sweep on their own: P = X V (this rank's
+ * row_count x r, fp64, ld r) and Q = X^T U (n x r, fp64, ld r, summed over ranks), on the
+ * contraction path the handle selected.  P or Q may be NULL to skip that pass. */
+enmf_status_t enmf_cross_terms(enmf_handle_t h, const float* U, int64_t ldu, const float* V,
+                               int64_t ldv, double* P, double* Q);
+
 /* End-to-end solve from HOST buffers (single GPU): X_host (m x n, ld = n), U_host
  * (m x r), V_host (n x r) and f_trace_host (n_iters) are host pointers.  Copies X to the
  * device through a pinned staging buffer, runs init + n_iters sweeps, copies U, V back. */

@@ -85,6 +85,7 @@ _sigs = {
                                     ctypes.POINTER(IterInfo)]),
     "enmf_objective": (ctypes.c_int, [_H, _P, _I64, _P, _I64, ctypes.c_int, _D]),
     "enmf_kkt_residual": (ctypes.c_int, [_H, _P, _I64, _P, _I64, ctypes.POINTER(Kkt)]),
+    "enmf_cross_terms": (ctypes.c_int, [_H, _P, _I64, _P, _I64, _P, _P]),
     "enmf_solve_host": (ctypes.c_int, [_H, _P, _P, _P, ctypes.c_int, _D,
                                        ctypes.POINTER(InitInfo)]),
     "enmf_launch_count": (ctypes.c_int64, [_H]),
@@ -252,6 +253,17 @@ class Enmf:
         _check(_lib.enmf_objective(self._h, pu, ldu, pv, ldv, int(bool(exact)), ctypes.byref(f)),
                "enmf_objective")
         return f.value
+
+    def cross_terms(self, U, V):
+        """(P, Q) = (X V, X^T U) as float64 CUDA tensors (the two X passes of a sweep)."""
+        import torch
+        pu, ldu = _mat(U, self.r, "U")
+        pv, ldv = _mat(V, self.r, "V")
+        P = torch.empty(self.rows, self.r, dtype=torch.float64, device="cuda")
+        Q = torch.empty(self.n, self.r, dtype=torch.float64, device="cuda")
+        _check(_lib.enmf_cross_terms(self._h, pu, ldu, pv, ldv, P.data_ptr(), Q.data_ptr()),
+               "enmf_cross_terms")
+        return P, Q
 
     def kkt(self, U, V):
         pu, ldu = _mat(U, self.r, "U")

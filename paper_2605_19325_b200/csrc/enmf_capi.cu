@@ -244,6 +244,23 @@ enmf_status_t enmf_get_profile(enmf_handle_t h, double* ms_host, int64_t* count_
   return ENMF_OK;
 }
 
+enmf_status_t enmf_cross_terms(enmf_handle_t h, const float* U, int64_t ldu, const float* V,
+                               int64_t ldv, double* P, double* Q) {
+  if (!h) return ENMF_ERR_INVALID_ARG;
+  if (!h->bound) return ENMF_ERR_STATE;
+  LaunchScope ls(h);
+  if (P) {
+    ENMF_TRY(validate_ld(V, ldv, h->r));
+    ENMF_TRY(contract_xv(h, V, ldv, P));
+  }
+  if (Q) {
+    ENMF_TRY(validate_ld(U, ldu, h->r));
+    ENMF_TRY(contract_xtu(h, U, ldu, Q));
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  return check_launch();
+}
+
 enmf_status_t enmf_nccl_unique_id(void* out128) {
   if (!out128) return ENMF_ERR_INVALID_ARG;
   return comm_unique_id(out128) == 0 ? ENMF_OK : ENMF_ERR_NCCL;

@@ -63,6 +63,7 @@ struct Params {
   int rp;                    // padded N (multiple of 16, <= 128)
   int r;                     // valid output columns
   int64_t out_rows;          // valid output rows
+  int promote;               // 64-deep stages per fp32 TMEM accumulation chunk
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const Params p) {
         uint32_t buf = 0;
         for (int ks = s0; ks < s1; ++ks) {
           const int t = ks - s0;
-          const bool first = (t % PROMOTE) == 0;
+          const bool first = (t % p.promote) == 0;
           if (first) {
             buf = chunk & 1;
             mbar_wait(bar_tempty + 8 * buf, ((chunk >> 1) & 1) ^ 1);
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const Params p) {
             tc_mma_f16(dt, al, bh, idesc, 1u);
           }
           tc_commit(bar_empty + 8 * stage);          // frees the smem slot when MMAs retire
-          if ((t % PROMOTE) == PROMOTE - 1 || ks == s1 - 1) {
+          if ((t % p.promote) == p.promote - 1 || ks == s1 - 1) {
             tc_commit(bar_tfull + 8 * buf);          // accumulator chunk ready
             ++chunk;
           }
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const Params p) {
       double acc[64];
 #pragma unroll
       for (int c = 0; c < 64; ++c) acc[c] = 0.0;
-      const int nchunks = (s1 - s0 + PROMOTE - 1) / PROMOTE;
+      const int nchunks = (s1 - s0 + p.promote - 1) / p.promote;
       for (int c = 0; c < nchunks; ++c) {
         const uint32_t buf = chunk & 1;
         mbar_wait(bar_tfull + 8 * buf, (chunk >> 1) & 1);
@@ -470,6 +471,7 @@ struct TcState {
   double* partial = nullptr;   // ksplit x (tiles_per_row/2 * 128) x r
   int ksplit = 1;
   int sms = kSMs;
+  int promote = PROMOTE;
 };
 
 bool tc_supported(int64_t rows, int64_t n, int64_t r) {
@@ -495,6 +497,7 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   s->Mt = (rows + BM - 1) / BM;
   s->tiles_per_row = ((n + 127) / 128) * 2;
   s->Kt2 = 2 * s->Mt;
+  if (const char* e = getenv("ENMF_TC_PROMOTE")) s->promote = std::max(1, atoi(e));
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, dev);
@@ -581,6 +584,7 @@ static int launch_gemm(TcState* s, int mode, double* out, int64_t out_ld, int64_
   p.rp = s->rp;
   p.r = (int)s->r;
   p.out_rows = out_rows;
+  p.promote = s->promote;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
