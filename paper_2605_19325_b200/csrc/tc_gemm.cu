@@ -1,29 +1,34 @@
 // tc_gemm.cu -- tcgen05 tensor-core path for the two X passes of a sweep (see tc.h).
 //
 // Per-iteration cost of eNMF is dominated by X V and X^T U.  At r = 128
-// these are compute-bound on SIMT units (64 flop per X byte), so they run on the 5th-gen
-// tensor cores:
+// each X pass carries 64 flop per fp32 byte, far beyond SIMT reach, so the passes run on the
+// 5th-gen tensor cores.  The accumulation must be EXACT: measured on B200, kind::f16 MMAs with
+// fp32 TMEM accumulation lose ~3e-7 relative per 64-deep K stage (not round-to-nearest fp32),
+// which the HALS update amplifies ~r-fold past BASELINE's 1e-5.  This path uses
+// integer MMAs instead:
 //
-//   * X is repacked ONCE (enmf_set_data) into two fp16 planes, X*sX = Xhi + Xlo (sX a power
-//     of two), 4 bytes per element -- the same HBM bytes per pass as fp32 X.  Tiles of
-//     128 rows x 64 columns are stored in the UMMA no-swizzle canonical layout with the
-//     8x8 core matrix (g, kc) at byte (kc*16 + g)*128, so that ONE packed copy is
-//       - a K-major A operand for P = X V   (SBO 128 B between 8-row groups, LBO 2048 B), and
-//       - an MN-major A operand for Q = X^T U (two column-adjacent tiles form 128 contiguous
-//         MN groups at a uniform 2048 B stride).
-//   * The factor (V for pass 1, U for pass 2) is packed per pass into the same form (B operand,
-//     K-major), with a power-of-two scale per column.
-//   * Per 64-deep K stage the MMA warp issues 4 k-steps x 3 products
-//       Xhi*Fhi + Xhi*Flo + Xlo*Fhi   (tcgen05.mma kind::f16, M=128, N=r padded to 16)
-//     into one fp32 TMEM accumulator; every PROMOTE stages (K = 512) the accumulator is drained
-//     by 8 epilogue warps into fp64 registers (double-buffered TMEM, 2 x 128 columns), which
-//     bounds the fp32 accumulation error.
-//   * Warp roles: warp 0 = producer (cp.async.bulk into a 3-stage smem ring, mbarrier
-//     complete_tx), warp 1 = TMEM allocator + single-thread MMA issuer, warps 2..9 = epilogue.
-//     Persistent grid: one CTA per SM walks the work units.
-#include <cuda_fp16.h>
+//   * Operands become three balanced base-2^7 int8 digits,  a*s = d0 + d1/2^7 + d2/2^14  with
+//     d0 in [-127, 127], d1, d2 in [-64, 64]  (X >= 0 uses s = 126/max X; factors use one scale
+//     per column, s_k = 127/max|F_k|).  X is repacked ONCE (enmf_set_data) into 3 byte planes
+//     (3 bytes per element); the factor is repacked per pass.
+//   * tcgen05.mma kind::i8 (M=128, N = r rounded to 16, K=32) accumulates exactly in int32 TMEM:
+//         acc0 = A0 B0,   acc1 = A0 B1 + A1 B0,   acc2 = A0 B2 + A1 B1 + A2 B0
+//     (6 MMAs per 32-deep k-step, 3 accumulators = 384 TMEM columns).  The epilogue forms
+//     (acc0 + acc1 2^-7 + acc2 2^-14) exactly in fp64 and applies 1/(s_X s_k): the only
+//     rounding is the digit truncation (~2^-22 of max, unbiased) and the omitted weight
+//     <= 2^-21 cross terms, so P and Q are far more accurate than fp32-accumulated GEMMs.
+//   * One packed copy serves both passes: tiles of 128 rows x 64 columns per plane in the
+//     UMMA no-swizzle canonical layout, core matrix (g, kc) at byte (kc*16 + g)*128 (8 rows x 16
+//     bytes); it is a K-major A operand for P = X V (SBO 128 B, LBO 2048 B) and, two column-
+//     adjacent tiles giving 8 MN groups at a uniform 2048 B stride, an MN-major A operand for
+//     Q = X^T U (gathered into SBO 1024 B / LBO 128 B in shared memory by 1 KB bulk copies).
+//   * Warp roles: warp 0 = producer (cp.async.bulk into a 4-stage ring, mbarrier complete_tx),
+//     warp 1 = TMEM allocator + single-thread MMA issuer, warps 2..9 = epilogue.  Persistent
+//     grid, one CTA per SM.  Units: pass 1 = one 128-row band over all of K; pass 2 = one
+//     128-column band over a K range (split-K, fixed-order fp64 reduction).
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -32,29 +37,28 @@
 #include "tc.h"
 
 namespace enmf {
-namespace tcg {
+namespace tci {
 
 constexpr int BM = 128;
-constexpr int BK = 64;
-constexpr int STAGES = 3;
-constexpr int PROMOTE = 8;
+constexpr int BK = 64;                          // K elements (= bytes) per stage per row
+constexpr int STAGES = 4;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 32 * (2 + EPI_WARPS);
-constexpr int TILE_A = BM * BK * 2;              // bytes per X tile per plane (16 KB)
-constexpr int MAX_TILE_B = 128 * BK * 2;         // bytes per factor tile per plane (<= 16 KB)
-constexpr int STAGE_BYTES = 2 * TILE_A + 2 * MAX_TILE_B;
+constexpr int PLANES = 3;
+constexpr int TILE_A = BM * BK;                 // bytes per X tile per plane (8 KB)
+constexpr int MAX_TILE_B = 128 * BK;            // bytes per factor tile per plane (<= 8 KB)
+constexpr int STAGE_BYTES = PLANES * TILE_A + PLANES * MAX_TILE_B;   // 48 KB
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;
-constexpr int TMEM_COLS = 256;
+constexpr int TMEM_COLS = 512;                  // 3 x 128 used
+constexpr int64_t MAX_UNIT_K = 65536;           // keeps |acc2| < 2^31 (3 * 127 * 64 * K)
 
 struct Params {
-  const uint8_t* xhi;
-  const uint8_t* xlo;
-  const uint8_t* fhi;
-  const uint8_t* flo;
+  const int8_t* xp[PLANES];
+  const int8_t* fp[PLANES];
   double* out;
   int64_t out_ld;
   int64_t split_stride;
-  const double* colscale;    // r values: 1 / (sX * sF_k)
+  const double* colscale;    // r values: 1 / (s_X * s_k)
   int mode;                  // 0: P = X V ; 1: Q = X^T U
   int num_units;
   int ksplit;
@@ -63,7 +67,6 @@ struct Params {
   int rp;                    // padded N (multiple of 16, <= 128)
   int r;                     // valid output columns
   int64_t out_rows;          // valid output rows
-  int promote;               // 64-deep stages per fp32 TMEM accumulation chunk
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -117,11 +120,11 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
                    "r"(bar)
                : "memory");
 }
-__device__ __forceinline__ void tc_mma_f16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc,
-                                           uint32_t idesc, uint32_t accumulate) {
+__device__ __forceinline__ void tc_mma_i8(uint32_t dtmem, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -145,42 +148,36 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 
 __device__ __forceinline__ void unit_range(const Params& p, int u, int& tile, int& s0, int& s1,
                                            int& split) {
-  if (p.mode == 0) {
-    tile = u;
-    split = 0;
-    s0 = 0;
-    s1 = p.stages_total;
-  } else {
-    tile = u / p.ksplit;
-    split = u % p.ksplit;
-    const int per = (p.stages_total + p.ksplit - 1) / p.ksplit;
-    s0 = split * per;
-    s1 = min(p.stages_total, s0 + per);
-    if (s1 < s0) s1 = s0;
-  }
+  tile = u / p.ksplit;
+  split = u % p.ksplit;
+  const int per = (p.stages_total + p.ksplit - 1) / p.ksplit;
+  s0 = split * per;
+  s1 = min(p.stages_total, s0 + per);
+  if (s1 < s0) s1 = s0;
 }
 
-__global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const Params p) {
+// (a-plane, b-plane, accumulator) of the six products, in issue order
+__constant__ int kProd[6][3] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2}, {2, 0, 2}};
+
+__global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t bars[2 * STAGES + 4];
+  __shared__ __align__(8) uint64_t bars[2 * STAGES + 2];
   __shared__ uint32_t tmem_base_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_full = smem_u32(&bars[0]);
   const uint32_t bar_empty = smem_u32(&bars[STAGES]);
   const uint32_t bar_tfull = smem_u32(&bars[2 * STAGES]);
-  const uint32_t bar_tempty = smem_u32(&bars[2 * STAGES + 2]);
-  const uint32_t tile_b = (uint32_t)p.rp * BK * 2;
+  const uint32_t bar_tempty = smem_u32(&bars[2 * STAGES + 1]);
+  const uint32_t tile_b = (uint32_t)p.rp * BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(bar_full + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(bar_tfull + 8 * b, 1);
-      mbar_init(bar_tempty + 8 * b, EPI_WARPS);
-    }
+    mbar_init(bar_tfull, 1);
+    mbar_init(bar_tempty, EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -196,7 +193,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const Params p) {
   const uint32_t tmem_base = tmem_base_s;
 
   if (warp == 0) {
-    // ===================== producer: bulk copies into the smem ring =====================
+    // ===================== producer =====================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -206,32 +203,32 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const Params p) {
         for (int ks = s0; ks < s1; ++ks) {
           mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const uint32_t fb = bar_full + 8 * stage;
-          mbar_expect_tx(fb, 2 * TILE_A + 2 * tile_b);
-          uint8_t* st = smem + (size_t)stage * STAGE_BYTES;
-          const uint32_t a_hi = smem_u32(st), a_lo = a_hi + TILE_A;
-          const uint32_t b_hi = a_hi + 2 * TILE_A, b_lo = b_hi + tile_b;
+          mbar_expect_tx(fb, PLANES * (TILE_A + tile_b));
+          const uint32_t st = smem_u32(smem + (size_t)stage * STAGE_BYTES);
           if (p.mode == 0) {
             const int64_t off = ((int64_t)tile * p.tiles_per_row + ks) * TILE_A;
-            bulk_g2s(a_hi, p.xhi + off, TILE_A, fb);
-            bulk_g2s(a_lo, p.xlo + off, TILE_A, fb);
+#pragma unroll
+            for (int pl = 0; pl < PLANES; ++pl) bulk_g2s(st + pl * TILE_A, p.xp[pl] + off, TILE_A, fb);
           } else {
-            // A = X^T: 128 output rows (j) = column tiles 2*tile, 2*tile+1 of row band
-            // ks/2; the K stage is the 64-row half (ks & 1) of that band.
+            // A = X^T: output rows j = column tiles 2*tile, 2*tile+1 of row band ks/2; the K
+            // stage is the 64-row half (ks & 1) of that band.
             const int64_t band = ks >> 1;
             const int half = ks & 1;
             for (int t = 0; t < 2; ++t) {
               const int64_t base = (band * p.tiles_per_row + 2 * tile + t) * TILE_A;
-              for (int kc = 0; kc < 8; ++kc) {
+              for (int kc = 0; kc < 4; ++kc) {
                 const int64_t src = base + (int64_t)(kc * 16 + 8 * half) * 128;
-                const uint32_t dst = (uint32_t)((t * 8 + kc) * 1024);
-                bulk_g2s(a_hi + dst, p.xhi + src, 1024, fb);
-                bulk_g2s(a_lo + dst, p.xlo + src, 1024, fb);
+                const uint32_t dst = (uint32_t)((t * 4 + kc) * 1024);
+#pragma unroll
+                for (int pl = 0; pl < PLANES; ++pl)
+                  bulk_g2s(st + pl * TILE_A + dst, p.xp[pl] + src, 1024, fb);
               }
             }
           }
           const int64_t foff = (int64_t)ks * tile_b;
-          bulk_g2s(b_hi, p.fhi + foff, tile_b, fb);
-          bulk_g2s(b_lo, p.flo + foff, tile_b, fb);
+          const uint32_t sb = st + PLANES * TILE_A;
+#pragma unroll
+          for (int pl = 0; pl < PLANES; ++pl) bulk_g2s(sb + pl * tile_b, p.fp[pl] + foff, tile_b, fb);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -239,97 +236,89 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const Params p) {
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
-      // instruction descriptor: F32 accumulate, F16 x F16, A K-major (mode 0) or MN-major
-      // (mode 1), B K-major, N = rp, M = 128
-      const uint32_t idesc = (1u << 4) | ((uint32_t)p.mode << 15) |
+      // idesc: S32 accumulate (c_format 2), signed int8 A and B, A K-major (mode 0) or
+      // MN-major (mode 1), B K-major, N = rp, M = 128
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.mode << 15) |
                              ((uint32_t)(p.rp >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
       const uint32_t a_lbo = p.mode == 0 ? 2048u : 128u;
       const uint32_t a_sbo = p.mode == 0 ? 128u : 1024u;
-      const uint32_t a_kstep = p.mode == 0 ? 4096u : 256u;
+      const uint32_t a_kstep = p.mode == 0 ? 4096u : 512u;
       const uint32_t b_lbo = (uint32_t)p.rp * 16u, b_sbo = 128u;
       const uint32_t b_kstep = (uint32_t)p.rp * 32u;
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t chunk = 0;
+      uint32_t nunit = 0;
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
         int tile, s0, s1, split;
         unit_range(p, u, tile, s0, s1, split);
-        uint32_t buf = 0;
+        if (s1 <= s0) continue;
+        mbar_wait(bar_tempty, (nunit & 1) ^ 1);    // epilogue drained the previous unit
+        tc_fence_after();
         for (int ks = s0; ks < s1; ++ks) {
-          const int t = ks - s0;
-          const bool first = (t % p.promote) == 0;
-          if (first) {
-            buf = chunk & 1;
-            mbar_wait(bar_tempty + 8 * buf, ((chunk >> 1) & 1) ^ 1);
-            tc_fence_after();
-          }
           mbar_wait(bar_full + 8 * stage, phase);
           tc_fence_after();
-          const uint32_t a_hi = smem_u32(smem + (size_t)stage * STAGE_BYTES);
-          const uint32_t a_lo = a_hi + TILE_A;
-          const uint32_t b_hi = a_hi + 2 * TILE_A, b_lo = b_hi + tile_b;
-          const uint32_t dt = tmem_base + buf * 128;
+          const uint32_t a0 = smem_u32(smem + (size_t)stage * STAGE_BYTES);
+          const uint32_t b0 = a0 + PLANES * TILE_A;
 #pragma unroll
-          for (int j = 0; j < BK / 16; ++j) {
-            const uint64_t ah = umma_desc(a_hi + j * a_kstep, a_lbo, a_sbo);
-            const uint64_t al = umma_desc(a_lo + j * a_kstep, a_lbo, a_sbo);
-            const uint64_t bh = umma_desc(b_hi + j * b_kstep, b_lbo, b_sbo);
-            const uint64_t bl = umma_desc(b_lo + j * b_kstep, b_lbo, b_sbo);
-            tc_mma_f16(dt, ah, bh, idesc, (first && j == 0) ? 0u : 1u);
-            tc_mma_f16(dt, ah, bl, idesc, 1u);
-            tc_mma_f16(dt, al, bh, idesc, 1u);
+          for (int j = 0; j < BK / 32; ++j) {
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+              const int pa = kProd[q][0], pb = kProd[q][1], ac = kProd[q][2];
+              const uint64_t ad = umma_desc(a0 + pa * TILE_A + j * a_kstep, a_lbo, a_sbo);
+              const uint64_t bd = umma_desc(b0 + pb * tile_b + j * b_kstep, b_lbo, b_sbo);
+              const bool fresh = ks == s0 && j == 0 && (q == 0 || q == 1 || q == 3);
+              tc_mma_i8(tmem_base + ac * 128, ad, bd, idesc, fresh ? 0u : 1u);
+            }
           }
           tc_commit(bar_empty + 8 * stage);          // frees the smem slot when MMAs retire
-          if ((t % p.promote) == p.promote - 1 || ks == s1 - 1) {
-            tc_commit(bar_tfull + 8 * buf);          // accumulator chunk ready
-            ++chunk;
-          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        tc_commit(bar_tfull);                        // unit's accumulators complete
+        ++nunit;
       }
     }
   } else {
-    // ===================== epilogue: TMEM fp32 chunks -> fp64 registers =====================
+    // ===================== epilogue: exact int32 -> fp64 =====================
     const int e = warp - 2;
     const int q = warp & 3;                 // TMEM lane quadrant of this warp
     const int hcol = e >> 2;                // columns [64*hcol, 64*hcol + 64)
     const int row_in_tile = 32 * q + lane;
-    uint32_t chunk = 0;
+    uint32_t nunit = 0;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
       int tile, s0, s1, split;
       unit_range(p, u, tile, s0, s1, split);
       if (s1 <= s0) continue;
-      double acc[64];
-#pragma unroll
-      for (int c = 0; c < 64; ++c) acc[c] = 0.0;
-      const int nchunks = (s1 - s0 + p.promote - 1) / p.promote;
-      for (int c = 0; c < nchunks; ++c) {
-        const uint32_t buf = chunk & 1;
-        mbar_wait(bar_tfull + 8 * buf, (chunk >> 1) & 1);
-        tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + buf * 128 + 64 * hcol;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t v[32];
-          TMEM_LD32(taddr + 32 * h, v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int i = 0; i < 32; ++i) acc[32 * h + i] += (double)__uint_as_float(v[i]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
-        ++chunk;
-      }
+      mbar_wait(bar_tfull, nunit & 1);
+      tc_fence_after();
       const int64_t row = (int64_t)tile * BM + row_in_tile;
-      if (row < p.out_rows) {
-        double* o = p.out + (int64_t)split * p.split_stride + row * p.out_ld;
+      double* o = p.out + (int64_t)split * p.split_stride + row * p.out_ld;
+      const uint32_t lane_addr = tmem_base + ((uint32_t)(32 * q) << 16);
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const int col = 64 * hcol + c;
-          if (col < p.r) o[col] = acc[c] * p.colscale[col];
+      for (int h = 0; h < 2; ++h) {
+        const int c0 = 64 * hcol + 32 * h;
+        if (c0 >= p.rp) break;
+        uint32_t v0[32], v1[32], v2[32];
+        TMEM_LD32(lane_addr + c0, v0);
+        TMEM_LD32(lane_addr + 128 + c0, v1);
+        TMEM_LD32(lane_addr + 256 + c0, v2);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < p.out_rows) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int col = c0 + i;
+            if (col < p.r) {
+              // exact in fp64: |acc| < 2^31 with 14 fractional bits
+              const double v = (double)(int)v0[i] + (double)(int)v1[i] * 0.0078125 +
+                               (double)(int)v2[i] * 6.103515625e-05;
+              o[col] = v * p.colscale[col];
+            }
+          }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_tempty);
+      ++nunit;
     }
   }
   tc_fence_before();
@@ -342,97 +331,103 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const Params p) {
 }
 
 // ------------------------------------------------------------------ packing
-__device__ __forceinline__ void split16(float v, __half& hi, __half& lo) {
-  hi = __float2half_rn(v);
-  lo = __float2half_rn(v - __half2float(hi));
+// Balanced base-2^7 digits of t (|t| <= 127.5): t = d0 + d1/2^7 + d2/2^14 + O(2^-15).
+__device__ __forceinline__ void digits3(double t, int8_t& d0, int8_t& d1, int8_t& d2) {
+  const double a = rint(t);
+  const double r1 = (t - a) * 128.0;
+  const double b = rint(r1);
+  const double c = rint((r1 - b) * 128.0);
+  d0 = (int8_t)a;
+  d1 = (int8_t)b;
+  d2 = (int8_t)c;
 }
 
-// X (rows x n, ld) * sx -> hi/lo planes of [Mt][tiles_per_row] tiles.  One thread writes one
-// 16-byte row chunk (8 consecutive columns) of each plane; consecutive threads read
+// X (rows x n, ld) * sx -> 3 digit planes of [Mt][tiles_per_row] tiles.  One thread writes one
+// 16-byte row chunk (16 consecutive columns) of each plane; consecutive threads read
 // consecutive chunks of an X row (coalesced reads).
 __global__ void pack_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n,
-                              float sx, int64_t tiles_per_row, int64_t Mt, uint4* hi, uint4* lo) {
-  const int64_t cpr = tiles_per_row * 8;                 // 16-byte chunks per padded row
+                              double sx, int64_t tiles_per_row, int64_t Mt, uint4* p0, uint4* p1,
+                              uint4* p2) {
+  const int64_t cpr = tiles_per_row * 4;                 // 16-byte chunks per padded row
   const int64_t total = Mt * BM * cpr;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < total;
        c += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = c / cpr, jc = c - i * cpr;
-    const int64_t j0 = jc * 8;
-    __align__(16) __half h[8], l[8];
+    const int64_t j0 = jc * 16;
+    __align__(16) int8_t d0[16], d1[16], d2[16];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 16; ++k) {
       const int64_t j = j0 + k;
-      const float v = (i < rows && j < n) ? X[i * ldx + j] * sx : 0.0f;
-      split16(v, h[k], l[k]);
+      const double v = (i < rows && j < n) ? (double)X[i * ldx + j] * sx : 0.0;
+      digits3(v, d0[k], d1[k], d2[k]);
     }
     const int64_t mt = i / BM, g = (i % BM) / 8, ri = i % 8;
-    const int64_t kt = j0 / BK, kc = (j0 % BK) / 8;
+    const int64_t kt = j0 / BK, kc = (j0 % BK) / 16;
     const int64_t byte = (mt * tiles_per_row + kt) * TILE_A + (kc * 16 + g) * 128 + ri * 16;
-    hi[byte / 16] = *reinterpret_cast<uint4*>(h);
-    lo[byte / 16] = *reinterpret_cast<uint4*>(l);
+    p0[byte / 16] = *reinterpret_cast<uint4*>(d0);
+    p1[byte / 16] = *reinterpret_cast<uint4*>(d1);
+    p2[byte / 16] = *reinterpret_cast<uint4*>(d2);
   }
 }
 
-// Factor F (K x r, ld) * colscale -> B tiles [Kt][rp x 64]: chunk (kc*(rp/8) + g)*128 + ri*16
-// holds F[kt*64 + kc*8 + 0..7][g*8 + ri].
-__global__ void pack_factor_kernel(const float* __restrict__ F, int64_t ldf, int64_t K, int r,
-                                   int rp, const float* __restrict__ fscale, int64_t Kt,
-                                   uint4* hi, uint4* lo) {
-  const int64_t chunks_per_tile = (int64_t)rp * BK / 8;
-  const int64_t total = Kt * chunks_per_tile;
+// Factor F (K x r, ld) * fscale[col] -> B tiles [Kt][rp x 64]: the 16-byte chunk at
+// (kc*(rp/8) + g)*128 + ri*16 holds F[kt*64 + kc*16 + 0..15][g*8 + ri].  A block stages 64
+// factor rows in shared memory so global reads are coalesced.
+__global__ void __launch_bounds__(256)
+pack_factor_kernel(const float* __restrict__ F, int64_t ldf, int64_t K, int r, int rp,
+                   const double* __restrict__ fscale, int64_t Kt, uint4* p0, uint4* p1, uint4* p2) {
+  __shared__ float tileF[BK][129];
   const int gpt = rp / 8;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < total;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t kt = c / chunks_per_tile;
-    const int64_t w = c - kt * chunks_per_tile;            // 16-byte chunk index in the tile
-    const int kc = (int)(w / (gpt * 8));
-    const int rem = (int)(w % (gpt * 8));
-    const int g = rem / 8, ri = rem % 8;
-    const int col = g * 8 + ri;
-    const float s = col < r ? fscale[col] : 0.0f;
-    __align__(16) __half h[8], l[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int64_t kk = kt * BK + kc * 8 + k;
-      const float v = (col < r && kk < K) ? F[kk * ldf + col] * s : 0.0f;
-      split16(v, h[k], l[k]);
+  const int chunks = 4 * gpt * 8;                        // 16-byte chunks per tile per plane
+  for (int64_t kt = blockIdx.x; kt < Kt; kt += gridDim.x) {
+    for (int e = threadIdx.x; e < BK * rp; e += blockDim.x) {
+      const int kk = e / rp, col = e % rp;
+      const int64_t row = kt * BK + kk;
+      tileF[kk][col] = (row < K && col < r) ? F[row * ldf + col] : 0.0f;
     }
-    hi[c] = *reinterpret_cast<uint4*>(h);
-    lo[c] = *reinterpret_cast<uint4*>(l);
+    __syncthreads();
+    for (int w = threadIdx.x; w < chunks; w += blockDim.x) {
+      const int kc = w / (gpt * 8);
+      const int rem = w % (gpt * 8);
+      const int col = (rem / 8) * 8 + rem % 8;
+      const double s = col < r ? fscale[col] : 0.0;
+      __align__(16) int8_t d0[16], d1[16], d2[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) digits3((double)tileF[kc * 16 + k][col] * s, d0[k], d1[k], d2[k]);
+      const int64_t idx = kt * chunks + w;
+      p0[idx] = *reinterpret_cast<uint4*>(d0);
+      p1[idx] = *reinterpret_cast<uint4*>(d1);
+      p2[idx] = *reinterpret_cast<uint4*>(d2);
+    }
+    __syncthreads();
   }
 }
 
 // Per-column max |F| (F rows x r) into maxbits[r] (float bits; max is order independent).
 __global__ void colmax_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
                               unsigned* maxbits) {
-  __shared__ float m[128];
-  for (int k = threadIdx.x; k < r; k += blockDim.x) m[k] = 0.0f;
+  __shared__ unsigned m[128];
+  for (int k = threadIdx.x; k < r; k += blockDim.x) m[k] = 0u;
   __syncthreads();
   const int64_t total = rows * (int64_t)r;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / r;
     const int k = (int)(e - i * r);
-    const float a = fabsf(F[i * ldf + k]);
-    atomicMax(reinterpret_cast<unsigned*>(&m[k]), __float_as_uint(a));
+    atomicMax(&m[k], __float_as_uint(fabsf(F[i * ldf + k])));
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < r; k += blockDim.x) atomicMax(&maxbits[k], __float_as_uint(m[k]));
+  for (int k = threadIdx.x; k < r; k += blockDim.x) atomicMax(&maxbits[k], m[k]);
 }
 
-// fscale[k] = 2^(14 - floor(log2 max|F_k|)) ; colscale[k] = 1 / (sx * fscale[k])  (exact).
-__global__ void scales_kernel(const unsigned* maxbits, int r, double sx, float* fscale,
+// fscale[k] = 127 / max|F_k| ; colscale[k] = 1 / (sx * fscale[k]).
+__global__ void scales_kernel(const unsigned* maxbits, int r, double sx, double* fscale,
                               double* colscale) {
   for (int k = threadIdx.x; k < r; k += blockDim.x) {
-    const float mx = __uint_as_float(maxbits[k]);
-    int e = 0;
-    if (mx > 0.0f) {
-      frexpf(mx, &e);                   // mx in [2^(e-1), 2^e)
-      e = 14 - (e - 1);
-    }
-    const float s = ldexpf(1.0f, e);
+    const double mx = (double)__uint_as_float(maxbits[k]);
+    const double s = mx > 0.0 ? 127.0 / mx : 1.0;
     fscale[k] = s;
-    colscale[k] = 1.0 / (sx * (double)s);
+    colscale[k] = 1.0 / (sx * s);
   }
 }
 
@@ -450,9 +445,9 @@ __global__ void maxabs_x_kernel(const float* __restrict__ X, int64_t ldx, int64_
   if ((threadIdx.x & 31) == 0) atomicMax(maxbits, m);
 }
 
-}  // namespace tcg
+}  // namespace tci
 
-using namespace tcg;
+using namespace tci;
 
 struct TcState {
   int64_t rows = 0, n = 0, r = 0;
@@ -461,17 +456,14 @@ struct TcState {
   int64_t tiles_per_row = 0;   // 64-column tiles per band (even: 128-column pairs)
   int64_t Kt2 = 0;             // 64-row K stages of pass 2 (= 2 Mt)
   double sx = 1.0;
-  uint8_t* xhi = nullptr;
-  uint8_t* xlo = nullptr;
-  uint8_t* fhi = nullptr;
-  uint8_t* flo = nullptr;
+  int8_t* xp[PLANES] = {nullptr, nullptr, nullptr};
+  int8_t* fp[PLANES] = {nullptr, nullptr, nullptr};
   unsigned* maxbits = nullptr; // r + 1
-  float* fscale = nullptr;     // r
+  double* fscale = nullptr;    // r
   double* colscale = nullptr;  // r
-  double* partial = nullptr;   // ksplit x (tiles_per_row/2 * 128) x r
-  int ksplit = 1;
+  double* partial = nullptr;   // ksplit2 x n x r  (pass 2)  /  ksplit1 x rows x r (pass 1)
+  int ksplit1 = 1, ksplit2 = 1;
   int sms = kSMs;
-  int promote = PROMOTE;
 };
 
 bool tc_supported(int64_t rows, int64_t n, int64_t r) {
@@ -480,10 +472,25 @@ bool tc_supported(int64_t rows, int64_t n, int64_t r) {
 
 void tc_destroy(TcState* s) {
   if (!s) return;
-  void* bufs[] = {s->xhi, s->xlo, s->fhi, s->flo, s->maxbits, s->fscale, s->colscale, s->partial};
+  for (int p = 0; p < PLANES; ++p) {
+    if (s->xp[p]) cudaFree(s->xp[p]);
+    if (s->fp[p]) cudaFree(s->fp[p]);
+  }
+  void* bufs[] = {s->maxbits, s->fscale, s->colscale, s->partial};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete s;
+}
+
+// Split count for `tiles` output bands over `stages` K stages: enough units to fill the GPU,
+// every unit K <= MAX_UNIT_K, no empty unit.
+static int choose_split(int64_t tiles, int64_t stages, int sms) {
+  int ks = (int)((4 * sms + tiles - 1) / tiles);
+  const int kmin = (int)((stages * BK + MAX_UNIT_K - 1) / MAX_UNIT_K);
+  ks = std::max(std::max(ks, kmin), 1);
+  ks = std::min<int64_t>(ks, stages);
+  const int64_t per = (stages + ks - 1) / ks;
+  return (int)((stages + per - 1) / per);
 }
 
 int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t n, int64_t r,
@@ -497,35 +504,32 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   s->Mt = (rows + BM - 1) / BM;
   s->tiles_per_row = ((n + 127) / 128) * 2;
   s->Kt2 = 2 * s->Mt;
-  if (const char* e = getenv("ENMF_TC_PROMOTE")) s->promote = std::max(1, atoi(e));
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, dev);
+  // pass 1 splits K only when a band alone would overflow int32 or the grid is too small
+  s->ksplit1 = 1;
+  if (s->tiles_per_row * BK > MAX_UNIT_K || s->Mt < s->sms)
+    s->ksplit1 = choose_split(s->Mt, s->tiles_per_row, s->sms);
+  s->ksplit2 = choose_split(s->tiles_per_row / 2, s->Kt2, s->sms);
   const size_t plane = (size_t)s->Mt * s->tiles_per_row * TILE_A;
   const int64_t fK = std::max<int64_t>(s->tiles_per_row, s->Kt2);
-  const size_t fplane = (size_t)fK * s->rp * BK * 2;
-  const int64_t n_pad = s->tiles_per_row / 2 * 128;
-  const int64_t units2 = s->tiles_per_row / 2;
-  int ks = (int)((4 * s->sms + units2 - 1) / units2);
-  ks = std::max(1, std::min<int>(ks, (int)s->Kt2));
-  const int per = (int)((s->Kt2 + ks - 1) / ks);
-  ks = (int)((s->Kt2 + per - 1) / per);          // no empty split ranges
-  s->ksplit = ks;
+  const size_t fplane = (size_t)fK * s->rp * BK;
+  const size_t part = std::max<size_t>((size_t)s->ksplit2 * n * r,
+                                       s->ksplit1 > 1 ? (size_t)s->ksplit1 * rows * r : 0);
   cudaError_t e = cudaSuccess;
-  if (!e) e = cudaMalloc(&s->xhi, plane);
-  if (!e) e = cudaMalloc(&s->xlo, plane);
-  if (!e) e = cudaMalloc(&s->fhi, fplane);
-  if (!e) e = cudaMalloc(&s->flo, fplane);
+  for (int p = 0; p < PLANES && !e; ++p) e = cudaMalloc(&s->xp[p], plane);
+  for (int p = 0; p < PLANES && !e; ++p) e = cudaMalloc(&s->fp[p], fplane);
   if (!e) e = cudaMalloc(&s->maxbits, sizeof(unsigned) * (r + 1));
-  if (!e) e = cudaMalloc(&s->fscale, sizeof(float) * r);
+  if (!e) e = cudaMalloc(&s->fscale, sizeof(double) * r);
   if (!e) e = cudaMalloc(&s->colscale, sizeof(double) * r);
-  if (!e) e = cudaMalloc(&s->partial, sizeof(double) * (size_t)ks * n_pad * r);
+  if (!e) e = cudaMalloc(&s->partial, sizeof(double) * std::max<size_t>(part, 1));
   if (e) {
     cudaGetLastError();
     tc_destroy(s);
     return e == cudaErrorMemoryAllocation ? 2 : 1;
   }
-  // global power-of-two scale of X: max|X| * sx in [2^14, 2^15)
+  // X scale: max X * sx = 126 (X >= 0, so the leading digit stays in [0, 126])
   cudaMemsetAsync(s->maxbits, 0, sizeof(unsigned), st);
   maxabs_x_kernel<<<4 * s->sms, 256, 0, st>>>(X, ldx, rows, n, s->maxbits);
   unsigned mb = 0;
@@ -536,14 +540,9 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   }
   float mx;
   memcpy(&mx, &mb, sizeof(mx));
-  int ex = 0;
-  if (mx > 0.0f) {
-    frexpf(mx, &ex);
-    ex = 14 - (ex - 1);
-  }
-  s->sx = ldexp(1.0, ex);
-  pack_x_kernel<<<8 * s->sms, 256, 0, st>>>(X, ldx, rows, n, (float)s->sx, s->tiles_per_row, s->Mt,
-                                            (uint4*)s->xhi, (uint4*)s->xlo);
+  s->sx = mx > 0.0f ? 126.0 / (double)mx : 1.0;
+  pack_x_kernel<<<8 * s->sms, 256, 0, st>>>(X, ldx, rows, n, s->sx, s->tiles_per_row, s->Mt,
+                                            (uint4*)s->xp[0], (uint4*)s->xp[1], (uint4*)s->xp[2]);
   count_launch(2);
   if (cudaGetLastError() != cudaSuccess) {
     tc_destroy(s);
@@ -559,56 +558,61 @@ static void pack_factor(TcState* s, const float* F, int64_t ldf, int64_t K, int6
   cudaMemsetAsync(s->maxbits, 0, sizeof(unsigned) * r, st);
   colmax_kernel<<<2 * s->sms, 256, 0, st>>>(F, ldf, K, r, s->maxbits);
   scales_kernel<<<1, 128, 0, st>>>(s->maxbits, r, s->sx, s->fscale, s->colscale);
-  pack_factor_kernel<<<4 * s->sms, 256, 0, st>>>(F, ldf, K, r, s->rp, s->fscale, Kt,
-                                                 (uint4*)s->fhi, (uint4*)s->flo);
+  pack_factor_kernel<<<(int)std::min<int64_t>(Kt, 8 * s->sms), 256, 0, st>>>(
+      F, ldf, K, r, s->rp, s->fscale, Kt, (uint4*)s->fp[0], (uint4*)s->fp[1], (uint4*)s->fp[2]);
   count_launch(3);
 }
 
 static int launch_gemm(TcState* s, int mode, double* out, int64_t out_ld, int64_t split_stride,
-                       int num_units, int ksplit, int stages_total, int64_t out_rows,
+                       int tiles, int ksplit, int stages_total, int64_t out_rows,
                        cudaStream_t st) {
   Params p;
-  p.xhi = s->xhi;
-  p.xlo = s->xlo;
-  p.fhi = s->fhi;
-  p.flo = s->flo;
+  for (int q = 0; q < PLANES; ++q) {
+    p.xp[q] = s->xp[q];
+    p.fp[q] = s->fp[q];
+  }
   p.out = out;
   p.out_ld = out_ld;
   p.split_stride = split_stride;
   p.colscale = s->colscale;
   p.mode = mode;
-  p.num_units = num_units;
+  p.num_units = tiles * ksplit;
   p.ksplit = ksplit;
   p.stages_total = stages_total;
   p.tiles_per_row = s->tiles_per_row;
   p.rp = s->rp;
   p.r = (int)s->r;
   p.out_rows = out_rows;
-  p.promote = s->promote;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(tc_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
-  const int grid = std::min(num_units, s->sms);
-  tc_gemm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(p);
+  const int grid = std::min(p.num_units, s->sms);
+  tc_i8_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(p);
   count_launch();
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st) {
-  // B = V (K = n), packed over all 64-column stages of X
+  // B = V (K = n), over all 64-column stages of X
   pack_factor(s, V, ldv, s->n, s->tiles_per_row, st);
-  return launch_gemm(s, 0, P, s->r, 0, (int)s->Mt, 1, (int)s->tiles_per_row, s->rows, st);
+  if (s->ksplit1 == 1)
+    return launch_gemm(s, 0, P, s->r, 0, (int)s->Mt, 1, (int)s->tiles_per_row, s->rows, st);
+  if (launch_gemm(s, 0, s->partial, s->r, s->rows * s->r, (int)s->Mt, s->ksplit1,
+                  (int)s->tiles_per_row, s->rows, st))
+    return 1;
+  reduce_parts(s->partial, s->ksplit1, s->rows * s->r, P, st);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st) {
   // B = U (K = rows of X), split-K partials reduced in a fixed order
   pack_factor(s, U, ldu, s->rows, s->Kt2, st);
-  const int units = (int)(s->tiles_per_row / 2) * s->ksplit;
-  if (launch_gemm(s, 1, s->partial, s->r, s->n * s->r, units, s->ksplit, (int)s->Kt2, s->n, st))
+  if (launch_gemm(s, 1, s->partial, s->r, s->n * s->r, (int)(s->tiles_per_row / 2), s->ksplit2,
+                  (int)s->Kt2, s->n, st))
     return 1;
-  reduce_parts(s->partial, s->ksplit, s->n * s->r, Q, st);
+  reduce_parts(s->partial, s->ksplit2, s->n * s->r, Q, st);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
