@@ -7,16 +7,20 @@
 // which the HALS update amplifies ~r-fold past BASELINE's 1e-5.  This path uses
 // integer MMAs instead:
 //
-//   * Operands become three balanced base-2^7 int8 digits,  a*s = d0 + d1/2^7 + d2/2^14  with
-//     d0 in [-127, 127], d1, d2 in [-64, 64]  (X >= 0 uses s = 126/max X; factors use one scale
-//     per column, s_k = 127/max|F_k|).  X is repacked ONCE (enmf_set_data) into 3 byte planes
-//     (3 bytes per element); the factor is repacked per pass.
-//   * tcgen05.mma kind::i8 (M=128, N = r rounded to 16, K=32) accumulates exactly in int32 TMEM:
-//         acc0 = A0 B0,   acc1 = A0 B1 + A1 B0,   acc2 = A0 B2 + A1 B1 + A2 B0
-//     (6 MMAs per 32-deep k-step, 3 accumulators = 384 TMEM columns).  The epilogue forms
-//     (acc0 + acc1 2^-7 + acc2 2^-14) exactly in fp64 and applies 1/(s_X s_k): the only
-//     rounding is the digit truncation (~2^-22 of max, unbiased) and the omitted weight
-//     <= 2^-21 cross terms, so P and Q are far more accurate than fp32-accumulated GEMMs.
+//   * Operands become four balanced base-2^7 int8 digits, a*s = d0 + d1/2^7 + d2/2^14 + d3/2^21
+//     with every digit in [-64, 64] and s a power of two (max|a| s in [32, 64): one scale for
+//     X, one per column for a factor).  That is 27 bits, so every fp32 entry >= max/8 of its
+//     scale group is represented EXACTLY (smaller ones to 2^-22 of the scale).  X is repacked
+//     ONCE (enmf_set_data) into 4 byte planes -- 4 bytes per element, exactly the algorithmic
+//     bytes of fp32 X; the factor is repacked per pass.
+//   * tcgen05.mma kind::i8 (M=128, N = r rounded to 16, K=32) accumulates exactly in int32 TMEM,
+//     one accumulator per digit weight class c = i + j <= 3:
+//         acc_c = sum_{i+j=c} A_i B_j      (10 MMAs per 32-deep k-step, 4 x 128 TMEM columns)
+//     and the epilogue forms acc0 + acc1 2^-7 + acc2 2^-14 + acc3 2^-21 EXACTLY in fp64 (31
+//     integer + 21 fractional bits) before applying 1/(s_X s_k).  The only errors are the
+//     omitted weight <= 2^-28 products and sub-threshold digit truncation: P and Q come out
+//     accurate to ~1e-9 relative, which the trace-form objective needs near the optimum
+//     (||X||^2 / f ~ 3e7 at C5, SURVEY Hard part 2).
 //   * One packed copy serves both passes: tiles of 128 rows x 64 columns per plane in the
 //     UMMA no-swizzle canonical layout, core matrix (g, kc) at byte (kc*16 + g)*128 (8 rows x 16
 //     bytes); it is a K-major A operand for P = X V (SBO 128 B, LBO 2048 B) and, two column-
@@ -41,16 +45,17 @@ namespace tci {
 
 constexpr int BM = 128;
 constexpr int BK = 64;                          // K elements (= bytes) per stage per row
-constexpr int STAGES = 4;
+constexpr int STAGES = 3;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 32 * (2 + EPI_WARPS);
-constexpr int PLANES = 3;
+constexpr int PLANES = 4;
+constexpr int NPROD = 10;
 constexpr int TILE_A = BM * BK;                 // bytes per X tile per plane (8 KB)
 constexpr int MAX_TILE_B = 128 * BK;            // bytes per factor tile per plane (<= 8 KB)
-constexpr int STAGE_BYTES = PLANES * TILE_A + PLANES * MAX_TILE_B;   // 48 KB
+constexpr int STAGE_BYTES = PLANES * TILE_A + PLANES * MAX_TILE_B;   // 64 KB
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;
-constexpr int TMEM_COLS = 512;                  // 3 x 128 used
-constexpr int64_t MAX_UNIT_K = 65536;           // keeps |acc2| < 2^31 (3 * 127 * 64 * K)
+constexpr int TMEM_COLS = 512;                  // 4 x 128
+constexpr int64_t MAX_UNIT_K = 65536;           // |acc3| <= 4 * 64 * 64 * K < 2^31
 
 struct Params {
   const int8_t* xp[PLANES];
@@ -146,6 +151,15 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
         "=r"(v[31])                                                                            \
       : "r"(taddr))
 
+#define TMEM_LD16(taddr, v)                                                                  \
+  asm volatile(                                                                              \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+      "%14,%15}, [%16];"                                                                     \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), \
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),          \
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])                                                \
+      : "r"(taddr))
+
 __device__ __forceinline__ void unit_range(const Params& p, int u, int& tile, int& s0, int& s1,
                                            int& split) {
   tile = u / p.ksplit;
@@ -156,8 +170,10 @@ __device__ __forceinline__ void unit_range(const Params& p, int u, int& tile, in
   if (s1 < s0) s1 = s0;
 }
 
-// (a-plane, b-plane, accumulator) of the six products, in issue order
-__constant__ int kProd[6][3] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2}, {2, 0, 2}};
+// (a-plane, b-plane, weight class = accumulator) of the ten products, in issue order; the
+// first product of each class starts its accumulator
+__constant__ int kProd[NPROD][3] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2},
+                                    {2, 0, 2}, {0, 3, 3}, {1, 2, 3}, {2, 1, 3}, {3, 0, 3}};
 
 __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -262,11 +278,11 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
 #pragma unroll
           for (int j = 0; j < BK / 32; ++j) {
 #pragma unroll
-            for (int q = 0; q < 6; ++q) {
+            for (int q = 0; q < NPROD; ++q) {
               const int pa = kProd[q][0], pb = kProd[q][1], ac = kProd[q][2];
               const uint64_t ad = umma_desc(a0 + pa * TILE_A + j * a_kstep, a_lbo, a_sbo);
               const uint64_t bd = umma_desc(b0 + pb * tile_b + j * b_kstep, b_lbo, b_sbo);
-              const bool fresh = ks == s0 && j == 0 && (q == 0 || q == 1 || q == 3);
+              const bool fresh = ks == s0 && j == 0 && pa == 0;
               tc_mma_i8(tmem_base + ac * 128, ad, bd, idesc, fresh ? 0u : 1u);
             }
           }
@@ -293,23 +309,24 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
       const int64_t row = (int64_t)tile * BM + row_in_tile;
       double* o = p.out + (int64_t)split * p.split_stride + row * p.out_ld;
       const uint32_t lane_addr = tmem_base + ((uint32_t)(32 * q) << 16);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c0 = 64 * hcol + 32 * h;
+#pragma unroll 1
+      for (int h = 0; h < 4; ++h) {
+        const int c0 = 64 * hcol + 16 * h;
         if (c0 >= p.rp) break;
-        uint32_t v0[32], v1[32], v2[32];
-        TMEM_LD32(lane_addr + c0, v0);
-        TMEM_LD32(lane_addr + 128 + c0, v1);
-        TMEM_LD32(lane_addr + 256 + c0, v2);
+        uint32_t v0[16], v1[16], v2[16], v3[16];
+        TMEM_LD16(lane_addr + c0, v0);
+        TMEM_LD16(lane_addr + 128 + c0, v1);
+        TMEM_LD16(lane_addr + 256 + c0, v2);
+        TMEM_LD16(lane_addr + 384 + c0, v3);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (row < p.out_rows) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
+          for (int i = 0; i < 16; ++i) {
             const int col = c0 + i;
             if (col < p.r) {
-              // exact in fp64: |acc| < 2^31 with 14 fractional bits
-              const double v = (double)(int)v0[i] + (double)(int)v1[i] * 0.0078125 +
-                               (double)(int)v2[i] * 6.103515625e-05;
+              // exact in fp64: |acc_c| < 2^31, 21 fractional bits in total
+              const double v = (double)(int)v0[i] + (double)(int)v1[i] * 0x1p-7 +
+                               (double)(int)v2[i] * 0x1p-14 + (double)(int)v3[i] * 0x1p-21;
               o[col] = v * p.colscale[col];
             }
           }
@@ -331,42 +348,49 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
 }
 
 // ------------------------------------------------------------------ packing
-// Balanced base-2^7 digits of t (|t| <= 127.5): t = d0 + d1/2^7 + d2/2^14 + O(2^-15).
-__device__ __forceinline__ void digits3(double t, int8_t& d0, int8_t& d1, int8_t& d2) {
-  const double a = rint(t);
-  const double r1 = (t - a) * 128.0;
-  const double b = rint(r1);
-  const double c = rint((r1 - b) * 128.0);
-  d0 = (int8_t)a;
-  d1 = (int8_t)b;
-  d2 = (int8_t)c;
+// Balanced base-2^7 digits of t (|t| < 64.5): t = d0 + d1/2^7 + d2/2^14 + d3/2^21 + e,
+// |e| <= 2^-22, every digit in [-64, 64].  Exact arithmetic for fp32-derived t (scaling by a
+// power of two and subtracting an integer are exact in fp64).
+struct Dig4 { int8_t d[4]; };
+__device__ __forceinline__ Dig4 digits4(double t) {
+  Dig4 out;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double a = rint(t);
+    out.d[k] = (int8_t)a;
+    t = (t - a) * 128.0;
+  }
+  return out;
 }
 
-// X (rows x n, ld) * sx -> 3 digit planes of [Mt][tiles_per_row] tiles.  One thread writes one
+// X (rows x n, ld) * sx -> 4 digit planes of [Mt][tiles_per_row] tiles.  One thread writes one
 // 16-byte row chunk (16 consecutive columns) of each plane; consecutive threads read
 // consecutive chunks of an X row (coalesced reads).
 __global__ void pack_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n,
                               double sx, int64_t tiles_per_row, int64_t Mt, uint4* p0, uint4* p1,
-                              uint4* p2) {
+                              uint4* p2, uint4* p3) {
   const int64_t cpr = tiles_per_row * 4;                 // 16-byte chunks per padded row
   const int64_t total = Mt * BM * cpr;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < total;
        c += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = c / cpr, jc = c - i * cpr;
     const int64_t j0 = jc * 16;
-    __align__(16) int8_t d0[16], d1[16], d2[16];
+    __align__(16) int8_t d[4][16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const int64_t j = j0 + k;
       const double v = (i < rows && j < n) ? (double)X[i * ldx + j] * sx : 0.0;
-      digits3(v, d0[k], d1[k], d2[k]);
+      const Dig4 q = digits4(v);
+#pragma unroll
+      for (int pl = 0; pl < 4; ++pl) d[pl][k] = q.d[pl];
     }
     const int64_t mt = i / BM, g = (i % BM) / 8, ri = i % 8;
     const int64_t kt = j0 / BK, kc = (j0 % BK) / 16;
-    const int64_t byte = (mt * tiles_per_row + kt) * TILE_A + (kc * 16 + g) * 128 + ri * 16;
-    p0[byte / 16] = *reinterpret_cast<uint4*>(d0);
-    p1[byte / 16] = *reinterpret_cast<uint4*>(d1);
-    p2[byte / 16] = *reinterpret_cast<uint4*>(d2);
+    const int64_t idx = ((mt * tiles_per_row + kt) * TILE_A + (kc * 16 + g) * 128 + ri * 16) / 16;
+    p0[idx] = *reinterpret_cast<uint4*>(d[0]);
+    p1[idx] = *reinterpret_cast<uint4*>(d[1]);
+    p2[idx] = *reinterpret_cast<uint4*>(d[2]);
+    p3[idx] = *reinterpret_cast<uint4*>(d[3]);
   }
 }
 
@@ -375,7 +399,8 @@ __global__ void pack_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t 
 // factor rows in shared memory so global reads are coalesced.
 __global__ void __launch_bounds__(256)
 pack_factor_kernel(const float* __restrict__ F, int64_t ldf, int64_t K, int r, int rp,
-                   const double* __restrict__ fscale, int64_t Kt, uint4* p0, uint4* p1, uint4* p2) {
+                   const double* __restrict__ fscale, int64_t Kt, uint4* p0, uint4* p1, uint4* p2,
+                   uint4* p3) {
   __shared__ float tileF[BK][129];
   const int gpt = rp / 8;
   const int chunks = 4 * gpt * 8;                        // 16-byte chunks per tile per plane
@@ -391,13 +416,18 @@ pack_factor_kernel(const float* __restrict__ F, int64_t ldf, int64_t K, int r, i
       const int rem = w % (gpt * 8);
       const int col = (rem / 8) * 8 + rem % 8;
       const double s = col < r ? fscale[col] : 0.0;
-      __align__(16) int8_t d0[16], d1[16], d2[16];
+      __align__(16) int8_t d[4][16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) digits3((double)tileF[kc * 16 + k][col] * s, d0[k], d1[k], d2[k]);
+      for (int k = 0; k < 16; ++k) {
+        const Dig4 q = digits4((double)tileF[kc * 16 + k][col] * s);
+#pragma unroll
+        for (int pl = 0; pl < 4; ++pl) d[pl][k] = q.d[pl];
+      }
       const int64_t idx = kt * chunks + w;
-      p0[idx] = *reinterpret_cast<uint4*>(d0);
-      p1[idx] = *reinterpret_cast<uint4*>(d1);
-      p2[idx] = *reinterpret_cast<uint4*>(d2);
+      p0[idx] = *reinterpret_cast<uint4*>(d[0]);
+      p1[idx] = *reinterpret_cast<uint4*>(d[1]);
+      p2[idx] = *reinterpret_cast<uint4*>(d[2]);
+      p3[idx] = *reinterpret_cast<uint4*>(d[3]);
     }
     __syncthreads();
   }
@@ -420,12 +450,19 @@ __global__ void colmax_kernel(const float* __restrict__ F, int64_t ldf, int64_t 
   for (int k = threadIdx.x; k < r; k += blockDim.x) atomicMax(&maxbits[k], m[k]);
 }
 
-// fscale[k] = 127 / max|F_k| ; colscale[k] = 1 / (sx * fscale[k]).
+// Power of two s with mx * s in [32, 64) (1 for mx = 0).
+__host__ __device__ inline double pow2_scale(double mx) {
+  if (!(mx > 0.0)) return 1.0;
+  int e = 0;
+  frexp(mx, &e);                      // mx in [2^(e-1), 2^e)
+  return ldexp(1.0, 6 - e);           // mx * s in [2^5, 2^6)
+}
+
+// fscale[k] = power of two with max|F_k| fscale in [32, 64); colscale[k] = 1/(sx fscale[k]).
 __global__ void scales_kernel(const unsigned* maxbits, int r, double sx, double* fscale,
                               double* colscale) {
   for (int k = threadIdx.x; k < r; k += blockDim.x) {
-    const double mx = (double)__uint_as_float(maxbits[k]);
-    const double s = mx > 0.0 ? 127.0 / mx : 1.0;
+    const double s = pow2_scale((double)__uint_as_float(maxbits[k]));
     fscale[k] = s;
     colscale[k] = 1.0 / (sx * s);
   }
@@ -456,8 +493,8 @@ struct TcState {
   int64_t tiles_per_row = 0;   // 64-column tiles per band (even: 128-column pairs)
   int64_t Kt2 = 0;             // 64-row K stages of pass 2 (= 2 Mt)
   double sx = 1.0;
-  int8_t* xp[PLANES] = {nullptr, nullptr, nullptr};
-  int8_t* fp[PLANES] = {nullptr, nullptr, nullptr};
+  int8_t* xp[PLANES] = {nullptr, nullptr, nullptr, nullptr};
+  int8_t* fp[PLANES] = {nullptr, nullptr, nullptr, nullptr};
   unsigned* maxbits = nullptr; // r + 1
   double* fscale = nullptr;    // r
   double* colscale = nullptr;  // r
@@ -529,7 +566,7 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
     tc_destroy(s);
     return e == cudaErrorMemoryAllocation ? 2 : 1;
   }
-  // X scale: max X * sx = 126 (X >= 0, so the leading digit stays in [0, 126])
+  // X scale: power of two with max X * sx in [32, 64)
   cudaMemsetAsync(s->maxbits, 0, sizeof(unsigned), st);
   maxabs_x_kernel<<<4 * s->sms, 256, 0, st>>>(X, ldx, rows, n, s->maxbits);
   unsigned mb = 0;
@@ -540,9 +577,10 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   }
   float mx;
   memcpy(&mx, &mb, sizeof(mx));
-  s->sx = mx > 0.0f ? 126.0 / (double)mx : 1.0;
+  s->sx = pow2_scale((double)mx);
   pack_x_kernel<<<8 * s->sms, 256, 0, st>>>(X, ldx, rows, n, s->sx, s->tiles_per_row, s->Mt,
-                                            (uint4*)s->xp[0], (uint4*)s->xp[1], (uint4*)s->xp[2]);
+                                            (uint4*)s->xp[0], (uint4*)s->xp[1], (uint4*)s->xp[2],
+                                            (uint4*)s->xp[3]);
   count_launch(2);
   if (cudaGetLastError() != cudaSuccess) {
     tc_destroy(s);
@@ -559,7 +597,8 @@ static void pack_factor(TcState* s, const float* F, int64_t ldf, int64_t K, int6
   colmax_kernel<<<2 * s->sms, 256, 0, st>>>(F, ldf, K, r, s->maxbits);
   scales_kernel<<<1, 128, 0, st>>>(s->maxbits, r, s->sx, s->fscale, s->colscale);
   pack_factor_kernel<<<(int)std::min<int64_t>(Kt, 8 * s->sms), 256, 0, st>>>(
-      F, ldf, K, r, s->rp, s->fscale, Kt, (uint4*)s->fp[0], (uint4*)s->fp[1], (uint4*)s->fp[2]);
+      F, ldf, K, r, s->rp, s->fscale, Kt, (uint4*)s->fp[0], (uint4*)s->fp[1], (uint4*)s->fp[2],
+      (uint4*)s->fp[3]);
   count_launch(3);
 }
 
