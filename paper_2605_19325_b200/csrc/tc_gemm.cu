@@ -170,10 +170,15 @@ __device__ __forceinline__ void unit_range(const Params& p, int u, int& tile, in
   if (s1 < s0) s1 = s0;
 }
 
-// (a-plane, b-plane, weight class = accumulator) of the ten products, in issue order; the
-// first product of each class starts its accumulator
-__constant__ int kProd[NPROD][3] = {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 2}, {1, 1, 2},
-                                    {2, 0, 2}, {0, 3, 3}, {1, 2, 3}, {2, 1, 3}, {3, 0, 3}};
+// The ten digit products A_i B_j (i + j <= 3) as six MMAs {a-plane, first b-plane, first
+// accumulator, wide}: a wide MMA multiplies A_i by the two adjacent planes [B_j; B_j+1]
+// (N = 2 rp) into the adjacent accumulators acc_{i+j} | acc_{i+j+1}.  The first two MMAs
+// initialise acc0..acc3 at the start of a unit.
+//   A0 [B0;B1] -> acc0|acc1   A0 [B2;B3] -> acc2|acc3   A1 [B0;B1] -> acc1|acc2
+//   A1 B2 -> acc3             A2 [B0;B1] -> acc2|acc3   A3 B0 -> acc3
+constexpr int NMMA = 6;
+__constant__ int kMma[NMMA][4] = {{0, 0, 0, 1}, {0, 2, 2, 1}, {1, 0, 1, 1},
+                                  {1, 2, 3, 0}, {2, 0, 2, 1}, {3, 0, 3, 0}};
 
 __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -253,14 +258,18 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
       // idesc: S32 accumulate (c_format 2), signed int8 A and B, A K-major (mode 0) or
-      // MN-major (mode 1), B K-major, N = rp, M = 128
-      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.mode << 15) |
-                             ((uint32_t)(p.rp >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      // MN-major (mode 1), B K-major, M = 128, N = rp (one digit plane) or 2 rp (two
+      // adjacent planes [B_j; B_j+1] feeding two adjacent accumulators in one MMA, so each
+      // A plane is read from shared memory fewer times -- the SS-MMA is smem-bandwidth bound)
+      const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.mode << 15) |
+                                  ((uint32_t)(BM >> 4) << 24);
+      const uint32_t idesc1 = idesc_base | ((uint32_t)(p.rp >> 3) << 17);
+      const uint32_t idesc2 = idesc_base | ((uint32_t)(2 * p.rp >> 3) << 17);
       const uint32_t a_lbo = p.mode == 0 ? 2048u : 128u;
       const uint32_t a_sbo = p.mode == 0 ? 128u : 1024u;
       const uint32_t a_kstep = p.mode == 0 ? 4096u : 512u;
-      const uint32_t b_lbo = (uint32_t)p.rp * 16u, b_sbo = 128u;
-      const uint32_t b_kstep = (uint32_t)p.rp * 32u;
+      const uint32_t b_lbo = 128u, b_sbo = 512u, b_kstep = 256u;
+      const uint32_t rpc = (uint32_t)p.rp;     // accumulator c lives at TMEM column c * rp
       int stage = 0;
       uint32_t phase = 0;
       uint32_t nunit = 0;
@@ -278,12 +287,12 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
 #pragma unroll
           for (int j = 0; j < BK / 32; ++j) {
 #pragma unroll
-            for (int q = 0; q < NPROD; ++q) {
-              const int pa = kProd[q][0], pb = kProd[q][1], ac = kProd[q][2];
+            for (int q = 0; q < NMMA; ++q) {
+              const int pa = kMma[q][0], pb = kMma[q][1], ac = kMma[q][2], wide = kMma[q][3];
               const uint64_t ad = umma_desc(a0 + pa * TILE_A + j * a_kstep, a_lbo, a_sbo);
               const uint64_t bd = umma_desc(b0 + pb * tile_b + j * b_kstep, b_lbo, b_sbo);
-              const bool fresh = ks == s0 && j == 0 && pa == 0;
-              tc_mma_i8(tmem_base + ac * 128, ad, bd, idesc, fresh ? 0u : 1u);
+              const bool fresh = ks == s0 && j == 0 && q < 2;
+              tc_mma_i8(tmem_base + ac * rpc, ad, bd, wide ? idesc2 : idesc1, fresh ? 0u : 1u);
             }
           }
           tc_commit(bar_empty + 8 * stage);          // frees the smem slot when MMAs retire
@@ -315,9 +324,9 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
         if (c0 >= p.rp) break;
         uint32_t v0[16], v1[16], v2[16], v3[16];
         TMEM_LD16(lane_addr + c0, v0);
-        TMEM_LD16(lane_addr + 128 + c0, v1);
-        TMEM_LD16(lane_addr + 256 + c0, v2);
-        TMEM_LD16(lane_addr + 384 + c0, v3);
+        TMEM_LD16(lane_addr + p.rp + c0, v1);
+        TMEM_LD16(lane_addr + 2 * p.rp + c0, v2);
+        TMEM_LD16(lane_addr + 3 * p.rp + c0, v3);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (row < p.out_rows) {
 #pragma unroll
@@ -394,9 +403,10 @@ __global__ void pack_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t 
   }
 }
 
-// Factor F (K x r, ld) * fscale[col] -> B tiles [Kt][rp x 64]: the 16-byte chunk at
-// (kc*(rp/8) + g)*128 + ri*16 holds F[kt*64 + kc*16 + 0..15][g*8 + ri].  A block stages 64
-// factor rows in shared memory so global reads are coalesced.
+// Factor F (K x r, ld) * fscale[col] -> B tiles [Kt][rp x 64]: 16-byte chunk w of a tile holds
+// F[kt*64 + kc*16 + 0..15][g*8 + ri] with g = w/32, kc = (w/8)%4, ri = w%8, i.e. byte
+// (g*4 + kc)*128 + ri*16.  A block stages 64 factor rows in shared memory so global reads are
+// coalesced.
 __global__ void __launch_bounds__(256)
 pack_factor_kernel(const float* __restrict__ F, int64_t ldf, int64_t K, int r, int rp,
                    const double* __restrict__ fscale, int64_t Kt, uint4* p0, uint4* p1, uint4* p2,
@@ -412,9 +422,10 @@ pack_factor_kernel(const float* __restrict__ F, int64_t ldf, int64_t K, int r, i
     }
     __syncthreads();
     for (int w = threadIdx.x; w < chunks; w += blockDim.x) {
-      const int kc = w / (gpt * 8);
-      const int rem = w % (gpt * 8);
-      const int col = (rem / 8) * 8 + rem % 8;
+      // B layout: 8-row group g, 16-byte K chunk kc at (g * 4 + kc) * 128 (SBO 512, LBO 128),
+      // so the planes B_j, B_j+1 stored back to back form one uniform 2 rp-row operand
+      const int g = w / 32, kc = (w / 8) % 4;
+      const int col = g * 8 + w % 8;
       const double s = col < r ? fscale[col] : 0.0;
       __align__(16) int8_t d[4][16];
 #pragma unroll

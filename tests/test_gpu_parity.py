@@ -72,8 +72,12 @@ def test_one_hals_sweep(cfg, prec):
 @pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
 @pytest.mark.parametrize("cfg", CASES[:4] + [CASES[6]], ids=IDS[:4] + [IDS[6]])
 def test_hals_trajectory_50_sweeps(cfg, prec):
-    """50 HALS sweeps from a shared feasible point: trace-form f within 1e-4 of the oracle's
-    direct f at every sweep, final factors within 1e-4."""
+    """50 HALS sweeps from a shared feasible point: final factors within 1e-4, the direct
+    objective within 1e-4, and the per-sweep trace-form f within 1e-4 of the oracle's direct f
+    -- or, on the tensor-core path, within its conditioning bound: the trace form
+    ||X||^2 - 2<X^T U, V> + <U^T U, V^T V> turns the ~1e-9 relative error of X^T U into a
+    (||X||^2 / f) * 2e-9 error of f (SURVEY Hard part 2), which exceeds 1e-4 on these small
+    near-exact planted shapes (not at C5 scale, where entry errors average over 6e6 terms)."""
     h, X, _ = make(cfg, precision=prec)
     U0, V0, _, _ = rotated_point(X, cfg.r)
     U0, V0 = np.abs(U0), np.abs(V0)
@@ -82,8 +86,11 @@ def test_hals_trajectory_50_sweeps(cfg, prec):
     f_gpu, info = h.iterate(U, V, 50)
     Uo, Vo, f_or = oracle_sweeps(X, U0, V0, oracle.SweepState(stage=1), 50, cfg.r)
     err = np.abs(f_gpu - f_or) / f_or
-    print(f"{cfg.name} prec={h.precision}: max f err {err.max():.2e}")
-    assert err.max() < 1e-4, err
+    cond = oracle.xnorm2(X) / f_or
+    bound = np.maximum(1e-4, 2e-9 * cond) if prec == TC else 1e-4
+    print(f"{cfg.name} prec={h.precision}: max f err {err.max():.2e} (max ||X||^2/f "
+          f"{cond.max():.1e})")
+    assert np.all(err < bound), err
     assert abs(h.objective(U, V, exact=True) - f_or[-1]) / f_or[-1] < 1e-4
     assert rel_fro(to_np(U), Uo) < 1e-4 and rel_fro(to_np(V), Vo) < 1e-4
 
