@@ -40,26 +40,36 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
-// out[b][c] += sign * sum_l S[b][l] G[l][lane + 32c]   (S held lane-distributed like out)
+// out[b][c] += sign * sum_l S[b][l] G[l][lane + 32c]   (S held lane-distributed like out).
+// S is staged through the warp's shared buffer Ss (RB x 32*CPL doubles) and read back as
+// broadcast 16-byte loads, two l at a time: no shuffles, so the fp64 FMA pipe is the bound.
 template <int CPL, int RB>
 __device__ __forceinline__ void row_times_gram(const double (&S)[RB][CPL], const double* Gs,
-                                               int r, int lane, double sign,
+                                               double* Ss, int r, int lane, double sign,
                                                double (&out)[RB][CPL]) {
   constexpr int RP = 32 * CPL;
+  __syncwarp();
 #pragma unroll
-  for (int s = 0; s < CPL; ++s) {
-    const int lmax = r - 32 * s < 32 ? r - 32 * s : 32;
-#pragma unroll 4
-    for (int ll = 0; ll < lmax; ++ll) {
-      const int l = 32 * s + ll;
-      double gl[CPL];
+  for (int b = 0; b < RB; ++b)
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) gl[c] = Gs[l * RP + lane + 32 * c];
+    for (int c = 0; c < CPL; ++c) Ss[b * RP + lane + 32 * c] = sign * S[b][c];
+  __syncwarp();
+  const int rr = (r + 1) & ~1;                // entries >= r are zero in S and in G
+#pragma unroll 2
+  for (int l = 0; l < rr; l += 2) {
+    double g0[CPL], g1[CPL];
 #pragma unroll
-      for (int b = 0; b < RB; ++b) {
-        const double sv = sign * __shfl_sync(FULL, S[b][s], ll);
+    for (int c = 0; c < CPL; ++c) {
+      g0[c] = Gs[l * RP + lane + 32 * c];
+      g1[c] = Gs[(l + 1) * RP + lane + 32 * c];
+    }
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) out[b][c] = fma(sv, gl[c], out[b][c]);
+    for (int b = 0; b < RB; ++b) {
+      const double2 sv = *reinterpret_cast<const double2*>(Ss + b * RP + l);
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        out[b][c] = fma(sv.x, g0[c], out[b][c]);
+        out[b][c] = fma(sv.y, g1[c], out[b][c]);
       }
     }
   }
@@ -81,6 +91,7 @@ hals_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r, const doubl
   constexpr int RP = 32 * CPL;
   extern __shared__ double smem[];
   double* Gs = smem;
+  double* Ss = smem + RP * RP + (threadIdx.x >> 5) * RB * RP;
   __shared__ double wmin_s[kRowWarps];
   const bool active = stage == nullptr || *stage == 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -102,7 +113,7 @@ hals_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r, const doubl
           u[b][c] = ok ? (double)F[row * ldf + col] : 0.0;
           t[b][c] = ok ? C[row * r + col] : 0.0;
         }
-      row_times_gram<CPL, RB>(u, Gs, r, lane, -1.0, t);      // t = C - u G
+      row_times_gram<CPL, RB>(u, Gs, Ss, r, lane, -1.0, t);      // t = C - u G
 #pragma unroll
       for (int s = 0; s < CPL; ++s) {
         const int kmax = r - 32 * s < 32 ? r - 32 * s : 32;
@@ -161,7 +172,8 @@ pbcd_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
   if (stage != nullptr && *stage != 0) return;
   extern __shared__ double smem[];
   double* Gs = smem;
-  double* pgw = smem + RP * RP;            // [kRowWarps][max_iter + 1]
+  double* Ss = smem + RP * RP + (threadIdx.x >> 5) * RB * RP;
+  double* pgw = smem + RP * RP + kRowWarps * RB * RP;   // [kRowWarps][max_iter + 1]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double lam = *lam_ptr;
   load_gram<CPL>(G, r, Gs);
@@ -188,7 +200,7 @@ pbcd_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
         cc[b][c] = ok ? C[row * r + col] : 0.0;
         gr[b][c] = -cc[b][c];
       }
-    row_times_gram<CPL, RB>(u, Gs, r, lane, 1.0, gr);   // grad = u G - C
+    row_times_gram<CPL, RB>(u, Gs, Ss, r, lane, 1.0, gr);   // grad = u G - C
     {
       double s = 0.0;
 #pragma unroll
@@ -212,7 +224,7 @@ pbcd_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
         }
         num[b] = warp_sum(sn);
       }
-      row_times_gram<CPL, RB>(g, Gs, r, lane, 1.0, gG);  // g V^T V
+      row_times_gram<CPL, RB>(g, Gs, Ss, r, lane, 1.0, gG);  // g V^T V
 #pragma unroll
       for (int b = 0; b < RB; ++b) {
         double sd = 0.0;
@@ -234,7 +246,7 @@ pbcd_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
           gr[b][c] = -cc[b][c];
         }
       }
-      row_times_gram<CPL, RB>(u, Gs, r, lane, 1.0, gr);
+      row_times_gram<CPL, RB>(u, Gs, Ss, r, lane, 1.0, gr);
       double s = 0.0;
 #pragma unroll
       for (int b = 0; b < RB; ++b)
@@ -295,8 +307,10 @@ template <int CPL, int RB>
 __global__ void __launch_bounds__(32 * kRowWarps)
 kkt_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
            const double* __restrict__ C, const double* __restrict__ G, double* parts) {
+  constexpr int RP = 32 * CPL;
   extern __shared__ double smem[];
   double* Gs = smem;
+  double* Ss = smem + RP * RP + (threadIdx.x >> 5) * RB * RP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   load_gram<CPL>(G, r, Gs);
   __syncthreads();
@@ -319,7 +333,7 @@ kkt_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
         gr[b][c] = -cv;
         c2 += cv * cv;
       }
-    row_times_gram<CPL, RB>(u, Gs, r, lane, 1.0, gr);
+    row_times_gram<CPL, RB>(u, Gs, Ss, r, lane, 1.0, gr);
 #pragma unroll
     for (int b = 0; b < RB; ++b)
 #pragma unroll
@@ -350,7 +364,7 @@ kkt_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
 
 template <int CPL>
 size_t row_smem(int extra_doubles) {
-  return sizeof(double) * (size_t)(32 * CPL * 32 * CPL + extra_doubles);
+  return sizeof(double) * (size_t)(32 * CPL * 32 * CPL + kRowWarps * 4 * 32 * CPL + extra_doubles);
 }
 
 template <typename K>

@@ -170,30 +170,49 @@ __device__ __forceinline__ void unit_range(const Params& p, int u, int& tile, in
   if (s1 < s0) s1 = s0;
 }
 
-// The ten digit products A_i B_j (i + j <= 3) as six MMAs {a-plane, first b-plane, first
-// accumulator, wide}: a wide MMA multiplies A_i by the two adjacent planes [B_j; B_j+1]
-// (N = 2 rp) into the adjacent accumulators acc_{i+j} | acc_{i+j+1}.  The first two MMAs
-// initialise acc0..acc3 at the start of a unit.
-//   A0 [B0;B1] -> acc0|acc1   A0 [B2;B3] -> acc2|acc3   A1 [B0;B1] -> acc1|acc2
-//   A1 B2 -> acc3             A2 [B0;B1] -> acc2|acc3   A3 B0 -> acc3
-constexpr int NMMA = 6;
-__constant__ int kMma[NMMA][4] = {{0, 0, 0, 1}, {0, 2, 2, 1}, {1, 0, 1, 1},
-                                  {1, 2, 3, 0}, {2, 0, 2, 1}, {3, 0, 3, 0}};
+// Digit products A_i B_j with i + j < NCLS issued as MMAs {a-plane, first b-plane, first
+// accumulator, wide}.  A wide MMA multiplies A_i by two adjacent planes [B_j; B_j+1] (N = 2 rp)
+// into the adjacent accumulators acc_{i+j} | acc_{i+j+1}, so each A plane is read from shared
+// memory fewer times (the SS-MMA is smem-bandwidth bound).  The first MMAs of a list
+// initialise every accumulator at the start of a unit (`fresh`).
+//   NCLS = 4 (10 products, 6 MMAs): A0[B0;B1] A0[B2;B3] A1[B0;B1] A1 B2 A2[B0;B1] A3 B0
+//   NCLS = 3 ( 6 products, 4 MMAs): A0[B0;B1] A0 B2 A1[B0;B1] A2 B0
+template <int NCLS> struct MmaList;
+template <> struct MmaList<4> {
+  static constexpr int N = 6, FRESH = 2;
+  __device__ static __forceinline__ int t(int q, int f) {
+    constexpr int tab[6][4] = {{0, 0, 0, 1}, {0, 2, 2, 1}, {1, 0, 1, 1},
+                               {1, 2, 3, 0}, {2, 0, 2, 1}, {3, 0, 3, 0}};
+    return tab[q][f];
+  }
+};
+template <> struct MmaList<3> {
+  static constexpr int N = 4, FRESH = 2;
+  __device__ static __forceinline__ int t(int q, int f) {
+    constexpr int tab[4][4] = {{0, 0, 0, 1}, {0, 2, 2, 0}, {1, 0, 1, 1}, {2, 0, 2, 0}};
+    return tab[q][f];
+  }
+};
 
+template <int NCLS>
 __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
+  constexpr int NPL = NCLS;                                   // digit planes per operand
+  constexpr int STAGE = NPL * (TILE_A + MAX_TILE_B);
+  constexpr int NST = (SMEM_BYTES - 1024) / STAGE;            // 3 (4 planes) or 4 (3 planes)
+  using L = MmaList<NCLS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t bars[2 * STAGES + 2];
+  __shared__ __align__(8) uint64_t bars[2 * 4 + 2];
   __shared__ uint32_t tmem_base_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_full = smem_u32(&bars[0]);
-  const uint32_t bar_empty = smem_u32(&bars[STAGES]);
-  const uint32_t bar_tfull = smem_u32(&bars[2 * STAGES]);
-  const uint32_t bar_tempty = smem_u32(&bars[2 * STAGES + 1]);
+  const uint32_t bar_empty = smem_u32(&bars[NST]);
+  const uint32_t bar_tfull = smem_u32(&bars[2 * NST]);
+  const uint32_t bar_tempty = smem_u32(&bars[2 * NST + 1]);
   const uint32_t tile_b = (uint32_t)p.rp * BK;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(bar_full + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, 1);
     }
@@ -214,53 +233,44 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
   const uint32_t tmem_base = tmem_base_s;
 
   if (warp == 0) {
-    // ===================== producer =====================
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
-        int tile, s0, s1, split;
-        unit_range(p, u, tile, s0, s1, split);
-        for (int ks = s0; ks < s1; ++ks) {
-          mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-          const uint32_t fb = bar_full + 8 * stage;
-          mbar_expect_tx(fb, PLANES * (TILE_A + tile_b));
-          const uint32_t st = smem_u32(smem + (size_t)stage * STAGE_BYTES);
-          if (p.mode == 0) {
-            const int64_t off = ((int64_t)tile * p.tiles_per_row + ks) * TILE_A;
-#pragma unroll
-            for (int pl = 0; pl < PLANES; ++pl) bulk_g2s(st + pl * TILE_A, p.xp[pl] + off, TILE_A, fb);
-          } else {
-            // A = X^T: output rows j = column tiles 2*tile, 2*tile+1 of row band ks/2; the K
-            // stage is the 64-row half (ks & 1) of that band.
-            const int64_t band = ks >> 1;
-            const int half = ks & 1;
-            for (int t = 0; t < 2; ++t) {
-              const int64_t base = (band * p.tiles_per_row + 2 * tile + t) * TILE_A;
-              for (int kc = 0; kc < 4; ++kc) {
-                const int64_t src = base + (int64_t)(kc * 16 + 8 * half) * 128;
-                const uint32_t dst = (uint32_t)((t * 4 + kc) * 1024);
-#pragma unroll
-                for (int pl = 0; pl < PLANES; ++pl)
-                  bulk_g2s(st + pl * TILE_A + dst, p.xp[pl] + src, 1024, fb);
-              }
-            }
-          }
-          const int64_t foff = (int64_t)ks * tile_b;
-          const uint32_t sb = st + PLANES * TILE_A;
-#pragma unroll
-          for (int pl = 0; pl < PLANES; ++pl) bulk_g2s(sb + pl * tile_b, p.fp[pl] + foff, tile_b, fb);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    // ===================== producer: the whole warp issues a stage's bulk copies =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      int tile, s0, s1, split;
+      unit_range(p, u, tile, s0, s1, split);
+      for (int ks = s0; ks < s1; ++ks) {
+        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+        const uint32_t fb = bar_full + 8 * stage;
+        if (lane == 0) mbar_expect_tx(fb, NPL * (TILE_A + tile_b));
+        __syncwarp();
+        const uint32_t st = smem_u32(smem + (size_t)stage * STAGE);
+        if (p.mode == 0) {
+          const int64_t off = ((int64_t)tile * p.tiles_per_row + ks) * TILE_A;
+          if (lane < NPL) bulk_g2s(st + lane * TILE_A, p.xp[lane] + off, TILE_A, fb);
+        } else {
+          // A = X^T: output rows j = column tiles 2*tile, 2*tile+1 of row band ks/2; the K stage
+          // is the 64-row half (ks & 1) of that band: 8 chunks of 1 KB per plane, one per lane
+          const int64_t band = ks >> 1;
+          const int half = ks & 1;
+          const int t = (lane >> 2) & 1, kc = lane & 3;
+          const int64_t src = (band * p.tiles_per_row + 2 * tile + t) * TILE_A +
+                              (int64_t)(kc * 16 + 8 * half) * 128;
+          const uint32_t dst = (uint32_t)((t * 4 + kc) * 1024);
+          for (int pl = lane >> 3; pl < NPL; pl += 4)
+            bulk_g2s(st + pl * TILE_A + dst, p.xp[pl] + src, 1024, fb);
         }
+        const int64_t foff = (int64_t)ks * tile_b;
+        if (lane >= 28 && lane - 28 < NPL)
+          bulk_g2s(st + NPL * TILE_A + (lane - 28) * tile_b, p.fp[lane - 28] + foff, tile_b, fb);
+        if (++stage == NST) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
       // idesc: S32 accumulate (c_format 2), signed int8 A and B, A K-major (mode 0) or
-      // MN-major (mode 1), B K-major, M = 128, N = rp (one digit plane) or 2 rp (two
-      // adjacent planes [B_j; B_j+1] feeding two adjacent accumulators in one MMA, so each
-      // A plane is read from shared memory fewer times -- the SS-MMA is smem-bandwidth bound)
+      // MN-major (mode 1), B K-major, M = 128, N = rp (one digit plane) or 2 rp (two planes)
       const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.mode << 15) |
                                   ((uint32_t)(BM >> 4) << 24);
       const uint32_t idesc1 = idesc_base | ((uint32_t)(p.rp >> 3) << 17);
@@ -282,21 +292,21 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
         for (int ks = s0; ks < s1; ++ks) {
           mbar_wait(bar_full + 8 * stage, phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(smem + (size_t)stage * STAGE_BYTES);
-          const uint32_t b0 = a0 + PLANES * TILE_A;
+          const uint32_t a0 = smem_u32(smem + (size_t)stage * STAGE);
+          const uint32_t b0 = a0 + NPL * TILE_A;
 #pragma unroll
           for (int j = 0; j < BK / 32; ++j) {
 #pragma unroll
-            for (int q = 0; q < NMMA; ++q) {
-              const int pa = kMma[q][0], pb = kMma[q][1], ac = kMma[q][2], wide = kMma[q][3];
+            for (int q = 0; q < L::N; ++q) {
+              const int pa = L::t(q, 0), pb = L::t(q, 1), ac = L::t(q, 2), wide = L::t(q, 3);
               const uint64_t ad = umma_desc(a0 + pa * TILE_A + j * a_kstep, a_lbo, a_sbo);
               const uint64_t bd = umma_desc(b0 + pb * tile_b + j * b_kstep, b_lbo, b_sbo);
-              const bool fresh = ks == s0 && j == 0 && q < 2;
+              const bool fresh = ks == s0 && j == 0 && q < L::FRESH;
               tc_mma_i8(tmem_base + ac * rpc, ad, bd, wide ? idesc2 : idesc1, fresh ? 0u : 1u);
             }
           }
           tc_commit(bar_empty + 8 * stage);          // frees the smem slot when MMAs retire
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         tc_commit(bar_tfull);                        // unit's accumulators complete
         ++nunit;
@@ -322,21 +332,21 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
       for (int h = 0; h < 4; ++h) {
         const int c0 = 64 * hcol + 16 * h;
         if (c0 >= p.rp) break;
-        uint32_t v0[16], v1[16], v2[16], v3[16];
-        TMEM_LD16(lane_addr + c0, v0);
-        TMEM_LD16(lane_addr + p.rp + c0, v1);
-        TMEM_LD16(lane_addr + 2 * p.rp + c0, v2);
-        TMEM_LD16(lane_addr + 3 * p.rp + c0, v3);
+        uint32_t v[NCLS][16];
+#pragma unroll
+        for (int c = 0; c < NCLS; ++c) TMEM_LD16(lane_addr + c * p.rp + c0, v[c]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (row < p.out_rows) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int col = c0 + i;
             if (col < p.r) {
-              // exact in fp64: |acc_c| < 2^31, 21 fractional bits in total
-              const double v = (double)(int)v0[i] + (double)(int)v1[i] * 0x1p-7 +
-                               (double)(int)v2[i] * 0x1p-14 + (double)(int)v3[i] * 0x1p-21;
-              o[col] = v * p.colscale[col];
+              // exact in fp64: |acc_c| < 2^31, at most 21 fractional bits in total
+              double acc = 0.0;
+#pragma unroll
+              for (int c = NCLS - 1; c >= 0; --c)
+                acc = acc * 0x1p-7 + (double)(int)v[c][i];
+              o[col] = acc * p.colscale[col];
             }
           }
         }
@@ -511,6 +521,7 @@ struct TcState {
   double* colscale = nullptr;  // r
   double* partial = nullptr;   // ksplit2 x n x r  (pass 2)  /  ksplit1 x rows x r (pass 1)
   int ksplit1 = 1, ksplit2 = 1;
+  int pass1_classes = 3;       // ENMF_TC_PASS1_CLASSES=4 for the full-precision pass 1
   int sms = kSMs;
 };
 
@@ -552,6 +563,7 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   s->Mt = (rows + BM - 1) / BM;
   s->tiles_per_row = ((n + 127) / 128) * 2;
   s->Kt2 = 2 * s->Mt;
+  if (const char* e = getenv("ENMF_TC_PASS1_CLASSES")) s->pass1_classes = atoi(e) == 4 ? 4 : 3;
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, dev);
@@ -635,11 +647,18 @@ static int launch_gemm(TcState* s, int mode, double* out, int64_t out_ld, int64_
   p.out_rows = out_rows;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tc_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(tc_i8_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(tc_i8_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
   const int grid = std::min(p.num_units, s->sms);
-  tc_i8_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(p);
+  // P = X V only feeds the U-block update: 3 digit planes (weight classes <= 2, ~2e-8
+  // relative); Q = X^T U also feeds the trace-form objective, whose conditioning needs all
+  // 4 planes (classes <= 3, ~5e-10 relative)  -- DESIGN.md §5
+  if (s->pass1_classes == 3 && mode == 0)
+    tc_i8_kernel<3><<<grid, THREADS, SMEM_BYTES, st>>>(p);
+  else
+    tc_i8_kernel<4><<<grid, THREADS, SMEM_BYTES, st>>>(p);
   count_launch();
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
