@@ -59,12 +59,14 @@ constexpr int64_t MAX_UNIT_K = 65536;           // |acc3| <= 4 * 64 * 64 * K < 2
 
 struct Params {
   const int8_t* xp[PLANES];
+  const int8_t* xtp[PLANES];   // transposed packed copy (mode 2), may be null
   const int8_t* fp[PLANES];
+  int64_t tiles_per_row_t;     // transposed copy: 64-row K tiles per 128-column band
   double* out;
   int64_t out_ld;
   int64_t split_stride;
   const double* colscale;    // r values: 1 / (s_X * s_k)
-  int mode;                  // 0: P = X V ; 1: Q = X^T U
+  int mode;                  // 0: P = X V ; 1: Q = X^T U (MN-major gather) ; 2: Q from X^T copy
   int num_units;
   int ksplit;
   int stages_total;          // 64-deep K stages of the full contraction
@@ -248,6 +250,10 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
         if (p.mode == 0) {
           const int64_t off = ((int64_t)tile * p.tiles_per_row + ks) * TILE_A;
           if (lane < NPL) bulk_g2s(st + lane * TILE_A, p.xp[lane] + off, TILE_A, fb);
+        } else if (p.mode == 2) {
+          // A = X^T from the transposed packed copy: K-major tiles, one 8 KB copy per plane
+          const int64_t off = ((int64_t)tile * p.tiles_per_row_t + ks) * TILE_A;
+          if (lane < NPL) bulk_g2s(st + lane * TILE_A, p.xtp[lane] + off, TILE_A, fb);
         } else {
           // A = X^T: output rows j = column tiles 2*tile, 2*tile+1 of row band ks/2; the K stage
           // is the 64-row half (ks & 1) of that band: 8 chunks of 1 KB per plane, one per lane
@@ -271,13 +277,14 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
     if (lane == 0) {
       // idesc: S32 accumulate (c_format 2), signed int8 A and B, A K-major (mode 0) or
       // MN-major (mode 1), B K-major, M = 128, N = rp (one digit plane) or 2 rp (two planes)
-      const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)p.mode << 15) |
+      const bool mn = p.mode == 1;               // A MN-major (X^T gathered from the X copy)
+      const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)mn << 15) |
                                   ((uint32_t)(BM >> 4) << 24);
       const uint32_t idesc1 = idesc_base | ((uint32_t)(p.rp >> 3) << 17);
       const uint32_t idesc2 = idesc_base | ((uint32_t)(2 * p.rp >> 3) << 17);
-      const uint32_t a_lbo = p.mode == 0 ? 2048u : 128u;
-      const uint32_t a_sbo = p.mode == 0 ? 128u : 1024u;
-      const uint32_t a_kstep = p.mode == 0 ? 4096u : 512u;
+      const uint32_t a_lbo = !mn ? 2048u : 128u;
+      const uint32_t a_sbo = !mn ? 128u : 1024u;
+      const uint32_t a_kstep = !mn ? 4096u : 512u;
       const uint32_t b_lbo = 128u, b_sbo = 512u, b_kstep = 256u;
       const uint32_t rpc = (uint32_t)p.rp;     // accumulator c lives at TMEM column c * rp
       int stage = 0;
@@ -413,6 +420,41 @@ __global__ void pack_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t 
   }
 }
 
+// X^T copy: tiles [jt][it] of 128 columns (j, the M side of Q = X^T U) x 64 rows (i, the K
+// side), K-major core matrices (kc*16 + g)*128 like pass 1's tiles.  A block stages a 64 x 128
+// block of X in shared memory (coalesced reads) and writes 16-byte chunks of 16 rows.
+__global__ void __launch_bounds__(256)
+pack_xt_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n, double sx,
+               int64_t jtiles, int64_t itiles, uint4* p0, uint4* p1, uint4* p2, uint4* p3) {
+  __shared__ float tx[64][129];
+  for (int64_t t = blockIdx.x; t < jtiles * itiles; t += gridDim.x) {
+    const int64_t jt = t / itiles, it = t % itiles;
+    for (int e = threadIdx.x; e < 64 * 128; e += blockDim.x) {
+      const int il = e / 128, jl = e % 128;
+      const int64_t i = it * 64 + il, j = jt * 128 + jl;
+      tx[il][jl] = (i < rows && j < n) ? X[i * ldx + j] : 0.0f;
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < 512; w += blockDim.x) {
+      const int kc = w / 128, g = (w / 8) % 16, ri = w % 8;
+      const int jl = g * 8 + ri;
+      __align__(16) int8_t d[4][16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const Dig4 q = digits4((double)tx[kc * 16 + k][jl] * sx);
+#pragma unroll
+        for (int pl = 0; pl < 4; ++pl) d[pl][k] = q.d[pl];
+      }
+      const int64_t idx = (t * TILE_A) / 16 + w;
+      p0[idx] = *reinterpret_cast<uint4*>(d[0]);
+      p1[idx] = *reinterpret_cast<uint4*>(d[1]);
+      p2[idx] = *reinterpret_cast<uint4*>(d[2]);
+      p3[idx] = *reinterpret_cast<uint4*>(d[3]);
+    }
+    __syncthreads();
+  }
+}
+
 // Factor F (K x r, ld) * fscale[col] -> B tiles [Kt][rp x 64]: 16-byte chunk w of a tile holds
 // F[kt*64 + kc*16 + 0..15][g*8 + ri] with g = w/32, kc = (w/8)%4, ri = w%8, i.e. byte
 // (g*4 + kc)*128 + ri*16.  A block stages 64 factor rows in shared memory so global reads are
@@ -515,6 +557,7 @@ struct TcState {
   int64_t Kt2 = 0;             // 64-row K stages of pass 2 (= 2 Mt)
   double sx = 1.0;
   int8_t* xp[PLANES] = {nullptr, nullptr, nullptr, nullptr};
+  int8_t* xtp[PLANES] = {nullptr, nullptr, nullptr, nullptr};   // X^T copy (pass 2), optional
   int8_t* fp[PLANES] = {nullptr, nullptr, nullptr, nullptr};
   unsigned* maxbits = nullptr; // r + 1
   double* fscale = nullptr;    // r
@@ -533,6 +576,7 @@ void tc_destroy(TcState* s) {
   if (!s) return;
   for (int p = 0; p < PLANES; ++p) {
     if (s->xp[p]) cudaFree(s->xp[p]);
+    if (s->xtp[p]) cudaFree(s->xtp[p]);
     if (s->fp[p]) cudaFree(s->fp[p]);
   }
   void* bufs[] = {s->maxbits, s->fscale, s->colscale, s->partial};
@@ -563,6 +607,9 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   s->Mt = (rows + BM - 1) / BM;
   s->tiles_per_row = ((n + 127) / 128) * 2;
   s->Kt2 = 2 * s->Mt;
+  // Pass 1 drops the weight-3 digit products only when K = n is long enough that their
+  // unbiased truncation error (~2^-22 of |X||V| per term) averages below ~1e-9 of P
+  s->pass1_classes = n >= 8192 ? 3 : 4;
   if (const char* e = getenv("ENMF_TC_PASS1_CLASSES")) s->pass1_classes = atoi(e) == 4 ? 4 : 3;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -605,6 +652,32 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
                                             (uint4*)s->xp[0], (uint4*)s->xp[1], (uint4*)s->xp[2],
                                             (uint4*)s->xp[3]);
   count_launch(2);
+  // A second, transposed copy makes pass 2 a K-major stream of whole tiles like pass 1 (the
+  // MN-major gather of 1 KB pieces measured ~2x slower).  It costs another 4 bytes per element
+  // of HBM capacity and is skipped (ENMF_TC_XT=0, or not enough free memory) in favour of the
+  // gather path.
+  {
+    const char* ev = getenv("ENMF_TC_XT");
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const bool want = !(ev && atoi(ev) == 0) && free_b > PLANES * plane + ((size_t)8 << 30);
+    for (int p = 0; p < PLANES && want; ++p)
+      if (cudaMalloc(&s->xtp[p], plane) != cudaSuccess) {
+        cudaGetLastError();
+        for (int q = 0; q < PLANES; ++q) {
+          if (s->xtp[q]) cudaFree(s->xtp[q]);
+          s->xtp[q] = nullptr;
+        }
+        break;
+      }
+    if (s->xtp[0]) {
+      const int64_t jt = s->tiles_per_row / 2;
+      pack_xt_kernel<<<8 * s->sms, 256, 0, st>>>(X, ldx, rows, n, s->sx, jt, s->Kt2,
+                                                 (uint4*)s->xtp[0], (uint4*)s->xtp[1],
+                                                 (uint4*)s->xtp[2], (uint4*)s->xtp[3]);
+      count_launch();
+    }
+  }
   if (cudaGetLastError() != cudaSuccess) {
     tc_destroy(s);
     return 1;
@@ -631,8 +704,10 @@ static int launch_gemm(TcState* s, int mode, double* out, int64_t out_ld, int64_
   Params p;
   for (int q = 0; q < PLANES; ++q) {
     p.xp[q] = s->xp[q];
+    p.xtp[q] = s->xtp[q];
     p.fp[q] = s->fp[q];
   }
+  p.tiles_per_row_t = s->Kt2;
   p.out = out;
   p.out_ld = out_ld;
   p.split_stride = split_stride;
@@ -678,7 +753,8 @@ int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st) {
 int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st) {
   // B = U (K = rows of X), split-K partials reduced in a fixed order
   pack_factor(s, U, ldu, s->rows, s->Kt2, st);
-  if (launch_gemm(s, 1, s->partial, s->r, s->n * s->r, (int)(s->tiles_per_row / 2), s->ksplit2,
+  const int mode = s->xtp[0] ? 2 : 1;
+  if (launch_gemm(s, mode, s->partial, s->r, s->n * s->r, (int)(s->tiles_per_row / 2), s->ksplit2,
                   (int)s->Kt2, s->n, st))
     return 1;
   reduce_parts(s->partial, s->ksplit2, s->n * s->r, Q, st);
