@@ -311,7 +311,8 @@ def run_enmf(args):
             "metric": METRIC, "value": sweeps_per_s, "unit": "sweeps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64" if h.precision == "fp64-simt" else "f16x2-split/f32-tmem/f64",
+            "dtype": "f64" if h.precision == "fp64-simt"
+                     else "i8 (4x7-bit digits of fp32 X, V, U) / exact i32 TMEM / f64",
             "data": "synthetic",
             "config": {"workload": cfg.name, "m": m, "n": n, "r": r,
                        "global_batch": m, "seq_len": n,

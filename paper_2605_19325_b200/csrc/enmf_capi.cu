@@ -268,7 +268,7 @@ enmf_status_t enmf_nccl_unique_id(void* out128) {
 
 const char* enmf_precision_name(enmf_handle_t h) {
   if (!h) return "none";
-  return h->precision == ENMF_PREC_TC ? "tc-i8x3-exact" : "fp64-simt";
+  return h->precision == ENMF_PREC_TC ? "tc-i8x4-exact" : "fp64-simt";
 }
 
 enmf_status_t enmf_destroy(enmf_handle_t h) {
