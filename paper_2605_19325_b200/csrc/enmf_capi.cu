@@ -136,8 +136,14 @@ enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
   int* stage = h->dint + I_STAGE;
   const int mi = h->opt.pbcd_max_iter;
   if (maybe_ascent) {
-    pbcd_rows(F, ldf, rows, r, C, G, h->dscal + lam_slot, mi, h->snaps, h->parts, stage, h->st);
-    reduce_parts(h->parts, pbcd_parts(), mi + 1, h->pgsum, h->st);
+    if (h->tc_pbcd) {
+      tc_pbcd_rows(F, ldf, rows, r, C, G, h->dscal + lam_slot, mi, h->snaps, h->parts,
+                   reinterpret_cast<int8_t*>(h->tcpb_ws + 128), h->tcpb_ws, stage, h->st);
+      reduce_parts(h->parts, tc_pbcd_parts(), mi + 1, h->pgsum, h->st);
+    } else {
+      pbcd_rows(F, ldf, rows, r, C, G, h->dscal + lam_slot, mi, h->snaps, h->parts, stage, h->st);
+      reduce_parts(h->parts, pbcd_parts(), mi + 1, h->pgsum, h->st);
+    }
     if (sharded) ENMF_TRY(ar(h, h->pgsum, (size_t)(mi + 1), CommOp::Sum));
     pbcd_commit(F, ldf, rows, r, h->snaps, h->pgsum, h->opt.pbcd_eps, mi, h->dint + kstar_slot,
                 stage, h->minparts, h->st);
@@ -275,7 +281,8 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
   if (!h) return ENMF_ERR_INVALID_ARG;
   if (h->st) cudaStreamSynchronize(h->st);
   void* bufs[] = {h->dscal, h->dint, h->P, h->Q, h->GU, h->GV, h->work, h->parts,
-                  h->minparts, h->pgsum, h->snaps, h->ftrace, h->x_owned, h->W64};
+                  h->minparts, h->pgsum, h->snaps, h->ftrace, h->x_owned, h->W64,
+                  h->tcpb_ws};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->tc) tc_destroy(h->tc);
@@ -329,7 +336,7 @@ enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
       {(int64_t)8 << 20, 40 * l * l, 2 * (int64_t)512 * 512, 8 * r * r});
   ALLOC(h->work, h->work_elems);
   h->parts_elems = (size_t)std::max<int64_t>(
-      {(int64_t)pbcd_parts() * (o.pbcd_max_iter + 1), (int64_t)kkt_parts() * 8,
+      {(int64_t)std::max(pbcd_parts(), tc_pbcd_parts()) * (o.pbcd_max_iter + 1), (int64_t)kkt_parts() * 8,
        (int64_t)colabsmax_parts() * 3 * std::max<int64_t>(r, 1), 3 * 4 * kSMs, 4096});
   ALLOC(h->parts, h->parts_elems);
   ALLOC(h->minparts, (size_t)kRowGrid);
@@ -383,6 +390,9 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
     int rc = tc_create(&h->tc, X, ldx, h->m_loc, h->n, h->r, h->st);
     if (rc != 0) return rc == 2 ? ENMF_ERR_OOM : ENMF_ERR_CUDA;
   }
+  const char* tpe = getenv("ENMF_TC_PBCD");   // diagnostics: 0 keeps the SIMT fp64 PBCD
+  h->tc_pbcd = prec == ENMF_PREC_TC && tc_pbcd_supported((int)h->r) && !(tpe && tpe[0] == '0');
+  if (h->tc_pbcd && !h->tcpb_ws) ENMF_TRY(dalloc(&h->tcpb_ws, 128 + 4 * 128 * 128 / 8));
   h->precision = prec;
   int zero[I_COUNT] = {0};
   CUDA_TRY(cudaMemcpyAsync(h->dint, zero, sizeof(zero), cudaMemcpyHostToDevice, h->st));

@@ -51,6 +51,8 @@ struct enmf_handle_s {
   double* ftrace = nullptr;
   int ftrace_cap = 0;
   enmf::TcState* tc = nullptr;
+  double* tcpb_ws = nullptr;  // tensor-core PBCD: G digits (64 KB) + 128 column scales
+  bool tc_pbcd = false;       // ascent PBCD on the tensor cores (precision TC, r <= 128)
   float* x_owned = nullptr;  // device copy of X owned by enmf_solve_host
   double* W64 = nullptr;     // (m_loc + n) x r fp64 [U*; V*] kept from enmf_svd for enmf_rotate
   // profiling of the X passes (enmf_set_profiling): CUDA events around every contraction

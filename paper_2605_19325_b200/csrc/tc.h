@@ -1,10 +1,12 @@
 // tc.h -- tensor-core (tcgen05) contraction path for large X.
 //
-// X is repacked once (enmf_set_data) into a handle-owned copy of three balanced base-2^7 int8
-// digit planes (3 bytes per element), laid out in UMMA canonical tiles that bulk copies move
-// straight into shared memory.  The two X passes of a sweep run as tcgen05.mma kind::i8 with
-// exact int32 accumulation in TMEM (6 digit products into 3 weight classes), combined exactly
-// in fp64 by the epilogue.
+// X is repacked once (enmf_set_data) into a handle-owned copy of four balanced base-2^7 int8
+// digit planes (4 bytes per element, power-of-two row scales), laid out in UMMA canonical tiles
+// that bulk copies move straight into shared memory (plus a K-major copy of X^T for pass 2 when
+// memory allows).  The two X passes of a sweep run as tcgen05.mma kind::i8 with exact int32
+// accumulation in TMEM (digit products grouped into 3 or 4 weight classes), combined exactly in
+// fp64 by the epilogue.  The ascent stage's PBCD (Alg. 2) runs its two r x r products per
+// inner iteration the same way (tc_pbcd.cu).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,5 +24,14 @@ void tc_destroy(TcState* s);
 // P (rows x r fp64) = X V ; Q (n x r fp64) = X^T U  (this rank's rows only).
 int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st);
 int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st);
+
+// Alg. 2 PBCD on the tensor cores: same contract as pbcd_rows (kernels_rows.cu); pgparts holds
+// tc_pbcd_parts() x (max_iter + 1) partials; gd_work >= 4*128*128 bytes, gscale_work >= 128.
+bool tc_pbcd_supported(int r);
+int tc_pbcd_parts();
+void tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
+                  const double* G, const double* lam, int max_iter, float* snaps,
+                  double* pgparts, int8_t* gd_work, double* gscale_work, const int* stage,
+                  cudaStream_t st);
 
 }  // namespace enmf
