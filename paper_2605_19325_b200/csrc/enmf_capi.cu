@@ -146,7 +146,7 @@ enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
     }
     if (sharded) ENMF_TRY(ar(h, h->pgsum, (size_t)(mi + 1), CommOp::Sum));
     pbcd_commit(F, ldf, rows, r, h->snaps, h->pgsum, h->opt.pbcd_eps, mi, h->dint + kstar_slot,
-                stage, h->minparts, h->st);
+                stage, h->minparts, h->tc_pbcd, h->st);
   }
   hals_rows(F, ldf, rows, r, C, G, stage, h->minparts, h->st);
   reduce_min(h->minparts, kRowGrid, h->dscal + min_slot, h->st);

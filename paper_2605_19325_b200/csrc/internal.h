@@ -71,10 +71,11 @@ void pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C
                double* pgparts, const int* stage, cudaStream_t st);
 int pbcd_parts();
 // Selects k* from the partials (eps rule of Alg. 2), copies snapshot k* into F and
-// writes min partials; records k* into *kstar.
+// writes min partials; records k* into *kstar.  tiled: snapshots in tc_pbcd.cu's tile-major
+// layout (see pbcd_copy_tiled_kernel), else row-major rows x r.
 void pbcd_commit(float* F, int64_t ldf, int64_t rows, int r, const float* snaps,
                  const double* pgparts, double eps, int max_iter, int* kstar,
-                 const int* stage, double* minparts, cudaStream_t st);
+                 const int* stage, double* minparts, bool tiled, cudaStream_t st);
 // KKT partial statistics of one block (F, C = cross term, G): 8 values per warp slot.
 void kkt_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
               const double* G, double* parts, cudaStream_t st);

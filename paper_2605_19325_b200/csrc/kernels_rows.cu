@@ -276,6 +276,53 @@ __global__ void pbcd_select_kernel(const double* __restrict__ pgsum, int max_ite
   }
 }
 
+// Same as pbcd_copy_kernel for the tile-major snapshot layout of tc_pbcd.cu: element (i, j)
+// at (i / 128) * 128 * r + j * nt + i % 128, nt = min(128, rows - 128 * (i / 128)) the rows of
+// that tile (so a snapshot still spans exactly rows * r floats).  A (tile, 32-column chunk) unit is transposed
+// through shared memory so that both the snapshot reads and the F writes are coalesced.
+__global__ void pbcd_copy_tiled_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r,
+                                       const float* __restrict__ snaps,
+                                       const int* __restrict__ kstar, const int* stage,
+                                       double* minparts) {
+  __shared__ float t[128][33];
+  __shared__ double red[256];
+  const bool active = stage == nullptr || *stage == 0;
+  double mn = DBL_MAX;
+  if (active) {
+    const float* src = snaps + (int64_t)(*kstar - 1) * rows * r;
+    const int64_t tiles = (rows + 127) / 128;
+    const int chunks = (r + 31) / 32;
+    for (int64_t unit = blockIdx.x; unit < tiles * chunks; unit += gridDim.x) {
+      const int64_t tile = unit / chunks;
+      const int j0 = (int)(unit - tile * chunks) * 32;
+      const float* ts = src + tile * 128 * (int64_t)r;
+      const int nt = (int)(rows - tile * 128 < 128 ? rows - tile * 128 : 128);
+      __syncthreads();
+      for (int e = threadIdx.x; e < 32 * 128; e += blockDim.x) {
+        const int jl = e >> 7, il = e & 127;
+        if (j0 + jl < r && il < nt) t[il][jl] = ts[(int64_t)(j0 + jl) * nt + il];
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < 128 * 32; e += blockDim.x) {
+        const int il = e >> 5, jl = e & 31;
+        const int64_t i = tile * 128 + il;
+        if (i < rows && j0 + jl < r) {
+          const float v = t[il][jl];
+          F[i * ldf + j0 + jl] = v;
+          mn = fmin(mn, (double)v);
+        }
+      }
+    }
+  }
+  red[threadIdx.x] = mn;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && active) minparts[blockIdx.x] = red[0];
+}
+
 __global__ void pbcd_copy_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r,
                                  const float* __restrict__ snaps, const int* __restrict__ kstar,
                                  const int* stage, double* minparts) {
@@ -416,9 +463,13 @@ void pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C
 
 void pbcd_commit(float* F, int64_t ldf, int64_t rows, int r, const float* snaps,
                  const double* pgsum, double eps, int max_iter, int* kstar, const int* stage,
-                 double* minparts, cudaStream_t st) {
+                 double* minparts, bool tiled, cudaStream_t st) {
   pbcd_select_kernel<<<1, 32, 0, st>>>(pgsum, max_iter, eps, kstar, stage);
-  pbcd_copy_kernel<<<kRowGrid, 256, 0, st>>>(F, ldf, rows, r, snaps, kstar, stage, minparts);
+  if (tiled)
+    pbcd_copy_tiled_kernel<<<kRowGrid, 256, 0, st>>>(F, ldf, rows, r, snaps, kstar, stage,
+                                                     minparts);
+  else
+    pbcd_copy_kernel<<<kRowGrid, 256, 0, st>>>(F, ldf, rows, r, snaps, kstar, stage, minparts);
   count_launch(2);
 }
 

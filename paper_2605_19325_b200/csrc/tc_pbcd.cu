@@ -34,8 +34,10 @@ constexpr int COMPUTE_WARPS = 8;
 constexpr int THREADS = 32 * COMPUTE_WARPS;   // 8 warps: 255 registers per thread available
 constexpr int KR = 128;                     // K (= r) padded to the MMA depth multiple
 constexpr int PLANE_A = BM * KR;            // 16 KB
-constexpr int PLANE_B = 128 * KR;           // <= 16 KB (rp rows)
-constexpr int SMEM_BYTES = 4 * PLANE_A + 4 * PLANE_B + 1024;
+constexpr int PLANE_B = 128 * KR;           // 16 KB (G padded to 128 rows)
+constexpr int CQ_LD = KR + 1;               // padded row stride (words): conflict-free row reads
+constexpr int CQ_BYTES = BM * CQ_LD * 4;    // the tile's c rows as int32 fixed point
+constexpr int SMEM_BYTES = 4 * PLANE_A + 4 * PLANE_B + CQ_BYTES + 1024;
 
 struct Params {
   const float* F;
@@ -94,6 +96,14 @@ __device__ __forceinline__ void pack_store(const Pack16& pk, uint8_t* Ad, int of
     *reinterpret_cast<uint4*>(Ad + pl * PLANE_A + off) =
         make_uint4(pk.w[pl][0], pk.w[pl][1], pk.w[pl][2], pk.w[pl][3]);
 }
+// mask bit c of a thread's 64 columns; opaque() stops the compiler from hoisting the 64 bit
+// tests out of the iteration loop (they would occupy 64 registers)
+__device__ __forceinline__ bool mbit(uint32_t lo, uint32_t hi, int c) {
+  return ((c < 32 ? lo >> c : hi >> (c - 32)) & 1u) != 0u;
+}
+__device__ __forceinline__ void opaque(uint32_t& a, uint32_t& b) {
+  asm volatile("" : "+r"(a), "+r"(b));
+}
 __device__ __forceinline__ int digit_at(const uint4& v, int k) {
   const uint32_t w = (k >> 2) == 0 ? v.x : ((k >> 2) == 1 ? v.y : ((k >> 2) == 2 ? v.z : v.w));
   return (int)(int8_t)(uint8_t)(w >> (8 * (k & 3)));
@@ -145,9 +155,10 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
   for (int j = threadIdx.x; j < 128; j += blockDim.x) gsc_s[j] = j < p.r ? p.gscale[j] : 0.0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_d = smem_u32(&bars[0]);     // MMA -> all warps: accumulators ready
-  const int rp = p.rp;
+  constexpr int rp = KR;                         // G padded to 128 columns (p.rp == KR)
   const int tiles = (int)((p.rows + BM - 1) / BM);
-  double* pgsm = reinterpret_cast<double*>(Bd + 4 * PLANE_B);   // max_iter + 1 running sums
+  int32_t* Cq = reinterpret_cast<int32_t*>(Bd + 4 * PLANE_B);    // c tile, fixed point per row
+  double* pgsm = reinterpret_cast<double*>(Bd + 4 * PLANE_B + CQ_BYTES);   // max_iter + 1 sums
 
   // G digits -> shared memory (once per CTA); zero the A planes' padding once
   for (int e = threadIdx.x; e < 4 * rp * KR / 16; e += blockDim.x)
@@ -179,10 +190,13 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
     const int hc = warp >> 2;                  // column half
     const int rt = 32 * q + lane;              // row in tile
     const int c0 = 64 * hc;
-    const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16);
+    // my TMEM lane quadrant and column half; class k of the accumulators at column k * KR
+    const uint32_t tcol = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
     const double lam = *p.lam;
     const int64_t snap_stride = p.rows * (int64_t)p.r;
     const int g8 = rt >> 3, ri = rt & 7;
+    // my 16-byte digit chunks in the A planes: chunk b of my half at abase + b * 16 * 128
+    uint8_t* const abase = Ad + ((c0 >> 4) * 16 + g8) * 128 + ri * 16;
     uint32_t round = 0;
     const double* gsc = gsc_s + c0;            // 1 / t_j for my columns (shared memory)
 
@@ -190,16 +204,34 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
       const int64_t row = (int64_t)t * BM + rt;
       const bool rok = row < p.rows;
       double u[64];
-      uint64_t msk = 0;
+      uint32_t mlo = 0, mhi = 0;   // M_{U+} bits of my 64 columns
 #pragma unroll
       for (int c = 0; c < 64; ++c) {
         const int col = c0 + c;
         double v = (rok && col < p.r) ? (double)p.F[row * p.ldf + col] : 0.0;
         if (v < 0.0) v += lam;                                     // Eq.(6)/(7) lift
         u[c] = v;
-        if (rok && col < p.r && v >= 0.0) msk |= (1ull << c);      // M_{U+} (R14)
+        if (rok && col < p.r && v >= 0.0) {                        // M_{U+} (R14)
+          if (c < 32) mlo |= 1u << c; else mhi |= 1u << (c - 32);
+        }
       }
-      const double* crow = p.C + row * p.r;
+      // c_i (row of P or Q) -> shared memory as int32 fixed point with a power-of-two row scale:
+      // c = cq * csc, |error| <= 2^-27 max_j |c_ij| (the same resolution as the u / g digits)
+      double cs;
+      {
+        const double* crow = p.C + row * p.r;
+        double cm = 0.0;
+        for (int c = 0; c < 64; ++c)
+          if (rok && c0 + c < p.r) cm = fmax(cm, fabs(crow[c0 + c]));
+        xch2[hc][rt] = cm;
+        bar_compute();
+        const double sc = pow2s(fmax(cm, xch2[1 - hc][rt]));
+        cs = 0x1p-21 / sc;
+        for (int c = 0; c < 64; ++c)
+          Cq[rt * CQ_LD + c0 + c] =
+              (rok && c0 + c < p.r) ? __double2int_rn(crow[c0 + c] * sc * 0x1p21) : 0;
+      }
+      const int32_t* cqrow = Cq + rt * CQ_LD + c0;
       for (int it = 0; it <= p.max_iter; ++it) {
         // ---------------- round A: T1 = u G ----------------
         double mx = 0.0;
@@ -215,8 +247,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
           pack_clear(pk);
 #pragma unroll
           for (int k = 0; k < 16; ++k) pack_put(pk, k, digits_word(u[16 * ch + k] * su));
-          const int kc = (c0 >> 4) + ch;
-          pack_store(pk, Ad, (kc * 16 + g8) * 128 + ri * 16);
+          pack_store(pk, abase, ch * 16 * 128);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         bar_compute();
@@ -225,13 +256,15 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
         ++round;
         tc_fence_after();
         // pass 1: grad = T1 / su - c ; ||M o grad||^2 (pg of iteration it), num, max|g|
-        double pg = 0.0, num = 0.0, gmx = 0.0;
+        double num = 0.0, gmx = 0.0;
+        opaque(mlo, mhi);
         const double isu = 1.0 / su;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
+#pragma unroll 1
+        for (int b = 0; b < 8; ++b) {       // rolled: keeps the kernel inside the icache
           uint32_t v[4][8];
 #pragma unroll
-          for (int cls = 0; cls < 4; ++cls) TMEM_LD8(taddr + cls * rp + c0 + 8 * b, v[cls]);
+          for (int cls = 0; cls < 4; ++cls) TMEM_LD8(tcol + cls * KR + 8 * b, v[cls]);
+          const uint32_t mb = ((b < 4 ? mlo : mhi) >> (8 * (b & 3))) & 255u;
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
@@ -239,15 +272,14 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
             double a = 0.0;
 #pragma unroll
             for (int cls = 3; cls >= 0; --cls) a = a * 0x1p-7 + (double)(int)v[cls][k];
-            const double gr = (c0 + c < p.r && rok) ? a * isu * gsc[c] - crow[c0 + c] : 0.0;
-            if ((msk >> c) & 1ull) {
-              pg = fma(gr, gr, pg);
-              num = fma(gr, gr, num);
-              gmx = fmax(gmx, fabs(gr));
-            }
+            const double gr = a * isu * gsc[c] - (double)cqrow[c] * cs;
+            const double gm = ((mb >> k) & 1u) ? gr : 0.0;     // M o grad
+            num = fma(gm, gm, num);
+            gmx = fmax(gmx, fabs(gm));
           }
         }
         // per-iteration partial of ||M o grad||^2 (fixed-order block reduction)
+        double pg = num;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) pg += __shfl_xor_sync(0xffffffffu, pg, o);
         if (lane == 0) wsum[w] = pg;
@@ -268,15 +300,17 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
         const double numr = hc == 0 ? num + xch2[1][rt] : xch2[0][rt] + num;
         const double sg = pow2s(fmax(gmx, xch[1 - hc][rt]));
         // pass 2: digits of g * sg (g = M o grad) into the A planes (T1 re-read from TMEM)
-#pragma unroll
+        opaque(mlo, mhi);
+#pragma unroll 1
         for (int b = 0; b < 4; ++b) {
           Pack16 pk;
           pack_clear(pk);
+          const uint32_t mb = ((b < 2 ? mlo : mhi) >> (16 * (b & 1))) & 65535u;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             uint32_t v[4][8];
 #pragma unroll
-            for (int cls = 0; cls < 4; ++cls) TMEM_LD8(taddr + cls * rp + c0 + 16 * b + 8 * h, v[cls]);
+            for (int cls = 0; cls < 4; ++cls) TMEM_LD8(tcol + cls * KR + 16 * b + 8 * h, v[cls]);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -284,13 +318,12 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
               double a = 0.0;
 #pragma unroll
               for (int cls = 3; cls >= 0; --cls) a = a * 0x1p-7 + (double)(int)v[cls][k];
-              const double gr = (c0 + c < p.r && rok) ? a * isu * gsc[c] - crow[c0 + c] : 0.0;
-              const double g = ((msk >> c) & 1ull) ? gr : 0.0;
+              const double gr = a * isu * gsc[c] - (double)cqrow[c] * cs;
+              const double g = ((mb >> (8 * h + k)) & 1u) ? gr : 0.0;
               pack_put(pk, 8 * h + k, digits_word(g * sg));
             }
           }
-          const int kc = (c0 >> 4) + b;
-          pack_store(pk, Ad, (kc * 16 + g8) * 128 + ri * 16);
+          pack_store(pk, abase, b * 16 * 128);
         }
         tc_fence_before();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -300,20 +333,21 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
         mbar_wait(bar_d, round & 1);
         ++round;
         tc_fence_after();
+        // den = sum_j g_j h_j with g = rebuild / sg, h = T2 gsc / sg: accumulate rebuild * T2 gsc
+        // and apply the exact power-of-two 1 / sg^2 once
         double den = 0.0;
         const double isg = 1.0 / sg;
-#pragma unroll
+#pragma unroll 1
         for (int b = 0; b < 4; ++b) {
-          const int kc = (c0 >> 4) + b;
-          const int off = (kc * 16 + g8) * 128 + ri * 16;
           uint4 dq[4];
 #pragma unroll
-          for (int pl = 0; pl < 4; ++pl) dq[pl] = *reinterpret_cast<const uint4*>(Ad + pl * PLANE_A + off);
+          for (int pl = 0; pl < 4; ++pl)
+            dq[pl] = *reinterpret_cast<const uint4*>(abase + pl * PLANE_A + b * 16 * 128);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             uint32_t v[4][8];
 #pragma unroll
-            for (int cls = 0; cls < 4; ++cls) TMEM_LD8(taddr + cls * rp + c0 + 16 * b + 8 * hh, v[cls]);
+            for (int cls = 0; cls < 4; ++cls) TMEM_LD8(tcol + cls * KR + 16 * b + 8 * hh, v[cls]);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -321,39 +355,38 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
               double a = 0.0;
 #pragma unroll
               for (int cls = 3; cls >= 0; --cls) a = a * 0x1p-7 + (double)(int)v[cls][k];
-              const double h = a * isg * gsc[c];
-              const double g = rebuild(dq, 8 * hh + k) * isg;
-              den = fma(g, h, den);
+              den = fma(rebuild(dq, 8 * hh + k), a * gsc[c], den);
             }
           }
         }
+        den *= isg * isg;
         tc_fence_before();
         xch[hc][rt] = den;
         bar_compute();
         const double denr = hc == 0 ? den + xch[1][rt] : xch[0][rt] + den;
         // Eq.(10): d_i = ||g_i||^2 / ||g_i V^T||^2 (0 on a zero denominator, R10); Eq.(8)
         const double dstep = denr > 0.0 ? numr / denr : 0.0;
+        opaque(mlo, mhi);
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const int kc = (c0 >> 4) + b;
-          const int off = (kc * 16 + g8) * 128 + ri * 16;
           uint4 dq[4];
 #pragma unroll
-          for (int pl = 0; pl < 4; ++pl) dq[pl] = *reinterpret_cast<const uint4*>(Ad + pl * PLANE_A + off);
+          for (int pl = 0; pl < 4; ++pl)
+            dq[pl] = *reinterpret_cast<const uint4*>(abase + pl * PLANE_A + b * 16 * 128);
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
             const int c = 16 * b + k;
-            if ((msk >> c) & 1ull) {
-              const double g = rebuild(dq, k) * isg;
-              u[c] = fmax(0.0, u[c] - dstep * g);
-            }
+            const double un = fmax(0.0, u[c] - dstep * (rebuild(dq, k) * isg));
+            u[c] = mbit(mlo, mhi, c) ? un : u[c];     // entries outside M_{U+} stay fixed
           }
         }
         if (rok) {
-          float* sn = p.snaps + (int64_t)it * snap_stride + row * p.r;
+          // snapshot, tile-major (pbcd_copy_tiled_kernel): a warp's 32 rows are contiguous
+          const int nt = (int)(p.rows - (int64_t)t * BM < BM ? p.rows - (int64_t)t * BM : BM);
+          float* sn = p.snaps + (int64_t)it * snap_stride + (int64_t)t * BM * p.r + rt;
 #pragma unroll
           for (int c = 0; c < 64; ++c)
-            if (c0 + c < p.r) sn[c0 + c] = (float)u[c];
+            if (c0 + c < p.r) sn[(int64_t)(c0 + c) * nt] = (float)u[c];
         }
         bar_compute();          // everyone has read the g digits before they are overwritten
       }
@@ -408,7 +441,7 @@ void tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double
                   double* pgparts, int8_t* gd_work, double* gscale_work, const int* stage,
                   cudaStream_t st) {
   using namespace tpb;
-  const int rp = (r + 15) / 16 * 16;
+  const int rp = KR;   // G padded to 128 columns: class k of the accumulators at column k * 128
   gdigits_kernel<<<1, 256, 0, st>>>(G, r, rp, gd_work, gscale_work, stage);
   Params p;
   p.F = F;
@@ -428,6 +461,7 @@ void tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc_pbcd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(tc_pbcd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr = true;
   }
   const int tiles = (int)((rows + BM - 1) / BM);
