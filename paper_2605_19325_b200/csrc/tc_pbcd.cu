@@ -37,7 +37,7 @@ constexpr int PLANE_A = BM * KR;            // 16 KB
 constexpr int PLANE_B = 128 * KR;           // 16 KB (G padded to 128 rows)
 constexpr int CQ_LD = KR + 1;               // padded row stride (words): conflict-free row reads
 constexpr int CQ_BYTES = BM * CQ_LD * 4;    // the tile's c rows as int32 fixed point
-constexpr int SMEM_BYTES = 4 * PLANE_A + 4 * PLANE_B + CQ_BYTES + 1024;
+constexpr int SMEM_BYTES = 4 * PLANE_A + 4 * PLANE_B + CQ_BYTES;
 
 struct Params {
   const float* F;
@@ -59,6 +59,23 @@ __device__ __forceinline__ double pow2s(double mx) {
   int e;
   frexp(mx, &e);
   return ldexp(1.0, 6 - e);
+}
+
+// pow2s from the high word of |x| (sign masked): only the exponent matters, so the maximum of
+// the high words of a row selects the same power of two as pow2s(max |x|).  Zero / subnormal
+// rows get 1 (their digits are zero anyway at 2^-22 resolution).
+__device__ __forceinline__ int hiabs(double x) { return __double2hiint(x) & 0x7fffffff; }
+__device__ __forceinline__ double pow2s_hi(int h) {
+  if (h < 0x00100000) return 1.0;
+  const int E = h >> 20;                       // biased exponent; frexp exponent e = E - 1022
+  return __hiloint2double((2051 - E) << 20, 0); // 2^(6 - e)
+}
+// The 4 weight classes of an accumulator column combined exactly: v0 2^21 + v1 2^14 + v2 2^7 + v3
+// (< 2^53, so the conversion to double is exact); callers fold 2^-21 into their scales.
+__device__ __forceinline__ double comb4(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3) {
+  const long long a = (long long)(int)v0 * 2097152ll + (long long)(int)v1 * 16384ll +
+                      (long long)(int)v2 * 128ll + (long long)(int)v3;
+  return (double)a;
 }
 
 __device__ __forceinline__ void bar_compute() {
@@ -142,17 +159,20 @@ __device__ __forceinline__ void issue_round(uint32_t a0, uint32_t b0, uint32_t t
 
 __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_raw;                  // no-swizzle operands need 16-byte alignment only
   uint8_t* Ad = smem;                        // 4 planes of A digits (128 x KR, K-major)
   uint8_t* Bd = smem + 4 * PLANE_A;          // 4 planes of G digits (rp x KR, K-major)
   __shared__ __align__(8) uint64_t bars[1];
   __shared__ uint32_t tmem_base_s;
   __shared__ double xch[2][BM];              // row exchange between the two column halves
+  __shared__ int xchi[2][BM];
   __shared__ double xch2[2][BM];
   __shared__ double wsum[COMPUTE_WARPS];
   __shared__ double gsc_s[128];
   if (p.stage != nullptr && *p.stage != 0) return;
-  for (int j = threadIdx.x; j < 128; j += blockDim.x) gsc_s[j] = j < p.r ? p.gscale[j] : 0.0;
+  // 2^-21 / t_j: the column scale with comb4's 2^-21 folded in (exact)
+  for (int j = threadIdx.x; j < 128; j += blockDim.x)
+    gsc_s[j] = j < p.r ? p.gscale[j] * 0x1p-21 : 0.0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_d = smem_u32(&bars[0]);     // MMA -> all warps: accumulators ready
   constexpr int rp = KR;                         // G padded to 128 columns (p.rp == KR)
@@ -234,12 +254,12 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
       const int32_t* cqrow = Cq + rt * CQ_LD + c0;
       for (int it = 0; it <= p.max_iter; ++it) {
         // ---------------- round A: T1 = u G ----------------
-        double mx = 0.0;
+        int mh = 0;
 #pragma unroll
-        for (int c = 0; c < 64; ++c) mx = fmax(mx, fabs(u[c]));
-        xch[hc][rt] = mx;
+        for (int c = 0; c < 64; ++c) mh = max(mh, hiabs(u[c]));
+        xchi[hc][rt] = mh;
         bar_compute();
-        const double su = pow2s(fmax(mx, xch[1 - hc][rt]));
+        const double su = pow2s_hi(max(mh, xchi[1 - hc][rt]));
         // digits of u * su into the A planes: chunk (kc, g8, ri), 16 columns each
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
@@ -256,7 +276,8 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
         ++round;
         tc_fence_after();
         // pass 1: grad = T1 / su - c ; ||M o grad||^2 (pg of iteration it), num, max|g|
-        double num = 0.0, gmx = 0.0;
+        double num = 0.0;
+        int gmh = 0;
         opaque(mlo, mhi);
         const double isu = 1.0 / su;
 #pragma unroll 1
@@ -269,13 +290,11 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const int c = 8 * b + k;
-            double a = 0.0;
-#pragma unroll
-            for (int cls = 3; cls >= 0; --cls) a = a * 0x1p-7 + (double)(int)v[cls][k];
+            const double a = comb4(v[0][k], v[1][k], v[2][k], v[3][k]);
             const double gr = a * isu * gsc[c] - (double)cqrow[c] * cs;
             const double gm = ((mb >> k) & 1u) ? gr : 0.0;     // M o grad
             num = fma(gm, gm, num);
-            gmx = fmax(gmx, fabs(gm));
+            gmh = max(gmh, hiabs(gm));
           }
         }
         // per-iteration partial of ||M o grad||^2 (fixed-order block reduction)
@@ -283,7 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) pg += __shfl_xor_sync(0xffffffffu, pg, o);
         if (lane == 0) wsum[w] = pg;
-        xch[hc][rt] = gmx;
+        xchi[hc][rt] = gmh;
         xch2[hc][rt] = num;
         bar_compute();
         if (threadIdx.x == 32) {
@@ -298,7 +317,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
           break;
         }
         const double numr = hc == 0 ? num + xch2[1][rt] : xch2[0][rt] + num;
-        const double sg = pow2s(fmax(gmx, xch[1 - hc][rt]));
+        const double sg = pow2s_hi(max(gmh, xchi[1 - hc][rt]));
         // pass 2: digits of g * sg (g = M o grad) into the A planes (T1 re-read from TMEM)
         opaque(mlo, mhi);
 #pragma unroll 1
@@ -315,9 +334,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const int c = 16 * b + 8 * h + k;
-              double a = 0.0;
-#pragma unroll
-              for (int cls = 3; cls >= 0; --cls) a = a * 0x1p-7 + (double)(int)v[cls][k];
+              const double a = comb4(v[0][k], v[1][k], v[2][k], v[3][k]);
               const double gr = a * isu * gsc[c] - (double)cqrow[c] * cs;
               const double g = ((mb >> (8 * h + k)) & 1u) ? gr : 0.0;
               pack_put(pk, 8 * h + k, digits_word(g * sg));
@@ -352,9 +369,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const int c = 16 * b + 8 * hh + k;
-              double a = 0.0;
-#pragma unroll
-              for (int cls = 3; cls >= 0; --cls) a = a * 0x1p-7 + (double)(int)v[cls][k];
+              const double a = comb4(v[0][k], v[1][k], v[2][k], v[3][k]);
               den = fma(rebuild(dq, 8 * hh + k), a * gsc[c], den);
             }
           }
