@@ -15,21 +15,25 @@
 //     bytes of fp32 X; the factor is repacked per pass.
 //   * tcgen05.mma kind::i8 (M=128, N = r rounded to 16, K=32) accumulates exactly in int32 TMEM,
 //     one accumulator per digit weight class c = i + j <= 3:
-//         acc_c = sum_{i+j=c} A_i B_j      (10 MMAs per 32-deep k-step, 4 x 128 TMEM columns)
-//     and the epilogue forms acc0 + acc1 2^-7 + acc2 2^-14 + acc3 2^-21 EXACTLY in fp64 (31
-//     integer + 21 fractional bits) before applying 1/(s_X s_k).  The only errors are the
-//     omitted weight <= 2^-28 products and sub-threshold digit truncation: P and Q come out
-//     accurate to ~1e-9 relative, which the trace-form objective needs near the optimum
-//     (||X||^2 / f ~ 3e7 at C5, SURVEY Hard part 2).
-//   * One packed copy serves both passes: tiles of 128 rows x 64 columns per plane in the
-//     UMMA no-swizzle canonical layout, core matrix (g, kc) at byte (kc*16 + g)*128 (8 rows x 16
-//     bytes); it is a K-major A operand for P = X V (SBO 128 B, LBO 2048 B) and, two column-
-//     adjacent tiles giving 8 MN groups at a uniform 2048 B stride, an MN-major A operand for
-//     Q = X^T U (gathered into SBO 1024 B / LBO 128 B in shared memory by 1 KB bulk copies).
-//   * Warp roles: warp 0 = producer (cp.async.bulk into a 4-stage ring, mbarrier complete_tx),
-//     warp 1 = TMEM allocator + single-thread MMA issuer, warps 2..9 = epilogue.  Persistent
-//     grid, one CTA per SM.  Units: pass 1 = one 128-row band over all of K; pass 2 = one
-//     128-column band over a K range (split-K, fixed-order fp64 reduction).
+//         acc_c = sum_{i+j=c} A_i B_j      (10 products, 4 x 128 TMEM columns)
+//     issued as 6 MMAs per 32-deep k-step: B planes of two classes are paired into one N = 2r
+//     MMA writing adjacent accumulators (MmaList<4>), halving the A-operand smem reads that ncu
+//     showed to limit the 10-MMA form.  Pass 1 with n >= 8192 uses 3 classes (6 products, 4
+//     MMAs, 3 X planes read).  The epilogue forms acc0 + acc1 2^-7 + acc2 2^-14 + acc3 2^-21
+//     EXACTLY in fp64 (31 integer + 21 fractional bits) before applying 1/(s_X s_k).  The only
+//     errors are the omitted low-weight products and sub-threshold digit truncation: P and Q
+//     come out accurate to ~1e-9 relative, which the trace-form objective needs near the
+//     optimum (||X||^2 / f ~ 3e7 at C5, SURVEY Hard part 2).
+//   * Layout: tiles of 128 rows x 64 columns per plane in the UMMA no-swizzle canonical layout,
+//     core matrix (g, kc) at byte (kc*16 + g)*128 (8 rows x 16 bytes): a K-major A operand for
+//     P = X V (SBO 128 B, LBO 2048 B).  Q = X^T U reads a second packed copy of X^T in the same
+//     K-major layout (mode 2); without it (ENMF_TC_XT=0 or not enough memory) the X copy is
+//     gathered as an MN-major A operand (mode 1: two column-adjacent tiles give 8 MN groups at a
+//     uniform 2048 B stride, 1 KB bulk copies into SBO 1024 B / LBO 128 B), ~40 % slower.
+//   * Warp roles: warp 0 = producer (cp.async.bulk into a 3-stage ring -- 4 with 3 planes --,
+//     mbarrier complete_tx), warp 1 = TMEM allocator + single-thread MMA issuer, warps 2..9 =
+//     epilogue.  Persistent grid, one CTA per SM.  Units: pass 1 = one 128-row band over all of
+//     K; pass 2 = one 128-column band over a K range (split-K, fixed-order fp64 reduction).
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
