@@ -93,11 +93,16 @@ hals_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r, const doubl
   double* Gs = smem;
   double* Ss = smem + RP * RP + (threadIdx.x >> 5) * RB * RP;
   __shared__ double wmin_s[kRowWarps];
+  __shared__ double ginv[RP];                 // 1 / G_kk, 0 where G_kk <= 0 (column skipped)
   const bool active = stage == nullptr || *stage == 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double wmin = DBL_MAX;
   if (active) {
     load_gram<CPL>(G, r, Gs);
+    for (int k = threadIdx.x; k < RP; k += blockDim.x) {
+      const double gkk = k < r ? G[k * r + k] : 0.0;
+      ginv[k] = gkk > 0.0 ? 1.0 / gkk : 0.0;
+    }
     __syncthreads();
     const int64_t nblk = (rows + RB - 1) / RB;
     for (int64_t rb = (int64_t)blockIdx.x * kRowWarps + warp; rb < nblk;
@@ -119,18 +124,19 @@ hals_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r, const doubl
         const int kmax = r - 32 * s < 32 ? r - 32 * s : 32;
         for (int kk = 0; kk < kmax; ++kk) {
           const int k = 32 * s + kk;
-          const double gkk = Gs[k * RP + k];
+          const double ig = ginv[k];
           double gk[CPL];
 #pragma unroll
           for (int c = 0; c < CPL; ++c) gk[c] = Gs[k * RP + lane + 32 * c];
 #pragma unroll
           for (int b = 0; b < RB; ++b) {
-            const double tk = __shfl_sync(FULL, t[b][s], kk);
-            const double uk = __shfl_sync(FULL, u[b][s], kk);
-            // U_ik <- max(0, U_ik + (C_ik - sum_l U_il G_lk) / G_kk)   (skip if G_kk <= 0)
-            const double nu = gkk > 0.0 ? fmax(0.0, uk + tk / gkk) : uk;
-            const double d = nu - uk;
+            // U_ik <- max(0, U_ik + (C_ik - sum_l U_il G_lk) / G_kk)   (skip if G_kk <= 0).
+            // Lane kk owns (u_k, t_k): every lane evaluates the update on its own pair (only
+            // lane kk's is meaningful) and lane kk's change d is broadcast -- one shuffle.
+            const double uo = u[b][s];
+            const double nu = ig > 0.0 ? fmax(0.0, fma(t[b][s], ig, uo)) : uo;
             if (lane == kk) u[b][s] = nu;
+            const double d = __shfl_sync(FULL, nu - uo, kk);
 #pragma unroll
             for (int c = 0; c < CPL; ++c) t[b][c] = fma(-d, gk[c], t[b][c]);
           }
