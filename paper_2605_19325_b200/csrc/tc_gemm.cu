@@ -79,6 +79,7 @@ struct Params {
   int rp;                    // padded N (multiple of 16, <= 128)
   int r;                     // valid output columns
   int64_t out_rows;          // valid output rows
+  int tiles;                 // 128-row output tiles (pair kernel: tile 2 t + rank may not exist)
 };
 
 using namespace tcp;
@@ -169,11 +170,12 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
         __syncwarp();
         const uint32_t st = smem_u32(smem + (size_t)stage * STAGE);
         if (p.mode == 0) {
-          const int64_t off = ((int64_t)tile * p.tiles_per_row + ks) * TILE_A;
+          // the NPL planes of a tile are contiguous: one bulk copy
+          const int64_t off = ((int64_t)tile * p.tiles_per_row + ks) * PLANES * TILE_A;
           if (lane < NPL) bulk_g2s(st + lane * TILE_A, p.xp[lane] + off, TILE_A, fb);
         } else if (p.mode == 2) {
-          // A = X^T from the transposed packed copy: K-major tiles, one 8 KB copy per plane
-          const int64_t off = ((int64_t)tile * p.tiles_per_row_t + ks) * TILE_A;
+          // A = X^T from the transposed packed copy: K-major tiles
+          const int64_t off = ((int64_t)tile * p.tiles_per_row_t + ks) * PLANES * TILE_A;
           if (lane < NPL) bulk_g2s(st + lane * TILE_A, p.xtp[lane] + off, TILE_A, fb);
         } else {
           // A = X^T: output rows j = column tiles 2*tile, 2*tile+1 of row band ks/2; the K stage
@@ -181,13 +183,13 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
           const int64_t band = ks >> 1;
           const int half = ks & 1;
           const int t = (lane >> 2) & 1, kc = lane & 3;
-          const int64_t src = (band * p.tiles_per_row + 2 * tile + t) * TILE_A +
+          const int64_t src = (band * p.tiles_per_row + 2 * tile + t) * PLANES * TILE_A +
                               (int64_t)(kc * 16 + 8 * half) * 128;
           const uint32_t dst = (uint32_t)((t * 4 + kc) * 1024);
           for (int pl = lane >> 3; pl < NPL; pl += 4)
             bulk_g2s(st + pl * TILE_A + dst, p.xp[pl] + src, 1024, fb);
         }
-        const int64_t foff = (int64_t)ks * tile_b;
+        const int64_t foff = (int64_t)ks * PLANES * tile_b;
         if (lane >= 28 && lane - 28 < NPL)
           bulk_g2s(st + NPL * TILE_A + (lane - 28) * tile_b, p.fp[lane - 28] + foff, tile_b, fb);
         if (++stage == NST) { stage = 0; phase ^= 1; }
@@ -251,7 +253,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
       int tile, s0, s1, split;
       unit_range(p, u, tile, s0, s1, split);
       if (s1 <= s0) continue;
-      mbar_wait(bar_tfull, nunit & 1);
+      mbar_wait_sleep(bar_tfull, nunit & 1);
       tc_fence_after();
       const int64_t row = (int64_t)tile * BM + row_in_tile;
       double* o = p.out + (int64_t)split * p.split_stride + row * p.out_ld;
@@ -294,6 +296,221 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
   }
 }
 
+// ------------------------------------------------------------------ CTA-pair kernel
+// cta_group::2: a cluster of two CTAs (two SMs of a TPC) computes a 256-row output band with
+// M = 256 MMAs issued by the even CTA.  Each CTA stages its own 128 rows of A (X or X^T digits,
+// tile 2 t + rank) and HALF of every B operand, at the same shared-memory offsets: for a wide
+// MMA [B_j; B_j+1] (N = 2 rp) CTA 0 holds plane j and CTA 1 plane j+1; for a narrow one (N = rp)
+// each holds rp/2 rows of the plane (a contiguous half of the canonical tile).  Per SM this
+// halves the B-operand shared-memory reads that co-limit the single-CTA kernel (ncu: smem tc
+// wavefronts 75 %), so the tensor pipe can run at its full int8 rate.
+// Synchronisation: each CTA's producer fills its own stage (cp.async.bulk, local mbarrier);
+// CTA 1's idle MMA warp relays its stage completion to the leader (remote mbarrier arrive);
+// the leader's commits are multicast to both CTAs (stage empty, accumulators full); both CTAs'
+// epilogues release the accumulators on the leader's barrier.
+constexpr int PAIR_SMEM = 230400;
+
+template <int NCLS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    tc_i8_pair_kernel(const Params p) {
+  constexpr int NPL = NCLS;
+  constexpr int NWIDE = NCLS == 4 ? 2 : 1;                        // wide B regions
+  constexpr int STAGE = NPL * TILE_A + (NWIDE + 1) * MAX_TILE_B;  // A planes | wide | 2 halves
+  constexpr int NST = (PAIR_SMEM - 1024) / STAGE;                 // 4 (4 planes) or 5 (3 planes)
+  using L = MmaList<NCLS>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t bars[3 * 8 + 2];
+  __shared__ uint32_t tmem_base_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t bar_full = smem_u32(&bars[0]);
+  const uint32_t bar_empty = smem_u32(&bars[NST]);
+  const uint32_t bar_peer = smem_u32(&bars[2 * NST]);       // leader: CTA 1's stage is full
+  const uint32_t bar_tfull = smem_u32(&bars[3 * NST]);
+  const uint32_t bar_tempty = smem_u32(&bars[3 * NST + 1]);  // leader: both epilogues drained
+  const uint32_t tile_b = (uint32_t)p.rp * BK;
+  const uint32_t half_b = tile_b / 2;
+  const uint32_t b_bytes = NWIDE * tile_b + 2 * half_b;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, 1);
+      mbar_init(bar_peer + 8 * s, 1);
+    }
+    mbar_init(bar_tfull, 1);
+    mbar_init(bar_tempty, 2 * EPI_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+
+  if (warp == 0) {
+    // ===================== producer (both CTAs): own A rows, own half of B =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = cid; u < p.num_units; u += ncl) {
+      int pt, s0, s1, split;
+      unit_range(p, u, pt, s0, s1, split);
+      const int tile = min(2 * pt + (int)rank, p.tiles - 1);   // a missing odd tile re-reads
+      for (int ks = s0; ks < s1; ++ks) {                       // the last one; not stored
+        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+        const uint32_t fb = bar_full + 8 * stage;
+        if (lane == 0) mbar_expect_tx(fb, NPL * TILE_A + b_bytes);
+        __syncwarp();
+        const uint32_t st = smem_u32(smem + (size_t)stage * STAGE);
+        if (lane == 0) {
+          const int8_t* src =
+              p.mode == 0 ? p.xp[0] + ((int64_t)tile * p.tiles_per_row + ks) * PLANES * TILE_A
+                          : p.xtp[0] + ((int64_t)tile * p.tiles_per_row_t + ks) * PLANES * TILE_A;
+          bulk_g2s(st, src, NPL * TILE_A, fb);
+        }
+        const int64_t foff = (int64_t)ks * PLANES * tile_b;
+        const uint32_t bst = st + NPL * TILE_A;
+        if (lane == 28) bulk_g2s(bst, p.fp[rank] + foff, tile_b, fb);                  // B0|B1
+        if (NWIDE == 2 && lane == 29)
+          bulk_g2s(bst + tile_b, p.fp[2 + rank] + foff, tile_b, fb);                   // B2|B3
+        if (lane == 30)                                                                // B2 half
+          bulk_g2s(bst + NWIDE * tile_b, p.fp[2] + foff + rank * half_b, half_b, fb);
+        if (lane == 31)                                                                // B0 half
+          bulk_g2s(bst + NWIDE * tile_b + half_b, p.fp[0] + foff + rank * half_b, half_b, fb);
+        if (++stage == NST) { stage = 0; phase ^= 1; }
+      }
+    }
+    // drain: the leader's last commits arrive on this CTA's empty barriers before it exits
+    for (int i = 0; i < NST; ++i) {
+      mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+      if (++stage == NST) { stage = 0; phase ^= 1; }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ===================== MMA issuer (leader CTA, one thread) =====================
+      const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 4) << 24);
+      const uint32_t idesc1 = idesc_base | ((uint32_t)(p.rp >> 3) << 17);
+      const uint32_t idesc2 = idesc_base | ((uint32_t)(2 * p.rp >> 3) << 17);
+      const uint32_t a_lbo = 2048u, a_sbo = 128u, a_kstep = 4096u;
+      const uint32_t b_lbo = 128u, b_sbo = 512u, b_kstep = 256u;
+      const uint32_t rpc = (uint32_t)p.rp;
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t nunit = 0;
+      for (int u = cid; u < p.num_units; u += ncl) {
+        int pt, s0, s1, split;
+        unit_range(p, u, pt, s0, s1, split);
+        if (s1 <= s0) continue;
+        mbar_wait_cluster(bar_tempty, (nunit & 1) ^ 1);
+        tc_fence_after();
+        for (int ks = s0; ks < s1; ++ks) {
+          mbar_wait(bar_full + 8 * stage, phase);
+          mbar_wait_cluster(bar_peer + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(smem + (size_t)stage * STAGE);
+          const uint32_t b0 = a0 + NPL * TILE_A;
+#pragma unroll
+          for (int j = 0; j < BK / 32; ++j) {
+#pragma unroll
+            for (int q = 0; q < L::N; ++q) {
+              const int pa = L::t(q, 0), pb = L::t(q, 1), ac = L::t(q, 2), wide = L::t(q, 3);
+              // B region: wide [B0;B1] / [B2;B3] at 0 / tile_b; narrow B2 / B0 halves after them
+              const uint32_t breg = wide ? (pb == 0 ? 0u : tile_b)
+                                         : NWIDE * tile_b + (pb == 0 ? half_b : 0u);
+              const uint64_t ad = umma_desc(a0 + pa * TILE_A + j * a_kstep, a_lbo, a_sbo);
+              const uint64_t bd = umma_desc(b0 + breg + j * b_kstep, b_lbo, b_sbo);
+              const bool fresh = ks == s0 && j == 0 && q < L::FRESH;
+              tc_mma_i8_pair(tmem_base + ac * rpc, ad, bd, wide ? idesc2 : idesc1,
+                             fresh ? 0u : 1u);
+            }
+          }
+          tc_commit_pair(bar_empty + 8 * stage, 3);     // frees the slot in both CTAs
+          if (++stage == NST) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_pair(bar_tfull, 3);                   // accumulators complete in both CTAs
+        ++nunit;
+      }
+    } else if (lane == 0) {
+      // ===================== relay (CTA 1): my stage is full -> leader =====================
+      const uint32_t peer0 = mapa_shared(bar_peer, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cid; u < p.num_units; u += ncl) {
+        int pt, s0, s1, split;
+        unit_range(p, u, pt, s0, s1, split);
+        for (int ks = s0; ks < s1; ++ks) {
+          mbar_wait(bar_full + 8 * stage, phase);
+          mbar_arrive_cluster(peer0 + 8 * stage);
+          if (++stage == NST) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ===================== epilogue (both CTAs): exact int32 -> fp64 of my 128 rows ==========
+    const int e = warp - 2;
+    const int q = warp & 3;
+    const int hcol = e >> 2;
+    const int row_in_tile = 32 * q + lane;
+    const uint32_t tempty0 = mapa_shared(bar_tempty, 0);
+    uint32_t nunit = 0;
+    for (int u = cid; u < p.num_units; u += ncl) {
+      int pt, s0, s1, split;
+      unit_range(p, u, pt, s0, s1, split);
+      if (s1 <= s0) continue;
+      mbar_wait_sleep(bar_tfull, nunit & 1);     // commit from the leader's tensor core
+      tc_fence_after();
+      const int tile = 2 * pt + (int)rank;
+      const int64_t row = (int64_t)tile * BM + row_in_tile;
+      const bool store = tile < p.tiles && row < p.out_rows;
+      double* o = p.out + (int64_t)split * p.split_stride + row * p.out_ld;
+      const uint32_t lane_addr = tmem_base + ((uint32_t)(32 * q) << 16);
+#pragma unroll 1
+      for (int h = 0; h < 4; ++h) {
+        const int c0 = 64 * hcol + 16 * h;
+        if (c0 >= p.rp) break;
+        uint32_t v[NCLS][16];
+#pragma unroll
+        for (int c = 0; c < NCLS; ++c) TMEM_LD16(lane_addr + c * p.rp + c0, v[c]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (store) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int col = c0 + i;
+            if (col < p.r) {
+              double acc = 0.0;
+#pragma unroll
+              for (int c = NCLS - 1; c >= 0; --c)
+                acc = acc * 0x1p-7 + (double)(int)v[c][i];
+              o[col] = acc * p.colscale[col];
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0);
+      ++nunit;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
 // ------------------------------------------------------------------ packing
 
 // X (rows x n, ld) * sx -> 4 digit planes of [Mt][tiles_per_row] tiles.  One thread writes one
@@ -319,7 +536,10 @@ __global__ void pack_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t 
     }
     const int64_t mt = i / BM, g = (i % BM) / 8, ri = i % 8;
     const int64_t kt = j0 / BK, kc = (j0 % BK) / 16;
-    const int64_t idx = ((mt * tiles_per_row + kt) * TILE_A + (kc * 16 + g) * 128 + ri * 16) / 16;
+    // planes interleaved per tile: tile t, plane pl at (t * PLANES + pl) * TILE_A (p_pl = base +
+    // pl * TILE_A), so one stage's planes are one contiguous bulk copy
+    const int64_t idx =
+        ((mt * tiles_per_row + kt) * PLANES * TILE_A + (kc * 16 + g) * 128 + ri * 16) / 16;
     p0[idx] = *reinterpret_cast<uint4*>(d[0]);
     p1[idx] = *reinterpret_cast<uint4*>(d[1]);
     p2[idx] = *reinterpret_cast<uint4*>(d[2]);
@@ -352,7 +572,7 @@ pack_xt_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n
 #pragma unroll
         for (int pl = 0; pl < 4; ++pl) d[pl][k] = q.d[pl];
       }
-      const int64_t idx = (t * TILE_A) / 16 + w;
+      const int64_t idx = (t * PLANES * TILE_A) / 16 + w;   // planes interleaved per tile
       p0[idx] = *reinterpret_cast<uint4*>(d[0]);
       p1[idx] = *reinterpret_cast<uint4*>(d[1]);
       p2[idx] = *reinterpret_cast<uint4*>(d[2]);
@@ -393,7 +613,7 @@ pack_factor_kernel(const float* __restrict__ F, int64_t ldf, int64_t K, int r, i
 #pragma unroll
         for (int pl = 0; pl < 4; ++pl) d[pl][k] = q.d[pl];
       }
-      const int64_t idx = kt * chunks + w;
+      const int64_t idx = kt * PLANES * chunks + w;       // planes interleaved per stage
       p0[idx] = *reinterpret_cast<uint4*>(d[0]);
       p1[idx] = *reinterpret_cast<uint4*>(d[1]);
       p2[idx] = *reinterpret_cast<uint4*>(d[2]);
@@ -471,6 +691,8 @@ struct TcState {
   double* colscale = nullptr;  // r
   double* partial = nullptr;   // ksplit2 x n x r  (pass 2)  /  ksplit1 x rows x r (pass 1)
   int ksplit1 = 1, ksplit2 = 1;
+  bool pair = false;           // cta_group::2 kernel (ENMF_TC_PAIR=1 enables)
+  int ksplit1p = 1, ksplit2p = 1;
   int pass1_classes = 3;       // ENMF_TC_PASS1_CLASSES=4 for the full-precision pass 1
   int sms = kSMs;
 };
@@ -481,11 +703,9 @@ bool tc_supported(int64_t rows, int64_t n, int64_t r) {
 
 void tc_destroy(TcState* s) {
   if (!s) return;
-  for (int p = 0; p < PLANES; ++p) {
-    if (s->xp[p]) cudaFree(s->xp[p]);
-    if (s->xtp[p]) cudaFree(s->xtp[p]);
-    if (s->fp[p]) cudaFree(s->fp[p]);
-  }
+  if (s->xp[0]) cudaFree(s->xp[0]);     // planes 1..3 point into the same allocation
+  if (s->xtp[0]) cudaFree(s->xtp[0]);
+  if (s->fp[0]) cudaFree(s->fp[0]);
   void* bufs[] = {s->maxbits, s->fscale, s->colscale, s->partial};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -526,14 +746,32 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   if (s->tiles_per_row * BK > MAX_UNIT_K || s->Mt < s->sms)
     s->ksplit1 = choose_split(s->Mt, s->tiles_per_row, s->sms);
   s->ksplit2 = choose_split(s->tiles_per_row / 2, s->Kt2, s->sms);
+  {
+    // cta_group::2 kernel: correct, but measured slower than the single-CTA kernel at C5
+    // (DESIGN.md §5.1); ENMF_TC_PAIR=1 selects it
+    const char* ev = getenv("ENMF_TC_PAIR");
+    s->pair = ev && atoi(ev) == 1 && s->sms >= 2;
+    const int64_t pairs1 = (s->Mt + 1) / 2, pairs2 = (s->tiles_per_row / 2 + 1) / 2;
+    s->ksplit1p = 1;
+    if (s->tiles_per_row * BK > MAX_UNIT_K || pairs1 < s->sms / 2)
+      s->ksplit1p = choose_split(pairs1, s->tiles_per_row, s->sms / 2);
+    s->ksplit2p = choose_split(pairs2, s->Kt2, s->sms / 2);
+  }
   const size_t plane = (size_t)s->Mt * s->tiles_per_row * TILE_A;
   const int64_t fK = std::max<int64_t>(s->tiles_per_row, s->Kt2);
   const size_t fplane = (size_t)fK * s->rp * BK;
-  const size_t part = std::max<size_t>((size_t)s->ksplit2 * n * r,
-                                       s->ksplit1 > 1 ? (size_t)s->ksplit1 * rows * r : 0);
+  const size_t part = std::max<size_t>(
+      (size_t)std::max(s->ksplit2, s->ksplit2p) * n * r,
+      std::max(s->ksplit1, s->ksplit1p) > 1 ? (size_t)std::max(s->ksplit1, s->ksplit1p) * rows * r
+                                             : 0);
   cudaError_t e = cudaSuccess;
-  for (int p = 0; p < PLANES && !e; ++p) e = cudaMalloc(&s->xp[p], plane);
-  for (int p = 0; p < PLANES && !e; ++p) e = cudaMalloc(&s->fp[p], fplane);
+  // one allocation per packed copy; planes interleaved per tile (plane p at + p * tile bytes)
+  e = cudaMalloc(&s->xp[0], PLANES * plane);
+  if (!e) e = cudaMalloc(&s->fp[0], PLANES * fplane);
+  for (int p = 1; p < PLANES && !e; ++p) {
+    s->xp[p] = s->xp[0] + p * TILE_A;
+    s->fp[p] = s->fp[0] + p * (size_t)s->rp * BK;
+  }
   if (!e) e = cudaMalloc(&s->maxbits, sizeof(unsigned) * (r + 1));
   if (!e) e = cudaMalloc(&s->fscale, sizeof(double) * r);
   if (!e) e = cudaMalloc(&s->colscale, sizeof(double) * r);
@@ -568,15 +806,11 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     const bool want = !(ev && atoi(ev) == 0) && free_b > PLANES * plane + ((size_t)8 << 30);
-    for (int p = 0; p < PLANES && want; ++p)
-      if (cudaMalloc(&s->xtp[p], plane) != cudaSuccess) {
-        cudaGetLastError();
-        for (int q = 0; q < PLANES; ++q) {
-          if (s->xtp[q]) cudaFree(s->xtp[q]);
-          s->xtp[q] = nullptr;
-        }
-        break;
-      }
+    if (want && cudaMalloc(&s->xtp[0], PLANES * plane) != cudaSuccess) {
+      cudaGetLastError();
+      s->xtp[0] = nullptr;
+    }
+    for (int p = 1; p < PLANES && s->xtp[0]; ++p) s->xtp[p] = s->xtp[0] + p * TILE_A;
     if (s->xtp[0]) {
       const int64_t jt = s->tiles_per_row / 2;
       pack_xt_kernel<<<8 * s->sms, 256, 0, st>>>(X, ldx, rows, n, s->sx, jt, s->Kt2,
@@ -605,9 +839,9 @@ static void pack_factor(TcState* s, const float* F, int64_t ldf, int64_t K, int6
   count_launch(3);
 }
 
-static int launch_gemm(TcState* s, int mode, double* out, int64_t out_ld, int64_t split_stride,
-                       int tiles, int ksplit, int stages_total, int64_t out_rows,
-                       cudaStream_t st) {
+static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out_ld,
+                       int64_t split_stride, int tiles, int ksplit, int stages_total,
+                       int64_t out_rows, cudaStream_t st) {
   Params p;
   for (int q = 0; q < PLANES; ++q) {
     p.xp[q] = s->xp[q];
@@ -620,7 +854,8 @@ static int launch_gemm(TcState* s, int mode, double* out, int64_t out_ld, int64_
   p.split_stride = split_stride;
   p.colscale = s->colscale;
   p.mode = mode;
-  p.num_units = tiles * ksplit;
+  p.tiles = tiles;
+  p.num_units = (pair ? (tiles + 1) / 2 : tiles) * ksplit;
   p.ksplit = ksplit;
   p.stages_total = stages_total;
   p.tiles_per_row = s->tiles_per_row;
@@ -631,16 +866,29 @@ static int launch_gemm(TcState* s, int mode, double* out, int64_t out_ld, int64_
   if (!attr) {
     cudaFuncSetAttribute(tc_i8_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(tc_i8_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(tc_i8_pair_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         PAIR_SMEM);
+    cudaFuncSetAttribute(tc_i8_pair_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         PAIR_SMEM);
     attr = true;
   }
-  const int grid = std::min(p.num_units, s->sms);
   // P = X V only feeds the U-block update: 3 digit planes (weight classes <= 2, ~2e-8
   // relative); Q = X^T U also feeds the trace-form objective, whose conditioning needs all
   // 4 planes (classes <= 3, ~5e-10 relative)  -- DESIGN.md §5
-  if (s->pass1_classes == 3 && mode == 0)
-    tc_i8_kernel<3><<<grid, THREADS, SMEM_BYTES, st>>>(p);
-  else
-    tc_i8_kernel<4><<<grid, THREADS, SMEM_BYTES, st>>>(p);
+  const bool three = s->pass1_classes == 3 && mode == 0;
+  if (pair) {
+    const int grid = 2 * std::min(p.num_units, s->sms / 2);
+    if (three)
+      tc_i8_pair_kernel<3><<<grid, THREADS, PAIR_SMEM, st>>>(p);
+    else
+      tc_i8_pair_kernel<4><<<grid, THREADS, PAIR_SMEM, st>>>(p);
+  } else {
+    const int grid = std::min(p.num_units, s->sms);
+    if (three)
+      tc_i8_kernel<3><<<grid, THREADS, SMEM_BYTES, st>>>(p);
+    else
+      tc_i8_kernel<4><<<grid, THREADS, SMEM_BYTES, st>>>(p);
+  }
   count_launch();
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
@@ -648,12 +896,14 @@ static int launch_gemm(TcState* s, int mode, double* out, int64_t out_ld, int64_
 int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st) {
   // B = V (K = n), over all 64-column stages of X
   pack_factor(s, V, ldv, s->n, s->tiles_per_row, st);
-  if (s->ksplit1 == 1)
-    return launch_gemm(s, 0, P, s->r, 0, (int)s->Mt, 1, (int)s->tiles_per_row, s->rows, st);
-  if (launch_gemm(s, 0, s->partial, s->r, s->rows * s->r, (int)s->Mt, s->ksplit1,
+  const bool pair = s->pair;
+  const int ks = pair ? s->ksplit1p : s->ksplit1;
+  if (ks == 1)
+    return launch_gemm(s, 0, pair, P, s->r, 0, (int)s->Mt, 1, (int)s->tiles_per_row, s->rows, st);
+  if (launch_gemm(s, 0, pair, s->partial, s->r, s->rows * s->r, (int)s->Mt, ks,
                   (int)s->tiles_per_row, s->rows, st))
     return 1;
-  reduce_parts(s->partial, s->ksplit1, s->rows * s->r, P, st);
+  reduce_parts(s->partial, ks, s->rows * s->r, P, st);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -661,10 +911,12 @@ int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st) 
   // B = U (K = rows of X), split-K partials reduced in a fixed order
   pack_factor(s, U, ldu, s->rows, s->Kt2, st);
   const int mode = s->xtp[0] ? 2 : 1;
-  if (launch_gemm(s, mode, s->partial, s->r, s->n * s->r, (int)(s->tiles_per_row / 2), s->ksplit2,
+  const bool pair = s->pair && mode == 2;   // the pair kernel reads K-major A only
+  const int ks = pair ? s->ksplit2p : s->ksplit2;
+  if (launch_gemm(s, mode, pair, s->partial, s->r, s->n * s->r, (int)(s->tiles_per_row / 2), ks,
                   (int)s->Kt2, s->n, st))
     return 1;
-  reduce_parts(s->partial, s->ksplit2, s->n * s->r, Q, st);
+  reduce_parts(s->partial, ks, s->n * s->r, Q, st);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

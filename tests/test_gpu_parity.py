@@ -252,13 +252,17 @@ def test_objective_and_kkt(cfg, prec):
         assert abs(k[key] - ko[key]) <= rtol * max(abs(ko[key]), 1e-300) + 1e-12 * ko["xnorm2"], key
 
 
+@pytest.mark.parametrize("pair", ["0", "1"], ids=["cta1", "cta2"])
 @pytest.mark.parametrize("signed", [False, True], ids=["nonneg", "signed"])
 @pytest.mark.parametrize("cfg", TC_CASES, ids=TC_IDS)
-def test_tc_contractions_match_oracle(cfg, signed):
+def test_tc_contractions_match_oracle(cfg, signed, pair, monkeypatch):
     """The tensor-core X passes (int8 digit planes, exact int32 TMEM accumulation) element by
     element against the oracle's fp64 X V and X^T U.  Error budget: digit truncation <= 2^-15
     of the operand's scale per entry (unbiased), so |err| <= ~1e-6 |X||V| entrywise and the
-    normwise error is ~1e-8."""
+    normwise error is ~1e-8.  pair=1 runs the cta_group::2 kernel (ENMF_TC_PAIR, read when X is
+    bound); the shapes include odd 128-row tile counts, whose missing pair partner is not
+    stored."""
+    monkeypatch.setenv("ENMF_TC_PAIR", pair)
     h, X, _ = make(cfg, precision=TC)
     assert h.precision.startswith("tc")
     g = np.random.default_rng(3)
