@@ -131,21 +131,33 @@ enmf_status_t svd_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t
   gaussian_fill(Om, n, l, h->opt.seed, h->st);
   GemmOut o;
   o.ldc = l;
-  o.C = Y;
-  gemm<float, double>(false, h->X, h->ldx, Om, l, mr, l, n, o, h->work, h->work_elems, h->st);
+  // the 2q + 2 X passes: on the tensor-core path as exact int8-digit products in blocks of
+  // <= 128 columns (tc_xf, ~1e-9 relative), else the SIMT fp64-accumulating GEMM
+  auto xprod = [&](bool trans, const double* F, double* out) -> enmf_status_t {
+    if (h->tc) {
+      const int rc = tc_xf(h->tc, trans, F, l, l, out, l, h->st);
+      return rc == 0 ? ENMF_OK : (rc == 2 ? ENMF_ERR_OOM : ENMF_ERR_CUDA);
+    }
+    GemmOut oo;
+    oo.ldc = l;
+    oo.C = out;
+    if (trans)
+      gemm<float, double>(true, h->X, h->ldx, F, l, n, l, mr, oo, h->work, h->work_elems, h->st);
+    else
+      gemm<float, double>(false, h->X, h->ldx, F, l, mr, l, n, oo, h->work, h->work_elems, h->st);
+    return ENMF_OK;
+  };
+  ENMF_TRY(xprod(false, Om, Y));                                     // Y = X Omega
   ENMF_TRY(cholqr(h, Y, tmp, mr, l, sh, G, R, Rinv, bad));
   for (int q = 0; q < h->opt.power_iters; ++q) {
-    o.C = Z;
-    gemm<float, double>(true, h->X, h->ldx, Y, l, n, l, mr, o, h->work, h->work_elems, h->st);
+    ENMF_TRY(xprod(true, Y, Z));                                     // Z = X^T Q
     ENMF_TRY(ar(h, Z, (size_t)(n * l), CommOp::Sum));
     ENMF_TRY(cholqr(h, Z, tmp, n, l, false, G, R, Rinv, bad));
-    o.C = Y;
-    gemm<float, double>(false, h->X, h->ldx, Z, l, mr, l, n, o, h->work, h->work_elems, h->st);
+    ENMF_TRY(xprod(false, Z, Y));                                    // Y = X Z
     ENMF_TRY(cholqr(h, Y, tmp, mr, l, sh, G, R, Rinv, bad));
   }
   // B^T = X^T Q (n x l); B B^T = Qt^T Qt = Ve diag(s) Ve^T; sigma = sqrt(s)
-  o.C = Qt;
-  gemm<float, double>(true, h->X, h->ldx, Y, l, n, l, mr, o, h->work, h->work_elems, h->st);
+  ENMF_TRY(xprod(true, Y, Qt));
   ENMF_TRY(ar(h, Qt, (size_t)(n * l), CommOp::Sum));
   o.C = G;
   gemm<double, double>(true, Qt, l, Qt, l, l, l, n, o, h->work, h->work_elems, h->st);
@@ -273,7 +285,8 @@ enmf_status_t rotate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int6
       ENMF_TRY(ar(h, M, (size_t)r * r, CommOp::Sum));
     }
     // R = C D^T from W^T B = C S D^T (orthogonal Procrustes)
-    jacobi_svd(M, r, Cs, sv, Ds, jw, h->st);
+    // warm start from the previous step's right singular vectors (t > 0)
+    jacobi_svd(M, r, Cs, sv, Ds, jw, h->st, t > 0 ? Ds : nullptr);
     procrustes_from_svd(Cs, sv, Ds, r, R, h->st);
   }
   ENMF_TRY(check_launch());

@@ -91,12 +91,13 @@ void frob_direct(const float* X, int64_t ldx, int64_t rows, int64_t n, const flo
 void chol_inv(const double* G, int k, double shift_rel, double* R, double* Rinv, int* bad,
               cudaStream_t st);
 // One-sided Jacobi SVD of a k x k matrix A (row-major): A = U diag(s) V^T, s descending.
-// Uo, Vo are k x k row-major.  work >= 2*k*k doubles.
+// Uo, Vo are k x k row-major.  work >= 2*k*k doubles.  J0 (k x k row-major orthogonal, may be
+// null): warm start, the rotations are accumulated onto J0 (B = A J0 initially).
 void jacobi_svd(const double* A, int k, double* Uo, double* s, double* Vo, double* work,
-                cudaStream_t st);
+                cudaStream_t st, const double* J0 = nullptr);
 // R = C D^T from the SVD W^T B = C S D^T (orthogonal Procrustes), completing C's basis
-// for zero singular values.
-void procrustes_from_svd(const double* Cm, const double* s, const double* Dm, int k, double* R,
+// (in place) for zero singular values.
+void procrustes_from_svd(double* Cm, const double* s, const double* Dm, int k, double* R,
                          cudaStream_t st);
 
 // ---------------------------------------------------------------- stage / scalars

@@ -254,30 +254,103 @@ chol_inv_kernel(const double* __restrict__ G, int k, double shift_rel, double* R
 }
 
 // One-sided (Hestenes) Jacobi SVD of a k x k matrix, parallel round-robin pair ordering.
-// work: B (k x k column-major) and J (k x k column-major).
+// B = A J is orthogonalised column-pairwise; J accumulates the rotations (J = J0 or I at start).
+// A warm start J0 (the previous ADMM step's D: consecutive Procrustes matrices differ little)
+// leaves B nearly column-orthogonal, so 1-3 sweeps replace ~8 from the identity.  B lives in
+// shared memory when k <= 128 (128 KB), J in `work`.
 __global__ void __launch_bounds__(1024)
-jacobi_svd_kernel(const double* __restrict__ A, int k, double* Uo, double* s, double* Vo,
-                  double* work) {
-  double* B = work;               // column c at B + c*k
+jacobi_svd_kernel(const double* __restrict__ A, int k, const double* J0,
+                  double* Uo, double* s, double* Vo, double* work) {
+  extern __shared__ double smB[];
+  const bool in_smem = k <= 128;
+  double* B = in_smem ? smB : work;               // column c at B + c*k
   double* J = work + (int64_t)k * k;
   __shared__ int rotated;
   __shared__ double nrm[512];
   __shared__ int ord[512];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int i = e / k, c = e % k;             // A row-major (i, c); J column-major
+    J[c * k + i] = J0 ? J0[i * k + c] : (i == c ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
     const int i = e / k, c = e % k;
-    B[c * k + i] = A[e];
-    J[c * k + i] = (i == c) ? 1.0 : 0.0;
+    double acc;
+    if (J0) {
+      acc = 0.0;                                  // B = A J0
+      for (int l = 0; l < k; ++l) acc = fma(A[i * k + l], J[c * k + l], acc);
+    } else {
+      acc = A[e];
+    }
+    B[c * k + i] = acc;
   }
   const int kk = (k + 1) & ~1;      // even number of players (one dummy if k is odd)
+  const double tol = 2.0 * sqrt((double)k) * DBL_EPSILON;
   __syncthreads();
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (threadIdx.x == 0) rotated = 0;
     __syncthreads();
     for (int rd = 0; rd < kk - 1; ++rd) {
+      // round-robin: player 0 fixed, others rotate ((x - 1 + rd) < 2 (kk - 1): no modulo)
+      auto pos = [&](int x) {
+        if (x == 0) return 0;
+        int v = x - 1 + rd;
+        if (v >= kk - 1) v -= kk - 1;
+        return 1 + v;
+      };
+      if (in_smem) {
+        // k <= 128: every load of a pair (B in shared memory, J in global) is issued before the
+        // dependent arithmetic, so a pair costs one L2 round trip instead of a chain of four
+        for (int pr = warp; pr < kk / 2; pr += nw) {
+          int p = pos(pr), q = pos(kk - 1 - pr);
+          if (p > q) { const int t = p; p = q; q = t; }
+          if (q >= k) continue;
+          double bp[4], bq[4], jp[4], jq[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int i = lane + 32 * t;
+            const bool ok = i < k;
+            bp[t] = ok ? B[p * k + i] : 0.0;
+            bq[t] = ok ? B[q * k + i] : 0.0;
+            jp[t] = ok ? J[p * k + i] : 0.0;
+            jq[t] = ok ? J[q * k + i] : 0.0;
+          }
+          double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            al += bp[t] * bp[t];
+            be += bq[t] * bq[t];
+            ga += bp[t] * bq[t];
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            al += __shfl_xor_sync(0xffffffffu, al, o);
+            be += __shfl_xor_sync(0xffffffffu, be, o);
+            ga += __shfl_xor_sync(0xffffffffu, ga, o);
+          }
+          if (ga == 0.0 || ga * ga <= tol * tol * (al * be)) continue;
+          // rotation angle (Rutishauser): zeta = (be - al) / (2 ga), t = sign / (|zeta| +
+          // sqrt(1 + zeta^2)), c = 1 / sqrt(1 + t^2), s = c t
+          const double zeta = (be - al) * (0.5 / ga);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = lane + 32 * u;
+            if (i < k) {
+              B[p * k + i] = c * bp[u] - sn * bq[u];
+              B[q * k + i] = sn * bp[u] + c * bq[u];
+              J[p * k + i] = c * jp[u] - sn * jq[u];
+              J[q * k + i] = sn * jp[u] + c * jq[u];
+            }
+          }
+          if (lane == 0) rotated = 1;
+        }
+        __syncthreads();
+        continue;
+      }
       for (int pr = warp; pr < kk / 2; pr += nw) {
-        // round-robin: player 0 fixed, others rotate
-        auto pos = [&](int x) { return x == 0 ? 0 : 1 + (x - 1 + rd) % (kk - 1); };
         int p = pos(pr), q = pos(kk - 1 - pr);
         if (p > q) { const int t = p; p = q; q = t; }
         if (q >= k) continue;
@@ -286,16 +359,24 @@ jacobi_svd_kernel(const double* __restrict__ A, int k, double* Uo, double* s, do
           const double bp = B[p * k + i], bq = B[q * k + i];
           al += bp * bp; be += bq * bq; ga += bp * bq;
         }
-        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-        if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {        // three independent butterflies
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        // converged pair: |cos| at the rounding level of a length-k dot product (2 sqrt(k) eps,
+        // as LAPACK's one-sided Jacobi uses sqrt(m) eps); a fixed 1e-15 sits below that noise
+        // for k >= ~64 and kept every sweep rotating until the 60-sweep cap
+        if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
         const double zeta = (be - al) / (2.0 * ga);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
         for (int i = lane; i < k; i += 32) {
           const double bp = B[p * k + i], bq = B[q * k + i];
+          const double jp = J[p * k + i], jq = J[q * k + i];
           B[p * k + i] = c * bp - sn * bq;
           B[q * k + i] = sn * bp + c * bq;
-          const double jp = J[p * k + i], jq = J[q * k + i];
           J[p * k + i] = c * jp - sn * jq;
           J[q * k + i] = sn * jp + c * jq;
         }
@@ -331,37 +412,42 @@ jacobi_svd_kernel(const double* __restrict__ A, int k, double* Uo, double* s, do
   for (int a = threadIdx.x; a < k; a += blockDim.x) s[a] = nrm[ord[a]];
 }
 
-// R = C D^T; columns of C with s = 0 are completed to an orthonormal basis first.
-__global__ void procrustes_kernel(double* Cm, const double* __restrict__ s,
-                                  const double* __restrict__ Dm, int k, double* R) {
-  if (threadIdx.x == 0) {
-    for (int a = 0; a < k; ++a) {
-      if (s[a] > 0.0) continue;
-      for (int e = 0; e < k; ++e) {
-        for (int i = 0; i < k; ++i) Cm[i * k + a] = (i == e) ? 1.0 : 0.0;
-        for (int pass = 0; pass < 2; ++pass)
-          for (int b = 0; b < k; ++b) {
-            if (b == a || (s[b] <= 0.0 && b > a)) continue;
-            double d = 0.0;
-            for (int i = 0; i < k; ++i) d += Cm[i * k + b] * Cm[i * k + a];
-            for (int i = 0; i < k; ++i) Cm[i * k + a] -= d * Cm[i * k + b];
-          }
-        double t = 0.0;
-        for (int i = 0; i < k; ++i) t += Cm[i * k + a] * Cm[i * k + a];
-        if (t > 1e-6) {
-          t = sqrt(t);
-          for (int i = 0; i < k; ++i) Cm[i * k + a] /= t;
-          break;
+// Columns of C with s = 0 are completed to an orthonormal basis (rank-deficient M only).
+__global__ void complete_basis_kernel(double* Cm, const double* __restrict__ s, int k) {
+  if (threadIdx.x != 0) return;
+  for (int a = 0; a < k; ++a) {
+    if (s[a] > 0.0) continue;
+    for (int e = 0; e < k; ++e) {
+      for (int i = 0; i < k; ++i) Cm[i * k + a] = (i == e) ? 1.0 : 0.0;
+      for (int pass = 0; pass < 2; ++pass)
+        for (int b = 0; b < k; ++b) {
+          if (b == a || (s[b] <= 0.0 && b > a)) continue;
+          double d = 0.0;
+          for (int i = 0; i < k; ++i) d += Cm[i * k + b] * Cm[i * k + a];
+          for (int i = 0; i < k; ++i) Cm[i * k + a] -= d * Cm[i * k + b];
         }
+      double t = 0.0;
+      for (int i = 0; i < k; ++i) t += Cm[i * k + a] * Cm[i * k + a];
+      if (t > 1e-6) {
+        t = sqrt(t);
+        for (int i = 0; i < k; ++i) Cm[i * k + a] /= t;
+        break;
       }
     }
   }
+}
+
+// R = C D^T: block a computes row a (C row staged in shared memory).
+__global__ void procrustes_kernel(const double* __restrict__ Cm, const double* __restrict__ Dm,
+                                  int k, double* R) {
+  __shared__ double crow[512];
+  const int a = blockIdx.x;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) crow[c] = Cm[a * k + c];
   __syncthreads();
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-    const int a = e / k, b = e % k;
+  for (int b = threadIdx.x; b < k; b += blockDim.x) {
     double acc = 0.0;
-    for (int c = 0; c < k; ++c) acc += Cm[a * k + c] * Dm[b * k + c];
-    R[e] = acc;
+    for (int c = 0; c < k; ++c) acc = fma(crow[c], Dm[b * k + c], acc);
+    R[a * k + b] = acc;
   }
 }
 
@@ -448,15 +534,23 @@ void chol_inv(const double* G, int k, double shift_rel, double* R, double* Rinv,
 }
 
 void jacobi_svd(const double* A, int k, double* Uo, double* s, double* Vo, double* work,
-                cudaStream_t st) {
-  jacobi_svd_kernel<<<1, 1024, 0, st>>>(A, k, Uo, s, Vo, work);
+                cudaStream_t st, const double* J0) {
+  const size_t sm = k <= 128 ? sizeof(double) * k * k : 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * 128 * 128));
+    attr = true;
+  }
+  jacobi_svd_kernel<<<1, 1024, sm, st>>>(A, k, J0, Uo, s, Vo, work);
   count_launch();
 }
 
-void procrustes_from_svd(const double* Cm, const double* s, const double* Dm, int k, double* R,
+void procrustes_from_svd(double* Cm, const double* s, const double* Dm, int k, double* R,
                          cudaStream_t st) {
-  procrustes_kernel<<<1, 256, 0, st>>>(const_cast<double*>(Cm), s, Dm, k, R);
-  count_launch();
+  complete_basis_kernel<<<1, 32, 0, st>>>(Cm, s, k);
+  procrustes_kernel<<<k, 128, 0, st>>>(Cm, Dm, k, R);
+  count_launch(2);
 }
 
 }  // namespace enmf

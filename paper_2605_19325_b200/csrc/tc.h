@@ -24,6 +24,11 @@ void tc_destroy(TcState* s);
 // P (rows x r fp64) = X V ; Q (n x r fp64) = X^T U  (this rank's rows only).
 int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st);
 int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st);
+// Column-block products for the randomised SVD (fp64 factors of any width):
+// out (ld ldo) = X F (F: n x ncols) or, transposed, X^T F (F: this rank's rows x ncols).
+// Returns 0, 1 (CUDA error) or 2 (OOM).
+int tc_xf(TcState* s, bool transposed, const double* F, int64_t ldf, int ncols, double* out,
+          int64_t ldo, cudaStream_t st);
 
 // Alg. 2 PBCD on the tensor cores: same contract as pbcd_rows (kernels_rows.cu); pgparts holds
 // tc_pbcd_parts() x (max_iter + 1) partials; gd_work >= 4*128*128 bytes, gscale_work >= 128.

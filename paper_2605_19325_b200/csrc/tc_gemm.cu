@@ -586,18 +586,20 @@ pack_xt_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n
 // F[kt*64 + kc*16 + 0..15][g*8 + ri] with g = w/32, kc = (w/8)%4, ri = w%8, i.e. byte
 // (g*4 + kc)*128 + ri*16.  A block stages 64 factor rows in shared memory so global reads are
 // coalesced.
+template <typename T>
 __global__ void __launch_bounds__(256)
-pack_factor_kernel(const float* __restrict__ F, int64_t ldf, int64_t K, int r, int rp,
+pack_factor_kernel(const T* __restrict__ F, int64_t ldf, int64_t K, int r, int rp,
                    const double* __restrict__ fscale, int64_t Kt, uint4* p0, uint4* p1, uint4* p2,
                    uint4* p3) {
-  __shared__ float tileF[BK][129];
+  extern __shared__ __align__(16) unsigned char pf_smem[];
+  T(*tileF)[129] = reinterpret_cast<T(*)[129]>(pf_smem);   // BK x 129
   const int gpt = rp / 8;
   const int chunks = 4 * gpt * 8;                        // 16-byte chunks per tile per plane
   for (int64_t kt = blockIdx.x; kt < Kt; kt += gridDim.x) {
     for (int e = threadIdx.x; e < BK * rp; e += blockDim.x) {
       const int kk = e / rp, col = e % rp;
       const int64_t row = kt * BK + kk;
-      tileF[kk][col] = (row < K && col < r) ? F[row * ldf + col] : 0.0f;
+      tileF[kk][col] = (row < K && col < r) ? F[row * ldf + col] : (T)0;
     }
     __syncthreads();
     for (int w = threadIdx.x; w < chunks; w += blockDim.x) {
@@ -623,21 +625,34 @@ pack_factor_kernel(const float* __restrict__ F, int64_t ldf, int64_t K, int r, i
   }
 }
 
-// Per-column max |F| (F rows x r) into maxbits[r] (float bits; max is order independent).
-__global__ void colmax_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
-                              unsigned* maxbits) {
-  __shared__ unsigned m[128];
-  for (int k = threadIdx.x; k < r; k += blockDim.x) m[k] = 0u;
+// Per-column max |F| (F rows x r) into maxbits[r] (bits of the fp64 |value|: non-negative
+// doubles order like their bit patterns, so the max is order independent).
+template <typename T>
+__global__ void colmax_kernel(const T* __restrict__ F, int64_t ldf, int64_t rows, int r,
+                              unsigned long long* maxbits) {
+  __shared__ unsigned long long m[128];
+  for (int k = threadIdx.x; k < r; k += blockDim.x) m[k] = 0ull;
   __syncthreads();
   const int64_t total = rows * (int64_t)r;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / r;
     const int k = (int)(e - i * r);
-    atomicMax(&m[k], __float_as_uint(fabsf(F[i * ldf + k])));
+    atomicMax(&m[k], (unsigned long long)__double_as_longlong(fabs((double)F[i * ldf + k])));
   }
   __syncthreads();
   for (int k = threadIdx.x; k < r; k += blockDim.x) atomicMax(&maxbits[k], m[k]);
+}
+
+// out[i, c0 + j] = buf[i, j] (rows x nb contiguous -> column block of a row-major ldo matrix)
+__global__ void scatter_cols_kernel(const double* __restrict__ buf, int64_t rows, int nb,
+                                    double* out, int64_t ldo, int c0) {
+  const int64_t total = rows * nb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / nb;
+    out[i * ldo + c0 + (e - i * nb)] = buf[e];
+  }
 }
 
 // Power of two s with mx * s in [32, 64) (1 for mx = 0).
@@ -649,10 +664,10 @@ __host__ __device__ inline double pow2_scale(double mx) {
 }
 
 // fscale[k] = power of two with max|F_k| fscale in [32, 64); colscale[k] = 1/(sx fscale[k]).
-__global__ void scales_kernel(const unsigned* maxbits, int r, double sx, double* fscale,
+__global__ void scales_kernel(const unsigned long long* maxbits, int r, double sx, double* fscale,
                               double* colscale) {
   for (int k = threadIdx.x; k < r; k += blockDim.x) {
-    const double s = pow2_scale((double)__uint_as_float(maxbits[k]));
+    const double s = pow2_scale(__longlong_as_double((long long)maxbits[k]));
     fscale[k] = s;
     colscale[k] = 1.0 / (sx * s);
   }
@@ -686,9 +701,11 @@ struct TcState {
   int8_t* xp[PLANES] = {nullptr, nullptr, nullptr, nullptr};
   int8_t* xtp[PLANES] = {nullptr, nullptr, nullptr, nullptr};   // X^T copy (pass 2), optional
   int8_t* fp[PLANES] = {nullptr, nullptr, nullptr, nullptr};
-  unsigned* maxbits = nullptr; // r + 1
-  double* fscale = nullptr;    // r
-  double* colscale = nullptr;  // r
+  unsigned* maxbits = nullptr; // X max (float bits)
+  unsigned long long* fmaxbits = nullptr;   // 128 factor column maxima (fp64 bits)
+  double* fscale = nullptr;    // 128
+  double* colscale = nullptr;  // 128
+  double* colbuf = nullptr;    // max(rows, n) x 128: column-block products (tc_xf), lazy
   double* partial = nullptr;   // ksplit2 x n x r  (pass 2)  /  ksplit1 x rows x r (pass 1)
   int ksplit1 = 1, ksplit2 = 1;
   bool pair = false;           // cta_group::2 kernel (ENMF_TC_PAIR=1 enables)
@@ -706,7 +723,7 @@ void tc_destroy(TcState* s) {
   if (s->xp[0]) cudaFree(s->xp[0]);     // planes 1..3 point into the same allocation
   if (s->xtp[0]) cudaFree(s->xtp[0]);
   if (s->fp[0]) cudaFree(s->fp[0]);
-  void* bufs[] = {s->maxbits, s->fscale, s->colscale, s->partial};
+  void* bufs[] = {s->maxbits, s->fmaxbits, s->fscale, s->colscale, s->partial, s->colbuf};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete s;
@@ -759,22 +776,24 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   }
   const size_t plane = (size_t)s->Mt * s->tiles_per_row * TILE_A;
   const int64_t fK = std::max<int64_t>(s->tiles_per_row, s->Kt2);
-  const size_t fplane = (size_t)fK * s->rp * BK;
+  const size_t fplane = (size_t)fK * 128 * BK;          // any factor block of <= 128 columns
   const size_t part = std::max<size_t>(
-      (size_t)std::max(s->ksplit2, s->ksplit2p) * n * r,
-      std::max(s->ksplit1, s->ksplit1p) > 1 ? (size_t)std::max(s->ksplit1, s->ksplit1p) * rows * r
-                                             : 0);
+      (size_t)std::max(s->ksplit2, s->ksplit2p) * n * 128,
+      std::max(s->ksplit1, s->ksplit1p) > 1
+          ? (size_t)std::max(s->ksplit1, s->ksplit1p) * rows * 128
+          : 0);
   cudaError_t e = cudaSuccess;
   // one allocation per packed copy; planes interleaved per tile (plane p at + p * tile bytes)
   e = cudaMalloc(&s->xp[0], PLANES * plane);
   if (!e) e = cudaMalloc(&s->fp[0], PLANES * fplane);
   for (int p = 1; p < PLANES && !e; ++p) {
     s->xp[p] = s->xp[0] + p * TILE_A;
-    s->fp[p] = s->fp[0] + p * (size_t)s->rp * BK;
+    s->fp[p] = nullptr;    // factor planes: fp[0] + q * rp * BK for the block's rp (per launch)
   }
-  if (!e) e = cudaMalloc(&s->maxbits, sizeof(unsigned) * (r + 1));
-  if (!e) e = cudaMalloc(&s->fscale, sizeof(double) * r);
-  if (!e) e = cudaMalloc(&s->colscale, sizeof(double) * r);
+  if (!e) e = cudaMalloc(&s->maxbits, sizeof(unsigned));
+  if (!e) e = cudaMalloc(&s->fmaxbits, sizeof(unsigned long long) * 128);
+  if (!e) e = cudaMalloc(&s->fscale, sizeof(double) * 128);
+  if (!e) e = cudaMalloc(&s->colscale, sizeof(double) * 128);
   if (!e) e = cudaMalloc(&s->partial, sizeof(double) * std::max<size_t>(part, 1));
   if (e) {
     cudaGetLastError();
@@ -827,26 +846,36 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   return 0;
 }
 
-static void pack_factor(TcState* s, const float* F, int64_t ldf, int64_t K, int64_t Kt,
-                        cudaStream_t st) {
-  const int r = (int)s->r;
-  cudaMemsetAsync(s->maxbits, 0, sizeof(unsigned) * r, st);
-  colmax_kernel<<<2 * s->sms, 256, 0, st>>>(F, ldf, K, r, s->maxbits);
-  scales_kernel<<<1, 128, 0, st>>>(s->maxbits, r, s->sx, s->fscale, s->colscale);
-  pack_factor_kernel<<<(int)std::min<int64_t>(Kt, 8 * s->sms), 256, 0, st>>>(
-      F, ldf, K, r, s->rp, s->fscale, Kt, (uint4*)s->fp[0], (uint4*)s->fp[1], (uint4*)s->fp[2],
-      (uint4*)s->fp[3]);
+// Packed factor block of rp (<= 128) padded columns: plane q of stage kt at
+// fp[0] + (kt * PLANES + q) * rp * BK.
+static int8_t* fplane(TcState* s, int q, int rp) { return s->fp[0] + (size_t)q * rp * BK; }
+
+template <typename T>
+static void pack_factor(TcState* s, const T* F, int64_t ldf, int64_t K, int64_t Kt, int ncols,
+                        int rp, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pack_factor_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(BK * 129 * sizeof(T)));
+    attr = true;
+  }
+  cudaMemsetAsync(s->fmaxbits, 0, sizeof(unsigned long long) * ncols, st);
+  colmax_kernel<T><<<2 * s->sms, 256, 0, st>>>(F, ldf, K, ncols, s->fmaxbits);
+  scales_kernel<<<1, 128, 0, st>>>(s->fmaxbits, ncols, s->sx, s->fscale, s->colscale);
+  pack_factor_kernel<T><<<(int)std::min<int64_t>(Kt, 8 * s->sms), 256, BK * 129 * sizeof(T), st>>>(
+      F, ldf, K, ncols, rp, s->fscale, Kt, (uint4*)fplane(s, 0, rp), (uint4*)fplane(s, 1, rp),
+      (uint4*)fplane(s, 2, rp), (uint4*)fplane(s, 3, rp));
   count_launch(3);
 }
 
 static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out_ld,
                        int64_t split_stride, int tiles, int ksplit, int stages_total,
-                       int64_t out_rows, cudaStream_t st) {
+                       int64_t out_rows, int ncols, int rp, cudaStream_t st) {
   Params p;
   for (int q = 0; q < PLANES; ++q) {
     p.xp[q] = s->xp[q];
     p.xtp[q] = s->xtp[q];
-    p.fp[q] = s->fp[q];
+    p.fp[q] = fplane(s, q, rp);
   }
   p.tiles_per_row_t = s->Kt2;
   p.out = out;
@@ -859,8 +888,8 @@ static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out
   p.ksplit = ksplit;
   p.stages_total = stages_total;
   p.tiles_per_row = s->tiles_per_row;
-  p.rp = s->rp;
-  p.r = (int)s->r;
+  p.rp = rp;
+  p.r = ncols;
   p.out_rows = out_rows;
   static bool attr = false;
   if (!attr) {
@@ -895,28 +924,73 @@ static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out
 
 int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st) {
   // B = V (K = n), over all 64-column stages of X
-  pack_factor(s, V, ldv, s->n, s->tiles_per_row, st);
+  const int r = (int)s->r;
+  pack_factor<float>(s, V, ldv, s->n, s->tiles_per_row, r, s->rp, st);
   const bool pair = s->pair;
   const int ks = pair ? s->ksplit1p : s->ksplit1;
   if (ks == 1)
-    return launch_gemm(s, 0, pair, P, s->r, 0, (int)s->Mt, 1, (int)s->tiles_per_row, s->rows, st);
-  if (launch_gemm(s, 0, pair, s->partial, s->r, s->rows * s->r, (int)s->Mt, ks,
-                  (int)s->tiles_per_row, s->rows, st))
+    return launch_gemm(s, 0, pair, P, r, 0, (int)s->Mt, 1, (int)s->tiles_per_row, s->rows, r,
+                       s->rp, st);
+  if (launch_gemm(s, 0, pair, s->partial, r, s->rows * r, (int)s->Mt, ks, (int)s->tiles_per_row,
+                  s->rows, r, s->rp, st))
     return 1;
-  reduce_parts(s->partial, ks, s->rows * s->r, P, st);
+  reduce_parts(s->partial, ks, s->rows * r, P, st);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st) {
   // B = U (K = rows of X), split-K partials reduced in a fixed order
-  pack_factor(s, U, ldu, s->rows, s->Kt2, st);
+  const int r = (int)s->r;
+  pack_factor<float>(s, U, ldu, s->rows, s->Kt2, r, s->rp, st);
   const int mode = s->xtp[0] ? 2 : 1;
   const bool pair = s->pair && mode == 2;   // the pair kernel reads K-major A only
   const int ks = pair ? s->ksplit2p : s->ksplit2;
-  if (launch_gemm(s, mode, pair, s->partial, s->r, s->n * s->r, (int)(s->tiles_per_row / 2), ks,
-                  (int)s->Kt2, s->n, st))
+  if (launch_gemm(s, mode, pair, s->partial, r, s->n * r, (int)(s->tiles_per_row / 2), ks,
+                  (int)s->Kt2, s->n, r, s->rp, st))
     return 1;
-  reduce_parts(s->partial, ks, s->n * s->r, Q, st);
+  reduce_parts(s->partial, ks, s->n * r, Q, st);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int tc_xf(TcState* s, bool transposed, const double* F, int64_t ldf, int ncols, double* out,
+          int64_t ldo, cudaStream_t st) {
+  const int64_t out_rows = transposed ? s->n : s->rows;
+  if (!s->colbuf) {
+    if (cudaMalloc(&s->colbuf, sizeof(double) * std::max(s->rows, s->n) * 128) != cudaSuccess) {
+      cudaGetLastError();
+      s->colbuf = nullptr;
+      return 2;
+    }
+  }
+  for (int c0 = 0; c0 < ncols; c0 += 128) {
+    const int nb = std::min(128, ncols - c0);
+    const int rp = (nb + 15) / 16 * 16;
+    int mode, tiles, ks, stages;
+    if (!transposed) {
+      pack_factor<double>(s, F + c0, ldf, s->n, s->tiles_per_row, nb, rp, st);
+      mode = 0;
+      tiles = (int)s->Mt;
+      ks = s->ksplit1;
+      stages = (int)s->tiles_per_row;
+    } else {
+      pack_factor<double>(s, F + c0, ldf, s->rows, s->Kt2, nb, rp, st);
+      mode = s->xtp[0] ? 2 : 1;
+      tiles = (int)(s->tiles_per_row / 2);
+      ks = s->ksplit2;
+      stages = (int)s->Kt2;
+    }
+    if (ks == 1) {
+      if (launch_gemm(s, mode, false, out + c0, ldo, 0, tiles, 1, stages, out_rows, nb, rp, st))
+        return 1;
+      continue;
+    }
+    if (launch_gemm(s, mode, false, s->partial, nb, out_rows * nb, tiles, ks, stages, out_rows,
+                    nb, rp, st))
+      return 1;
+    reduce_parts(s->partial, ks, out_rows * nb, s->colbuf, st);
+    scatter_cols_kernel<<<2 * s->sms, 256, 0, st>>>(s->colbuf, out_rows, nb, out, ldo, c0);
+    count_launch();
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

@@ -183,15 +183,19 @@ def test_final_objective_and_factors_c1():
 
 
 # ----------------------------------------------------------------------------- init
+@pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
 @pytest.mark.parametrize("cfg", [synth.C1, synth.C3.scaled(160, 900, 32, 32),
-                                 synth.C5.scaled(600, 500, 16, 16, name="C5-shape-r16")],
-                         ids=["C1", "C3-scaled", "C5-shape-r16"])
-def test_randomised_svd_matches_converged_svd(cfg):
+                                 synth.C5.scaled(600, 500, 16, 16, name="C5-shape-r16"),
+                                 synth.C5.scaled(700, 650, 128, 128, name="C5-shape-r128")],
+                         ids=["C1", "C3-scaled", "C5-shape-r16", "C5-shape-r128"])
+def test_randomised_svd_matches_converged_svd(cfg, prec):
     """Randomised range finder (q = 2) vs the oracle's converged subspace iteration on gapped
-    spectra: singular values and balanced factors U* = U S^1/2, V* = V S^1/2."""
+    spectra: singular values and balanced factors U* = U S^1/2, V* = V S^1/2.  prec=tc runs the
+    2q + 2 X passes as tensor-core column-block products (tc_xf; l = 138 > 128 at r = 128 takes
+    two blocks)."""
     X = synth.x_full(cfg)
     import paper_2605_19325_b200 as E
-    h = E.Enmf(cfg.m, cfg.n, cfg.r)
+    h = E.Enmf(cfg.m, cfg.n, cfg.r, precision=prec)
     h.set_data(to_dev(X))
     U = to_dev(np.zeros((cfg.m, cfg.r)))
     V = to_dev(np.zeros((cfg.n, cfg.r)))
