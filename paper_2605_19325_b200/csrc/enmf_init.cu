@@ -229,6 +229,8 @@ enmf_status_t rotate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int6
   ENMF_TRY(db.get(&sv, (size_t)r));
   ENMF_TRY(db.get(&jw, (size_t)2 * r * r));
   ENMF_TRY(db.get(&third, 1));
+  int* pfail = nullptr;
+  ENMF_TRY(db.get(&pfail, 1));
   CUDA_TRY(cudaMemsetAsync(third, 0, sizeof(unsigned long long), h->st));
   double* W = h->W64;
   // negativity of the unrotated point (info) and max|W| for reading R7
@@ -285,9 +287,16 @@ enmf_status_t rotate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int6
       ENMF_TRY(ar(h, M, (size_t)r * r, CommOp::Sum));
     }
     // R = C D^T from W^T B = C S D^T (orthogonal Procrustes)
-    // warm start from the previous step's right singular vectors (t > 0)
-    jacobi_svd(M, r, Cs, sv, Ds, jw, h->st, t > 0 ? Ds : nullptr);
-    procrustes_from_svd(Cs, sv, Ds, r, R, h->st);
+    // R = polar factor of M: scaled Newton (polar_newton); if M is numerically singular the
+    // device flag `third + 1` gates the Jacobi SVD + basis completion path (rank deficiency)
+    if (polar_supported(r)) {
+      polar_newton(M, r, R, pfail, h->st);
+      jacobi_svd(M, r, Cs, sv, Ds, jw, h->st, nullptr, pfail);
+      procrustes_from_svd(Cs, sv, Ds, r, R, h->st, pfail);
+    } else {
+      jacobi_svd(M, r, Cs, sv, Ds, jw, h->st, t > 0 ? Ds : nullptr);
+      procrustes_from_svd(Cs, sv, Ds, r, R, h->st);
+    }
   }
   ENMF_TRY(check_launch());
   unsigned long long third_h = 0;

@@ -93,12 +93,19 @@ void chol_inv(const double* G, int k, double shift_rel, double* R, double* Rinv,
 // One-sided Jacobi SVD of a k x k matrix A (row-major): A = U diag(s) V^T, s descending.
 // Uo, Vo are k x k row-major.  work >= 2*k*k doubles.  J0 (k x k row-major orthogonal, may be
 // null): warm start, the rotations are accumulated onto J0 (B = A J0 initially).
+// gate (device int, may be null): the kernel runs only if *gate != 0.
 void jacobi_svd(const double* A, int k, double* Uo, double* s, double* Vo, double* work,
-                cudaStream_t st, const double* J0 = nullptr);
+                cudaStream_t st, const double* J0 = nullptr, const int* gate = nullptr);
 // R = C D^T from the SVD W^T B = C S D^T (orthogonal Procrustes), completing C's basis
 // (in place) for zero singular values.
 void procrustes_from_svd(double* Cm, const double* s, const double* Dm, int k, double* R,
-                         cudaStream_t st);
+                         cudaStream_t st, const int* gate = nullptr);
+// Orthogonal polar factor of a nonsingular k x k row-major M (k <= 128) by scaled Newton
+// iteration: R = C D^T for M = C S D^T.  *fail (device) = 1 if M is numerically singular or
+// the iteration did not converge (R untouched) -- then gate the Jacobi path on it.
+bool polar_supported(int k);
+void polar_newton(const double* M, int k, double* R, int* fail, cudaStream_t st,
+                  int* iters = nullptr);
 
 // ---------------------------------------------------------------- stage / scalars
 // stage[0]: 0 ascent, 1 HALS.  Switches to HALS when min U >= 0 and min V >= 0.

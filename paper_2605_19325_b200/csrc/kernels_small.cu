@@ -260,7 +260,8 @@ chol_inv_kernel(const double* __restrict__ G, int k, double shift_rel, double* R
 // shared memory when k <= 128 (128 KB), J in `work`.
 __global__ void __launch_bounds__(1024)
 jacobi_svd_kernel(const double* __restrict__ A, int k, const double* J0,
-                  double* Uo, double* s, double* Vo, double* work) {
+                  double* Uo, double* s, double* Vo, double* work, const int* gate) {
+  if (gate && *gate == 0) return;
   extern __shared__ double smB[];
   const bool in_smem = k <= 128;
   double* B = in_smem ? smB : work;               // column c at B + c*k
@@ -412,9 +413,186 @@ jacobi_svd_kernel(const double* __restrict__ A, int k, const double* J0,
   for (int a = threadIdx.x; a < k; a += blockDim.x) s[a] = nrm[ord[a]];
 }
 
+
+// Orthogonal polar factor R of a nonsingular k x k matrix M (k <= 128; R = C D^T for
+// M = C S D^T, i.e. the Procrustes rotation) by the scaled Newton iteration
+// X <- (zeta X + X^{-T} / zeta) / 2, X0 = M, Frobenius scaling zeta = (|X^-1|_F / |X|_F)^1/2
+// while far from convergence.  One CTA of 1024 threads; X lives in R (global, L2) between
+// iterations; X^{-1} by Gauss-Jordan with partial pivoting held in REGISTERS: thread
+// (row ei = tid / 8, columns ec0 + 8 t, ec0 = tid % 8, t < 16) owns 16 entries, and each
+// elimination step exchanges only the pivot column and row through shared memory (shared-
+// memory traffic of an in-place smem elimination bounded it at ~0.3 ms per inverse).
+// *fail = 1 when M is numerically singular or the iteration does not converge (R is then
+// garbage): the caller gates the Jacobi-SVD Procrustes on it (rank deficiency).
+constexpr int kPolarLd = 129;
+constexpr int kPolarTPR = 4;                    // threads per row
+constexpr int kPolarCPT = 128 / kPolarTPR;      // columns per thread
+constexpr int kPolarThreads = 128 * kPolarTPR;  // 512: 128 registers per thread
+__global__ void __launch_bounds__(kPolarThreads)
+polar_newton_kernel(const double* __restrict__ M, int k, double* R, int* fail, int* iters) {
+  extern __shared__ double Inv[];               // k x kPolarLd: X^{-1} of the iteration
+  __shared__ double red[kPolarThreads];
+  __shared__ double colb[2][128];               // pivot column (double-buffered by step)
+  __shared__ double rowJ[128], rowP[128], rowN[128];
+  __shared__ int perm[128], dst[128], src[128];
+  __shared__ int bad_s;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int ei = tid / kPolarTPR, ec0 = tid % kPolarTPR;
+  const bool mine = ei < k;
+  for (int e = tid; e < k * k; e += blockDim.x) R[e] = M[e];
+  if (tid == 0) bad_s = 0;
+  __syncthreads();
+  bool scaling = true, done = false;
+  int it = 0;
+  for (; it < 40 && !done; ++it) {
+    double a[kPolarCPT];
+    double amax = 0.0;
+#pragma unroll
+    for (int t = 0; t < kPolarCPT; ++t) {
+      const int c = ec0 + kPolarTPR * t;
+      a[t] = (mine && c < k) ? R[ei * k + c] : 0.0;
+      amax = fmax(amax, fabs(a[t]));
+    }
+    amax = block_reduce<2>(amax, red);
+    for (int j = 0; j < k; ++j) {
+      double* col = colb[j & 1];
+      const int tj = j / kPolarTPR;
+      if (mine && ec0 == j % kPolarTPR) {
+        double v = 0.0;
+#pragma unroll
+        for (int t = 0; t < kPolarCPT; ++t) v = t == tj ? a[t] : v;
+        col[ei] = v;
+      }
+      __syncthreads();
+      // every warp finds the pivot (max |col[i]|, i >= j; ties: lowest i) redundantly
+      double bv = -1.0;
+      int bi = j;
+      for (int i = j + lane; i < k; i += 32) {
+        const double v = fabs(col[i]);
+        if (v > bv) { bv = v; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if (!(bv > 1e-13 * amax)) {                   // numerically singular: give up
+        if (tid == 0) bad_s = 1;
+        break;
+      }
+      const int pr = bi;
+      if (tid == 0) perm[j] = pr;
+      // publish rows j and pr (pre-swap)
+      if (ei == j || ei == pr) {
+#pragma unroll
+        for (int t = 0; t < kPolarCPT; ++t) {
+          const int c = ec0 + kPolarTPR * t;
+          if (c < k) (ei == j ? rowJ : rowP)[c] = a[t];
+        }
+      }
+      __syncthreads();
+      const double piv = col[pr];
+      const double ip = 1.0 / piv;
+      // swap rows j <-> pr in registers; the new row j is normalised and published
+      if (ei == j) {
+        const double* srow = pr == j ? rowJ : rowP;   // no interchange: row j itself
+#pragma unroll
+        for (int t = 0; t < kPolarCPT; ++t) {
+          const int c = ec0 + kPolarTPR * t;
+          if (c < k) {
+            const double v = c == j ? ip : srow[c] * ip;
+            a[t] = v;
+            rowN[c] = v;
+          }
+        }
+      } else if (ei == pr) {
+#pragma unroll
+        for (int t = 0; t < kPolarCPT; ++t) {
+          const int c = ec0 + kPolarTPR * t;
+          if (c < k) a[t] = rowJ[c];
+        }
+      }
+      __syncthreads();
+      if (mine && ei != j) {
+        // f = A[ei][j] after the swap: row pr now holds old row j's entry
+        const double f = ei == pr ? col[j] : col[ei];
+#pragma unroll
+        for (int t = 0; t < kPolarCPT; ++t) {
+          const int c = ec0 + kPolarTPR * t;
+          if (c < k) a[t] = c == j ? -f * ip : fma(-f, rowN[c], a[t]);
+        }
+      }
+    }
+    __syncthreads();
+    if (bad_s) break;
+    // column unpermutation: swaps (j, perm[j]) for j = k-1 .. 0  ->  Inv[i][dst[c]] = a[i][c]
+    if (tid == 0) {
+      for (int c = 0; c < k; ++c) src[c] = c;
+      for (int j = k - 1; j >= 0; --j) {
+        const int t = src[j];
+        src[j] = src[perm[j]];
+        src[perm[j]] = t;
+      }
+      for (int q = 0; q < k; ++q) dst[src[q]] = q;
+    }
+    __syncthreads();
+    if (mine) {
+#pragma unroll
+      for (int t = 0; t < kPolarCPT; ++t) {
+        const int c = ec0 + kPolarTPR * t;
+        if (c < k) Inv[ei * kPolarLd + dst[c]] = a[t];
+      }
+    }
+    __syncthreads();
+    // ---- X <- (zeta X + X^{-T} / zeta) / 2 ----
+    double zeta = 1.0;
+    if (scaling) {
+      double nx = 0.0, ni = 0.0;
+      if (mine) {
+#pragma unroll
+        for (int t = 0; t < kPolarCPT; ++t) {
+          const int c = ec0 + kPolarTPR * t;
+          if (c < k) {
+            const double xv = R[ei * k + c], iv = Inv[ei * kPolarLd + c];
+            nx += xv * xv;
+            ni += iv * iv;
+          }
+        }
+      }
+      nx = block_reduce<0>(nx, red);
+      ni = block_reduce<0>(ni, red);
+      zeta = sqrt(sqrt(ni / nx));
+    }
+    double dif = 0.0, nn = 0.0;
+    if (mine) {
+#pragma unroll
+      for (int t = 0; t < kPolarCPT; ++t) {
+        const int c = ec0 + kPolarTPR * t;
+        if (c < k) {
+          const double xo = R[ei * k + c];
+          const double xn = 0.5 * (zeta * xo + Inv[c * kPolarLd + ei] / zeta);   // X^{-T}
+          dif += (xn - xo) * (xn - xo);
+          nn += xn * xn;
+          R[ei * k + c] = xn;
+        }
+      }
+    }
+    dif = block_reduce<0>(dif, red);
+    nn = block_reduce<0>(nn, red);
+    if (dif <= 1e-4 * nn) scaling = false;          // quadratic phase: unscaled steps
+    if (dif <= 1e-28 * nn) done = true;             // |dX| <= 1e-14 |X|
+  }
+  if (tid == 0) {
+    *fail = (bad_s || !done) ? 1 : 0;
+    if (iters) *iters = it;
+  }
+}
+
 // Columns of C with s = 0 are completed to an orthonormal basis (rank-deficient M only).
-__global__ void complete_basis_kernel(double* Cm, const double* __restrict__ s, int k) {
-  if (threadIdx.x != 0) return;
+__global__ void complete_basis_kernel(double* Cm, const double* __restrict__ s, int k,
+                                      const int* gate) {
+  if (threadIdx.x != 0 || (gate && *gate == 0)) return;
   for (int a = 0; a < k; ++a) {
     if (s[a] > 0.0) continue;
     for (int e = 0; e < k; ++e) {
@@ -439,7 +617,8 @@ __global__ void complete_basis_kernel(double* Cm, const double* __restrict__ s, 
 
 // R = C D^T: block a computes row a (C row staged in shared memory).
 __global__ void procrustes_kernel(const double* __restrict__ Cm, const double* __restrict__ Dm,
-                                  int k, double* R) {
+                                  int k, double* R, const int* gate) {
+  if (gate && *gate == 0) return;
   __shared__ double crow[512];
   const int a = blockIdx.x;
   for (int c = threadIdx.x; c < k; c += blockDim.x) crow[c] = Cm[a * k + c];
@@ -534,7 +713,7 @@ void chol_inv(const double* G, int k, double shift_rel, double* R, double* Rinv,
 }
 
 void jacobi_svd(const double* A, int k, double* Uo, double* s, double* Vo, double* work,
-                cudaStream_t st, const double* J0) {
+                cudaStream_t st, const double* J0, const int* gate) {
   const size_t sm = k <= 128 ? sizeof(double) * k * k : 0;
   static bool attr = false;
   if (!attr) {
@@ -542,15 +721,29 @@ void jacobi_svd(const double* A, int k, double* Uo, double* s, double* Vo, doubl
                          (int)(sizeof(double) * 128 * 128));
     attr = true;
   }
-  jacobi_svd_kernel<<<1, 1024, sm, st>>>(A, k, J0, Uo, s, Vo, work);
+  jacobi_svd_kernel<<<1, 1024, sm, st>>>(A, k, J0, Uo, s, Vo, work, gate);
   count_launch();
 }
 
 void procrustes_from_svd(double* Cm, const double* s, const double* Dm, int k, double* R,
-                         cudaStream_t st) {
-  complete_basis_kernel<<<1, 32, 0, st>>>(Cm, s, k);
-  procrustes_kernel<<<k, 128, 0, st>>>(Cm, Dm, k, R);
+                         cudaStream_t st, const int* gate) {
+  complete_basis_kernel<<<1, 32, 0, st>>>(Cm, s, k, gate);
+  procrustes_kernel<<<k, 128, 0, st>>>(Cm, Dm, k, R, gate);
   count_launch(2);
+}
+
+bool polar_supported(int k) { return k >= 1 && k <= 128; }
+
+void polar_newton(const double* M, int k, double* R, int* fail, cudaStream_t st, int* iters) {
+  const size_t sm = sizeof(double) * (size_t)k * kPolarLd;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(polar_newton_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * 128 * kPolarLd));
+    attr = true;
+  }
+  polar_newton_kernel<<<1, kPolarThreads, sm, st>>>(M, k, R, fail, iters);
+  count_launch();
 }
 
 }  // namespace enmf
