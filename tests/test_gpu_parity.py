@@ -333,3 +333,26 @@ def test_zero_sweeps_and_launch_count():
     assert len(f) == 0 and np.array_equal(to_np(U), U0)
     h.iterate(U, V, 2)
     assert h.launch_count > n0
+
+
+@pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
+def test_rank_deficient_init_rotation(prec):
+    """X of exact rank 2 (small integers: exact in fp32) with r = 4: the SVD zero-fills the two
+    deficient columns, so the ADMM Procrustes matrix W^T B is singular -- the
+    Newton polar iteration reports failure and the gated Jacobi-SVD path with basis completion
+    computes R (kernels_small.cu).  R must stay orthogonal: the rotated U V^T equals the SVD
+    point's, which reproduces X (f = ||X||^2 - sum sigma^2 = 0)."""
+    import paper_2605_19325_b200 as E
+    g = np.random.default_rng(11)
+    m, n, r = 300, 220, 4
+    A, B = g.integers(0, 8, (m, 2)), g.integers(0, 8, (n, 2))
+    X = (A @ B.T).astype(np.float64)
+    h = E.Enmf(m, n, r, precision=prec)
+    U, V = to_dev(np.zeros((m, r))), to_dev(np.zeros((n, r)))
+    info = h.init(to_dev(X), U, V)
+    Ur, Vr = to_np(U), to_np(V)
+    assert info["rank_deficient"] == 2
+    assert np.all(np.isfinite(Ur)) and np.all(np.isfinite(Vr))
+    err = rel_fro(Ur @ Vr.T, X)
+    print(f"prec={h.precision}: |U V^T - X| / |X| = {err:.2e}")
+    assert err < 1e-6
