@@ -125,16 +125,19 @@ hals_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r, const doubl
         for (int kk = 0; kk < kmax; ++kk) {
           const int k = 32 * s + kk;
           const double ig = ginv[k];
+          if (ig == 0.0) continue;                  // G_kk <= 0: column skipped (warp-uniform)
           double gk[CPL];
 #pragma unroll
           for (int c = 0; c < CPL; ++c) gk[c] = Gs[k * RP + lane + 32 * c];
 #pragma unroll
           for (int b = 0; b < RB; ++b) {
-            // U_ik <- max(0, U_ik + (C_ik - sum_l U_il G_lk) / G_kk)   (skip if G_kk <= 0).
+            // U_ik <- max(0, U_ik + (C_ik - sum_l U_il G_lk) / G_kk).
             // Lane kk owns (u_k, t_k): every lane evaluates the update on its own pair (only
             // lane kk's is meaningful) and lane kk's change d is broadcast -- one shuffle.
+            // (a compare-select instead of fmax: no NaN-quieting sequence in the inner loop)
             const double uo = u[b][s];
-            const double nu = ig > 0.0 ? fmax(0.0, fma(t[b][s], ig, uo)) : uo;
+            const double v = fma(t[b][s], ig, uo);
+            const double nu = v > 0.0 ? v : 0.0;
             if (lane == kk) u[b][s] = nu;
             const double d = __shfl_sync(FULL, nu - uo, kk);
 #pragma unroll
