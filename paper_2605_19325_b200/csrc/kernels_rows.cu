@@ -419,8 +419,8 @@ kkt_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
 }
 
 template <int CPL>
-size_t row_smem(int extra_doubles) {
-  return sizeof(double) * (size_t)(32 * CPL * 32 * CPL + kRowWarps * 4 * 32 * CPL + extra_doubles);
+size_t row_smem(int extra_doubles, int rb = 4) {
+  return sizeof(double) * (size_t)(32 * CPL * 32 * CPL + kRowWarps * rb * 32 * CPL + extra_doubles);
 }
 
 template <typename K>
@@ -442,8 +442,8 @@ void hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, cons
                const int* stage, double* minparts, cudaStream_t st) {
 #define CALL(CPL)                                                                      \
   {                                                                                    \
-    auto k = hals_kernel<CPL, 4>;                                                      \
-    size_t sm = row_smem<CPL>(0);                                                      \
+    auto k = hals_kernel<CPL, 8>;                                                      \
+    size_t sm = row_smem<CPL>(0, 8);                                                   \
     set_smem(k, sm);                                                                   \
     k<<<kRowGrid, 32 * kRowWarps, sm, st>>>(F, ldf, rows, r, C, G, stage, minparts);   \
   }
