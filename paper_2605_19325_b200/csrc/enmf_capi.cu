@@ -137,8 +137,9 @@ enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
   const int mi = h->opt.pbcd_max_iter;
   if (maybe_ascent) {
     if (h->tc_pbcd) {
-      tc_pbcd_rows(F, ldf, rows, r, C, G, h->dscal + lam_slot, mi, h->snaps, h->parts,
-                   reinterpret_cast<int8_t*>(h->tcpb_ws + 128), h->tcpb_ws, stage, h->st);
+      if (tc_pbcd_rows(F, ldf, rows, r, C, G, h->dscal + lam_slot, mi, h->snaps, h->parts,
+                       reinterpret_cast<int8_t*>(h->tcpb_ws + 128), h->tcpb_ws, stage, h->st))
+        return ENMF_ERR_CUDA;
       reduce_parts(h->parts, tc_pbcd_parts(), mi + 1, h->pgsum, h->st);
     } else {
       pbcd_rows(F, ldf, rows, r, C, G, h->dscal + lam_slot, mi, h->snaps, h->parts, stage, h->st);

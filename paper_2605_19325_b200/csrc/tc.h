@@ -32,9 +32,10 @@ int tc_xf(TcState* s, bool transposed, const double* F, int64_t ldf, int ncols, 
 
 // Alg. 2 PBCD on the tensor cores: same contract as pbcd_rows (kernels_rows.cu); pgparts holds
 // tc_pbcd_parts() x (max_iter + 1) partials; gd_work >= 4*128*128 bytes, gscale_work >= 128.
+// Returns 0, or 1 on a launch / configuration error.
 bool tc_pbcd_supported(int r);
 int tc_pbcd_parts();
-void tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
+int tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
                   const double* G, const double* lam, int max_iter, float* snaps,
                   double* pgparts, int8_t* gd_work, double* gscale_work, const int* stage,
                   cudaStream_t st);

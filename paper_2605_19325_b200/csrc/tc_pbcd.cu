@@ -451,7 +451,7 @@ int tc_pbcd_parts() { return kSMs; }
 bool tc_pbcd_supported(int r) { return r >= 1 && r <= 128; }
 
 // Same contract as pbcd_rows (kernels_rows.cu); pgparts holds gridDim x (max_iter + 1).
-void tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
+int tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
                   const double* G, const double* lam, int max_iter, float* snaps,
                   double* pgparts, int8_t* gd_work, double* gscale_work, const int* stage,
                   cudaStream_t st) {
@@ -473,11 +473,15 @@ void tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double
   p.pgparts = pgparts;
   p.stage = stage;
   const size_t smem = SMEM_BYTES + sizeof(double) * (max_iter + 1);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_pbcd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  // the dynamic size grows with max_iter; static shared memory (row exchanges) counts against
+  // the same 227 KB, so the attribute is the exact dynamic request, raised when it grows
+  static size_t attr = 0;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(tc_pbcd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return 1;
     cudaFuncSetAttribute(tc_pbcd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    attr = true;
+    attr = smem;
   }
   const int tiles = (int)((rows + BM - 1) / BM);
   const int grid = tiles < kSMs ? tiles : kSMs;
@@ -485,6 +489,7 @@ void tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double
   tc_pbcd_kernel<<<kSMs, THREADS, smem, st>>>(p);
   (void)grid;
   count_launch(2);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 }  // namespace enmf
