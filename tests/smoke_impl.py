@@ -50,5 +50,27 @@ def run_smoke():
     eu = np.linalg.norm(Ud.cpu().numpy() - Uo) / np.linalg.norm(Uo)
     ev = np.linalg.norm(Vd.cpu().numpy() - Vo) / np.linalg.norm(Vo)
     assert eu < 1e-5 and ev < 1e-5, (eu, ev)
+    # (4) one ascent sweep (lift + PBCD) with the tensor-core PBCD kernel, from the oracle's
+    # rotated point, within max(1e-5, 10 x the oracle's own one-ulp spread) (R26)
+    from tests.gpu_common import oracle_floor, rotated_point
+    Ur, Vr, lu, lv = rotated_point(X, cfg.r)
+    ht = E.Enmf(cfg.m, cfg.n, cfg.r, precision=E.PREC_TC)
+    ht.set_data(torch.from_numpy(X).cuda())
+    Ut, Vt = torch.from_numpy(Ur.astype(np.float32)).cuda(), torch.from_numpy(
+        Vr.astype(np.float32)).cuda()
+    ht.set_stage(0, lu, lv)
+    _, it4 = ht.iterate(Ut, Vt, 1)
+    assert it4["ascent_sweeps"] == 1, it4
+
+    def run(Ua, Va):
+        Uo4, Vo4, _, _ = oracle.sweep(X, Ua, Va, oracle.SweepState(0, lu, lv, 0),
+                                      oracle.options(cfg.r, round_f32=1))
+        return Uo4, Vo4
+
+    (Uo4, Vo4), floor = oracle_floor(run, Ur, Vr)
+    ea = np.linalg.norm(Ut.cpu().numpy() - Uo4) / np.linalg.norm(Uo4)
+    eb = np.linalg.norm(Vt.cpu().numpy() - Vo4) / np.linalg.norm(Vo4)
+    assert ea < max(1e-5, 10 * floor[0]) and eb < max(1e-5, 10 * floor[1]), (ea, eb, floor)
     print(f"smoke ok: HALS f rel err {rel.max():.2e}; tc path ({h5.precision}) U {eu:.2e} "
-          f"V {ev:.2e}; launches {h.launch_count + h5.launch_count}")
+          f"V {ev:.2e}; tc ascent U {ea:.2e} V {eb:.2e} (floor {floor[0]:.1e}/{floor[1]:.1e}); "
+          f"launches {h.launch_count + h5.launch_count + ht.launch_count}")
