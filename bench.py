@@ -221,7 +221,6 @@ def run_enmf(args):
     U.copy_(U_rot)
     V.copy_(V_rot)
     h.set_stage(*stage0)
-    del U_rot, V_rot
 
     # ---- timed region: K sweeps, CUDA events on the handle's stream, max over ranks
     sampler = ClockSampler(gpu_index(local))
@@ -261,6 +260,34 @@ def run_enmf(args):
                 "kernel": f"X pass ({h.precision})", "peak_kind": peak_kind,
                 "pass_ms": pass_ms,
                 "share_of_step": (prof["xv"][0] + prof["xtu"][0]) / max(ms, 1e-9)}
+
+    # ---- per-stage rates: a few HALS sweeps from the final (feasible) state
+    # and a few ascent sweeps from the rotated point; the timed region above is the blend
+    def stage_rate(k):
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _, inf = h.iterate(U, V, k)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return k / (maxr(a.elapsed_time(b)) / 1000.0), inf
+    stage_rates = {}
+    U_end, V_end, stage_end = U.clone(), V.clone(), h.get_stage()
+    if stage_end[0] == 1:
+        rate, inf = stage_rate(5)
+        if inf["ascent_sweeps"] == 0:
+            stage_rates["hals_sweeps_per_s"] = rate
+    U.copy_(U_rot)
+    V.copy_(V_rot)
+    h.set_stage(*stage0)
+    if stage0[0] == 0:
+        rate, inf = stage_rate(3)
+        if inf["hals_sweeps"] == 0:
+            stage_rates["ascent_sweeps_per_s"] = rate
+    U.copy_(U_end)
+    V.copy_(V_end)
+    h.set_stage(*stage_end)
+    del U_rot, V_rot, U_end, V_end
 
     # ---- end to end through the public API: each step uploads the factor state (U, V)
     # from pinned host memory, runs one sweep, and reads U, V and f back.
@@ -322,7 +349,8 @@ def run_enmf(args):
                        "timed_sweeps": {"ascent": info_t["ascent_sweeps"],
                                         "hals": info_t["hals_sweeps"]},
                        "warmup_sweeps": {"ascent": info_w["ascent_sweeps"],
-                                         "hals": info_w["hals_sweeps"]}},
+                                         "hals": info_w["hals_sweeps"]},
+                       "stage_rates": stage_rates},
             "hbm_gbs_over_x": gbs,
             "init_s": init_s,
             "roofline": roofline,

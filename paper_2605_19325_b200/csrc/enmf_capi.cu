@@ -75,10 +75,11 @@ static void prof_collect(enmf_handle_t h) {
 }
 
 // P = X V (this rank's rows): the first X pass of a sweep.
-enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* P) {
+enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* P,
+                          const unsigned long long* vmax) {
   ENMF_TRY(prof_mark(h, 0));
   if (h->tc) {
-    if (tc_xv(h->tc, V, ldv, P, h->st) != 0) return ENMF_ERR_CUDA;
+    if (tc_xv(h->tc, V, ldv, P, h->st, vmax) != 0) return ENMF_ERR_CUDA;
   } else {
     GemmOut o;
     o.C = P;
@@ -90,10 +91,11 @@ enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* 
 }
 
 // Q = X^T U summed over ranks: the second X pass.
-enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q) {
+enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q,
+                           const unsigned long long* umax) {
   ENMF_TRY(prof_mark(h, 1));
   if (h->tc) {
-    if (tc_xtu(h->tc, U, ldu, Q, h->st) != 0) return ENMF_ERR_CUDA;
+    if (tc_xtu(h->tc, U, ldu, Q, h->st, umax) != 0) return ENMF_ERR_CUDA;
   } else {
     GemmOut o;
     o.C = Q;
@@ -131,8 +133,11 @@ namespace {
 // In the ascent stage: lift + mask + PBCD (Eqs.(6)-(10), Alg. 2); in HALS: the column sweep.
 enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
                            const double* C, const double* G, int lam_slot, int kstar_slot,
-                           int min_slot, bool sharded, bool maybe_ascent) {
+                           int min_slot, bool sharded, bool maybe_ascent,
+                           unsigned long long* colmax = nullptr) {
   const int r = (int)h->r;
+  if (colmax)
+    CUDA_TRY(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * r, h->st));
   int* stage = h->dint + I_STAGE;
   const int mi = h->opt.pbcd_max_iter;
   if (maybe_ascent) {
@@ -147,9 +152,9 @@ enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
     }
     if (sharded) ENMF_TRY(ar(h, h->pgsum, (size_t)(mi + 1), CommOp::Sum));
     pbcd_commit(F, ldf, rows, r, h->snaps, h->pgsum, h->opt.pbcd_eps, mi, h->dint + kstar_slot,
-                stage, h->minparts, h->tc_pbcd, h->st);
+                stage, h->minparts, h->tc_pbcd, h->st, h->tc_pbcd ? colmax : nullptr);
   }
-  hals_rows(F, ldf, rows, r, C, G, stage, h->minparts, h->st);
+  hals_rows(F, ldf, rows, r, C, G, stage, h->minparts, h->st, colmax);
   reduce_min(h->minparts, kRowGrid, h->dscal + min_slot, h->st);
   return sharded ? ar(h, h->dscal + min_slot, 1, CommOp::Min) : ENMF_OK;
 }
@@ -178,14 +183,21 @@ enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ld
   // stage control: HALS once U >= 0 and V >= 0
   stage_update(h->dint + I_STAGE, h->dscal + S_MINU, h->dscal + S_MINV, h->dint + I_CNT_ASC, st);
   // U block: P = X V, G_V = V^T V (G_V carried over from the previous sweep's end)
-  ENMF_TRY(contract_xv(h, V, ldv, h->P));
+  // colmax fusion (tc path): the U / V block update writes max |F| per column, which the next
+  // X pass uses for the digit scales.  Only when one of PBCD (tiled copy) / HALS writes every
+  // row: PBCD runs on the tensor-core kernel whenever the tc path is active.
+  unsigned long long* umax = h->fmax_uv && (h->tc_pbcd || !maybe_ascent) ? h->fmax_uv : nullptr;
+  unsigned long long* vmax = umax ? h->fmax_uv + 128 : nullptr;
+  ENMF_TRY(contract_xv(h, V, ldv, h->P, h->vmax_valid ? h->fmax_uv + 128 : nullptr));
   ENMF_TRY(block_update(h, U, ldu, h->m_loc, h->P, h->GV, S_LAMU, I_KSTAR_U, S_MINU, sh,
-                        maybe_ascent));
+                        maybe_ascent, umax));
+  h->umax_valid = umax != nullptr;
   // V block: Q = X^T U_new (allreduced), G_U = U_new^T U_new (PAPER.md:220 uses U^(k+1))
   ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh));
-  ENMF_TRY(contract_xtu(h, U, ldu, h->Q));
+  ENMF_TRY(contract_xtu(h, U, ldu, h->Q, h->umax_valid ? h->fmax_uv : nullptr));
   ENMF_TRY(block_update(h, V, ldv, h->n, h->Q, h->GU, S_LAMV, I_KSTAR_V, S_MINV, false,
-                        maybe_ascent));
+                        maybe_ascent, vmax));
+  h->vmax_valid = vmax != nullptr;
   // objective f = ||X||^2 - 2 <X^T U, V> + <U^T U, V^T V>   (BASELINE.json:5)
   ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
   dot_f64_f32(h->Q, V, ldv, h->n, h->r, h->parts, h->dscal + S_CROSS, st);
@@ -283,7 +295,7 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
   if (h->st) cudaStreamSynchronize(h->st);
   void* bufs[] = {h->dscal, h->dint, h->P, h->Q, h->GU, h->GV, h->work, h->parts,
                   h->minparts, h->pgsum, h->snaps, h->ftrace, h->x_owned, h->W64,
-                  h->tcpb_ws};
+                  h->tcpb_ws, h->fmax_uv};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->tc) tc_destroy(h->tc);
@@ -394,6 +406,8 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
   const char* tpe = getenv("ENMF_TC_PBCD");   // diagnostics: 0 keeps the SIMT fp64 PBCD
   h->tc_pbcd = prec == ENMF_PREC_TC && tc_pbcd_supported((int)h->r) && !(tpe && tpe[0] == '0');
   if (h->tc_pbcd && !h->tcpb_ws) ENMF_TRY(dalloc(&h->tcpb_ws, 128 + 4 * 128 * 128 / 8));
+  if (prec == ENMF_PREC_TC && !h->fmax_uv) ENMF_TRY(dalloc(&h->fmax_uv, 256));
+  h->umax_valid = h->vmax_valid = false;
   h->precision = prec;
   int zero[I_COUNT] = {0};
   CUDA_TRY(cudaMemcpyAsync(h->dint, zero, sizeof(zero), cudaMemcpyHostToDevice, h->st));
@@ -444,7 +458,9 @@ enmf_status_t enmf_iterate(enmf_handle_t h, float* U, int64_t ldu, float* V, int
   ENMF_TRY(min_factor(h, U, ldu, h->m_loc, S_MINU, sh));
   ENMF_TRY(min_factor(h, V, ldv, h->n, S_MINV, false));
   ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
+  h->umax_valid = h->vmax_valid = false;   // the caller may have changed U / V since
   for (int t = 0; t < n_iters; ++t) ENMF_TRY(sweep(h, U, ldu, V, ldv, t, maybe_ascent));
+  h->umax_valid = h->vmax_valid = false;
   // final stage flag (does not consume a sweep) and host-side bookkeeping
   int hi[I_COUNT];
   CUDA_TRY(cudaMemcpyAsync(hi, h->dint, sizeof(hi), cudaMemcpyDeviceToHost, h->st));

@@ -53,6 +53,10 @@ struct enmf_handle_s {
   enmf::TcState* tc = nullptr;
   double* tcpb_ws = nullptr;  // tensor-core PBCD: G digits (64 KB) + 128 column scales
   bool tc_pbcd = false;       // ascent PBCD on the tensor cores (precision TC, r <= 128)
+  // tensor-core path: column maxima of |U| / |V| written by the block-update kernels, so the
+  // next X pass packs the factor without a separate scan; valid only within one iterate call
+  unsigned long long* fmax_uv = nullptr;   // [2][128]: U, V
+  bool umax_valid = false, vmax_valid = false;
   float* x_owned = nullptr;  // device copy of X owned by enmf_solve_host
   double* W64 = nullptr;     // (m_loc + n) x r fp64 [U*; V*] kept from enmf_svd for enmf_rotate
   // profiling of the X passes (enmf_set_profiling): CUDA events around every contraction
@@ -94,8 +98,10 @@ enmf_status_t dalloc(T** p, size_t count) {
   return dalloc_bytes((void**)p, sizeof(T) * (count ? count : 1));
 }
 enmf_status_t ar(enmf_handle_t h, double* buf, size_t count, CommOp op);
-enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* P);
-enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q);
+enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* P,
+                          const unsigned long long* vmax = nullptr);
+enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q,
+                           const unsigned long long* umax = nullptr);
 enmf_status_t gram_f32(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, double* G,
                        bool sharded);
 enmf_status_t min_factor(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, int slot,

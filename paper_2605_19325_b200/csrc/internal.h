@@ -60,10 +60,13 @@ void gaussian_fill(double* A, int64_t rows, int64_t cols, uint64_t seed, cudaStr
 // ---------------------------------------------------------------- row-block updates
 // HALS on F (rows x r fp32) with cross term C (rows x r fp64) and Gram G (r x r fp64).
 // Runs only if *stage == want (device flag).  min partials to minparts[kRowGrid].
+// colmax (optional, u64[r], zeroed by the caller): atomicMax of the fp64 bits of max |F| per
+// column over the rows written -- the next X pass's digit scales without a separate scan.
 constexpr int kRowGrid = 2 * kSMs;
 constexpr int kRowWarps = 8;
 void hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
-               const int* stage, double* minparts, cudaStream_t st);
+               const int* stage, double* minparts, cudaStream_t st,
+               unsigned long long* colmax = nullptr);
 // PBCD phase A (all max_iter inner iterations, snapshots of every iterate, per-warp
 // partial ||M o grad||^2 for each iteration 0..max_iter), runs only in the ascent stage.
 void pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
@@ -75,7 +78,8 @@ int pbcd_parts();
 // layout (see pbcd_copy_tiled_kernel), else row-major rows x r.
 void pbcd_commit(float* F, int64_t ldf, int64_t rows, int r, const float* snaps,
                  const double* pgparts, double eps, int max_iter, int* kstar,
-                 const int* stage, double* minparts, bool tiled, cudaStream_t st);
+                 const int* stage, double* minparts, bool tiled, cudaStream_t st,
+                 unsigned long long* colmax = nullptr);
 // KKT partial statistics of one block (F, C = cross term, G): 8 values per warp slot.
 void kkt_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
               const double* G, double* parts, cudaStream_t st);

@@ -87,7 +87,8 @@ __device__ __forceinline__ void load_gram(const double* G, int r, double* Gs) {
 template <int CPL, int RB>
 __global__ void __launch_bounds__(32 * kRowWarps)
 hals_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r, const double* __restrict__ C,
-            const double* __restrict__ G, const int* __restrict__ stage, double* minparts) {
+            const double* __restrict__ G, const int* __restrict__ stage, double* minparts,
+            unsigned long long* colmax) {
   constexpr int RP = 32 * CPL;
   extern __shared__ double smem[];
   double* Gs = smem;
@@ -97,6 +98,9 @@ hals_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r, const doubl
   const bool active = stage == nullptr || *stage == 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double wmin = DBL_MAX;
+  double cmax[CPL];                  // max |F| of my columns lane + 32 c over my rows
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) cmax[c] = 0.0;
   if (active) {
     load_gram<CPL>(G, r, Gs);
     for (int k = threadIdx.x; k < RP; k += blockDim.x) {
@@ -155,9 +159,25 @@ hals_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r, const doubl
             const float v = (float)u[b][c];
             F[row * ldf + col] = v;
             wmin = fmin(wmin, (double)v);
+            cmax[c] = fmax(cmax[c], fabs((double)v));
           }
         }
     }
+  }
+  // column maxima for the next pass's digit packing (tc path): bits of non-negative doubles
+  // order like the values, so an integer atomicMax is exact and order independent; reduced in
+  // shared memory first (one global atomic per column per block)
+  if (colmax && active) {
+    __shared__ unsigned long long cm_s[32 * CPL];
+    for (int c = threadIdx.x; c < 32 * CPL; c += blockDim.x) cm_s[c] = 0ull;
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+      if (lane + 32 * c < r)
+        atomicMax(&cm_s[lane + 32 * c], (unsigned long long)__double_as_longlong(cmax[c]));
+    __syncthreads();
+    for (int c = threadIdx.x; c < r; c += blockDim.x)
+      if (cm_s[c]) atomicMax(&colmax[c], cm_s[c]);
   }
   if (minparts) {
     wmin = warp_min(wmin);
@@ -292,9 +312,12 @@ __global__ void pbcd_select_kernel(const double* __restrict__ pgsum, int max_ite
 __global__ void pbcd_copy_tiled_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r,
                                        const float* __restrict__ snaps,
                                        const int* __restrict__ kstar, const int* stage,
-                                       double* minparts) {
+                                       double* minparts, unsigned long long* colmax) {
   __shared__ float t[128][33];
   __shared__ double red[256];
+  __shared__ unsigned long long cm[128];
+  for (int c = threadIdx.x; c < 128; c += blockDim.x) cm[c] = 0ull;
+  __syncthreads();
   const bool active = stage == nullptr || *stage == 0;
   double mn = DBL_MAX;
   if (active) {
@@ -319,6 +342,8 @@ __global__ void pbcd_copy_tiled_kernel(float* __restrict__ F, int64_t ldf, int64
           const float v = t[il][jl];
           F[i * ldf + j0 + jl] = v;
           mn = fmin(mn, (double)v);
+          if (colmax)
+            atomicMax(&cm[j0 + jl], (unsigned long long)__double_as_longlong(fabs((double)v)));
         }
       }
     }
@@ -330,6 +355,9 @@ __global__ void pbcd_copy_tiled_kernel(float* __restrict__ F, int64_t ldf, int64
     __syncthreads();
   }
   if (threadIdx.x == 0 && active) minparts[blockIdx.x] = red[0];
+  if (colmax && active)
+    for (int c = threadIdx.x; c < r; c += blockDim.x)
+      if (cm[c]) atomicMax(&colmax[c], cm[c]);
 }
 
 __global__ void pbcd_copy_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r,
@@ -439,13 +467,14 @@ void set_smem(K kernel, size_t bytes) {
   } while (0)
 
 void hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
-               const int* stage, double* minparts, cudaStream_t st) {
+               const int* stage, double* minparts, cudaStream_t st,
+               unsigned long long* colmax) {
 #define CALL(CPL)                                                                      \
   {                                                                                    \
     auto k = hals_kernel<CPL, 8>;                                                      \
     size_t sm = row_smem<CPL>(0, 8);                                                   \
     set_smem(k, sm);                                                                   \
-    k<<<kRowGrid, 32 * kRowWarps, sm, st>>>(F, ldf, rows, r, C, G, stage, minparts);   \
+    k<<<kRowGrid, 32 * kRowWarps, sm, st>>>(F, ldf, rows, r, C, G, stage, minparts, colmax); \
   }
   ENMF_CPL_DISPATCH(r, CALL);
 #undef CALL
@@ -472,11 +501,11 @@ void pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C
 
 void pbcd_commit(float* F, int64_t ldf, int64_t rows, int r, const float* snaps,
                  const double* pgsum, double eps, int max_iter, int* kstar, const int* stage,
-                 double* minparts, bool tiled, cudaStream_t st) {
+                 double* minparts, bool tiled, cudaStream_t st, unsigned long long* colmax) {
   pbcd_select_kernel<<<1, 32, 0, st>>>(pgsum, max_iter, eps, kstar, stage);
   if (tiled)
     pbcd_copy_tiled_kernel<<<kRowGrid, 256, 0, st>>>(F, ldf, rows, r, snaps, kstar, stage,
-                                                     minparts);
+                                                     minparts, colmax);
   else
     pbcd_copy_kernel<<<kRowGrid, 256, 0, st>>>(F, ldf, rows, r, snaps, kstar, stage, minparts);
   count_launch(2);

@@ -21,9 +21,13 @@ bool tc_supported(int64_t rows, int64_t n, int64_t r);
 int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t n, int64_t r,
               cudaStream_t st);
 void tc_destroy(TcState* s);
-// P (rows x r fp64) = X V ; Q (n x r fp64) = X^T U  (this rank's rows only).
-int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st);
-int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st);
+// P (rows x r fp64) = X V ; Q (n x r fp64) = X^T U  (this rank's rows only).  vmax / umax
+// (optional, device u64[r]): fp64 bits of the factor's column maxima |F| when the kernel that
+// wrote the factor already computed them (hals / pbcd copy); else a scan computes them.
+int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st,
+          const unsigned long long* vmax = nullptr);
+int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st,
+           const unsigned long long* umax = nullptr);
 // Column-block products for the randomised SVD (fp64 factors of any width):
 // out (ld ldo) = X F (F: n x ncols) or, transposed, X^T F (F: this rank's rows x ncols).
 // Returns 0, 1 (CUDA error) or 2 (OOM).

@@ -852,20 +852,24 @@ static int8_t* fplane(TcState* s, int q, int rp) { return s->fp[0] + (size_t)q *
 
 template <typename T>
 static void pack_factor(TcState* s, const T* F, int64_t ldf, int64_t K, int64_t Kt, int ncols,
-                        int rp, cudaStream_t st) {
+                        int rp, cudaStream_t st, const unsigned long long* premax = nullptr) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(pack_factor_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(BK * 129 * sizeof(T)));
     attr = true;
   }
-  cudaMemsetAsync(s->fmaxbits, 0, sizeof(unsigned long long) * ncols, st);
-  colmax_kernel<T><<<2 * s->sms, 256, 0, st>>>(F, ldf, K, ncols, s->fmaxbits);
-  scales_kernel<<<1, 128, 0, st>>>(s->fmaxbits, ncols, s->sx, s->fscale, s->colscale);
+  if (!premax) {                  // column maxima not provided by the producing kernel
+    cudaMemsetAsync(s->fmaxbits, 0, sizeof(unsigned long long) * ncols, st);
+    colmax_kernel<T><<<2 * s->sms, 256, 0, st>>>(F, ldf, K, ncols, s->fmaxbits);
+    count_launch();
+  }
+  scales_kernel<<<1, 128, 0, st>>>(premax ? premax : s->fmaxbits, ncols, s->sx, s->fscale,
+                                   s->colscale);
   pack_factor_kernel<T><<<(int)std::min<int64_t>(Kt, 8 * s->sms), 256, BK * 129 * sizeof(T), st>>>(
       F, ldf, K, ncols, rp, s->fscale, Kt, (uint4*)fplane(s, 0, rp), (uint4*)fplane(s, 1, rp),
       (uint4*)fplane(s, 2, rp), (uint4*)fplane(s, 3, rp));
-  count_launch(3);
+  count_launch(2);
 }
 
 static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out_ld,
@@ -922,10 +926,11 @@ static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
-int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st) {
+int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st,
+          const unsigned long long* vmax) {
   // B = V (K = n), over all 64-column stages of X
   const int r = (int)s->r;
-  pack_factor<float>(s, V, ldv, s->n, s->tiles_per_row, r, s->rp, st);
+  pack_factor<float>(s, V, ldv, s->n, s->tiles_per_row, r, s->rp, st, vmax);
   const bool pair = s->pair;
   const int ks = pair ? s->ksplit1p : s->ksplit1;
   if (ks == 1)
@@ -938,10 +943,11 @@ int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
-int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st) {
+int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st,
+           const unsigned long long* umax) {
   // B = U (K = rows of X), split-K partials reduced in a fixed order
   const int r = (int)s->r;
-  pack_factor<float>(s, U, ldu, s->rows, s->Kt2, r, s->rp, st);
+  pack_factor<float>(s, U, ldu, s->rows, s->Kt2, r, s->rp, st, umax);
   const int mode = s->xtp[0] ? 2 : 1;
   const bool pair = s->pair && mode == 2;   // the pair kernel reads K-major A only
   const int ks = pair ? s->ksplit2p : s->ksplit2;
