@@ -110,10 +110,16 @@ enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double*
 // G = A^T A of an fp32 factor (rows x r); sum over ranks if `sharded`.
 enmf_status_t gram_f32(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, double* G,
                        bool sharded) {
-  GemmOut o;
-  o.C = G;
-  o.ldc = h->r;
-  gemm<float, float>(true, A, lda, A, lda, h->r, h->r, rows, o, h->work, h->work_elems, h->st);
+  if (gram_supported((int)h->r) &&
+      h->work_elems >= (size_t)128 * 128 * (1 + (size_t)gram_parts())) {
+    // upper-triangle fp64 Gram (kernels_gram.cu): Gu = work[0 .. 128^2), per-SM partials after
+    gram_sym(A, lda, rows, (int)h->r, h->work + 128 * 128, h->work, G, h->st);
+  } else {
+    GemmOut o;
+    o.C = G;
+    o.ldc = h->r;
+    gemm<float, float>(true, A, lda, A, lda, h->r, h->r, rows, o, h->work, h->work_elems, h->st);
+  }
   return sharded ? ar(h, G, (size_t)(h->r * h->r), CommOp::Sum) : ENMF_OK;
 }
 

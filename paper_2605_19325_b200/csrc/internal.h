@@ -35,6 +35,13 @@ void gemm(bool transA, const TA* A, int64_t lda, const TB* B, int64_t ldb, int64
           int64_t N, int64_t K, GemmOut out, double* work, size_t work_elems,
           cudaStream_t st);
 
+// G = A^T A (r x r fp64, ld r) of an fp32 rows x r matrix, upper-triangle tiles, fixed-order
+// reduction of per-SM partials: parts >= gram_parts() * 128^2 doubles, Gu >= 128^2.
+bool gram_supported(int r);
+int gram_parts();
+void gram_sym(const float* A, int64_t lda, int64_t rows, int r, double* parts, double* Gu,
+              double* G, cudaStream_t st);
+
 // Deterministic sum of `parts` contiguous blocks of `len` doubles into out.
 void reduce_parts(const double* parts, int nparts, int64_t len, double* out, cudaStream_t st);
 
