@@ -284,20 +284,17 @@ def run_enmf(args):
         rate, inf = stage_rate(3)
         if inf["hals_sweeps"] == 0:
             stage_rates["ascent_sweeps_per_s"] = rate
-    U.copy_(U_end)
-    V.copy_(V_end)
-    h.set_stage(*stage_end)
-    del U_rot, V_rot, U_end, V_end
-
-    # ---- end to end through the public API: each step uploads the factor state (U, V)
-    # from pinned host memory, runs one sweep, and reads U, V and f back.
+    # ---- end to end through the public API, on the same K-sweep schedule as the timed
+    # region (from the rotated point: ascent sweeps, then HALS): each step uploads the factor
+    # state (U, V) from pinned host memory, runs one sweep, and reads U, V and f back.
     e2e = None
     if not args.no_e2e:
         Uh = torch.empty(count, r, dtype=torch.float32).pin_memory()
         Vh = torch.empty(n, r, dtype=torch.float32).pin_memory()
-        Uh.copy_(U)
-        Vh.copy_(V)
-        k2 = max(3, min(args.steps, 10))
+        Uh.copy_(U_rot)
+        Vh.copy_(V_rot)
+        h.set_stage(*stage0)
+        k2 = args.steps
         barrier()
         t0 = time.perf_counter()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -319,7 +316,11 @@ def run_enmf(args):
                "h2d_bytes_per_step": int((count + n) * r * 4),
                "d2h_bytes_per_step": int((count + n) * r * 4 + 8),
                "what": "per step: H2D of (U, V) from pinned host, enmf_iterate(1), D2H of "
-                       "(U, V, f); X resident"}
+                       "(U, V, f); X resident; same K-sweep schedule as the timed region"}
+    U.copy_(U_end)
+    V.copy_(V_end)
+    h.set_stage(*stage_end)
+    del U_rot, V_rot, U_end, V_end
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
