@@ -173,6 +173,15 @@ enmf_status_t enmf_kkt_residual(enmf_handle_t h, const float* U, int64_t ldu, co
 enmf_status_t enmf_cross_terms(enmf_handle_t h, const float* U, int64_t ldu, const float* V,
                                int64_t ldv, double* P, double* Q);
 
+/* enmf_iterate with the factor state in HOST memory: U_host (this rank's row_count x r, ld r)
+ * and V_host (n x r, ld r), updated in place (page-locked buffers make the copies
+ * asynchronous).  Per call: V is uploaded on the handle's stream (the first X V pass needs
+ * it), U on an internal copy stream overlapping that pass; U is downloaded behind the last V
+ * block and V at the end.  Uses handle-owned device copies of U and V (allocated on the first
+ * call).  Same semantics, errors and f_trace_host / info_host as enmf_iterate; synchronises. */
+enmf_status_t enmf_iterate_host(enmf_handle_t h, float* U_host, float* V_host, int n_iters,
+                                double* f_trace_host, enmf_iter_info_t* info_host);
+
 /* End-to-end solve from HOST buffers (single GPU): X_host (m x n, ld = n), U_host
  * (m x r), V_host (n x r) and f_trace_host (n_iters) are host pointers.  Copies X to the
  * device through a pinned staging buffer, runs init + n_iters sweeps, copies U, V back. */
@@ -194,7 +203,7 @@ enmf_status_t enmf_get_profile(enmf_handle_t h, double* ms_host, int64_t* count_
  * in enmf_problem_t.nccl_unique_id on every rank). */
 enmf_status_t enmf_nccl_unique_id(void* out128);
 
-/* Name of the contraction path selected by enmf_set_data ("fp64-simt" or "tc-split-f16/f64"). */
+/* Name of the contraction path selected by enmf_set_data ("fp64-simt" or "tc-i8x4-exact"). */
 const char* enmf_precision_name(enmf_handle_t h);
 
 const char* enmf_status_string(enmf_status_t s);

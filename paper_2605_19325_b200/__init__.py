@@ -83,6 +83,8 @@ _sigs = {
     "enmf_get_stage": (ctypes.c_int, [_H, ctypes.POINTER(ctypes.c_int), _D, _D]),
     "enmf_iterate": (ctypes.c_int, [_H, _P, _I64, _P, _I64, ctypes.c_int, _D,
                                     ctypes.POINTER(IterInfo)]),
+    "enmf_iterate_host": (ctypes.c_int, [_H, _P, _P, ctypes.c_int, _D,
+                                         ctypes.POINTER(IterInfo)]),
     "enmf_objective": (ctypes.c_int, [_H, _P, _I64, _P, _I64, ctypes.c_int, _D]),
     "enmf_kkt_residual": (ctypes.c_int, [_H, _P, _I64, _P, _I64, ctypes.POINTER(Kkt)]),
     "enmf_cross_terms": (ctypes.c_int, [_H, _P, _I64, _P, _I64, _P, _P]),
@@ -244,6 +246,28 @@ class Enmf:
         _check(_lib.enmf_iterate(self._h, pu, ldu, pv, ldv, int(n_iters),
                                  f.ctypes.data_as(_D) if trace else None, ctypes.byref(info)),
                "enmf_iterate")
+        return f[: int(n_iters)], _info_dict(info)
+
+    def iterate_host(self, U, V, n_iters, trace=True):
+        """enmf_iterate_host: U (row_count x r) and V (n x r) are contiguous fp32 CPU tensors
+        (pinned for asynchronous copies) or numpy arrays, updated in place."""
+        for name, A, rows in (("U", U, self.rows), ("V", V, self.n)):
+            shape = tuple(A.shape)
+            dev = getattr(A, "device", None)
+            contig = A.is_contiguous() if hasattr(A, "is_contiguous") else \
+                A.flags["C_CONTIGUOUS"]
+            if shape != (rows, self.r) or (dev is not None and dev.type != "cpu") or not contig:
+                raise EnmfError(-1, f"iterate_host: {name} must be a contiguous CPU "
+                                    f"({rows}, {self.r}) array")
+            if str(getattr(A, "dtype", "")) not in ("torch.float32", "float32"):
+                raise EnmfError(-1, f"iterate_host: {name} must be float32")
+        pu = U.data_ptr() if hasattr(U, "data_ptr") else U.ctypes.data
+        pv = V.data_ptr() if hasattr(V, "data_ptr") else V.ctypes.data
+        f = np.zeros(max(int(n_iters), 1))
+        info = IterInfo()
+        _check(_lib.enmf_iterate_host(self._h, ctypes.c_void_p(pu), ctypes.c_void_p(pv),
+                                      int(n_iters), f.ctypes.data_as(_D) if trace else None,
+                                      ctypes.byref(info)), "enmf_iterate_host")
         return f[: int(n_iters)], _info_dict(info)
 
     def objective(self, U, V, exact=False):

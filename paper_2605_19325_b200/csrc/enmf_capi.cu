@@ -182,22 +182,41 @@ enmf_status_t ensure_ftrace(enmf_handle_t h, int n) {
 }
 
 // One sweep (U block then V block) with the trace-form objective into ftrace[t].
+// Host-transfer hooks of enmf_iterate_host (null for enmf_iterate): u_ready = event after which
+// U is on the device (the first sweep's X V pass runs before it); u_download = host buffer that
+// receives U on the copy stream as soon as the last sweep's U block is done.
+struct SweepHooks {
+  cudaEvent_t u_ready = nullptr;
+  float* u_download = nullptr;
+};
+
 enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv, int t,
-                    bool maybe_ascent) {
+                    bool maybe_ascent, const SweepHooks& hk = SweepHooks()) {
   const bool sh = h->prob.world_size > 1;
   cudaStream_t st = h->st;
-  // stage control (PAPER.md:334): HALS once U >= 0 and V >= 0
-  stage_update(h->dint + I_STAGE, h->dscal + S_MINU, h->dscal + S_MINV, h->dint + I_CNT_ASC, st);
-  // U block: P = X V, G_V = V^T V (G_V carried over from the previous sweep's end)
+  // U block: P = X V, G_V = V^T V (G_V carried over from the previous sweep's end).  The X V
+  // pass depends on V only, so it is issued before the stage decision (which reads min U).
   // colmax fusion (tc path): the U / V block update writes max |F| per column, which the next
   // X pass uses for the digit scales.  Only when one of PBCD (tiled copy) / HALS writes every
   // row: PBCD runs on the tensor-core kernel whenever the tc path is active.
   unsigned long long* umax = h->fmax_uv && (h->tc_pbcd || !maybe_ascent) ? h->fmax_uv : nullptr;
   unsigned long long* vmax = umax ? h->fmax_uv + 128 : nullptr;
   ENMF_TRY(contract_xv(h, V, ldv, h->P, h->vmax_valid ? h->fmax_uv + 128 : nullptr));
+  if (hk.u_ready) {                    // U arrives on the copy stream during the X V pass
+    CUDA_TRY(cudaStreamWaitEvent(st, hk.u_ready, 0));
+    ENMF_TRY(min_factor(h, U, ldu, h->m_loc, S_MINU, sh));
+  }
+  // stage control (PAPER.md:334): HALS once U >= 0 and V >= 0
+  stage_update(h->dint + I_STAGE, h->dscal + S_MINU, h->dscal + S_MINV, h->dint + I_CNT_ASC, st);
   ENMF_TRY(block_update(h, U, ldu, h->m_loc, h->P, h->GV, S_LAMU, I_KSTAR_U, S_MINU, sh,
                         maybe_ascent, umax));
   h->umax_valid = umax != nullptr;
+  if (hk.u_download) {                 // U is final: download it behind the V block
+    CUDA_TRY(cudaEventRecord(h->ev_a, st));
+    CUDA_TRY(cudaStreamWaitEvent(h->st2, h->ev_a, 0));
+    CUDA_TRY(cudaMemcpyAsync(hk.u_download, U, sizeof(float) * h->m_loc * h->r,
+                             cudaMemcpyDeviceToHost, h->st2));
+  }
   // V block: Q = X^T U_new (allreduced), G_U = U_new^T U_new (PAPER.md:220 uses U^(k+1))
   ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh));
   ENMF_TRY(contract_xtu(h, U, ldu, h->Q, h->umax_valid ? h->fmax_uv : nullptr));
@@ -301,9 +320,15 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
   if (h->st) cudaStreamSynchronize(h->st);
   void* bufs[] = {h->dscal, h->dint, h->P, h->Q, h->GU, h->GV, h->work, h->parts,
                   h->minparts, h->pgsum, h->snaps, h->ftrace, h->x_owned, h->W64,
-                  h->tcpb_ws, h->fmax_uv};
+                  h->tcpb_ws, h->fmax_uv, h->Ud, h->Vd};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  if (h->st2) {
+    cudaStreamSynchronize(h->st2);
+    cudaStreamDestroy(h->st2);
+    cudaEventDestroy(h->ev_a);
+    cudaEventDestroy(h->ev_b);
+  }
   if (h->tc) tc_destroy(h->tc);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   comm_destroy(h->comm);
@@ -448,25 +473,36 @@ enmf_status_t enmf_get_stage(enmf_handle_t h, int* stage, double* lambda_u, doub
   return ENMF_OK;
 }
 
-enmf_status_t enmf_iterate(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
-                           int n_iters, double* f_trace_host, enmf_iter_info_t* info) {
-  if (!h || n_iters < 0) return ENMF_ERR_INVALID_ARG;
-  if (!h->bound) return ENMF_ERR_STATE;
-  ENMF_TRY(validate_ld(U, ldu, h->r));
-  ENMF_TRY(validate_ld(V, ldv, h->r));
+}  // extern "C"
+
+namespace {
+// The sweep loop behind enmf_iterate and enmf_iterate_host.  hk0 applies to the first sweep
+// (U upload), u_dl_host to the last (U download); v_dl_host receives V at the end.
+enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                           int n_iters, double* f_trace_host, enmf_iter_info_t* info,
+                           cudaEvent_t u_ready, float* u_dl_host, float* v_dl_host) {
   LaunchScope ls(h);
   const bool sh = h->prob.world_size > 1;
   const bool maybe_ascent = !h->stage_known_hals;
   if (maybe_ascent) ENMF_TRY(ensure_snaps(h));
   ENMF_TRY(ensure_ftrace(h, std::max(n_iters, 1)));
   CUDA_TRY(cudaMemsetAsync(h->dint + I_CNT_ASC, 0, 2 * sizeof(int), h->st));
-  // entry state: mins of the factors as given, G_V of the given V
-  ENMF_TRY(min_factor(h, U, ldu, h->m_loc, S_MINU, sh));
+  // entry state: mins of the factors as given, G_V of the given V (min U after its upload)
+  if (!u_ready) ENMF_TRY(min_factor(h, U, ldu, h->m_loc, S_MINU, sh));
   ENMF_TRY(min_factor(h, V, ldv, h->n, S_MINV, false));
   ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
   h->umax_valid = h->vmax_valid = false;   // the caller may have changed U / V since
-  for (int t = 0; t < n_iters; ++t) ENMF_TRY(sweep(h, U, ldu, V, ldv, t, maybe_ascent));
+  for (int t = 0; t < n_iters; ++t) {
+    SweepHooks hk;
+    if (t == 0) hk.u_ready = u_ready;
+    if (t == n_iters - 1) hk.u_download = u_dl_host;
+    ENMF_TRY(sweep(h, U, ldu, V, ldv, t, maybe_ascent, hk));
+  }
+  if (u_ready && n_iters == 0) CUDA_TRY(cudaStreamWaitEvent(h->st, u_ready, 0));
   h->umax_valid = h->vmax_valid = false;
+  if (v_dl_host)
+    CUDA_TRY(cudaMemcpyAsync(v_dl_host, V, sizeof(float) * h->n * h->r, cudaMemcpyDeviceToHost,
+                             h->st));
   // final stage flag (does not consume a sweep) and host-side bookkeeping
   int hi[I_COUNT];
   CUDA_TRY(cudaMemcpyAsync(hi, h->dint, sizeof(hi), cudaMemcpyDeviceToHost, h->st));
@@ -476,6 +512,7 @@ enmf_status_t enmf_iterate(enmf_handle_t h, float* U, int64_t ldu, float* V, int
     CUDA_TRY(cudaMemcpyAsync(f_trace_host, h->ftrace, sizeof(double) * n_iters,
                              cudaMemcpyDeviceToHost, h->st));
   CUDA_TRY(cudaStreamSynchronize(h->st));
+  if (h->st2) CUDA_TRY(cudaStreamSynchronize(h->st2));
   ENMF_TRY(check_launch());
   prof_collect(h);
   if (hi[I_STAGE] == 1) h->stage_known_hals = true;
@@ -490,6 +527,44 @@ enmf_status_t enmf_iterate(enmf_handle_t h, float* U, int64_t ldu, float* V, int
     for (int t = 0; t < n_iters; ++t)
       if (!isfinite(f_trace_host[t])) return ENMF_ERR_NONFINITE;
   return ENMF_OK;
+}
+}  // namespace
+
+extern "C" {
+
+enmf_status_t enmf_iterate(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                           int n_iters, double* f_trace_host, enmf_iter_info_t* info) {
+  if (!h || n_iters < 0) return ENMF_ERR_INVALID_ARG;
+  if (!h->bound) return ENMF_ERR_STATE;
+  ENMF_TRY(validate_ld(U, ldu, h->r));
+  ENMF_TRY(validate_ld(V, ldv, h->r));
+  return iterate_core(h, U, ldu, V, ldv, n_iters, f_trace_host, info, nullptr, nullptr,
+                      nullptr);
+}
+
+enmf_status_t enmf_iterate_host(enmf_handle_t h, float* U_host, float* V_host, int n_iters,
+                                double* f_trace_host, enmf_iter_info_t* info) {
+  if (!h || !U_host || !V_host || n_iters < 0) return ENMF_ERR_INVALID_ARG;
+  if (!h->bound) return ENMF_ERR_STATE;
+  if (!h->Ud) ENMF_TRY(dalloc(&h->Ud, (size_t)(h->m_loc * h->r)));
+  if (!h->Vd) ENMF_TRY(dalloc(&h->Vd, (size_t)(h->n * h->r)));
+  if (!h->st2) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
+  }
+  const int64_t r = h->r;
+  // V first on the compute stream (the X V pass needs it); U on the copy stream, overlapping
+  // that pass; U comes back behind the V block, V and f at the end
+  CUDA_TRY(cudaMemcpyAsync(h->Vd, V_host, sizeof(float) * h->n * r, cudaMemcpyHostToDevice,
+                           h->st));
+  CUDA_TRY(cudaEventRecord(h->ev_b, h->st));
+  CUDA_TRY(cudaStreamWaitEvent(h->st2, h->ev_b, 0));
+  CUDA_TRY(cudaMemcpyAsync(h->Ud, U_host, sizeof(float) * h->m_loc * r, cudaMemcpyHostToDevice,
+                           h->st2));
+  CUDA_TRY(cudaEventRecord(h->ev_b, h->st2));
+  return iterate_core(h, h->Ud, r, h->Vd, r, n_iters, f_trace_host, info, h->ev_b,
+                      n_iters > 0 ? U_host : nullptr, V_host);
 }
 
 enmf_status_t enmf_objective(enmf_handle_t h, const float* U, int64_t ldu, const float* V,

@@ -57,6 +57,11 @@ struct enmf_handle_s {
   // next X pass packs the factor without a separate scan; valid only within one iterate call
   unsigned long long* fmax_uv = nullptr;   // [2][128]: U, V
   bool umax_valid = false, vmax_valid = false;
+  // enmf_iterate_host: device copies of the factor state and a copy stream for the transfers
+  float* Ud = nullptr;
+  float* Vd = nullptr;
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   float* x_owned = nullptr;  // device copy of X owned by enmf_solve_host
   double* W64 = nullptr;     // (m_loc + n) x r fp64 [U*; V*] kept from enmf_svd for enmf_rotate
   // profiling of the X passes (enmf_set_profiling): CUDA events around every contraction
