@@ -188,7 +188,8 @@ enmf_status_t ensure_ftrace(enmf_handle_t h, int n) {
 struct SweepHooks {
   cudaEvent_t u_ready = nullptr;
   float* u_download = nullptr;
-};
+  float* v_download = nullptr;       // V is final after the V block: download it on the copy
+};                                   // stream while the Grams / objective finish the sweep
 
 enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv, int t,
                     bool maybe_ascent, const SweepHooks& hk = SweepHooks()) {
@@ -223,6 +224,12 @@ enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ld
   ENMF_TRY(block_update(h, V, ldv, h->n, h->Q, h->GU, S_LAMV, I_KSTAR_V, S_MINV, false,
                         maybe_ascent, vmax));
   h->vmax_valid = vmax != nullptr;
+  if (hk.v_download) {
+    CUDA_TRY(cudaEventRecord(h->ev_a, st));
+    CUDA_TRY(cudaStreamWaitEvent(h->st2, h->ev_a, 0));
+    CUDA_TRY(cudaMemcpyAsync(hk.v_download, V, sizeof(float) * h->n * h->r,
+                             cudaMemcpyDeviceToHost, h->st2));
+  }
   // objective f = ||X||^2 - 2 <X^T U, V> + <U^T U, V^T V>   (BASELINE.json:5)
   ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
   dot_f64_f32(h->Q, V, ldv, h->n, h->r, h->parts, h->dscal + S_CROSS, st);
@@ -495,12 +502,15 @@ enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int
   for (int t = 0; t < n_iters; ++t) {
     SweepHooks hk;
     if (t == 0) hk.u_ready = u_ready;
-    if (t == n_iters - 1) hk.u_download = u_dl_host;
+    if (t == n_iters - 1) {
+      hk.u_download = u_dl_host;
+      hk.v_download = v_dl_host;
+    }
     ENMF_TRY(sweep(h, U, ldu, V, ldv, t, maybe_ascent, hk));
   }
   if (u_ready && n_iters == 0) CUDA_TRY(cudaStreamWaitEvent(h->st, u_ready, 0));
   h->umax_valid = h->vmax_valid = false;
-  if (v_dl_host)
+  if (v_dl_host && n_iters == 0)
     CUDA_TRY(cudaMemcpyAsync(v_dl_host, V, sizeof(float) * h->n * h->r, cudaMemcpyDeviceToHost,
                              h->st));
   // final stage flag (does not consume a sweep) and host-side bookkeeping
