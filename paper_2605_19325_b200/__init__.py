@@ -165,7 +165,7 @@ class Enmf:
 
     # -- lifecycle
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:   # _lib is None at interpreter exit
             _lib.enmf_destroy(self._h)
             self._h = None
 

@@ -327,9 +327,10 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
   if (h->st) cudaStreamSynchronize(h->st);
   void* bufs[] = {h->dscal, h->dint, h->P, h->Q, h->GU, h->GV, h->work, h->parts,
                   h->minparts, h->pgsum, h->snaps, h->ftrace, h->x_owned, h->W64,
-                  h->tcpb_ws, h->fmax_uv, h->Ud, h->Vd};
+                  h->tcpb_ws, h->fmax_uv, h->Ud, h->Vd, h->arena};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  for (void* b : h->arena_extra) cudaFree(b);
   if (h->st2) {
     cudaStreamSynchronize(h->st2);
     cudaStreamDestroy(h->st2);
@@ -418,12 +419,12 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
   h->ldx = ldx;
   h->bound = false;
   const int np = x_stats_parts(h->m_loc);
-  double* out3 = h->work;   // [sum, min, nonfinite]
+  double* out3 = h->work;   // [sum, min, nonfinite, max|X| of this rank's rows]
   x_stats(X, ldx, h->m_loc, h->n, h->parts, np, out3, h->st);
   ENMF_TRY(ar(h, out3, 1, CommOp::Sum));
   ENMF_TRY(ar(h, out3 + 1, 1, CommOp::Min));
   ENMF_TRY(ar(h, out3 + 2, 1, CommOp::Sum));
-  double hv[3];
+  double hv[4];
   CUDA_TRY(cudaMemcpyAsync(hv, out3, sizeof(hv), cudaMemcpyDeviceToHost, h->st));
   CUDA_TRY(cudaStreamSynchronize(h->st));
   if (hv[2] > 0) return ENMF_ERR_NONFINITE;
@@ -438,7 +439,7 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
   if (prec == ENMF_PREC_TC && !tc_supported(h->m_loc, h->n, h->r)) return ENMF_ERR_SHAPE;
   if (h->tc) { tc_destroy(h->tc); h->tc = nullptr; }
   if (prec == ENMF_PREC_TC) {
-    int rc = tc_create(&h->tc, X, ldx, h->m_loc, h->n, h->r, h->st);
+    int rc = tc_create(&h->tc, X, ldx, h->m_loc, h->n, h->r, h->st, hv[3]);
     if (rc != 0) return rc == 2 ? ENMF_ERR_OOM : ENMF_ERR_CUDA;
   }
   const char* tpe = getenv("ENMF_TC_PBCD");   // diagnostics: 0 keeps the SIMT fp64 PBCD

@@ -13,16 +13,43 @@ using namespace enmf;
 
 namespace {
 
+// Init workspaces: a handle-owned arena (h->arena, grown on demand and kept until
+// enmf_destroy) handed out bump-style per call -- the rotation alone needs ~1 GB at C5, and a
+// cudaMalloc / cudaFree of that per call costs more than the 100 ADMM steps' Procrustes work.
+// The arena is grown only between calls; a call that needs more than the current capacity
+// allocates the full requirement first (first-fit by size recorded in h->arena_need).
 struct DevBuf {
-  std::vector<void*> ptrs;
+  enmf_handle_t h;
+  size_t used = 0;
+  bool overflow = false;
+  explicit DevBuf(enmf_handle_t hh) : h(hh) {}
   ~DevBuf() {
-    for (void* p : ptrs) cudaFree(p);
+    if (used > h->arena_need) h->arena_need = used;
   }
   template <typename T>
   enmf_status_t get(T** p, size_t count) {
-    enmf_status_t s = dalloc(p, count);
-    if (s == ENMF_OK) ptrs.push_back((void*)*p);
-    return s;
+    const size_t bytes = ((sizeof(T) * (count ? count : 1)) + 255) & ~(size_t)255;
+    if (used + bytes > h->arena_bytes) {
+      // grow: free the old arena (the stream is idle at the start of an init call) and
+      // allocate the larger of the recorded need and what this call needs so far
+      if (used != 0) {
+        // buffers already handed out live in the old arena: fall back to a private allocation
+        overflow = true;
+        enmf_status_t s = dalloc(p, count);
+        if (s == ENMF_OK) h->arena_extra.push_back((void*)*p);
+        return s;
+      }
+      if (h->arena) cudaFree(h->arena);
+      h->arena = nullptr;
+      h->arena_bytes = 0;
+      const size_t want = std::max(h->arena_need, bytes);
+      enmf_status_t s = dalloc_bytes((void**)&h->arena, want);
+      if (s != ENMF_OK) return s;
+      h->arena_bytes = want;
+    }
+    *p = reinterpret_cast<T*>(h->arena + used);
+    used += bytes;
+    return ENMF_OK;
   }
 };
 
@@ -108,7 +135,7 @@ enmf_status_t svd_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t
   l64 = std::min<int64_t>(l64, 512);
   const int l = (int)l64;
   const bool sh = h->prob.world_size > 1;
-  DevBuf db;
+  DevBuf db(h);
   double *Om, *Y, *Z, *Qt, *tmp, *G, *R, *Rinv, *Ue, *Ve, *sv, *jw, *Us;
   int* bad;
   const int64_t big = std::max(mr, n);
@@ -215,7 +242,7 @@ enmf_status_t rotate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int6
   const int r = (int)h->r;
   const int64_t count = rows * r;
   const bool sh = h->prob.world_size > 1;
-  DevBuf db;
+  DevBuf db(h);
   double *WR, *Yh, *Z, *B, *R, *M, *Cs, *Ds, *sv, *jw;
   unsigned long long* third;
   ENMF_TRY(db.get(&WR, (size_t)count));
@@ -231,6 +258,10 @@ enmf_status_t rotate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int6
   ENMF_TRY(db.get(&third, 1));
   int* pfail = nullptr;
   ENMF_TRY(db.get(&pfail, 1));
+  int* nsst = nullptr;
+  ENMF_TRY(db.get(&nsst, 2));
+  double* nsw = nullptr;
+  ENMF_TRY(db.get(&nsw, (size_t)3 * r * r + 256));
   CUDA_TRY(cudaMemsetAsync(third, 0, sizeof(unsigned long long), h->st));
   double* W = h->W64;
   // negativity of the unrotated point (info) and max|W| for reading R7
@@ -290,7 +321,10 @@ enmf_status_t rotate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int6
     // R = polar factor of M: scaled Newton (polar_newton); if M is numerically singular the
     // device flag `third + 1` gates the Jacobi SVD + basis completion path (rank deficiency)
     if (polar_supported(r)) {
-      polar_newton(M, r, R, pfail, h->st);
+      // Newton-Schulz (multi-CTA, ~20-30 cheap steps) -> scaled Newton if it did not converge
+      // -> Jacobi SVD if M is numerically singular; each stage gated by a device flag
+      polar_ns(M, r, R, nsst, nsw, 40, h->st);
+      polar_newton(M, r, R, pfail, h->st, nullptr, nsst + 1);
       jacobi_svd(M, r, Cs, sv, Ds, jw, h->st, nullptr, pfail);
       procrustes_from_svd(Cs, sv, Ds, r, R, h->st, pfail);
     } else {
@@ -425,10 +459,12 @@ enmf_status_t enmf_solve_host(enmf_handle_t h, const float* X_host, float* U_hos
   cudaFreeHost(pin[1]);
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
-  float *dU, *dV;
-  DevBuf db;
-  ENMF_TRY(db.get(&dU, (size_t)(m * r)));
-  ENMF_TRY(db.get(&dV, (size_t)(n * r)));
+  // device factor state: the handle's iterate_host buffers (not the init arena, which
+  // enmf_init below reuses)
+  if (!h->Ud) ENMF_TRY(dalloc(&h->Ud, (size_t)(m * r)));
+  if (!h->Vd) ENMF_TRY(dalloc(&h->Vd, (size_t)(n * r)));
+  float* dU = h->Ud;
+  float* dV = h->Vd;
   ENMF_TRY(enmf_init(h, h->x_owned, n, dU, r, dV, r, info));
   ENMF_TRY(enmf_iterate(h, dU, r, dV, r, n_iters, f_trace_host, nullptr));
   CUDA_TRY(cudaMemcpyAsync(U_host, dU, sizeof(float) * m * r, cudaMemcpyDeviceToHost, h->st));

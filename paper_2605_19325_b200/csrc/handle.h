@@ -57,6 +57,10 @@ struct enmf_handle_s {
   // next X pass packs the factor without a separate scan; valid only within one iterate call
   unsigned long long* fmax_uv = nullptr;   // [2][128]: U, V
   bool umax_valid = false, vmax_valid = false;
+  // init workspace arena (enmf_init.cu DevBuf): kept across calls, grown on demand
+  uint8_t* arena = nullptr;
+  size_t arena_bytes = 0, arena_need = 0;
+  std::vector<void*> arena_extra;   // one-off overflow allocations, freed with the handle
   // enmf_iterate_host: device copies of the factor state and a copy stream for the transfers
   float* Ud = nullptr;
   float* Vd = nullptr;

@@ -46,9 +46,10 @@ void gram_sym(const float* A, int64_t lda, int64_t rows, int r, double* parts, d
 void reduce_parts(const double* parts, int nparts, int64_t len, double* out, cudaStream_t st);
 
 // ---------------------------------------------------------------- elementwise / reductions
-// sum of squares, min and non-finite count of X (rows x n): writes {sum, min, nonfinite}.
+// sum of squares, min, non-finite count and max |.| of X (rows x n), one pass:
+// writes out4 = {sum, min, nonfinite, max|X|}; parts >= 4 * nparts.
 void x_stats(const float* X, int64_t ldx, int64_t rows, int64_t n, double* parts, int nparts,
-             double* out3, cudaStream_t st);
+             double* out4, cudaStream_t st);
 int x_stats_parts(int64_t rows);
 // min over an fp32 matrix (rows x cols, ld): partials then out[0].
 void min_f32(const float* A, int64_t ld, int64_t rows, int64_t cols, double* parts,
@@ -116,7 +117,12 @@ void procrustes_from_svd(double* Cm, const double* s, const double* Dm, int k, d
 // the iteration did not converge (R untouched) -- then gate the Jacobi path on it.
 bool polar_supported(int k);
 void polar_newton(const double* M, int k, double* R, int* fail, cudaStream_t st,
-                  int* iters = nullptr);
+                  int* iters = nullptr, const int* gate = nullptr);
+// Polar factor by the Newton-Schulz iteration (multi-CTA, device-side convergence, no host
+// sync): state[2] (device) = {done, fail}; fail = 1 if |X^T X - I| did not reach tolerance in
+// max_iter steps (gate polar_newton on state + 1).  work >= 3 k^2 + 16 doubles.
+void polar_ns(const double* M, int k, double* R, int* state, double* work, int max_iter,
+              cudaStream_t st);
 
 // ---------------------------------------------------------------- stage / scalars
 // stage[0]: 0 ascent, 1 HALS.  Switches to HALS when min U >= 0 and min V >= 0.

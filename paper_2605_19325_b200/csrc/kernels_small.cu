@@ -35,40 +35,63 @@ __device__ double block_reduce(double v, double* red) {
 
 constexpr int kStatGrid = 4 * kSMs;
 
-__global__ void x_stats_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows,
-                               int64_t n, double* parts) {
+// ||X||^2, min X, #non-finite and max |X| of this rank's rows in one pass (4 partials per
+// block).  Rows by blocks, a row's columns by threads (float4 when aligned): no 64-bit division
+// per element.
+__global__ void __launch_bounds__(256)
+x_stats_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n,
+               double* parts) {
   __shared__ double red[256];
-  double s = 0.0, mn = DBL_MAX, bad = 0.0;
-  const int64_t total = rows * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / n, j = e - i * n;
-    const float v = X[i * ldx + j];
-    if (!isfinite(v)) { bad += 1.0; continue; }
-    s += (double)v * (double)v;
+  double s = 0.0, mn = DBL_MAX, bad = 0.0, mx = 0.0;
+  const bool vec = (ldx & 3) == 0 && (n & 3) == 0 && ((uintptr_t)X & 15) == 0;
+  auto take = [&](float v) {
+    if (!isfinite(v)) {
+      bad += 1.0;
+      return;
+    }
+    s = fma((double)v, (double)v, s);
     mn = fmin(mn, (double)v);
+    mx = fmax(mx, fabs((double)v));
+  };
+  for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
+    const float* xr = X + i * ldx;
+    if (vec) {
+      for (int64_t j = 4 * (int64_t)threadIdx.x; j < n; j += 4 * (int64_t)blockDim.x) {
+        const float4 f = *reinterpret_cast<const float4*>(xr + j);
+        take(f.x);
+        take(f.y);
+        take(f.z);
+        take(f.w);
+      }
+    } else {
+      for (int64_t j = threadIdx.x; j < n; j += blockDim.x) take(xr[j]);
+    }
   }
   s = block_reduce<0>(s, red);
   mn = block_reduce<1>(mn, red);
   bad = block_reduce<0>(bad, red);
+  mx = block_reduce<2>(mx, red);
   if (threadIdx.x == 0) {
-    parts[3 * blockIdx.x] = s;
-    parts[3 * blockIdx.x + 1] = mn;
-    parts[3 * blockIdx.x + 2] = bad;
+    parts[4 * blockIdx.x] = s;
+    parts[4 * blockIdx.x + 1] = mn;
+    parts[4 * blockIdx.x + 2] = bad;
+    parts[4 * blockIdx.x + 3] = mx;
   }
 }
 
-__global__ void x_stats_finish(const double* parts, int nparts, double* out3) {
+__global__ void x_stats_finish(const double* parts, int nparts, double* out4) {
   if (threadIdx.x != 0) return;
-  double s = 0.0, mn = DBL_MAX, bad = 0.0;
+  double s = 0.0, mn = DBL_MAX, bad = 0.0, mx = 0.0;
   for (int p = 0; p < nparts; ++p) {
-    s += parts[3 * p];
-    mn = fmin(mn, parts[3 * p + 1]);
-    bad += parts[3 * p + 2];
+    s += parts[4 * p];
+    mn = fmin(mn, parts[4 * p + 1]);
+    bad += parts[4 * p + 2];
+    mx = fmax(mx, parts[4 * p + 3]);
   }
-  out3[0] = s;
-  out3[1] = mn;
-  out3[2] = bad;
+  out4[0] = s;
+  out4[1] = mn;
+  out4[2] = bad;
+  out4[3] = mx;
 }
 
 __global__ void min_f32_kernel(const float* __restrict__ A, int64_t ld, int64_t rows,
@@ -429,7 +452,12 @@ constexpr int kPolarTPR = 4;                    // threads per row
 constexpr int kPolarCPT = 128 / kPolarTPR;      // columns per thread
 constexpr int kPolarThreads = 128 * kPolarTPR;  // 512: 128 registers per thread
 __global__ void __launch_bounds__(kPolarThreads)
-polar_newton_kernel(const double* __restrict__ M, int k, double* R, int* fail, int* iters) {
+polar_newton_kernel(const double* __restrict__ M, int k, double* R, int* fail, int* iters,
+                    const int* gate) {
+  if (gate && *gate == 0) {                     // an earlier method already produced R
+    if (threadIdx.x == 0) *fail = 0;
+    return;
+  }
   extern __shared__ double Inv[];               // k x kPolarLd: X^{-1} of the iteration
   __shared__ double red[kPolarThreads];
   __shared__ double colb[2][128];               // pivot column (double-buffered by step)
@@ -589,6 +617,109 @@ polar_newton_kernel(const double* __restrict__ M, int k, double* R, int* fail, i
   }
 }
 
+
+// ---------------------------------------------------------------- Newton-Schulz polar factor
+// R = polar(M) by the Newton-Schulz iteration X <- X (3 I - X^T X) / 2 from X0 = M / |M|_F
+// (all singular values in (0, 1]; each step maps a small sigma to ~1.5 sigma, then converges
+// quadratically).  Two small multi-CTA kernels per iteration (32 x 32 output tiles of the
+// k x k products, k <= 128), no host synchronisation: ns_gram_kernel forms Y = X^T X and the
+// per-tile partials of |Y - I|_F^2; ns_step_kernel sums the partials in a fixed order and, when
+// |Y - I|_F <= tol, copies X to R and raises the done flag (every later kernel of the sequence
+// returns at once), else writes X (1.5 I - 0.5 Y) to the other buffer.  state = {done, fail}.
+constexpr int kNsTile = 16;              // 16 x 16 output tiles: 64 CTAs at k = 128
+
+__global__ void ns_init_kernel(const double* __restrict__ M, int k, double* X, int* state) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) s += M[e] * M[e];
+  s = block_reduce<0>(s, red);
+  const double inv = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) X[e] = M[e] * inv;
+  if (threadIdx.x == 0) {
+    state[0] = s > 0.0 ? 0 : 1;       // done (nothing to do for M = 0: left to the fallback)
+    state[1] = s > 0.0 ? 1 : 1;       // fail until converged
+  }
+}
+
+// Y[I, J] tile = sum_l X[l][I] X[l][J]; partial |Y - I|^2 of the tile
+__global__ void __launch_bounds__(256) ns_gram_kernel(const double* __restrict__ X, int k,
+                                                      double* Y, double* part,
+                                                      const int* state) {
+  if (state[0]) return;
+  __shared__ double Xi[128][kNsTile + 1], Xj[128][kNsTile + 1];
+  __shared__ double red[256];
+  const int nt = (k + kNsTile - 1) / kNsTile;
+  const int ti = blockIdx.x / nt, tj = blockIdx.x % nt;
+  for (int e = threadIdx.x; e < k * kNsTile; e += blockDim.x) {
+    const int l = e / kNsTile, c = e % kNsTile;
+    const int ci = ti * kNsTile + c, cj = tj * kNsTile + c;
+    Xi[l][c] = ci < k ? X[l * k + ci] : 0.0;
+    Xj[l][c] = cj < k ? X[l * k + cj] : 0.0;
+  }
+  __syncthreads();
+  double dev = 0.0;
+  for (int o = threadIdx.x; o < kNsTile * kNsTile; o += blockDim.x) {
+    const int a = o / kNsTile, b = o % kNsTile;
+    double acc = 0.0;
+    for (int l = 0; l < k; ++l) acc = fma(Xi[l][a], Xj[l][b], acc);
+    const int i = ti * kNsTile + a, j = tj * kNsTile + b;
+    if (i < k && j < k) {
+      Y[i * k + j] = acc;
+      const double d = acc - (i == j ? 1.0 : 0.0);
+      dev = fma(d, d, dev);
+    }
+  }
+  dev = block_reduce<0>(dev, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = dev;
+}
+
+// X_out[I, J] = sum_l X[I][l] (1.5 delta_lJ - 0.5 Y[l][J]), or R = X when converged
+__global__ void __launch_bounds__(256) ns_step_kernel(const double* __restrict__ X, int k,
+                                                      const double* __restrict__ Y,
+                                                      const double* __restrict__ part,
+                                                      int nparts, double tol2, double* Xout,
+                                                      double* R, int* state) {
+  if (state[0]) return;
+  __shared__ double Xr[kNsTile][128 + 1], Yc[128][kNsTile + 1];
+  double dev = 0.0;
+  for (int q = 0; q < nparts; ++q) dev += part[q];          // fixed order: same on every CTA
+  if (dev <= tol2) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x)
+      R[e] = X[e];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      state[1] = 0;
+      __threadfence();
+    }
+    // state[0] (done) is raised by ns_done_kernel after this grid: no CTA may skip the copy
+    return;
+  }
+  const int nt = (k + kNsTile - 1) / kNsTile;
+  const int ti = blockIdx.x / nt, tj = blockIdx.x % nt;
+  for (int e = threadIdx.x; e < kNsTile * k; e += blockDim.x) {
+    const int a = e / k, l = e % k;
+    const int i = ti * kNsTile + a;
+    Xr[a][l] = i < k ? X[i * k + l] : 0.0;
+  }
+  for (int e = threadIdx.x; e < k * kNsTile; e += blockDim.x) {
+    const int l = e / kNsTile, b = e % kNsTile;
+    const int j = tj * kNsTile + b;
+    Yc[l][b] = j < k ? (l == j ? 1.5 : 0.0) - 0.5 * Y[l * k + j] : 0.0;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < kNsTile * kNsTile; o += blockDim.x) {
+    const int a = o / kNsTile, b = o % kNsTile;
+    double acc = 0.0;
+    for (int l = 0; l < k; ++l) acc = fma(Xr[a][l], Yc[l][b], acc);
+    const int i = ti * kNsTile + a, j = tj * kNsTile + b;
+    if (i < k && j < k) Xout[i * k + j] = acc;
+  }
+}
+
+// done flag after a converged step (separate launch: every CTA of the step saw done = 0)
+__global__ void ns_done_kernel(int* state) {
+  if (threadIdx.x == 0 && state[0] == 0 && state[1] == 0) state[0] = 1;
+}
+
 // Columns of C with s = 0 are completed to an orthonormal basis (rank-deficient M only).
 __global__ void complete_basis_kernel(double* Cm, const double* __restrict__ s, int k,
                                       const int* gate) {
@@ -640,9 +771,9 @@ inline int grid_for(int64_t n) {
 int x_stats_parts(int64_t rows) { (void)rows; return kStatGrid; }
 
 void x_stats(const float* X, int64_t ldx, int64_t rows, int64_t n, double* parts, int nparts,
-             double* out3, cudaStream_t st) {
+             double* out4, cudaStream_t st) {
   x_stats_kernel<<<nparts, 256, 0, st>>>(X, ldx, rows, n, parts);
-  x_stats_finish<<<1, 32, 0, st>>>(parts, nparts, out3);
+  x_stats_finish<<<1, 32, 0, st>>>(parts, nparts, out4);
   count_launch(2);
 }
 
@@ -734,7 +865,27 @@ void procrustes_from_svd(double* Cm, const double* s, const double* Dm, int k, d
 
 bool polar_supported(int k) { return k >= 1 && k <= 128; }
 
-void polar_newton(const double* M, int k, double* R, int* fail, cudaStream_t st, int* iters) {
+void polar_ns(const double* M, int k, double* R, int* state, double* work, int max_iter,
+              cudaStream_t st) {
+  const int nt = (k + kNsTile - 1) / kNsTile;
+  double* X0 = work;
+  double* X1 = work + (size_t)k * k;
+  double* Y = work + (size_t)2 * k * k;
+  double* part = work + (size_t)3 * k * k;
+  const double tol2 = 1e-26 * k;          // |X^T X - I|_F <= 1e-13 sqrt(k)
+  ns_init_kernel<<<1, 256, 0, st>>>(M, k, X0, state);
+  for (int it = 0; it < max_iter; ++it) {
+    const double* Xc = (it & 1) ? X1 : X0;
+    double* Xn = (it & 1) ? X0 : X1;
+    ns_gram_kernel<<<nt * nt, 256, 0, st>>>(Xc, k, Y, part, state);
+    ns_step_kernel<<<nt * nt, 256, 0, st>>>(Xc, k, Y, part, nt * nt, tol2, Xn, R, state);
+    ns_done_kernel<<<1, 32, 0, st>>>(state);
+  }
+  count_launch(1 + 3 * max_iter);
+}
+
+void polar_newton(const double* M, int k, double* R, int* fail, cudaStream_t st, int* iters,
+                  const int* gate) {
   const size_t sm = sizeof(double) * (size_t)k * kPolarLd;
   static bool attr = false;
   if (!attr) {
@@ -742,7 +893,7 @@ void polar_newton(const double* M, int k, double* R, int* fail, cudaStream_t st,
                          (int)(sizeof(double) * 128 * kPolarLd));
     attr = true;
   }
-  polar_newton_kernel<<<1, kPolarThreads, sm, st>>>(M, k, R, fail, iters);
+  polar_newton_kernel<<<1, kPolarThreads, sm, st>>>(M, k, R, fail, iters, gate);
   count_launch();
 }
 

@@ -18,8 +18,9 @@ struct TcState;
 // True when the shape is handled by the tensor-core kernels.
 bool tc_supported(int64_t rows, int64_t n, int64_t r);
 // Build the digit-plane copy of X (rows x n, ld).  Returns 0, 1 (CUDA error) or 2 (OOM).
+// xmax: max |X| of these rows if already known (x_stats), else < 0 to scan.
 int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t n, int64_t r,
-              cudaStream_t st);
+              cudaStream_t st, double xmax = -1.0);
 void tc_destroy(TcState* s);
 // P (rows x r fp64) = X V ; Q (n x r fp64) = X^T U  (this rank's rows only).  vmax / umax
 // (optional, device u64[r]): fp64 bits of the factor's column maxima |F| when the kernel that

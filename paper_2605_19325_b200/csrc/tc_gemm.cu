@@ -516,34 +516,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 // X (rows x n, ld) * sx -> 4 digit planes of [Mt][tiles_per_row] tiles.  One thread writes one
 // 16-byte row chunk (16 consecutive columns) of each plane; consecutive threads read
 // consecutive chunks of an X row (coalesced reads).
-__global__ void pack_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n,
-                              double sx, int64_t tiles_per_row, int64_t Mt, uint4* p0, uint4* p1,
-                              uint4* p2, uint4* p3) {
+// 16 consecutive values (val(k), |val| < 64.5) -> the 16-byte chunks of the 4 digit planes,
+// w[plane][k / 4] byte k % 4, built in registers (no addressable local arrays).
+template <typename F>
+__device__ __forceinline__ void pack_digits16(F val, uint32_t (&w)[4][4]) {
+#pragma unroll
+  for (int pl = 0; pl < 4; ++pl)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[pl][q] = 0u;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const uint32_t dw = digits_word(val(k));
+#pragma unroll
+    for (int pl = 0; pl < 4; ++pl) w[pl][k >> 2] |= ((dw >> (8 * pl)) & 255u) << (8 * (k & 3));
+  }
+}
+
+__global__ void __launch_bounds__(256)
+pack_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n, double sx,
+              int64_t tiles_per_row, int64_t Mt, uint4* p0, uint4* p1, uint4* p2, uint4* p3) {
   const int64_t cpr = tiles_per_row * 4;                 // 16-byte chunks per padded row
-  const int64_t total = Mt * BM * cpr;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < total;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = c / cpr, jc = c - i * cpr;
-    const int64_t j0 = jc * 16;
-    __align__(16) int8_t d[4][16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const int64_t j = j0 + k;
-      const double v = (i < rows && j < n) ? (double)X[i * ldx + j] * sx : 0.0;
-      const Dig4 q = digits4(v);
-#pragma unroll
-      for (int pl = 0; pl < 4; ++pl) d[pl][k] = q.d[pl];
-    }
+  const bool vec = (ldx & 3) == 0 && (n & 3) == 0 && ((uintptr_t)X & 15) == 0;
+  // rows by blocks, a row's chunks by threads: no 64-bit division per element
+  for (int64_t i = blockIdx.x; i < Mt * BM; i += gridDim.x) {
+    const float* xr = X + i * ldx;
     const int64_t mt = i / BM, g = (i % BM) / 8, ri = i % 8;
-    const int64_t kt = j0 / BK, kc = (j0 % BK) / 16;
-    // planes interleaved per tile: tile t, plane pl at (t * PLANES + pl) * TILE_A (p_pl = base +
-    // pl * TILE_A), so one stage's planes are one contiguous bulk copy
-    const int64_t idx =
-        ((mt * tiles_per_row + kt) * PLANES * TILE_A + (kc * 16 + g) * 128 + ri * 16) / 16;
-    p0[idx] = *reinterpret_cast<uint4*>(d[0]);
-    p1[idx] = *reinterpret_cast<uint4*>(d[1]);
-    p2[idx] = *reinterpret_cast<uint4*>(d[2]);
-    p3[idx] = *reinterpret_cast<uint4*>(d[3]);
+    for (int64_t jc = threadIdx.x; jc < cpr; jc += blockDim.x) {
+      const int64_t j0 = jc * 16;
+      float v[16];
+      if (i < rows && vec && j0 + 16 <= n) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 f = *reinterpret_cast<const float4*>(xr + j0 + 4 * q);
+          v[4 * q] = f.x;
+          v[4 * q + 1] = f.y;
+          v[4 * q + 2] = f.z;
+          v[4 * q + 3] = f.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = (i < rows && j0 + k < n) ? xr[j0 + k] : 0.0f;
+      }
+      // digits of X sx (exact: fp32 times a power of two), packed in registers
+      uint32_t w[4][4];
+      pack_digits16([&](int k) { return (double)v[k] * sx; }, w);
+      const int64_t kt = j0 / BK, kc = (j0 % BK) / 16;
+      // planes interleaved per tile: tile t, plane pl at (t * PLANES + pl) * TILE_A (p_pl = base +
+      // pl * TILE_A), so one stage's planes are one contiguous bulk copy
+      const int64_t idx =
+          ((mt * tiles_per_row + kt) * PLANES * TILE_A + (kc * 16 + g) * 128 + ri * 16) / 16;
+      p0[idx] = make_uint4(w[0][0], w[0][1], w[0][2], w[0][3]);
+      p1[idx] = make_uint4(w[1][0], w[1][1], w[1][2], w[1][3]);
+      p2[idx] = make_uint4(w[2][0], w[2][1], w[2][2], w[2][3]);
+      p3[idx] = make_uint4(w[3][0], w[3][1], w[3][2], w[3][3]);
+    }
   }
 }
 
@@ -565,18 +591,13 @@ pack_xt_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n
     for (int w = threadIdx.x; w < 512; w += blockDim.x) {
       const int kc = w / 128, g = (w / 8) % 16, ri = w % 8;
       const int jl = g * 8 + ri;
-      __align__(16) int8_t d[4][16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const Dig4 q = digits4((double)tx[kc * 16 + k][jl] * sx);
-#pragma unroll
-        for (int pl = 0; pl < 4; ++pl) d[pl][k] = q.d[pl];
-      }
+      uint32_t wd[4][4];
+      pack_digits16([&](int k) { return (double)tx[kc * 16 + k][jl] * sx; }, wd);
       const int64_t idx = (t * PLANES * TILE_A) / 16 + w;   // planes interleaved per tile
-      p0[idx] = *reinterpret_cast<uint4*>(d[0]);
-      p1[idx] = *reinterpret_cast<uint4*>(d[1]);
-      p2[idx] = *reinterpret_cast<uint4*>(d[2]);
-      p3[idx] = *reinterpret_cast<uint4*>(d[3]);
+      p0[idx] = make_uint4(wd[0][0], wd[0][1], wd[0][2], wd[0][3]);
+      p1[idx] = make_uint4(wd[1][0], wd[1][1], wd[1][2], wd[1][3]);
+      p2[idx] = make_uint4(wd[2][0], wd[2][1], wd[2][2], wd[2][3]);
+      p3[idx] = make_uint4(wd[3][0], wd[3][1], wd[3][2], wd[3][3]);
     }
     __syncthreads();
   }
@@ -608,18 +629,13 @@ pack_factor_kernel(const T* __restrict__ F, int64_t ldf, int64_t K, int r, int r
       const int g = w / 32, kc = (w / 8) % 4;
       const int col = g * 8 + w % 8;
       const double s = col < r ? fscale[col] : 0.0;
-      __align__(16) int8_t d[4][16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const Dig4 q = digits4((double)tileF[kc * 16 + k][col] * s);
-#pragma unroll
-        for (int pl = 0; pl < 4; ++pl) d[pl][k] = q.d[pl];
-      }
+      uint32_t wd[4][4];
+      pack_digits16([&](int k) { return (double)tileF[kc * 16 + k][col] * s; }, wd);
       const int64_t idx = kt * PLANES * chunks + w;       // planes interleaved per stage
-      p0[idx] = *reinterpret_cast<uint4*>(d[0]);
-      p1[idx] = *reinterpret_cast<uint4*>(d[1]);
-      p2[idx] = *reinterpret_cast<uint4*>(d[2]);
-      p3[idx] = *reinterpret_cast<uint4*>(d[3]);
+      p0[idx] = make_uint4(wd[0][0], wd[0][1], wd[0][2], wd[0][3]);
+      p1[idx] = make_uint4(wd[1][0], wd[1][1], wd[1][2], wd[1][3]);
+      p2[idx] = make_uint4(wd[2][0], wd[2][1], wd[2][2], wd[2][3]);
+      p3[idx] = make_uint4(wd[3][0], wd[3][1], wd[3][2], wd[3][3]);
     }
     __syncthreads();
   }
@@ -741,7 +757,7 @@ static int choose_split(int64_t tiles, int64_t stages, int sms) {
 }
 
 int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t n, int64_t r,
-              cudaStream_t st) {
+              cudaStream_t st, double xmax) {
   *out = nullptr;
   TcState* s = new TcState();
   s->rows = rows;
@@ -801,21 +817,25 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
     return e == cudaErrorMemoryAllocation ? 2 : 1;
   }
   // X scale: power of two with max X * sx in [32, 64)
-  cudaMemsetAsync(s->maxbits, 0, sizeof(unsigned), st);
-  maxabs_x_kernel<<<4 * s->sms, 256, 0, st>>>(X, ldx, rows, n, s->maxbits);
-  unsigned mb = 0;
-  cudaMemcpyAsync(&mb, s->maxbits, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess) {
-    tc_destroy(s);
-    return 1;
+  if (xmax < 0.0) {                     // not supplied by the caller's statistics pass
+    cudaMemsetAsync(s->maxbits, 0, sizeof(unsigned), st);
+    maxabs_x_kernel<<<4 * s->sms, 256, 0, st>>>(X, ldx, rows, n, s->maxbits);
+    unsigned mb = 0;
+    cudaMemcpyAsync(&mb, s->maxbits, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+      tc_destroy(s);
+      return 1;
+    }
+    float mx;
+    memcpy(&mx, &mb, sizeof(mx));
+    xmax = (double)mx;
+    count_launch();
   }
-  float mx;
-  memcpy(&mx, &mb, sizeof(mx));
-  s->sx = pow2_scale((double)mx);
+  s->sx = pow2_scale(xmax);
   pack_x_kernel<<<8 * s->sms, 256, 0, st>>>(X, ldx, rows, n, s->sx, s->tiles_per_row, s->Mt,
                                             (uint4*)s->xp[0], (uint4*)s->xp[1], (uint4*)s->xp[2],
                                             (uint4*)s->xp[3]);
-  count_launch(2);
+  count_launch();
   // A second, transposed copy makes pass 2 a K-major stream of whole tiles like pass 1 (the
   // MN-major gather of 1 KB pieces measured ~2x slower).  It costs another 4 bytes per element
   // of HBM capacity and is skipped (ENMF_TC_XT=0, or not enough free memory) in favour of the

@@ -82,20 +82,7 @@ __device__ __forceinline__ void bar_compute() {
   asm volatile("bar.sync 1, %0;" ::"n"(32 * COMPUTE_WARPS) : "memory");
 }
 
-// Register-only digit handling (no addressable local arrays).  digits_word(t), |t| < 64.5:
-// t rounded to the 2^-21 grid (error <= 2^-22, the digits4 bound) split into balanced base-2^7
-// digits d0 + d1/2^7 + d2/2^14 + d3/2^21, digit pl in byte pl -- integer arithmetic only.
-__device__ __forceinline__ uint32_t digits_word(double t) {
-  int n = __double2int_rn(t * 0x1p21);
-  const int d3 = ((n + 64) & 127) - 64;
-  n = (n - d3) >> 7;
-  const int d2 = ((n + 64) & 127) - 64;
-  n = (n - d2) >> 7;
-  const int d1 = ((n + 64) & 127) - 64;
-  const int d0 = (n - d1) >> 7;
-  return (uint32_t)(d0 & 255) | ((uint32_t)(d1 & 255) << 8) | ((uint32_t)(d2 & 255) << 16) |
-         ((uint32_t)(d3 & 255) << 24);
-}
+// digits_word(t): tc_ptx.cuh
 struct Pack16 { uint32_t w[4][4]; };   // [plane][word]: 16 columns of the 4 digit planes
 __device__ __forceinline__ void pack_put(Pack16& pk, int k, uint32_t dw) {
 #pragma unroll

@@ -75,9 +75,11 @@ def test_hals_trajectory_50_sweeps(cfg, prec):
     """50 HALS sweeps from a shared feasible point: final factors within 1e-4, the direct
     objective within 1e-4, and the per-sweep trace-form f within 1e-4 of the oracle's direct f
     -- or, on the tensor-core path, within its conditioning bound: the trace form
-    ||X||^2 - 2<X^T U, V> + <U^T U, V^T V> turns the ~1e-9 relative error of X^T U into a
-    (||X||^2 / f) * 2e-9 error of f (SURVEY Hard part 2), which exceeds 1e-4 on these small
-    near-exact planted shapes (not at C5 scale, where entry errors average over 6e6 terms)."""
+    ||X||^2 - 2<X^T U, V> + <U^T U, V^T V> turns the relative error eps of the cross term
+    <X^T U, V> into a (||X||^2 / f) * eps error of f (SURVEY Hard part 2), which exceeds 1e-4
+    on these small near-exact shapes (not at C5 scale, where entry errors average over 6e6
+    terms).  eps = 1e-8 is the cross-term bound test_tc_contractions_match_oracle asserts
+    (measured 1e-9 .. 4e-9 at these K)."""
     h, X, _ = make(cfg, precision=prec)
     U0, V0, _, _ = rotated_point(X, cfg.r)
     U0, V0 = np.abs(U0), np.abs(V0)
@@ -87,7 +89,7 @@ def test_hals_trajectory_50_sweeps(cfg, prec):
     Uo, Vo, f_or = oracle_sweeps(X, U0, V0, oracle.SweepState(stage=1), 50, cfg.r)
     err = np.abs(f_gpu - f_or) / f_or
     cond = oracle.xnorm2(X) / f_or
-    bound = np.maximum(1e-4, 2e-9 * cond) if prec == TC else 1e-4
+    bound = np.maximum(1e-4, 1e-8 * cond) if prec == TC else 1e-4
     print(f"{cfg.name} prec={h.precision}: max f err {err.max():.2e} (max ||X||^2/f "
           f"{cond.max():.1e})")
     assert np.all(err < bound), err
@@ -143,7 +145,7 @@ def test_ascent_then_hals_trajectory(cfg, prec):
     err = np.abs(f_gpu - f_or) / f_or
     bound = max(1e-4, 10 * floor[0])
     if prec == TC:
-        bound = np.maximum(bound, 2e-9 * oracle.xnorm2(X) / f_or)
+        bound = np.maximum(bound, 1e-8 * oracle.xnorm2(X) / f_or)
     print(f"{cfg.name} prec={h.precision}: max f err {err.max():.2e}, oracle 1-ulp spread "
           f"{floor[0]:.2e}, stages {info['ascent_sweeps']}+{info['hals_sweeps']}")
     assert np.all(err < bound), err

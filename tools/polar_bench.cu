@@ -34,6 +34,24 @@ int main() {
   enmf::polar_newton(M, k, R, fail, 0, iters);
   int fh, ih; cudaMemcpy(&fh, fail, 4, cudaMemcpyDeviceToHost); cudaMemcpy(&ih, iters, 4, cudaMemcpyDeviceToHost);
   printf("polar_newton: %.3f ms/call fail=%d iters=%d (%s)\n", ms / 10, fh, ih, cudaGetErrorString(cudaGetLastError()));
+  {
+    double* nsw; int* st2;
+    cudaMalloc(&nsw, 8 * (3 * k * k + 256)); cudaMalloc(&st2, 8);
+    double* R3; cudaMalloc(&R3, 8 * k * k);
+    enmf::polar_ns(M, k, R3, st2, nsw, 48, 0);
+    cudaEventRecord(a);
+    for (int i = 0; i < 10; ++i) enmf::polar_ns(M, k, R3, st2, nsw, 48, 0);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    int sh[2]; cudaMemcpy(sh, st2, 8, cudaMemcpyDeviceToHost);
+    std::vector<double> r3(k * k), r1(k * k);
+    cudaMemcpy(r3.data(), R3, 8 * k * k, cudaMemcpyDeviceToHost);
+    cudaMemcpy(r1.data(), R, 8 * k * k, cudaMemcpyDeviceToHost);
+    double d = 0, n = 0;
+    for (int i = 0; i < k * k; ++i) { d += (r1[i] - r3[i]) * (r1[i] - r3[i]); n += r1[i] * r1[i]; }
+    printf("polar_ns: %.3f ms/call done=%d fail=%d |R_ns - R_newton|/|R| = %.3e (%s)\n", ms / 10,
+           sh[0], sh[1], sqrt(d / n), cudaGetErrorString(cudaGetLastError()));
+  }
   cudaEventRecord(a);
   for (int i = 0; i < 3; ++i) {
     enmf::jacobi_svd(M, k, Cs, sv, Ds, jw, 0);
