@@ -61,7 +61,8 @@ typedef struct {
   int64_t row_count;       /* X/U rows owned by this rank (m_global when world_size == 1) */
   int world_size;          /* ranks (GPUs) */
   int rank;                /* this rank */
-  const void* nccl_unique_id; /* 128-byte ncclUniqueId from rank 0; NULL if world_size == 1 */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId from rank 0; NULL if world_size == 1,
+                              or NULL with world_size > 1 to use enmf_set_host_allreduce */
   void* cuda_stream;       /* cudaStream_t for every call; NULL = legacy default stream */
 } enmf_problem_t;
 
@@ -198,6 +199,15 @@ int64_t enmf_launch_count(enmf_handle_t h);
  * enmf_set_profiling call (synchronises the stream). */
 enmf_status_t enmf_set_profiling(enmf_handle_t h, int on);
 enmf_status_t enmf_get_profile(enmf_handle_t h, double* ms_host, int64_t* count_host);
+
+/* Host-mediated collectives for a multi-rank handle created without an NCCL id: every
+ * allreduce of the method (fp64) stages its buffer through pinned host memory and calls
+ * fn(ctx, buf_host, count, op) with op 0 = sum, 1 = min, 2 = max; fn must reduce in place
+ * across the ranks (same call order on every rank) and return 0.  Meant for validating the
+ * sharded path (e.g. gloo ranks sharing one GPU in tests); NCCL is the production path.
+ * ENMF_ERR_STATE if the handle already has an NCCL communicator. */
+typedef int (*enmf_host_allreduce_fn)(void* ctx, double* buf_host, int64_t count, int op);
+enmf_status_t enmf_set_host_allreduce(enmf_handle_t h, enmf_host_allreduce_fn fn, void* ctx);
 
 /* 128-byte ncclUniqueId for a multi-GPU job (call on rank 0, broadcast the bytes, pass them
  * in enmf_problem_t.nccl_unique_id on every rank). */

@@ -93,10 +93,14 @@ _sigs = {
     "enmf_launch_count": (ctypes.c_int64, [_H]),
     "enmf_set_profiling": (ctypes.c_int, [_H, ctypes.c_int]),
     "enmf_get_profile": (ctypes.c_int, [_H, _D, ctypes.POINTER(ctypes.c_int64)]),
+    "enmf_set_host_allreduce": (ctypes.c_int, [_H, ctypes.c_void_p, ctypes.c_void_p]),
     "enmf_nccl_unique_id": (ctypes.c_int, [_P]),
     "enmf_precision_name": (ctypes.c_char_p, [_H]),
     "enmf_status_string": (ctypes.c_char_p, [ctypes.c_int]),
 }
+_HOST_AR = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                            ctypes.c_int64, ctypes.c_int)
+
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(_lib, _name)
     _f.restype = _res
@@ -149,10 +153,11 @@ class Enmf:
         self.rows = int(row_count if row_count is not None else m)
         self._stream = stream if stream is not None else torch.cuda.current_stream()
         self._uid = None
-        if world_size > 1:
-            if nccl_id is None or len(nccl_id) != 128:
-                raise ValueError("world_size > 1 needs the 128-byte ncclUniqueId")
+        if world_size > 1 and nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("nccl_id must be the 128-byte ncclUniqueId")
             self._uid = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        # world_size > 1 without nccl_id: collectives via set_host_allreduce
         prob = Problem(self.m, self.n, self.r, self.row_begin, self.rows, int(world_size),
                        int(rank), ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None,
                        self._stream.cuda_stream)
@@ -247,6 +252,26 @@ class Enmf:
                                  f.ctypes.data_as(_D) if trace else None, ctypes.byref(info)),
                "enmf_iterate")
         return f[: int(n_iters)], _info_dict(info)
+
+    def set_host_allreduce(self, fn):
+        """Multi-rank handle without an NCCL id: fn(buf, op) reduces the float64 numpy array
+        buf in place across the ranks (op 'sum' | 'min' | 'max'); see enmf_set_host_allreduce.
+        Typically a torch.distributed (gloo) all_reduce on torch.from_numpy(buf)."""
+        ops = {0: "sum", 1: "min", 2: "max"}
+
+        def tramp(ctx, buf, count, op):
+            try:
+                arr = np.ctypeslib.as_array(buf, shape=(count,))
+                fn(arr, ops[op])
+                return 0
+            except Exception:           # noqa: BLE001 -- reported as ENMF_ERR_NCCL
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._host_ar = _HOST_AR(tramp)        # keep the callback alive with the handle
+        _check(_lib.enmf_set_host_allreduce(self._h, ctypes.cast(self._host_ar, ctypes.c_void_p),
+                                            None), "enmf_set_host_allreduce")
 
     def iterate_host(self, U, V, n_iters, trace=True):
         """enmf_iterate_host: U (row_count x r) and V (n x r) are contiguous fp32 CPU tensors

@@ -36,9 +36,29 @@ enmf_status_t dalloc_bytes(void** p, size_t bytes) {
 }
 
 enmf_status_t ar(enmf_handle_t h, double* buf, size_t count, CommOp op) {
-  if (h->prob.world_size <= 1) return ENMF_OK;
-  return comm_allreduce(h->comm, buf, count, CommType::F64, op, h->st) == 0 ? ENMF_OK
-                                                                           : ENMF_ERR_NCCL;
+  if (h->prob.world_size <= 1 || count == 0) return ENMF_OK;
+  if (h->comm)
+    return comm_allreduce(h->comm, buf, count, CommType::F64, op, h->st) == 0 ? ENMF_OK
+                                                                             : ENMF_ERR_NCCL;
+  if (!h->host_ar) return ENMF_ERR_STATE;
+  // host-mediated collective (enmf_set_host_allreduce): stream-ordered staging through a
+  // pinned buffer; no device-side waiting on other ranks
+  if (h->host_ar_cap < count) {
+    if (h->host_ar_buf) cudaFreeHost(h->host_ar_buf);
+    h->host_ar_buf = nullptr;
+    h->host_ar_cap = 0;
+    CUDA_TRY(cudaMallocHost((void**)&h->host_ar_buf, sizeof(double) * count));
+    h->host_ar_cap = count;
+  }
+  CUDA_TRY(cudaMemcpyAsync(h->host_ar_buf, buf, sizeof(double) * count, cudaMemcpyDeviceToHost,
+                           h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  const int o = op == CommOp::Sum ? 0 : (op == CommOp::Min ? 1 : 2);
+  if (h->host_ar(h->host_ar_ctx, h->host_ar_buf, (int64_t)count, o) != 0) return ENMF_ERR_NCCL;
+  CUDA_TRY(cudaMemcpyAsync(buf, h->host_ar_buf, sizeof(double) * count, cudaMemcpyHostToDevice,
+                           h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));   // the pinned buffer is reused by the next call
+  return ENMF_OK;
 }
 
 enmf_status_t validate_ld(const void* p, int64_t ld, int64_t cols) {
@@ -312,6 +332,14 @@ enmf_status_t enmf_cross_terms(enmf_handle_t h, const float* U, int64_t ldu, con
   return check_launch();
 }
 
+enmf_status_t enmf_set_host_allreduce(enmf_handle_t h, enmf_host_allreduce_fn fn, void* ctx) {
+  if (!h) return ENMF_ERR_INVALID_ARG;
+  if (h->comm) return ENMF_ERR_STATE;          // the handle already has an NCCL communicator
+  h->host_ar = fn;
+  h->host_ar_ctx = ctx;
+  return ENMF_OK;
+}
+
 enmf_status_t enmf_nccl_unique_id(void* out128) {
   if (!out128) return ENMF_ERR_INVALID_ARG;
   return comm_unique_id(out128) == 0 ? ENMF_OK : ENMF_ERR_NCCL;
@@ -331,6 +359,7 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (void* b : h->arena_extra) cudaFree(b);
+  if (h->host_ar_buf) cudaFreeHost(h->host_ar_buf);
   if (h->st2) {
     cudaStreamSynchronize(h->st2);
     cudaStreamDestroy(h->st2);
@@ -360,7 +389,7 @@ enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
     return ENMF_ERR_SHAPE;
   if (prob->world_size == 1 && (prob->row_begin != 0 || prob->row_count != m))
     return ENMF_ERR_SHAPE;
-  if (prob->world_size > 1 && !prob->nccl_unique_id) return ENMF_ERR_INVALID_ARG;
+  // world_size > 1 without an NCCL id: collectives go through enmf_set_host_allreduce
   if (o.oversample < 0 || o.power_iters < 0 || o.admm_iters < 0 || o.lift_steps < 1 ||
       o.pbcd_max_iter < 1 || o.pbcd_max_iter > 1000 || !(o.pbcd_eps >= 0.0) ||
       o.precision < ENMF_PREC_AUTO || o.precision > ENMF_PREC_TC)
@@ -394,7 +423,7 @@ enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
   ALLOC(h->minparts, (size_t)kRowGrid);
   ALLOC(h->pgsum, (size_t)(o.pbcd_max_iter + 1));
 #undef ALLOC
-  if (s == ENMF_OK && prob->world_size > 1) {
+  if (s == ENMF_OK && prob->world_size > 1 && prob->nccl_unique_id) {
     if (comm_init(&h->comm, prob->nccl_unique_id, prob->world_size, prob->rank) != 0)
       s = ENMF_ERR_NCCL;
   }

@@ -57,6 +57,11 @@ struct enmf_handle_s {
   // next X pass packs the factor without a separate scan; valid only within one iterate call
   unsigned long long* fmax_uv = nullptr;   // [2][128]: U, V
   bool umax_valid = false, vmax_valid = false;
+  // host-mediated collectives (enmf_set_host_allreduce) when there is no NCCL communicator
+  enmf_host_allreduce_fn host_ar = nullptr;
+  void* host_ar_ctx = nullptr;
+  double* host_ar_buf = nullptr;   // pinned staging
+  size_t host_ar_cap = 0;
   // init workspace arena (enmf_init.cu DevBuf): kept across calls, grown on demand
   uint8_t* arena = nullptr;
   size_t arena_bytes = 0, arena_need = 0;

@@ -47,8 +47,10 @@ def test_create_rejects_bad_shapes_without_gpu():
     assert E._lib.enmf_create(ctypes.byref(prob), None, ctypes.byref(h)) == -2
     prob = E.Problem(10, 5, 2, 3, 10, 1, 0, None, None)     # row range outside m
     assert E._lib.enmf_create(ctypes.byref(prob), None, ctypes.byref(h)) == -2
-    prob = E.Problem(10, 5, 2, 0, 5, 2, 0, None, None)      # world 2 without NCCL id
+    prob = E.Problem(10, 5, 2, 0, 5, 2, 2, None, None)      # rank outside the world
     assert E._lib.enmf_create(ctypes.byref(prob), None, ctypes.byref(h)) == -1
+    # (world 2 without an NCCL id is valid: collectives then go through
+    # enmf_set_host_allreduce -- tests/test_gpu_multirank.py)
 
 
 @pytest.mark.parametrize("m,world", [(200000, 8), (10, 3), (7, 7), (5, 1)])

@@ -1,0 +1,99 @@
+"""The multi-rank C-ABI path (X and U row-sharded, V replicated, allreduce of
+X^T U, the Grams, the PBCD stopping partials and the init collectives) exercised on ONE GPU:
+two processes (gloo) share cuda:0 and the handle's collectives go through
+enmf_set_host_allreduce -- stream-synchronous host staging, so no kernel of one rank ever waits
+on the other's.  NCCL itself is not exercised here (one GPU); everything around it is:
+  * V and the objective trace come out bitwise identical on both ranks;
+  * HALS sweeps from a shared feasible point match a single-rank run (the sharded sums differ
+    only in summation order);
+  * the sharded randomised SVD matches the single-rank singular values."""
+import multiprocessing as mp
+import socket
+
+import numpy as np
+import pytest
+
+from tests import multirank_worker
+
+pytestmark = pytest.mark.gpu
+
+FP64, TC = 1, 2
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawn(cfg_args, prec, mode, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=multirank_worker.run, args=(r, world, port, cfg_args, prec, mode, q))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=120)
+    errs = [r["error"] for r in res if "error" in r]
+    assert not errs, errs[0]
+    return sorted(res, key=lambda r: r["rank"])
+
+
+def _single(cfg_args, prec, mode):
+    import torch
+
+    import paper_2605_19325_b200 as E
+    import synth
+    from tests.gpu_common import to_dev
+    cfg = synth.ALL[cfg_args[0]].scaled(*cfg_args[1:]) if len(cfg_args) > 1 else \
+        synth.ALL[cfg_args[0]]
+    X = to_dev(synth.x_full(cfg))
+    h = E.Enmf(cfg.m, cfg.n, cfg.r, precision=prec)
+    if mode == "init":
+        U = torch.empty(cfg.m, cfg.r, device="cuda")
+        V = torch.empty(cfg.n, cfg.r, device="cuda")
+        info = h.init(X, U, V)
+        f, _ = h.iterate(U, V, 12)
+        return np.array(info["sigma"]), f, U.cpu().numpy(), V.cpu().numpy()
+    g = np.random.default_rng(5)
+    U0 = g.random((cfg.m, cfg.r)).astype(np.float32)
+    V0 = g.random((cfg.n, cfg.r)).astype(np.float32)
+    h.set_data(X)
+    U, V = torch.from_numpy(U0).cuda(), torch.from_numpy(V0).cuda()
+    h.set_stage(1)
+    f, _ = h.iterate(U, V, 5)
+    return None, f, U.cpu().numpy(), V.cpu().numpy()
+
+
+CASES = [(("C1-planted",), FP64), (("C5-large-planted", 400, 300, 128, 128), TC)]
+
+
+@pytest.mark.parametrize("cfg_args,prec", CASES, ids=["C1-fp64", "C5shape-tc"])
+def test_two_ranks_hals_match_single_rank(cfg_args, prec):
+    r0, r1 = _spawn(cfg_args, prec, "hals")
+    assert np.array_equal(r0["V"], r1["V"]), "V must be bitwise identical on all ranks"
+    assert np.array_equal(r0["f"], r1["f"])
+    _, f, U, V = _single(cfg_args, prec, "hals")
+    Ug = np.vstack([r0["U"], r1["U"]])
+    tol = 1e-9 if prec == FP64 else 2e-6
+    eu = np.linalg.norm(Ug - U) / np.linalg.norm(U)
+    ev = np.linalg.norm(r0["V"] - V) / np.linalg.norm(V)
+    ef = np.max(np.abs(r0["f"] - f) / f)
+    print(f"{cfg_args[0]} prec={prec}: U {eu:.2e} V {ev:.2e} f {ef:.2e}")
+    assert eu < tol and ev < tol and ef < tol
+
+
+@pytest.mark.parametrize("cfg_args,prec", CASES, ids=["C1-fp64", "C5shape-tc"])
+def test_two_ranks_init_and_ascent_consistent(cfg_args, prec):
+    r0, r1 = _spawn(cfg_args, prec, "init")
+    assert np.array_equal(r0["V"], r1["V"])
+    assert np.array_equal(r0["f"], r1["f"])
+    assert np.array_equal(r0["sigma"], r1["sigma"])
+    assert r0["it"]["ascent_sweeps"] == r1["it"]["ascent_sweeps"] == 10
+    sigma, _, _, _ = _single(cfg_args, prec, "init")
+    es = np.max(np.abs(r0["sigma"] - sigma) / sigma)
+    print(f"{cfg_args[0]} prec={prec}: sigma {es:.2e}")
+    assert es < (1e-10 if prec == FP64 else 1e-7)
