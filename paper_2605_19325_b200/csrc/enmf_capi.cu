@@ -241,9 +241,23 @@ enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ld
   // V block: Q = X^T U_new (allreduced), G_U = U_new^T U_new (PAPER.md:220 uses U^(k+1))
   ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh));
   ENMF_TRY(contract_xtu(h, U, ldu, h->Q, h->umax_valid ? h->fmax_uv : nullptr));
-  ENMF_TRY(block_update(h, V, ldv, h->n, h->Q, h->GU, S_LAMV, I_KSTAR_V, S_MINV, false,
-                        maybe_ascent, vmax));
-  h->vmax_valid = vmax != nullptr;
+  if (sh) {
+    // V block sharded by rows (V rows are independent given Q and G_U): each
+    // rank updates its slice (PBCD stopping partials and min allreduced like the U block),
+    // then the full V is reassembled bitwise identically on every rank
+    const int64_t vb = h->v_begin, vc = h->v_count, r = h->r;
+    ENMF_TRY(block_update(h, V + vb * ldv, ldv, vc, h->Q + vb * r, h->GU, S_LAMV, I_KSTAR_V,
+                          S_MINV, true, maybe_ascent, nullptr));
+    CUDA_TRY(cudaMemsetAsync(h->Vg, 0, sizeof(double) * h->n * r, st));
+    if (vc > 0) f32_to_f64(V + vb * ldv, ldv, vc, r, h->Vg + vb * r, st);
+    ENMF_TRY(ar(h, h->Vg, (size_t)(h->n * r), CommOp::Sum));
+    f64_to_f32(h->Vg, h->n, r, nullptr, V, ldv, st);
+    h->vmax_valid = false;
+  } else {
+    ENMF_TRY(block_update(h, V, ldv, h->n, h->Q, h->GU, S_LAMV, I_KSTAR_V, S_MINV, false,
+                          maybe_ascent, vmax));
+    h->vmax_valid = vmax != nullptr;
+  }
   if (hk.v_download) {
     CUDA_TRY(cudaEventRecord(h->ev_a, st));
     CUDA_TRY(cudaStreamWaitEvent(h->st2, h->ev_a, 0));
@@ -355,7 +369,7 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
   if (h->st) cudaStreamSynchronize(h->st);
   void* bufs[] = {h->dscal, h->dint, h->P, h->Q, h->GU, h->GV, h->work, h->parts,
                   h->minparts, h->pgsum, h->snaps, h->ftrace, h->x_owned, h->W64,
-                  h->tcpb_ws, h->fmax_uv, h->Ud, h->Vd, h->arena};
+                  h->tcpb_ws, h->fmax_uv, h->Ud, h->Vd, h->arena, h->Vg};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (void* b : h->arena_extra) cudaFree(b);
@@ -423,6 +437,13 @@ enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
   ALLOC(h->minparts, (size_t)kRowGrid);
   ALLOC(h->pgsum, (size_t)(o.pbcd_max_iter + 1));
 #undef ALLOC
+  if (s == ENMF_OK && prob->world_size > 1) {
+    // V slice of this rank: contiguous blocks, the first n % world ranks one row longer
+    const int64_t base = n / prob->world_size, extra = n % prob->world_size;
+    h->v_begin = prob->rank * base + std::min<int64_t>(prob->rank, extra);
+    h->v_count = base + (prob->rank < extra ? 1 : 0);
+    s = dalloc(&h->Vg, (size_t)(n * r));
+  }
   if (s == ENMF_OK && prob->world_size > 1 && prob->nccl_unique_id) {
     if (comm_init(&h->comm, prob->nccl_unique_id, prob->world_size, prob->rank) != 0)
       s = ENMF_ERR_NCCL;

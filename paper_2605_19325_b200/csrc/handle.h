@@ -57,6 +57,10 @@ struct enmf_handle_s {
   // next X pass packs the factor without a separate scan; valid only within one iterate call
   unsigned long long* fmax_uv = nullptr;   // [2][128]: U, V
   bool umax_valid = false, vmax_valid = false;
+  // multi-rank V block: this rank updates V rows [v_begin, v_begin + v_count) and the full V
+  // is reassembled by a zero-padded fp64 allreduce (exact: adding zeros), SURVEY §8(e)
+  int64_t v_begin = 0, v_count = 0;
+  double* Vg = nullptr;            // n x r fp64 staging of the gather
   // host-mediated collectives (enmf_set_host_allreduce) when there is no NCCL communicator
   enmf_host_allreduce_fn host_ar = nullptr;
   void* host_ar_ctx = nullptr;

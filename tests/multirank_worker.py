@@ -5,6 +5,16 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def ascent_point(cfg):
+    """A deterministic infeasible fp32 point and its lift constants 1.001 |min| / L (R9)."""
+    import numpy as np
+    g = np.random.default_rng(7)
+    U0 = (g.random((cfg.m, cfg.r)) - 0.15).astype(np.float32)
+    V0 = (g.random((cfg.n, cfg.r)) - 0.15).astype(np.float32)
+    lam = lambda A: 1.001 * abs(min(float(A.min()), 0.0)) / 10.0   # noqa: E731
+    return U0, V0, lam(U0), lam(V0)
+
+
 def run(rank, world, port, cfg_args, prec, mode, out_q):
     sys.path.insert(0, ROOT)
     import numpy as np
@@ -39,6 +49,14 @@ def run(rank, world, port, cfg_args, prec, mode, out_q):
             info = h.init(X, U, V)
             f, it = h.iterate(U, V, 12)
             res.update(sigma=np.array(info["sigma"]), f=f, it=it)
+        elif mode == "ascent":                  # lift + PBCD sweeps from a shared point
+            U0, V0, lu, lv = ascent_point(cfg)
+            h.set_data(X)
+            U = torch.from_numpy(U0[begin:begin + count]).cuda()
+            V = torch.from_numpy(V0).cuda()
+            h.set_stage(0, lu, lv)
+            f, it = h.iterate(U, V, 3)
+            res.update(f=f, it=it)
         else:                                   # HALS sweeps from a shared feasible point
             g = np.random.default_rng(5)
             U0 = g.random((cfg.m, cfg.r)).astype(np.float32)

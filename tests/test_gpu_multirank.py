@@ -58,6 +58,13 @@ def _single(cfg_args, prec, mode):
         info = h.init(X, U, V)
         f, _ = h.iterate(U, V, 12)
         return np.array(info["sigma"]), f, U.cpu().numpy(), V.cpu().numpy()
+    if mode == "ascent":
+        U0, V0, lu, lv = multirank_worker.ascent_point(cfg)
+        h.set_data(X)
+        U, V = torch.from_numpy(U0).cuda(), torch.from_numpy(V0).cuda()
+        h.set_stage(0, lu, lv)
+        f, _ = h.iterate(U, V, 3)
+        return None, f, U.cpu().numpy(), V.cpu().numpy()
     g = np.random.default_rng(5)
     U0 = g.random((cfg.m, cfg.r)).astype(np.float32)
     V0 = g.random((cfg.n, cfg.r)).astype(np.float32)
@@ -99,3 +106,21 @@ def test_two_ranks_init_and_ascent_consistent(cfg_args, prec):
     es = np.max(np.abs(r0["sigma"] - sigma) / sigma)
     print(f"{cfg_args[0]} prec={prec}: sigma {es:.2e}")
     assert es < (1e-10 if prec == FP64 else 1e-6)   # tc: the rtol of the SVD-vs-oracle test
+
+
+@pytest.mark.parametrize("cfg_args,prec", CASES, ids=["C1-fp64", "C5shape-tc"])
+def test_two_ranks_ascent_sharded_v(cfg_args, prec):
+    """Lift + PBCD sweeps with the V block sharded across the ranks (Alg. 2's stopping rule
+    summed over both slices): V and f bitwise identical on the ranks; on the fp64 path the
+    factors equal the single-rank run's up to the summation order of the stopping sums."""
+    r0, r1 = _spawn(cfg_args, prec, "ascent")
+    assert np.array_equal(r0["V"], r1["V"])
+    assert np.array_equal(r0["f"], r1["f"])
+    assert r0["it"] == r1["it"] and r0["it"]["ascent_sweeps"] == 3
+    if prec == FP64:
+        _, f, U, V = _single(cfg_args, prec, "ascent")
+        Ug = np.vstack([r0["U"], r1["U"]])
+        eu = np.linalg.norm(Ug - U) / np.linalg.norm(U)
+        ev = np.linalg.norm(r0["V"] - V) / np.linalg.norm(V)
+        print(f"{cfg_args[0]} ascent: U {eu:.2e} V {ev:.2e}")
+        assert eu < 1e-12 and ev < 1e-12
