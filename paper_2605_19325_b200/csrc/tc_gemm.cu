@@ -535,40 +535,46 @@ __device__ __forceinline__ void pack_digits16(F val, uint32_t (&w)[4][4]) {
 __global__ void __launch_bounds__(256)
 pack_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n, double sx,
               int64_t tiles_per_row, int64_t Mt, uint4* p0, uint4* p1, uint4* p2, uint4* p3) {
-  const int64_t cpr = tiles_per_row * 4;                 // 16-byte chunks per padded row
-  const bool vec = (ldx & 3) == 0 && (n & 3) == 0 && ((uintptr_t)X & 15) == 0;
-  // rows by blocks, a row's chunks by threads: no 64-bit division per element
-  for (int64_t i = blockIdx.x; i < Mt * BM; i += gridDim.x) {
-    const float* xr = X + i * ldx;
-    const int64_t mt = i / BM, g = (i % BM) / 8, ri = i % 8;
-    for (int64_t jc = threadIdx.x; jc < cpr; jc += blockDim.x) {
-      const int64_t j0 = jc * 16;
-      float v[16];
-      if (i < rows && vec && j0 + 16 <= n) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 f = *reinterpret_cast<const float4*>(xr + j0 + 4 * q);
-          v[4 * q] = f.x;
-          v[4 * q + 1] = f.y;
-          v[4 * q + 2] = f.z;
-          v[4 * q + 3] = f.w;
+  // one 128-row x 64-column tile at a time: coalesced row reads into shared memory, then the
+  // tile's 512 16-byte chunks per plane in memory order (chunk w = (kc*16 + g)*8 + ri), so the
+  // writes are contiguous too (the row-by-row form wrote 16 B per 2 KB stride)
+  __shared__ float tx[BM][BK + 1];
+  const bool vec = (ldx & 3) == 0 && ((uintptr_t)X & 15) == 0;
+  for (int64_t t = blockIdx.x; t < Mt * tiles_per_row; t += gridDim.x) {
+    const int64_t mt = t / tiles_per_row, kt = t - mt * tiles_per_row;
+    __syncthreads();
+    for (int e = threadIdx.x; e < BM * BK / 4; e += blockDim.x) {
+      const int il = e / (BK / 4), jq = e % (BK / 4);
+      const int64_t i = mt * BM + il, j = kt * BK + 4 * jq;
+      float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < rows) {
+        const float* xr = X + i * ldx;
+        if (vec && j + 4 <= n) {
+          f = *reinterpret_cast<const float4*>(xr + j);
+        } else {
+          if (j < n) f.x = xr[j];
+          if (j + 1 < n) f.y = xr[j + 1];
+          if (j + 2 < n) f.z = xr[j + 2];
+          if (j + 3 < n) f.w = xr[j + 3];
         }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = (i < rows && j0 + k < n) ? xr[j0 + k] : 0.0f;
       }
-      // digits of X sx (exact: fp32 times a power of two), packed in registers
-      uint32_t w[4][4];
-      pack_digits16([&](int k) { return (double)v[k] * sx; }, w);
-      const int64_t kt = j0 / BK, kc = (j0 % BK) / 16;
-      // planes interleaved per tile: tile t, plane pl at (t * PLANES + pl) * TILE_A (p_pl = base +
-      // pl * TILE_A), so one stage's planes are one contiguous bulk copy
-      const int64_t idx =
-          ((mt * tiles_per_row + kt) * PLANES * TILE_A + (kc * 16 + g) * 128 + ri * 16) / 16;
-      p0[idx] = make_uint4(w[0][0], w[0][1], w[0][2], w[0][3]);
-      p1[idx] = make_uint4(w[1][0], w[1][1], w[1][2], w[1][3]);
-      p2[idx] = make_uint4(w[2][0], w[2][1], w[2][2], w[2][3]);
-      p3[idx] = make_uint4(w[3][0], w[3][1], w[3][2], w[3][3]);
+      tx[il][4 * jq] = f.x;
+      tx[il][4 * jq + 1] = f.y;
+      tx[il][4 * jq + 2] = f.z;
+      tx[il][4 * jq + 3] = f.w;
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < BM * BK / 16; w += blockDim.x) {
+      const int kc = w >> 7, g = (w >> 3) & 15, ri = w & 7;
+      const int il = g * 8 + ri;
+      uint32_t wd[4][4];
+      pack_digits16([&](int k) { return (double)tx[il][kc * 16 + k] * sx; }, wd);
+      // planes interleaved per tile: tile t, plane pl at (t * PLANES + pl) * TILE_A
+      const int64_t idx = (t * PLANES * TILE_A) / 16 + w;
+      p0[idx] = make_uint4(wd[0][0], wd[0][1], wd[0][2], wd[0][3]);
+      p1[idx] = make_uint4(wd[1][0], wd[1][1], wd[1][2], wd[1][3]);
+      p2[idx] = make_uint4(wd[2][0], wd[2][1], wd[2][2], wd[2][3]);
+      p3[idx] = make_uint4(wd[3][0], wd[3][1], wd[3][2], wd[3][3]);
     }
   }
 }
