@@ -63,3 +63,64 @@ def test_c5_fullsize_hals_sweep_sampled():
     ev = np.linalg.norm(Vg[cols] - Vo) / np.linalg.norm(Vo)
     print(f"C5 full size, sampled HALS update: U rows {eu:.2e}, V rows {ev:.2e}")
     assert eu < 1e-5 and ev < 1e-5
+
+
+def test_c5_fullsize_ascent_sweep_sampled():
+    """One ascent sweep (lift + tensor-core PBCD on both blocks) at C5 full size.  PBCD rows
+    are independent given (C, G) and the global iteration count k* (Alg. 2's stopping rule
+    sums over all rows), so sampled rows are recomputed by the oracle running exactly the
+    GPU's k* iterations (eps = 0).  Tolerance as for every ascent check (R26):
+    max(1e-5, 10 x the oracle's own one-ulp spread on the same rows)."""
+    import torch
+    import paper_2605_19325_b200 as E
+    from tests.gpu_common import ulp_perturb
+    if not _mem_ok():
+        pytest.skip("needs ~110 GB of free device memory")
+    cfg = synth.C5
+    m, n, r = cfg.m, cfg.n, cfg.r
+    X = torch.empty(m, n, device="cuda")
+    synth.x_rows_device(cfg, 0, m, X)
+    g = np.random.default_rng(11)
+    U0 = (g.random((m, r)) - 0.15).astype(np.float32)
+    V0 = (g.random((n, r)) - 0.15).astype(np.float32)
+    lu = 1.001 * abs(float(U0.min())) / 10.0          # R9 lift constants
+    lv = 1.001 * abs(float(V0.min())) / 10.0
+    U, V = torch.from_numpy(U0).cuda(), torch.from_numpy(V0).cuda()
+    h = E.Enmf(m, n, r, precision=E.PREC_TC)
+    h.set_data(X)
+    h.set_stage(0, lu, lv)
+    f, info = h.iterate(U, V, 1)
+    assert info["ascent_sweeps"] == 1
+    ku, kv = info["pbcd_iters_u"], info["pbcd_iters_v"]
+    Ug, Vg = U.cpu().numpy().astype(np.float64), V.cpu().numpy().astype(np.float64)
+    del X
+    torch.cuda.empty_cache()
+
+    def block(F0, C, G, lam, k):
+        Fl = oracle.lift(F0.astype(np.float64), lam)
+        M = (Fl >= 0).astype(np.uint8)
+        out, _, _, _ = oracle.pbcd(Fl, C, G, M, eps=0.0, max_iter=k)
+        return out.astype(np.float32).astype(np.float64)
+
+    # U block on 48 sampled rows: P_i = X_i V0, G = V0^T V0 (the V the U block saw)
+    r0 = int(g.integers(0, m - 48))
+    rows = np.arange(r0, r0 + 48)
+    V0d = V0.astype(np.float64)
+    G = V0d.T @ V0d
+    Pr = oracle.xv(synth.x_block(cfg, r0, 48, 0, n), V0d)
+    Uo = block(U0[rows], Pr, G, lu, ku)
+    Up = block(ulp_perturb(U0[rows].astype(np.float64), 1), Pr, G, lu, ku)
+    eu = np.linalg.norm(Ug[rows] - Uo) / np.linalg.norm(Uo)
+    fu = np.linalg.norm(Up - Uo) / np.linalg.norm(Uo)
+    # V block on 16 sampled rows: Q_j = X[:, j]^T U_new (the GPU's), H = U_new^T U_new
+    c0 = int(g.integers(0, n - 16))
+    cols = np.arange(c0, c0 + 16)
+    H = Ug.T @ Ug
+    Qc = oracle.xtu(synth.x_block(cfg, 0, m, c0, 16), Ug)
+    Vo = block(V0[cols], Qc, H, lv, kv)
+    Vp = block(ulp_perturb(V0[cols].astype(np.float64), 2), Qc, H, lv, kv)
+    ev = np.linalg.norm(Vg[cols] - Vo) / np.linalg.norm(Vo)
+    fv = np.linalg.norm(Vp - Vo) / np.linalg.norm(Vo)
+    print(f"C5 full size, sampled ascent update (k* = {ku}/{kv}): U rows {eu:.2e} "
+          f"(floor {fu:.1e}), V rows {ev:.2e} (floor {fv:.1e})")
+    assert eu < max(1e-5, 10 * fu) and ev < max(1e-5, 10 * fv)
