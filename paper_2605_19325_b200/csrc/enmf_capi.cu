@@ -709,7 +709,6 @@ enmf_status_t enmf_kkt_residual(enmf_handle_t h, const float* U, int64_t ldu, co
   fold(hv, sv);
   if (sh) {
     // combine the U-block statistics over ranks (V is replicated: counted once)
-    double* d = h->dscal + S_SCRATCH;
     double sums[3] = {su[1], su[3], su[6]}, maxs[2] = {su[0], su[2]}, mins[2] = {su[4], su[5]};
     double* buf = h->work;
     CUDA_TRY(cudaMemcpyAsync(buf, sums, sizeof(sums), cudaMemcpyHostToDevice, h->st));
@@ -721,7 +720,6 @@ enmf_status_t enmf_kkt_residual(enmf_handle_t h, const float* U, int64_t ldu, co
     double all[7];
     CUDA_TRY(cudaMemcpyAsync(all, buf, sizeof(all), cudaMemcpyDeviceToHost, h->st));
     CUDA_TRY(cudaStreamSynchronize(h->st));
-    (void)d;
     su[1] = all[0]; su[3] = all[1]; su[6] = all[2]; su[0] = all[3]; su[2] = all[4];
     su[4] = all[5]; su[5] = all[6];
   }

@@ -54,7 +54,6 @@ constexpr int STAGES = 3;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 32 * (2 + EPI_WARPS);
 constexpr int PLANES = 4;
-constexpr int NPROD = 10;
 constexpr int TILE_A = BM * BK;                 // bytes per X tile per plane (8 KB)
 constexpr int MAX_TILE_B = 128 * BK;            // bytes per factor tile per plane (<= 8 KB)
 constexpr int STAGE_BYTES = PLANES * TILE_A + PLANES * MAX_TILE_B;   // 64 KB

@@ -66,7 +66,7 @@ def run(rank, world, port, cfg_args, prec, mode, out_q):
             V = torch.from_numpy(V0).cuda()
             h.set_stage(1)
             f, it = h.iterate(U, V, 5)
-            res.update(f=f, it=it)
+            res.update(f=f, it=it, kkt=h.kkt(U, V), fx=h.objective(U, V, exact=True))
         res.update(U=U.cpu().numpy(), V=V.cpu().numpy())
         out_q.put(res)
         dist.destroy_process_group()

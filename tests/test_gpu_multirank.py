@@ -72,6 +72,8 @@ def _single(cfg_args, prec, mode):
     U, V = torch.from_numpy(U0).cuda(), torch.from_numpy(V0).cuda()
     h.set_stage(1)
     f, _ = h.iterate(U, V, 5)
+    _single.kkt = h.kkt(U, V)
+    _single.fx = h.objective(U, V, exact=True)
     return None, f, U.cpu().numpy(), V.cpu().numpy()
 
 
@@ -91,6 +93,13 @@ def test_two_ranks_hals_match_single_rank(cfg_args, prec):
     ef = np.max(np.abs(r0["f"] - f) / f)
     print(f"{cfg_args[0]} prec={prec}: U {eu:.2e} V {ev:.2e} f {ef:.2e}")
     assert eu < tol and ev < tol and ef < tol
+    # the sharded KKT statistics and direct objective (rank-combined) match the single rank
+    assert r0["kkt"] == r1["kkt"] and r0["fx"] == r1["fx"]
+    assert abs(r0["fx"] - _single.fx) <= tol * _single.fx
+    rtol = 1e-9 if prec == FP64 else 1e-5     # as test_objective_and_kkt (per-rank digit scales)
+    for key in ("min_u", "min_v", "comp_max", "dual_viol"):
+        a, b = r0["kkt"][key], _single.kkt[key]
+        assert abs(a - b) <= rtol * max(abs(b), 1e-12 * _single.kkt["xnorm2"]), key
 
 
 @pytest.mark.parametrize("cfg_args,prec", CASES, ids=["C1-fp64", "C5shape-tc"])
