@@ -180,7 +180,13 @@ enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
     pbcd_commit(F, ldf, rows, r, h->snaps, h->pgsum, h->opt.pbcd_eps, mi, h->dint + kstar_slot,
                 stage, h->minparts, h->tc_pbcd, h->st, h->tc_pbcd ? colmax : nullptr);
   }
-  hals_rows(F, ldf, rows, r, C, G, stage, h->minparts, h->st, colmax);
+  if (h->tc_hals) {
+    if (tc_hals_rows(F, ldf, rows, r, C, G, reinterpret_cast<int8_t*>(h->tcpb_ws + 128),
+                     h->tcpb_ws, stage, h->minparts, kRowGrid, colmax, nullptr, h->st))
+      return ENMF_ERR_CUDA;
+  } else {
+    hals_rows(F, ldf, rows, r, C, G, stage, h->minparts, h->st, colmax);
+  }
   reduce_min(h->minparts, kRowGrid, h->dscal + min_slot, h->st);
   return sharded ? ar(h, h->dscal + min_slot, 1, CommOp::Min) : ENMF_OK;
 }
@@ -495,6 +501,8 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
   const char* tpe = getenv("ENMF_TC_PBCD");   // diagnostics: 0 keeps the SIMT fp64 PBCD
   h->tc_pbcd = prec == ENMF_PREC_TC && tc_pbcd_supported((int)h->r) && !(tpe && tpe[0] == '0');
   if (h->tc_pbcd && !h->tcpb_ws) ENMF_TRY(dalloc(&h->tcpb_ws, 128 + 4 * 128 * 128 / 8));
+  const char* the = getenv("ENMF_TC_HALS");   // diagnostics: 0 keeps the SIMT fp64 HALS
+  h->tc_hals = h->tc_pbcd && !(the && the[0] == '0');
   if (prec == ENMF_PREC_TC && !h->fmax_uv) ENMF_TRY(dalloc(&h->fmax_uv, 256));
   h->umax_valid = h->vmax_valid = false;
   h->precision = prec;

@@ -53,6 +53,7 @@ struct enmf_handle_s {
   enmf::TcState* tc = nullptr;
   double* tcpb_ws = nullptr;  // tensor-core PBCD: G digits (64 KB) + 128 column scales
   bool tc_pbcd = false;       // ascent PBCD on the tensor cores (precision TC, r <= 128)
+  bool tc_hals = false;       // HALS sweep on the tensor cores (tc_hals_rows)
   // tensor-core path: column maxima of |U| / |V| written by the block-update kernels, so the
   // next X pass packs the factor without a separate scan; valid only within one iterate call
   unsigned long long* fmax_uv = nullptr;   // [2][128]: U, V

@@ -44,5 +44,14 @@ int tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double*
                   const double* G, const double* lam, int max_iter, float* snaps,
                   double* pgparts, int8_t* gd_work, double* gscale_work, const int* stage,
                   cudaStream_t st);
+// HALS sweep of the rows with t = C - u G from exact int8-digit tcgen05
+// rounds, 32-column Gauss-Seidel blocks in registers (tc_pbcd.cu).  Runs only if *stage == 1.
+// Writes minparts[0, nparts) (nparts >= tc_hals_parts()); colmax (u64[r]) as hals_rows;
+// fallbacks (optional) counts rows redone in fp64 because u outgrew its digit scale.
+// gd_work / gscale_work as tc_pbcd_rows (the two never run in the same stage).  0 = launched.
+int tc_hals_parts();
+int tc_hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
+                 int8_t* gd_work, double* gscale_work, const int* stage, double* minparts,
+                 int nparts, unsigned long long* colmax, int* fallbacks, cudaStream_t st);
 
 }  // namespace enmf

@@ -409,8 +409,8 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
 // G (r x r fp64, symmetric) -> 4 digit planes of the B operand (row j of B = column j of G,
 // power-of-two scale t_j per column), layout (g * (KR/16) + kc) * 128 + ri * 16 + ki.
 __global__ void gdigits_kernel(const double* __restrict__ G, int r, int rp, int8_t* gd,
-                               double* gscale, const int* stage) {
-  if (stage != nullptr && *stage != 0) return;
+                               double* gscale, const int* stage, int want) {
+  if (stage != nullptr && *stage != want) return;
   __shared__ double t[128];
   for (int j = threadIdx.x; j < rp; j += blockDim.x) {
     double mx = 0.0;
@@ -431,6 +431,461 @@ __global__ void gdigits_kernel(const double* __restrict__ G, int r, int rp, int8
   }
 }
 
+
+// ------------------------------------------------------------------------------ HALS
+// HALS (reading R12) on the tensor cores, blocked Gauss-Seidel: a CTA holds
+// a 128-row tile, one thread per row.  t = c - u G for the remaining columns comes from an
+// exact int8-digit MMA round (u digits x G digits, 4 weight classes, as in PBCD) against the
+// CURRENT u; the sequential column updates then run in registers 32 columns at a time:
+//   for k in block:  u_k <- max(0, u_k + t_k / G_kk);  t_j -= (u_k' - u_k) G_kj  (j > k in block)
+// after which the block's new u is final (written to F), and a correction round adds
+// (u_new - u_old) G for the columns to its right (K = 32: the first round is the only full-K
+// product; the change is taken on the digit grid, so T = digits(u_new) G as if recomputed).
+// Same update as hals_kernel (the cross-block coupling is exact up to the digit rounding of u,
+// 2^-26 of its row maximum); r^2 of the 2 r^2 fp64 FMAs per row move to the tensor pipe, and
+// the per-(row, column) shuffles of the SIMT kernel disappear.  A row's c and the block's old
+// u are prefetched one block ahead with cp.async into the row's shared-memory slot (coalesced
+// per warp; consumers wait and __syncwarp), and the tile's digits are encoded a row per warp
+// step with coalesced loads.  A row
+// whose updated u outgrows its digit scale (|u| su >= 64, two bits of headroom) finishes the
+// columns right of that block with the plain sequential fp64 update (counted in *fallbacks).
+constexpr int HT = 128;                       // threads: one per row of the tile
+constexpr int HB = 32;                        // columns per Gauss-Seidel block
+constexpr int GT_BLK = HB * (HB + 1) / 2;     // packed upper triangle of a diagonal G block
+constexpr int CS_LD = 34;                     // doubles per thread slot (16-byte aligned rows)
+constexpr int US_LD = 36;                     // floats per thread slot
+constexpr int H_SMEM = 4 * PLANE_A + 4 * PLANE_B + (KR / HB) * GT_BLK * 8 + HT * CS_LD * 8 +
+                       HT * US_LD * 4;
+
+struct HParams {
+  float* F;
+  int64_t ldf;
+  int64_t rows;
+  int r;
+  const double* C;
+  const double* G;
+  const int8_t* gd;
+  const double* gscale;
+  const int* stage;
+  double* minparts;                           // nparts >= gridDim (the rest set to DBL_MAX)
+  int nparts;
+  unsigned long long* colmax;                 // optional, u64[r]
+  int* fallbacks;                             // optional
+};
+
+// (k, j), j >= k, of a packed upper-triangular 32 x 32 block; (k, k) holds 1 / G_kk (the
+// diagonal itself is never needed: t_k is dead once u_k is updated)
+__host__ __device__ constexpr int tri(int k, int j) { return HB * k - k * (k - 1) / 2 + (j - k); }
+
+__device__ __forceinline__ void cp_async(uint32_t dst, const void* src, int bytes, int src_bytes) {
+  if (bytes == 16)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                 "r"(src_bytes) : "memory");
+  else if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+                 "r"(src_bytes) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
+                 "r"(src_bytes) : "memory");
+}
+
+// my row's c[cs, cs+32) and u[cs, cs+32) -> my slots (zero beyond r or for an idle row)
+__device__ __forceinline__ void prefetch_block(const HParams& p, int64_t row, bool rok, int cs,
+                                               bool vc, bool vu, uint32_t cslot, uint32_t uslot) {
+  const double* crow = p.C + (rok ? row : 0) * p.r;
+  const float* frow = p.F + (rok ? row : 0) * p.ldf;
+  if (vc && vu && rok && cs + HB <= p.r) {             // the common case: whole block, 16 B
+#pragma unroll
+    for (int q = 0; q < HB / 2; ++q) cp_async(cslot + 16 * q, crow + cs + 2 * q, 16, 16);
+#pragma unroll
+    for (int q = 0; q < HB / 4; ++q) cp_async(uslot + 16 * q, frow + cs + 4 * q, 16, 16);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    return;
+  }
+  if (vc) {
+#pragma unroll
+    for (int q = 0; q < HB / 2; ++q) {
+      const int c = cs + 2 * q;
+      const int nb = rok ? (c + 2 <= p.r ? 16 : (c < p.r ? 8 : 0)) : 0;
+      cp_async(cslot + 16 * q, crow + (nb ? c : 0), 16, nb);
+    }
+  } else {
+    for (int q = 0; q < HB; ++q) {
+      const int c = cs + q;
+      const int nb = rok && c < p.r ? 8 : 0;
+      cp_async(cslot + 8 * q, crow + (nb ? c : 0), 8, nb);
+    }
+  }
+  if (vu) {
+#pragma unroll
+    for (int q = 0; q < HB / 4; ++q) {
+      const int c = cs + 4 * q;
+      const int nb = rok && c < p.r ? 16 : 0;            // vu implies r % 4 == 0
+      cp_async(uslot + 16 * q, frow + (nb ? c : 0), 16, nb);
+    }
+  } else {
+    for (int q = 0; q < HB; ++q) {
+      const int c = cs + q;
+      const int nb = rok && c < p.r ? 4 : 0;
+      cp_async(uslot + 4 * q, frow + (nb ? c : 0), 4, nb);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// The same for the 32 rows of a warp, coalesced (2 rows of c / 4 rows of u per instruction):
+// only when all 32 rows and the whole block exist and the 16-byte copies are allowed.  The
+// slots are then written by other lanes: consumers wait (cp.async.wait_all) and __syncwarp.
+__device__ __forceinline__ void prefetch_block_warp(const HParams& p, int64_t roww, int cs,
+                                                    uint32_t cs_w, uint32_t us_w, int lane) {
+#pragma unroll
+  for (int i = 0; i < HB / 2; ++i) {
+    const int rr = 2 * i + (lane >> 4), c2 = 2 * (lane & 15);
+    cp_async(cs_w + (rr * CS_LD + c2) * 8, p.C + (roww + rr) * p.r + cs + c2, 16, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < HB / 4; ++i) {
+    const int rr = 4 * i + (lane >> 3), c4 = 4 * (lane & 7);
+    cp_async(us_w + (rr * US_LD + c4) * 4, p.F + (roww + rr) * p.ldf + cs + c4, 16, 16);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// MMAs of the first round: T[:, cs:128] = u G[:, cs:128] (4 classes, 10 narrow products)
+__device__ __forceinline__ void issue_hals_round(uint32_t a0, uint32_t b0, uint32_t tmem_base,
+                                                 int r, int cs, uint32_t bar_d) {
+  const int rem = KR - cs;
+  const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BM >> 4) << 24) |
+                         ((uint32_t)(rem >> 3) << 17);
+  const uint32_t a_lbo = 2048, a_sbo = 128, a_kstep = 4096;
+  const uint32_t b_lbo = 128, b_sbo = 8 * KR, b_kstep = 256;
+  const uint32_t bcol = (uint32_t)(cs / 8) * (8 * KR);     // first output column's row group
+  const int ksteps = (r + 31) / 32;
+  constexpr int prs[10][2] = {{0, 0}, {0, 1}, {1, 0}, {0, 2}, {1, 1},
+                              {2, 0}, {0, 3}, {1, 2}, {2, 1}, {3, 0}};
+  tc_fence_after();
+  for (int j = 0; j < ksteps; ++j) {
+#pragma unroll
+    for (int q = 0; q < 10; ++q) {
+      const int ia = prs[q][0], ib = prs[q][1], cls = ia + ib;
+      const uint64_t ad = umma_desc(a0 + ia * PLANE_A + j * a_kstep, a_lbo, a_sbo);
+      const uint64_t bd = umma_desc(b0 + ib * KR * KR + bcol + j * b_kstep, b_lbo, b_sbo);
+      // first product of each class at k-step 0 initialises its accumulator
+      const bool fresh = j == 0 && (q == 0 || q == 1 || q == 3 || q == 6);
+      tc_mma_i8(tmem_base + cls * KR + cs, ad, bd, idesc, fresh ? 0u : 1u);
+    }
+  }
+  tc_commit(bar_d);
+}
+
+// Correction round: T[:, cs:128] += du G[kb-slice, cs:128], du = the digit-integer change of
+// block kb's u (K = 32, one k-step, 10 narrow products accumulating onto round 0's sums)
+__device__ __forceinline__ void issue_hals_corr(uint32_t a0, uint32_t b0, uint32_t tmem_base,
+                                                int kb, int cs, uint32_t bar_d) {
+  const int rem = KR - cs;
+  const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BM >> 4) << 24) |
+                         ((uint32_t)(rem >> 3) << 17);
+  const uint32_t bcol = (uint32_t)(cs / 8) * (8 * KR);
+  constexpr int prs[10][2] = {{0, 0}, {0, 1}, {1, 0}, {0, 2}, {1, 1},
+                              {2, 0}, {0, 3}, {1, 2}, {2, 1}, {3, 0}};
+  tc_fence_after();
+#pragma unroll
+  for (int q = 0; q < 10; ++q) {
+    const int ia = prs[q][0], ib = prs[q][1], cls = ia + ib;
+    const uint64_t ad = umma_desc(a0 + ia * PLANE_A + kb * 4096, 2048, 128);
+    const uint64_t bd = umma_desc(b0 + ib * KR * KR + bcol + kb * 256, 128, 8 * KR);
+    tc_mma_i8(tmem_base + cls * KR + cs, ad, bd, idesc, 1u);
+  }
+  tc_commit(bar_d);
+}
+
+__device__ __forceinline__ int rebuild_n(const uint4 (&dq)[4], int k) {
+  return (digit_at(dq[0], k) << 21) + (digit_at(dq[1], k) << 14) + (digit_at(dq[2], k) << 7) +
+         digit_at(dq[3], k);
+}
+
+__device__ __forceinline__ void bar_hals() {
+  asm volatile("bar.sync 1, %0;" ::"n"(HT) : "memory");
+}
+
+__global__ void __launch_bounds__(HT, 1) tc_hals_kernel(const HParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* Ad = smem_raw;                                        // u digits, 4 planes
+  uint8_t* Bd = smem_raw + 4 * PLANE_A;                          // G digits, 4 planes
+  double* Gt = reinterpret_cast<double*>(Bd + 4 * PLANE_B);      // diagonal G blocks (packed)
+  double* Cs = Gt + (KR / HB) * GT_BLK;                          // per-thread c slots
+  float* Us = reinterpret_cast<float*>(Cs + HT * CS_LD);         // per-thread u slots
+  __shared__ __align__(8) uint64_t bars[1];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ double gsc_s[KR];
+  __shared__ unsigned cm_s[KR];                                  // fp32 bits of max |u|
+  __shared__ double wmin_s[HT / 32];
+  if (p.stage != nullptr && *p.stage != 1) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = p.r;
+  const int nblk = (r + HB - 1) / HB;
+  for (int j = threadIdx.x; j < KR; j += blockDim.x) {
+    gsc_s[j] = j < r ? p.gscale[j] * 0x1p-21 : 0.0;
+    cm_s[j] = 0u;
+  }
+  for (int e = threadIdx.x; e < (KR / HB) * HB * HB; e += blockDim.x) {
+    const int b = e / (HB * HB), k = (e / HB) % HB, j = e % HB;
+    if (j < k) continue;
+    const int gk = HB * b + k, gj = HB * b + j;
+    double v = 0.0;
+    if (gk < r && gj < r) {
+      v = p.G[(int64_t)gk * r + gj];
+      if (j == k) v = v > 0.0 ? 1.0 / v : 0.0;                   // column skipped if G_kk <= 0
+    }
+    Gt[b * GT_BLK + tri(k, j)] = v;
+  }
+  for (int e = threadIdx.x; e < 4 * KR * KR / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(Bd)[e] = reinterpret_cast<const uint4*>(p.gd)[e];
+  const uint32_t bar_d = smem_u32(&bars[0]);
+  if (threadIdx.x == 0) {
+    mbar_init(bar_d, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+  const uint32_t a_s = smem_u32(Ad), b_s = smem_u32(Bd);
+  const int rt = threadIdx.x;                                     // row in tile
+  const uint32_t tlane = tmem_base + ((uint32_t)(32 * warp) << 16);
+  uint8_t* const abase = Ad + (rt >> 3) * 128 + (rt & 7) * 16;    // chunk kc at + kc * 2048
+  double* const cslot = Cs + rt * CS_LD;
+  float* const uslot = Us + rt * US_LD;
+  const uint32_t cslot_s = smem_u32(cslot), uslot_s = smem_u32(uslot);
+  // 16-byte copies where rows and columns allow (uniform)
+  const bool vc = (r % 2) == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0;
+  const bool vu = (r % 4) == 0 && (p.ldf % 4) == 0 && (reinterpret_cast<uintptr_t>(p.F) & 15) == 0;
+  const int tiles = (int)((p.rows + BM - 1) / BM);
+  uint32_t round = 0;
+  double wmin = DBL_MAX;
+  int nfall = 0;
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t row0 = (int64_t)t * BM;
+    const int nt = (int)(p.rows - row0 < BM ? p.rows - row0 : BM);
+    const bool rok = rt < nt;
+    const int64_t row = row0 + rt;
+    float* const frow = p.F + (rok ? row : 0) * p.ldf;
+    const int64_t roww = row0 + 32 * warp;                        // my warp's first row
+    const bool wfull = 32 * warp + 32 <= nt;                      // all 32 rows exist
+    const uint32_t cs_w = smem_u32(Cs + 32 * warp * CS_LD), us_w = smem_u32(Us + 32 * warp * US_LD);
+    auto prefetch = [&](int cs) {
+      if (vc && vu && wfull && cs + HB <= r) prefetch_block_warp(p, roww, cs, cs_w, us_w, lane);
+      else prefetch_block(p, row, rok, cs, vc, vu, cslot_s, uslot_s);
+    };
+    prefetch(0);
+    // digits of the warp's rows, one row per step, coalesced (lane: columns 4 lane .. + 3):
+    // scale with two bits of headroom, max |u| su in [16, 32); lane i keeps row i's scale
+    double su = 0.5;
+    {
+      // all 32 rows' loads in flight first (one 16-byte load per lane and row)
+      float4 q[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int rr = 32 * warp + i;
+        const float* fr = p.F + (row0 + rr) * p.ldf;
+        q[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (rr < nt) {
+          if (vu) {
+            if (4 * lane < r) q[i] = *reinterpret_cast<const float4*>(fr + 4 * lane);
+          } else {
+            if (4 * lane < r) q[i].x = fr[4 * lane];
+            if (4 * lane + 1 < r) q[i].y = fr[4 * lane + 1];
+            if (4 * lane + 2 < r) q[i].z = fr[4 * lane + 2];
+            if (4 * lane + 3 < r) q[i].w = fr[4 * lane + 3];
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int rr = 32 * warp + i;
+        const float v[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
+        unsigned mb = 0u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mb = max(mb, __float_as_uint(v[k]) & 0x7fffffffu);
+        mb = __reduce_max_sync(0xffffffffu, mb);
+        const double sr = 0.5 * pow2s_hi(hiabs((double)__uint_as_float(mb)));
+        if (lane == i) su = sr;
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t dw = digits_word((double)v[k] * sr);
+#pragma unroll
+          for (int pl = 0; pl < 4; ++pl) w[pl] |= ((dw >> (8 * pl)) & 255u) << (8 * k);
+        }
+        uint8_t* dst = Ad + (lane >> 2) * 2048 + (rr >> 3) * 128 + (rr & 7) * 16 + 4 * (lane & 3);
+#pragma unroll
+        for (int pl = 0; pl < 4; ++pl) *reinterpret_cast<uint32_t*>(dst + pl * PLANE_A) = w[pl];
+      }
+    }
+    const double isu = 1.0 / su;
+    const int ovf_hi = __double2hiint(64.0 * isu);
+    int bover = -1;                    // first block whose new u outgrew the digit scale
+#pragma unroll 1
+    for (int b = 0; b < nblk; ++b) {
+      const int cs = HB * b;
+      // publish the digits (and finish reading the previous round's TMEM), then the round
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      bar_hals();
+      if (threadIdx.x == 0) {
+        if (b == 0) issue_hals_round(a_s, b_s, tmem_base, r, 0, bar_d);
+        else issue_hals_corr(a_s, b_s, tmem_base, b - 1, cs, bar_d);
+      }
+      mbar_wait(bar_d, round & 1);
+      ++round;
+      tc_fence_after();
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncwarp();
+      // t = c - u G on this block's columns (exact class combine, 2^-21 / t_j folded in gsc)
+      double tt[HB], uu[HB];
+#pragma unroll
+      for (int h = 0; h < HB / 8; ++h) {
+        uint32_t v[4][8];
+#pragma unroll
+        for (int cls = 0; cls < 4; ++cls) TMEM_LD8(tlane + cls * KR + cs + 8 * h, v[cls]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double a = comb4(v[0][k], v[1][k], v[2][k], v[3][k]);
+          tt[8 * h + k] = cslot[8 * h + k] - a * isu * gsc_s[cs + 8 * h + k];
+          uu[8 * h + k] = (double)uslot[8 * h + k];
+        }
+      }
+      // the slot's values are in registers (tt, uu depend on them): prefetch the next block
+      __syncwarp();                    // every lane of the warp has read its slot
+      if (b + 1 < nblk) prefetch(cs + HB);
+      // sequential Gauss-Seidel over the block's columns
+      const double* gt = Gt + b * GT_BLK;
+#pragma unroll
+      for (int k = 0; k < HB; ++k) {
+        const double ig = gt[tri(k, k)];
+        const double vn = fma(tt[k], ig, uu[k]);
+        const double nu = ig == 0.0 ? uu[k] : (vn > 0.0 ? vn : 0.0);   // G_kk <= 0: skipped
+        const double d = nu - uu[k];
+        uu[k] = nu;
+#pragma unroll
+        for (int j = k + 1; j < HB; ++j) tt[j] = fma(-d, gt[tri(k, j)], tt[j]);
+      }
+      // the block is final for this sweep: store (unless an earlier block overflowed: then the
+      // fallback redoes these columns), column maxima, minimum; digits for the next rounds
+      const bool keep = rok && bover < 0;
+      int hmax = 0;                    // u >= 0: |u| su >= 64 <=> high word >= that of 64 / su
+#pragma unroll
+      for (int k = 0; k < HB; ++k) hmax = max(hmax, __double2hiint(uu[k]));
+      const bool ovf = hmax >= ovf_hi;
+      float uo[HB];
+#pragma unroll
+      for (int k = 0; k < HB; ++k) uo[k] = (float)uu[k];
+      if (keep) {
+        if (vu) {
+#pragma unroll
+          for (int q = 0; q < HB / 4; ++q)
+            if (cs + 4 * q < r)
+              *reinterpret_cast<float4*>(frow + cs + 4 * q) =
+                  make_float4(uo[4 * q], uo[4 * q + 1], uo[4 * q + 2], uo[4 * q + 3]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < HB; ++k)
+            if (cs + k < r) frow[cs + k] = uo[k];
+        }
+        float mn[HB / 2];
+#pragma unroll
+        for (int k = 0; k < HB / 2; ++k)
+          mn[k] = cs + HB <= r ? fminf(uo[k], uo[k + HB / 2])
+                               : fminf(cs + k < r ? uo[k] : FLT_MAX,
+                                       cs + k + HB / 2 < r ? uo[k + HB / 2] : FLT_MAX);
+#pragma unroll
+        for (int w = HB / 4; w > 0; w >>= 1)
+#pragma unroll
+          for (int k = 0; k < w; ++k) mn[k] = fminf(mn[k], mn[k + w]);
+        wmin = fmin(wmin, (double)mn[0]);
+      }
+      // u >= 0 (HALS projects), so the fp32 bits order like the values
+      unsigned mine = 0u;
+#pragma unroll
+      for (int k = 0; k < HB; ++k) {
+        const unsigned m = __reduce_max_sync(0xffffffffu, keep ? __float_as_uint(uo[k]) : 0u);
+        if (lane == k) mine = m;
+      }
+      if (mine) atomicMax(&cm_s[cs + lane], mine);
+      if (bover < 0 && ovf) bover = b;
+      if (b + 1 < nblk) {
+        // the block's slice of the A planes now holds the digits of du = n(u_new) - n(u_old)
+        // (integers on the 2^-21 / su grid; |du| < 96 * 2^21 keeps d0 within int8), so the
+        // correction round leaves T = digits(u_new) G up to the dropped weight classes
+#pragma unroll
+        for (int ch = 0; ch < HB / 16; ++ch) {
+          const int off = (cs / 16 + ch) * 16 * 128;
+          uint4 dq[4];
+#pragma unroll
+          for (int pl = 0; pl < 4; ++pl)
+            dq[pl] = *reinterpret_cast<const uint4*>(abase + pl * PLANE_A + off);
+          Pack16 pk;
+          pack_clear(pk);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int nn = __double2int_rn(uu[16 * ch + k] * su * 0x1p21);
+            pack_put(pk, k, digits_n(nn - rebuild_n(dq, k)));
+          }
+          pack_store(pk, abase, off);
+        }
+      }
+    }
+    // rows whose u outgrew the digit scale: the columns right of that block, sequentially in
+    // fp64 against F (columns left of k already hold this sweep's values, as in hals_kernel)
+    if (rok && bover >= 0 && HB * (bover + 1) < r) {
+      ++nfall;
+      for (int k = HB * (bover + 1); k < r; ++k) {
+        double s = p.C[row * r + k];
+        for (int l = 0; l < r; ++l) s -= (double)frow[l] * p.G[(int64_t)l * r + k];
+        const double gkk = p.G[(int64_t)k * r + k];
+        if (!(gkk > 0.0)) continue;
+        const double uo = (double)frow[k];
+        const double vn = fma(s, 1.0 / gkk, uo);
+        const float nu = (float)(vn > 0.0 ? vn : 0.0);
+        frow[k] = nu;
+        wmin = fmin(wmin, (double)nu);
+        atomicMax(&cm_s[k], __float_as_uint(nu));
+      }
+    }
+  }
+  if (p.fallbacks && nfall) atomicAdd(p.fallbacks, nfall);
+  // block minimum and column maxima
+  double m = wmin;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) wmin_s[warp] = m;
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0 && p.minparts) {
+    double mm = DBL_MAX;
+    for (int w = 0; w < HT / 32; ++w) mm = fmin(mm, wmin_s[w]);
+    p.minparts[blockIdx.x] = mm;
+    for (int q = blockIdx.x + gridDim.x; q < p.nparts; q += gridDim.x) p.minparts[q] = DBL_MAX;
+  }
+  if (p.colmax)
+    for (int j = threadIdx.x; j < r; j += blockDim.x)
+      if (cm_s[j])
+        atomicMax(&p.colmax[j],
+                  (unsigned long long)__double_as_longlong((double)__uint_as_float(cm_s[j])));
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
 }  // namespace tpb
 
 int tc_pbcd_parts() { return kSMs; }
@@ -444,7 +899,7 @@ int tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double*
                   cudaStream_t st) {
   using namespace tpb;
   const int rp = KR;   // G padded to 128 columns: class k of the accumulators at column k * 128
-  gdigits_kernel<<<1, 256, 0, st>>>(G, r, rp, gd_work, gscale_work, stage);
+  gdigits_kernel<<<1, 256, 0, st>>>(G, r, rp, gd_work, gscale_work, stage, 0);
   Params p;
   p.F = F;
   p.ldf = ldf;
@@ -475,6 +930,39 @@ int tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double*
   // unused CTAs of the persistent grid still write their (zero) partials: launch kSMs always
   tc_pbcd_kernel<<<kSMs, THREADS, smem, st>>>(p);
   (void)grid;
+  count_launch(2);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int tc_hals_parts() { return kSMs; }
+
+int tc_hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
+                 int8_t* gd_work, double* gscale_work, const int* stage, double* minparts,
+                 int nparts, unsigned long long* colmax, int* fallbacks, cudaStream_t st) {
+  using namespace tpb;
+  gdigits_kernel<<<1, 256, 0, st>>>(G, r, KR, gd_work, gscale_work, stage, 1);
+  HParams p;
+  p.F = F;
+  p.ldf = ldf;
+  p.rows = rows;
+  p.r = r;
+  p.C = C;
+  p.G = G;
+  p.gd = gd_work;
+  p.gscale = gscale_work;
+  p.stage = stage;
+  p.minparts = minparts;
+  p.nparts = nparts;
+  p.colmax = colmax;
+  p.fallbacks = fallbacks;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(tc_hals_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             H_SMEM) != cudaSuccess)
+      return 1;
+    attr = true;
+  }
+  tc_hals_kernel<<<kSMs, HT, H_SMEM, st>>>(p);
   count_launch(2);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

@@ -177,8 +177,7 @@ __device__ __forceinline__ Dig4 digits4(double t) {
 // Register-only form of digits4 (no addressable local arrays).  digits_word(t), |t| < 64.5:
 // t rounded to the 2^-21 grid (error <= 2^-22, the digits4 bound) split into balanced base-2^7
 // digits d0 + d1/2^7 + d2/2^14 + d3/2^21, digit pl in byte pl -- integer arithmetic only.
-__device__ __forceinline__ uint32_t digits_word(double t) {
-  int n = __double2int_rn(t * 0x1p21);
+__device__ __forceinline__ uint32_t digits_n(int n) {
   const int d3 = ((n + 64) & 127) - 64;
   n = (n - d3) >> 7;
   const int d2 = ((n + 64) & 127) - 64;
@@ -187,6 +186,9 @@ __device__ __forceinline__ uint32_t digits_word(double t) {
   const int d0 = (n - d1) >> 7;
   return (uint32_t)(d0 & 255) | ((uint32_t)(d1 & 255) << 8) | ((uint32_t)(d2 & 255) << 16) |
          ((uint32_t)(d3 & 255) << 24);
+}
+__device__ __forceinline__ uint32_t digits_word(double t) {
+  return digits_n(__double2int_rn(t * 0x1p21));
 }
 }  // namespace tcp
 }  // namespace enmf
