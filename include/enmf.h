@@ -102,6 +102,8 @@ typedef struct {
   int feasible;            /* 1 if U, V >= 0 on return */
   int pbcd_iters_u;        /* PBCD inner iterations of the last ascent U block (k*) */
   int pbcd_iters_v;        /* same for the V block */
+  int hals_fallback_rows;  /* tensor-core HALS: row updates finished by the sequential fp64
+                              fallback because u outgrew its digit scale (diagnostic) */
 } enmf_iter_info_t;
 
 typedef struct {

@@ -57,7 +57,7 @@ class InitInfo(ctypes.Structure):
 class IterInfo(ctypes.Structure):
     _fields_ = [("ascent_sweeps", ctypes.c_int), ("hals_sweeps", ctypes.c_int),
                 ("feasible", ctypes.c_int), ("pbcd_iters_u", ctypes.c_int),
-                ("pbcd_iters_v", ctypes.c_int)]
+                ("pbcd_iters_v", ctypes.c_int), ("hals_fallback_rows", ctypes.c_int)]
 
 
 class Kkt(ctypes.Structure):

@@ -182,7 +182,8 @@ enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
   }
   if (h->tc_hals) {
     if (tc_hals_rows(F, ldf, rows, r, C, G, reinterpret_cast<int8_t*>(h->tcpb_ws + 128),
-                     h->tcpb_ws, stage, h->minparts, kRowGrid, colmax, nullptr, h->st))
+                     h->tcpb_ws, stage, h->minparts, kRowGrid, colmax, h->dint + I_HALS_FB,
+                     h->st))
       return ENMF_ERR_CUDA;
   } else {
     hals_rows(F, ldf, rows, r, C, G, stage, h->minparts, h->st, colmax);
@@ -553,6 +554,7 @@ enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int
   if (maybe_ascent) ENMF_TRY(ensure_snaps(h));
   ENMF_TRY(ensure_ftrace(h, std::max(n_iters, 1)));
   CUDA_TRY(cudaMemsetAsync(h->dint + I_CNT_ASC, 0, 2 * sizeof(int), h->st));
+  CUDA_TRY(cudaMemsetAsync(h->dint + I_HALS_FB, 0, sizeof(int), h->st));
   // entry state: mins of the factors as given, G_V of the given V (min U after its upload)
   if (!u_ready) ENMF_TRY(min_factor(h, U, ldu, h->m_loc, S_MINU, sh));
   ENMF_TRY(min_factor(h, V, ldv, h->n, S_MINV, false));
@@ -591,6 +593,7 @@ enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int
     info->feasible = mins[0] >= 0.0 && mins[1] >= 0.0;
     info->pbcd_iters_u = hi[I_KSTAR_U];
     info->pbcd_iters_v = hi[I_KSTAR_V];
+    info->hals_fallback_rows = hi[I_HALS_FB];
   }
   if (f_trace_host)
     for (int t = 0; t < n_iters; ++t)

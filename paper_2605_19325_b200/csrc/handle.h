@@ -19,7 +19,7 @@ enum {
   S_WMAX, S_COUNT = 16
 };
 // device int slots
-enum { I_STAGE = 0, I_KSTAR_U, I_KSTAR_V, I_CNT_ASC, I_CNT_HALS, I_BAD, I_COUNT = 8 };
+enum { I_STAGE = 0, I_KSTAR_U, I_KSTAR_V, I_CNT_ASC, I_CNT_HALS, I_BAD, I_HALS_FB, I_COUNT = 8 };
 
 }  // namespace enmf
 

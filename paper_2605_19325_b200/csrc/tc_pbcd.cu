@@ -70,12 +70,14 @@ __device__ __forceinline__ double pow2s_hi(int h) {
   const int E = h >> 20;                       // biased exponent; frexp exponent e = E - 1022
   return __hiloint2double((2051 - E) << 20, 0); // 2^(6 - e)
 }
-// The 4 weight classes of an accumulator column combined exactly: v0 2^21 + v1 2^14 + v2 2^7 + v3
-// (< 2^53, so the conversion to double is exact); callers fold 2^-21 into their scales.
+// The 4 weight classes of an accumulator column combined exactly: v0 2^21 + v1 2^14 + v2 2^7 + v3;
+// callers fold 2^-21 into their scales.  With K <= 128 and |digits| <= 64 (97 for the HALS
+// corrections) every |v_c| < 2^21, so v0 2^7 + v1 and v2 2^7 + v3 are exact int32 and the final
+// hi 2^14 + lo (< 2^42) is exact in fp64: 2 int32 IMADs, 2 conversions, 1 DFMA.
 __device__ __forceinline__ double comb4(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3) {
-  const long long a = (long long)(int)v0 * 2097152ll + (long long)(int)v1 * 16384ll +
-                      (long long)(int)v2 * 128ll + (long long)(int)v3;
-  return (double)a;
+  const int hi = (int)v0 * 128 + (int)v1;
+  const int lo = (int)v2 * 128 + (int)v3;
+  return fma((double)hi, 16384.0, (double)lo);
 }
 
 __device__ __forceinline__ void bar_compute() {
@@ -385,10 +387,14 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
         if (rok) {
           // snapshot, tile-major (pbcd_copy_tiled_kernel): a warp's 32 rows are contiguous
           const int nt = (int)(p.rows - (int64_t)t * BM < BM ? p.rows - (int64_t)t * BM : BM);
-          float* sn = p.snaps + (int64_t)it * snap_stride + (int64_t)t * BM * p.r + rt;
+          float* sn = p.snaps + (int64_t)it * snap_stride + (int64_t)t * BM * p.r +
+                      (int64_t)c0 * nt + rt;
+          const int ncol = p.r - c0 < 64 ? p.r - c0 : 64;   // columns of my half that exist
 #pragma unroll
-          for (int c = 0; c < 64; ++c)
-            if (c0 + c < p.r) sn[(int64_t)(c0 + c) * nt] = (float)u[c];
+          for (int c = 0; c < 64; ++c) {
+            if (c < ncol) *sn = (float)u[c];
+            sn += nt;
+          }
         }
         bar_compute();          // everyone has read the g digits before they are overwritten
       }

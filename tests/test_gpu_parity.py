@@ -70,6 +70,31 @@ def test_one_hals_sweep(cfg, prec):
 
 
 @pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
+@pytest.mark.parametrize("cfg", [CASES[1], CASES[6]], ids=[IDS[1], IDS[6]])
+def test_hals_sweep_rows_outgrowing_digit_scale(cfg, prec):
+    """Every third row of U scaled by 1e-6: the sweep grows it by ~1e6, past the digit scale
+    tc_hals_kernel chose from the old row (|u| su >= 64 after the first 32-column block), so
+    those rows finish with the kernel's sequential fp64 fallback.  Same bar as one sweep."""
+    h, X, _ = make(cfg, precision=prec)
+    U0, V0, _, _ = rotated_point(X, cfg.r)
+    U0, V0 = np.abs(U0), np.abs(V0)
+    U0[::3] *= np.float32(1e-6)
+    U, V = to_dev(U0), to_dev(V0)
+    h.set_stage(1)
+    _, info = h.iterate(U, V, 1)
+    if prec == TC:   # the fallback really ran
+        assert info["hals_fallback_rows"] > 0, info
+    else:
+        assert info["hals_fallback_rows"] == 0
+    Uo, Vo, _, _ = oracle.sweep(X, U0, V0, oracle.SweepState(stage=1), F32STATE(cfg.r))
+    eu, ev = rel_fro(to_np(U), Uo), rel_fro(to_np(V), Vo)
+    eu3 = rel_fro(to_np(U)[::3], Uo[::3])
+    print(f"{cfg.name} prec={h.precision}: U {eu:.2e} (scaled rows {eu3:.2e}) V {ev:.2e} "
+          f"fallback rows {info['hals_fallback_rows']}")
+    assert eu < 1e-5 and ev < 1e-5 and eu3 < 1e-5
+
+
+@pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
 @pytest.mark.parametrize("cfg", CASES[:4] + [CASES[6]], ids=IDS[:4] + [IDS[6]])
 def test_hals_trajectory_50_sweeps(cfg, prec):
     """50 HALS sweeps from a shared feasible point: final factors within 1e-4, the direct
