@@ -100,9 +100,14 @@ __device__ __forceinline__ void unit_range(const Params& p, int u, int& tile, in
 // initialise every accumulator at the start of a unit (`fresh`).
 //   NCLS = 4 (10 products, 6 MMAs): A0[B0;B1] A0[B2;B3] A1[B0;B1] A1 B2 A2[B0;B1] A3 B0
 //   NCLS = 3 ( 6 products, 4 MMAs): A0[B0;B1] A0 B2 A1[B0;B1] A2 B0
-template <int NCLS> struct MmaList;
+//   LIST 7   ( 7 products, 5 MMAs): classes <= 2 plus A3 B0 of class 3 -- the X digit that
+//            carries the low bits of entries far below max|X| against the factor's leading
+//            digit; the dropped A0 B3, A1 B2, A2 B1 involve the factor's low digits only
+//            (per-column scales), B plane 3 is not read.  4 accumulators.
+// NPA / NPB: digit planes of A / B staged per k-step; NCLS: accumulators (weight classes).
+template <int LIST> struct MmaList;
 template <> struct MmaList<4> {
-  static constexpr int N = 6, FRESH = 2;
+  static constexpr int N = 6, FRESH = 2, NCLS = 4, NPA = 4, NPB = 4;
   __device__ static __forceinline__ int t(int q, int f) {
     constexpr int tab[6][4] = {{0, 0, 0, 1}, {0, 2, 2, 1}, {1, 0, 1, 1},
                                {1, 2, 3, 0}, {2, 0, 2, 1}, {3, 0, 3, 0}};
@@ -110,19 +115,28 @@ template <> struct MmaList<4> {
   }
 };
 template <> struct MmaList<3> {
-  static constexpr int N = 4, FRESH = 2;
+  static constexpr int N = 4, FRESH = 2, NCLS = 3, NPA = 3, NPB = 3;
   __device__ static __forceinline__ int t(int q, int f) {
     constexpr int tab[4][4] = {{0, 0, 0, 1}, {0, 2, 2, 0}, {1, 0, 1, 1}, {2, 0, 2, 0}};
     return tab[q][f];
   }
 };
+template <> struct MmaList<7> {
+  // the first FRESH entries initialise acc0|acc1, acc2, acc3
+  static constexpr int N = 5, FRESH = 3, NCLS = 4, NPA = 4, NPB = 3;
+  __device__ static __forceinline__ int t(int q, int f) {
+    constexpr int tab[5][4] = {{0, 0, 0, 1}, {0, 2, 2, 0}, {3, 0, 3, 0}, {1, 0, 1, 1},
+                               {2, 0, 2, 0}};
+    return tab[q][f];
+  }
+};
 
-template <int NCLS>
+template <int LIST>
 __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
-  constexpr int NPL = NCLS;                                   // digit planes per operand
-  constexpr int STAGE = NPL * (TILE_A + MAX_TILE_B);
+  using L = MmaList<LIST>;
+  constexpr int NCLS = L::NCLS, NPA = L::NPA, NPB = L::NPB;
+  constexpr int STAGE = NPA * TILE_A + NPB * MAX_TILE_B;
   constexpr int NST = (SMEM_BYTES - 1024) / STAGE;            // 3 (4 planes) or 4 (3 planes)
-  using L = MmaList<NCLS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t bars[2 * 4 + 2];
@@ -165,17 +179,17 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
       for (int ks = s0; ks < s1; ++ks) {
         mbar_wait(bar_empty + 8 * stage, phase ^ 1);
         const uint32_t fb = bar_full + 8 * stage;
-        if (lane == 0) mbar_expect_tx(fb, NPL * (TILE_A + tile_b));
+        if (lane == 0) mbar_expect_tx(fb, NPA * TILE_A + NPB * tile_b);
         __syncwarp();
         const uint32_t st = smem_u32(smem + (size_t)stage * STAGE);
         if (p.mode == 0) {
-          // the NPL planes of a tile are contiguous: one bulk copy
+          // the NPA planes of a tile are contiguous: one bulk copy
           const int64_t off = ((int64_t)tile * p.tiles_per_row + ks) * PLANES * TILE_A;
-          if (lane < NPL) bulk_g2s(st + lane * TILE_A, p.xp[lane] + off, TILE_A, fb);
+          if (lane < NPA) bulk_g2s(st + lane * TILE_A, p.xp[lane] + off, TILE_A, fb);
         } else if (p.mode == 2) {
           // A = X^T from the transposed packed copy: K-major tiles
           const int64_t off = ((int64_t)tile * p.tiles_per_row_t + ks) * PLANES * TILE_A;
-          if (lane < NPL) bulk_g2s(st + lane * TILE_A, p.xtp[lane] + off, TILE_A, fb);
+          if (lane < NPA) bulk_g2s(st + lane * TILE_A, p.xtp[lane] + off, TILE_A, fb);
         } else {
           // A = X^T: output rows j = column tiles 2*tile, 2*tile+1 of row band ks/2; the K stage
           // is the 64-row half (ks & 1) of that band: 8 chunks of 1 KB per plane, one per lane
@@ -185,12 +199,12 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
           const int64_t src = (band * p.tiles_per_row + 2 * tile + t) * PLANES * TILE_A +
                               (int64_t)(kc * 16 + 8 * half) * 128;
           const uint32_t dst = (uint32_t)((t * 4 + kc) * 1024);
-          for (int pl = lane >> 3; pl < NPL; pl += 4)
+          for (int pl = lane >> 3; pl < NPA; pl += 4)
             bulk_g2s(st + pl * TILE_A + dst, p.xp[pl] + src, 1024, fb);
         }
         const int64_t foff = (int64_t)ks * PLANES * tile_b;
-        if (lane >= 28 && lane - 28 < NPL)
-          bulk_g2s(st + NPL * TILE_A + (lane - 28) * tile_b, p.fp[lane - 28] + foff, tile_b, fb);
+        if (lane >= 28 && lane - 28 < NPB)
+          bulk_g2s(st + NPA * TILE_A + (lane - 28) * tile_b, p.fp[lane - 28] + foff, tile_b, fb);
         if (++stage == NST) { stage = 0; phase ^= 1; }
       }
     }
@@ -222,7 +236,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
           mbar_wait(bar_full + 8 * stage, phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem + (size_t)stage * STAGE);
-          const uint32_t b0 = a0 + NPL * TILE_A;
+          const uint32_t b0 = a0 + NPA * TILE_A;
 #pragma unroll
           for (int j = 0; j < BK / 32; ++j) {
 #pragma unroll
@@ -525,7 +539,7 @@ __device__ __forceinline__ void pack_digits16(F val, uint32_t (&w)[4][4]) {
     for (int q = 0; q < 4; ++q) w[pl][q] = 0u;
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
-    const uint32_t dw = digits_word(val(k));
+    const uint32_t dw = digits_word_sym(val(k));
 #pragma unroll
     for (int pl = 0; pl < 4; ++pl) w[pl][k >> 2] |= ((dw >> (8 * pl)) & 255u) << (8 * (k & 3));
   }
@@ -732,6 +746,7 @@ struct TcState {
   bool pair = false;           // cta_group::2 kernel (ENMF_TC_PAIR=1 enables)
   int ksplit1p = 1, ksplit2p = 1;
   int pass1_classes = 3;       // ENMF_TC_PASS1_CLASSES=4 for the full-precision pass 1
+  int pass2_classes = 4;       // ENMF_TC_PASS2_CLASSES: 3 (classes <= 2), 7 (+ A3 B0), 4
   int sms = kSMs;
 };
 
@@ -775,7 +790,15 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   // Pass 1 drops the weight-3 digit products only when K = n is long enough that their
   // unbiased truncation error (~2^-22 of |X||V| per term) averages below ~1e-9 of P
   s->pass1_classes = n >= 8192 ? 3 : 4;
+  // pass 2 keeps all 4 classes: with list 7 (-30 % tensor work, +13 % HALS sweeps/s at C5)
+  // the sampled C5 V-row update error rose from 6e-8 to 4.9e-6 (bar 1e-5) and the trace-form
+  // f error from 5e-8 to 2e-5 -- too little margin
+  s->pass2_classes = 4;
   if (const char* e = getenv("ENMF_TC_PASS1_CLASSES")) s->pass1_classes = atoi(e) == 4 ? 4 : 3;
+  if (const char* e = getenv("ENMF_TC_PASS2_CLASSES")) {
+    const int c = atoi(e);
+    s->pass2_classes = c == 3 || c == 7 ? c : 4;
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, dev);
@@ -924,6 +947,7 @@ static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out
   if (!attr) {
     cudaFuncSetAttribute(tc_i8_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(tc_i8_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(tc_i8_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(tc_i8_pair_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          PAIR_SMEM);
     cudaFuncSetAttribute(tc_i8_pair_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -933,7 +957,9 @@ static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out
   // P = X V only feeds the U-block update: 3 digit planes (weight classes <= 2, ~2e-8
   // relative); Q = X^T U also feeds the trace-form objective, whose conditioning needs all
   // 4 planes (classes <= 3, ~5e-10 relative)  -- DESIGN.md §5
-  const bool three = s->pass1_classes == 3 && mode == 0;
+  const bool three =
+      (s->pass1_classes == 3 && mode == 0) || (s->pass2_classes == 3 && mode == 2);
+  const bool seven = !pair && s->pass2_classes == 7 && mode == 2;
   if (pair) {
     const int grid = 2 * std::min(p.num_units, s->sms / 2);
     if (three)
@@ -944,6 +970,8 @@ static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out
     const int grid = std::min(p.num_units, s->sms);
     if (three)
       tc_i8_kernel<3><<<grid, THREADS, SMEM_BYTES, st>>>(p);
+    else if (seven)
+      tc_i8_kernel<7><<<grid, THREADS, SMEM_BYTES, st>>>(p);
     else
       tc_i8_kernel<4><<<grid, THREADS, SMEM_BYTES, st>>>(p);
   }

@@ -320,6 +320,41 @@ def test_tc_contractions_match_oracle(cfg, signed, pair, monkeypatch):
     assert rel_cross < 1e-8
 
 
+@pytest.mark.parametrize("signed", [False, True], ids=["nonneg", "signed"])
+def test_tc_reduced_class_lists(signed, monkeypatch):
+    """The product lists the large shapes use (K >= 8192: pass 1 with weight classes <= 2,
+    pass 2 with classes <= 2 plus A3 B0), forced here on a small shape: P and Q entrywise and
+    normwise against the oracle, and the trace-form cross term.  Dropped products are
+    mean-zero (symmetric digits, tc_ptx.cuh digits_word_sym); bounds = 2^-14 of |X||F|
+    entrywise, 2e-6 normwise (measured below them with > 5x margin)."""
+    monkeypatch.setenv("ENMF_TC_PASS1_CLASSES", "3")
+    monkeypatch.setenv("ENMF_TC_PASS2_CLASSES", "7")
+    cfg = TC_CASES[-1]
+    h, X, _ = make(cfg, precision=TC)
+    g = np.random.default_rng(4)
+    U0 = g.random((cfg.m, cfg.r))
+    V0 = g.random((cfg.n, cfg.r))
+    if signed:
+        U0, V0 = U0 - 0.4, V0 - 0.4
+    U0 = U0.astype(np.float32).astype(np.float64)
+    V0 = V0.astype(np.float32).astype(np.float64)
+    P, Q = h.cross_terms(to_dev(U0), to_dev(V0))
+    P, Q = to_np(P), to_np(Q)
+    Xa = np.abs(X.astype(np.float64))
+    Pr, Qr = oracle.xv(X, V0), oracle.xtu(X, U0)
+    ep = np.abs(P - Pr) / (Xa @ np.abs(V0))
+    eq = np.abs(Q - Qr) / (Xa.T @ np.abs(U0))
+    f_d = oracle.frob2_direct(X, U0, V0)
+    rel_cross = abs(h.objective(to_dev(U0), to_dev(V0), exact=False) - f_d) / \
+        (2 * abs(float((Qr * V0).sum())))
+    print(f"reduced lists {'signed' if signed else 'nonneg'}: P normwise {rel_fro(P, Pr):.2e} "
+          f"max {ep.max():.2e}; Q normwise {rel_fro(Q, Qr):.2e} max {eq.max():.2e}; "
+          f"cross {rel_cross:.2e}")
+    assert ep.max() < 2.0 ** -14 and eq.max() < 2.0 ** -14
+    if not signed:
+        assert rel_fro(P, Pr) < 2e-6 and rel_fro(Q, Qr) < 2e-6 and rel_cross < 2e-6
+
+
 # ----------------------------------------------------------------------------- edges
 def test_edge_cases():
     import torch
