@@ -17,6 +17,11 @@ SHORT="python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu-baseline"
 ncu --set full --clock-control none --import-source on -k regex:"tc_i8_kernel" -s 18 -c 2 \
     -o $OUT/prof_tc $SHORT > $OUT/ncu_full.log 2>&1
 echo "full tc rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"tc_pbcd_kernel|hals_kernel" -s 4 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:"tc_pbcd_kernel" -s 2 -c 1 \
     -o $OUT/prof_rows $SHORT > $OUT/ncu_full_rows.log 2>&1
-echo "full rows rc=$?"
+echo "full pbcd rc=$?"
+# tc_hals_kernel: launches before the HALS stage return at once; the 27th is an active U block
+ncu --set full --clock-control none --import-source on -k regex:"tc_hals_kernel" -s 26 -c 1 \
+    -o $OUT/prof_hals python bench.py --steps 40 --warmup 3 --no-e2e --no-cpu-baseline \
+    > $OUT/ncu_full_hals.log 2>&1
+echo "full hals rc=$?"
