@@ -1,7 +1,8 @@
 // comm.cpp -- NCCL over NVLink/NVSwitch for the row-sharded path.
 // NCCL is resolved at run time with dlopen("libnccl.so.2") so the process uses the NCCL
-// already loaded by torch (or the system one when used from plain C).  Only ncclAllReduce
-// is needed: the n x r partial X^T U, the r x r Grams, and a handful of scalars.
+// already loaded by torch (or the system one when used from plain C).  ncclAllReduce for the
+// r x r Grams, the PBCD stopping partials and scalars; in a sweep the n x r partial X^T U is
+// reduce-scattered (each rank updates its V slice) and the V slices are all-gathered (fp32).
 #include <dlfcn.h>
 #include <nccl.h>
 #include <stdio.h>
@@ -16,6 +17,8 @@ struct Api {
   void* so = nullptr;
   decltype(&ncclCommInitRank) init = nullptr;
   decltype(&ncclAllReduce) allreduce = nullptr;
+  decltype(&ncclReduceScatter) reduce_scatter = nullptr;
+  decltype(&ncclAllGather) allgather = nullptr;
   decltype(&ncclCommDestroy) destroy = nullptr;
   decltype(&ncclGetErrorString) errstr = nullptr;
 };
@@ -29,6 +32,8 @@ Api& api() {
     if (a.so) {
       a.init = (decltype(a.init))dlsym(a.so, "ncclCommInitRank");
       a.allreduce = (decltype(a.allreduce))dlsym(a.so, "ncclAllReduce");
+      a.reduce_scatter = (decltype(a.reduce_scatter))dlsym(a.so, "ncclReduceScatter");
+      a.allgather = (decltype(a.allgather))dlsym(a.so, "ncclAllGather");
       a.destroy = (decltype(a.destroy))dlsym(a.so, "ncclCommDestroy");
       a.errstr = (decltype(a.errstr))dlsym(a.so, "ncclGetErrorString");
     }
@@ -46,7 +51,7 @@ struct Comm {
 int comm_init(Comm** out, const void* uid128, int world, int rank) {
   *out = nullptr;
   Api& a = api();
-  if (!a.init || !a.allreduce) return -1;
+  if (!a.init || !a.allreduce || !a.reduce_scatter || !a.allgather) return -1;
   ncclUniqueId id;
   static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
   memcpy(&id, uid128, sizeof(id));
@@ -68,6 +73,27 @@ int comm_allreduce(Comm* c, void* buf, size_t count, CommType t, CommOp op, cuda
   ncclDataType_t dt = t == CommType::F64 ? ncclFloat64 : ncclFloat32;
   ncclRedOp_t o = op == CommOp::Sum ? ncclSum : (op == CommOp::Min ? ncclMin : ncclMax);
   ncclResult_t rc = api().allreduce(buf, buf, count, dt, o, c->comm, st);
+  return rc == ncclSuccess ? 0 : -1;
+}
+
+int comm_reduce_scatter(Comm* c, void* buf, size_t count, CommType t, cudaStream_t st) {
+  if (!c || c->world == 1 || count == 0) return 0;
+  const ncclDataType_t dt = t == CommType::F64 ? ncclFloat64 : ncclFloat32;
+  const size_t esz = t == CommType::F64 ? 8 : 4;
+  char* b = static_cast<char*>(buf);
+  // in place: recvbuff = sendbuff + rank * recvcount (NCCL's in-place convention)
+  ncclResult_t rc = api().reduce_scatter(b, b + (size_t)c->rank * count * esz, count, dt, ncclSum,
+                                         c->comm, st);
+  return rc == ncclSuccess ? 0 : -1;
+}
+
+int comm_allgather(Comm* c, void* buf, size_t count, CommType t, cudaStream_t st) {
+  if (!c || c->world == 1 || count == 0) return 0;
+  const ncclDataType_t dt = t == CommType::F64 ? ncclFloat64 : ncclFloat32;
+  const size_t esz = t == CommType::F64 ? 8 : 4;
+  char* b = static_cast<char*>(buf);
+  // in place: sendbuff = recvbuff + rank * sendcount
+  ncclResult_t rc = api().allgather(b + (size_t)c->rank * count * esz, b, count, dt, c->comm, st);
   return rc == ncclSuccess ? 0 : -1;
 }
 

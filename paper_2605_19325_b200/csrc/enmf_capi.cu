@@ -110,9 +110,11 @@ enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* 
   return prof_mark(h, 0);
 }
 
-// Q = X^T U summed over ranks: the second X pass.
+// Q = X^T U summed over ranks: the second X pass.  slice: only this rank's V
+// slice of Q is needed (the sweep's sharded V block) -- with NCCL a reduce-scatter (Q holds
+// world x v_pad rows), otherwise the full allreduce (which includes the slice).
 enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q,
-                           const unsigned long long* umax) {
+                           const unsigned long long* umax, bool slice) {
   ENMF_TRY(prof_mark(h, 1));
   if (h->tc) {
     if (tc_xtu(h->tc, U, ldu, Q, h->st, umax) != 0) return ENMF_ERR_CUDA;
@@ -124,6 +126,10 @@ enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double*
                        h->work_elems, h->st);
   }
   ENMF_TRY(prof_mark(h, 1));
+  if (slice && h->comm && h->prob.world_size > 1)
+    return comm_reduce_scatter(h->comm, Q, (size_t)(h->v_pad * h->r), CommType::F64, h->st) == 0
+               ? ENMF_OK
+               : ENMF_ERR_NCCL;
   return ar(h, Q, (size_t)(h->n * h->r), CommOp::Sum);
 }
 
@@ -247,18 +253,31 @@ enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ld
   }
   // V block: Q = X^T U_new (allreduced), G_U = U_new^T U_new (PAPER.md:220 uses U^(k+1))
   ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh));
-  ENMF_TRY(contract_xtu(h, U, ldu, h->Q, h->umax_valid ? h->fmax_uv : nullptr));
+  ENMF_TRY(contract_xtu(h, U, ldu, h->Q, h->umax_valid ? h->fmax_uv : nullptr, sh));
+  const int64_t vb = h->v_begin, vc = h->v_count, r = h->r;
   if (sh) {
     // V block sharded by rows (V rows are independent given Q and G_U): each
     // rank updates its slice (PBCD stopping partials and min allreduced like the U block),
-    // then the full V is reassembled bitwise identically on every rank
-    const int64_t vb = h->v_begin, vc = h->v_count, r = h->r;
+    // then the full V is reassembled bitwise identically on every rank: NCCL all-gather of
+    // the fp32 slices (no arithmetic), or through the host collective as a zero-padded fp64
+    // sum (exact: one nonzero term per entry)
     ENMF_TRY(block_update(h, V + vb * ldv, ldv, vc, h->Q + vb * r, h->GU, S_LAMV, I_KSTAR_V,
                           S_MINV, true, maybe_ascent, nullptr));
-    CUDA_TRY(cudaMemsetAsync(h->Vg, 0, sizeof(double) * h->n * r, st));
-    if (vc > 0) f32_to_f64(V + vb * ldv, ldv, vc, r, h->Vg + vb * r, st);
-    ENMF_TRY(ar(h, h->Vg, (size_t)(h->n * r), CommOp::Sum));
-    f64_to_f32(h->Vg, h->n, r, nullptr, V, ldv, st);
+    if (h->comm) {
+      const size_t rb = sizeof(float) * r;
+      if (vc > 0)
+        CUDA_TRY(cudaMemcpy2DAsync(h->Vpad + vb * r, rb, V + vb * ldv, sizeof(float) * ldv, rb,
+                                   vc, cudaMemcpyDeviceToDevice, st));
+      if (comm_allgather(h->comm, h->Vpad, (size_t)(h->v_pad * r), CommType::F32, st) != 0)
+        return ENMF_ERR_NCCL;
+      CUDA_TRY(cudaMemcpy2DAsync(V, sizeof(float) * ldv, h->Vpad, rb, rb, h->n,
+                                 cudaMemcpyDeviceToDevice, st));
+    } else {
+      CUDA_TRY(cudaMemsetAsync(h->Vg, 0, sizeof(double) * h->n * r, st));
+      if (vc > 0) f32_to_f64(V + vb * ldv, ldv, vc, r, h->Vg + vb * r, st);
+      ENMF_TRY(ar(h, h->Vg, (size_t)(h->n * r), CommOp::Sum));
+      f64_to_f32(h->Vg, h->n, r, nullptr, V, ldv, st);
+    }
     h->vmax_valid = false;
   } else {
     ENMF_TRY(block_update(h, V, ldv, h->n, h->Q, h->GU, S_LAMV, I_KSTAR_V, S_MINV, false,
@@ -271,9 +290,17 @@ enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ld
     CUDA_TRY(cudaMemcpyAsync(hk.v_download, V, sizeof(float) * h->n * h->r,
                              cudaMemcpyDeviceToHost, h->st2));
   }
-  // objective f = ||X||^2 - 2 <X^T U, V> + <U^T U, V^T V>   (BASELINE.json:5)
-  ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
-  dot_f64_f32(h->Q, V, ldv, h->n, h->r, h->parts, h->dscal + S_CROSS, st);
+  // objective f = ||X||^2 - 2 <X^T U, V> + <U^T U, V^T V>   (BASELINE.json:5); sharded:
+  // G_V and <Q, V> from this rank's V slice (the only valid part of Q after the
+  // reduce-scatter), summed over ranks
+  if (sh) {
+    ENMF_TRY(gram_f32(h, V + vb * ldv, ldv, vc, h->GV, true));
+    dot_f64_f32(h->Q + vb * r, V + vb * ldv, ldv, vc, r, h->parts, h->dscal + S_CROSS, st);
+    ENMF_TRY(ar(h, h->dscal + S_CROSS, 1, CommOp::Sum));
+  } else {
+    ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
+    dot_f64_f32(h->Q, V, ldv, h->n, h->r, h->parts, h->dscal + S_CROSS, st);
+  }
   objective_finish(h->dscal + S_XNORM2, h->dscal + S_CROSS, h->GU, h->GV, (int)h->r,
                    h->ftrace + t, st);
   return check_launch();
@@ -376,7 +403,7 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
   if (h->st) cudaStreamSynchronize(h->st);
   void* bufs[] = {h->dscal, h->dint, h->P, h->Q, h->GU, h->GV, h->work, h->parts,
                   h->minparts, h->pgsum, h->snaps, h->ftrace, h->x_owned, h->W64,
-                  h->tcpb_ws, h->fmax_uv, h->Ud, h->Vd, h->arena, h->Vg};
+                  h->tcpb_ws, h->fmax_uv, h->Ud, h->Vd, h->arena, h->Vg, h->Vpad};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (void* b : h->arena_extra) cudaFree(b);
@@ -429,7 +456,10 @@ enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
   ALLOC(h->dscal, S_COUNT);
   ALLOC(h->dint, I_COUNT);
   ALLOC(h->P, (size_t)(h->m_loc * r));
-  ALLOC(h->Q, (size_t)(n * r));
+  // V slices: ceil(n / world) rows per rank; Q holds world such blocks for the in-place
+  // reduce-scatter
+  h->v_pad = (n + prob->world_size - 1) / prob->world_size;
+  ALLOC(h->Q, (size_t)(std::max<int64_t>(n, h->v_pad * prob->world_size) * r));
   ALLOC(h->GU, (size_t)(r * r));
   ALLOC(h->GV, (size_t)(r * r));
   // split-K partials: enough for the small GEMMs (r x r, l x l) and for the SVD panels
@@ -445,11 +475,13 @@ enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
   ALLOC(h->pgsum, (size_t)(o.pbcd_max_iter + 1));
 #undef ALLOC
   if (s == ENMF_OK && prob->world_size > 1) {
-    // V slice of this rank: contiguous blocks, the first n % world ranks one row longer
-    const int64_t base = n / prob->world_size, extra = n % prob->world_size;
-    h->v_begin = prob->rank * base + std::min<int64_t>(prob->rank, extra);
-    h->v_count = base + (prob->rank < extra ? 1 : 0);
-    s = dalloc(&h->Vg, (size_t)(n * r));
+    // V slice of this rank: rows [rank v_pad, rank v_pad + v_count), the last one(s) shorter
+    h->v_begin = std::min<int64_t>(n, prob->rank * h->v_pad);
+    h->v_count = std::min<int64_t>(h->v_pad, n - h->v_begin);
+    if (prob->nccl_unique_id)
+      s = dalloc(&h->Vpad, (size_t)(h->v_pad * prob->world_size * r));
+    else
+      s = dalloc(&h->Vg, (size_t)(n * r));
   }
   if (s == ENMF_OK && prob->world_size > 1 && prob->nccl_unique_id) {
     if (comm_init(&h->comm, prob->nccl_unique_id, prob->world_size, prob->rank) != 0)

@@ -61,6 +61,8 @@ struct enmf_handle_s {
   // multi-rank V block: this rank updates V rows [v_begin, v_begin + v_count) and the full V
   // is reassembled by a zero-padded fp64 allreduce (exact: adding zeros), SURVEY §8(e)
   int64_t v_begin = 0, v_count = 0;
+  int64_t v_pad = 0;               // rows per V slice (ceil(n / world)); v_begin = rank v_pad
+  float* Vpad = nullptr;           // world x v_pad x r fp32: all-gather of the V slices (NCCL)
   double* Vg = nullptr;            // n x r fp64 staging of the gather
   // host-mediated collectives (enmf_set_host_allreduce) when there is no NCCL communicator
   enmf_host_allreduce_fn host_ar = nullptr;
@@ -120,7 +122,7 @@ enmf_status_t ar(enmf_handle_t h, double* buf, size_t count, CommOp op);
 enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* P,
                           const unsigned long long* vmax = nullptr);
 enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q,
-                           const unsigned long long* umax = nullptr);
+                           const unsigned long long* umax = nullptr, bool slice = false);
 enmf_status_t gram_f32(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, double* G,
                        bool sharded);
 enmf_status_t min_factor(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, int slot,
