@@ -414,29 +414,28 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
 
 // G (r x r fp64, symmetric) -> 4 digit planes of the B operand (row j of B = column j of G,
 // power-of-two scale t_j per column), layout (g * (KR/16) + kc) * 128 + ri * 16 + ki.
-__global__ void gdigits_kernel(const double* __restrict__ G, int r, int rp, int8_t* gd,
-                               double* gscale, const int* stage, int want) {
+__global__ void __launch_bounds__(KR) gdigits_kernel(const double* __restrict__ G, int r, int rp,
+                                                     int8_t* gd, double* gscale, const int* stage,
+                                                     int want) {
+  // one block per B row j (= column j of G), one thread per k index l
   if (stage != nullptr && *stage != want) return;
-  __shared__ double t[128];
-  for (int j = threadIdx.x; j < rp; j += blockDim.x) {
-    double mx = 0.0;
-    if (j < r)
-      for (int l = 0; l < r; ++l) mx = fmax(mx, fabs(G[l * r + j]));
-    t[j] = pow2s(mx);
-    if (j < r) gscale[j] = 1.0 / t[j];
-  }
-  __syncthreads();
-  const int plane = rp * KR;
-  for (int e = threadIdx.x; e < rp * KR; e += blockDim.x) {
-    const int j = e / KR, l = e % KR;
-    const double v = (j < r && l < r) ? G[l * r + j] * t[j] : 0.0;
-    const Dig4 z = digits4(v);
-    const int off = ((j >> 3) * (KR / 16) + (l >> 4)) * 128 + (j & 7) * 16 + (l & 15);
+  __shared__ double wmax[KR / 32];
+  const int j = blockIdx.x, l = threadIdx.x;
+  const double g = (j < r && l < r) ? G[(int64_t)l * r + j] : 0.0;
+  double mx = fabs(g);
 #pragma unroll
-    for (int pl = 0; pl < 4; ++pl) gd[pl * plane + off] = z.d[pl];
-  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((l & 31) == 0) wmax[l >> 5] = mx;
+  __syncthreads();
+  mx = fmax(fmax(wmax[0], wmax[1]), fmax(wmax[2], wmax[3]));
+  const double t = pow2s(mx);
+  if (l == 0 && j < r) gscale[j] = 1.0 / t;
+  const Dig4 z = digits4(g * t);
+  const int plane = rp * KR;
+  const int off = ((j >> 3) * (KR / 16) + (l >> 4)) * 128 + (j & 7) * 16 + (l & 15);
+#pragma unroll
+  for (int pl = 0; pl < 4; ++pl) gd[pl * plane + off] = z.d[pl];
 }
-
 
 // ------------------------------------------------------------------------------ HALS
 // HALS (reading R12) on the tensor cores, blocked Gauss-Seidel: a CTA holds
@@ -905,7 +904,7 @@ int tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double*
                   cudaStream_t st) {
   using namespace tpb;
   const int rp = KR;   // G padded to 128 columns: class k of the accumulators at column k * 128
-  gdigits_kernel<<<1, 256, 0, st>>>(G, r, rp, gd_work, gscale_work, stage, 0);
+  gdigits_kernel<<<rp, KR, 0, st>>>(G, r, rp, gd_work, gscale_work, stage, 0);
   Params p;
   p.F = F;
   p.ldf = ldf;
@@ -946,7 +945,7 @@ int tc_hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, co
                  int8_t* gd_work, double* gscale_work, const int* stage, double* minparts,
                  int nparts, unsigned long long* colmax, int* fallbacks, cudaStream_t st) {
   using namespace tpb;
-  gdigits_kernel<<<1, 256, 0, st>>>(G, r, KR, gd_work, gscale_work, stage, 1);
+  gdigits_kernel<<<KR, KR, 0, st>>>(G, r, KR, gd_work, gscale_work, stage, 1);
   HParams p;
   p.F = F;
   p.ldf = ldf;
