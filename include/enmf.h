@@ -149,6 +149,16 @@ enmf_status_t enmf_rotate(enmf_handle_t h, float* U, int64_t ldu, float* V, int6
 enmf_status_t enmf_init(enmf_handle_t h, const float* X, int64_t ldx, float* U, int64_t ldu,
                         float* V, int64_t ldv, enmf_init_info_t* info_host);
 
+/* Post-rotation variant (ii) of the paper's ablation (Table
+ * ablation_projection): "direct projection onto the nonnegative orthant followed by HALS
+ * descent".  U (this rank's row_count x r, ld ldu) and V (n x r, ld ldv), device pointers,
+ * caller-owned, are replaced in place by max(0, .) and the handle enters the HALS stage, so
+ * the next enmf_iterate runs HALS sweeps from the projected point instead of the ascent
+ * (lift + PBCD, the method's own feasibility stage).  Stream-ordered, synchronises before
+ * returning.  ENMF_ERR_INVALID_ARG on NULL pointers or ld < r; V is replicated, so every rank
+ * projects the same V identically. */
+enmf_status_t enmf_project(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv);
+
 /* Stage machine access (checkpoint/resume and shared-init parity runs): stage 0 = ascent,
  * 1 = HALS; lambda_u / lambda_v are the lift constants (reading R9). */
 enmf_status_t enmf_set_stage(enmf_handle_t h, int stage, double lambda_u, double lambda_v);

@@ -56,6 +56,8 @@ def lib():
             getattr(L, f).restype = ctypes.c_double
         L.or_xnorm2.argtypes = [_F, _i64, _i64]
         L.or_xnorm2.restype = ctypes.c_double
+        L.or_project.argtypes = [_D, _i64]
+        L.or_project.restype = None
         L.or_negativity.argtypes = [_D, _i64]
         L.or_negativity.restype = ctypes.c_double
         L.or_svd_jacobi.argtypes = [_D, _i64, ctypes.c_int, _D, _D, _D]
@@ -147,6 +149,13 @@ def xnorm2(X):
 def negativity(A):
     A, pa = _f64(A)
     return lib().or_negativity(pa, A.size)
+
+
+def project(A):
+    """Post-rotation variant (ii) of the ablation: max(0, A) on a copy."""
+    A = np.array(A, dtype=np.float64, order="C")
+    lib().or_project(A.ctypes.data_as(_D), A.size)
+    return A
 
 
 def svd_jacobi(A):

@@ -112,6 +112,13 @@ double or_negativity(const double* A, int64_t count) {
   return s;
 }
 
+/* PAPER.md:2096-2099 (Table ablation_projection, variant (ii)): "direct projection onto the
+ * nonnegative orthant" -- the Euclidean projection, entrywise max{0, a}. */
+void or_project(double* A, int64_t count) {
+  for (int64_t e = 0; e < count; ++e)
+    if (A[e] < 0.0) A[e] = 0.0;
+}
+
 /* ------------------------------------------------------------------------- */
 /* Dense small linear algebra.                                               */
 /* ------------------------------------------------------------------------- */

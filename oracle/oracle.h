@@ -60,6 +60,10 @@ void or_procrustes(const double* W, const double* B, int64_t rows, int r, double
 int64_t or_admm_rotate(const double* W, int64_t rows, int r, double rho, int T, double* R,
                        double* neg_trace);
 
+/* ---- post-rotation variant "direct projection onto the nonnegative orthant" (ablation,
+ * PAPER.md:2096-2099, Table ablation_projection (ii)): A <- max(0, A) elementwise ---- */
+void or_project(double* A, int64_t count);
+
 /* ---- feasibility stage, Alg. 2 PAPER.md:230-244 ---- */
 void or_lift(double* A, int64_t count, double lam);             /* Eq.(6)/(7) */
 /* PBCD on F (rows x r) with fixed cross term C (rows x r) and Gram G (r x r):

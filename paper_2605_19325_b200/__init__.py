@@ -81,6 +81,7 @@ _sigs = {
     "enmf_init": (ctypes.c_int, [_H, _P, _I64, _P, _I64, _P, _I64, ctypes.POINTER(InitInfo)]),
     "enmf_set_stage": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_double, ctypes.c_double]),
     "enmf_get_stage": (ctypes.c_int, [_H, ctypes.POINTER(ctypes.c_int), _D, _D]),
+    "enmf_project": (ctypes.c_int, [_H, _P, _I64, _P, _I64]),
     "enmf_iterate": (ctypes.c_int, [_H, _P, _I64, _P, _I64, ctypes.c_int, _D,
                                     ctypes.POINTER(IterInfo)]),
     "enmf_iterate_host": (ctypes.c_int, [_H, _P, _P, ctypes.c_int, _D,
@@ -242,6 +243,13 @@ class Enmf:
         _check(_lib.enmf_get_stage(self._h, ctypes.byref(s), ctypes.byref(lu), ctypes.byref(lv)),
                "enmf_get_stage")
         return s.value, lu.value, lv.value
+
+    def project(self, U, V):
+        """Post-rotation variant 'projection + HALS': U, V <- max(0, .)
+        in place and the HALS stage."""
+        pu, ldu = _mat(U, self.r, "U")
+        pv, ldv = _mat(V, self.r, "V")
+        _check(_lib.enmf_project(self._h, pu, ldu, pv, ldv), "enmf_project")
 
     def iterate(self, U, V, n_iters, trace=True):
         pu, ldu = _mat(U, self.r, "U")

@@ -559,6 +559,20 @@ enmf_status_t enmf_set_stage(enmf_handle_t h, int stage, double lambda_u, double
   return ENMF_OK;
 }
 
+enmf_status_t enmf_project(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv) {
+  if (!h || !U || !V || ldu < h->r || ldv < h->r) return ENMF_ERR_INVALID_ARG;
+  LaunchScope ls(h);
+  project_f32(U, ldu, h->m_loc, h->r, h->st);
+  project_f32(V, ldv, h->n, h->r, h->st);
+  int st = 1;
+  CUDA_TRY(cudaMemcpyAsync(h->dint + I_STAGE, &st, sizeof(int), cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  ENMF_TRY(check_launch());
+  h->stage_known_hals = true;
+  h->umax_valid = h->vmax_valid = false;
+  return ENMF_OK;
+}
+
 enmf_status_t enmf_get_stage(enmf_handle_t h, int* stage, double* lambda_u, double* lambda_v) {
   if (!h) return ENMF_ERR_INVALID_ARG;
   int st = 0;

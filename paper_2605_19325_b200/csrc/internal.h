@@ -51,6 +51,8 @@ void reduce_parts(const double* parts, int nparts, int64_t len, double* out, cud
 void x_stats(const float* X, int64_t ldx, int64_t rows, int64_t n, double* parts, int nparts,
              double* out4, cudaStream_t st);
 int x_stats_parts(int64_t rows);
+// A <- max(0, A) in place (rows x cols, ld): post-rotation projection.
+void project_f32(float* A, int64_t ld, int64_t rows, int64_t cols, cudaStream_t st);
 // min over an fp32 matrix (rows x cols, ld): partials then out[0].
 void min_f32(const float* A, int64_t ld, int64_t rows, int64_t cols, double* parts,
              double* out, cudaStream_t st);

@@ -108,6 +108,33 @@ __global__ void min_f32_kernel(const float* __restrict__ A, int64_t ld, int64_t 
   if (threadIdx.x == 0) parts[blockIdx.x] = mn;
 }
 
+// Post-rotation variant (ii) of the ablation: A <- max(0, A) in place,
+// float4 along rows when the rows are 16-byte aligned (HBM-bound: 8 B per element).
+__global__ void project_f32_kernel(float* __restrict__ A, int64_t ld, int64_t rows, int64_t cols,
+                                   bool vec) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (vec) {
+    const int64_t c4 = cols / 4, total = rows * c4;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += stride) {
+      const int64_t i = e / c4, j = e - i * c4;
+      float4* p = reinterpret_cast<float4*>(A + i * ld) + j;
+      float4 v = *p;
+      v.x = v.x < 0.f ? 0.f : v.x;
+      v.y = v.y < 0.f ? 0.f : v.y;
+      v.z = v.z < 0.f ? 0.f : v.z;
+      v.w = v.w < 0.f ? 0.f : v.w;
+      *p = v;
+    }
+  } else {
+    const int64_t total = rows * cols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += stride) {
+      const int64_t i = e / cols, j = e - i * cols;
+      float* p = A + i * ld + j;
+      if (*p < 0.f) *p = 0.f;
+    }
+  }
+}
+
 __global__ void reduce_min_kernel(const double* parts, int n, double* out) {
   if (threadIdx.x != 0) return;
   double mn = DBL_MAX;
@@ -782,6 +809,13 @@ void min_f32(const float* A, int64_t ld, int64_t rows, int64_t cols, double* par
   min_f32_kernel<<<kStatGrid, 256, 0, st>>>(A, ld, rows, cols, parts);
   reduce_min_kernel<<<1, 32, 0, st>>>(parts, kStatGrid, out);
   count_launch(2);
+}
+
+void project_f32(float* A, int64_t ld, int64_t rows, int64_t cols, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  const bool vec = cols % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+  project_f32_kernel<<<kStatGrid, 256, 0, st>>>(A, ld, rows, cols, vec);
+  count_launch();
 }
 
 void reduce_min(const double* parts, int n, double* out, cudaStream_t st) {

@@ -95,6 +95,38 @@ def test_hals_sweep_rows_outgrowing_digit_scale(cfg, prec):
 
 
 @pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
+@pytest.mark.parametrize("cfg", [CASES[0], CASES[4], CASES[6]], ids=[IDS[0], IDS[4], IDS[6]])
+def test_projection_then_hals(cfg, prec):
+    """Post-rotation variant (ii) of the ablation: enmf_project on the
+    rotated (infeasible) point, then HALS sweeps, against oracle.project + oracle HALS sweeps.
+    The projection is exact (bitwise); the sweeps are held to the HALS bars (one sweep 1e-5,
+    10-sweep f trajectory 1e-4 or the TC conditioning bound)."""
+    h, X, _ = make(cfg, precision=prec)
+    U0, V0, _, _ = rotated_point(X, cfg.r)
+    U, V = to_dev(U0), to_dev(V0)
+    h.project(U, V)
+    Up, Vp = oracle.project(U0), oracle.project(V0)
+    assert np.array_equal(to_np(U), Up.astype(np.float32)) and \
+        np.array_equal(to_np(V), Vp.astype(np.float32))
+    assert h.get_stage()[0] == 1
+    f_gpu, info = h.iterate(U, V, 10)
+    assert info["hals_sweeps"] == 10 and info["ascent_sweeps"] == 0
+    U1, V1, _, _ = oracle.sweep(X, Up, Vp, oracle.SweepState(stage=1), F32STATE(cfg.r))
+    Uo, Vo, f_or = oracle_sweeps(X, Up, Vp, oracle.SweepState(stage=1), 10, cfg.r)
+    err = np.abs(f_gpu - f_or) / f_or
+    cond = oracle.xnorm2(X) / f_or
+    bound = np.maximum(1e-4, 1e-8 * cond) if prec == TC else 1e-4
+    print(f"{cfg.name} prec={h.precision}: projection + 10 HALS sweeps, max f err {err.max():.2e}")
+    assert np.all(err < bound), err
+    # one sweep from the projected point: BASELINE's per-update bar
+    h2, _, _ = make(cfg, precision=prec)
+    U, V = to_dev(U0), to_dev(V0)
+    h2.project(U, V)
+    h2.iterate(U, V, 1)
+    assert rel_fro(to_np(U), U1) < 1e-5 and rel_fro(to_np(V), V1) < 1e-5
+
+
+@pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
 @pytest.mark.parametrize("cfg", CASES[:4] + [CASES[6]], ids=IDS[:4] + [IDS[6]])
 def test_hals_trajectory_50_sweeps(cfg, prec):
     """50 HALS sweeps from a shared feasible point: final factors within 1e-4, the direct

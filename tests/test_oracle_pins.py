@@ -277,6 +277,23 @@ def test_pbcd_state_rounding_sensitivity():
 
 
 # ---------------------------------------------------------------- P5 HALS
+def test_project_is_the_bounded_least_squares_solution():
+    """or_project (ablation variant (ii)) against the Euclidean projection
+    onto {Y >= 0} computed by a bounded least-squares solver (scipy lsq_linear on the identity
+    system, bounds [0, inf)) -- a different algorithm for the same minimiser -- plus the
+    special cases: idempotent, fixes the orthant, zero on the negative orthant."""
+    from scipy.optimize import lsq_linear
+    g = np.random.default_rng(11)
+    A = g.normal(size=(6, 5))
+    P = oracle.project(A)
+    ref = lsq_linear(np.eye(A.size), A.ravel(), bounds=(0.0, np.inf), tol=1e-14).x
+    assert np.allclose(P.ravel(), ref, atol=1e-12)
+    assert np.array_equal(oracle.project(P), P)
+    B = np.abs(A)
+    assert np.array_equal(oracle.project(B), B)
+    assert np.array_equal(oracle.project(-B), np.zeros_like(B))
+
+
 def test_hals_matches_textbook_residual_form():
     """HALS (cited Cichocki & Phan): column k is the projected
     least-squares solution max(0, (X - sum_{l!=k} U_l V_l^T) V_k / ||V_k||^2)."""
