@@ -133,6 +133,22 @@ enmf_status_t enmf_destroy(enmf_handle_t h);
  * Resets the stage machine. */
 enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx);
 
+/* Sparse X (the paper's sparse Reuters experiment):
+ * bind this rank's rows of X as CSR instead of a dense matrix.  row_ptr (row_count + 1,
+ * int64, row_ptr[0] = 0), col_idx (nnz, int32, strictly ascending within a row, in [0, n))
+ * and vals (nnz, fp32, >= 0, finite) are DEVICE pointers, caller-owned, read-only and kept
+ * (not copied) until the next set_data call or destroy; zeros not stored are zeros of X.
+ * The handle builds a CSC copy for X^T U (deterministic: entries of a column in ascending
+ * row order) and computes ||X||^2 over the stored values.  Every later call treats X through
+ * P = X V and Q = X^T U (fp64-accumulating SpMM), so init / iterate / objective / kkt work
+ * unchanged; enmf_objective(exact = 1) evaluates ||X||^2 - 2 sum_stored x_ij u_i.v_j +
+ * <U^T U, V^T V>.  Block updates run on the tensor-core row kernels unless the precision
+ * option is ENMF_PREC_FP64.  Errors: ENMF_ERR_INVALID_ARG (NULL pointers, bad row ranges or
+ * column order), ENMF_ERR_SHAPE (nnz or n above 2^31 - 1), ENMF_ERR_NEGATIVE_X,
+ * ENMF_ERR_NONFINITE, ENMF_ERR_OOM. */
+enmf_status_t enmf_set_data_csr(enmf_handle_t h, const int64_t* row_ptr, const int32_t* col_idx,
+                                const float* vals, int64_t nnz);
+
 /* Rank-r truncated SVD with balanced scaling U* = U S^1/2, V* = V S^1/2 by
  * a randomised range finder (reading R3); sign rule R5.  Writes U* (this
  * rank's rows) into U and V* into V; sigma_host (r values) may be NULL. */

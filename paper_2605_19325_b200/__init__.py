@@ -76,6 +76,7 @@ _sigs = {
                                    ctypes.POINTER(_H)]),
     "enmf_destroy": (ctypes.c_int, [_H]),
     "enmf_set_data": (ctypes.c_int, [_H, _P, _I64]),
+    "enmf_set_data_csr": (ctypes.c_int, [_H, _P, _P, _P, _I64]),
     "enmf_svd": (ctypes.c_int, [_H, _P, _I64, _P, _I64, _D]),
     "enmf_rotate": (ctypes.c_int, [_H, _P, _I64, _P, _I64, ctypes.POINTER(InitInfo)]),
     "enmf_init": (ctypes.c_int, [_H, _P, _I64, _P, _I64, _P, _I64, ctypes.POINTER(InitInfo)]),
@@ -207,6 +208,21 @@ class Enmf:
         px, ldx = _mat(X, self.n, "X")
         self._X = X
         _check(_lib.enmf_set_data(self._h, px, ldx), "enmf_set_data")
+
+    def set_data_csr(self, row_ptr, col_idx, vals):
+        """Bind this rank's rows of a sparse X as CSR CUDA tensors (row_ptr int64 of length
+        row_count + 1, col_idx int32 ascending per row, vals float32); see enmf_set_data_csr."""
+        import torch
+        for t, dt, name in ((row_ptr, torch.int64, "row_ptr"), (col_idx, torch.int32, "col_idx"),
+                            (vals, torch.float32, "vals")):
+            if not (t.is_cuda and t.dtype == dt and t.is_contiguous()):
+                raise TypeError(f"{name}: contiguous CUDA {dt} tensor required")
+        if row_ptr.numel() != self.rows + 1 or col_idx.numel() != vals.numel():
+            raise ValueError("row_ptr / col_idx / vals sizes")
+        self._X = (row_ptr, col_idx, vals)
+        _check(_lib.enmf_set_data_csr(self._h, row_ptr.data_ptr(), col_idx.data_ptr() or None,
+                                      vals.data_ptr() or None, int(vals.numel())),
+               "enmf_set_data_csr")
 
     def svd(self, U, V):
         pu, ldu = _mat(U, self.r, "U")

@@ -2,6 +2,7 @@
 // Alg. 3 on one stream.  All arithmetic runs in the kernels of this
 // library; this file only sequences launches and NCCL collectives.
 #include <cuda_runtime.h>
+#include <float.h>
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -98,7 +99,9 @@ static void prof_collect(enmf_handle_t h) {
 enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* P,
                           const unsigned long long* vmax) {
   ENMF_TRY(prof_mark(h, 0));
-  if (h->tc) {
+  if (h->sparse) {
+    spmm<float>(h->csr_ptr, h->csr_col, h->csr_val, h->m_loc, V, ldv, (int)h->r, P, h->r, h->st);
+  } else if (h->tc) {
     if (tc_xv(h->tc, V, ldv, P, h->st, vmax) != 0) return ENMF_ERR_CUDA;
   } else {
     GemmOut o;
@@ -116,7 +119,9 @@ enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* 
 enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q,
                            const unsigned long long* umax, bool slice) {
   ENMF_TRY(prof_mark(h, 1));
-  if (h->tc) {
+  if (h->sparse) {
+    spmm<float>(h->csc_ptr, h->csc_row, h->csc_val, h->n, U, ldu, (int)h->r, Q, h->r, h->st);
+  } else if (h->tc) {
     if (tc_xtu(h->tc, U, ldu, Q, h->st, umax) != 0) return ENMF_ERR_CUDA;
   } else {
     GemmOut o;
@@ -187,10 +192,13 @@ enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
                 stage, h->minparts, h->tc_pbcd, h->st, h->tc_pbcd ? colmax : nullptr);
   }
   if (h->tc_hals) {
+    // tensor-core HALS; if G has a column too ill-conditioned for the digit coupling the
+    // device flag I_HALS_ILL hands the sweep to the SIMT fp64 kernel (no host sync)
     if (tc_hals_rows(F, ldf, rows, r, C, G, reinterpret_cast<int8_t*>(h->tcpb_ws + 128),
                      h->tcpb_ws, stage, h->minparts, kRowGrid, colmax, h->dint + I_HALS_FB,
-                     h->st))
+                     h->dint + I_HALS_ILL, h->st))
       return ENMF_ERR_CUDA;
+    hals_rows(F, ldf, rows, r, C, G, stage, h->minparts, h->st, colmax, h->dint + I_HALS_ILL);
   } else {
     hals_rows(F, ldf, rows, r, C, G, stage, h->minparts, h->st, colmax);
   }
@@ -395,6 +403,7 @@ enmf_status_t enmf_nccl_unique_id(void* out128) {
 
 const char* enmf_precision_name(enmf_handle_t h) {
   if (!h) return "none";
+  if (h->sparse) return h->tc_pbcd ? "csr-f64-spmm+tc-rows" : "csr-f64-spmm";
   return h->precision == ENMF_PREC_TC ? "tc-i8x4-exact" : "fp64-simt";
 }
 
@@ -403,7 +412,8 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
   if (h->st) cudaStreamSynchronize(h->st);
   void* bufs[] = {h->dscal, h->dint, h->P, h->Q, h->GU, h->GV, h->work, h->parts,
                   h->minparts, h->pgsum, h->snaps, h->ftrace, h->x_owned, h->W64,
-                  h->tcpb_ws, h->fmax_uv, h->Ud, h->Vd, h->arena, h->Vg, h->Vpad};
+                  h->tcpb_ws, h->fmax_uv, h->Ud, h->Vd, h->arena, h->Vg, h->Vpad,
+                  h->csc_ptr, h->csc_row, h->csc_val};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (void* b : h->arena_extra) cudaFree(b);
@@ -507,6 +517,7 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
   h->X = X;
   h->ldx = ldx;
   h->bound = false;
+  h->sparse = false;
   const int np = x_stats_parts(h->m_loc);
   double* out3 = h->work;   // [sum, min, nonfinite, max|X| of this rank's rows]
   x_stats(X, ldx, h->m_loc, h->n, h->parts, np, out3, h->st);
@@ -539,6 +550,82 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
   if (prec == ENMF_PREC_TC && !h->fmax_uv) ENMF_TRY(dalloc(&h->fmax_uv, 256));
   h->umax_valid = h->vmax_valid = false;
   h->precision = prec;
+  int zero[I_COUNT] = {0};
+  CUDA_TRY(cudaMemcpyAsync(h->dint, zero, sizeof(zero), cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  h->stage_known_hals = false;
+  h->bound = true;
+  return check_launch();
+}
+
+enmf_status_t enmf_set_data_csr(enmf_handle_t h, const int64_t* row_ptr, const int32_t* col_idx,
+                                const float* vals, int64_t nnz) {
+  if (!h || !row_ptr || nnz < 0 || (nnz > 0 && (!col_idx || !vals))) return ENMF_ERR_INVALID_ARG;
+  if (nnz > INT32_MAX || h->n > INT32_MAX) return ENMF_ERR_SHAPE;
+  LaunchScope ls(h);
+  h->bound = false;
+  h->X = nullptr;
+  h->ldx = 0;
+  // layout check: row ranges valid, columns strictly ascending in [0, n)
+  int* bad = reinterpret_cast<int*>(h->work);
+  if (csr_check(row_ptr, col_idx, h->m_loc, h->n, nnz, bad, h->st)) return ENMF_ERR_CUDA;
+  int bad_h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  if (bad_h) return ENMF_ERR_INVALID_ARG;
+  // ||X||^2, min, non-finite count over the stored values (as 4096-wide rows plus a tail)
+  double hv[2][4] = {{0.0, DBL_MAX, 0.0, 0.0}, {0.0, DBL_MAX, 0.0, 0.0}};
+  const int64_t W = 4096, full = nnz / W, tail = nnz - full * W;
+  double* out4 = h->work;
+  if (full > 0) {
+    x_stats(vals, W, full, W, h->parts, x_stats_parts(full), out4, h->st);
+    CUDA_TRY(cudaMemcpyAsync(hv[0], out4, sizeof(hv[0]), cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+  }
+  if (tail > 0) {
+    x_stats(vals + full * W, tail, 1, tail, h->parts, x_stats_parts(1), out4, h->st);
+    CUDA_TRY(cudaMemcpyAsync(hv[1], out4, sizeof(hv[1]), cudaMemcpyDeviceToHost, h->st));
+    CUDA_TRY(cudaStreamSynchronize(h->st));
+  }
+  double st3[3] = {hv[0][0] + hv[1][0], std::min(hv[0][1], hv[1][1]), hv[0][2] + hv[1][2]};
+  CUDA_TRY(cudaMemcpyAsync(out4, st3, sizeof(st3), cudaMemcpyHostToDevice, h->st));
+  ENMF_TRY(ar(h, out4, 1, CommOp::Sum));
+  ENMF_TRY(ar(h, out4 + 1, 1, CommOp::Min));
+  ENMF_TRY(ar(h, out4 + 2, 1, CommOp::Sum));
+  CUDA_TRY(cudaMemcpyAsync(st3, out4, sizeof(st3), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  if (st3[2] > 0) return ENMF_ERR_NONFINITE;
+  if (st3[1] < 0) return ENMF_ERR_NEGATIVE_X;
+  CUDA_TRY(cudaMemcpyAsync(h->dscal + S_XNORM2, out4, sizeof(double), cudaMemcpyDeviceToDevice,
+                           h->st));
+  // CSC copy for X^T U
+  if (h->csc_ptr) cudaFree(h->csc_ptr);
+  if (h->csc_row) cudaFree(h->csc_row);
+  if (h->csc_val) cudaFree(h->csc_val);
+  h->csc_ptr = nullptr;
+  h->csc_row = nullptr;
+  h->csc_val = nullptr;
+  ENMF_TRY(dalloc(&h->csc_ptr, (size_t)(h->n + 1)));
+  ENMF_TRY(dalloc(&h->csc_row, (size_t)std::max<int64_t>(nnz, 1)));
+  ENMF_TRY(dalloc(&h->csc_val, (size_t)std::max<int64_t>(nnz, 1)));
+  const int rc = csr_to_csc(row_ptr, col_idx, vals, h->m_loc, h->n, nnz, h->csc_ptr, h->csc_row,
+                            h->csc_val, h->st);
+  if (rc) return rc == 2 ? ENMF_ERR_OOM : ENMF_ERR_CUDA;
+  h->csr_ptr = row_ptr;
+  h->csr_col = col_idx;
+  h->csr_val = vals;
+  h->nnz = nnz;
+  h->sparse = true;
+  // X passes: fp64 SpMM; block updates on the tensor-core row kernels unless precision FP64
+  if (h->tc) { tc_destroy(h->tc); h->tc = nullptr; }
+  const char* tpe = getenv("ENMF_TC_PBCD");
+  h->tc_pbcd = h->opt.precision != ENMF_PREC_FP64 && tc_pbcd_supported((int)h->r) &&
+               !(tpe && tpe[0] == '0');
+  if (h->tc_pbcd && !h->tcpb_ws) ENMF_TRY(dalloc(&h->tcpb_ws, 128 + 4 * 128 * 128 / 8));
+  const char* the = getenv("ENMF_TC_HALS");
+  h->tc_hals = h->tc_pbcd && !(the && the[0] == '0');
+  h->umax_valid = h->vmax_valid = false;
+  h->precision = ENMF_PREC_FP64;
   int zero[I_COUNT] = {0};
   CUDA_TRY(cudaMemcpyAsync(h->dint, zero, sizeof(zero), cudaMemcpyHostToDevice, h->st));
   CUDA_TRY(cudaStreamSynchronize(h->st));
@@ -694,7 +781,24 @@ enmf_status_t enmf_objective(enmf_handle_t h, const float* U, int64_t ldu, const
   LaunchScope ls(h);
   const bool sh = h->prob.world_size > 1;
   double* f = h->dscal + S_SCRATCH;
-  if (exact) {
+  if (exact && h->sparse) {
+    // sparse X: ||X||^2 - 2 sum over stored entries x_ij (u_i . v_j) + ||U V^T||^2, the cross
+    // term entry by entry (not through Q) and ||U V^T||^2 = <U^T U, V^T V> exactly
+    double* parts = nullptr;
+    CUDA_TRY(cudaMallocAsync(&parts, sizeof(double) * sddmm_parts(h->m_loc), h->st));
+    sddmm_dot(h->csr_ptr, h->csr_col, h->csr_val, h->m_loc, U, ldu, V, ldv, (int)h->r, parts,
+              h->dscal + S_CROSS, h->st);
+    CUDA_TRY(cudaFreeAsync(parts, h->st));
+    ENMF_TRY(ar(h, h->dscal + S_CROSS, 1, CommOp::Sum));
+    ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh));
+    double* gv = h->work + h->work_elems - (size_t)(h->r * h->r);
+    GemmOut o;
+    o.C = gv;
+    o.ldc = h->r;
+    gemm<float, float>(true, V, ldv, V, ldv, h->r, h->r, h->n, o, h->work,
+                       h->work_elems - (size_t)(h->r * h->r), h->st);
+    objective_finish(h->dscal + S_XNORM2, h->dscal + S_CROSS, h->GU, gv, (int)h->r, f, h->st);
+  } else if (exact) {
     int np = 0;
     frob_direct(h->X, h->ldx, h->m_loc, h->n, U, ldu, V, ldv, (int)h->r, h->parts, &np, h->st);
     reduce_parts(h->parts, np, 1, f, h->st);

@@ -161,6 +161,13 @@ enmf_status_t svd_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t
   // the 2q + 2 X passes: on the tensor-core path as exact int8-digit products in blocks of
   // <= 128 columns (tc_xf, ~1e-9 relative), else the SIMT fp64-accumulating GEMM
   auto xprod = [&](bool trans, const double* F, double* out) -> enmf_status_t {
+    if (h->sparse) {                 // CSR / CSC SpMM in fp64 (kernels_sparse.cu)
+      if (trans)
+        spmm<double>(h->csc_ptr, h->csc_row, h->csc_val, n, F, l, l, out, l, h->st);
+      else
+        spmm<double>(h->csr_ptr, h->csr_col, h->csr_val, mr, F, l, l, out, l, h->st);
+      return ENMF_OK;
+    }
     if (h->tc) {
       const int rc = tc_xf(h->tc, trans, F, l, l, out, l, h->st);
       return rc == 0 ? ENMF_OK : (rc == 2 ? ENMF_ERR_OOM : ENMF_ERR_CUDA);

@@ -19,7 +19,7 @@ enum {
   S_WMAX, S_COUNT = 16
 };
 // device int slots
-enum { I_STAGE = 0, I_KSTAR_U, I_KSTAR_V, I_CNT_ASC, I_CNT_HALS, I_BAD, I_HALS_FB, I_COUNT = 8 };
+enum { I_STAGE = 0, I_KSTAR_U, I_KSTAR_V, I_CNT_ASC, I_CNT_HALS, I_BAD, I_HALS_FB, I_HALS_ILL, I_COUNT = 8 };
 
 }  // namespace enmf
 
@@ -61,7 +61,17 @@ struct enmf_handle_s {
   // multi-rank V block: this rank updates V rows [v_begin, v_begin + v_count) and the full V
   // is reassembled by a zero-padded fp64 allreduce (exact: adding zeros), SURVEY §8(e)
   int64_t v_begin = 0, v_count = 0;
-  int64_t v_pad = 0;               // rows per V slice (ceil(n / world)); v_begin = rank v_pad
+  int64_t v_pad = 0;
+  // sparse X (enmf_set_data_csr): this rank's rows as CSR (caller-owned) and a handle-owned
+  // CSC copy for X^T U
+  bool sparse = false;
+  const int64_t* csr_ptr = nullptr;
+  const int32_t* csr_col = nullptr;
+  const float* csr_val = nullptr;
+  int64_t nnz = 0;
+  int64_t* csc_ptr = nullptr;
+  int32_t* csc_row = nullptr;
+  float* csc_val = nullptr;               // rows per V slice (ceil(n / world)); v_begin = rank v_pad
   float* Vpad = nullptr;           // world x v_pad x r fp32: all-gather of the V slices (NCCL)
   double* Vg = nullptr;            // n x r fp64 staging of the gather
   // host-mediated collectives (enmf_set_host_allreduce) when there is no NCCL communicator

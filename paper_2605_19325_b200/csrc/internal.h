@@ -51,6 +51,22 @@ void reduce_parts(const double* parts, int nparts, int64_t len, double* out, cud
 void x_stats(const float* X, int64_t ldx, int64_t rows, int64_t n, double* parts, int nparts,
              double* out4, cudaStream_t st);
 int x_stats_parts(int64_t rows);
+// Sparse X (kernels_sparse.cu): out (rows x ncols, ld ldo, fp64) = A B for a CSR / CSC block
+// A (ptr rows + 1, idx, val) and a dense B (ld ldb); ncols any (128-column launches).
+template <typename T>
+void spmm(const int64_t* ptr, const int32_t* idx, const float* val, int64_t rows, const T* B,
+          int64_t ldb, int ncols, double* out, int64_t ldo, cudaStream_t st);
+// nonzero *bad_dev if a row range is invalid or its columns are not strictly ascending in [0, n)
+int csr_check(const int64_t* ptr, const int32_t* col, int64_t rows, int64_t n, int64_t nnz,
+              int* bad_dev, cudaStream_t st);
+// CSC copy (colptr n + 1, rowidx, cval: nnz) of a CSR block; 0 ok, 2 out of memory / too big.
+int csr_to_csc(const int64_t* ptr, const int32_t* col, const float* val, int64_t rows, int64_t n,
+               int64_t nnz, int64_t* colptr, int32_t* rowidx, float* cval, cudaStream_t st);
+// out = sum over stored entries x_ij (u_i . v_j); parts >= sddmm_parts(rows) doubles.
+int sddmm_parts(int64_t rows);
+void sddmm_dot(const int64_t* ptr, const int32_t* idx, const float* val, int64_t rows,
+               const float* U, int64_t ldu, const float* V, int64_t ldv, int r, double* parts,
+               double* out, cudaStream_t st);
 // A <- max(0, A) in place (rows x cols, ld): post-rotation projection.
 void project_f32(float* A, int64_t ld, int64_t rows, int64_t cols, cudaStream_t st);
 // min over an fp32 matrix (rows x cols, ld): partials then out[0].
@@ -76,7 +92,8 @@ constexpr int kRowGrid = 2 * kSMs;
 constexpr int kRowWarps = 8;
 void hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
                const int* stage, double* minparts, cudaStream_t st,
-               unsigned long long* colmax = nullptr);
+               unsigned long long* colmax = nullptr, const int* gate = nullptr);
+// (gate: run only if *gate != 0 -- the device-side fallback of tc_hals_rows)
 // PBCD phase A (all max_iter inner iterations, snapshots of every iterate, per-warp
 // partial ||M o grad||^2 for each iteration 0..max_iter), runs only in the ascent stage.
 void pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,

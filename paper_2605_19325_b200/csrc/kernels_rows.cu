@@ -88,14 +88,14 @@ template <int CPL, int RB>
 __global__ void __launch_bounds__(32 * kRowWarps)
 hals_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r, const double* __restrict__ C,
             const double* __restrict__ G, const int* __restrict__ stage, double* minparts,
-            unsigned long long* colmax) {
+            unsigned long long* colmax, const int* __restrict__ gate) {
   constexpr int RP = 32 * CPL;
   extern __shared__ double smem[];
   double* Gs = smem;
   double* Ss = smem + RP * RP + (threadIdx.x >> 5) * RB * RP;
   __shared__ double wmin_s[kRowWarps];
   __shared__ double ginv[RP];                 // 1 / G_kk, 0 where G_kk <= 0 (column skipped)
-  const bool active = stage == nullptr || *stage == 1;
+  const bool active = (stage == nullptr || *stage == 1) && (gate == nullptr || *gate != 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double wmin = DBL_MAX;
   double cmax[CPL];                  // max |F| of my columns lane + 32 c over my rows
@@ -468,13 +468,13 @@ void set_smem(K kernel, size_t bytes) {
 
 void hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
                const int* stage, double* minparts, cudaStream_t st,
-               unsigned long long* colmax) {
+               unsigned long long* colmax, const int* gate) {
 #define CALL(CPL)                                                                      \
   {                                                                                    \
     auto k = hals_kernel<CPL, 8>;                                                      \
     size_t sm = row_smem<CPL>(0, 8);                                                   \
     set_smem(k, sm);                                                                   \
-    k<<<kRowGrid, 32 * kRowWarps, sm, st>>>(F, ldf, rows, r, C, G, stage, minparts, colmax); \
+    k<<<kRowGrid, 32 * kRowWarps, sm, st>>>(F, ldf, rows, r, C, G, stage, minparts, colmax, gate); \
   }
   ENMF_CPL_DISPATCH(r, CALL);
 #undef CALL

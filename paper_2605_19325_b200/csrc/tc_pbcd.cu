@@ -416,18 +416,33 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
 // power-of-two scale t_j per column), layout (g * (KR/16) + kc) * 128 + ri * 16 + ki.
 __global__ void __launch_bounds__(KR) gdigits_kernel(const double* __restrict__ G, int r, int rp,
                                                      int8_t* gd, double* gscale, const int* stage,
-                                                     int want) {
+                                                     int want, int* ill) {
   // one block per B row j (= column j of G), one thread per k index l
   if (stage != nullptr && *stage != want) return;
-  __shared__ double wmax[KR / 32];
+  __shared__ double wmax[KR / 32], wsum[KR / 32];
   const int j = blockIdx.x, l = threadIdx.x;
   const double g = (j < r && l < r) ? G[(int64_t)l * r + j] : 0.0;
-  double mx = fabs(g);
+  double mx = fabs(g), sm = fabs(g);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((l & 31) == 0) wmax[l >> 5] = mx;
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+  }
+  if ((l & 31) == 0) {
+    wmax[l >> 5] = mx;
+    wsum[l >> 5] = sm;
+  }
   __syncthreads();
   mx = fmax(fmax(wmax[0], wmax[1]), fmax(wmax[2], wmax[3]));
+  // HALS conditioning guard: the digit coupling errs by ~2^-26 max|u| sum_l |G_lj| in t_j,
+  // i.e. 2^-26 sum_l |G_lj| / G_jj relative in the update of u_j.  A column whose diagonal is
+  // 2^16 below its absolute column sum (a nearly-zero factor column still coupled to the
+  // others) would lose all accuracy, so the SIMT fp64 kernel takes the sweep (*ill != 0).
+  if (ill != nullptr && l == 0 && j < r) {
+    const double colsum = (wsum[0] + wsum[1]) + (wsum[2] + wsum[3]);
+    const double gjj = G[(int64_t)j * r + j];
+    if (gjj > 0.0 && colsum > 65536.0 * gjj) atomicOr(ill, 1);
+  }
   const double t = pow2s(mx);
   if (l == 0 && j < r) gscale[j] = 1.0 / t;
   const Dig4 z = digits4(g * t);
@@ -476,6 +491,7 @@ struct HParams {
   int nparts;
   unsigned long long* colmax;                 // optional, u64[r]
   int* fallbacks;                             // optional
+  const int* ill;                             // optional: nonzero -> the SIMT kernel runs
 };
 
 // (k, j), j >= k, of a packed upper-triangular 32 x 32 block; (k, k) holds 1 / G_kk (the
@@ -626,6 +642,7 @@ __global__ void __launch_bounds__(HT, 1) tc_hals_kernel(const HParams p) {
   __shared__ unsigned cm_s[KR];                                  // fp32 bits of max |u|
   __shared__ double wmin_s[HT / 32];
   if (p.stage != nullptr && *p.stage != 1) return;
+  if (p.ill != nullptr && *p.ill != 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = p.r;
   const int nblk = (r + HB - 1) / HB;
@@ -735,6 +752,7 @@ __global__ void __launch_bounds__(HT, 1) tc_hals_kernel(const HParams p) {
       }
     }
     const double isu = 1.0 / su;
+    const double snap = 0x1p-14 * isu;            // max |u| su in [16, 32): 2^-18..2^-19 of it
     const int ovf_hi = __double2hiint(64.0 * isu);
     int bover = -1;                    // first block whose new u outgrew the digit scale
 #pragma unroll 1
@@ -777,7 +795,10 @@ __global__ void __launch_bounds__(HT, 1) tc_hals_kernel(const HParams p) {
       for (int k = 0; k < HB; ++k) {
         const double ig = gt[tri(k, k)];
         const double vn = fma(tt[k], ig, uu[k]);
-        const double nu = ig == 0.0 ? uu[k] : (vn > 0.0 ? vn : 0.0);   // G_kk <= 0: skipped
+        // projection; below `snap` (2^-18 of the row's maximum, far above the coupling's
+        // ~2^-26 error) an update counts as zero, so a column the exact update drives to
+        // zero stays exactly zero (R28); G_kk <= 0: column skipped
+        const double nu = ig == 0.0 ? uu[k] : (vn > snap ? vn : 0.0);
         const double d = nu - uu[k];
         uu[k] = nu;
 #pragma unroll
@@ -904,7 +925,7 @@ int tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double*
                   cudaStream_t st) {
   using namespace tpb;
   const int rp = KR;   // G padded to 128 columns: class k of the accumulators at column k * 128
-  gdigits_kernel<<<rp, KR, 0, st>>>(G, r, rp, gd_work, gscale_work, stage, 0);
+  gdigits_kernel<<<rp, KR, 0, st>>>(G, r, rp, gd_work, gscale_work, stage, 0, nullptr);
   Params p;
   p.F = F;
   p.ldf = ldf;
@@ -943,9 +964,11 @@ int tc_hals_parts() { return kSMs; }
 
 int tc_hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
                  int8_t* gd_work, double* gscale_work, const int* stage, double* minparts,
-                 int nparts, unsigned long long* colmax, int* fallbacks, cudaStream_t st) {
+                 int nparts, unsigned long long* colmax, int* fallbacks, int* ill,
+                 cudaStream_t st) {
   using namespace tpb;
-  gdigits_kernel<<<KR, KR, 0, st>>>(G, r, KR, gd_work, gscale_work, stage, 1);
+  if (ill != nullptr && cudaMemsetAsync(ill, 0, sizeof(int), st) != cudaSuccess) return 1;
+  gdigits_kernel<<<KR, KR, 0, st>>>(G, r, KR, gd_work, gscale_work, stage, 1, ill);
   HParams p;
   p.F = F;
   p.ldf = ldf;
@@ -960,6 +983,7 @@ int tc_hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, co
   p.nparts = nparts;
   p.colmax = colmax;
   p.fallbacks = fallbacks;
+  p.ill = ill;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(tc_hals_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

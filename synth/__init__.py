@@ -9,7 +9,8 @@ import os
 
 import numpy as np
 
-from .configs import ALL, C1, C2, C3, C4, C5, IMAGE, PLANTED, RATINGS, SPECTRO, Config  # noqa: F401
+from .configs import (ALL, C1, C2, C3, C4, C5, C6, IMAGE, PLANTED, RATINGS, SPARSE,  # noqa: F401
+                      SPECTRO, Config)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _cpu = None
@@ -35,6 +36,9 @@ def _load_cpu():
         lib.synth_factor.argtypes = [ctypes.c_int, u64, ctypes.c_int, i64, i64, ctypes.c_int,
                                      ctypes.c_void_p]
         lib.synth_philox.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        lib.synth_csr_rows.argtypes = [u64, i64, i64, ctypes.c_int, dbl, dbl, i64, i64,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, i64]
+        lib.synth_csr_rows.restype = i64
         lib.synth_normal.argtypes = [u64, ctypes.c_uint32, u64]
         lib.synth_normal.restype = dbl
         lib.synth_log.argtypes = [dbl]
@@ -59,6 +63,10 @@ def _load_gpu():
         lib.synth_gpu_smax.argtypes = [ctypes.c_int, u64, i64, i64, ctypes.c_int,
                                        ctypes.POINTER(dbl), ctypes.c_void_p]
         lib.synth_gpu_smax.restype = ctypes.c_int
+        lib.synth_gpu_csr_rows.argtypes = [u64, i64, i64, ctypes.c_int, dbl, dbl, i64, i64,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p]
+        lib.synth_gpu_csr_rows.restype = ctypes.c_int
         _gpu = lib
     return _gpu
 
@@ -77,6 +85,8 @@ def normal(seed, stream, idx):
 
 
 def _smax_cpu(cfg: Config) -> float:
+    if cfg.recipe == SPARSE:
+        return cfg.density          # SPARSE reads its density from the smax argument
     if cfg.recipe != IMAGE or not cfg.normalised:
         return 0.0
     return _load_cpu().synth_smax(cfg.recipe, cfg.seed, cfg.m, cfg.n, cfg.k)
@@ -124,7 +134,7 @@ def x_rows_device(cfg: Config, row_begin, row_count, out, stream_ptr=0):
     lib = _load_gpu()
     ptr = out.data_ptr() if hasattr(out, "data_ptr") else int(out)
     ld = out.stride(0) if hasattr(out, "stride") else cfg.n
-    smax = 0.0
+    smax = cfg.density if cfg.recipe == SPARSE else 0.0
     if cfg.recipe == IMAGE and cfg.normalised:
         s = ctypes.c_double(0.0)
         rc = lib.synth_gpu_smax(cfg.recipe, cfg.seed, cfg.m, cfg.n, cfg.k, ctypes.byref(s),
@@ -136,3 +146,45 @@ def x_rows_device(cfg: Config, row_begin, row_count, out, stream_ptr=0):
                               row_begin, row_count, ptr, ld, stream_ptr)
     if rc:
         raise RuntimeError(f"synth_gpu_x_rows failed: cudaError {rc}")
+
+
+def csr_rows(cfg: Config, row_begin=0, row_count=None):
+    """SPARSE recipe rows as CSR numpy arrays (rowptr int64, colidx int32, vals float32),
+    bit-identical to the stored entries of x_rows(cfg, ...)."""
+    if row_count is None:
+        row_count = cfg.m - row_begin
+    lib = _load_cpu()
+    nnz = lib.synth_csr_rows(cfg.seed, cfg.m, cfg.n, cfg.k, cfg.noise, cfg.density, row_begin,
+                             row_count, None, None, None, 0)
+    if nnz < 0:
+        raise ValueError("synth_csr_rows: bad row range")
+    rowptr = np.empty(row_count + 1, dtype=np.int64)
+    colidx = np.empty(max(nnz, 1), dtype=np.int32)
+    vals = np.empty(max(nnz, 1), dtype=np.float32)
+    lib.synth_csr_rows(cfg.seed, cfg.m, cfg.n, cfg.k, cfg.noise, cfg.density, row_begin,
+                       row_count, rowptr.ctypes.data, colidx.ctypes.data, vals.ctypes.data, nnz)
+    return rowptr, colidx[:nnz], vals[:nnz]
+
+
+def csr_rows_device(cfg: Config, row_begin, row_count, stream_ptr=0):
+    """SPARSE recipe rows generated on the GPU: (rowptr int64, colidx int32, vals float32) CUDA
+    tensors, bit-identical to csr_rows()."""
+    import torch
+    lib = _load_gpu()
+    counts = torch.empty(max(row_count, 1), dtype=torch.int64, device="cuda")
+    rc = lib.synth_gpu_csr_rows(cfg.seed, cfg.m, cfg.n, cfg.k, cfg.noise, cfg.density, row_begin,
+                                row_count, counts.data_ptr(), None, None, None, stream_ptr)
+    if rc:
+        raise RuntimeError(f"synth_gpu_csr_rows (count) failed: cudaError {rc}")
+    rowptr = torch.zeros(row_count + 1, dtype=torch.int64, device="cuda")
+    if row_count:
+        rowptr[1:] = torch.cumsum(counts[:row_count], 0)
+    nnz = int(rowptr[-1].item())
+    colidx = torch.empty(max(nnz, 1), dtype=torch.int32, device="cuda")
+    vals = torch.empty(max(nnz, 1), dtype=torch.float32, device="cuda")
+    rc = lib.synth_gpu_csr_rows(cfg.seed, cfg.m, cfg.n, cfg.k, cfg.noise, cfg.density, row_begin,
+                                row_count, None, rowptr.data_ptr(), colidx.data_ptr(),
+                                vals.data_ptr(), stream_ptr)
+    if rc:
+        raise RuntimeError(f"synth_gpu_csr_rows (fill) failed: cudaError {rc}")
+    return rowptr, colidx[:nnz], vals[:nnz]

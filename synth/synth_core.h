@@ -21,6 +21,9 @@
  *            B = Exp(1)*[u>=0.7]                                     (C3, R22)
  *   RATINGS  X_ij = c in {1..5} w.p. 0.045, cat(.06,.11,.26,.35,.22);
  *            else 0                                                  (C4, R23)
+ *   SPARSE   X_ij = (A B^T)_ij + noise*|z| w.p. density (A, B as PLANTED), else 0:
+ *            the stand-in for the sparse Reuters matrix (
+ *            density is passed in the smax argument)                 (C6, R27)
  * Factor entries are rounded to fp32 before the inner product, so every
  * product A_ic*B_jc is exact in fp64; the k-sum runs in ascending c order.
  */
@@ -36,7 +39,7 @@
 #define SYN_FN static inline
 #endif
 
-enum { SYN_PLANTED = 1, SYN_IMAGE = 2, SYN_SPECTRO = 3, SYN_RATINGS = 4 };
+enum { SYN_PLANTED = 1, SYN_IMAGE = 2, SYN_SPECTRO = 3, SYN_RATINGS = 4, SYN_SPARSE = 5 };
 enum { SYN_STREAM_ROWF = 1, SYN_STREAM_COLF = 2, SYN_STREAM_NOISE = 3, SYN_STREAM_X = 4 };
 
 typedef struct { uint32_t v[4]; } syn_u32x4;
@@ -199,6 +202,12 @@ SYN_FN double syn_dot(const float* a, const float* b, int k) {
   return s;
 }
 
+/* SPARSE support: entry (i, j) is stored w.p. density (X stream, word 0). */
+SYN_FN int syn_sparse_keep(uint64_t seed, uint64_t i, uint64_t j, uint64_t n, double density) {
+  syn_u32x4 w = syn_draw(seed, SYN_STREAM_X, i * n + j);
+  return syn_u01(w.v[0]) < density;
+}
+
 /* Final X_ij from the planted inner product S (ignored for RATINGS).
  * smax: global max of S (IMAGE recipe, normalised reading R21; <=0 selects
  * the literal unnormalised reading). */
@@ -216,6 +225,12 @@ SYN_FN float syn_x_from_s(int recipe, uint64_t seed, uint64_t i, uint64_t j,
       if (c < 0.43) return 3.0f;
       if (c < 0.78) return 4.0f;
       return 5.0f;
+    }
+    case SYN_SPARSE: {
+      if (!syn_sparse_keep(seed, i, j, n, smax)) return 0.0f;
+      double z = syn_normal(seed, SYN_STREAM_NOISE, e);
+      double az = z < 0.0 ? -z : z;
+      return (float)(s + noise * az);
     }
     case SYN_IMAGE: {
       double z = syn_normal(seed, SYN_STREAM_NOISE, e);

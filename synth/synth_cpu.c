@@ -97,3 +97,39 @@ int synth_x_rows(int recipe, uint64_t seed, int64_t m, int64_t n, int k, double 
   free(B);
   return 0;
 }
+
+/* SPARSE recipe as CSR rows [row_begin, row_begin + row_count) (columns ascending).
+ * rowptr == NULL: returns the entry count of the range; else fills rowptr (row_count + 1,
+ * rowptr[0] = 0), colidx and vals (capacity cap) and returns the count (-1 on overflow). */
+int64_t synth_csr_rows(uint64_t seed, int64_t m, int64_t n, int k, double noise, double density,
+                       int64_t row_begin, int64_t row_count, int64_t* rowptr, int32_t* colidx,
+                       float* vals, int64_t cap) {
+  if (row_begin < 0 || row_count < 0 || row_begin + row_count > m) return -1;
+  int64_t nnz = 0;
+  float* A = NULL;
+  float* B = NULL;
+  if (rowptr) {
+    A = (float*)malloc(sizeof(float) * (size_t)(row_count > 0 ? row_count : 1) * k);
+    B = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1) * k);
+    synth_factor(SYN_SPARSE, seed, 0, row_begin, row_count, k, A);
+    synth_factor(SYN_SPARSE, seed, 1, 0, n, k, B);
+    rowptr[0] = 0;
+  }
+  for (int64_t r = 0; r < row_count; ++r) {
+    uint64_t i = (uint64_t)(row_begin + r);
+    for (int64_t j = 0; j < n; ++j) {
+      if (!syn_sparse_keep(seed, i, (uint64_t)j, (uint64_t)n, density)) continue;
+      if (rowptr) {
+        if (nnz >= cap) { free(A); free(B); return -1; }
+        double s = syn_dot(A + r * k, B + j * k, k);
+        colidx[nnz] = (int32_t)j;
+        vals[nnz] = syn_x_from_s(SYN_SPARSE, seed, i, (uint64_t)j, (uint64_t)n, s, noise, density);
+      }
+      ++nnz;
+    }
+    if (rowptr) rowptr[r + 1] = nnz;
+  }
+  free(A);
+  free(B);
+  return nnz;
+}

@@ -81,9 +81,67 @@ __global__ void __launch_bounds__(256) x_kernel(int recipe, uint64_t seed, int64
   if (MODE == 1) atomicMax(smax_bits, (unsigned long long)__double_as_longlong(local_max));
 }
 
+// SPARSE recipe, warp per row: entry counts (fill == false) or the CSR fill (columns
+// ascending; positions from a ballot prefix).  A: rows of this range, B: all columns.
+template <bool FILL>
+__global__ void __launch_bounds__(256) csr_kernel(uint64_t seed, int64_t n, int k, double noise,
+                                                  double density, int64_t row_begin,
+                                                  int64_t row_count, const float* __restrict__ A,
+                                                  const float* __restrict__ B, int64_t* counts,
+                                                  const int64_t* rowptr, int32_t* colidx,
+                                                  float* vals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (r >= row_count) return;
+  const uint64_t i = (uint64_t)(row_begin + r);
+  int64_t pos = FILL ? rowptr[r] : 0;
+  for (int64_t j0 = 0; j0 < n; j0 += 32) {
+    const int64_t j = j0 + lane;
+    const int keep = j < n && syn_sparse_keep(seed, i, (uint64_t)j, (uint64_t)n, density);
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (FILL && keep) {
+      const int64_t p = pos + __popc(mask & ((1u << lane) - 1u));
+      const double s = syn_dot(A + r * k, B + j * k, k);
+      colidx[p] = (int32_t)j;
+      vals[p] = syn_x_from_s(SYN_SPARSE, seed, i, (uint64_t)j, (uint64_t)n, s, noise, density);
+    }
+    pos += __popc(mask);
+  }
+  if (!FILL && lane == 0) counts[r] = pos;
+}
+
 }  // namespace
 
 extern "C" {
+
+// SPARSE recipe on the device: counts (row_count entries) when rowptr == NULL, else the CSR
+// fill of colidx / vals given rowptr (row_count + 1, exclusive prefix of the counts).
+int synth_gpu_csr_rows(uint64_t seed, int64_t m, int64_t n, int k, double noise, double density,
+                       int64_t row_begin, int64_t row_count, int64_t* counts,
+                       const int64_t* rowptr, int32_t* colidx, float* vals, void* stream_ptr) {
+  if (row_begin < 0 || row_count < 0 || row_begin + row_count > m) return 1;
+  if (row_count == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream_ptr;
+  const unsigned grid = (unsigned)((row_count * 32 + 255) / 256);
+  if (!rowptr) {
+    csr_kernel<false><<<grid, 256, 0, st>>>(seed, n, k, noise, density, row_begin, row_count,
+                                            nullptr, nullptr, counts, nullptr, nullptr, nullptr);
+    return cudaGetLastError();
+  }
+  float* A = nullptr;
+  float* B = nullptr;
+  cudaError_t err;
+  if ((err = cudaMallocAsync(&A, sizeof(float) * row_count * k, st))) return err;
+  if ((err = cudaMallocAsync(&B, sizeof(float) * n * k, st))) return err;
+  factor_kernel<<<1184, 256, 0, st>>>(SYN_SPARSE, seed, 0, row_begin, row_count, k, A);
+  factor_kernel<<<1184, 256, 0, st>>>(SYN_SPARSE, seed, 1, 0, n, k, B);
+  csr_kernel<true><<<grid, 256, 0, st>>>(seed, n, k, noise, density, row_begin, row_count, A, B,
+                                         nullptr, rowptr, colidx, vals);
+  err = cudaGetLastError();
+  cudaFreeAsync(A, st);
+  cudaFreeAsync(B, st);
+  return err;
+}
 
 // Returns a cudaError_t value (0 = success).
 int synth_gpu_x_rows(int recipe, uint64_t seed, int64_t m, int64_t n, int k, double noise,

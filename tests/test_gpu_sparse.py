@@ -1,0 +1,170 @@
+"""Sparse X (the paper's sparse Reuters experiment): the
+CSR path (enmf_set_data_csr, fp64-accumulating SpMM X passes) against the fp64 oracle run on
+the same X densified.  The oracle needs no sparse code: P = X V and Q = X^T U of a matrix
+with stored zeros are the same numbers.  Inputs: the SPARSE recipe (planted product sampled
+at a density, synth_core.h, reading R27) at sizes the oracle finishes in seconds, with ragged
+row lengths and empty rows."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.gpu_common import oracle_floor, rel_fro, rotated_point, to_dev, to_np
+
+pytestmark = pytest.mark.gpu
+
+FP64, AUTO = 1, 0
+CASES = [
+    synth.C6.scaled(300, 220, 12, 12, density=0.05, name="sparse-300x220-r12"),
+    synth.C6.scaled(700, 650, 100, 100, density=0.02, name="sparse-700x650-r100"),
+    synth.C6.scaled(257, 131, 33, 33, density=0.004, name="sparse-ragged-empty-rows"),
+]
+IDS = [c.name for c in CASES]
+PRECS = [(FP64, "rows-fp64"), (AUTO, "rows-tc")]
+
+
+def bind(cfg, precision=AUTO):
+    import torch
+    import paper_2605_19325_b200 as E
+    rp, ci, v = synth.csr_rows(cfg)
+    h = E.Enmf(cfg.m, cfg.n, cfg.r, precision=precision)
+    dev = (torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(), torch.from_numpy(v).cuda())
+    h.set_data_csr(*dev)
+    return h, synth.x_full(cfg), dev
+
+
+def test_csr_device_generator_matches_host():
+    cfg = CASES[1]
+    rp, ci, v = synth.csr_rows(cfg, 100, 400)
+    drp, dci, dv = synth.csr_rows_device(cfg, 100, 400)
+    assert np.array_equal(drp.cpu().numpy(), rp)
+    assert np.array_equal(dci.cpu().numpy(), ci) and np.array_equal(dv.cpu().numpy(), v)
+
+
+@pytest.mark.parametrize("cfg", CASES, ids=IDS)
+def test_sparse_contractions_and_objective(cfg):
+    """P = X V, Q = X^T U (CSR and CSC SpMM, fp64 accumulation of the fp32 products) entry by
+    entry, and both objective forms, against the oracle on the densified X.  Only the
+    summation order differs: bound 1e-12 of |X||F| per entry."""
+    h, X, _ = bind(cfg)
+    assert h.precision.startswith("csr")
+    g = np.random.default_rng(2)
+    U0 = g.random((cfg.m, cfg.r)).astype(np.float32).astype(np.float64)
+    V0 = g.random((cfg.n, cfg.r)).astype(np.float32).astype(np.float64)
+    P, Q = h.cross_terms(to_dev(U0), to_dev(V0))
+    P, Q = to_np(P), to_np(Q)
+    Xa = np.abs(X.astype(np.float64))
+    ep = np.abs(P - oracle.xv(X, V0)) / np.maximum(Xa @ np.abs(V0), 1e-300)
+    eq = np.abs(Q - oracle.xtu(X, U0)) / np.maximum(Xa.T @ np.abs(U0), 1e-300)
+    print(f"{cfg.name}: nnz {int((X != 0).sum())}, P max {ep.max():.1e}, Q max {eq.max():.1e}")
+    assert ep.max() < 1e-12 and eq.max() < 1e-12
+    f_d = oracle.frob2_direct(X, U0, V0)
+    for exact in (False, True):
+        f = h.objective(to_dev(U0), to_dev(V0), exact=exact)
+        assert abs(f - f_d) <= 1e-10 * f_d, (exact, f, f_d)
+
+
+@pytest.mark.parametrize("prec,pid", PRECS, ids=[p[1] for p in PRECS])
+@pytest.mark.parametrize("cfg", CASES, ids=IDS)
+def test_sparse_svd_and_hals_sweep(cfg, prec, pid):
+    """The randomised SVD (Alg. 3) through the SpMM passes against the same
+    algorithm on the densified X through the dense fp64 passes (same seeded Omega; the
+    range finder itself is pinned to the oracle's converged SVD by the dense tests -- a
+    sampled planted product has no spectral gap, so q = 2 is not converged here): sigma and
+    the balanced factors within 1e-8.  Then one HALS sweep from a shared feasible point
+    against the oracle (BASELINE's 1e-5 per factor)."""
+    import paper_2605_19325_b200 as E
+    h, X, _ = bind(cfg, prec)
+    U = to_dev(np.zeros((cfg.m, cfg.r)))
+    V = to_dev(np.zeros((cfg.n, cfg.r)))
+    sig = h.svd(U, V)
+    hd = E.Enmf(cfg.m, cfg.n, cfg.r, precision=FP64)
+    hd.set_data(to_dev(X))
+    Ud = to_dev(np.zeros((cfg.m, cfg.r)))
+    Vd = to_dev(np.zeros((cfg.n, cfg.r)))
+    sig_d = hd.svd(Ud, Vd)
+    print(f"{cfg.name}: sigma rel {np.max(np.abs(sig - sig_d) / sig_d[0]):.1e}, "
+          f"U {rel_fro(to_np(U), to_np(Ud)):.1e}")
+    assert np.max(np.abs(sig - sig_d)) <= 1e-8 * sig_d[0]
+    assert rel_fro(to_np(U), to_np(Ud)) < 1e-6 and rel_fro(to_np(V), to_np(Vd)) < 1e-6
+    U0, V0, _, _ = rotated_point(X, cfg.r)
+    U0, V0 = np.abs(U0), np.abs(V0)
+    U, V = to_dev(U0), to_dev(V0)
+    h.set_stage(1)
+    h.iterate(U, V, 1)
+    Uo, Vo, _, _ = oracle.sweep(X, U0, V0, oracle.SweepState(stage=1),
+                                oracle.options(cfg.r, round_f32=1))
+    eu, ev = rel_fro(to_np(U), Uo), rel_fro(to_np(V), Vo)
+    print(f"{cfg.name} {h.precision}: HALS sweep U {eu:.2e} V {ev:.2e}")
+    assert eu < 1e-5 and ev < 1e-5
+
+
+@pytest.mark.parametrize("prec,pid", PRECS, ids=[p[1] for p in PRECS])
+@pytest.mark.parametrize("cfg", [CASES[0], CASES[2]], ids=[IDS[0], IDS[2]])
+def test_sparse_ascent_then_hals_trajectory(cfg, prec, pid):
+    """20 sweeps from the oracle's rotated point (ascent stage, then HALS): every sweep's f
+    within max(1e-4, 10 x the oracle's 1-ulp spread), as on the dense path."""
+    h, X, _ = bind(cfg, prec)
+    U0, V0, lu, lv = rotated_point(X, cfg.r)
+    U, V = to_dev(U0), to_dev(V0)
+    h.set_stage(0, lu, lv)
+    f_gpu, info = h.iterate(U, V, 20)
+
+    def run(Ua, Va):
+        st = oracle.SweepState(0, lu, lv, 0)
+        f = []
+        for _ in range(20):
+            Ua, Va, _, _ = oracle.sweep(X, Ua, Va, st, oracle.options(cfg.r, round_f32=1))
+            f.append(oracle.frob2_direct(X, Ua, Va))
+        return (np.array(f),)
+
+    (f_or,), floor = oracle_floor(run, U0, V0)
+    err = np.abs(f_gpu - f_or) / f_or
+    print(f"{cfg.name} {h.precision}: max f err {err.max():.2e}, floor {floor[0]:.2e}, "
+          f"stages {info['ascent_sweeps']}+{info['hals_sweeps']}")
+    assert np.all(err < max(1e-4, 10 * floor[0])), err
+
+
+def test_sparse_input_checks():
+    import torch
+    import paper_2605_19325_b200 as E
+    cfg = CASES[0]
+    rp, ci, v = synth.csr_rows(cfg)
+    h = E.Enmf(cfg.m, cfg.n, cfg.r)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()   # noqa: E731
+    bad = ci.copy()
+    r0 = int(np.argmax(np.diff(rp) >= 2))            # a row with two entries: swap them
+    bad[rp[r0]], bad[rp[r0] + 1] = bad[rp[r0] + 1], bad[rp[r0]]
+    with pytest.raises(RuntimeError, match="-1"):
+        h.set_data_csr(dev(rp), dev(bad), dev(v))
+    neg = v.copy()
+    neg[3] = -1.0
+    with pytest.raises(RuntimeError, match="-3"):
+        h.set_data_csr(dev(rp), dev(ci), dev(neg))
+    h.set_data_csr(dev(rp), dev(ci), dev(v))        # and a valid bind afterwards works
+    assert h.precision.startswith("csr")
+
+
+def test_tc_hals_ill_conditioned_gram_hands_over_to_fp64():
+    """The ragged sparse case is rank deficient: the rotated factors keep columns of size
+    ~1e-36 that are still coupled to the others, so G_jj is ~2^-200 of its column sum and the
+    tensor-core HALS (u on a per-row digit grid) would lose the update of u_j entirely.  The
+    G-digit pass flags such a G and the SIMT fp64 kernel takes the sweep: one HALS sweep on the
+    DENSE tensor-core path within BASELINE's 1e-5 of the oracle, no fallback rows."""
+    import paper_2605_19325_b200 as E
+    cfg = CASES[2]
+    X = synth.x_full(cfg)
+    h = E.Enmf(cfg.m, cfg.n, cfg.r, precision=2)
+    h.set_data(to_dev(X))
+    assert h.precision.startswith("tc")
+    U0, V0, _, _ = rotated_point(X, cfg.r)
+    U0, V0 = np.abs(U0), np.abs(V0)
+    U, V = to_dev(U0), to_dev(V0)
+    h.set_stage(1)
+    _, info = h.iterate(U, V, 1)
+    Uo, Vo, _, _ = oracle.sweep(X, U0, V0, oracle.SweepState(stage=1),
+                                oracle.options(cfg.r, round_f32=1))
+    eu, ev = rel_fro(to_np(U), Uo), rel_fro(to_np(V), Vo)
+    print(f"ill-conditioned G, {h.precision}: U {eu:.2e} V {ev:.2e}, fallback rows "
+          f"{info['hals_fallback_rows']}")
+    assert eu < 1e-5 and ev < 1e-5
