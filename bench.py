@@ -190,8 +190,14 @@ def run_enmf(args):
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     stream = torch.cuda.current_stream()
-    X = torch.empty(count, n, device="cuda", dtype=torch.float32)
-    synth.x_rows_device(cfg, begin, count, X, stream.cuda_stream)
+    sparse = cfg.recipe == synth.SPARSE        # C6: CSR X
+    if sparse:
+        X = None
+        csr = synth.csr_rows_device(cfg, begin, count, stream.cuda_stream)
+        nnz_local = int(csr[2].numel())
+    else:
+        X = torch.empty(count, n, device="cuda", dtype=torch.float32)
+        synth.x_rows_device(cfg, begin, count, X, stream.cuda_stream)
     U = torch.empty(count, r, device="cuda")
     V = torch.empty(n, r, device="cuda")
     prec = {"auto": E.PREC_AUTO, "fp64": E.PREC_FP64, "tc": E.PREC_TC}[args.precision]
@@ -211,7 +217,12 @@ def run_enmf(args):
 
     barrier()
     t0 = time.perf_counter()
-    info = h.init(X, U, V)
+    if sparse:
+        h.set_data_csr(*csr)
+        h.svd(U, V)
+        info = h.rotate(U, V)
+    else:
+        info = h.init(X, U, V)
     torch.cuda.synchronize()
     init_s = maxr(time.perf_counter() - t0)
     # warm-up sweeps run on the rotated point and are then rolled back, so the timed
@@ -243,24 +254,47 @@ def run_enmf(args):
     h.set_profiling(False)
     launches = h.launch_count - l0
     sweeps_per_s = args.steps / (ms / 1000.0)
-    x_bytes_pass = float(m) * n * 4
+    if sparse:
+        t_nnz = torch.tensor([float(nnz_local)], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t_nnz)
+        nnz_all = float(t_nnz.item())
+        x_bytes_pass = nnz_all * 8 + (m + 1) * 8.0      # CSR: value + column index, row ptr
+    else:
+        x_bytes_pass = float(m) * n * 4
     gbs = 2.0 * x_bytes_pass * sweeps_per_s / 1e9
 
     peaks, peak_kind = measured_peaks()
     # dominant kernel: the X passes (X V and X^T U) -- algorithmic bytes = this rank's X
     pass_ms = (prof["xv"][0] + prof["xtu"][0]) / max(1, prof["xv"][1] + prof["xtu"][1])
-    achieved = float(count) * n * 4 / (pass_ms / 1000.0) / 1e9
+    achieved = float(count) * n * 4 / (pass_ms / 1000.0) / 1e9 if not sparse else None
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             tj = json.load(fh)
         traffic = tj.get(h.precision, {}).get("bytes_per_pass")
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                "kernel": f"X pass ({h.precision})", "peak_kind": peak_kind,
-                "pass_ms": pass_ms,
-                "share_of_step": (prof["xv"][0] + prof["xtu"][0]) / max(ms, 1e-9)}
+    if sparse:
+        # SpMM X pass: 2 r flops per stored entry in fp64 FMA (one warp per row), CSR bytes
+        # streamed once; peak = 148 SMs x 64 DFMA/clk x 2 flop at the max SM clock
+        flops = 2.0 * nnz_local * r
+        achieved = flops / (pass_ms / 1000.0) / 1e12
+        peak = 148 * 64 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "kernel": "SpMM X pass (fp64 FMA)",
+                    "peak_kind": "derived: 148 SMs x 64 fp64 FMA/clk x 2 x sm_max_mhz",
+                    "pass_ms": pass_ms, "csr_gbs": x_bytes_pass / (pass_ms / 1000.0) / 1e9,
+                    # per stored entry the warp gathers one factor row (r x 4 B, mostly L2 hits):
+                    # the rate that actually bounds the pass (ncu: L2 hit 69-94 %)
+                    "gather_gbs": nnz_local * r * 4.0 / (pass_ms / 1000.0) / 1e9,
+                    "share_of_step": (prof["xv"][0] + prof["xtu"][0]) / max(ms, 1e-9)}
+    else:
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                    "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                    "kernel": f"X pass ({h.precision})", "peak_kind": peak_kind,
+                    "pass_ms": pass_ms,
+                    "share_of_step": (prof["xv"][0] + prof["xtu"][0]) / max(ms, 1e-9)}
 
     # ---- per-stage rates: a few HALS sweeps from the final (feasible) state
     # and a few ascent sweeps from the rotated point; the timed region above is the blend
@@ -356,13 +390,17 @@ def run_enmf(args):
             "metric": METRIC, "value": sweeps_per_s, "unit": "sweeps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64" if h.precision == "fp64-simt"
-                     else "i8 (4x7-bit digits of fp32 X, V, U) / exact i32 TMEM / f64",
+            "dtype": "f64" if h.precision in ("fp64-simt", "csr-f64-spmm")
+                     else ("f64 SpMM X passes / i8-digit tensor-core row updates"
+                           if sparse else
+                           "i8 (4x7-bit digits of fp32 X, V, U) / exact i32 TMEM / f64"),
             "data": "synthetic",
             "config": {"workload": cfg.name, "m": m, "n": n, "r": r,
                        "global_batch": m, "seq_len": n,
                        "parallelism": f"row-shard x{world} (NCCL reduce-scatter of X^T U, all-gather of V slices, allreduce of Grams)",
-                       "l2": "inputs larger than L2 (X is 40 GB), no flush",
+                       "l2": (f"CSR of X {x_bytes_pass / 1e9:.2f} GB > L2, no flush"
+                              if sparse else "inputs larger than L2 (X is 40 GB), no flush"),
+                       "nnz": int(nnz_all) if sparse else m * n,
                        "precision_path": h.precision,
                        "timed_sweeps": {"ascent": info_t["ascent_sweeps"],
                                         "hals": info_t["hals_sweeps"]},

@@ -8,7 +8,8 @@
 //     per enmf_set_data_csr (stable radix sort of the column indices, so every column lists
 //     its entries in ascending row order and Q is summed in a fixed order: deterministic);
 //   * one warp per output row, lane l owns columns l, l + 32, l + 64, l + 96 of a <= 128-wide
-//     column block; per stored entry the warp reads (index, value) once (broadcast) and the
+//     column block; the warp loads 32 (index, value) pairs at once (coalesced, then shuffled),
+//     keeps 8 factor rows in flight per step, and for each stored entry reads the
 //     factor row coalesced (128 x 4 B from L2: the factor is 25-100 MB and stays resident in
 //     the 126 MB L2 far better than X streams), and accumulates x * f in fp64 (the objective's
 //     conditioning needs P, Q to ~1e-12, as the dense fp64 path provides).
@@ -36,34 +37,41 @@ spmm_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
   if (row >= rows) return;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const int64_t e0 = ptr[row], e1 = ptr[row + 1];
-  int64_t e = e0;
-  // two entries per step: both factor rows in flight before the FMAs
-  for (; e + 1 < e1; e += 2) {
-    const int64_t j0 = idx[e], j1 = idx[e + 1];
-    const double x0 = val[e], x1 = val[e + 1];
-    const T* b0 = B + j0 * ldb;
-    const T* b1 = B + j1 * ldb;
-    T f0[4], f1[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int col = lane + 32 * c;
-      f0[c] = col < ncols ? b0[col] : T(0);
-      f1[c] = col < ncols ? b1[col] : T(0);
+  // 32 (index, value) pairs per coalesced load, then 8 factor rows in flight per step; the
+  // accumulation order is the entry order (deterministic); padding entries add x = 0
+  for (int64_t base = e0; base < e1; base += 32) {
+    const int cnt = (int)(e1 - base < 32 ? e1 - base : 32);
+    int myj = 0;
+    double myx = 0.0;
+    if (lane < cnt) {
+      myj = idx[base + lane];
+      myx = (double)val[base + lane];
     }
+    const int j_pad = __shfl_sync(0xffffffffu, myj, 0);
+    for (int q = 0; q < cnt; q += 8) {
+      int jj[8];
+      double xx[8];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      acc[c] = fma(x0, (double)f0[c], acc[c]);
-      acc[c] = fma(x1, (double)f1[c], acc[c]);
-    }
-  }
-  if (e < e1) {
-    const int64_t j0 = idx[e];
-    const double x0 = val[e];
-    const T* b0 = B + j0 * ldb;
+      for (int u = 0; u < 8; ++u) {
+        const int jv = __shfl_sync(0xffffffffu, myj, (q + u) & 31);
+        const double xv = __shfl_sync(0xffffffffu, myx, (q + u) & 31);
+        jj[u] = q + u < cnt ? jv : j_pad;
+        xx[u] = q + u < cnt ? xv : 0.0;
+      }
+      T f[8][4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int col = lane + 32 * c;
-      if (col < ncols) acc[c] = fma(x0, (double)b0[col], acc[c]);
+      for (int u = 0; u < 8; ++u) {
+        const T* bu = B + (int64_t)jj[u] * ldb;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int col = lane + 32 * c;
+          f[u][c] = col < ncols ? bu[col] : T(0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c] = fma(xx[u], (double)f[u][c], acc[c]);
     }
   }
   double* o = out + row * ldo;
