@@ -15,6 +15,37 @@ def ascent_point(cfg):
     return U0, V0, lam(U0), lam(V0)
 
 
+def load_x(cfg, begin, count):
+    """This rank's rows of X on the device: a dense tensor, or CSR tensors (SPARSE recipe)."""
+    import torch
+
+    import synth
+    if cfg.recipe == synth.SPARSE:
+        rp, ci, v = synth.csr_rows(cfg, begin, count)
+        return tuple(torch.from_numpy(a).cuda() for a in (rp, ci, v))
+    X = torch.empty(count, cfg.n, device="cuda")
+    synth.x_rows_device(cfg, begin, count, X, torch.cuda.current_stream().cuda_stream)
+    return X
+
+
+def bind(h, X):
+    if isinstance(X, tuple):
+        h.set_data_csr(*X)
+    else:
+        h.set_data(X)
+
+
+def init(h, X, U, V):
+    """Alg. 3 lines 331-333 (enmf_init, or set_data_csr + svd + rotate for a sparse X)."""
+    if not isinstance(X, tuple):
+        return h.init(X, U, V)
+    bind(h, X)
+    sig = h.svd(U, V)
+    info = h.rotate(U, V)
+    info["sigma"] = sig
+    return info
+
+
 def run(rank, world, port, cfg_args, prec, mode, out_q):
     sys.path.insert(0, ROOT)
     import numpy as np
@@ -30,9 +61,7 @@ def run(rank, world, port, cfg_args, prec, mode, out_q):
         cfg = synth.ALL[cfg_args[0]].scaled(*cfg_args[1:]) if len(cfg_args) > 1 else \
             synth.ALL[cfg_args[0]]
         begin, count = E.row_partition(cfg.m, world, rank)
-        st = torch.cuda.current_stream()
-        X = torch.empty(count, cfg.n, device="cuda")
-        synth.x_rows_device(cfg, begin, count, X, st.cuda_stream)
+        X = load_x(cfg, begin, count)
         h = E.Enmf(cfg.m, cfg.n, cfg.r, row_begin=begin, row_count=count, world_size=world,
                    rank=rank, precision=prec)
         rop = {"sum": dist.ReduceOp.SUM, "min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX}
@@ -46,12 +75,12 @@ def run(rank, world, port, cfg_args, prec, mode, out_q):
         if mode == "init":
             U = torch.empty(count, cfg.r, device="cuda")
             V = torch.empty(cfg.n, cfg.r, device="cuda")
-            info = h.init(X, U, V)
+            info = init(h, X, U, V)
             f, it = h.iterate(U, V, 12)
             res.update(sigma=np.array(info["sigma"]), f=f, it=it)
         elif mode == "ascent":                  # lift + PBCD sweeps from a shared point
             U0, V0, lu, lv = ascent_point(cfg)
-            h.set_data(X)
+            bind(h, X)
             U = torch.from_numpy(U0[begin:begin + count]).cuda()
             V = torch.from_numpy(V0).cuda()
             h.set_stage(0, lu, lv)
@@ -61,7 +90,7 @@ def run(rank, world, port, cfg_args, prec, mode, out_q):
             g = np.random.default_rng(5)
             U0 = g.random((cfg.m, cfg.r)).astype(np.float32)
             V0 = g.random((cfg.n, cfg.r)).astype(np.float32)
-            h.set_data(X)
+            bind(h, X)
             U = torch.from_numpy(U0[begin:begin + count]).cuda()
             V = torch.from_numpy(V0).cuda()
             h.set_stage(1)

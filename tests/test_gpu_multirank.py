@@ -50,17 +50,18 @@ def _single(cfg_args, prec, mode):
     from tests.gpu_common import to_dev
     cfg = synth.ALL[cfg_args[0]].scaled(*cfg_args[1:]) if len(cfg_args) > 1 else \
         synth.ALL[cfg_args[0]]
-    X = to_dev(synth.x_full(cfg))
+    X = multirank_worker.load_x(cfg, 0, cfg.m) if cfg.recipe == synth.SPARSE else \
+        to_dev(synth.x_full(cfg))
     h = E.Enmf(cfg.m, cfg.n, cfg.r, precision=prec)
     if mode == "init":
         U = torch.empty(cfg.m, cfg.r, device="cuda")
         V = torch.empty(cfg.n, cfg.r, device="cuda")
-        info = h.init(X, U, V)
+        info = multirank_worker.init(h, X, U, V)
         f, _ = h.iterate(U, V, 12)
         return np.array(info["sigma"]), f, U.cpu().numpy(), V.cpu().numpy()
     if mode == "ascent":
         U0, V0, lu, lv = multirank_worker.ascent_point(cfg)
-        h.set_data(X)
+        multirank_worker.bind(h, X)
         U, V = torch.from_numpy(U0).cuda(), torch.from_numpy(V0).cuda()
         h.set_stage(0, lu, lv)
         f, _ = h.iterate(U, V, 3)
@@ -68,7 +69,7 @@ def _single(cfg_args, prec, mode):
     g = np.random.default_rng(5)
     U0 = g.random((cfg.m, cfg.r)).astype(np.float32)
     V0 = g.random((cfg.n, cfg.r)).astype(np.float32)
-    h.set_data(X)
+    multirank_worker.bind(h, X)
     U, V = torch.from_numpy(U0).cuda(), torch.from_numpy(V0).cuda()
     h.set_stage(1)
     f, _ = h.iterate(U, V, 5)
@@ -77,10 +78,11 @@ def _single(cfg_args, prec, mode):
     return None, f, U.cpu().numpy(), V.cpu().numpy()
 
 
-CASES = [(("C1-planted",), FP64), (("C5-large-planted", 400, 300, 128, 128), TC)]
+CASES = [(("C1-planted",), FP64), (("C5-large-planted", 400, 300, 128, 128), TC),
+         (("C6-reuters-like", 400, 300, 24, 24, None, 0.05), TC)]
 
 
-@pytest.mark.parametrize("cfg_args,prec", CASES, ids=["C1-fp64", "C5shape-tc"])
+@pytest.mark.parametrize("cfg_args,prec", CASES, ids=["C1-fp64", "C5shape-tc", "C6shape-csr"])
 def test_two_ranks_hals_match_single_rank(cfg_args, prec):
     r0, r1 = _spawn(cfg_args, prec, "hals")
     assert np.array_equal(r0["V"], r1["V"]), "V must be bitwise identical on all ranks"
@@ -105,7 +107,7 @@ def test_two_ranks_hals_match_single_rank(cfg_args, prec):
         assert abs(a - b) <= rtol * max(abs(b), 1e-12 * _single.kkt["xnorm2"]), key
 
 
-@pytest.mark.parametrize("cfg_args,prec", CASES, ids=["C1-fp64", "C5shape-tc"])
+@pytest.mark.parametrize("cfg_args,prec", CASES, ids=["C1-fp64", "C5shape-tc", "C6shape-csr"])
 def test_two_ranks_init_and_ascent_consistent(cfg_args, prec):
     r0, r1 = _spawn(cfg_args, prec, "init")
     assert np.array_equal(r0["V"], r1["V"])
@@ -120,7 +122,7 @@ def test_two_ranks_init_and_ascent_consistent(cfg_args, prec):
     assert es < (1e-10 if prec == FP64 else 1e-6)   # tc: the rtol of the SVD-vs-oracle test
 
 
-@pytest.mark.parametrize("cfg_args,prec", CASES, ids=["C1-fp64", "C5shape-tc"])
+@pytest.mark.parametrize("cfg_args,prec", CASES, ids=["C1-fp64", "C5shape-tc", "C6shape-csr"])
 def test_two_ranks_ascent_sharded_v(cfg_args, prec):
     """Lift + PBCD sweeps with the V block sharded across the ranks (Alg. 2's stopping rule
     summed over both slices): V and f bitwise identical on the ranks; on the fp64 path the
