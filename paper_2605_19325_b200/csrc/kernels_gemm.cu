@@ -77,9 +77,29 @@ __global__ void reduce_parts_kernel(const double* __restrict__ parts, int nparts
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len;
        e += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += parts[(int64_t)p * len + e];
+#pragma unroll 8
+    for (int p = 0; p < nparts; ++p) s += parts[(int64_t)p * len + e];   // loads batched, order kept
     out[e] = s;
   }
+}
+
+// short outputs (len <= 64: scalars, the PBCD stopping vector): one block per element, the
+// parts strided over 256 threads and a fixed-order tree -- deterministic, and no single
+// thread walking hundreds of dependent loads
+__global__ void __launch_bounds__(256) reduce_parts_short_kernel(const double* __restrict__ parts,
+                                                                 int nparts, int64_t len,
+                                                                 double* __restrict__ out) {
+  __shared__ double red[256];
+  const int64_t e = blockIdx.x;
+  double s = 0.0;
+  for (int p = threadIdx.x; p < nparts; p += 256) s += parts[(int64_t)p * len + e];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[e] = red[0];
 }
 
 __global__ void f64_to_f32_kernel(const double* __restrict__ A, int64_t rows, int64_t cols,
@@ -177,7 +197,11 @@ template void gemm<double, float>(bool, const double*, int64_t, const float*, in
                                   int64_t, int64_t, GemmOut, double*, size_t, cudaStream_t);
 
 void reduce_parts(const double* parts, int nparts, int64_t len, double* out, cudaStream_t st) {
-  reduce_parts_kernel<<<grid_for(len), 256, 0, st>>>(parts, nparts, len, out);
+  if (len <= 0) return;
+  if (len <= 64 && nparts > 64)
+    reduce_parts_short_kernel<<<(unsigned)len, 256, 0, st>>>(parts, nparts, len, out);
+  else
+    reduce_parts_kernel<<<grid_for(len), 256, 0, st>>>(parts, nparts, len, out);
   count_launch();
 }
 

@@ -136,22 +136,20 @@ __global__ void project_f32_kernel(float* __restrict__ A, int64_t ld, int64_t ro
 }
 
 __global__ void reduce_min_kernel(const double* parts, int n, double* out) {
-  if (threadIdx.x != 0) return;
+  __shared__ double red[256];
   double mn = DBL_MAX;
-  for (int p = 0; p < n; ++p) mn = fmin(mn, parts[p]);
-  *out = mn;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) mn = fmin(mn, parts[p]);   // exact in any order
+  mn = block_reduce<1>(mn, red);
+  if (threadIdx.x == 0) *out = mn;
 }
 
 __global__ void dot_kernel(const double* __restrict__ A, const float* __restrict__ B,
                            int64_t ldb, int64_t rows, int64_t cols, double* parts) {
   __shared__ double red[256];
   double s = 0.0;
-  const int64_t total = rows * cols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / cols, j = e - i * cols;
-    s += A[e] * (double)B[i * ldb + j];
-  }
+  // rows by blocks, a row's columns by threads (no per-element 64-bit division)
+  for (int64_t i = blockIdx.x; i < rows; i += gridDim.x)
+    for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) s += A[i * cols + j] * (double)B[i * ldb + j];
   s = block_reduce<0>(s, red);
   if (threadIdx.x == 0) parts[blockIdx.x] = s;
 }
@@ -192,6 +190,7 @@ __global__ void objective_finish_kernel(const double* xnorm2, const double* cros
                                         double* fout) {
   __shared__ double red[256];
   double s = 0.0;
+#pragma unroll 8
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) s += gu[e] * gv[e];
   s = block_reduce<0>(s, red);
   if (threadIdx.x == 0) *fout = *xnorm2 - 2.0 * (*cross) + s;
@@ -807,7 +806,7 @@ void x_stats(const float* X, int64_t ldx, int64_t rows, int64_t n, double* parts
 void min_f32(const float* A, int64_t ld, int64_t rows, int64_t cols, double* parts, double* out,
              cudaStream_t st) {
   min_f32_kernel<<<kStatGrid, 256, 0, st>>>(A, ld, rows, cols, parts);
-  reduce_min_kernel<<<1, 32, 0, st>>>(parts, kStatGrid, out);
+  reduce_min_kernel<<<1, 256, 0, st>>>(parts, kStatGrid, out);
   count_launch(2);
 }
 
@@ -819,7 +818,7 @@ void project_f32(float* A, int64_t ld, int64_t rows, int64_t cols, cudaStream_t 
 }
 
 void reduce_min(const double* parts, int n, double* out, cudaStream_t st) {
-  reduce_min_kernel<<<1, 32, 0, st>>>(parts, n, out);
+  reduce_min_kernel<<<1, 256, 0, st>>>(parts, n, out);
   count_launch();
 }
 

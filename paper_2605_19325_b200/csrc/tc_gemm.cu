@@ -767,13 +767,26 @@ void tc_destroy(TcState* s) {
 
 // Split count for `tiles` output bands over `stages` K stages: enough units to fill the GPU,
 // every unit K <= MAX_UNIT_K, no empty unit.
-static int choose_split(int64_t tiles, int64_t stages, int sms) {
-  int ks = (int)((4 * sms + tiles - 1) / tiles);
-  const int kmin = (int)((stages * BK + MAX_UNIT_K - 1) / MAX_UNIT_K);
-  ks = std::max(std::max(ks, kmin), 1);
-  ks = std::min<int64_t>(ks, stages);
-  const int64_t per = (stages + ks - 1) / ks;
-  return (int)((stages + per - 1) / per);
+// K split of a pass: units = tiles x ks are dealt round-robin to `sms` persistent CTAs, so
+// the pass takes ceil(units / sms) units of ceil(stages / ks) stages each.  Pick the ks that
+// minimises that makespan (the old rule, ks = ceil(4 sms / tiles), left pass 2 at C5 with
+// 782 units = 5.28 waves, i.e. 12 % of the SMs idle in the last wave), with a small per-split
+// charge for the fp64 partials and their reduction (`split_cost` per extra split).
+static int choose_split(int64_t tiles, int64_t stages, int sms, double split_cost) {
+  const int kmin = std::max(1, (int)((stages * BK + MAX_UNIT_K - 1) / MAX_UNIT_K));
+  int best = kmin;
+  double best_t = 1e300;
+  for (int ks = kmin; ks <= std::max(kmin, 16) && ks <= stages; ++ks) {
+    const int64_t per = (stages + ks - 1) / ks;
+    const int64_t kse = (stages + per - 1) / per;
+    const double t = (double)((tiles * kse + sms - 1) / sms) * (double)per *
+                     (1.0 + split_cost * (double)(kse - 1));
+    if (t < best_t * (1.0 - 1e-9)) {
+      best_t = t;
+      best = (int)kse;
+    }
+  }
+  return best;
 }
 
 int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t n, int64_t r,
@@ -802,11 +815,10 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, dev);
-  // pass 1 splits K only when a band alone would overflow int32 or the grid is too small
-  s->ksplit1 = 1;
-  if (s->tiles_per_row * BK > MAX_UNIT_K || s->Mt < s->sms)
-    s->ksplit1 = choose_split(s->Mt, s->tiles_per_row, s->sms);
-  s->ksplit2 = choose_split(s->tiles_per_row / 2, s->Kt2, s->sms);
+  // pass 1 writes P directly unless splitting pays for its fp64 partials (rows x r x ks,
+  // written and reduced: charged 5 % per extra split); pass 2 is split-K anyway (0.2 %)
+  s->ksplit1 = choose_split(s->Mt, s->tiles_per_row, s->sms, 0.05);
+  s->ksplit2 = choose_split(s->tiles_per_row / 2, s->Kt2, s->sms, 0.002);
   {
     // cta_group::2 kernel: correct, but measured slower than the single-CTA kernel at C5
     // (DESIGN.md §5.1); ENMF_TC_PAIR=1 selects it
@@ -815,8 +827,8 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
     const int64_t pairs1 = (s->Mt + 1) / 2, pairs2 = (s->tiles_per_row / 2 + 1) / 2;
     s->ksplit1p = 1;
     if (s->tiles_per_row * BK > MAX_UNIT_K || pairs1 < s->sms / 2)
-      s->ksplit1p = choose_split(pairs1, s->tiles_per_row, s->sms / 2);
-    s->ksplit2p = choose_split(pairs2, s->Kt2, s->sms / 2);
+      s->ksplit1p = choose_split(pairs1, s->tiles_per_row, s->sms / 2, 0.05);
+    s->ksplit2p = choose_split(pairs2, s->Kt2, s->sms / 2, 0.002);
   }
   const size_t plane = (size_t)s->Mt * s->tiles_per_row * TILE_A;
   const int64_t fK = std::max<int64_t>(s->tiles_per_row, s->Kt2);
