@@ -147,9 +147,15 @@ __global__ void dot_kernel(const double* __restrict__ A, const float* __restrict
                            int64_t ldb, int64_t rows, int64_t cols, double* parts) {
   __shared__ double red[256];
   double s = 0.0;
-  // rows by blocks, a row's columns by threads (no per-element 64-bit division)
-  for (int64_t i = blockIdx.x; i < rows; i += gridDim.x)
-    for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) s += A[i * cols + j] * (double)B[i * ldb + j];
+  // rows by blocks, a row's columns by threads (no per-element 64-bit division); narrow rows
+  // (cols <= 128, the factor width) take blockDim / 128 rows per step so no thread idles
+  const int per = cols <= 128 ? (int)(blockDim.x / 128) : 1;
+  const int sub = cols <= 128 ? (int)(threadIdx.x / 128) : 0;
+  const int j0 = cols <= 128 ? (int)(threadIdx.x % 128) : (int)threadIdx.x;
+  const int js = cols <= 128 ? 128 : (int)blockDim.x;
+#pragma unroll 4
+  for (int64_t i = (int64_t)blockIdx.x * per + sub; i < rows; i += (int64_t)gridDim.x * per)
+    for (int64_t j = j0; j < cols; j += js) s += A[i * cols + j] * (double)B[i * ldb + j];
   s = block_reduce<0>(s, red);
   if (threadIdx.x == 0) parts[blockIdx.x] = s;
 }
@@ -190,8 +196,19 @@ __global__ void objective_finish_kernel(const double* xnorm2, const double* cros
                                         double* fout) {
   __shared__ double red[256];
   double s = 0.0;
-#pragma unroll 8
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) s += gu[e] * gv[e];
+  const int nn = r * r;     // <= 128^2 = 64 x 256
+  // 16 products' loads in flight before they are summed (in the same order as before)
+  for (int q0 = 0; q0 < 64 && q0 * 256 < nn; q0 += 16) {
+    double a[16], b[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int e = threadIdx.x + (q0 + q) * 256;
+      a[q] = e < nn ? gu[e] : 0.0;
+      b[q] = e < nn ? gv[e] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) s += a[q] * b[q];
+  }
   s = block_reduce<0>(s, red);
   if (threadIdx.x == 0) *fout = *xnorm2 - 2.0 * (*cross) + s;
 }
