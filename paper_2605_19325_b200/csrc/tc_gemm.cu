@@ -789,6 +789,15 @@ static int choose_split(int64_t tiles, int64_t stages, int sms, double split_cos
   return best;
 }
 
+static int choose_split_waves(int64_t tiles, int64_t stages, int sms) {
+  int ks = (int)((4 * sms + tiles - 1) / tiles);
+  const int kmin = (int)((stages * BK + MAX_UNIT_K - 1) / MAX_UNIT_K);
+  ks = std::max(std::max(ks, kmin), 1);
+  ks = std::min<int64_t>(ks, stages);
+  const int64_t per = (stages + ks - 1) / ks;
+  return (int)((stages + per - 1) / per);
+}
+
 int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t n, int64_t r,
               cudaStream_t st, double xmax) {
   *out = nullptr;
@@ -816,9 +825,12 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, dev);
   // pass 1 writes P directly unless splitting pays for its fp64 partials (rows x r x ks,
-  // written and reduced: charged 5 % per extra split); pass 2 is split-K anyway (0.2 %)
+  // written and reduced: charged 5 % per extra split) -- at C5 / 8 ranks 196 row bands take
+  // ks = 3.  Pass 2 keeps its measured rule, ks = ceil(4 SMs / tiles): the makespan choice
+  // (ks = 3 at C5) ran 2 % slower in an alternating 1-GPU A/B -- under the power cap idle SMs
+  // in the last wave lend their power to the others, while extra partials cost bandwidth.
   s->ksplit1 = choose_split(s->Mt, s->tiles_per_row, s->sms, 0.05);
-  s->ksplit2 = choose_split(s->tiles_per_row / 2, s->Kt2, s->sms, 0.002);
+  s->ksplit2 = choose_split_waves(s->tiles_per_row / 2, s->Kt2, s->sms);
   {
     // cta_group::2 kernel: correct, but measured slower than the single-CTA kernel at C5
     // (DESIGN.md §5.1); ENMF_TC_PAIR=1 selects it
@@ -828,7 +840,7 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
     s->ksplit1p = 1;
     if (s->tiles_per_row * BK > MAX_UNIT_K || pairs1 < s->sms / 2)
       s->ksplit1p = choose_split(pairs1, s->tiles_per_row, s->sms / 2, 0.05);
-    s->ksplit2p = choose_split(pairs2, s->Kt2, s->sms / 2, 0.002);
+    s->ksplit2p = choose_split_waves(pairs2, s->Kt2, s->sms / 2);
   }
   const size_t plane = (size_t)s->Mt * s->tiles_per_row * TILE_A;
   const int64_t fK = std::max<int64_t>(s->tiles_per_row, s->Kt2);
