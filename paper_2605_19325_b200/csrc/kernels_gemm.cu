@@ -200,6 +200,8 @@ void reduce_parts(const double* parts, int nparts, int64_t len, double* out, cud
   if (len <= 0) return;
   if (len <= 64 && nparts > 64)
     reduce_parts_short_kernel<<<(unsigned)len, 256, 0, st>>>(parts, nparts, len, out);
+  else if (len < (int64_t)kSMs * 256)   // e.g. the Gram partials (16384 x 296): 64-thread
+    reduce_parts_kernel<<<grid_for(len, 64), 64, 0, st>>>(parts, nparts, len, out);   // blocks
   else
     reduce_parts_kernel<<<grid_for(len), 256, 0, st>>>(parts, nparts, len, out);
   count_launch();
