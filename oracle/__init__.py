@@ -25,7 +25,8 @@ class Options(ctypes.Structure):
                 ("svd_max_iter", ctypes.c_int), ("admm_iters", ctypes.c_int),
                 ("admm_rho", ctypes.c_double), ("lift_steps", ctypes.c_int),
                 ("pbcd_eps", ctypes.c_double), ("pbcd_max_iter", ctypes.c_int),
-                ("round_f32", ctypes.c_int)]
+                ("round_f32", ctypes.c_int), ("step_rule", ctypes.c_int),
+                ("descent", ctypes.c_int)]
 
 
 class State(ctypes.Structure):
@@ -34,11 +35,13 @@ class State(ctypes.Structure):
 
 
 def options(r, oversample=10, svd_tol=1e-13, svd_max_iter=500, admm_iters=100, admm_rho=0.0,
-            lift_steps=10, pbcd_eps=1e-2, pbcd_max_iter=50, round_f32=0):
+            lift_steps=10, pbcd_eps=1e-2, pbcd_max_iter=50, round_f32=0, step_rule=0,
+            descent=0):
     """round_f32=1: factor state stored in fp32 at block boundaries, as the C-ABI stores
-    U and V (reading R26); the arithmetic itself stays fp64."""
+    U and V (reading R26); the arithmetic itself stays fp64.  step_rule / descent select the
+    ablation variants (fixed 1/lambda_max ascent step; projected-gradient descent; R29)."""
     return Options(r, oversample, svd_tol, svd_max_iter, admm_iters, admm_rho, lift_steps,
-                   pbcd_eps, pbcd_max_iter, round_f32)
+                   pbcd_eps, pbcd_max_iter, round_f32, step_rule, descent)
 
 
 def lib():
@@ -78,6 +81,13 @@ def lib():
                               _D, _D]
         L.or_pbcd.restype = ctypes.c_int
         L.or_hals.argtypes = [_D, _i64, ctypes.c_int, _D, _D]
+        L.or_pbcd_step.argtypes = [_D, _i64, ctypes.c_int, _D, _D, _U8, ctypes.c_double,
+                                   ctypes.c_int, ctypes.c_double, _D, _D]
+        L.or_pbcd_step.restype = ctypes.c_int
+        L.or_pgd.argtypes = [_D, _i64, ctypes.c_int, _D, _D, ctypes.c_double]
+        L.or_pgd.restype = None
+        L.or_lambda_max.argtypes = [_D, ctypes.c_int]
+        L.or_lambda_max.restype = ctypes.c_double
         L.or_sweep.argtypes = [_F, _i64, _i64, _D, _D, ctypes.POINTER(Options),
                                ctypes.POINTER(State), ctypes.POINTER(ctypes.c_int)]
         L.or_sweep.restype = ctypes.c_int
@@ -227,6 +237,32 @@ def pbcd(F, C, G, M, eps=1e-2, max_iter=50):
     it = lib().or_pbcd(F.ctypes.data_as(_D), F.shape[0], F.shape[1], pc, pg,
                        M.ctypes.data_as(_U8), eps, max_iter, ctypes.byref(g0), ctypes.byref(g1))
     return F, it, g0.value, g1.value
+
+
+def pbcd_step(F, C, G, M, step, eps=1e-2, max_iter=50):
+    F = np.array(F, dtype=np.float64, order="C")
+    C, pc = _f64(C)
+    G, pg = _f64(G)
+    M = np.ascontiguousarray(M, dtype=np.uint8)
+    g0 = ctypes.c_double()
+    g1 = ctypes.c_double()
+    it = lib().or_pbcd_step(F.ctypes.data_as(_D), F.shape[0], F.shape[1], pc, pg,
+                            M.ctypes.data_as(_U8), eps, max_iter, step, ctypes.byref(g0),
+                            ctypes.byref(g1))
+    return F, it, g0.value, g1.value
+
+
+def pgd(F, C, G, step):
+    F = np.array(F, dtype=np.float64, order="C")
+    C, pc = _f64(C)
+    G, pg = _f64(G)
+    lib().or_pgd(F.ctypes.data_as(_D), F.shape[0], F.shape[1], pc, pg, step)
+    return F
+
+
+def lambda_max(G):
+    G, pg = _f64(G)
+    return lib().or_lambda_max(pg, G.shape[0])
 
 
 def hals(F, C, G):

@@ -419,6 +419,15 @@ static double masked_grad_norm(const double* F, int64_t rows, int r, const doubl
 int or_pbcd(double* F, int64_t rows, int r, const double* C, const double* G,
             const unsigned char* M, double eps, int max_iter, double* pg0_out,
             double* pg_out) {
+  return or_pbcd_step(F, rows, r, C, G, M, eps, max_iter, 0.0, pg0_out, pg_out);
+}
+
+/* Alg. 2 with the step rule as a parameter: step <= 0 is Eq.(10)'s optimal row step d_i;
+ * step > 0 a fixed step for every row -- the "fixed step size" feasibility variant of the
+ * ablation (Table ablation_stepsize; reading R29: step = 1 / lambda_max(G)). */
+int or_pbcd_step(double* F, int64_t rows, int r, const double* C, const double* G,
+                 const unsigned char* M, double eps, int max_iter, double step, double* pg0_out,
+                 double* pg_out) {
   double* grad = (double*)malloc(sizeof(double) * (size_t)r);
   double* g = (double*)malloc(sizeof(double) * (size_t)r);
   double pg0 = masked_grad_norm(F, rows, r, C, G, M);   /* line 235 */
@@ -440,7 +449,7 @@ int or_pbcd(double* F, int64_t rows, int r, const double* C, const double* G,
         for (int l = 0; l < r; ++l) gg += g[l] * G[IDX(l, j, r)];
         den += gg * g[j];
       }
-      double d = den > 0.0 ? num / den : 0.0;
+      double d = step > 0.0 ? step : (den > 0.0 ? num / den : 0.0);
       /* Eq.(8): U_ij <- (U_ij - d_i grad_ij)_+ on I_+ */
       for (int j = 0; j < r; ++j)
         if (M[IDX(i, j, r)]) {
@@ -474,6 +483,34 @@ void or_hals(double* F, int64_t rows, int r, const double* C, const double* G) {
   }
 }
 
+/* "Standard gradient descent" of the ablation (variants (iv)/(v); reading
+ * R29): one projected-gradient step on the block, all entries of a row from the old row,
+ * F <- max(0, F - step (F G - C)). */
+void or_pgd(double* F, int64_t rows, int r, const double* C, const double* G, double step) {
+  double* grad = (double*)malloc(sizeof(double) * (size_t)r);
+  for (int64_t i = 0; i < rows; ++i) {
+    for (int j = 0; j < r; ++j) {
+      double s = -C[IDX(i, j, r)];
+      for (int l = 0; l < r; ++l) s += F[IDX(i, l, r)] * G[IDX(l, j, r)];
+      grad[j] = s;
+    }
+    for (int j = 0; j < r; ++j) {
+      double v = F[IDX(i, j, r)] - step * grad[j];
+      F[IDX(i, j, r)] = v > 0.0 ? v : 0.0;
+    }
+  }
+  free(grad);
+}
+
+/* lambda_max of the symmetric PSD Gram G (r x r) = its largest singular value (Jacobi SVD). */
+double or_lambda_max(const double* G, int r) {
+  double* s = (double*)malloc(sizeof(double) * (size_t)r);
+  or_svd_jacobi(G, r, r, NULL, s, NULL);
+  double lm = s[0];
+  free(s);
+  return lm;
+}
+
 /* Reading R26: the C-ABI keeps U and V in fp32 between block updates. */
 static void round_state(double* A, int64_t count, int on) {
   if (!on) return;
@@ -502,24 +539,28 @@ int or_sweep(const float* X, int64_t m, int64_t n, double* U, double* V,
     for (int64_t e = 0; e < m * r; ++e) M[e] = U[e] >= 0.0;   /* reading R14 */
     or_xv(X, m, n, V, r, C);
     or_gram(V, n, r, G);
-    int iu = or_pbcd(U, m, r, C, G, M, opt->pbcd_eps, opt->pbcd_max_iter, NULL, NULL);
+    int iu = or_pbcd_step(U, m, r, C, G, M, opt->pbcd_eps, opt->pbcd_max_iter,
+                          opt->step_rule ? 1.0 / or_lambda_max(G, r) : 0.0, NULL, NULL);
     round_state(U, m * r, opt->round_f32);
     /* V block with X^T and the new U (lines 338-340; Eq.(11) uses U^(k+1)) */
     or_lift(V, n * r, st->lambda_v);
     for (int64_t e = 0; e < n * r; ++e) M[e] = V[e] >= 0.0;
     or_xtu(X, m, n, U, r, C);
     or_gram(U, m, r, G);
-    int iv = or_pbcd(V, n, r, C, G, M, opt->pbcd_eps, opt->pbcd_max_iter, NULL, NULL);
+    int iv = or_pbcd_step(V, n, r, C, G, M, opt->pbcd_eps, opt->pbcd_max_iter,
+                          opt->step_rule ? 1.0 / or_lambda_max(G, r) : 0.0, NULL, NULL);
     round_state(V, n * r, opt->round_f32);
     if (iters) { iters[0] = iu; iters[1] = iv; }
   } else {
     or_xv(X, m, n, V, r, C);
     or_gram(V, n, r, G);
-    or_hals(U, m, r, C, G);
+    if (opt->descent) or_pgd(U, m, r, C, G, 1.0 / or_lambda_max(G, r));
+    else or_hals(U, m, r, C, G);
     round_state(U, m * r, opt->round_f32);
     or_xtu(X, m, n, U, r, C);
     or_gram(U, m, r, G);
-    or_hals(V, n, r, C, G);
+    if (opt->descent) or_pgd(V, n, r, C, G, 1.0 / or_lambda_max(G, r));
+    else or_hals(V, n, r, C, G);
     round_state(V, n * r, opt->round_f32);
     if (iters) { iters[0] = 0; iters[1] = 0; }
   }

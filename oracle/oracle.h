@@ -71,6 +71,15 @@ void or_lift(double* A, int64_t count, double lam);             /* Eq.(6)/(7) */
  * Returns inner iterations performed; pg0/pg_last out (may be NULL). */
 int or_pbcd(double* F, int64_t rows, int r, const double* C, const double* G,
             const unsigned char* M, double eps, int max_iter, double* pg0, double* pg_last);
+/* Same with the step rule as a parameter: step <= 0 Eq.(10), step > 0 fixed (ablation
+ * "fixed step size"; reading R29). */
+int or_pbcd_step(double* F, int64_t rows, int r, const double* C, const double* G,
+                 const unsigned char* M, double eps, int max_iter, double step, double* pg0,
+                 double* pg_last);
+/* One projected-gradient step F <- max(0, F - step (F G - C)) ("standard gradient descent"
+ * of the ablation; reading R29), and lambda_max of a PSD Gram. */
+void or_pgd(double* F, int64_t rows, int r, const double* C, const double* G, double step);
+double or_lambda_max(const double* G, int r);
 /* HALS column sweep (cited PAPER.md:322-324, 341; reading R12). */
 void or_hals(double* F, int64_t rows, int r, const double* C, const double* G);
 
@@ -87,6 +96,8 @@ typedef struct {
   int pbcd_max_iter;   /* default 50 (R10) */
   int round_f32;       /* 1: the factor state is stored in fp32 at block boundaries, as the
                           C-ABI stores U and V (reading R26); 0: fp64 state throughout */
+  int step_rule;       /* ascent step: 0 Eq.(10) optimal d_i, 1 fixed 1 / lambda_max(G) (R29) */
+  int descent;         /* descent stage: 0 HALS, 1 projected gradient, step 1 / lambda_max (R29) */
 } or_options_t;
 
 typedef struct {

@@ -294,6 +294,66 @@ def test_project_is_the_bounded_least_squares_solution():
     assert np.array_equal(oracle.project(-B), np.zeros_like(B))
 
 
+def _block_f(F, C, G):
+    """f(F) - const = 1/2 tr(F G F^T) - tr(F^T C) for the block problem min 1/2 ||X - F W^T||^2
+    with C = X W, G = W^T W."""
+    return 0.5 * np.sum((F @ G) * F) - np.sum(F * C)
+
+
+def test_lambda_max_against_eigvalsh():
+    g = np.random.default_rng(21)
+    for r in (1, 5, 33):
+        A = g.random((60, r))
+        G = A.T @ A
+        assert abs(oracle.lambda_max(G) - np.linalg.eigvalsh(G)[-1]) <= 1e-12 * np.linalg.eigvalsh(G)[-1]
+
+
+def test_pgd_descent_lemma_and_nnls_fixed_point():
+    """or_pgd (ablation 'standard gradient descent', reading R29): with step 1/lambda_max(G)
+    the projected-gradient step cannot increase the block objective (descent lemma + the
+    projection's non-expansiveness), and the exact per-row NNLS solution (scipy nnls, an
+    active-set method) is a fixed point."""
+    from scipy.optimize import nnls
+    g = np.random.default_rng(22)
+    X = g.random((40, 30))
+    W = g.random((30, 6))
+    C, G = X @ W, W.T @ W
+    L = oracle.lambda_max(G)
+    F = g.normal(size=(40, 6))
+    f_prev = _block_f(np.maximum(F, 0), C, G)
+    F = np.maximum(F, 0)
+    for _ in range(20):
+        F = oracle.pgd(F, C, G, 1.0 / L)
+        f = _block_f(F, C, G)
+        assert f <= f_prev + 1e-12 * abs(f_prev)
+        f_prev = f
+    Fs = np.array([nnls(W, X[i])[0] for i in range(X.shape[0])])
+    assert np.allclose(oracle.pgd(Fs, C, G, 1.0 / L), Fs, atol=1e-9)
+
+
+def test_pbcd_fixed_step_is_monotone():
+    """or_pbcd_step with the fixed step 1/lambda_max(G) (ablation 'fixed step size', R29) and
+    every entry free: the block objective is non-increasing over the inner iterations, and
+    step <= 0 reproduces or_pbcd (Eq.(10))."""
+    g = np.random.default_rng(23)
+    X = g.random((25, 20))
+    W = g.random((20, 5))
+    C, G = X @ W, W.T @ W
+    F0 = np.abs(g.normal(size=(25, 5)))
+    M = np.ones_like(F0, dtype=np.uint8)
+    L = oracle.lambda_max(G)
+    f_prev = _block_f(F0, C, G)
+    F = F0
+    for _ in range(10):
+        F, it, _, _ = oracle.pbcd_step(F, C, G, M, 1.0 / L, eps=0.0, max_iter=1)
+        f = _block_f(F, C, G)
+        assert f <= f_prev + 1e-12 * abs(f_prev)
+        f_prev = f
+    a = oracle.pbcd(F0, C, G, M, max_iter=7)
+    b = oracle.pbcd_step(F0, C, G, M, 0.0, max_iter=7)
+    assert np.array_equal(a[0], b[0]) and a[1] == b[1]
+
+
 def test_hals_matches_textbook_residual_form():
     """HALS (cited Cichocki & Phan): column k is the projected
     least-squares solution max(0, (X - sum_{l!=k} U_l V_l^T) V_k / ||V_k||^2)."""
