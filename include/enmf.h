@@ -83,6 +83,12 @@ typedef struct {
   double pbcd_eps;         /* epsilon of Alg. 2 (R10); default 1e-2 */
   int pbcd_max_iter;       /* max_iter of Alg. 2 (R10); default 50 */
   int precision;           /* enmf_precision_t */
+  int step_rule;           /* ascent (Alg. 2) step: 0 = Eq.(10)'s optimal row step (default),
+                              1 = fixed step 1 / lambda_max(G) -- the "fixed step size"
+                              ablation variant (reading R29) */
+  int descent;             /* descent stage: 0 = HALS (default), 1 = projected gradient with
+                              step 1 / lambda_max(G) -- the "gradient descent" ablation
+                              variants (reading R29) */
 } enmf_options_t;
 
 typedef struct {
@@ -174,6 +180,12 @@ enmf_status_t enmf_init(enmf_handle_t h, const float* X, int64_t ldx, float* U, 
  * returning.  ENMF_ERR_INVALID_ARG on NULL pointers or ld < r; V is replicated, so every rank
  * projects the same V identically. */
 enmf_status_t enmf_project(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv);
+
+/* Switch the ablation variants of an existing handle (the enmf_options_t fields step_rule and
+ * descent, reading R29) without rebuilding it -- a handle bound to a large X holds repacked
+ * copies of X, so comparing variants on one handle avoids a second copy.  Takes effect at the
+ * next enmf_iterate.  ENMF_ERR_INVALID_ARG unless both values are 0 or 1. */
+enmf_status_t enmf_set_ablation(enmf_handle_t h, int step_rule, int descent);
 
 /* Stage machine access (checkpoint/resume and shared-init parity runs): stage 0 = ascent,
  * 1 = HALS; lambda_u / lambda_v are the lift constants (reading R9). */

@@ -43,7 +43,8 @@ class Options(ctypes.Structure):
                 ("power_iters", ctypes.c_int), ("admm_iters", ctypes.c_int),
                 ("admm_rho", ctypes.c_double), ("lift_steps", ctypes.c_int),
                 ("pbcd_eps", ctypes.c_double), ("pbcd_max_iter", ctypes.c_int),
-                ("precision", ctypes.c_int)]
+                ("precision", ctypes.c_int), ("step_rule", ctypes.c_int),
+                ("descent", ctypes.c_int)]
 
 
 class InitInfo(ctypes.Structure):
@@ -83,6 +84,7 @@ _sigs = {
     "enmf_set_stage": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_double, ctypes.c_double]),
     "enmf_get_stage": (ctypes.c_int, [_H, ctypes.POINTER(ctypes.c_int), _D, _D]),
     "enmf_project": (ctypes.c_int, [_H, _P, _I64, _P, _I64]),
+    "enmf_set_ablation": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_int]),
     "enmf_iterate": (ctypes.c_int, [_H, _P, _I64, _P, _I64, ctypes.c_int, _D,
                                     ctypes.POINTER(IterInfo)]),
     "enmf_iterate_host": (ctypes.c_int, [_H, _P, _P, ctypes.c_int, _D,
@@ -266,6 +268,10 @@ class Enmf:
         pu, ldu = _mat(U, self.r, "U")
         pv, ldv = _mat(V, self.r, "V")
         _check(_lib.enmf_project(self._h, pu, ldu, pv, ldv), "enmf_project")
+
+    def set_ablation(self, step_rule=0, descent=0):
+        """Ablation variants (R29): fixed ascent step 1/lambda_max, projected-gradient descent."""
+        _check(_lib.enmf_set_ablation(self._h, int(step_rule), int(descent)), "enmf_set_ablation")
 
     def iterate(self, U, V, n_iters, trace=True):
         pu, ldu = _mat(U, self.r, "U")

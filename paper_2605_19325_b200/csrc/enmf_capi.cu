@@ -177,19 +177,37 @@ enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
     CUDA_TRY(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * r, h->st));
   int* stage = h->dint + I_STAGE;
   const int mi = h->opt.pbcd_max_iter;
+  // ablation variants (R29): fixed ascent step / projected-gradient descent, step 1/lambda_max(G)
+  const double* fstep = nullptr;
+  if ((maybe_ascent && h->opt.step_rule) || h->opt.descent) {
+    // stepws: s (128) | Jacobi work (2 x 128^2) | U, V of the SVD (128^2 each, unused)
+    if (!h->stepws) ENMF_TRY(dalloc(&h->stepws, (size_t)(128 + 4 * 128 * 128)));
+    double* sv = h->stepws;
+    double* wk = sv + 128;
+    jacobi_svd(G, r, wk + 2 * 128 * 128, sv, wk + 3 * 128 * 128, wk, h->st);
+    recip_first(h->stepws, h->dscal + S_STEP, h->st);
+    fstep = h->dscal + S_STEP;
+  }
   if (maybe_ascent) {
-    if (h->tc_pbcd) {
+    if (h->tc_pbcd && !h->opt.step_rule) {
       if (tc_pbcd_rows(F, ldf, rows, r, C, G, h->dscal + lam_slot, mi, h->snaps, h->parts,
                        reinterpret_cast<int8_t*>(h->tcpb_ws + 128), h->tcpb_ws, stage, h->st))
         return ENMF_ERR_CUDA;
       reduce_parts(h->parts, tc_pbcd_parts(), mi + 1, h->pgsum, h->st);
     } else {
-      pbcd_rows(F, ldf, rows, r, C, G, h->dscal + lam_slot, mi, h->snaps, h->parts, stage, h->st);
+      pbcd_rows(F, ldf, rows, r, C, G, h->dscal + lam_slot, mi, h->snaps, h->parts, stage, h->st,
+                h->opt.step_rule ? fstep : nullptr);
       reduce_parts(h->parts, pbcd_parts(), mi + 1, h->pgsum, h->st);
     }
     if (sharded) ENMF_TRY(ar(h, h->pgsum, (size_t)(mi + 1), CommOp::Sum));
+    const bool tiled = h->tc_pbcd && !h->opt.step_rule;
     pbcd_commit(F, ldf, rows, r, h->snaps, h->pgsum, h->opt.pbcd_eps, mi, h->dint + kstar_slot,
-                stage, h->minparts, h->tc_pbcd, h->st, h->tc_pbcd ? colmax : nullptr);
+                stage, h->minparts, tiled, h->st, tiled ? colmax : nullptr);
+  }
+  if (h->opt.descent) {
+    pgd_rows(F, ldf, rows, r, C, G, stage, fstep, h->minparts, h->st, colmax);
+    reduce_min(h->minparts, kRowGrid, h->dscal + min_slot, h->st);
+    return sharded ? ar(h, h->dscal + min_slot, 1, CommOp::Min) : ENMF_OK;
   }
   if (h->tc_hals) {
     // tensor-core HALS; if G has a column too ill-conditioned for the digit coupling the
@@ -241,7 +259,8 @@ enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ld
   // colmax fusion (tc path): the U / V block update writes max |F| per column, which the next
   // X pass uses for the digit scales.  Only when one of PBCD (tiled copy) / HALS writes every
   // row: PBCD runs on the tensor-core kernel whenever the tc path is active.
-  unsigned long long* umax = h->fmax_uv && (h->tc_pbcd || !maybe_ascent) ? h->fmax_uv : nullptr;
+  unsigned long long* umax =
+      h->fmax_uv && ((h->tc_pbcd && !h->opt.step_rule) || !maybe_ascent) ? h->fmax_uv : nullptr;
   unsigned long long* vmax = umax ? h->fmax_uv + 128 : nullptr;
   ENMF_TRY(contract_xv(h, V, ldv, h->P, h->vmax_valid ? h->fmax_uv + 128 : nullptr));
   if (hk.u_ready) {                    // U arrives on the copy stream during the X V pass
@@ -330,6 +349,8 @@ void enmf_default_options(enmf_options_t* o) {
   o->pbcd_eps = 1e-2;
   o->pbcd_max_iter = 50;
   o->precision = ENMF_PREC_AUTO;
+  o->step_rule = 0;
+  o->descent = 0;
 }
 
 const char* enmf_status_string(enmf_status_t s) {
@@ -413,7 +434,7 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
   void* bufs[] = {h->dscal, h->dint, h->P, h->Q, h->GU, h->GV, h->work, h->parts,
                   h->minparts, h->pgsum, h->snaps, h->ftrace, h->x_owned, h->W64,
                   h->tcpb_ws, h->fmax_uv, h->Ud, h->Vd, h->arena, h->Vg, h->Vpad,
-                  h->csc_ptr, h->csc_row, h->csc_val};
+                  h->csc_ptr, h->csc_row, h->csc_val, h->stepws};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (void* b : h->arena_extra) cudaFree(b);
@@ -656,6 +677,15 @@ enmf_status_t enmf_project(enmf_handle_t h, float* U, int64_t ldu, float* V, int
   CUDA_TRY(cudaStreamSynchronize(h->st));
   ENMF_TRY(check_launch());
   h->stage_known_hals = true;
+  h->umax_valid = h->vmax_valid = false;
+  return ENMF_OK;
+}
+
+enmf_status_t enmf_set_ablation(enmf_handle_t h, int step_rule, int descent) {
+  if (!h || (step_rule != 0 && step_rule != 1) || (descent != 0 && descent != 1))
+    return ENMF_ERR_INVALID_ARG;
+  h->opt.step_rule = step_rule;
+  h->opt.descent = descent;
   h->umax_valid = h->vmax_valid = false;
   return ENMF_OK;
 }

@@ -16,7 +16,7 @@ namespace enmf {
 // device scalar slots (doubles)
 enum {
   S_XNORM2 = 0, S_XMIN, S_XBAD, S_MINU, S_MINV, S_CROSS, S_LAMU, S_LAMV, S_NEG, S_SCRATCH,
-  S_WMAX, S_COUNT = 16
+  S_WMAX, S_STEP, S_COUNT = 16
 };
 // device int slots
 enum { I_STAGE = 0, I_KSTAR_U, I_KSTAR_V, I_CNT_ASC, I_CNT_HALS, I_BAD, I_HALS_FB, I_HALS_ILL, I_COUNT = 8 };
@@ -51,7 +51,8 @@ struct enmf_handle_s {
   double* ftrace = nullptr;
   int ftrace_cap = 0;
   enmf::TcState* tc = nullptr;
-  double* tcpb_ws = nullptr;  // tensor-core PBCD: G digits (64 KB) + 128 column scales
+  double* tcpb_ws = nullptr;
+  double* stepws = nullptr;   // lambda_max workspace of the ablation step rules (R29)  // tensor-core PBCD: G digits (64 KB) + 128 column scales
   bool tc_pbcd = false;       // ascent PBCD on the tensor cores (precision TC, r <= 128)
   bool tc_hals = false;       // HALS sweep on the tensor cores (tc_hals_rows)
   // tensor-core path: column maxima of |U| / |V| written by the block-update kernels, so the

@@ -98,7 +98,14 @@ void hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, cons
 // partial ||M o grad||^2 for each iteration 0..max_iter), runs only in the ascent stage.
 void pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
                const double* G, const double* lam, int max_iter, float* snaps,
-               double* pgparts, const int* stage, cudaStream_t st);
+               double* pgparts, const int* stage, cudaStream_t st,
+               const double* fixed_step = nullptr);   // fixed_step: device, > 0 -> fixed step
+// Projected-gradient step F <- max(0, F - step (F G - C)) (ablation, R29); runs if *stage == 1.
+void pgd_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
+              const int* stage, const double* step, double* minparts, cudaStream_t st,
+              unsigned long long* colmax = nullptr);
+// *out = 1 / s[0] (0 if s[0] <= 0): the fixed step 1 / lambda_max from a singular-value list.
+void recip_first(const double* s, double* out, cudaStream_t st);
 int pbcd_parts();
 // Selects k* from the partials (eps rule of Alg. 2), copies snapshot k* into F and
 // writes min partials; records k* into *kstar.  tiled: snapshots in tc_pbcd.cu's tile-major

@@ -196,9 +196,11 @@ __global__ void __launch_bounds__(32 * kRowWarps)
 pbcd_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
             const double* __restrict__ C, const double* __restrict__ G,
             const double* __restrict__ lam_ptr, int max_iter, float* __restrict__ snaps,
-            double* __restrict__ pgparts, const int* __restrict__ stage) {
+            double* __restrict__ pgparts, const int* __restrict__ stage,
+            const double* __restrict__ fixed_step) {
   constexpr int RP = 32 * CPL;
   if (stage != nullptr && *stage != 0) return;
+  const double fstep = fixed_step ? *fixed_step : 0.0;   // > 0: fixed step (ablation, R29)
   extern __shared__ double smem[];
   double* Gs = smem;
   double* Ss = smem + RP * RP + (threadIdx.x >> 5) * RB * RP;
@@ -264,7 +266,7 @@ pbcd_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
 #pragma unroll
       for (int b = 0; b < RB; ++b) {
         // Eq.(10): d_i = ||g_i||^2 / ||g_i V^T||^2 ; 0 on a zero denominator (R10)
-        const double d = den[b] > 0.0 ? num[b] / den[b] : 0.0;
+        const double d = fstep > 0.0 ? fstep : (den[b] > 0.0 ? num[b] / den[b] : 0.0);
         const int64_t row = rb * RB + b;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
@@ -288,6 +290,87 @@ pbcd_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
   __syncwarp();
   for (int it = lane; it <= max_iter; it += 32)
     pgparts[((int64_t)blockIdx.x * kRowWarps + warp) * (max_iter + 1) + it] = mypg[it];
+}
+
+// Projected-gradient descent step (ablation variants (iv)/(v); reading
+// R29): F <- max(0, F - step (F G - C)), all columns of a row from the old row (Jacobi), the
+// step 1/lambda_max(G) read from the device.  Same row layout as hals_kernel.
+template <int CPL, int RB>
+__global__ void __launch_bounds__(32 * kRowWarps)
+pgd_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r, const double* __restrict__ C,
+           const double* __restrict__ G, const int* __restrict__ stage, const double* step_ptr,
+           double* minparts, unsigned long long* colmax) {
+  extern __shared__ double smem[];
+  double* Gs = smem;
+  double* Ss = smem + 32 * CPL * 32 * CPL + (threadIdx.x >> 5) * RB * 32 * CPL;
+  __shared__ double wmin_s[kRowWarps];
+  const bool active = stage == nullptr || *stage == 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double wmin = DBL_MAX;
+  double cmax[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) cmax[c] = 0.0;
+  if (active) {
+    const double step = *step_ptr;
+    load_gram<CPL>(G, r, Gs);
+    __syncthreads();
+    const int64_t nblk = (rows + RB - 1) / RB;
+    for (int64_t rb = (int64_t)blockIdx.x * kRowWarps + warp; rb < nblk;
+         rb += (int64_t)gridDim.x * kRowWarps) {
+      double u[RB][CPL], t[RB][CPL];
+#pragma unroll
+      for (int b = 0; b < RB; ++b)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int64_t row = rb * RB + b;
+          const int col = lane + 32 * c;
+          const bool ok = row < rows && col < r;
+          u[b][c] = ok ? (double)F[row * ldf + col] : 0.0;
+          t[b][c] = ok ? C[row * r + col] : 0.0;
+        }
+      row_times_gram<CPL, RB>(u, Gs, Ss, r, lane, -1.0, t);      // t = C - u G = -grad
+#pragma unroll
+      for (int b = 0; b < RB; ++b)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int64_t row = rb * RB + b;
+          const int col = lane + 32 * c;
+          const double v = fma(step, t[b][c], u[b][c]);
+          const float nu = (float)(v > 0.0 ? v : 0.0);
+          if (row < rows && col < r) {
+            F[row * ldf + col] = nu;
+            wmin = fmin(wmin, (double)nu);
+            cmax[c] = fmax(cmax[c], (double)nu);
+          }
+        }
+    }
+  }
+  if (colmax && active) {
+    __shared__ unsigned long long cm_s[32 * CPL];
+    for (int c = threadIdx.x; c < 32 * CPL; c += blockDim.x) cm_s[c] = 0ull;
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+      if (lane + 32 * c < r)
+        atomicMax(&cm_s[lane + 32 * c], (unsigned long long)__double_as_longlong(cmax[c]));
+    __syncthreads();
+    for (int c = threadIdx.x; c < r; c += blockDim.x)
+      if (cm_s[c]) atomicMax(&colmax[c], cm_s[c]);
+  }
+  if (minparts) {
+    wmin = warp_min(wmin);
+    if (lane == 0) wmin_s[warp] = wmin;
+    __syncthreads();
+    if (threadIdx.x == 0 && active) {
+      double m = DBL_MAX;
+      for (int w = 0; w < kRowWarps; ++w) m = fmin(m, wmin_s[w]);
+      minparts[blockIdx.x] = m;
+    }
+  }
+}
+
+__global__ void recip_first_kernel(const double* s, double* out) {
+  if (threadIdx.x == 0) *out = s[0] > 0.0 ? 1.0 / s[0] : 0.0;
 }
 
 // k* = first inner iteration whose projected gradient drops below eps * initial
@@ -481,18 +564,38 @@ void hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, cons
   count_launch();
 }
 
+void pgd_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
+              const int* stage, const double* step, double* minparts, cudaStream_t st,
+              unsigned long long* colmax) {
+#define CALL(CPL)                                                                      \
+  {                                                                                    \
+    auto k = pgd_kernel<CPL, 8>;                                                       \
+    size_t sm = row_smem<CPL>(0, 8);                                                   \
+    set_smem(k, sm);                                                                   \
+    k<<<kRowGrid, 32 * kRowWarps, sm, st>>>(F, ldf, rows, r, C, G, stage, step, minparts, colmax); \
+  }
+  ENMF_CPL_DISPATCH(r, CALL);
+#undef CALL
+  count_launch();
+}
+
+void recip_first(const double* s, double* out, cudaStream_t st) {
+  recip_first_kernel<<<1, 32, 0, st>>>(s, out);
+  count_launch();
+}
+
 int pbcd_parts() { return kRowGrid * kRowWarps; }
 
 void pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
                const double* G, const double* lam, int max_iter, float* snaps,
-               double* pgparts, const int* stage, cudaStream_t st) {
+               double* pgparts, const int* stage, cudaStream_t st, const double* fixed_step) {
 #define CALL(CPL)                                                                           \
   {                                                                                         \
     auto k = pbcd_kernel<CPL, 4>;                                                           \
     size_t sm = row_smem<CPL>(kRowWarps * (max_iter + 1));                                  \
     set_smem(k, sm);                                                                        \
     k<<<kRowGrid, 32 * kRowWarps, sm, st>>>(F, ldf, rows, r, C, G, lam, max_iter, snaps,    \
-                                           pgparts, stage);                                 \
+                                           pgparts, stage, fixed_step);                     \
   }
   ENMF_CPL_DISPATCH(r, CALL);
 #undef CALL

@@ -127,6 +127,66 @@ def test_projection_then_hals(cfg, prec):
 
 
 @pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
+@pytest.mark.parametrize("cfg", [CASES[0], CASES[4], CASES[6]], ids=[IDS[0], IDS[4], IDS[6]])
+def test_ablation_gradient_descent(cfg, prec):
+    """Descent-stage variant 'standard gradient descent' of the ablation (options.descent = 1,
+    PAPER.md:2096-2099, reading R29): projected-gradient sweeps with step 1/lambda_max(G)
+    from a shared feasible point -- one sweep within 1e-5 of the oracle, 10-sweep f trajectory
+    at the HALS-stage bars."""
+    h, X, _ = make(cfg, precision=prec, descent=1)
+    U0, V0, _, _ = rotated_point(X, cfg.r)
+    U0, V0 = np.abs(U0), np.abs(V0)
+    opts = oracle.options(cfg.r, round_f32=1, descent=1)
+    U, V = to_dev(U0), to_dev(V0)
+    h.set_stage(1)
+    h.iterate(U, V, 1)
+    Uo, Vo, _, _ = oracle.sweep(X, U0, V0, oracle.SweepState(stage=1), opts)
+    eu, ev = rel_fro(to_np(U), Uo), rel_fro(to_np(V), Vo)
+    U, V = to_dev(U0), to_dev(V0)
+    h.set_stage(1)
+    f_gpu, info = h.iterate(U, V, 10)
+    st = oracle.SweepState(stage=1)
+    Ua, Va, f_or = U0, V0, []
+    for _ in range(10):
+        Ua, Va, _, _ = oracle.sweep(X, Ua, Va, st, opts)
+        f_or.append(oracle.frob2_direct(X, Ua, Va))
+    f_or = np.array(f_or)
+    err = np.abs(f_gpu - f_or) / f_or
+    bound = np.maximum(1e-4, 1e-8 * oracle.xnorm2(X) / f_or) if prec == TC else 1e-4
+    print(f"{cfg.name} prec={h.precision}: PGD sweep U {eu:.2e} V {ev:.2e}, 10-sweep f err "
+          f"{err.max():.2e}")
+    assert eu < 1e-5 and ev < 1e-5
+    assert info["hals_sweeps"] == 10 and np.all(err < bound)
+
+
+@pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
+@pytest.mark.parametrize("cfg", [CASES[1], CASES[6]], ids=[IDS[1], IDS[6]])
+def test_ablation_fixed_step_ascent(cfg, prec):
+    """Feasibility-stage variant 'fixed step size' (options.step_rule = 1, PAPER.md:2160-2165,
+    reading R29): one lift + PBCD sweep with the step 1/lambda_max(G) for every row, against
+    the oracle at the ascent bar max(1e-5, 10 x the oracle's 1-ulp floor)."""
+    h, X, _ = make(cfg, precision=prec, step_rule=1)
+    U0, V0, lu, lv = rotated_point(X, cfg.r)
+    if U0.min() >= 0 and V0.min() >= 0:
+        pytest.skip("rotated point already feasible (one-shot case)")
+    opts = oracle.options(cfg.r, round_f32=1, step_rule=1)
+    U, V = to_dev(U0), to_dev(V0)
+    h.set_stage(0, lu, lv)
+    _, info = h.iterate(U, V, 1)
+
+    def run(Ua, Va):
+        Uo, Vo, _, _ = oracle.sweep(X, Ua, Va, oracle.SweepState(0, lu, lv, 0), opts)
+        return Uo, Vo
+
+    (Uo, Vo), floor = oracle_floor(run, U0, V0)
+    eu, ev = rel_fro(to_np(U), Uo), rel_fro(to_np(V), Vo)
+    print(f"{cfg.name} prec={h.precision}: fixed-step ascent U {eu:.2e} V {ev:.2e}, floor "
+          f"{floor[0]:.1e}/{floor[1]:.1e}, k* {info['pbcd_iters_u']}/{info['pbcd_iters_v']}")
+    assert info["ascent_sweeps"] == 1
+    assert eu < max(1e-5, 10 * floor[0]) and ev < max(1e-5, 10 * floor[1])
+
+
+@pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
 @pytest.mark.parametrize("cfg", CASES[:4] + [CASES[6]], ids=IDS[:4] + [IDS[6]])
 def test_hals_trajectory_50_sweeps(cfg, prec):
     """50 HALS sweeps from a shared feasible point: final factors within 1e-4, the direct
