@@ -323,7 +323,7 @@ def run_enmf(args):
     # direct projection onto the orthant + HALS, from the same rotated point for the same K
     # sweeps; the timed region above is variant (i), the method (feasibility stage + HALS)
     ablation = None
-    if not args.no_ablation:
+    if not args.no_ablation and world == 1:     # single-GPU runs only (no extra collectives)
         U.copy_(U_rot)
         V.copy_(V_rot)
         barrier()
