@@ -157,6 +157,13 @@ def test_ablation_gradient_descent(cfg, prec):
           f"{err.max():.2e}")
     assert eu < 1e-5 and ev < 1e-5
     assert info["hals_sweeps"] == 10 and np.all(err < bound)
+    # the same variant switched on a handle created with the defaults (enmf_set_ablation)
+    h2, _, _ = make(cfg, precision=prec)
+    h2.set_ablation(0, 1)
+    U, V = to_dev(U0), to_dev(V0)
+    h2.set_stage(1)
+    f2, _ = h2.iterate(U, V, 10)
+    assert np.array_equal(f2, f_gpu)
 
 
 @pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
