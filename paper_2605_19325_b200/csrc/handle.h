@@ -51,8 +51,9 @@ struct enmf_handle_s {
   double* ftrace = nullptr;
   int ftrace_cap = 0;
   enmf::TcState* tc = nullptr;
-  double* tcpb_ws = nullptr;
-  double* stepws = nullptr;   // lambda_max workspace of the ablation step rules (R29)  // tensor-core PBCD: G digits (64 KB) + 128 column scales
+  double* tcpb_ws = nullptr;  // tensor-core PBCD: G digits (64 KB) + 128 column scales
+  double* stepws = nullptr;   // lambda_max workspace of the ablation step rules (R29)
+  bool step_warm[2] = {false, false};   // stepws holds a warm start per block (U, V)
   bool tc_pbcd = false;       // ascent PBCD on the tensor cores (precision TC, r <= 128)
   bool tc_hals = false;       // HALS sweep on the tensor cores (tc_hals_rows)
   // tensor-core path: column maxima of |U| / |V| written by the block-update kernels, so the
