@@ -81,27 +81,34 @@ class ClockSampler:
             self.proc = None
 
     def stop(self):
+        """Median SM clock over the samples taken under load: the sampler starts right before
+        and stops right after the timed region, and a sample counts as under load when its
+        power draw is at least half of the maximum seen (the idle edges of the 200 ms grid
+        are dropped)."""
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
-        sm, smax, reasons = [], None, set()
+        rows, smax = [], None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
             try:
-                sm.append(float(f[1]))
+                sm, pw = float(f[1]), float(f[3])
                 smax = float(f[2])
             except ValueError:
                 continue
-            for nm, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        med = float(np.median(sm)) if sm else None
-        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+            rows.append((sm, pw, {nm for nm, v in zip(names, f[5:9]) if v.lower() == "active"}))
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": smax, "reasons": [], "samples": 0}
+        pmax = max(r[1] for r in rows)
+        load = [r for r in rows if r[1] >= 0.5 * pmax]
+        reasons = set().union(*[r[2] for r in load]) if load else set()
+        return {"sm_mhz": float(np.median([r[0] for r in load])), "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(load), "samples_all": len(rows),
+                "power_w_max": pmax}
 
 
 def gpu_index(local_rank):
@@ -166,6 +173,46 @@ def run_reference(args):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def x_pass_roofline(precision, prof, rows, n, r, peaks, peak_kind, traffic_j, step_ms):
+    """Roofline of the dominant kernel: each X pass on its own (P = X V, Q = X^T U), the
+    slower one as the headline.  achieved = ALGORITHMIC bytes (fp32 X, rows x n x 4 B per
+    pass) / the pass's mean device time; `physical` = what the pass actually
+    reads from HBM (the tensor-core path streams 3 int8 digit planes = 3 B per element, the
+    fp64 path fp32 X) against the same peak; `tensor` = its int8 digit products (6 per
+    element on the tensor-core path: 2 rows n r ops each) against the int8 dense peak, taken as
+    2 x the measured bf16 throughput (sustained: the passes run inside a long step) -- the
+    limiter that shares the bound with HBM.  traffic = ncu DRAM bytes per
+    launch of that kernel (profiles/ncu_traffic.json), None if not captured."""
+    tc = precision.startswith("tc")
+    alg = float(rows) * n * 4
+    phys = float(rows) * n * (3 if tc else 4)
+    int8_peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0))
+    passes = {}
+    for key, name in (("xv", "pass1_P=XV"), ("xtu", "pass2_Q=XtU")):
+        t_ms = prof[key][0] / max(1, prof[key][1])
+        a = alg / (t_ms / 1000.0) / 1e9
+        d = {"ms": t_ms, "launches": prof[key][1], "achieved_gbs": a,
+             "frac": a / peaks["hbm_gbs"],
+             "physical_gbs": phys / (t_ms / 1000.0) / 1e9,
+             "physical_frac": phys / (t_ms / 1000.0) / 1e9 / peaks["hbm_gbs"],
+             "traffic": traffic_j.get(f"{key}_bytes")}
+        if tc:
+            tops = 6 * 2.0 * rows * n * r / (t_ms / 1000.0) / 1e12
+            d["tensor"] = {"int8_tops": tops, "peak_tops": int8_peak, "frac": tops / int8_peak}
+        passes[name] = d
+    dom_key = max(passes, key=lambda k: passes[k]["ms"])
+    dom = passes[dom_key]
+    return {"bound": "hbm", "achieved": dom["achieved_gbs"], "peak": peaks["hbm_gbs"],
+            "unit": "GB/s", "frac": dom["frac"], "traffic": dom["traffic"],
+            "kernel": f"{dom_key} ({precision}: tc_i8_kernel)" if tc else f"{dom_key} ({precision})",
+            "peak_kind": peak_kind,
+            "bytes_per_launch": {"algorithmic": alg, "physical": phys},
+            "limiter": ("int8 tensor pipe (6 digit products per element) co-limiting with HBM "
+                        "(3 B per element)") if tc else "fp64 FMA (SIMT)",
+            "passes": passes,
+            "share_of_step": (prof["xv"][0] + prof["xtu"][0]) / max(step_ms, 1e-9)}
 
 
 def run_enmf(args):
@@ -238,7 +285,6 @@ def run_enmf(args):
     sampler = ClockSampler(gpu_index(local))
     barrier()
     sampler.start()
-    time.sleep(0.3)
     l0 = h.launch_count
     h.set_profiling(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -265,15 +311,14 @@ def run_enmf(args):
     gbs = 2.0 * x_bytes_pass * sweeps_per_s / 1e9
 
     peaks, peak_kind = measured_peaks()
-    # dominant kernel: the X passes (X V and X^T U) -- algorithmic bytes = this rank's X
+    # the X passes (X V and X^T U), timed separately: CUDA events on the handle's stream around
+    # every pass (enmf_set_profiling), algorithmic bytes = this rank's fp32 X
     pass_ms = (prof["xv"][0] + prof["xtu"][0]) / max(1, prof["xv"][1] + prof["xtu"][1])
-    achieved = float(count) * n * 4 / (pass_ms / 1000.0) / 1e9 if not sparse else None
-    traffic = None
+    traffic_j = {}
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
-            tj = json.load(fh)
-        traffic = tj.get(h.precision, {}).get("bytes_per_pass")
+            traffic_j = json.load(fh).get(h.precision, {})
     if sparse:
         # SpMM X pass: 2 r flops per stored entry in fp64 FMA (one warp per row), CSR bytes
         # streamed once; peak = 148 SMs x 64 DFMA/clk x 2 flop at the max SM clock
@@ -290,11 +335,8 @@ def run_enmf(args):
                     "gather_gbs": nnz_local * r * 4.0 / (pass_ms / 1000.0) / 1e9,
                     "share_of_step": (prof["xv"][0] + prof["xtu"][0]) / max(ms, 1e-9)}
     else:
-        roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
-                    "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                    "kernel": f"X pass ({h.precision})", "peak_kind": peak_kind,
-                    "pass_ms": pass_ms,
-                    "share_of_step": (prof["xv"][0] + prof["xtu"][0]) / max(ms, 1e-9)}
+        roofline = x_pass_roofline(h.precision, prof, count, n, r, peaks, peak_kind,
+                                   traffic_j, ms)
 
     # ---- per-stage rates: a few HALS sweeps from the final (feasible) state
     # and a few ascent sweeps from the rotated point; the timed region above is the blend
@@ -418,7 +460,7 @@ def run_enmf(args):
             "dtype": "f64" if h.precision in ("fp64-simt", "csr-f64-spmm")
                      else ("f64 SpMM X passes / i8-digit tensor-core row updates"
                            if sparse else
-                           "i8 (4x7-bit digits of fp32 X, V, U) / exact i32 TMEM / f64"),
+                           "i8 (3 digits, radix 8/8/7, of fp32 X, V, U) / exact i32 TMEM / f64"),
             "data": "synthetic",
             "config": {"workload": cfg.name, "m": m, "n": n, "r": r,
                        "global_batch": m, "seq_len": n,

@@ -67,10 +67,15 @@ typedef struct {
 } enmf_problem_t;
 
 typedef enum {
-  ENMF_PREC_AUTO = 0,      /* tensor-core split path when profitable, else FP64 */
+  ENMF_PREC_AUTO = 0,      /* TC when the average rank holds >= 2.5e8 entries of X and
+                              max|X| <= 64 rms(X) (decided from global statistics, the same on
+                              every rank), else FP64 */
   ENMF_PREC_FP64 = 1,      /* SIMT contractions with fp64 accumulation */
-  ENMF_PREC_TC = 2         /* tcgen05 split-fp16 X (X = Xhi + Xlo), fp32 TMEM chunks
-                              promoted to fp64 */
+  ENMF_PREC_TC = 2         /* tcgen05 kind::i8: X, V, U as three int8 digits (radix 8/8/7) of
+                              a power-of-two-scaled fp32 value (one scale per X row for X V,
+                              per X column for X^T U, per factor column), six digit products
+                              accumulated exactly in int32 TMEM and combined in fp64; ~2^-22 of
+                              each scale group's maximum per operand entry */
 } enmf_precision_t;
 
 typedef struct {
@@ -134,14 +139,18 @@ enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
 enmf_status_t enmf_destroy(enmf_handle_t h);
 
 /* Bind this rank's rows of X (device, row_count x n, leading dim ldx >= n).  Computes
- * ||X||_F^2 and checks X >= 0 and finite (ENMF_ERR_NEGATIVE_X / ENMF_ERR_NONFINITE).  On
- * the tensor-core path also builds the handle-owned split copy X = Xhi + Xlo (fp16 pair).
+ * ||X||_F^2 and checks X >= 0 and finite (ENMF_ERR_NEGATIVE_X / ENMF_ERR_NONFINITE), then
+ * selects the contraction path (enmf_precision_t).  On the tensor-core path it also builds the
+ * handle-owned int8 digit copies of X (3 B per element) and, when device memory allows, of X^T
+ * (another 3 B per element; without it X^T U gathers from the X copy, ~40 % slower) -- X
+ * itself is not read again by enmf_iterate (ENMF_ERR_OOM if the X copy does not fit).
  * Resets the stage machine. */
 enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx);
 
 /* Sparse X (the paper's sparse Reuters experiment):
  * bind this rank's rows of X as CSR instead of a dense matrix.  row_ptr (row_count + 1,
- * int64, row_ptr[0] = 0), col_idx (nnz, int32, strictly ascending within a row, in [0, n))
+ * int64, row_ptr[0] = 0, row_ptr[row_count] = nnz, non-decreasing), col_idx (nnz, int32,
+ * strictly ascending within a row, in [0, n))
  * and vals (nnz, fp32, >= 0, finite) are DEVICE pointers, caller-owned, read-only and kept
  * (not copied) until the next set_data call or destroy; zeros not stored are zeros of X.
  * The handle builds a CSC copy for X^T U (deterministic: entries of a column in ascending
@@ -149,8 +158,8 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx);
  * P = X V and Q = X^T U (fp64-accumulating SpMM), so init / iterate / objective / kkt work
  * unchanged; enmf_objective(exact = 1) evaluates ||X||^2 - 2 sum_stored x_ij u_i.v_j +
  * <U^T U, V^T V>.  Block updates run on the tensor-core row kernels unless the precision
- * option is ENMF_PREC_FP64.  Errors: ENMF_ERR_INVALID_ARG (NULL pointers, bad row ranges or
- * column order), ENMF_ERR_SHAPE (nnz or n above 2^31 - 1), ENMF_ERR_NEGATIVE_X,
+ * option is ENMF_PREC_FP64.  Errors: ENMF_ERR_INVALID_ARG (NULL pointers, a row_ptr that
+ * does not start at 0 / end at nnz / decrease, column order), ENMF_ERR_SHAPE (nnz or n above 2^31 - 1), ENMF_ERR_NEGATIVE_X,
  * ENMF_ERR_NONFINITE, ENMF_ERR_OOM. */
 enmf_status_t enmf_set_data_csr(enmf_handle_t h, const int64_t* row_ptr, const int32_t* col_idx,
                                 const float* vals, int64_t nnz);
@@ -195,7 +204,10 @@ enmf_status_t enmf_get_stage(enmf_handle_t h, int* stage, double* lambda_u, doub
 /* n_iters sweeps of Alg. 3's loop: each sweep is one U block and one
  * V block, ascent (lift + mask + PBCD) while min(U) < 0 or min(V) < 0, HALS afterwards.
  * f_trace_host (n_iters doubles, may be NULL) receives ||X - U V^T||_F^2 after every
- * sweep in trace form ||X||^2 - 2<X^T U, V> + <U^T U, V^T V> (fp64 terms). */
+ * sweep in trace form ||X||^2 - 2<X^T U, V> + <U^T U, V^T V> (fp64 terms); on the
+ * tensor-core path the terms are those of the quantised operands the X pass multiplied,
+ * ||X~||^2 - 2<X~^T U~, V> + <U~^T U~, V^T V> = ||X~ - U~ V^T||^2 up to the dropped digit
+ * products, which keeps the ||X||^2 / f conditioning of the trace form out of f. */
 enmf_status_t enmf_iterate(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
                            int n_iters, double* f_trace_host, enmf_iter_info_t* info_host);
 
@@ -253,7 +265,8 @@ enmf_status_t enmf_set_host_allreduce(enmf_handle_t h, enmf_host_allreduce_fn fn
  * in enmf_problem_t.nccl_unique_id on every rank). */
 enmf_status_t enmf_nccl_unique_id(void* out128);
 
-/* Name of the contraction path selected by enmf_set_data ("fp64-simt" or "tc-i8x4-exact"). */
+/* Name of the contraction path selected by enmf_set_data ("fp64-simt", "tc-i8x3-exact",
+ * "csr-f64-spmm" or "csr-f64-spmm+tc-rows"). */
 const char* enmf_precision_name(enmf_handle_t h);
 
 const char* enmf_status_string(enmf_status_t s);

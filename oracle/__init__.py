@@ -95,6 +95,25 @@ def lib():
                               _D, ctypes.POINTER(State)]
         L.or_enmf.restype = ctypes.c_int
         L.or_kkt.argtypes = [_F, _i64, _i64, _D, _D, ctypes.c_int, _D]
+        _I64P = ctypes.POINTER(ctypes.c_int64)
+        _I32P = ctypes.POINTER(ctypes.c_int32)
+        L.or_nmc_objective.argtypes = [_I64P, _I32P, _F, _i64, _D, _D, ctypes.c_int]
+        L.or_nmc_objective.restype = ctypes.c_double
+        L.or_nmc_grad.argtypes = [_I64P, _I32P, _F, _i64, _D, _D, ctypes.c_int, _D]
+        L.or_nmc_grad.restype = None
+        L.or_nmc_pbcd.argtypes = [_I64P, _I32P, _F, _i64, _D, _D, ctypes.c_int, _U8,
+                                  ctypes.c_double, ctypes.c_int, _D, _D]
+        L.or_nmc_pbcd.restype = ctypes.c_int
+        L.or_csr_transpose.argtypes = [_I64P, _I32P, _F, _i64, _i64, _I64P, _I32P, _F]
+        L.or_csr_transpose.restype = None
+        L.or_nmc_sweep.argtypes = [_I64P, _I32P, _F, _I64P, _I32P, _F, _i64, _i64, _D, _D,
+                                   ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                   ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                   ctypes.POINTER(ctypes.c_int)]
+        L.or_nmc_sweep.restype = None
+        L.or_softimpute.argtypes = [_I64P, _I32P, _F, _i64, _i64, ctypes.c_int, _D,
+                                    ctypes.c_int, _D, _D, _D]
+        L.or_softimpute.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -322,3 +341,97 @@ def kkt(X, U, V):
     out, po = _out((9,))
     lib().or_kkt(px, X.shape[0], X.shape[1], pu, pv, U.shape[1], po)
     return dict(zip(KKT_FIELDS, out.tolist()))
+
+
+# ---------------------------------------------------------------- eNMC (oracle_nmc.c)
+class Observed:
+    """Observed entries of an m x n X (eNMC) as CSR lists plus the
+    transposed (CSC) lists the V block reads; built from a dense X and a boolean mask."""
+
+    def __init__(self, X, mask):
+        X = np.asarray(X, dtype=np.float32)
+        mask = np.asarray(mask, dtype=bool)
+        self.m, self.n = X.shape
+        rows, cols = np.nonzero(mask)            # row-major order: columns ascend per row
+        self.ptr = np.zeros(self.m + 1, dtype=np.int64)
+        np.add.at(self.ptr, rows + 1, 1)
+        self.ptr = np.cumsum(self.ptr).astype(np.int64)
+        self.idx = cols.astype(np.int32)
+        self.val = X[rows, cols].astype(np.float32)
+        self.tptr = np.zeros(self.n + 1, dtype=np.int64)
+        self.tidx = np.zeros(len(self.idx), dtype=np.int32)
+        self.tval = np.zeros(len(self.idx), dtype=np.float32)
+        lib().or_csr_transpose(*self._csr(), self.m, self.n, _p64(self.tptr), _p32(self.tidx),
+                               self.tval.ctypes.data_as(_F))
+
+    def _csr(self):
+        return _p64(self.ptr), _p32(self.idx), self.val.ctypes.data_as(_F)
+
+    def _csc(self):
+        return _p64(self.tptr), _p32(self.tidx), self.tval.ctypes.data_as(_F)
+
+
+def _p64(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+def _p32(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def nmc_objective(obs, U, V):
+    U, pu = _f64(U)
+    V, pv = _f64(V)
+    return lib().or_nmc_objective(*obs._csr(), obs.m, pu, pv, U.shape[1])
+
+
+def nmc_grad(obs, U, V, block="U"):
+    """grad_U f^ = (M_E o (U V^T - X)) V, or grad_V (block="V") from the transposed lists."""
+    U, pu = _f64(U)
+    V, pv = _f64(V)
+    if block == "U":
+        G, pg = _out(U.shape)
+        lib().or_nmc_grad(*obs._csr(), obs.m, pu, pv, U.shape[1], pg)
+    else:
+        G, pg = _out(V.shape)
+        lib().or_nmc_grad(*obs._csc(), obs.n, pv, pu, V.shape[1], pg)
+    return G
+
+
+def nmc_pbcd(obs, F, O, M, block="U", eps=1e-2, max_iter=50):
+    """PBCD of one block (F = U with O = V for block "U", F = V with O = U for "V");
+    returns (F_new, iterations, pg0, pg_last)."""
+    F = np.array(F, dtype=np.float64, order="C")
+    O, po = _f64(O)
+    M = np.ascontiguousarray(M, dtype=np.uint8)
+    g0, g1 = ctypes.c_double(), ctypes.c_double()
+    lists = obs._csr() if block == "U" else obs._csc()
+    rows = obs.m if block == "U" else obs.n
+    it = lib().or_nmc_pbcd(*lists, rows, F.ctypes.data_as(_D), po, F.shape[1],
+                           M.ctypes.data_as(_U8), eps, max_iter, ctypes.byref(g0),
+                           ctypes.byref(g1))
+    return F, it, g0.value, g1.value
+
+
+def nmc_sweep(obs, U, V, lambda_u, lambda_v, eps=1e-2, max_iter=50, round_f32=1):
+    """One eNMC sweep (Alg. NMC loop body); returns (U, V, (iters_u, iters_v))."""
+    U = np.array(U, dtype=np.float64, order="C")
+    V = np.array(V, dtype=np.float64, order="C")
+    it = (ctypes.c_int * 2)()
+    lib().or_nmc_sweep(*obs._csr(), *obs._csc(), obs.m, obs.n, U.ctypes.data_as(_D),
+                       V.ctypes.data_as(_D), U.shape[1], lambda_u, lambda_v, eps, max_iter,
+                       round_f32, it)
+    return U, V, (it[0], it[1])
+
+
+def softimpute(obs, U0, iters):
+    """softImpute-ALS, lambda = 0 (reading R31): returns (A, B, d)."""
+    U0, pu = _f64(U0)
+    r = U0.shape[1]
+    A, pa = _out((obs.m, r))
+    B, pb = _out((obs.n, r))
+    d, pd = _out((r,))
+    rc = lib().or_softimpute(*obs._csr(), obs.m, obs.n, r, pu, iters, pa, pb, pd)
+    if rc != 0:
+        raise ValueError("softimpute: a half-step product has a zero singular value")
+    return A, B, d

@@ -126,6 +126,26 @@ int or_enmf(const float* X, int64_t m, int64_t n, const or_options_t* opt, int n
 void or_kkt(const float* X, int64_t m, int64_t n, const double* U, const double* V, int r,
             double* out);
 
+/* ---- eNMC, exterior nonnegative matrix completion (App. C; Alg. NMC)
+ * -- oracle_nmc.c.  Observed entries of X as CSR lists (ptr: rows + 1, idx ascending within
+ * a row, val); unlisted entries are missing.  Readings R30-R32. ---- */
+double or_nmc_objective(const int64_t* ptr, const int32_t* idx, const float* val, int64_t m,
+                        const double* U, const double* V, int r);
+void or_nmc_grad(const int64_t* ptr, const int32_t* idx, const float* val, int64_t rows,
+                 const double* F, const double* O, int r, double* grad);
+int or_nmc_pbcd(const int64_t* ptr, const int32_t* idx, const float* val, int64_t rows,
+                double* F, const double* O, int r, const unsigned char* M, double eps,
+                int max_iter, double* pg0_out, double* pg_out);
+void or_csr_transpose(const int64_t* ptr, const int32_t* idx, const float* val, int64_t m,
+                      int64_t n, int64_t* tptr, int32_t* tidx, float* tval);
+void or_nmc_sweep(const int64_t* ptr, const int32_t* idx, const float* val,
+                  const int64_t* tptr, const int32_t* tidx, const float* tval, int64_t m,
+                  int64_t n, double* U, double* V, int r, double lambda_u, double lambda_v,
+                  double eps, int max_iter, int round32, int* iters);
+int or_softimpute(const int64_t* ptr, const int32_t* idx, const float* val, int64_t m,
+                  int64_t n, int r, const double* U0, int iters, double* A, double* B,
+                  double* d);
+
 #ifdef __cplusplus
 }
 #endif

@@ -140,12 +140,13 @@ enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double*
 
 // G = A^T A of an fp32 factor (rows x r); sum over ranks if `sharded`.
 enmf_status_t gram_f32(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, double* G,
-                       bool sharded) {
+                       bool sharded, const double* qscale) {
   if (gram_supported((int)h->r) &&
       h->work_elems >= (size_t)128 * 128 * (1 + (size_t)gram_parts())) {
     // upper-triangle fp64 Gram (kernels_gram.cu): Gu = work[0 .. 128^2), per-SM partials after
-    gram_sym(A, lda, rows, (int)h->r, h->work + 128 * 128, h->work, G, h->st);
+    gram_sym(A, lda, rows, (int)h->r, h->work + 128 * 128, h->work, G, h->st, qscale);
   } else {
+    if (qscale) return ENMF_ERR_STATE;
     GemmOut o;
     o.C = G;
     o.ldc = h->r;
@@ -283,9 +284,11 @@ enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ld
     CUDA_TRY(cudaMemcpyAsync(hk.u_download, U, sizeof(float) * h->m_loc * h->r,
                              cudaMemcpyDeviceToHost, h->st2));
   }
-  // V block: Q = X^T U_new (allreduced), G_U = U_new^T U_new (PAPER.md:220 uses U^(k+1))
-  ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh));
+  // V block: Q = X^T U_new (allreduced), G_U = U_new^T U_new (PAPER.md:220 uses U^(k+1));
+  // on the tensor-core path G_U is the Gram of the quantised U the X pass multiplied
+  // (qgram_scales), so that the V update and the trace-form objective see one operand
   ENMF_TRY(contract_xtu(h, U, ldu, h->Q, h->umax_valid ? h->fmax_uv : nullptr, sh));
+  ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh, qgram_scales(h)));
   const int64_t vb = h->v_begin, vc = h->v_count, r = h->r;
   if (sh) {
     // V block sharded by rows (V rows are independent given Q and G_U): each
@@ -333,7 +336,7 @@ enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ld
     ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
     dot_f64_f32(h->Q, V, ldv, h->n, h->r, h->parts, h->dscal + S_CROSS, st);
   }
-  objective_finish(h->dscal + S_XNORM2, h->dscal + S_CROSS, h->GU, h->GV, (int)h->r,
+  objective_finish(xnorm2_trace(h), h->dscal + S_CROSS, h->GU, h->GV, (int)h->r,
                    h->ftrace + t, st);
   return check_launch();
 }
@@ -430,7 +433,7 @@ enmf_status_t enmf_nccl_unique_id(void* out128) {
 const char* enmf_precision_name(enmf_handle_t h) {
   if (!h) return "none";
   if (h->sparse) return h->tc_pbcd ? "csr-f64-spmm+tc-rows" : "csr-f64-spmm";
-  return h->precision == ENMF_PREC_TC ? "tc-i8x4-exact" : "fp64-simt";
+  return h->precision == ENMF_PREC_TC ? "tc-i8x3-exact" : "fp64-simt";
 }
 
 enmf_status_t enmf_destroy(enmf_handle_t h) {
@@ -550,6 +553,7 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
   ENMF_TRY(ar(h, out3, 1, CommOp::Sum));
   ENMF_TRY(ar(h, out3 + 1, 1, CommOp::Min));
   ENMF_TRY(ar(h, out3 + 2, 1, CommOp::Sum));
+  ENMF_TRY(ar(h, out3 + 3, 1, CommOp::Max));
   double hv[4];
   CUDA_TRY(cudaMemcpyAsync(hv, out3, sizeof(hv), cudaMemcpyDeviceToHost, h->st));
   CUDA_TRY(cudaStreamSynchronize(h->st));
@@ -557,16 +561,29 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
   if (hv[1] < 0) return ENMF_ERR_NEGATIVE_X;
   CUDA_TRY(cudaMemcpyAsync(h->dscal + S_XNORM2, out3, sizeof(double), cudaMemcpyDeviceToDevice,
                            h->st));
-  // precision selection: the tensor-core split path pays off on large X
+  // precision selection (the same on every rank: global statistics, average rank size): the
+  // tensor-core digit path pays off on large X and keeps ~1e-9 accuracy when
+  // the entries are not far below their scale group's maximum -- it rounds every entry to
+  // ~2^-23 of its row's (column's) maximum, so AUTO requires max|X| <= 64 rms(X); heavy-tailed
+  // data (counts, tf-idf) stays on the fp64 path
   int prec = h->opt.precision;
-  if (prec == ENMF_PREC_AUTO)
-    prec = (tc_supported(h->m_loc, h->n, h->r) && (double)h->m_loc * h->n >= 2.5e8)
+  if (prec == ENMF_PREC_AUTO) {
+    const double mn = (double)h->prob.m_global * (double)h->n;
+    const double rms = sqrt(hv[0] / mn);
+    prec = (tc_supported(h->m_loc, h->n, h->r) && mn / h->prob.world_size >= 2.5e8 &&
+            hv[3] <= 64.0 * rms)
                ? ENMF_PREC_TC : ENMF_PREC_FP64;
+  }
   if (prec == ENMF_PREC_TC && !tc_supported(h->m_loc, h->n, h->r)) return ENMF_ERR_SHAPE;
   if (h->tc) { tc_destroy(h->tc); h->tc = nullptr; }
   if (prec == ENMF_PREC_TC) {
-    int rc = tc_create(&h->tc, X, ldx, h->m_loc, h->n, h->r, h->st, hv[3]);
+    int rc = tc_create(&h->tc, X, ldx, h->m_loc, h->n, h->r, h->st, h->parts,
+                       (int)std::min<size_t>(h->parts_elems, 1 << 20));
     if (rc != 0) return rc == 2 ? ENMF_ERR_OOM : ENMF_ERR_CUDA;
+    // ||X~||^2 of the quantised X (all ranks): the trace-form objective's first term
+    CUDA_TRY(cudaMemcpyAsync(h->dscal + S_XQNORM2, tc_xq_norm2(h->tc), sizeof(double),
+                             cudaMemcpyDeviceToDevice, h->st));
+    ENMF_TRY(ar(h, h->dscal + S_XQNORM2, 1, CommOp::Sum));
   }
   const char* tpe = getenv("ENMF_TC_PBCD");   // diagnostics: 0 keeps the SIMT fp64 PBCD
   h->tc_pbcd = prec == ENMF_PREC_TC && tc_pbcd_supported((int)h->r) && !(tpe && tpe[0] == '0');
@@ -841,7 +858,7 @@ enmf_status_t enmf_objective(enmf_handle_t h, const float* U, int64_t ldu, const
     ENMF_TRY(ar(h, f, 1, CommOp::Sum));
   } else {
     ENMF_TRY(contract_xtu(h, U, ldu, h->Q));
-    ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh));
+    ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh, qgram_scales(h)));
     double* gv = h->work + h->work_elems - (size_t)(h->r * h->r);
     GemmOut o;
     o.C = gv;
@@ -849,7 +866,7 @@ enmf_status_t enmf_objective(enmf_handle_t h, const float* U, int64_t ldu, const
     gemm<float, float>(true, V, ldv, V, ldv, h->r, h->r, h->n, o, h->work,
                        h->work_elems - (size_t)(h->r * h->r), h->st);
     dot_f64_f32(h->Q, V, ldv, h->n, h->r, h->parts, h->dscal + S_CROSS, h->st);
-    objective_finish(h->dscal + S_XNORM2, h->dscal + S_CROSS, h->GU, gv, (int)h->r, f, h->st);
+    objective_finish(xnorm2_trace(h), h->dscal + S_CROSS, h->GU, gv, (int)h->r, f, h->st);
   }
   CUDA_TRY(cudaMemcpyAsync(f_host, f, sizeof(double), cudaMemcpyDeviceToHost, h->st));
   CUDA_TRY(cudaStreamSynchronize(h->st));
@@ -868,7 +885,7 @@ enmf_status_t enmf_kkt_residual(enmf_handle_t h, const float* U, int64_t ldu, co
   // grad_U f = U G_V - X V ; grad_V f = V G_U - X^T U
   ENMF_TRY(contract_xv(h, V, ldv, h->P));
   ENMF_TRY(contract_xtu(h, U, ldu, h->Q));
-  ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh));
+  ENMF_TRY(gram_f32(h, U, ldu, h->m_loc, h->GU, sh, qgram_scales(h)));
   double* gv = h->GV;   // recomputed at the next enmf_iterate entry
   ENMF_TRY(gram_f32(h, V, ldv, h->n, gv, false));
   const int np = kkt_parts();

@@ -158,9 +158,13 @@ enmf_status_t svd_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t
   gaussian_fill(Om, n, l, h->opt.seed, h->st);
   GemmOut o;
   o.ldc = l;
-  // the 2q + 2 X passes: on the tensor-core path as exact int8-digit products in blocks of
-  // <= 128 columns (tc_xf, ~1e-9 relative), else the SIMT fp64-accumulating GEMM
-  auto xprod = [&](bool trans, const double* F, double* out) -> enmf_status_t {
+  // the 2q + 2 X passes: the range finder's on the tensor-core path as int8-digit products in
+  // blocks of <= 128 columns (tc_xf; any basis that captures the range serves, so its ~2^-22
+  // operand rounding is harmless), else -- and for the final Rayleigh-Ritz pass B^T = X^T Q,
+  // which fixes sigma and the factors (X's 2^-22 rounding alone moves the balanced factors of
+  // a C5-shape problem by 1e-5, tools/digit_sim.py) -- the SIMT fp64-accumulating GEMM on the
+  // caller's fp32 X
+  auto xprod = [&](bool trans, const double* F, double* out, bool exact = false) -> enmf_status_t {
     if (h->sparse) {                 // CSR / CSC SpMM in fp64 (kernels_sparse.cu)
       if (trans)
         spmm<double>(h->csc_ptr, h->csc_row, h->csc_val, n, F, l, l, out, l, h->st);
@@ -168,7 +172,7 @@ enmf_status_t svd_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t
         spmm<double>(h->csr_ptr, h->csr_col, h->csr_val, mr, F, l, l, out, l, h->st);
       return ENMF_OK;
     }
-    if (h->tc) {
+    if (h->tc && !exact) {
       const int rc = tc_xf(h->tc, trans, F, l, l, out, l, h->st);
       return rc == 0 ? ENMF_OK : (rc == 2 ? ENMF_ERR_OOM : ENMF_ERR_CUDA);
     }
@@ -191,7 +195,7 @@ enmf_status_t svd_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t
     ENMF_TRY(cholqr(h, Y, tmp, mr, l, sh, G, R, Rinv, bad));
   }
   // B^T = X^T Q (n x l); B B^T = Qt^T Qt = Ve diag(s) Ve^T; sigma = sqrt(s)
-  ENMF_TRY(xprod(true, Y, Qt));
+  ENMF_TRY(xprod(true, Y, Qt, true));
   ENMF_TRY(ar(h, Qt, (size_t)(n * l), CommOp::Sum));
   o.C = G;
   gemm<double, double>(true, Qt, l, Qt, l, l, l, n, o, h->work, h->work_elems, h->st);

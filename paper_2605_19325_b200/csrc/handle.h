@@ -16,7 +16,9 @@ namespace enmf {
 // device scalar slots (doubles)
 enum {
   S_XNORM2 = 0, S_XMIN, S_XBAD, S_MINU, S_MINV, S_CROSS, S_LAMU, S_LAMV, S_NEG, S_SCRATCH,
-  S_WMAX, S_STEP, S_COUNT = 16
+  S_WMAX, S_STEP,
+  S_XQNORM2,   // ||X~||^2 of the tensor-core path's quantised X (trace-form objective)
+  S_COUNT = 16
 };
 // device int slots
 enum { I_STAGE = 0, I_KSTAR_U, I_KSTAR_V, I_CNT_ASC, I_CNT_HALS, I_BAD, I_HALS_FB, I_HALS_ILL, I_COUNT = 8 };
@@ -136,7 +138,16 @@ enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* 
 enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q,
                            const unsigned long long* umax = nullptr, bool slice = false);
 enmf_status_t gram_f32(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, double* G,
-                       bool sharded);
+                       bool sharded, const double* qscale = nullptr);
+// Tensor-core path: the digit scales of the factor the last X pass packed (for the Gram of the
+// quantised factor), else null.  The trace-form objective's ||X||^2 term: ||X~||^2 of the
+// quantised X on the tensor-core path (tc_gemm.cu), else ||X||^2.
+inline const double* qgram_scales(enmf_handle_t h) {
+  return h->tc && !h->sparse ? tc_factor_scales(h->tc) : nullptr;
+}
+inline const double* xnorm2_trace(enmf_handle_t h) {
+  return h->dscal + (h->tc && !h->sparse ? S_XQNORM2 : S_XNORM2);
+}
 enmf_status_t min_factor(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, int slot,
                          bool sharded);
 enmf_status_t validate_ld(const void* p, int64_t ld, int64_t cols);

@@ -37,10 +37,12 @@ void gemm(bool transA, const TA* A, int64_t lda, const TB* B, int64_t ldb, int64
 
 // G = A^T A (r x r fp64, ld r) of an fp32 rows x r matrix, upper-triangle tiles, fixed-order
 // reduction of per-SM partials: parts >= gram_parts() * 128^2 doubles, Gu >= 128^2.
+// qscale (device, r powers of two, may be null): Gram of the quantised A, entries
+// rint(a s 2^15) / (s 2^15) -- the operand the tensor-core X pass multiplied.
 bool gram_supported(int r);
 int gram_parts();
 void gram_sym(const float* A, int64_t lda, int64_t rows, int r, double* parts, double* Gu,
-              double* G, cudaStream_t st);
+              double* G, cudaStream_t st, const double* qscale = nullptr);
 
 // Deterministic sum of `parts` contiguous blocks of `len` doubles into out.
 void reduce_parts(const double* parts, int nparts, int64_t len, double* out, cudaStream_t st);

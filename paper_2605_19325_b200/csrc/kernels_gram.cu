@@ -3,6 +3,10 @@
 // objective).  The objective's third term <G_U, G_V> is ~||X||^2 while f can be ~3e-8 of it, so
 // the Grams stay fp64-exact products of the fp32 entries (no digit split here).
 //
+// With qscale (the tensor-core path's digit scales of the factor, tc_factor_scales) the Gram
+// is that of the quantised factor the X pass multiplied, so that the trace-form objective is
+// ||X~ - U~ V^T||^2 of the same operands (tc_gemm.cu).
+//
 // Only the upper triangle is computed: the 128 x 128 output is a 16 x 16 grid of 8 x 8 tiles,
 // and the 136 tiles with ti <= tj go to 136 threads (64 fp64 accumulators each).  Rows are
 // split across a persistent grid (two CTAs per SM); a CTA stages 32 rows at a time in shared
@@ -19,7 +23,7 @@ constexpr int kGramLd = 128 + 2;             // padded fp64 row stride
 
 __global__ void __launch_bounds__(kGramThreads, 2)
 gram_upper_kernel(const float* __restrict__ A, int64_t lda, int64_t rows, int r,
-                  double* __restrict__ parts) {
+                  const double* __restrict__ qscale, double* __restrict__ parts) {
   __shared__ __align__(16) double S[kGramRows * kGramLd];
   const int tid = threadIdx.x;
   // tile t -> (ti, tj), ti <= tj, row-major over the upper triangle
@@ -47,7 +51,13 @@ gram_upper_kernel(const float* __restrict__ A, int64_t lda, int64_t rows, int r,
     for (int e = tid; e < kGramRows * 128; e += blockDim.x) {
       const int i = e >> 7, c = e & 127;
       const int64_t row = base + i;
-      S[i * kGramLd + c] = (row < r1 && c < r) ? (double)A[row * lda + c] : 0.0;
+      double v = (row < r1 && c < r) ? (double)A[row * lda + c] : 0.0;
+      if (qscale && c < r) {
+        // the value the tensor-core X pass multiplies: rint(v s 2^15) / (s 2^15), s = 2^k
+        const double s = qscale[c] * 32768.0;
+        v = rint(v * s) / s;
+      }
+      S[i * kGramLd + c] = v;
     }
     __syncthreads();
     if (tile_on) {
@@ -99,8 +109,8 @@ int gram_parts() { return kGramGrid; }
 bool gram_supported(int r) { return r >= 1 && r <= 128; }
 
 void gram_sym(const float* A, int64_t lda, int64_t rows, int r, double* parts, double* Gu,
-              double* G, cudaStream_t st) {
-  gram_upper_kernel<<<kGramGrid, kGramThreads, 0, st>>>(A, lda, rows, r, parts);
+              double* G, cudaStream_t st, const double* qscale) {
+  gram_upper_kernel<<<kGramGrid, kGramThreads, 0, st>>>(A, lda, rows, r, qscale, parts);
   reduce_parts(parts, kGramGrid, 128 * 128, Gu, st);
   gram_mirror_kernel<<<(r * r + 255) / 256, 256, 0, st>>>(Gu, r, G);
   count_launch(2);

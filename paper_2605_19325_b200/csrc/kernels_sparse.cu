@@ -117,9 +117,11 @@ __global__ void csc_gather_kernel(const int32_t* __restrict__ perm, const int32_
   }
 }
 
-// column indices in range and ascending within each row (the layout the paths assume)
+// column indices in range and ascending within each row, row_ptr[0] = 0 and
+// row_ptr[rows] = nnz (the layout the paths assume: every stored entry belongs to a row)
 __global__ void csr_check_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
                                  int64_t rows, int64_t n, int64_t nnz, int* bad) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (ptr[0] != 0 || ptr[rows] != nnz)) atomicOr(bad, 1);
   for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < rows;
        row += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e0 = ptr[row], e1 = ptr[row + 1];

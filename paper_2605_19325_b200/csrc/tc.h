@@ -1,12 +1,13 @@
 // tc.h -- tensor-core (tcgen05) contraction path for large X.
 //
-// X is repacked once (enmf_set_data) into a handle-owned copy of four balanced base-2^7 int8
-// digit planes (4 bytes per element, power-of-two row scales), laid out in UMMA canonical tiles
-// that bulk copies move straight into shared memory (plus a K-major copy of X^T for pass 2 when
-// memory allows).  The two X passes of a sweep run as tcgen05.mma kind::i8 with exact int32
-// accumulation in TMEM (digit products grouped into 3 or 4 weight classes), combined exactly in
-// fp64 by the epilogue.  The ascent stage's PBCD (Alg. 2) runs its two r x r products per
-// inner iteration the same way (tc_pbcd.cu).
+// X is repacked once (enmf_set_data) into a handle-owned copy of three int8 digit planes
+// (mixed radix 8/8/7) (3 bytes per element, a power-of-two scale per X row), laid out in UMMA
+// canonical tiles that bulk copies move straight into shared memory, plus a K-major copy of
+// X^T (a scale per X column) for pass 2 when memory allows.  The two X passes of a sweep run
+// as tcgen05.mma kind::i8 with exact int32 accumulation in TMEM (six digit products in four
+// accumulators), combined exactly in fp64 by the epilogue (tc_gemm.cu).  The ascent stage's
+// PBCD (Alg. 2) and the HALS sweep run their r x r products the same way (tc_pbcd.cu, with
+// their own base-2^7 digits).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -17,10 +18,17 @@ struct TcState;
 
 // True when the shape is handled by the tensor-core kernels.
 bool tc_supported(int64_t rows, int64_t n, int64_t r);
-// Build the digit-plane copy of X (rows x n, ld).  Returns 0, 1 (CUDA error) or 2 (OOM).
-// xmax: max |X| of these rows if already known (x_stats), else < 0 to scan.
+// Build the digit-plane copies of X (rows x n, ld, X >= 0).  q2parts: device scratch of
+// q2cap >= 1 doubles (partials of ||X~||^2).  Returns 0, 1 (CUDA error) or 2 (OOM).
 int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t n, int64_t r,
-              cudaStream_t st, double xmax = -1.0);
+              cudaStream_t st, double* q2parts, int q2cap);
+// Device pointer to ||X~||^2 of the quantised X that pass 2 (Q = X^T U) reads: with it and
+// the Gram of the quantised U (tc_factor_scales) the trace-form objective is exactly
+// ||X~ - U~ V^T||^2.
+const double* tc_xq_norm2(const TcState* s);
+// Device pointer to the digit scales s_k (power of two, r entries) of the factor packed by the
+// last tc_xv / tc_xtu call: its quantised columns are rint(F s_k 2^15) / (s_k 2^15).
+const double* tc_factor_scales(const TcState* s);
 void tc_destroy(TcState* s);
 // P (rows x r fp64) = X V ; Q (n x r fp64) = X^T U  (this rank's rows only).  vmax / umax
 // (optional, device u64[r]): fp64 bits of the factor's column maxima |F| when the kernel that

@@ -7,33 +7,40 @@
 // which the HALS update amplifies ~r-fold past BASELINE's 1e-5.  This path uses
 // integer MMAs instead:
 //
-//   * Operands become four balanced base-2^7 int8 digits, a*s = d0 + d1/2^7 + d2/2^14 + d3/2^21
-//     with every digit in [-64, 64] and s a power of two (max|a| s in [32, 64): one scale for
-//     X, one per column for a factor).  That is 27 bits, so every fp32 entry >= max/8 of its
-//     scale group is represented EXACTLY (smaller ones to 2^-22 of the scale).  X is repacked
-//     ONCE (enmf_set_data) into 4 byte planes -- 4 bytes per element, exactly the algorithmic
-//     bytes of fp32 X; the factor is repacked per pass.
-//   * tcgen05.mma kind::i8 (M=128, N = r rounded to 16, K=32) accumulates exactly in int32 TMEM,
-//     one accumulator per digit weight class c = i + j <= 3:
-//         acc_c = sum_{i+j=c} A_i B_j      (10 products, 4 x 128 TMEM columns)
-//     issued as 6 MMAs per 32-deep k-step: B planes of two classes are paired into one N = 2r
-//     MMA writing adjacent accumulators (MmaList<4>), halving the A-operand smem reads that ncu
-//     showed to limit the 10-MMA form.  Pass 1 with n >= 8192 uses 3 classes (6 products, 4
-//     MMAs, 3 X planes read).  The epilogue forms acc0 + acc1 2^-7 + acc2 2^-14 + acc3 2^-21
-//     EXACTLY in fp64 (31 integer + 21 fractional bits) before applying 1/(s_X s_k).  The only
-//     errors are the omitted low-weight products and sub-threshold digit truncation: P and Q
-//     come out accurate to ~1e-9 relative, which the trace-form objective needs near the
-//     optimum (||X||^2 / f ~ 3e7 at C5, SURVEY Hard part 2).
+//   * Operands become three int8 digits in mixed radix (8, 8, 7), t = a s = d0 + d1/2^8 +
+//     d2/2^15 (t rounded to the 2^-15 grid, |d0| <= 126, d1 in [-128, 127], d2 symmetric in
+//     [-64, 64]: tc_ptx.cuh digits3_n) with s a power of two, max|a| s in [63, 126): one scale
+//     per ROW of X for P = X V (the output row), one per COLUMN of X for Q = X^T U (the output
+//     row of the transposed product), one per column of the factor.  22 bits relative to the
+//     scale group's maximum.  X is repacked ONCE (enmf_set_data) into 3 byte planes per copy --
+//     3 bytes per element, 3/4 of the fp32 X bytes; the factor is repacked per pass.
+//   * tcgen05.mma kind::i8 (M = 128, N = r rounded to 16, K = 32) accumulates exactly in int32
+//     TMEM.  The six products of weight >= 2^-16 are issued as 4 MMAs per 32-deep k-step into
+//     4 accumulators (4 x 128 TMEM columns), one per weight:
+//         acc0 = A0 B0 (1), acc1 = A0 B1 + A1 B0 (2^-8), acc2 = A1 B1 (2^-16),
+//         acc3 = A0 B2 + A2 B0 (2^-15)
+//     (B planes 0 and 1 are adjacent, so A0 [B0;B1] and A1 [B0;B1] are N = 2r MMAs writing
+//     adjacent accumulators; A1 [B0;B1] accumulates into acc1 and acc2 together, so the
+//     epilogue zeroes acc2 for the next unit; |acc| <= 2 * 126 * 128 * K < 2^31 for unit
+//     K <= 65536).  The epilogue forms acc0 + 2^-8 (acc1 + 2^-8 (acc2 + 2 acc3)) EXACTLY in
+//     fp64 (49 bits) and applies 1/(s_row s_col), a power of two.  The dropped products
+//     (weight 2^-23 and below) each contain a symmetric last digit: unbiased, ~2^-23 of |X||F|
+//     per term.  Measured in tools/digit_sim.py at a C5-recipe shape: Q ~6e-9 relative, one
+//     HALS V block ~4e-7 from the fp64 update; the trace-form objective is formed from the
+//     SAME quantised operands (||X~||^2 of the pass-2 copy, the Gram of the quantised U:
+//     tc_xq_norm2, tc_factor_scales) so it equals ||X~ - U~ V^T||^2 up to the dropped
+//     products' noise, and its error does not scale with ||X||^2 / f.
 //   * Layout: tiles of 128 rows x 64 columns per plane in the UMMA no-swizzle canonical layout,
 //     core matrix (g, kc) at byte (kc*16 + g)*128 (8 rows x 16 bytes): a K-major A operand for
 //     P = X V (SBO 128 B, LBO 2048 B).  Q = X^T U reads a second packed copy of X^T in the same
 //     K-major layout (mode 2); without it (ENMF_TC_XT=0 or not enough memory) the X copy is
 //     gathered as an MN-major A operand (mode 1: two column-adjacent tiles give 8 MN groups at a
-//     uniform 2048 B stride, 1 KB bulk copies into SBO 1024 B / LBO 128 B), ~40 % slower.
-//   * Warp roles: warp 0 = producer (cp.async.bulk into a 3-stage ring -- 4 with 3 planes --,
-//     mbarrier complete_tx), warp 1 = TMEM allocator + single-thread MMA issuer, warps 2..9 =
-//     epilogue.  Persistent grid, one CTA per SM.  Units: pass 1 = one 128-row band over all of
-//     K; pass 2 = one 128-column band over a K range (split-K, fixed-order fp64 reduction).
+//     uniform 2048 B stride, 1 KB bulk copies into SBO 1024 B / LBO 128 B), ~40 % slower; the
+//     X copy then uses one scale for all rows (a per-row scale would vary along K).
+//   * Warp roles: warp 0 = producer (cp.async.bulk into a 4-stage ring, mbarrier complete_tx),
+//     warp 1 = TMEM allocator + single-thread MMA issuer, warps 2..9 = epilogue.  Persistent
+//     grid, one CTA per SM.  Units: pass 1 = one 128-row band over all of K; pass 2 = one
+//     128-column band over a K range (split-K, fixed-order fp64 reduction).
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -50,16 +57,18 @@ namespace tci {
 
 constexpr int BM = 128;
 constexpr int BK = 64;                          // K elements (= bytes) per stage per row
-constexpr int STAGES = 3;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 32 * (2 + EPI_WARPS);
-constexpr int PLANES = 4;
+constexpr int PLANES = 3;                       // digit planes of X and of the factor
+constexpr int NACC = 4;                         // TMEM accumulators
 constexpr int TILE_A = BM * BK;                 // bytes per X tile per plane (8 KB)
 constexpr int MAX_TILE_B = 128 * BK;            // bytes per factor tile per plane (<= 8 KB)
-constexpr int STAGE_BYTES = PLANES * TILE_A + PLANES * MAX_TILE_B;   // 64 KB
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;
+constexpr int STAGE_BYTES = PLANES * TILE_A + PLANES * MAX_TILE_B;   // 48 KB
+constexpr int NST = 4;                          // pipeline stages
+constexpr int SMEM_BYTES = NST * STAGE_BYTES + 1024;
 constexpr int TMEM_COLS = 512;                  // 4 x 128
-constexpr int64_t MAX_UNIT_K = 65536;           // |acc3| <= 4 * 64 * 64 * K < 2^31
+constexpr int64_t MAX_UNIT_K = 65536;           // |acc| <= 2 * 126 * 128 * K < 2^31
+constexpr double TOP = 126.0;                   // max |t| of a scale group (digits3_n bound)
 
 struct Params {
   const int8_t* xp[PLANES];
@@ -69,7 +78,8 @@ struct Params {
   double* out;
   int64_t out_ld;
   int64_t split_stride;
-  const double* colscale;    // r values: 1 / (s_X * s_k)
+  const double* colscale;    // r values: 1 / s_k of the factor column
+  const double* rowinv;      // out_rows values: 1 / s of the X row (mode 0) / column (1, 2)
   int mode;                  // 0: P = X V ; 1: Q = X^T U (MN-major gather) ; 2: Q from X^T copy
   int num_units;
   int ksplit;
@@ -93,53 +103,43 @@ __device__ __forceinline__ void unit_range(const Params& p, int u, int& tile, in
   if (s1 < s0) s1 = s0;
 }
 
-// Digit products A_i B_j with i + j < NCLS issued as MMAs {a-plane, first b-plane, first
-// accumulator, wide}.  A wide MMA multiplies A_i by two adjacent planes [B_j; B_j+1] (N = 2 rp)
-// into the adjacent accumulators acc_{i+j} | acc_{i+j+1}, so each A plane is read from shared
-// memory fewer times (the SS-MMA is smem-bandwidth bound).  The first MMAs of a list
-// initialise every accumulator at the start of a unit (`fresh`).
-//   NCLS = 4 (10 products, 6 MMAs): A0[B0;B1] A0[B2;B3] A1[B0;B1] A1 B2 A2[B0;B1] A3 B0
-//   NCLS = 3 ( 6 products, 4 MMAs): A0[B0;B1] A0 B2 A1[B0;B1] A2 B0
-//   LIST 7   ( 7 products, 5 MMAs): classes <= 2 plus A3 B0 of class 3 -- the X digit that
-//            carries the low bits of entries far below max|X| against the factor's leading
-//            digit; the dropped A0 B3, A1 B2, A2 B1 involve the factor's low digits only
-//            (per-column scales), B plane 3 is not read.  4 accumulators.
-// NPA / NPB: digit planes of A / B staged per k-step; NCLS: accumulators (weight classes).
-template <int LIST> struct MmaList;
-template <> struct MmaList<4> {
-  static constexpr int N = 6, FRESH = 2, NCLS = 4, NPA = 4, NPB = 4;
+// The six digit products of weight >= 2^-16, issued per 32-deep k-step as 4 MMAs
+// {a-plane, first b-plane, accumulator, wide}.  A wide MMA multiplies A_i by the adjacent
+// planes [B0; B1] (N = 2 rp) into the adjacent accumulators acc_c | acc_c+1.  The first FRESH
+// MMAs of a unit initialise acc0|acc1 and acc3; acc2 (written only by the accumulating wide
+// A1 [B0;B1]) is zeroed by the epilogue before the unit (ZERO_ACC).
+struct Mma {
+  static constexpr int N = 4, FRESH = 2, ZERO_ACC = 2;
   __device__ static __forceinline__ int t(int q, int f) {
-    constexpr int tab[6][4] = {{0, 0, 0, 1}, {0, 2, 2, 1}, {1, 0, 1, 1},
-                               {1, 2, 3, 0}, {2, 0, 2, 1}, {3, 0, 3, 0}};
-    return tab[q][f];
-  }
-};
-template <> struct MmaList<3> {
-  static constexpr int N = 4, FRESH = 2, NCLS = 3, NPA = 3, NPB = 3;
-  __device__ static __forceinline__ int t(int q, int f) {
-    constexpr int tab[4][4] = {{0, 0, 0, 1}, {0, 2, 2, 0}, {1, 0, 1, 1}, {2, 0, 2, 0}};
-    return tab[q][f];
-  }
-};
-template <> struct MmaList<7> {
-  // the first FRESH entries initialise acc0|acc1, acc2, acc3
-  static constexpr int N = 5, FRESH = 3, NCLS = 4, NPA = 4, NPB = 3;
-  __device__ static __forceinline__ int t(int q, int f) {
-    constexpr int tab[5][4] = {{0, 0, 0, 1}, {0, 2, 2, 0}, {3, 0, 3, 0}, {1, 0, 1, 1},
-                               {2, 0, 2, 0}};
+    constexpr int tab[4][4] = {{0, 0, 0, 1}, {0, 2, 3, 0}, {2, 0, 3, 0}, {1, 0, 1, 1}};
     return tab[q][f];
   }
 };
 
-template <int LIST>
+// acc0 + 2^-8 (acc1 + 2^-8 (acc2 + 2 acc3)), exact in fp64 (|acc| < 2^31: <= 49 bits)
+__device__ __forceinline__ double combine(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3) {
+  const double lo = (double)(int)v2 + 2.0 * (double)(int)v3;
+  return (double)(int)v0 + ((double)(int)v1 + lo * 0x1p-8) * 0x1p-8;
+}
+
+// Zero the rows (TMEM lanes 32 q .. 32 q + 31) x columns [64 hcol, 64 hcol + 64) of the
+// accumulator ZERO_ACC that this epilogue warp owns, before the MMAs of the next unit.
+__device__ __forceinline__ void zero_acc_slice(uint32_t tmem_base, int q, int hcol, int rp) {
+  const uint32_t lane_addr = tmem_base + ((uint32_t)(32 * q) << 16);
+#pragma unroll 1
+  for (int h = 0; h < 4; ++h) {
+    const int c0 = 64 * hcol + 16 * h;
+    if (c0 >= rp) break;
+    TMEM_ST16_ZERO(lane_addr + Mma::ZERO_ACC * rp + c0);
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
-  using L = MmaList<LIST>;
-  constexpr int NCLS = L::NCLS, NPA = L::NPA, NPB = L::NPB;
-  constexpr int STAGE = NPA * TILE_A + NPB * MAX_TILE_B;
-  constexpr int NST = (SMEM_BYTES - 1024) / STAGE;            // 3 (4 planes) or 4 (3 planes)
+  constexpr int STAGE = STAGE_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t bars[2 * 4 + 2];
+  __shared__ __align__(8) uint64_t bars[2 * NST + 2];
   __shared__ uint32_t tmem_base_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_full = smem_u32(&bars[0]);
@@ -168,6 +168,10 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
+  if (warp >= 2) zero_acc_slice(tmem_base, warp & 3, (warp - 2) >> 2, p.rp);   // first unit
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   if (warp == 0) {
     // ===================== producer: the whole warp issues a stage's bulk copies =====================
@@ -179,17 +183,17 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
       for (int ks = s0; ks < s1; ++ks) {
         mbar_wait(bar_empty + 8 * stage, phase ^ 1);
         const uint32_t fb = bar_full + 8 * stage;
-        if (lane == 0) mbar_expect_tx(fb, NPA * TILE_A + NPB * tile_b);
+        if (lane == 0) mbar_expect_tx(fb, PLANES * TILE_A + PLANES * tile_b);
         __syncwarp();
         const uint32_t st = smem_u32(smem + (size_t)stage * STAGE);
         if (p.mode == 0) {
-          // the NPA planes of a tile are contiguous: one bulk copy
+          // the planes of a tile are contiguous: one bulk copy
           const int64_t off = ((int64_t)tile * p.tiles_per_row + ks) * PLANES * TILE_A;
-          if (lane < NPA) bulk_g2s(st + lane * TILE_A, p.xp[lane] + off, TILE_A, fb);
+          if (lane == 0) bulk_g2s(st, p.xp[0] + off, PLANES * TILE_A, fb);
         } else if (p.mode == 2) {
           // A = X^T from the transposed packed copy: K-major tiles
           const int64_t off = ((int64_t)tile * p.tiles_per_row_t + ks) * PLANES * TILE_A;
-          if (lane < NPA) bulk_g2s(st + lane * TILE_A, p.xtp[lane] + off, TILE_A, fb);
+          if (lane == 0) bulk_g2s(st, p.xtp[0] + off, PLANES * TILE_A, fb);
         } else {
           // A = X^T: output rows j = column tiles 2*tile, 2*tile+1 of row band ks/2; the K stage
           // is the 64-row half (ks & 1) of that band: 8 chunks of 1 KB per plane, one per lane
@@ -199,21 +203,21 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
           const int64_t src = (band * p.tiles_per_row + 2 * tile + t) * PLANES * TILE_A +
                               (int64_t)(kc * 16 + 8 * half) * 128;
           const uint32_t dst = (uint32_t)((t * 4 + kc) * 1024);
-          for (int pl = lane >> 3; pl < NPA; pl += 4)
+          for (int pl = lane >> 3; pl < PLANES; pl += 4)
             bulk_g2s(st + pl * TILE_A + dst, p.xp[pl] + src, 1024, fb);
         }
+        // the factor planes of a stage are contiguous too
         const int64_t foff = (int64_t)ks * PLANES * tile_b;
-        if (lane >= 28 && lane - 28 < NPB)
-          bulk_g2s(st + NPA * TILE_A + (lane - 28) * tile_b, p.fp[lane - 28] + foff, tile_b, fb);
+        if (lane == 31) bulk_g2s(st + PLANES * TILE_A, p.fp[0] + foff, PLANES * tile_b, fb);
         if (++stage == NST) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
-      // idesc: S32 accumulate (c_format 2), signed int8 A and B, A K-major (mode 0) or
+      // idesc: S32 accumulate (c_format 2), signed int8 A and B, A K-major (mode 0, 2) or
       // MN-major (mode 1), B K-major, M = 128, N = rp (one digit plane) or 2 rp (two planes)
-      const bool mn = p.mode == 1;               // A MN-major (X^T gathered from the X copy)
+      const bool mn = p.mode == 1;
       const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)mn << 15) |
                                   ((uint32_t)(BM >> 4) << 24);
       const uint32_t idesc1 = idesc_base | ((uint32_t)(p.rp >> 3) << 17);
@@ -236,15 +240,15 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
           mbar_wait(bar_full + 8 * stage, phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem + (size_t)stage * STAGE);
-          const uint32_t b0 = a0 + NPA * TILE_A;
+          const uint32_t b0 = a0 + PLANES * TILE_A;
 #pragma unroll
           for (int j = 0; j < BK / 32; ++j) {
 #pragma unroll
-            for (int q = 0; q < L::N; ++q) {
-              const int pa = L::t(q, 0), pb = L::t(q, 1), ac = L::t(q, 2), wide = L::t(q, 3);
+            for (int q = 0; q < Mma::N; ++q) {
+              const int pa = Mma::t(q, 0), pb = Mma::t(q, 1), ac = Mma::t(q, 2), wide = Mma::t(q, 3);
               const uint64_t ad = umma_desc(a0 + pa * TILE_A + j * a_kstep, a_lbo, a_sbo);
               const uint64_t bd = umma_desc(b0 + pb * tile_b + j * b_kstep, b_lbo, b_sbo);
-              const bool fresh = ks == s0 && j == 0 && q < L::FRESH;
+              const bool fresh = ks == s0 && j == 0 && q < Mma::FRESH;
               tc_mma_i8(tmem_base + ac * rpc, ad, bd, wide ? idesc2 : idesc1, fresh ? 0u : 1u);
             }
           }
@@ -270,30 +274,26 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
       tc_fence_after();
       const int64_t row = (int64_t)tile * BM + row_in_tile;
       double* o = p.out + (int64_t)split * p.split_stride + row * p.out_ld;
+      const double rinv = row < p.out_rows ? p.rowinv[row] : 0.0;
       const uint32_t lane_addr = tmem_base + ((uint32_t)(32 * q) << 16);
 #pragma unroll 1
       for (int h = 0; h < 4; ++h) {
         const int c0 = 64 * hcol + 16 * h;
         if (c0 >= p.rp) break;
-        uint32_t v[NCLS][16];
+        uint32_t v[NACC][16];
 #pragma unroll
-        for (int c = 0; c < NCLS; ++c) TMEM_LD16(lane_addr + c * p.rp + c0, v[c]);
+        for (int c = 0; c < NACC; ++c) TMEM_LD16(lane_addr + c * p.rp + c0, v[c]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (row < p.out_rows) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int col = c0 + i;
-            if (col < p.r) {
-              // exact in fp64: |acc_c| < 2^31, at most 21 fractional bits in total
-              double acc = 0.0;
-#pragma unroll
-              for (int c = NCLS - 1; c >= 0; --c)
-                acc = acc * 0x1p-7 + (double)(int)v[c][i];
-              o[col] = acc * p.colscale[col];
-            }
+            if (col < p.r)       // 1/(s_row s_col) is a power of two: one rounding
+              o[col] = combine(v[0][i], v[1][i], v[2][i], v[3][i]) * (p.colscale[col] * rinv);
           }
         }
       }
+      zero_acc_slice(tmem_base, q, hcol, p.rp);   // acc2 starts at 0 for the next unit
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_tempty);
@@ -312,25 +312,20 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
 // ------------------------------------------------------------------ CTA-pair kernel
 // cta_group::2: a cluster of two CTAs (two SMs of a TPC) computes a 256-row output band with
 // M = 256 MMAs issued by the even CTA.  Each CTA stages its own 128 rows of A (X or X^T digits,
-// tile 2 t + rank) and HALF of every B operand, at the same shared-memory offsets: for a wide
-// MMA [B_j; B_j+1] (N = 2 rp) CTA 0 holds plane j and CTA 1 plane j+1; for a narrow one (N = rp)
-// each holds rp/2 rows of the plane (a contiguous half of the canonical tile).  Per SM this
-// halves the B-operand shared-memory reads that co-limit the single-CTA kernel (ncu: smem tc
-// wavefronts 75 %), so the tensor pipe can run at its full int8 rate.
+// tile 2 t + rank) and HALF of every B operand, at the same shared-memory offsets: for the wide
+// MMA [B0; B1] (N = 2 rp) CTA 0 holds plane 0 and CTA 1 plane 1; for a narrow one (B2, B0) each
+// holds rp/2 rows of the plane (a contiguous half of the canonical tile).  Per SM this halves
+// the B-operand shared-memory reads.
 // Synchronisation: each CTA's producer fills its own stage (cp.async.bulk, local mbarrier);
 // CTA 1's idle MMA warp relays its stage completion to the leader (remote mbarrier arrive);
 // the leader's commits are multicast to both CTAs (stage empty, accumulators full); both CTAs'
 // epilogues release the accumulators on the leader's barrier.
 constexpr int PAIR_SMEM = 230400;
 
-template <int NCLS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc_i8_pair_kernel(const Params p) {
-  constexpr int NPL = NCLS;
-  constexpr int NWIDE = NCLS == 4 ? 2 : 1;                        // wide B regions
-  constexpr int STAGE = NPL * TILE_A + (NWIDE + 1) * MAX_TILE_B;  // A planes | wide | 2 halves
-  constexpr int NST = (PAIR_SMEM - 1024) / STAGE;                 // 4 (4 planes) or 5 (3 planes)
-  using L = MmaList<NCLS>;
+  constexpr int STAGE = PLANES * TILE_A + 2 * MAX_TILE_B;         // A planes | [B0|B1] | 2 halves
+  constexpr int PNST = (PAIR_SMEM - 1024) / STAGE;                // 5
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t bars[3 * 8 + 2];
@@ -339,16 +334,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const uint32_t rank = cluster_rank();
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const uint32_t bar_full = smem_u32(&bars[0]);
-  const uint32_t bar_empty = smem_u32(&bars[NST]);
-  const uint32_t bar_peer = smem_u32(&bars[2 * NST]);       // leader: CTA 1's stage is full
-  const uint32_t bar_tfull = smem_u32(&bars[3 * NST]);
-  const uint32_t bar_tempty = smem_u32(&bars[3 * NST + 1]);  // leader: both epilogues drained
+  const uint32_t bar_empty = smem_u32(&bars[PNST]);
+  const uint32_t bar_peer = smem_u32(&bars[2 * PNST]);       // leader: CTA 1's stage is full
+  const uint32_t bar_tfull = smem_u32(&bars[3 * PNST]);
+  const uint32_t bar_tempty = smem_u32(&bars[3 * PNST + 1]);  // leader: both epilogues drained
   const uint32_t tile_b = (uint32_t)p.rp * BK;
   const uint32_t half_b = tile_b / 2;
-  const uint32_t b_bytes = NWIDE * tile_b + 2 * half_b;
+  const uint32_t b_bytes = tile_b + 2 * half_b;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) {
+    for (int s = 0; s < PNST; ++s) {
       mbar_init(bar_full + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, 1);
       mbar_init(bar_peer + 8 * s, 1);
@@ -369,6 +364,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
+  if (warp >= 2) zero_acc_slice(tmem_base, warp & 3, (warp - 2) >> 2, p.rp);   // first unit
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
 
   if (warp == 0) {
     // ===================== producer (both CTAs): own A rows, own half of B =====================
@@ -381,31 +381,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int ks = s0; ks < s1; ++ks) {                       // the last one; not stored
         mbar_wait(bar_empty + 8 * stage, phase ^ 1);
         const uint32_t fb = bar_full + 8 * stage;
-        if (lane == 0) mbar_expect_tx(fb, NPL * TILE_A + b_bytes);
+        if (lane == 0) mbar_expect_tx(fb, PLANES * TILE_A + b_bytes);
         __syncwarp();
         const uint32_t st = smem_u32(smem + (size_t)stage * STAGE);
         if (lane == 0) {
           const int8_t* src =
               p.mode == 0 ? p.xp[0] + ((int64_t)tile * p.tiles_per_row + ks) * PLANES * TILE_A
                           : p.xtp[0] + ((int64_t)tile * p.tiles_per_row_t + ks) * PLANES * TILE_A;
-          bulk_g2s(st, src, NPL * TILE_A, fb);
+          bulk_g2s(st, src, PLANES * TILE_A, fb);
         }
         const int64_t foff = (int64_t)ks * PLANES * tile_b;
-        const uint32_t bst = st + NPL * TILE_A;
+        const uint32_t bst = st + PLANES * TILE_A;
         if (lane == 28) bulk_g2s(bst, p.fp[rank] + foff, tile_b, fb);                  // B0|B1
-        if (NWIDE == 2 && lane == 29)
-          bulk_g2s(bst + tile_b, p.fp[2 + rank] + foff, tile_b, fb);                   // B2|B3
         if (lane == 30)                                                                // B2 half
-          bulk_g2s(bst + NWIDE * tile_b, p.fp[2] + foff + rank * half_b, half_b, fb);
+          bulk_g2s(bst + tile_b, p.fp[2] + foff + rank * half_b, half_b, fb);
         if (lane == 31)                                                                // B0 half
-          bulk_g2s(bst + NWIDE * tile_b + half_b, p.fp[0] + foff + rank * half_b, half_b, fb);
-        if (++stage == NST) { stage = 0; phase ^= 1; }
+          bulk_g2s(bst + tile_b + half_b, p.fp[0] + foff + rank * half_b, half_b, fb);
+        if (++stage == PNST) { stage = 0; phase ^= 1; }
       }
     }
     // drain: the leader's last commits arrive on this CTA's empty barriers before it exits
-    for (int i = 0; i < NST; ++i) {
+    for (int i = 0; i < PNST; ++i) {
       mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-      if (++stage == NST) { stage = 0; phase ^= 1; }
+      if (++stage == PNST) { stage = 0; phase ^= 1; }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
@@ -430,24 +428,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           mbar_wait_cluster(bar_peer + 8 * stage, phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem + (size_t)stage * STAGE);
-          const uint32_t b0 = a0 + NPL * TILE_A;
+          const uint32_t b0 = a0 + PLANES * TILE_A;
 #pragma unroll
           for (int j = 0; j < BK / 32; ++j) {
 #pragma unroll
-            for (int q = 0; q < L::N; ++q) {
-              const int pa = L::t(q, 0), pb = L::t(q, 1), ac = L::t(q, 2), wide = L::t(q, 3);
-              // B region: wide [B0;B1] / [B2;B3] at 0 / tile_b; narrow B2 / B0 halves after them
-              const uint32_t breg = wide ? (pb == 0 ? 0u : tile_b)
-                                         : NWIDE * tile_b + (pb == 0 ? half_b : 0u);
+            for (int q = 0; q < Mma::N; ++q) {
+              const int pa = Mma::t(q, 0), pb = Mma::t(q, 1), ac = Mma::t(q, 2), wide = Mma::t(q, 3);
+              // B region: wide [B0;B1] at 0; narrow B2 / B0 halves after it
+              const uint32_t breg = wide ? 0u : tile_b + (pb == 0 ? half_b : 0u);
               const uint64_t ad = umma_desc(a0 + pa * TILE_A + j * a_kstep, a_lbo, a_sbo);
               const uint64_t bd = umma_desc(b0 + breg + j * b_kstep, b_lbo, b_sbo);
-              const bool fresh = ks == s0 && j == 0 && q < L::FRESH;
+              const bool fresh = ks == s0 && j == 0 && q < Mma::FRESH;
               tc_mma_i8_pair(tmem_base + ac * rpc, ad, bd, wide ? idesc2 : idesc1,
                              fresh ? 0u : 1u);
             }
           }
           tc_commit_pair(bar_empty + 8 * stage, 3);     // frees the slot in both CTAs
-          if (++stage == NST) { stage = 0; phase ^= 1; }
+          if (++stage == PNST) { stage = 0; phase ^= 1; }
         }
         tc_commit_pair(bar_tfull, 3);                   // accumulators complete in both CTAs
         ++nunit;
@@ -463,7 +460,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int ks = s0; ks < s1; ++ks) {
           mbar_wait(bar_full + 8 * stage, phase);
           mbar_arrive_cluster(peer0 + 8 * stage);
-          if (++stage == NST) { stage = 0; phase ^= 1; }
+          if (++stage == PNST) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -485,29 +482,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const int64_t row = (int64_t)tile * BM + row_in_tile;
       const bool store = tile < p.tiles && row < p.out_rows;
       double* o = p.out + (int64_t)split * p.split_stride + row * p.out_ld;
+      const double rinv = store ? p.rowinv[row] : 0.0;
       const uint32_t lane_addr = tmem_base + ((uint32_t)(32 * q) << 16);
 #pragma unroll 1
       for (int h = 0; h < 4; ++h) {
         const int c0 = 64 * hcol + 16 * h;
         if (c0 >= p.rp) break;
-        uint32_t v[NCLS][16];
+        uint32_t v[NACC][16];
 #pragma unroll
-        for (int c = 0; c < NCLS; ++c) TMEM_LD16(lane_addr + c * p.rp + c0, v[c]);
+        for (int c = 0; c < NACC; ++c) TMEM_LD16(lane_addr + c * p.rp + c0, v[c]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (store) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int col = c0 + i;
-            if (col < p.r) {
-              double acc = 0.0;
-#pragma unroll
-              for (int c = NCLS - 1; c >= 0; --c)
-                acc = acc * 0x1p-7 + (double)(int)v[c][i];
-              o[col] = acc * p.colscale[col];
-            }
+            if (col < p.r)
+              o[col] = combine(v[0][i], v[1][i], v[2][i], v[3][i]) * (p.colscale[col] * rinv);
           }
         }
       }
+      zero_acc_slice(tmem_base, q, hcol, p.rp);   // acc2 starts at 0 for the next unit
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty0);
@@ -526,33 +520,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
 // ------------------------------------------------------------------ packing
 
-// X (rows x n, ld) * sx -> 4 digit planes of [Mt][tiles_per_row] tiles.  One thread writes one
-// 16-byte row chunk (16 consecutive columns) of each plane; consecutive threads read
-// consecutive chunks of an X row (coalesced reads).
-// 16 consecutive values (val(k), |val| < 64.5) -> the 16-byte chunks of the 4 digit planes,
-// w[plane][k / 4] byte k % 4, built in registers (no addressable local arrays).
+// 16 consecutive values t(k) (|t| < TOP) -> the 16-byte chunks of the 3 digit planes,
+// w[plane][k / 4] byte k % 4, built in registers (no addressable local arrays).  Returns
+// sum_k n_k^2 (n = rint(t 2^15), exact: < 2^49) for the norm of the quantised operand.
 template <typename F>
-__device__ __forceinline__ void pack_digits16(F val, uint32_t (&w)[4][4]) {
+__device__ __forceinline__ double pack_digits16(F val, uint32_t (&w)[PLANES][4]) {
 #pragma unroll
-  for (int pl = 0; pl < 4; ++pl)
+  for (int pl = 0; pl < PLANES; ++pl)
 #pragma unroll
     for (int q = 0; q < 4; ++q) w[pl][q] = 0u;
+  double n2 = 0.0;
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
-    const uint32_t dw = digits_word_sym(val(k));
+    const int n = __double2int_rn(val(k) * 32768.0);
+    n2 += (double)n * (double)n;
+    const uint32_t dw = digits3_n(n);
 #pragma unroll
-    for (int pl = 0; pl < 4; ++pl) w[pl][k >> 2] |= ((dw >> (8 * pl)) & 255u) << (8 * (k & 3));
+    for (int pl = 0; pl < PLANES; ++pl) w[pl][k >> 2] |= ((dw >> (8 * pl)) & 255u) << (8 * (k & 3));
+  }
+  return n2;
+}
+
+// Block sum of v (blockDim.x <= 1024, a multiple of 32) into *out by thread 0.
+__device__ __forceinline__ void block_sum_to(double v, double* out) {
+  __shared__ double red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) *out = v;
   }
 }
 
+// X (rows x n, ld) -> 3 digit planes of [Mt][tiles_per_row] tiles, row i scaled by
+// 1 / rinv[i] (a power of two).  One 128-row x 64-column tile at a time: coalesced row reads
+// into shared memory, then the tile's 512 16-byte chunks per plane in memory order (chunk
+// w = (kc*16 + g)*8 + ri), so the writes are contiguous too.  q2parts (optional, one per
+// block): sum of the squared quantised values, ||X~||^2 of this copy.
 __global__ void __launch_bounds__(256)
-pack_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n, double sx,
-              int64_t tiles_per_row, int64_t Mt, uint4* p0, uint4* p1, uint4* p2, uint4* p3) {
-  // one 128-row x 64-column tile at a time: coalesced row reads into shared memory, then the
-  // tile's 512 16-byte chunks per plane in memory order (chunk w = (kc*16 + g)*8 + ri), so the
-  // writes are contiguous too (the row-by-row form wrote 16 B per 2 KB stride)
+pack_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n,
+              const double* __restrict__ rinv, int64_t tiles_per_row, int64_t Mt, uint4* out,
+              double* q2parts) {
   __shared__ float tx[BM][BK + 1];
   const bool vec = (ldx & 3) == 0 && ((uintptr_t)X & 15) == 0;
+  double q2 = 0.0;
   for (int64_t t = blockIdx.x; t < Mt * tiles_per_row; t += gridDim.x) {
     const int64_t mt = t / tiles_per_row, kt = t - mt * tiles_per_row;
     __syncthreads();
@@ -580,25 +596,31 @@ pack_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n,
     for (int w = threadIdx.x; w < BM * BK / 16; w += blockDim.x) {
       const int kc = w >> 7, g = (w >> 3) & 15, ri = w & 7;
       const int il = g * 8 + ri;
-      uint32_t wd[4][4];
-      pack_digits16([&](int k) { return (double)tx[il][kc * 16 + k] * sx; }, wd);
+      const int64_t i = mt * BM + il;
+      const double s = i < rows ? 1.0 / rinv[i] : 0.0;        // exact: a power of two
+      uint32_t wd[PLANES][4];
+      const double n2 = pack_digits16([&](int k) { return (double)tx[il][kc * 16 + k] * s; }, wd);
+      if (i < rows) q2 += n2 * (rinv[i] * rinv[i]);
       // planes interleaved per tile: tile t, plane pl at (t * PLANES + pl) * TILE_A
       const int64_t idx = (t * PLANES * TILE_A) / 16 + w;
-      p0[idx] = make_uint4(wd[0][0], wd[0][1], wd[0][2], wd[0][3]);
-      p1[idx] = make_uint4(wd[1][0], wd[1][1], wd[1][2], wd[1][3]);
-      p2[idx] = make_uint4(wd[2][0], wd[2][1], wd[2][2], wd[2][3]);
-      p3[idx] = make_uint4(wd[3][0], wd[3][1], wd[3][2], wd[3][3]);
+#pragma unroll
+      for (int pl = 0; pl < PLANES; ++pl)
+        out[idx + pl * (TILE_A / 16)] = make_uint4(wd[pl][0], wd[pl][1], wd[pl][2], wd[pl][3]);
     }
   }
+  if (q2parts) block_sum_to(q2 * 0x1p-30, q2parts + blockIdx.x);
 }
 
 // X^T copy: tiles [jt][it] of 128 columns (j, the M side of Q = X^T U) x 64 rows (i, the K
-// side), K-major core matrices (kc*16 + g)*128 like pass 1's tiles.  A block stages a 64 x 128
-// block of X in shared memory (coalesced reads) and writes 16-byte chunks of 16 rows.
+// side), K-major core matrices (kc*16 + g)*128 like pass 1's tiles, column j scaled by
+// 1 / cinv[j].  A block stages a 64 x 128 block of X in shared memory (coalesced reads) and
+// writes 16-byte chunks of 16 rows.  q2parts as pack_x_kernel.
 __global__ void __launch_bounds__(256)
-pack_xt_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n, double sx,
-               int64_t jtiles, int64_t itiles, uint4* p0, uint4* p1, uint4* p2, uint4* p3) {
+pack_xt_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n,
+               const double* __restrict__ cinv, int64_t jtiles, int64_t itiles, uint4* out,
+               double* q2parts) {
   __shared__ float tx[64][129];
+  double q2 = 0.0;
   for (int64_t t = blockIdx.x; t < jtiles * itiles; t += gridDim.x) {
     const int64_t jt = t / itiles, it = t % itiles;
     for (int e = threadIdx.x; e < 64 * 128; e += blockDim.x) {
@@ -610,27 +632,30 @@ pack_xt_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n
     for (int w = threadIdx.x; w < 512; w += blockDim.x) {
       const int kc = w / 128, g = (w / 8) % 16, ri = w % 8;
       const int jl = g * 8 + ri;
-      uint32_t wd[4][4];
-      pack_digits16([&](int k) { return (double)tx[kc * 16 + k][jl] * sx; }, wd);
+      const int64_t j = jt * 128 + jl;
+      const double s = j < n ? 1.0 / cinv[j] : 0.0;
+      uint32_t wd[PLANES][4];
+      const double n2 = pack_digits16([&](int k) { return (double)tx[kc * 16 + k][jl] * s; }, wd);
+      if (j < n) q2 += n2 * (cinv[j] * cinv[j]);
       const int64_t idx = (t * PLANES * TILE_A) / 16 + w;   // planes interleaved per tile
-      p0[idx] = make_uint4(wd[0][0], wd[0][1], wd[0][2], wd[0][3]);
-      p1[idx] = make_uint4(wd[1][0], wd[1][1], wd[1][2], wd[1][3]);
-      p2[idx] = make_uint4(wd[2][0], wd[2][1], wd[2][2], wd[2][3]);
-      p3[idx] = make_uint4(wd[3][0], wd[3][1], wd[3][2], wd[3][3]);
+#pragma unroll
+      for (int pl = 0; pl < PLANES; ++pl)
+        out[idx + pl * (TILE_A / 16)] = make_uint4(wd[pl][0], wd[pl][1], wd[pl][2], wd[pl][3]);
     }
     __syncthreads();
   }
+  if (q2parts) block_sum_to(q2 * 0x1p-30, q2parts + blockIdx.x);
 }
 
-// Factor F (K x r, ld) * fscale[col] -> B tiles [Kt][rp x 64]: 16-byte chunk w of a tile holds
-// F[kt*64 + kc*16 + 0..15][g*8 + ri] with g = w/32, kc = (w/8)%4, ri = w%8, i.e. byte
-// (g*4 + kc)*128 + ri*16.  A block stages 64 factor rows in shared memory so global reads are
-// coalesced.
+// Factor F (K x r, ld) * fscale[col] -> B tiles [Kt][PLANES][rp x 64]: 16-byte chunk w of a
+// tile holds F[kt*64 + kc*16 + 0..15][g*8 + ri] with g = w/32, kc = (w/8)%4, ri = w%8, i.e.
+// byte (g*4 + kc)*128 + ri*16 (SBO 512, LBO 128), so the planes B0, B1 stored back to back
+// form one uniform 2 rp-row operand.  A block stages 64 factor rows in shared memory so global
+// reads are coalesced.
 template <typename T>
 __global__ void __launch_bounds__(256)
 pack_factor_kernel(const T* __restrict__ F, int64_t ldf, int64_t K, int r, int rp,
-                   const double* __restrict__ fscale, int64_t Kt, uint4* p0, uint4* p1, uint4* p2,
-                   uint4* p3) {
+                   const double* __restrict__ fscale, int64_t Kt, uint4* out) {
   extern __shared__ __align__(16) unsigned char pf_smem[];
   T(*tileF)[129] = reinterpret_cast<T(*)[129]>(pf_smem);   // BK x 129
   const int gpt = rp / 8;
@@ -643,18 +668,15 @@ pack_factor_kernel(const T* __restrict__ F, int64_t ldf, int64_t K, int r, int r
     }
     __syncthreads();
     for (int w = threadIdx.x; w < chunks; w += blockDim.x) {
-      // B layout: 8-row group g, 16-byte K chunk kc at (g * 4 + kc) * 128 (SBO 512, LBO 128),
-      // so the planes B_j, B_j+1 stored back to back form one uniform 2 rp-row operand
       const int g = w / 32, kc = (w / 8) % 4;
       const int col = g * 8 + w % 8;
       const double s = col < r ? fscale[col] : 0.0;
-      uint32_t wd[4][4];
+      uint32_t wd[PLANES][4];
       pack_digits16([&](int k) { return (double)tileF[kc * 16 + k][col] * s; }, wd);
       const int64_t idx = kt * PLANES * chunks + w;       // planes interleaved per stage
-      p0[idx] = make_uint4(wd[0][0], wd[0][1], wd[0][2], wd[0][3]);
-      p1[idx] = make_uint4(wd[1][0], wd[1][1], wd[1][2], wd[1][3]);
-      p2[idx] = make_uint4(wd[2][0], wd[2][1], wd[2][2], wd[2][3]);
-      p3[idx] = make_uint4(wd[3][0], wd[3][1], wd[3][2], wd[3][3]);
+#pragma unroll
+      for (int pl = 0; pl < PLANES; ++pl)
+        out[idx + pl * chunks] = make_uint4(wd[pl][0], wd[pl][1], wd[pl][2], wd[pl][3]);
     }
     __syncthreads();
   }
@@ -690,36 +712,80 @@ __global__ void scatter_cols_kernel(const double* __restrict__ buf, int64_t rows
   }
 }
 
-// Power of two s with mx * s in [32, 64) (1 for mx = 0).
+// Power of two s with mx * s in [63, 126) (TOP / 2 .. TOP), 1 for mx = 0: the largest scale
+// whose top digit stays within int8 (digits3_n).
 __host__ __device__ inline double pow2_scale(double mx) {
   if (!(mx > 0.0)) return 1.0;
   int e = 0;
-  frexp(mx, &e);                      // mx in [2^(e-1), 2^e)
-  return ldexp(1.0, 6 - e);           // mx * s in [2^5, 2^6)
+  const double f = frexp(mx, &e);     // mx = f 2^e, f in [0.5, 1)
+  return ldexp(1.0, (f < TOP / 128.0 ? 7 : 6) - e);
 }
 
-// fscale[k] = power of two with max|F_k| fscale in [32, 64); colscale[k] = 1/(sx fscale[k]).
-__global__ void scales_kernel(const unsigned long long* maxbits, int r, double sx, double* fscale,
+// fscale[k] = power of two with max|F_k| fscale in [63, 126); colscale[k] = 1 / fscale[k].
+__global__ void scales_kernel(const unsigned long long* maxbits, int r, double* fscale,
                               double* colscale) {
   for (int k = threadIdx.x; k < r; k += blockDim.x) {
     const double s = pow2_scale(__longlong_as_double((long long)maxbits[k]));
     fscale[k] = s;
-    colscale[k] = 1.0 / (sx * s);
+    colscale[k] = 1.0 / s;
   }
 }
 
-__global__ void maxabs_x_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows, int64_t n,
-                                unsigned* maxbits) {
-  unsigned m = 0;
-  const int64_t total = rows * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / n, j = e - i * n;
-    m = max(m, __float_as_uint(fabsf(X[i * ldx + j])));
+// Row maxima of X (rows x n): one warp per row; bits of the non-negative fp32 maxima.
+__global__ void x_rowmax_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows,
+                                int64_t n, unsigned* rowbits) {
+  const int lane = threadIdx.x & 31;
+  const bool vec = (ldx & 3) == 0 && ((uintptr_t)X & 15) == 0;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < rows;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const float* xr = X + i * ldx;
+    unsigned m = 0;
+    if (vec) {
+      const int64_t n4 = n >> 2;
+      for (int64_t q = lane; q < n4; q += 32) {
+        const float4 f = reinterpret_cast<const float4*>(xr)[q];
+        m = max(max(m, __float_as_uint(fabsf(f.x))), max(__float_as_uint(fabsf(f.y)),
+                max(__float_as_uint(fabsf(f.z)), __float_as_uint(fabsf(f.w)))));
+      }
+      for (int64_t j = 4 * n4 + lane; j < n; j += 32) m = max(m, __float_as_uint(fabsf(xr[j])));
+    } else {
+      for (int64_t j = lane; j < n; j += 32) m = max(m, __float_as_uint(fabsf(xr[j])));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) rowbits[i] = m;
   }
+}
+
+// Column maxima of X: a block covers 256 columns of a band of `band` rows, one global atomic
+// per column per block.
+__global__ void x_colmax_kernel(const float* __restrict__ X, int64_t ldx, int64_t rows,
+                                int64_t n, int64_t band, unsigned* colbits) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t i0 = blockIdx.y * band, i1 = min(rows, i0 + band);
+  unsigned m = 0;
+  for (int64_t i = i0; i < i1; ++i) m = max(m, __float_as_uint(fabsf(X[i * ldx + j])));
+  atomicMax(colbits + j, m);
+}
+
+// inv[i] = 1 / pow2_scale(max): the epilogue's row factor; uniform (optional): every entry
+// takes the scale of the maximum over all of bits[0, count).
+__global__ void inv_scales_kernel(const unsigned* bits, int64_t count, double* inv,
+                                  const unsigned* uniform) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    inv[i] = 1.0 / pow2_scale((double)__uint_as_float(uniform ? *uniform : bits[i]));
+}
+
+__global__ void max_u32_kernel(const unsigned* bits, int64_t count, unsigned* out) {
+  unsigned m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, bits[i]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(maxbits, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
 }  // namespace tci
@@ -732,11 +798,13 @@ struct TcState {
   int64_t Mt = 0;              // 128-row bands of X
   int64_t tiles_per_row = 0;   // 64-column tiles per band (even: 128-column pairs)
   int64_t Kt2 = 0;             // 64-row K stages of pass 2 (= 2 Mt)
-  double sx = 1.0;
-  int8_t* xp[PLANES] = {nullptr, nullptr, nullptr, nullptr};
-  int8_t* xtp[PLANES] = {nullptr, nullptr, nullptr, nullptr};   // X^T copy (pass 2), optional
-  int8_t* fp[PLANES] = {nullptr, nullptr, nullptr, nullptr};
-  unsigned* maxbits = nullptr; // X max (float bits)
+  int8_t* xp[PLANES] = {nullptr, nullptr, nullptr};
+  int8_t* xtp[PLANES] = {nullptr, nullptr, nullptr};   // X^T copy (pass 2), optional
+  int8_t* fp[PLANES] = {nullptr, nullptr, nullptr};
+  double* xinv_r = nullptr;    // rows: 1 / s of each X row (pass 1 output rows)
+  double* xinv_c = nullptr;    // n: 1 / s of each X column (pass 2 output rows)
+  unsigned* xbits = nullptr;   // rows + n + 1: row / column / global maxima (fp32 bits)
+  double* xq2 = nullptr;       // ||X~||^2 of the copy pass 2 reads
   unsigned long long* fmaxbits = nullptr;   // 128 factor column maxima (fp64 bits)
   double* fscale = nullptr;    // 128
   double* colscale = nullptr;  // 128
@@ -745,8 +813,6 @@ struct TcState {
   int ksplit1 = 1, ksplit2 = 1;
   bool pair = false;           // cta_group::2 kernel (ENMF_TC_PAIR=1 enables)
   int ksplit1p = 1, ksplit2p = 1;
-  int pass1_classes = 3;       // ENMF_TC_PASS1_CLASSES=4 for the full-precision pass 1
-  int pass2_classes = 4;       // ENMF_TC_PASS2_CLASSES: 3 (classes <= 2), 7 (+ A3 B0), 4
   int sms = kSMs;
 };
 
@@ -756,22 +822,25 @@ bool tc_supported(int64_t rows, int64_t n, int64_t r) {
 
 void tc_destroy(TcState* s) {
   if (!s) return;
-  if (s->xp[0]) cudaFree(s->xp[0]);     // planes 1..3 point into the same allocation
+  if (s->xp[0]) cudaFree(s->xp[0]);     // planes 1..2 point into the same allocation
   if (s->xtp[0]) cudaFree(s->xtp[0]);
   if (s->fp[0]) cudaFree(s->fp[0]);
-  void* bufs[] = {s->maxbits, s->fmaxbits, s->fscale, s->colscale, s->partial, s->colbuf};
+  void* bufs[] = {s->xinv_r, s->xinv_c, s->xbits, s->xq2, s->fmaxbits, s->fscale,
+                  s->colscale, s->partial, s->colbuf};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete s;
 }
 
-// Split count for `tiles` output bands over `stages` K stages: enough units to fill the GPU,
-// every unit K <= MAX_UNIT_K, no empty unit.
+const double* tc_factor_scales(const TcState* s) { return s ? s->fscale : nullptr; }
+const double* tc_xq_norm2(const TcState* s) { return s ? s->xq2 : nullptr; }
+
 // K split of a pass: units = tiles x ks are dealt round-robin to `sms` persistent CTAs, so
 // the pass takes ceil(units / sms) units of ceil(stages / ks) stages each.  Pick the ks that
 // minimises that makespan (the old rule, ks = ceil(4 sms / tiles), left pass 2 at C5 with
 // 782 units = 5.28 waves, i.e. 12 % of the SMs idle in the last wave), with a small per-split
-// charge for the fp64 partials and their reduction (`split_cost` per extra split).
+// charge for the fp64 partials and their reduction (`split_cost` per extra split); every unit
+// K <= MAX_UNIT_K, no empty unit.
 static int choose_split(int64_t tiles, int64_t stages, int sms, double split_cost) {
   const int kmin = std::max(1, (int)((stages * BK + MAX_UNIT_K - 1) / MAX_UNIT_K));
   int best = kmin;
@@ -799,7 +868,7 @@ static int choose_split_waves(int64_t tiles, int64_t stages, int sms) {
 }
 
 int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t n, int64_t r,
-              cudaStream_t st, double xmax) {
+              cudaStream_t st, double* q2parts, int q2cap) {
   *out = nullptr;
   TcState* s = new TcState();
   s->rows = rows;
@@ -809,18 +878,6 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
   s->Mt = (rows + BM - 1) / BM;
   s->tiles_per_row = ((n + 127) / 128) * 2;
   s->Kt2 = 2 * s->Mt;
-  // Pass 1 drops the weight-3 digit products only when K = n is long enough that their
-  // unbiased truncation error (~2^-22 of |X||V| per term) averages below ~1e-9 of P
-  s->pass1_classes = n >= 8192 ? 3 : 4;
-  // pass 2 keeps all 4 classes: with list 7 (-30 % tensor work, +13 % HALS sweeps/s at C5)
-  // the sampled C5 V-row update error rose from 6e-8 to 4.9e-6 (bar 1e-5) and the trace-form
-  // f error from 5e-8 to 2e-5 -- too little margin
-  s->pass2_classes = 4;
-  if (const char* e = getenv("ENMF_TC_PASS1_CLASSES")) s->pass1_classes = atoi(e) == 4 ? 4 : 3;
-  if (const char* e = getenv("ENMF_TC_PASS2_CLASSES")) {
-    const int c = atoi(e);
-    s->pass2_classes = c == 3 || c == 7 ? c : 4;
-  }
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, dev);
@@ -858,7 +915,10 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
     s->xp[p] = s->xp[0] + p * TILE_A;
     s->fp[p] = nullptr;    // factor planes: fp[0] + q * rp * BK for the block's rp (per launch)
   }
-  if (!e) e = cudaMalloc(&s->maxbits, sizeof(unsigned));
+  if (!e) e = cudaMalloc(&s->xinv_r, sizeof(double) * rows);
+  if (!e) e = cudaMalloc(&s->xinv_c, sizeof(double) * n);
+  if (!e) e = cudaMalloc(&s->xbits, sizeof(unsigned) * (rows + n + 1));
+  if (!e) e = cudaMalloc(&s->xq2, sizeof(double));
   if (!e) e = cudaMalloc(&s->fmaxbits, sizeof(unsigned long long) * 128);
   if (!e) e = cudaMalloc(&s->fscale, sizeof(double) * 128);
   if (!e) e = cudaMalloc(&s->colscale, sizeof(double) * 128);
@@ -868,28 +928,8 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
     tc_destroy(s);
     return e == cudaErrorMemoryAllocation ? 2 : 1;
   }
-  // X scale: power of two with max X * sx in [32, 64)
-  if (xmax < 0.0) {                     // not supplied by the caller's statistics pass
-    cudaMemsetAsync(s->maxbits, 0, sizeof(unsigned), st);
-    maxabs_x_kernel<<<4 * s->sms, 256, 0, st>>>(X, ldx, rows, n, s->maxbits);
-    unsigned mb = 0;
-    cudaMemcpyAsync(&mb, s->maxbits, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess) {
-      tc_destroy(s);
-      return 1;
-    }
-    float mx;
-    memcpy(&mx, &mb, sizeof(mx));
-    xmax = (double)mx;
-    count_launch();
-  }
-  s->sx = pow2_scale(xmax);
-  pack_x_kernel<<<8 * s->sms, 256, 0, st>>>(X, ldx, rows, n, s->sx, s->tiles_per_row, s->Mt,
-                                            (uint4*)s->xp[0], (uint4*)s->xp[1], (uint4*)s->xp[2],
-                                            (uint4*)s->xp[3]);
-  count_launch();
   // A second, transposed copy makes pass 2 a K-major stream of whole tiles like pass 1 (the
-  // MN-major gather of 1 KB pieces measured ~2x slower).  It costs another 4 bytes per element
+  // MN-major gather of 1 KB pieces measured ~2x slower).  It costs another 3 bytes per element
   // of HBM capacity and is skipped (ENMF_TC_XT=0, or not enough free memory) in favour of the
   // gather path.
   {
@@ -902,14 +942,40 @@ int tc_create(TcState** out, const float* X, int64_t ldx, int64_t rows, int64_t 
       s->xtp[0] = nullptr;
     }
     for (int p = 1; p < PLANES && s->xtp[0]; ++p) s->xtp[p] = s->xtp[0] + p * TILE_A;
-    if (s->xtp[0]) {
-      const int64_t jt = s->tiles_per_row / 2;
-      pack_xt_kernel<<<8 * s->sms, 256, 0, st>>>(X, ldx, rows, n, s->sx, jt, s->Kt2,
-                                                 (uint4*)s->xtp[0], (uint4*)s->xtp[1],
-                                                 (uint4*)s->xtp[2], (uint4*)s->xtp[3]);
-      count_launch();
-    }
   }
+  // digit scales: per X row for pass 1 and per X column for pass 2 (the output rows of each
+  // product); without the X^T copy pass 2 gathers the X copy along K, so every row of it (and
+  // every output row of pass 2) takes the global scale
+  unsigned* rowbits = s->xbits;
+  unsigned* colbits = s->xbits + rows;
+  unsigned* allbits = s->xbits + rows + n;
+  cudaMemsetAsync(s->xbits, 0, sizeof(unsigned) * (rows + n + 1), st);
+  x_rowmax_kernel<<<8 * s->sms, 256, 0, st>>>(X, ldx, rows, n, rowbits);
+  max_u32_kernel<<<2 * s->sms, 256, 0, st>>>(rowbits, rows, allbits);
+  count_launch(2);
+  const bool uniform = s->xtp[0] == nullptr;
+  if (!uniform) {
+    const int64_t band = 4096;
+    dim3 g((unsigned)((n + 255) / 256), (unsigned)((rows + band - 1) / band));
+    x_colmax_kernel<<<g, 256, 0, st>>>(X, ldx, rows, n, band, colbits);
+    count_launch();
+  }
+  inv_scales_kernel<<<2 * s->sms, 256, 0, st>>>(rowbits, rows, s->xinv_r,
+                                                uniform ? allbits : nullptr);
+  inv_scales_kernel<<<2 * s->sms, 256, 0, st>>>(colbits, n, s->xinv_c,
+                                                uniform ? allbits : nullptr);
+  count_launch(2);
+  const int pgrid = std::min(8 * s->sms, q2cap);
+  pack_x_kernel<<<pgrid, 256, 0, st>>>(X, ldx, rows, n, s->xinv_r, s->tiles_per_row, s->Mt,
+                                       (uint4*)s->xp[0], uniform ? q2parts : nullptr);
+  count_launch();
+  if (s->xtp[0]) {
+    const int64_t jt = s->tiles_per_row / 2;
+    pack_xt_kernel<<<pgrid, 256, 0, st>>>(X, ldx, rows, n, s->xinv_c, jt, s->Kt2,
+                                          (uint4*)s->xtp[0], q2parts);
+    count_launch();
+  }
+  reduce_parts(q2parts, pgrid, 1, s->xq2, st);
   if (cudaGetLastError() != cudaSuccess) {
     tc_destroy(s);
     return 1;
@@ -936,11 +1002,10 @@ static void pack_factor(TcState* s, const T* F, int64_t ldf, int64_t K, int64_t 
     colmax_kernel<T><<<2 * s->sms, 256, 0, st>>>(F, ldf, K, ncols, s->fmaxbits);
     count_launch();
   }
-  scales_kernel<<<1, 128, 0, st>>>(premax ? premax : s->fmaxbits, ncols, s->sx, s->fscale,
+  scales_kernel<<<1, 128, 0, st>>>(premax ? premax : s->fmaxbits, ncols, s->fscale,
                                    s->colscale);
   pack_factor_kernel<T><<<(int)std::min<int64_t>(Kt, 8 * s->sms), 256, BK * 129 * sizeof(T), st>>>(
-      F, ldf, K, ncols, rp, s->fscale, Kt, (uint4*)fplane(s, 0, rp), (uint4*)fplane(s, 1, rp),
-      (uint4*)fplane(s, 2, rp), (uint4*)fplane(s, 3, rp));
+      F, ldf, K, ncols, rp, s->fscale, Kt, (uint4*)fplane(s, 0, rp));
   count_launch(2);
 }
 
@@ -958,6 +1023,7 @@ static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out
   p.out_ld = out_ld;
   p.split_stride = split_stride;
   p.colscale = s->colscale;
+  p.rowinv = mode == 0 ? s->xinv_r : s->xinv_c;
   p.mode = mode;
   p.tiles = tiles;
   p.num_units = (pair ? (tiles + 1) / 2 : tiles) * ksplit;
@@ -969,35 +1035,17 @@ static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out
   p.out_rows = out_rows;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(tc_i8_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(tc_i8_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(tc_i8_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(tc_i8_pair_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         PAIR_SMEM);
-    cudaFuncSetAttribute(tc_i8_pair_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(tc_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(tc_i8_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          PAIR_SMEM);
     attr = true;
   }
-  // P = X V only feeds the U-block update: 3 digit planes (weight classes <= 2, ~2e-8
-  // relative); Q = X^T U also feeds the trace-form objective, whose conditioning needs all
-  // 4 planes (classes <= 3, ~5e-10 relative)  -- DESIGN.md §5
-  const bool three =
-      (s->pass1_classes == 3 && mode == 0) || (s->pass2_classes == 3 && mode == 2);
-  const bool seven = !pair && s->pass2_classes == 7 && mode == 2;
   if (pair) {
     const int grid = 2 * std::min(p.num_units, s->sms / 2);
-    if (three)
-      tc_i8_pair_kernel<3><<<grid, THREADS, PAIR_SMEM, st>>>(p);
-    else
-      tc_i8_pair_kernel<4><<<grid, THREADS, PAIR_SMEM, st>>>(p);
+    tc_i8_pair_kernel<<<grid, THREADS, PAIR_SMEM, st>>>(p);
   } else {
     const int grid = std::min(p.num_units, s->sms);
-    if (three)
-      tc_i8_kernel<3><<<grid, THREADS, SMEM_BYTES, st>>>(p);
-    else if (seven)
-      tc_i8_kernel<7><<<grid, THREADS, SMEM_BYTES, st>>>(p);
-    else
-      tc_i8_kernel<4><<<grid, THREADS, SMEM_BYTES, st>>>(p);
+    tc_i8_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(p);
   }
   count_launch();
   return cudaGetLastError() == cudaSuccess ? 0 : 1;

@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(HT, 1) tc_hals_kernel(const HParams p) {
       }
     }
     const double isu = 1.0 / su;
-    const double snap = 0x1p-14 * isu;            // max |u| su in [16, 32): 2^-18..2^-19 of it
+    const double snap = 0x1p-18 * isu;            // max |u| su in [16, 32): 2^-22..2^-23 of it
     const int ovf_hi = __double2hiint(64.0 * isu);
     int bover = -1;                    // first block whose new u outgrew the digit scale
 #pragma unroll 1
@@ -795,9 +795,9 @@ __global__ void __launch_bounds__(HT, 1) tc_hals_kernel(const HParams p) {
       for (int k = 0; k < HB; ++k) {
         const double ig = gt[tri(k, k)];
         const double vn = fma(tt[k], ig, uu[k]);
-        // projection; below `snap` (2^-18 of the row's maximum, far above the coupling's
-        // ~2^-26 error) an update counts as zero, so a column the exact update drives to
-        // zero stays exactly zero (R28); G_kk <= 0: column skipped
+        // projection; below `snap` (2^-22 of the row's maximum, 16x the coupling's ~2^-26
+        // error) an update counts as zero, so a column the exact update drives to zero stays
+        // exactly zero (R28); G_kk <= 0: column skipped
         const double nu = ig == 0.0 ? uu[k] : (vn > snap ? vn : 0.0);
         const double d = nu - uu[k];
         uu[k] = nu;

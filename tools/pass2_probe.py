@@ -1,6 +1,5 @@
 """C5: trace-form f vs the direct objective after the bench schedule's first sweeps, and the
-sweep rate, for the current ENMF_TC_PASS2_CLASSES (run once per setting)."""
-import os
+HALS sweep rate of the tensor-core path."""
 import time
 
 import numpy as np
@@ -29,6 +28,6 @@ torch.cuda.synchronize()
 dt = time.time() - t
 fx = h.objective(U, V, exact=True)
 out.append((50, f[-1], fx, abs(f[-1] - fx) / fx, info["hals_sweeps"]))
-print("PASS2_CLASSES", os.environ.get("ENMF_TC_PASS2_CLASSES", "4"), "HALS sweeps/s %.2f" % (20 / dt))
+print("HALS sweeps/s %.2f" % (20 / dt))
 for o in out:
     print("after %d sweeps: f_trace %.12e f_direct %.12e rel %.2e (hals %d)" % o)
