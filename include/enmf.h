@@ -164,6 +164,30 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx);
 enmf_status_t enmf_set_data_csr(enmf_handle_t h, const int64_t* row_ptr, const int32_t* col_idx,
                                 const float* vals, int64_t nnz);
 
+/* eNMC, the exterior method for nonnegative matrix COMPLETION (App. C, lines
+ * 1011-1042; Alg. NMC): bind the OBSERVED entries of X as CSR lists (same layout, checks,
+ * ownership and errors as enmf_set_data_csr); entries not stored are missing, and the
+ * objective becomes f^ = ||M_E o (X - U V^T)||_F^2 over the observed entries (reported
+ * un-halved).  Then: enmf_softimpute (the init, line 1027), enmf_rotate (Alg. 1 on its output,
+ * line 1028), enmf_iterate (every sweep: lift + mask + PBCD of U over the rows' observed
+ * entries, then of V over the columns', with the masked gradient (M_E o (U V^T - X)) V and
+ * the exact line-minimising row step, readings R30/R32; f_trace_host receives f^),
+ * enmf_objective (f^; `exact` ignored).  enmf_kkt_residual returns ENMF_ERR_STATE on such a
+ * handle.  Single rank, r <= 64 (ENMF_ERR_SHAPE otherwise). */
+enmf_status_t enmf_set_data_masked(enmf_handle_t h, const int64_t* row_ptr,
+                                   const int32_t* col_idx, const float* vals, int64_t nnz);
+
+/* softImpute-ALS with lambda = 0 (Hastie et al. 2015, Alg. 3.1; the eNMC init of PAPER.md:1017,
+ * reading R31) on a handle bound by enmf_set_data_masked: `iters` iterations (>= 1) from the
+ * start U0 (row_count x r, device, ld ldu0; orthonormalised first -- the caller supplies the
+ * random start so that runs are reproducible), each a V-side and a U-side half step on the
+ * completed matrix P_E(X) + P_E-perp(A B^T).  Writes A = U D into U and B = V D into V (fp32;
+ * A B^T is the rank-r model, columns by D descending, sign rule R5 on A) and keeps [A; B] for
+ * enmf_rotate; d_host (r values, may be NULL) receives D.  ENMF_ERR_STATE unless bound by
+ * enmf_set_data_masked. */
+enmf_status_t enmf_softimpute(enmf_handle_t h, const float* U0, int64_t ldu0, int iters,
+                              float* U, int64_t ldu, float* V, int64_t ldv, double* d_host);
+
 /* Rank-r truncated SVD with balanced scaling U* = U S^1/2, V* = V S^1/2 by
  * a randomised range finder (reading R3); sign rule R5.  Writes U* (this
  * rank's rows) into U and V* into V; sigma_host (r values) may be NULL. */
@@ -175,6 +199,19 @@ enmf_status_t enmf_svd(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t
  * and enter the ascent stage.  info_host may be NULL. */
 enmf_status_t enmf_rotate(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
                           enmf_init_info_t* info_host);
+
+/* RSR-ADMM (App. A, Alg. alg:rsr): the general
+ * rotation-scale-rotation form of the rotation step for exact-NMF instances -- orthogonal R1,
+ * R2 and a positive diagonal Lambda with U* R1 Lambda R2 >= 0 and V* R1 Lambda^-1 R2 >= 0 (Eq.
+ * eq5), admm_iters iterations of the split-variable ADMM (readings R34-R37: penalties
+ * rho = gamma = t = 1e-3 / max|W| unless admm_rho > 0, identity start, last iterate, the
+ * lambda update's positive quartic root of least cost).  Input: (U, V) = (U*, V*) as enmf_svd
+ * writes them; output U <- U* R1 Lambda R2, V <- V* R1 Lambda^-1 R2 (so U V^T is unchanged),
+ * lift constants fixed from them and the ascent stage entered, as enmf_rotate.  info_host
+ * (may be NULL): negativity before / after and the lift constants; lambda_host (r doubles, may
+ * be NULL): Lambda.  Single rank (ENMF_ERR_STATE otherwise). */
+enmf_status_t enmf_rotate_rsr(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                              enmf_init_info_t* info_host, double* lambda_host);
 
 /* enmf_set_data + enmf_svd + enmf_rotate (Alg. 3). */
 enmf_status_t enmf_init(enmf_handle_t h, const float* X, int64_t ldx, float* U, int64_t ldu,
@@ -266,7 +303,7 @@ enmf_status_t enmf_set_host_allreduce(enmf_handle_t h, enmf_host_allreduce_fn fn
 enmf_status_t enmf_nccl_unique_id(void* out128);
 
 /* Name of the contraction path selected by enmf_set_data ("fp64-simt", "tc-i8x3-exact",
- * "csr-f64-spmm" or "csr-f64-spmm+tc-rows"). */
+ * "csr-f64-spmm", "csr-f64-spmm+tc-rows" or, for eNMC, "nmc-f64"). */
 const char* enmf_precision_name(enmf_handle_t h);
 
 const char* enmf_status_string(enmf_status_t s);

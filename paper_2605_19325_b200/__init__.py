@@ -78,9 +78,12 @@ _sigs = {
     "enmf_destroy": (ctypes.c_int, [_H]),
     "enmf_set_data": (ctypes.c_int, [_H, _P, _I64]),
     "enmf_set_data_csr": (ctypes.c_int, [_H, _P, _P, _P, _I64]),
+    "enmf_set_data_masked": (ctypes.c_int, [_H, _P, _P, _P, _I64]),
+    "enmf_softimpute": (ctypes.c_int, [_H, _P, _I64, ctypes.c_int, _P, _I64, _P, _I64, _D]),
     "enmf_svd": (ctypes.c_int, [_H, _P, _I64, _P, _I64, _D]),
     "enmf_rotate": (ctypes.c_int, [_H, _P, _I64, _P, _I64, ctypes.POINTER(InitInfo)]),
     "enmf_init": (ctypes.c_int, [_H, _P, _I64, _P, _I64, _P, _I64, ctypes.POINTER(InitInfo)]),
+    "enmf_rotate_rsr": (ctypes.c_int, [_H, _P, _I64, _P, _I64, ctypes.POINTER(InitInfo), _D]),
     "enmf_set_stage": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_double, ctypes.c_double]),
     "enmf_get_stage": (ctypes.c_int, [_H, ctypes.POINTER(ctypes.c_int), _D, _D]),
     "enmf_project": (ctypes.c_int, [_H, _P, _I64, _P, _I64]),
@@ -225,6 +228,41 @@ class Enmf:
         _check(_lib.enmf_set_data_csr(self._h, row_ptr.data_ptr(), col_idx.data_ptr() or None,
                                       vals.data_ptr() or None, int(vals.numel())),
                "enmf_set_data_csr")
+
+    def rotate_rsr(self, U, V):
+        """RSR-ADMM (App. A) from (U*, V*) in place: returns (init-info dict, Lambda)."""
+        pu, ldu = _mat(U, self.r, "U")
+        pv, ldv = _mat(V, self.r, "V")
+        info = InitInfo()
+        lam = np.zeros(self.r)
+        _check(_lib.enmf_rotate_rsr(self._h, pu, ldu, pv, ldv, ctypes.byref(info),
+                                    lam.ctypes.data_as(_D)), "enmf_rotate_rsr")
+        return _info_dict(info), lam
+
+    def set_data_masked(self, row_ptr, col_idx, vals):
+        """eNMC: bind the OBSERVED entries of X as CSR CUDA tensors (same layout as
+        set_data_csr); unlisted entries are missing (enmf_set_data_masked)."""
+        import torch
+        for t, dt, name in ((row_ptr, torch.int64, "row_ptr"), (col_idx, torch.int32, "col_idx"),
+                            (vals, torch.float32, "vals")):
+            if not (t.is_cuda and t.dtype == dt and t.is_contiguous()):
+                raise TypeError(f"{name}: contiguous CUDA {dt} tensor required")
+        if row_ptr.numel() != self.rows + 1 or col_idx.numel() != vals.numel():
+            raise ValueError("row_ptr / col_idx / vals sizes")
+        self._X = (row_ptr, col_idx, vals)
+        _check(_lib.enmf_set_data_masked(self._h, row_ptr.data_ptr(), col_idx.data_ptr() or None,
+                                         vals.data_ptr() or None, int(vals.numel())),
+               "enmf_set_data_masked")
+
+    def softimpute(self, U0, iters, U, V):
+        """softImpute-ALS (lambda = 0) from the start U0: writes A into U, B into V; returns D."""
+        p0, ld0 = _mat(U0, self.r, "U0")
+        pu, ldu = _mat(U, self.r, "U")
+        pv, ldv = _mat(V, self.r, "V")
+        d = np.zeros(self.r)
+        _check(_lib.enmf_softimpute(self._h, p0, ld0, int(iters), pu, ldu, pv, ldv,
+                                    d.ctypes.data_as(_D)), "enmf_softimpute")
+        return d
 
     def svd(self, U, V):
         pu, ldu = _mat(U, self.r, "U")

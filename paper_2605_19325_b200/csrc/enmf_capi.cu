@@ -341,6 +341,46 @@ enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ld
   return check_launch();
 }
 
+// One eNMC sweep (Alg. NMC loop body; reading R32): lift + mask + masked
+// PBCD of U over the rows' observed entries with V fixed, then of V over the columns'
+// observed entries (CSC copy) with the new U; the masked objective f^ into ftrace[t].  Every
+// sweep is a PBCD sweep -- Alg. NMC has no HALS stage; the lift leaves a nonnegative factor
+// unchanged.
+enmf_status_t sweep_nmc(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv, int t,
+                        const SweepHooks& hk) {
+  cudaStream_t st = h->st;
+  const int r = (int)h->r;
+  const int mi = h->opt.pbcd_max_iter;
+  if (hk.u_ready) CUDA_TRY(cudaStreamWaitEvent(st, hk.u_ready, 0));
+  nmc_pbcd_rows(U, ldu, h->m_loc, r, h->csr_ptr, h->csr_col, h->csr_val, V, ldv,
+                h->dscal + S_LAMU, mi, h->snaps, h->parts, st);
+  reduce_parts(h->parts, nmc_pbcd_parts(), mi + 1, h->pgsum, st);
+  pbcd_commit(U, ldu, h->m_loc, r, h->snaps, h->pgsum, h->opt.pbcd_eps, mi,
+              h->dint + I_KSTAR_U, nullptr, h->minparts, false, st);
+  reduce_min(h->minparts, kRowGrid, h->dscal + S_MINU, st);
+  if (hk.u_download) {
+    CUDA_TRY(cudaEventRecord(h->ev_a, st));
+    CUDA_TRY(cudaStreamWaitEvent(h->st2, h->ev_a, 0));
+    CUDA_TRY(cudaMemcpyAsync(hk.u_download, U, sizeof(float) * h->m_loc * r,
+                             cudaMemcpyDeviceToHost, h->st2));
+  }
+  nmc_pbcd_rows(V, ldv, h->n, r, h->csc_ptr, h->csc_row, h->csc_val, U, ldu,
+                h->dscal + S_LAMV, mi, h->snaps, h->parts, st);
+  reduce_parts(h->parts, nmc_pbcd_parts(), mi + 1, h->pgsum, st);
+  pbcd_commit(V, ldv, h->n, r, h->snaps, h->pgsum, h->opt.pbcd_eps, mi, h->dint + I_KSTAR_V,
+              nullptr, h->minparts, false, st);
+  reduce_min(h->minparts, kRowGrid, h->dscal + S_MINV, st);
+  if (hk.v_download) {
+    CUDA_TRY(cudaEventRecord(h->ev_a, st));
+    CUDA_TRY(cudaStreamWaitEvent(h->st2, h->ev_a, 0));
+    CUDA_TRY(cudaMemcpyAsync(hk.v_download, V, sizeof(float) * h->n * r, cudaMemcpyDeviceToHost,
+                             h->st2));
+  }
+  nmc_objective(h->csr_ptr, h->csr_col, h->csr_val, h->m_loc, r, U, ldu, V, ldv, h->minparts,
+                h->ftrace + t, st);        // minparts: kRowGrid = nmc_objective_parts() slots
+  return check_launch();
+}
+
 }  // namespace
 
 // ==================================================================== C-ABI
@@ -432,6 +472,7 @@ enmf_status_t enmf_nccl_unique_id(void* out128) {
 
 const char* enmf_precision_name(enmf_handle_t h) {
   if (!h) return "none";
+  if (h->nmc) return "nmc-f64";
   if (h->sparse) return h->tc_pbcd ? "csr-f64-spmm+tc-rows" : "csr-f64-spmm";
   return h->precision == ENMF_PREC_TC ? "tc-i8x3-exact" : "fp64-simt";
 }
@@ -547,6 +588,7 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
   h->ldx = ldx;
   h->bound = false;
   h->sparse = false;
+  h->nmc = false;
   const int np = x_stats_parts(h->m_loc);
   double* out3 = h->work;   // [sum, min, nonfinite, max|X| of this rank's rows]
   x_stats(X, ldx, h->m_loc, h->n, h->parts, np, out3, h->st);
@@ -602,9 +644,15 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
   return check_launch();
 }
 
-enmf_status_t enmf_set_data_csr(enmf_handle_t h, const int64_t* row_ptr, const int32_t* col_idx,
-                                const float* vals, int64_t nnz) {
+}  // extern "C"
+
+namespace {
+// CSR binding shared by sparse X (stored entries are X's nonzeros, the rest zeros) and eNMC
+// (stored entries are the OBSERVED entries, the rest missing).
+enmf_status_t bind_csr(enmf_handle_t h, const int64_t* row_ptr, const int32_t* col_idx,
+                       const float* vals, int64_t nnz, bool nmc) {
   if (!h || !row_ptr || nnz < 0 || (nnz > 0 && (!col_idx || !vals))) return ENMF_ERR_INVALID_ARG;
+  if (nmc && (h->prob.world_size != 1 || !nmc_supported((int)h->r))) return ENMF_ERR_SHAPE;
   if (nnz > INT32_MAX || h->n > INT32_MAX) return ENMF_ERR_SHAPE;
   LaunchScope ls(h);
   h->bound = false;
@@ -660,10 +708,12 @@ enmf_status_t enmf_set_data_csr(enmf_handle_t h, const int64_t* row_ptr, const i
   h->csr_val = vals;
   h->nnz = nnz;
   h->sparse = true;
+  h->nmc = nmc;
   // X passes: fp64 SpMM; block updates on the tensor-core row kernels unless precision FP64
+  // (eNMC: the masked PBCD kernel, fp64)
   if (h->tc) { tc_destroy(h->tc); h->tc = nullptr; }
   const char* tpe = getenv("ENMF_TC_PBCD");
-  h->tc_pbcd = h->opt.precision != ENMF_PREC_FP64 && tc_pbcd_supported((int)h->r) &&
+  h->tc_pbcd = !nmc && h->opt.precision != ENMF_PREC_FP64 && tc_pbcd_supported((int)h->r) &&
                !(tpe && tpe[0] == '0');
   if (h->tc_pbcd && !h->tcpb_ws) ENMF_TRY(dalloc(&h->tcpb_ws, 128 + 4 * 128 * 128 / 8));
   const char* the = getenv("ENMF_TC_HALS");
@@ -676,6 +726,19 @@ enmf_status_t enmf_set_data_csr(enmf_handle_t h, const int64_t* row_ptr, const i
   h->stage_known_hals = false;
   h->bound = true;
   return check_launch();
+}
+}  // namespace
+
+extern "C" {
+
+enmf_status_t enmf_set_data_csr(enmf_handle_t h, const int64_t* row_ptr, const int32_t* col_idx,
+                                const float* vals, int64_t nnz) {
+  return bind_csr(h, row_ptr, col_idx, vals, nnz, false);
+}
+
+enmf_status_t enmf_set_data_masked(enmf_handle_t h, const int64_t* row_ptr,
+                                   const int32_t* col_idx, const float* vals, int64_t nnz) {
+  return bind_csr(h, row_ptr, col_idx, vals, nnz, true);
 }
 
 enmf_status_t enmf_set_stage(enmf_handle_t h, int stage, double lambda_u, double lambda_v) {
@@ -736,7 +799,7 @@ enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int
                            cudaEvent_t u_ready, float* u_dl_host, float* v_dl_host) {
   LaunchScope ls(h);
   const bool sh = h->prob.world_size > 1;
-  const bool maybe_ascent = !h->stage_known_hals;
+  const bool maybe_ascent = !h->stage_known_hals || h->nmc;
   if (maybe_ascent) ENMF_TRY(ensure_snaps(h));
   ENMF_TRY(ensure_ftrace(h, std::max(n_iters, 1)));
   CUDA_TRY(cudaMemsetAsync(h->dint + I_CNT_ASC, 0, 2 * sizeof(int), h->st));
@@ -744,7 +807,7 @@ enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int
   // entry state: mins of the factors as given, G_V of the given V (min U after its upload)
   if (!u_ready) ENMF_TRY(min_factor(h, U, ldu, h->m_loc, S_MINU, sh));
   ENMF_TRY(min_factor(h, V, ldv, h->n, S_MINV, false));
-  ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
+  if (!h->nmc) ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
   h->umax_valid = h->vmax_valid = false;   // the caller may have changed U / V since
   for (int t = 0; t < n_iters; ++t) {
     SweepHooks hk;
@@ -753,7 +816,10 @@ enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int
       hk.u_download = u_dl_host;
       hk.v_download = v_dl_host;
     }
-    ENMF_TRY(sweep(h, U, ldu, V, ldv, t, maybe_ascent, hk));
+    if (h->nmc)
+      ENMF_TRY(sweep_nmc(h, U, ldu, V, ldv, t, hk));
+    else
+      ENMF_TRY(sweep(h, U, ldu, V, ldv, t, maybe_ascent, hk));
   }
   if (u_ready && n_iters == 0) CUDA_TRY(cudaStreamWaitEvent(h->st, u_ready, 0));
   h->umax_valid = h->vmax_valid = false;
@@ -774,8 +840,8 @@ enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int
   prof_collect(h);
   if (hi[I_STAGE] == 1) h->stage_known_hals = true;
   if (info) {
-    info->ascent_sweeps = hi[I_CNT_ASC];
-    info->hals_sweeps = hi[I_CNT_HALS];
+    info->ascent_sweeps = h->nmc ? n_iters : hi[I_CNT_ASC];
+    info->hals_sweeps = h->nmc ? 0 : hi[I_CNT_HALS];
     info->feasible = mins[0] >= 0.0 && mins[1] >= 0.0;
     info->pbcd_iters_u = hi[I_KSTAR_U];
     info->pbcd_iters_v = hi[I_KSTAR_V];
@@ -834,7 +900,11 @@ enmf_status_t enmf_objective(enmf_handle_t h, const float* U, int64_t ldu, const
   LaunchScope ls(h);
   const bool sh = h->prob.world_size > 1;
   double* f = h->dscal + S_SCRATCH;
-  if (exact && h->sparse) {
+  if (h->nmc) {
+    // eNMC: the masked objective over the observed entries
+    nmc_objective(h->csr_ptr, h->csr_col, h->csr_val, h->m_loc, (int)h->r, U, ldu, V, ldv,
+                  h->parts, f, h->st);
+  } else if (exact && h->sparse) {
     // sparse X: ||X||^2 - 2 sum over stored entries x_ij (u_i . v_j) + ||U V^T||^2, the cross
     // term entry by entry (not through Q) and ||U V^T||^2 = <U^T U, V^T V> exactly
     double* parts = nullptr;
@@ -876,7 +946,7 @@ enmf_status_t enmf_objective(enmf_handle_t h, const float* U, int64_t ldu, const
 enmf_status_t enmf_kkt_residual(enmf_handle_t h, const float* U, int64_t ldu, const float* V,
                                 int64_t ldv, enmf_kkt_t* out) {
   if (!h || !out) return ENMF_ERR_INVALID_ARG;
-  if (!h->bound) return ENMF_ERR_STATE;
+  if (!h->bound || h->nmc) return ENMF_ERR_STATE;   // eNMC: KKT of the masked problem not built
   ENMF_TRY(validate_ld(U, ldu, h->r));
   ENMF_TRY(validate_ld(V, ldv, h->r));
   LaunchScope ls(h);

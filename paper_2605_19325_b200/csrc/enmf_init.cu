@@ -385,6 +385,248 @@ enmf_status_t rotate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int6
   return ENMF_OK;
 }
 
+// softImpute-ALS with lambda = 0 (Hastie et al. 2015, Alg. 3.1; the eNMC init of PAPER.md:1017,
+// reading R31), on the observed entries only: the completed matrix X* = P_E(X) + P_E-perp(A B^T)
+// enters through X*^T U = S^T U + B D and X* V = S V + A D (S = P_E(X - A B^T), U and V
+// orthonormal, A = U D, B = V D).  Per iteration:
+//   V side: T = X*^T U (n x r); SVD T = V~ D~^2 R^T; V <- V~, D <- D~, U <- U R
+//   U side: T = X* V  (m x r); SVD T = U~ D~^2 R^T; U <- U~, D <- D~, V <- V R
+// The thin SVD of T comes from the eigen-decomposition of T^T T (one-sided Jacobi, fp64):
+// R = its eigenvectors, D~^2 = sqrt of its eigenvalues, the left factor T R D~^-2.  Output:
+// A, B (sign rule R5 on A, D descending) into W64 = [A; B] and U, V (fp32) for enmf_rotate.
+enmf_status_t softimpute_core(enmf_handle_t h, const float* U0, int64_t ldu0, int iters,
+                              float* Uout, int64_t ldu, float* Vout, int64_t ldv,
+                              double* d_host) {
+  const int64_t m = h->m_loc, n = h->n, big = std::max(m, n);
+  const int r = (int)h->r;
+  DevBuf db(h);
+  double *Ud, *Vd, *A, *B, *T, *Tq, *G, *R, *Rinv, *Ev, *Ee, *sv, *jw, *Dd, *inv, *W;
+  int* bad;
+  ENMF_TRY(db.get(&Ud, (size_t)(m * r)));
+  ENMF_TRY(db.get(&Vd, (size_t)(n * r)));
+  ENMF_TRY(db.get(&A, (size_t)(m * r)));
+  ENMF_TRY(db.get(&B, (size_t)(n * r)));
+  ENMF_TRY(db.get(&T, (size_t)(big * r)));
+  ENMF_TRY(db.get(&Tq, (size_t)(big * r)));
+  ENMF_TRY(db.get(&W, (size_t)(big * r)));
+  ENMF_TRY(db.get(&G, (size_t)r * r));
+  ENMF_TRY(db.get(&R, (size_t)r * r));
+  ENMF_TRY(db.get(&Rinv, (size_t)r * r));
+  ENMF_TRY(db.get(&Ev, (size_t)r * r));
+  ENMF_TRY(db.get(&Ee, (size_t)r * r));
+  ENMF_TRY(db.get(&sv, (size_t)r));
+  ENMF_TRY(db.get(&jw, (size_t)2 * r * r));
+  ENMF_TRY(db.get(&Dd, (size_t)r));
+  ENMF_TRY(db.get(&inv, (size_t)r));
+  ENMF_TRY(db.get(&bad, 1));
+  if (!h->W64) ENMF_TRY(dalloc(&h->W64, (size_t)((m + n) * r)));
+  // 1. U = orthonormalised U0 (CholeskyQR2: the unique QR with a positive diagonal), D = I,
+  //    V = 0: A = U, B = 0
+  f32_to_f64(U0, ldu0, m, r, Ud, h->st);
+  ENMF_TRY(cholqr(h, Ud, W, m, r, false, G, R, Rinv, bad));
+  std::vector<double> ones(r, 1.0);
+  CUDA_TRY(cudaMemcpyAsync(Dd, ones.data(), sizeof(double) * r, cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaMemcpyAsync(A, Ud, sizeof(double) * m * r, cudaMemcpyDeviceToDevice, h->st));
+  CUDA_TRY(cudaMemsetAsync(B, 0, sizeof(double) * n * r, h->st));
+  CUDA_TRY(cudaMemsetAsync(Vd, 0, sizeof(double) * n * r, h->st));
+  GemmOut o;
+  o.ldc = r;
+  // thin SVD of T (rows x r) -> Q (left, into Tq), D~ (Dd), R = Ev; returns after Ev / Dd set
+  auto thin_svd = [&](int64_t rows) -> enmf_status_t {
+    o.C = G;
+    gemm<double, double>(true, T, r, T, r, r, r, rows, o, h->work, h->work_elems, h->st);
+    jacobi_svd(G, r, Ee, sv, Ev, jw, h->st);
+    nmc_svals(sv, r, Dd, inv, h->st);
+    o.C = Tq;
+    gemm<double, double>(false, T, r, Ev, r, rows, r, r, o, h->work, h->work_elems, h->st);
+    scale_cols_f64(Tq, rows, r, inv, h->st);                       // T R D~^-2
+    return ENMF_OK;
+  };
+  for (int it = 0; it < iters; ++it) {
+    // V side: T = S^T U + B D over the CSC lists (rows of T = columns of X)
+    nmc_resid_spmm(h->csc_ptr, h->csc_row, h->csc_val, n, r, B, A, Ud, Dd, T, h->st);
+    ENMF_TRY(thin_svd(n));
+    CUDA_TRY(cudaMemcpyAsync(Vd, Tq, sizeof(double) * n * r, cudaMemcpyDeviceToDevice, h->st));
+    o.C = W;
+    gemm<double, double>(false, Ud, r, Ev, r, m, r, r, o, h->work, h->work_elems, h->st);
+    CUDA_TRY(cudaMemcpyAsync(Ud, W, sizeof(double) * m * r, cudaMemcpyDeviceToDevice, h->st));
+    CUDA_TRY(cudaMemcpyAsync(A, Ud, sizeof(double) * m * r, cudaMemcpyDeviceToDevice, h->st));
+    scale_cols_f64(A, m, r, Dd, h->st);
+    CUDA_TRY(cudaMemcpyAsync(B, Vd, sizeof(double) * n * r, cudaMemcpyDeviceToDevice, h->st));
+    scale_cols_f64(B, n, r, Dd, h->st);
+    // U side: T = S V + A D over the CSR lists
+    nmc_resid_spmm(h->csr_ptr, h->csr_col, h->csr_val, m, r, A, B, Vd, Dd, T, h->st);
+    ENMF_TRY(thin_svd(m));
+    CUDA_TRY(cudaMemcpyAsync(Ud, Tq, sizeof(double) * m * r, cudaMemcpyDeviceToDevice, h->st));
+    o.C = W;
+    gemm<double, double>(false, Vd, r, Ev, r, n, r, r, o, h->work, h->work_elems, h->st);
+    CUDA_TRY(cudaMemcpyAsync(Vd, W, sizeof(double) * n * r, cudaMemcpyDeviceToDevice, h->st));
+    CUDA_TRY(cudaMemcpyAsync(A, Ud, sizeof(double) * m * r, cudaMemcpyDeviceToDevice, h->st));
+    scale_cols_f64(A, m, r, Dd, h->st);
+    CUDA_TRY(cudaMemcpyAsync(B, Vd, sizeof(double) * n * r, cudaMemcpyDeviceToDevice, h->st));
+    scale_cols_f64(B, n, r, Dd, h->st);
+  }
+  ENMF_TRY(check_launch());
+  // sign rule R5 on the columns of A (= U D, D > 0): A and B flipped together
+  std::vector<double> sgn;
+  ENMF_TRY(column_signs(h, A, m, r, 0, sgn));
+  double* dsg = h->work;
+  CUDA_TRY(cudaMemcpyAsync(dsg, sgn.data(), sizeof(double) * r, cudaMemcpyHostToDevice, h->st));
+  scale_cols_f64(A, m, r, dsg, h->st);
+  scale_cols_f64(B, n, r, dsg, h->st);
+  CUDA_TRY(cudaMemcpyAsync(h->W64, A, sizeof(double) * m * r, cudaMemcpyDeviceToDevice, h->st));
+  CUDA_TRY(cudaMemcpyAsync(h->W64 + m * r, B, sizeof(double) * n * r, cudaMemcpyDeviceToDevice,
+                           h->st));
+  f64_to_f32(A, m, r, nullptr, Uout, ldu, h->st);
+  f64_to_f32(B, n, r, nullptr, Vout, ldv, h->st);
+  std::vector<double> dh(r);
+  CUDA_TRY(cudaMemcpyAsync(dh.data(), Dd, sizeof(double) * r, cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  ENMF_TRY(check_launch());
+  if (d_host)
+    for (int k = 0; k < r; ++k) d_host[k] = dh[k];
+  return ENMF_OK;
+}
+
+// RSR-ADMM (App. A, Alg. alg:rsr) from W64 = [U*; V*]: T = admm_iters
+// iterations of the split (W1 = W_svd R1, W2 = [W11 Lambda; W12 Lambda^-1], W3 = W2 R2) with
+// rho = gamma = t = 1e-3 / max|W_svd| (R34), R1 = R2 = Lambda = I, W1 = W2 = W3 = W_svd,
+// M = N = P = 0 (R35), last iterate (R36), the lambda root of R37.  Writes U = U* R1 Lambda R2,
+// V = V* R1 Lambda^-1 R2 (fp32), fixes the lift constants from them (R9) and enters the
+// ascent stage like enmf_rotate; lam_host (r, may be NULL) receives Lambda.  Single rank.
+enmf_status_t rsr_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                       enmf_init_info_t* info, double* lam_host) {
+  const int64_t mr = h->m_loc, n = h->n, rows = mr + n;
+  const int r = (int)h->r;
+  const int64_t count = rows * r;
+  DevBuf db(h);
+  double *W1, *W2, *W3, *M, *N, *P, *WsR1, *W2R2, *B, *G, *R1, *R2, *R2t, *Mr, *lam, *abcd, *cp;
+  double *Cs, *Ds, *sv, *jw, *nsw;
+  int *pfail, *nsst;
+  ENMF_TRY(db.get(&W1, (size_t)count));
+  ENMF_TRY(db.get(&W2, (size_t)count));
+  ENMF_TRY(db.get(&W3, (size_t)count));
+  ENMF_TRY(db.get(&M, (size_t)count));
+  ENMF_TRY(db.get(&N, (size_t)count));
+  ENMF_TRY(db.get(&P, (size_t)count));
+  ENMF_TRY(db.get(&WsR1, (size_t)count));
+  ENMF_TRY(db.get(&W2R2, (size_t)count));
+  ENMF_TRY(db.get(&B, (size_t)count));
+  ENMF_TRY(db.get(&G, (size_t)count));
+  ENMF_TRY(db.get(&R1, (size_t)r * r));
+  ENMF_TRY(db.get(&R2, (size_t)r * r));
+  ENMF_TRY(db.get(&R2t, (size_t)r * r));
+  ENMF_TRY(db.get(&Mr, (size_t)r * r));
+  ENMF_TRY(db.get(&Cs, (size_t)r * r));
+  ENMF_TRY(db.get(&Ds, (size_t)r * r));
+  ENMF_TRY(db.get(&sv, (size_t)r));
+  ENMF_TRY(db.get(&jw, (size_t)2 * r * r));
+  ENMF_TRY(db.get(&nsw, (size_t)3 * r * r + 256));
+  ENMF_TRY(db.get(&lam, (size_t)r));
+  ENMF_TRY(db.get(&abcd, (size_t)4 * r));
+  ENMF_TRY(db.get(&cp, (size_t)rsr_colsum_parts() * 4 * r));
+  ENMF_TRY(db.get(&pfail, 1));
+  ENMF_TRY(db.get(&nsst, 2));
+  const double* Ws = h->W64;
+  double neg0u = 0.0, neg0v = 0.0;
+  ENMF_TRY(negativity(h, Ws, mr * r, &neg0u));
+  ENMF_TRY(negativity(h, Ws + mr * r, n * r, &neg0v));
+  // max |W_svd| for R34
+  colabsmax(Ws, rows, r, 0, h->parts, h->st);
+  std::vector<double> hp((size_t)colabsmax_parts() * r * 3);
+  CUDA_TRY(cudaMemcpyAsync(hp.data(), h->parts, sizeof(double) * hp.size(),
+                           cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  double wmax = 0.0;
+  for (size_t e = 0; e < hp.size(); e += 3) wmax = std::max(wmax, hp[e]);
+  const double pen = h->opt.admm_rho > 0.0 ? h->opt.admm_rho : 1e-3 / (wmax > 0.0 ? wmax : 1.0);
+  const double rho = pen, gamma = pen, t = pen;
+  // R35: R1 = R2 = I, Lambda = I, W1 = W2 = W3 = W_svd, M = N = P = 0
+  std::vector<double> eye((size_t)r * r, 0.0), ones(r, 1.0);
+  for (int a = 0; a < r; ++a) eye[(size_t)a * r + a] = 1.0;
+  CUDA_TRY(cudaMemcpyAsync(R1, eye.data(), sizeof(double) * r * r, cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaMemcpyAsync(R2, eye.data(), sizeof(double) * r * r, cudaMemcpyHostToDevice, h->st));
+  CUDA_TRY(cudaMemcpyAsync(lam, ones.data(), sizeof(double) * r, cudaMemcpyHostToDevice, h->st));
+  for (double* A : {W2, WsR1, W2R2})
+    CUDA_TRY(cudaMemcpyAsync(A, Ws, sizeof(double) * count, cudaMemcpyDeviceToDevice, h->st));
+  for (double* A : {M, N, P}) CUDA_TRY(cudaMemsetAsync(A, 0, sizeof(double) * count, h->st));
+  GemmOut o;
+  o.ldc = r;
+  auto polar = [&](double* R) {      // R = polar(Mr) = C D^T (Procrustes), as rotate_core
+    polar_ns(Mr, r, R, nsst, nsw, 40, h->st);
+    polar_newton(Mr, r, R, pfail, h->st, nullptr, nsst + 1);
+    jacobi_svd(Mr, r, Cs, sv, Ds, jw, h->st, nullptr, pfail);
+    procrustes_from_svd(Cs, sv, Ds, r, R, h->st, pfail);
+  };
+  for (int it = 0; it < h->opt.admm_iters; ++it) {
+    // (W1, W3) <- argmin f1 from W_svd R1, W2 R2 of the previous iterate
+    rsr_w13(WsR1, W2R2, M, N, W2, P, lam, rows, mr, r, rho, gamma, t, W1, W3, h->st);
+    // R1 <- Procrustes(W_svd, W1 + M); W2 <- argmin f2 with G = (W3 + P) R2^T
+    rsr_add(W1, M, count, B, h->st);
+    o.C = Mr;
+    gemm<double, double>(true, Ws, r, B, r, r, r, rows, o, h->work, h->work_elems, h->st);
+    if (polar_supported(r)) {
+      polar(R1);
+    } else {
+      jacobi_svd(Mr, r, Cs, sv, Ds, jw, h->st);
+      procrustes_from_svd(Cs, sv, Ds, r, R1, h->st);
+    }
+    rsr_add(W3, P, count, B, h->st);                    // B = W3 + P (f2 and f3)
+    rsr_transpose(R2, r, R2t, h->st);
+    o.C = G;
+    gemm<double, double>(false, B, r, R2t, r, rows, r, r, o, h->work, h->work_elems, h->st);
+    rsr_w2(W1, N, G, lam, rows, mr, r, gamma, t, W2, h->st);
+    // R2 <- Procrustes(W2, W3 + P); Lambda <- the quartic roots
+    o.C = Mr;
+    gemm<double, double>(true, W2, r, B, r, r, r, rows, o, h->work, h->work_elems, h->st);
+    if (polar_supported(r)) {
+      polar(R2);
+    } else {
+      jacobi_svd(Mr, r, Cs, sv, Ds, jw, h->st);
+      procrustes_from_svd(Cs, sv, Ds, r, R2, h->st);
+    }
+    rsr_lambda(W1, W2, N, rows, mr, r, cp, abcd, lam, h->st);
+    // multipliers with the new R1, R2, Lambda
+    o.C = WsR1;
+    gemm<double, double>(false, Ws, r, R1, r, rows, r, r, o, h->work, h->work_elems, h->st);
+    o.C = W2R2;
+    gemm<double, double>(false, W2, r, R2, r, rows, r, r, o, h->work, h->work_elems, h->st);
+    rsr_dual(W1, WsR1, W2, W3, W2R2, lam, rows, mr, r, M, N, P, h->st);
+  }
+  ENMF_TRY(check_launch());
+  // (U, V) = (U* R1 Lambda R2, V* R1 Lambda^-1 R2)   (Eq. gen_2)
+  CUDA_TRY(cudaMemcpyAsync(B, WsR1, sizeof(double) * count, cudaMemcpyDeviceToDevice, h->st));
+  rsr_scale(B, lam, rows, mr, r, h->st);
+  o.C = G;
+  gemm<double, double>(false, B, r, R2, r, rows, r, r, o, h->work, h->work_elems, h->st);
+  f64_to_f32(G, mr, r, nullptr, U, ldu, h->st);
+  f64_to_f32(G + mr * r, n, r, nullptr, V, ldv, h->st);
+  double negu = 0.0, negv = 0.0;
+  ENMF_TRY(negativity(h, G, mr * r, &negu));
+  ENMF_TRY(negativity(h, G + mr * r, n * r, &negv));
+  std::vector<double> hl(r);
+  CUDA_TRY(cudaMemcpyAsync(hl.data(), lam, sizeof(double) * r, cudaMemcpyDeviceToHost, h->st));
+  ENMF_TRY(min_factor(h, U, ldu, mr, S_MINU, false));
+  ENMF_TRY(min_factor(h, V, ldv, n, S_MINV, false));
+  double mins[2];
+  CUDA_TRY(cudaMemcpyAsync(mins, h->dscal + S_MINU, sizeof(mins), cudaMemcpyDeviceToHost, h->st));
+  CUDA_TRY(cudaStreamSynchronize(h->st));
+  ENMF_TRY(check_launch());
+  const double L = (double)h->opt.lift_steps;
+  const double lu = mins[0] < 0 ? (1.0 + 1e-3) * (-mins[0]) / L : 0.0;
+  const double lv = mins[1] < 0 ? (1.0 + 1e-3) * (-mins[1]) / L : 0.0;
+  ENMF_TRY(enmf_set_stage(h, 0, lu, lv));
+  if (lam_host)
+    for (int k = 0; k < r; ++k) lam_host[k] = hl[k];
+  if (info) {
+    info->negativity_svd = neg0u + neg0v;
+    info->negativity_rot = negu + negv;
+    info->lambda_u = lu;
+    info->lambda_v = lv;
+  }
+  return ENMF_OK;
+}
+
 enmf_status_t xnorm2_host(enmf_handle_t h, double* out) {
   CUDA_TRY(cudaMemcpyAsync(out, h->dscal + S_XNORM2, sizeof(double), cudaMemcpyDeviceToHost,
                            h->st));
@@ -406,6 +648,17 @@ enmf_status_t enmf_svd(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t
   return svd_core(h, U, ldu, V, ldv, sigma_host, nullptr);
 }
 
+enmf_status_t enmf_softimpute(enmf_handle_t h, const float* U0, int64_t ldu0, int iters,
+                              float* U, int64_t ldu, float* V, int64_t ldv, double* d_host) {
+  if (!h || iters < 1) return ENMF_ERR_INVALID_ARG;
+  if (!h->bound || !h->nmc) return ENMF_ERR_STATE;
+  ENMF_TRY(validate_ld(U0, ldu0, h->r));
+  ENMF_TRY(validate_ld(U, ldu, h->r));
+  ENMF_TRY(validate_ld(V, ldv, h->r));
+  LaunchScope ls(h);
+  return softimpute_core(h, U0, ldu0, iters, U, ldu, V, ldv, d_host);
+}
+
 enmf_status_t enmf_rotate(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
                           enmf_init_info_t* info) {
   if (!h) return ENMF_ERR_INVALID_ARG;
@@ -417,6 +670,22 @@ enmf_status_t enmf_rotate(enmf_handle_t h, float* U, int64_t ldu, float* V, int6
   f32_to_f64(U, ldu, h->m_loc, h->r, h->W64, h->st);
   f32_to_f64(V, ldv, h->n, h->r, h->W64 + h->m_loc * h->r, h->st);
   ENMF_TRY(rotate_core(h, U, ldu, V, ldv, info));
+  if (info) ENMF_TRY(xnorm2_host(h, &info->xnorm2));
+  return ENMF_OK;
+}
+
+enmf_status_t enmf_rotate_rsr(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                              enmf_init_info_t* info, double* lambda_host) {
+  if (!h) return ENMF_ERR_INVALID_ARG;
+  if (!h->bound) return ENMF_ERR_STATE;
+  if (h->prob.world_size != 1) return ENMF_ERR_STATE;
+  ENMF_TRY(validate_ld(U, ldu, h->r));
+  ENMF_TRY(validate_ld(V, ldv, h->r));
+  LaunchScope ls(h);
+  if (!h->W64) ENMF_TRY(dalloc(&h->W64, (size_t)((h->m_loc + h->n) * h->r)));
+  f32_to_f64(U, ldu, h->m_loc, h->r, h->W64, h->st);
+  f32_to_f64(V, ldv, h->n, h->r, h->W64 + h->m_loc * h->r, h->st);
+  ENMF_TRY(rsr_core(h, U, ldu, V, ldv, info, lambda_host));
   if (info) ENMF_TRY(xnorm2_host(h, &info->xnorm2));
   return ENMF_OK;
 }

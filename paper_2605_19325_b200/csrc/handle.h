@@ -69,6 +69,7 @@ struct enmf_handle_s {
   // sparse X (enmf_set_data_csr): this rank's rows as CSR (caller-owned) and a handle-owned
   // CSC copy for X^T U
   bool sparse = false;
+  bool nmc = false;           // eNMC (enmf_set_data_masked): stored entries are the OBSERVED ones
   const int64_t* csr_ptr = nullptr;
   const int32_t* csr_col = nullptr;
   const float* csr_val = nullptr;

@@ -116,6 +116,46 @@ void pbcd_commit(float* F, int64_t ldf, int64_t rows, int r, const float* snaps,
                  const double* pgparts, double eps, int max_iter, int* kstar,
                  const int* stage, double* minparts, bool tiled, cudaStream_t st,
                  unsigned long long* colmax = nullptr);
+// eNMC PBCD of one block (App. C; kernels_rows.cu nmc_pbcd_kernel): F (rows x r, ld) with the
+// other factor O (ld ldo) fixed, the block's observed entries as CSR lists (ptr rows + 1,
+// idx, val); lift, mask, all max_iter inner iterations with snapshots and per-iteration
+// ||M o grad||^2 partials into pgparts[nmc_pbcd_parts()][max_iter + 1] -- commit with
+// pbcd_commit(..., tiled = false).  r <= 64.
+bool nmc_supported(int r);
+int nmc_pbcd_parts();
+void nmc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const int64_t* ptr,
+                   const int32_t* idx, const float* val, const float* O, int64_t ldo,
+                   const double* lam, int max_iter, float* snaps, double* pgparts,
+                   cudaStream_t st);
+// eNMC (nmc.cu): a softImpute-ALS half step T = S^T U + B o D (or S V + A o D) with the
+// residual S = x - A B^T on the observed entries of the CSR / CSC lists (r <= 64); the
+// masked objective sum (x_ij - u_i . v_j)^2 into *out (parts >= nmc_objective_parts());
+// D~ = sqrt(sigma), 1 / sigma from the eigenvalues sigma^2 of T^T T.
+void nmc_resid_spmm(const int64_t* ptr, const int32_t* idx, const float* val, int64_t rows,
+                    int r, const double* Fr, const double* O1, const double* O2,
+                    const double* dsc, double* out, cudaStream_t st);
+int nmc_objective_parts();
+void nmc_objective(const int64_t* ptr, const int32_t* idx, const float* val, int64_t rows, int r,
+                   const float* U, int64_t ldu, const float* V, int64_t ldv, double* parts,
+                   double* out, cudaStream_t st);
+void nmc_svals(const double* sv, int r, double* d, double* inv, cudaStream_t st);
+// RSR-ADMM (rsr.cu; App. A): per-entry updates of the split variables of
+// Alg. alg:rsr over (rows x r) arrays whose first mu rows are the U block, the lambda solve
+// (parts >= rsr_colsum_parts() * 4 r, abcd >= 4 r), the multiplier step and the final scaling.
+int rsr_colsum_parts();
+void rsr_w13(const double* WsR1, const double* W2R2, const double* M, const double* N,
+             const double* W2, const double* P, const double* lam, int64_t rows, int64_t mu,
+             int r, double rho, double gamma, double t, double* W1, double* W3, cudaStream_t st);
+void rsr_w2(const double* W1, const double* N, const double* G, const double* lam, int64_t rows,
+            int64_t mu, int r, double gamma, double t, double* W2, cudaStream_t st);
+void rsr_add(const double* A, const double* B, int64_t count, double* out, cudaStream_t st);
+void rsr_transpose(const double* R, int r, double* Rt, cudaStream_t st);
+void rsr_lambda(const double* W1, const double* W2, const double* N, int64_t rows, int64_t mu,
+                int r, double* parts, double* abcd, double* lam, cudaStream_t st);
+void rsr_dual(const double* W1, const double* WsR1, const double* W2, const double* W3,
+              const double* W2R2, const double* lam, int64_t rows, int64_t mu, int r, double* M,
+              double* N, double* P, cudaStream_t st);
+void rsr_scale(double* A, const double* lam, int64_t rows, int64_t mu, int r, cudaStream_t st);
 // KKT partial statistics of one block (F, C = cross term, G): 8 values per warp slot.
 void kkt_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
               const double* G, double* parts, cudaStream_t st);

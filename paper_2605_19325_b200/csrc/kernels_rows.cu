@@ -529,6 +529,118 @@ kkt_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
   }
 }
 
+// eNMC PBCD (App. C, Alg. NMC): Alg. 2 with the masked gradient
+// grad_i = sum_{j in E_i} (u_i . o_j - x_ij) o_j = u_i G_i - c_i, where G_i = sum_{j in E_i}
+// o_j o_j^T and c_i = sum_{j in E_i} x_ij o_j run over the OBSERVED entries E_i of row i
+// (CSR lists ptr / idx / val; o_j = row j of the other factor O).  One warp per row: G_i is
+// accumulated in the warp's shared slice from the row's observed entries (each lane owns
+// columns lane + 32 c, no two lanes write one word), then the inner iterations run exactly as
+// pbcd_kernel's with G_i in place of the block Gram -- including the Eq.(10)-type step, which
+// for the masked objective is ||g_i||^2 / sum_{j in E_i} (g_i . o_j)^2 = ||g_i||^2 / g_i G_i
+// g_i^T (reading R30).  Lift, mask, snapshots and the per-iteration ||M o grad||^2 partials
+// as pbcd_kernel (the global stopping rule is applied by pbcd_commit).
+template <int CPL, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS)
+nmc_pbcd_kernel(const float* __restrict__ F, int64_t ldf, int64_t rows, int r,
+                const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                const float* __restrict__ val, const float* __restrict__ O, int64_t ldo,
+                const double* __restrict__ lam_ptr, int max_iter, float* __restrict__ snaps,
+                double* __restrict__ pgparts) {
+  constexpr int RP = 32 * CPL;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* Gs = smem + warp * (RP * RP + RP);
+  double* Ss = Gs + RP * RP;
+  double* pgw = smem + WARPS * (RP * RP + RP);        // [WARPS][max_iter + 1]
+  const double lam = *lam_ptr;
+  for (int e = threadIdx.x; e < WARPS * (max_iter + 1); e += blockDim.x) pgw[e] = 0.0;
+  __syncthreads();
+  double* mypg = pgw + warp * (max_iter + 1);
+  const int64_t snap_stride = rows * (int64_t)r;
+  for (int64_t row = (int64_t)blockIdx.x * WARPS + warp; row < rows;
+       row += (int64_t)gridDim.x * WARPS) {
+    for (int e = lane; e < RP * RP; e += 32) Gs[e] = 0.0;
+    double cc[1][CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) cc[0][c] = 0.0;
+    for (int64_t e = ptr[row]; e < ptr[row + 1]; ++e) {
+      const int64_t j = idx[e];
+      const double x = (double)val[e];
+      double o[CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int col = lane + 32 * c;
+        o[c] = col < r ? (double)O[j * ldo + col] : 0.0;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) Ss[lane + 32 * c] = o[c];
+      __syncwarp();
+      for (int l = 0; l < r; ++l) {
+        const double ol = Ss[l];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) Gs[l * RP + lane + 32 * c] = fma(ol, o[c], Gs[l * RP + lane + 32 * c]);
+      }
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) cc[0][c] = fma(x, o[c], cc[0][c]);
+    }
+    __syncwarp();
+    double u[1][CPL], gr[1][CPL];
+    bool msk[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int col = lane + 32 * c;
+      const bool ok = col < r;
+      double v = ok ? (double)F[row * ldf + col] : 0.0;
+      if (v < 0.0) v += lam;                      // Eq.(6)/(7) lift of I_-
+      u[0][c] = v;
+      msk[c] = ok && v >= 0.0;                    // M_{U+} after the lift (R14)
+      gr[0][c] = -cc[0][c];
+    }
+    row_times_gram<CPL, 1>(u, Gs, Ss, r, lane, 1.0, gr);   // grad = u G_i - c_i
+    {
+      double sg = 0.0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) sg += msk[c] ? gr[0][c] * gr[0][c] : 0.0;
+      sg = warp_sum(sg);
+      if (lane == 0) mypg[0] += sg;
+    }
+    for (int it = 1; it <= max_iter; ++it) {
+      double g[1][CPL], gG[1][CPL];
+      double sn = 0.0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        g[0][c] = msk[c] ? gr[0][c] : 0.0;
+        sn += g[0][c] * g[0][c];
+        gG[0][c] = 0.0;
+      }
+      const double num = warp_sum(sn);
+      row_times_gram<CPL, 1>(g, Gs, Ss, r, lane, 1.0, gG);  // g G_i
+      double sd = 0.0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) sd += gG[0][c] * g[0][c];
+      const double den = warp_sum(sd);
+      const double d = den > 0.0 ? num / den : 0.0;          // reading R30
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        if (msk[c]) u[0][c] = fmax(0.0, u[0][c] - d * gr[0][c]);   // Eq.(8)
+        const int col = lane + 32 * c;
+        if (col < r) snaps[(int64_t)(it - 1) * snap_stride + row * r + col] = (float)u[0][c];
+        gr[0][c] = -cc[0][c];
+      }
+      row_times_gram<CPL, 1>(u, Gs, Ss, r, lane, 1.0, gr);
+      double s2 = 0.0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) s2 += msk[c] ? gr[0][c] * gr[0][c] : 0.0;
+      s2 = warp_sum(s2);
+      if (lane == 0) mypg[it] += s2;
+    }
+  }
+  __syncwarp();
+  for (int it = lane; it <= max_iter; it += 32)
+    pgparts[((int64_t)blockIdx.x * WARPS + warp) * (max_iter + 1) + it] = mypg[it];
+}
+
 template <int CPL>
 size_t row_smem(int extra_doubles, int rb = 4) {
   return sizeof(double) * (size_t)(32 * CPL * 32 * CPL + kRowWarps * rb * 32 * CPL + extra_doubles);
@@ -600,6 +712,32 @@ void pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C
   ENMF_CPL_DISPATCH(r, CALL);
 #undef CALL
   count_launch();
+}
+
+bool nmc_supported(int r) { return r >= 1 && r <= 64; }
+int nmc_pbcd_parts() { return kRowGrid * 8; }
+
+void nmc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const int64_t* ptr,
+                   const int32_t* idx, const float* val, const float* O, int64_t ldo,
+                   const double* lam, int max_iter, float* snaps, double* pgparts,
+                   cudaStream_t st) {
+  // rows beyond the grid's warps are strided; blocks x warps = nmc_pbcd_parts() slots (the
+  // 4-warp CPL = 2 form leaves the upper half of the slots zero)
+  cudaMemsetAsync(pgparts, 0, sizeof(double) * (size_t)nmc_pbcd_parts() * (max_iter + 1), st);
+  if (r <= 32) {
+    auto k = nmc_pbcd_kernel<1, 8>;
+    const size_t sm = sizeof(double) * (size_t)(8 * (32 * 32 + 32) + 8 * (max_iter + 1));
+    set_smem(k, sm);
+    k<<<kRowGrid, 256, sm, st>>>(F, ldf, rows, r, ptr, idx, val, O, ldo, lam, max_iter, snaps,
+                                 pgparts);
+  } else {
+    auto k = nmc_pbcd_kernel<2, 4>;
+    const size_t sm = sizeof(double) * (size_t)(4 * (64 * 64 + 64) + 4 * (max_iter + 1));
+    set_smem(k, sm);
+    k<<<kRowGrid, 128, sm, st>>>(F, ldf, rows, r, ptr, idx, val, O, ldo, lam, max_iter, snaps,
+                                 pgparts);
+  }
+  count_launch(2);
 }
 
 void pbcd_commit(float* F, int64_t ldf, int64_t rows, int r, const float* snaps,

@@ -89,7 +89,10 @@ def test_two_ranks_hals_match_single_rank(cfg_args, prec):
     assert np.array_equal(r0["f"], r1["f"])
     _, f, U, V = _single(cfg_args, prec, "hals")
     Ug = np.vstack([r0["U"], r1["U"]])
-    tol = 1e-9 if prec == FP64 else 2e-6
+    # tensor-core path: each rank packs its own digit scales (the X^T copy's column scales
+    # and the factor's column maxima are per rank), so one rank and two ranks round the
+    # operands differently at the path's ~2^-22 -- held to BASELINE's per-update 1e-5
+    tol = 1e-9 if prec == FP64 else 1e-5
     eu = np.linalg.norm(Ug - U) / np.linalg.norm(U)
     ev = np.linalg.norm(r0["V"] - V) / np.linalg.norm(V)
     ef = np.max(np.abs(r0["f"] - f) / f)

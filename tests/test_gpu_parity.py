@@ -98,17 +98,18 @@ def test_hals_sweep_rows_outgrowing_digit_scale(cfg, prec):
 @pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
 def test_hals_keeps_tiny_positive_entries(prec):
     """The HALS projection is max(0, .): legitimately tiny positive entries
-    survive.  Planted X = U0 V0^T (fp32) with a quarter of U0's entries at 2^-20 of their row's
+    survive.  Planted X = U0 V0^T (fp32) with a quarter of U0's entries at 2^-19 of their row's
     maximum, started at the planted point (a fixed point of the exact update): after one
-    sweep every tiny entry is still positive and within 2^-20 of its row maximum of the
-    oracle's value (the tensor-core HALS's zero snap, reading R28, acts only below 2^-22 of
-    the row maximum), and the factors match at 1e-5."""
+    sweep every tiny entry is still positive and within 2^-21 of its row maximum of the
+    oracle's value (the tensor-core path's operands carry ~2^-22 of their scale group's
+    maximum; its HALS zero snap, reading R28, acts only below 2^-22 of the row maximum --
+    the round-1 snap at 2^-18 zeroed these entries), and the factors match at 1e-5."""
     g = np.random.default_rng(5)
     m, n, r = 300, 260, 16
     U0 = 0.5 + g.random((m, r))
     V0 = 0.5 + g.random((n, r))
     tiny = g.random((m, r)) < 0.25
-    U0[tiny] *= 2.0 ** -20
+    U0[tiny] *= 2.0 ** -19
     U0 = U0.astype(np.float32).astype(np.float64)
     V0 = V0.astype(np.float32).astype(np.float64)
     X = (U0 @ V0.T).astype(np.float32)
@@ -123,7 +124,7 @@ def test_hals_keeps_tiny_positive_entries(prec):
     print(f"prec={h.precision}: {tiny.sum()} tiny entries, min gpu {Ug[tiny].min():.3e}, max "
           f"deviation {dev.max():.2e} of the row max; U {rel_fro(Ug, Uo):.2e} V {rel_fro(Vg, Vo):.2e}")
     assert np.all(Ug[tiny] > 0)
-    assert dev.max() < 2.0 ** -20
+    assert dev.max() < 2.0 ** -21
     assert rel_fro(Ug, Uo) < 1e-5 and rel_fro(Vg, Vo) < 1e-5
 
 
@@ -373,10 +374,12 @@ def test_tc_contractions_match_oracle(cfg, signed, pair, monkeypatch):
     assert ep.max() < 2e-6 and eq.max() < 2e-6
     if not signed:
         assert rel_fro(P, Pr) < 1e-7 and rel_fro(Q, Qr) < 1e-7
+    # the trace-form objective of the quantised operands (tc_gemm.cu): first-order error
+    # 2 <E, X - U V^T> with |E| <= 2^-22 of the scale groups' maxima, plus the dropped
+    # products' noise -- the bound test_objective_and_kkt states
     f_d = oracle.frob2_direct(X, U0, V0)
-    rel_cross = abs(h.objective(to_dev(U0), to_dev(V0), exact=False) - f_d) / \
-        (2 * abs(float((Qr * V0).sum())))
-    assert rel_cross < 1e-8
+    f_t = h.objective(to_dev(U0), to_dev(V0), exact=False)
+    assert abs(f_t - f_d) < 1e-6 * f_d + 1e-10 * oracle.xnorm2(X)
 
 
 # ----------------------------------------------------------------------------- edges
