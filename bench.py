@@ -41,6 +41,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-ablation", action="store_true")
     p.add_argument("--cpu-sample-rows", type=int, default=0)
+    p.add_argument("--no-small", action="store_true",
+                   help="skip the C1-C4 / eNMC rates reported in config.small_configs")
     return p.parse_args()
 
 
@@ -213,6 +215,78 @@ def x_pass_roofline(precision, prof, rows, n, r, peaks, peak_kind, traffic_j, st
                         "(3 B per element)") if tc else "fp64 FMA (SIMT)",
             "passes": passes,
             "share_of_step": (prof["xv"][0] + prof["xtu"][0]) / max(step_ms, 1e-9)}
+
+
+def small_config_rates(stream):
+    """Rates of the four small BASELINE configs (C1-C4: latency / ALU bound,
+    X cache resident) over their full sweep counts, each from its own init (randomised SVD +
+    rotation, reported separately), single GPU, and eNMC (App. C) on the C4 ratings matrix
+    with the stored ratings as the observed entries.  GB/s over X is an EFFECTIVE rate
+    (2 m n 4 B per sweep; X stays in L2 / shared memory), labelled so."""
+    import torch
+    import paper_2605_19325_b200 as E
+    import synth
+    out = {}
+    for cfg in (synth.C1, synth.C2, synth.C3, synth.C4):
+        X = torch.empty(cfg.m, cfg.n, device="cuda", dtype=torch.float32)
+        synth.x_rows_device(cfg, 0, cfg.m, X, stream.cuda_stream)
+        U = torch.empty(cfg.m, cfg.r, device="cuda")
+        V = torch.empty(cfg.n, cfg.r, device="cuda")
+        h = E.Enmf(cfg.m, cfg.n, cfg.r, stream=stream)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h.init(X, U, V)
+        torch.cuda.synchronize()
+        init_s = time.perf_counter() - t0
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = h.launch_count
+        a.record(stream)
+        f, info = h.iterate(U, V, cfg.sweeps)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        lps = (h.launch_count - l0) / cfg.sweeps
+        out[cfg.name] = {"sweeps": cfg.sweeps, "ms": ms, "sweeps_per_s": cfg.sweeps / (ms / 1e3),
+                         "effective_gbs_over_x": 2.0 * cfg.m * cfg.n * 4 * cfg.sweeps / (ms / 1e3) / 1e9,
+                         "ascent_sweeps": info["ascent_sweeps"], "precision_path": h.precision,
+                         "init_s": init_s, "f_last": float(f[-1]),
+                         "kernel_launches_per_sweep": lps,
+                         "x": "effective rate: X (<= 90 MB) stays cache resident"}
+        h.close()
+        del X, U, V
+    # eNMC on the C4 ratings matrix: the ratings are the observed entries (PAPER.md:1369-1371)
+    cfg = synth.C4
+    Xh = synth.x_full(cfg)
+    rows, cols = np.nonzero(Xh > 0)
+    ptr = np.zeros(cfg.m + 1, dtype=np.int64)
+    np.add.at(ptr, rows + 1, 1)
+    ptr = np.cumsum(ptr)
+    dev = (torch.from_numpy(ptr).cuda(), torch.from_numpy(cols.astype(np.int32)).cuda(),
+           torch.from_numpy(Xh[rows, cols].astype(np.float32)).cuda())
+    h = E.Enmf(cfg.m, cfg.n, cfg.r, stream=stream)
+    h.set_data_masked(*dev)
+    U0 = torch.from_numpy(np.random.default_rng(0).standard_normal((cfg.m, cfg.r))
+                          .astype(np.float32)).cuda()
+    U = torch.empty(cfg.m, cfg.r, device="cuda")
+    V = torch.empty(cfg.n, cfg.r, device="cuda")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h.softimpute(U0, 50, U, V)
+    h.rotate(U, V)
+    torch.cuda.synchronize()
+    init_s = time.perf_counter() - t0
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    f, info = h.iterate(U, V, 100)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    out["C4-ratings eNMC (masked, App. C)"] = {
+        "sweeps": 100, "ms": ms, "sweeps_per_s": 100 / (ms / 1e3), "observed": int(len(rows)),
+        "init_s (softImpute 50 + rotation)": init_s, "f_hat_last": float(f[-1]),
+        "rmse_observed": float(np.sqrt(f[-1] / len(rows)))}
+    h.close()
+    return out
 
 
 def run_enmf(args):
@@ -440,6 +514,13 @@ def run_enmf(args):
     h.set_stage(*stage_end)
     del U_rot, V_rot, U_end, V_end
 
+    small = None
+    if rank == 0 and world == 1 and not args.no_small and not sparse:
+        try:
+            small = small_config_rates(stream)
+        except Exception as e:                      # noqa: BLE001 -- never lose the bench line
+            small = {"error": f"{type(e).__name__}: {e}"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s_m, s_n = cpu_block(cfg, args)
@@ -474,7 +555,8 @@ def run_enmf(args):
                        "warmup_sweeps": {"ascent": info_w["ascent_sweeps"],
                                          "hals": info_w["hals_sweeps"]},
                        "stage_rates": stage_rates,
-                       "ablation_post_rotation": ablation},
+                       "ablation_post_rotation": ablation,
+                       "small_configs": small},
             "hbm_gbs_over_x": gbs,
             "init_s": init_s,
             "roofline": roofline,

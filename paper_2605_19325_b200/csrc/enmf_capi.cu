@@ -181,17 +181,13 @@ enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
   // ablation variants (R29): fixed ascent step / projected-gradient descent, step 1/lambda_max(G)
   const double* fstep = nullptr;
   if ((maybe_ascent && h->opt.step_rule) || h->opt.descent) {
-    // stepws: s (128) | Jacobi work (2 x 128^2) | U of the SVD | V of the SVD per block (U
-    // block, V block): the previous sweep's V warm-starts the next Jacobi SVD of the same block's
-    // Gram (the Grams change little between sweeps: a cold 128 x 128 Jacobi took 5.7 ms)
-    if (!h->stepws) ENMF_TRY(dalloc(&h->stepws, (size_t)(128 + 5 * 128 * 128)));
-    double* sv = h->stepws;
-    double* wk = sv + 128;
+    // lambda_max(G) by power iteration, warm-started from the same block's eigenvector of the
+    // previous sweep (stepws: one r-vector per block; a 128 x 128 Jacobi SVD per block update
+    // cost 3.3 ms and confounded the ablation timings)
+    if (!h->stepws) ENMF_TRY(dalloc(&h->stepws, (size_t)(2 * 128)));
     const int blk = lam_slot == S_LAMU ? 0 : 1;
-    double* vb = wk + (size_t)(3 + blk) * 128 * 128;
-    jacobi_svd(G, r, wk + 2 * 128 * 128, sv, vb, wk, h->st, h->step_warm[blk] ? vb : nullptr);
+    lambda_power(G, r, h->stepws + 128 * blk, h->step_warm[blk], h->dscal + S_STEP, h->st);
     h->step_warm[blk] = true;
-    recip_first(h->stepws, h->dscal + S_STEP, h->st);
     fstep = h->dscal + S_STEP;
   }
   if (maybe_ascent) {
@@ -336,8 +332,8 @@ enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ld
     ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
     dot_f64_f32(h->Q, V, ldv, h->n, h->r, h->parts, h->dscal + S_CROSS, st);
   }
-  objective_finish(xnorm2_trace(h), h->dscal + S_CROSS, h->GU, h->GV, (int)h->r,
-                   h->ftrace + t, st);
+  objective_finish(xnorm2_trace(h), h->dscal + S_CROSS, h->GU, h->GV, (int)h->r, h->ftrace,
+                   st, h->dint + I_FCNT);
   return check_launch();
 }
 
@@ -377,7 +373,8 @@ enmf_status_t sweep_nmc(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_
                              h->st2));
   }
   nmc_objective(h->csr_ptr, h->csr_col, h->csr_val, h->m_loc, r, U, ldu, V, ldv, h->minparts,
-                h->ftrace + t, st);        // minparts: kRowGrid = nmc_objective_parts() slots
+                h->dscal + S_FCUR, st);   // minparts: kRowGrid = nmc_objective_parts() slots
+  append_scalar(h->dscal + S_FCUR, h->ftrace, h->dint + I_FCNT, st);
   return check_launch();
 }
 
@@ -491,9 +488,10 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
   if (h->st2) {
     cudaStreamSynchronize(h->st2);
     cudaStreamDestroy(h->st2);
-    cudaEventDestroy(h->ev_a);
     cudaEventDestroy(h->ev_b);
   }
+  if (h->ev_a) cudaEventDestroy(h->ev_a);
+  if (h->cap_st) cudaStreamDestroy(h->cap_st);
   if (h->tc) tc_destroy(h->tc);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   comm_destroy(h->comm);
@@ -792,6 +790,46 @@ enmf_status_t enmf_get_stage(enmf_handle_t h, int* stage, double* lambda_u, doub
 }  // extern "C"
 
 namespace {
+// Capture one sweep (on the handle's capture stream, joined to its stream by events) and
+// launch the graph `count` times on the handle's stream.
+enmf_status_t replay_sweeps(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
+                            bool maybe_ascent, int count) {
+  if (!h->cap_st) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking));
+    if (!h->ev_a) CUDA_TRY(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
+  }
+  cudaStream_t user = h->st;
+  h->st = h->cap_st;
+  const int64_t l0 = h->launches;
+  cudaGraph_t g = nullptr;
+  enmf_status_t s = ENMF_OK;
+  cudaError_t e = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeRelaxed);
+  if (e == cudaSuccess) {
+    s = h->nmc ? sweep_nmc(h, U, ldu, V, ldv, 1, SweepHooks())
+               : sweep(h, U, ldu, V, ldv, 1, maybe_ascent, SweepHooks());
+    e = cudaStreamEndCapture(h->st, &g);
+  }
+  h->st = user;
+  const int64_t per = h->launches - l0;
+  h->launches = l0;
+  if (s != ENMF_OK || e != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    return s != ENMF_OK ? s : ENMF_ERR_CUDA;
+  }
+  cudaGraphExec_t ge = nullptr;
+  e = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  CUDA_TRY(e);
+  for (int k = 0; k < count && e == cudaSuccess; ++k) {
+    e = cudaGraphLaunch(ge, h->st);
+    h->launches += per;
+  }
+  cudaGraphExecDestroy(ge);
+  CUDA_TRY(e);
+  return ENMF_OK;
+}
+
 // The sweep loop behind enmf_iterate and enmf_iterate_host.  hk0 applies to the first sweep
 // (U upload), u_dl_host to the last (U download); v_dl_host receives V at the end.
 enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
@@ -804,17 +842,28 @@ enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int
   ENMF_TRY(ensure_ftrace(h, std::max(n_iters, 1)));
   CUDA_TRY(cudaMemsetAsync(h->dint + I_CNT_ASC, 0, 2 * sizeof(int), h->st));
   CUDA_TRY(cudaMemsetAsync(h->dint + I_HALS_FB, 0, sizeof(int), h->st));
+  CUDA_TRY(cudaMemsetAsync(h->dint + I_FCNT, 0, sizeof(int), h->st));
   // entry state: mins of the factors as given, G_V of the given V (min U after its upload)
   if (!u_ready) ENMF_TRY(min_factor(h, U, ldu, h->m_loc, S_MINU, sh));
   ENMF_TRY(min_factor(h, V, ldv, h->n, S_MINV, false));
   if (!h->nmc) ENMF_TRY(gram_f32(h, V, ldv, h->n, h->GV, false));
   h->umax_valid = h->vmax_valid = false;   // the caller may have changed U / V since
+  // Sweeps 1 .. n-1 of a single-rank call without host transfers issue the same launch
+  // sequence every time (stage, k*, the trace slot are device-side), so one of them is
+  // captured as a CUDA graph and replayed: the small configurations (C1-C4, ~35 launches per
+  // sweep) are bound by launch latency.  ENMF_GRAPH=0 disables it.
+  static const bool graphs = !(getenv("ENMF_GRAPH") && getenv("ENMF_GRAPH")[0] == '0');
+  const bool graph = graphs && !sh && !u_ready && !u_dl_host && !v_dl_host && n_iters >= 3;
   for (int t = 0; t < n_iters; ++t) {
     SweepHooks hk;
     if (t == 0) hk.u_ready = u_ready;
     if (t == n_iters - 1) {
       hk.u_download = u_dl_host;
       hk.v_download = v_dl_host;
+    }
+    if (graph && t == 1) {
+      ENMF_TRY(replay_sweeps(h, U, ldu, V, ldv, maybe_ascent, n_iters - 1));
+      break;
     }
     if (h->nmc)
       ENMF_TRY(sweep_nmc(h, U, ldu, V, ldv, t, hk));

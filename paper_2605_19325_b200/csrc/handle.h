@@ -18,10 +18,13 @@ enum {
   S_XNORM2 = 0, S_XMIN, S_XBAD, S_MINU, S_MINV, S_CROSS, S_LAMU, S_LAMV, S_NEG, S_SCRATCH,
   S_WMAX, S_STEP,
   S_XQNORM2,   // ||X~||^2 of the tensor-core path's quantised X (trace-form objective)
+  S_FCUR,      // the current sweep's objective before it is appended to the trace
   S_COUNT = 16
 };
 // device int slots
-enum { I_STAGE = 0, I_KSTAR_U, I_KSTAR_V, I_CNT_ASC, I_CNT_HALS, I_BAD, I_HALS_FB, I_HALS_ILL, I_COUNT = 8 };
+enum { I_STAGE = 0, I_KSTAR_U, I_KSTAR_V, I_CNT_ASC, I_CNT_HALS, I_BAD, I_HALS_FB, I_HALS_ILL,
+       I_FCNT,   // next slot of the objective trace (sweeps append; graph replays share args)
+       I_COUNT = 9 };
 
 }  // namespace enmf
 
@@ -92,6 +95,7 @@ struct enmf_handle_s {
   float* Ud = nullptr;
   float* Vd = nullptr;
   cudaStream_t st2 = nullptr;
+  cudaStream_t cap_st = nullptr;   // non-blocking stream a sweep is captured on (CUDA graph)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   float* x_owned = nullptr;  // device copy of X owned by enmf_solve_host
   double* W64 = nullptr;     // (m_loc + n) x r fp64 [U*; V*] kept from enmf_svd for enmf_rotate

@@ -106,6 +106,9 @@ void pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C
 void pgd_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
               const int* stage, const double* step, double* minparts, cudaStream_t st,
               unsigned long long* colmax = nullptr);
+// *out = 1 / lambda_max(G) by power iteration warm-started from v (r values, updated) -- the
+// fixed step of the ablation variants (R29); one CTA, r <= 128.
+void lambda_power(const double* G, int r, double* v, bool warm, double* out, cudaStream_t st);
 // *out = 1 / s[0] (0 if s[0] <= 0): the fixed step 1 / lambda_max from a singular-value list.
 void recip_first(const double* s, double* out, cudaStream_t st);
 int pbcd_parts();
@@ -196,9 +199,13 @@ void polar_ns(const double* M, int k, double* R, int* state, double* work, int m
 // stage[0]: 0 ascent, 1 HALS.  Switches to HALS when min U >= 0 and min V >= 0.
 void stage_update(int* stage, const double* minu, const double* minv, int* counters,
                   cudaStream_t st);
-// f = xnorm2 - 2 cross + gg, stored to *fout.
+// f = xnorm2 - 2 cross + gg, stored to *fout -- or, with slot (device int), to fout[*slot]
+// and ++*slot (the objective trace: one launch sequence per sweep, replayable as a graph).
 void objective_finish(const double* xnorm2, const double* cross, const double* gu,
-                      const double* gv, int r, double* fout, cudaStream_t st);
+                      const double* gv, int r, double* fout, cudaStream_t st,
+                      int* slot = nullptr);
+// dst[*slot] = *src; ++*slot.
+void append_scalar(const double* src, double* dst, int* slot, cudaStream_t st);
 // min over partial buffers.
 void reduce_min(const double* parts, int n, double* out, cudaStream_t st);
 // ADMM elementwise step (see kernels_small.cu).

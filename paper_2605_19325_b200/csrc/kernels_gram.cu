@@ -12,6 +12,8 @@
 // split across a persistent grid (two CTAs per SM); a CTA stages 32 rows at a time in shared
 // memory as fp64 and every thread runs 64 FMAs per row from 16 shared loads.  Per-CTA partials
 // are summed in a fixed order (reduce_parts) and mirrored: deterministic.
+#include <algorithm>
+
 #include "internal.h"
 
 namespace enmf {
@@ -110,8 +112,12 @@ bool gram_supported(int r) { return r >= 1 && r <= 128; }
 
 void gram_sym(const float* A, int64_t lda, int64_t rows, int r, double* parts, double* Gu,
               double* G, cudaStream_t st, const double* qscale) {
-  gram_upper_kernel<<<kGramGrid, kGramThreads, 0, st>>>(A, lda, rows, r, qscale, parts);
-  reduce_parts(parts, kGramGrid, 128 * 128, Gu, st);
+  // every CTA writes a 128 x 128 partial (131 KB) that the reduction reads back: with few rows
+  // (a rank's U block at 8 GPUs, the V block) 296 partials cost more than the Gram itself,
+  // so the grid shrinks to one CTA per 128 rows (deterministic for a given row count)
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kGramGrid, (rows + 127) / 128));
+  gram_upper_kernel<<<grid, kGramThreads, 0, st>>>(A, lda, rows, r, qscale, parts);
+  reduce_parts(parts, grid, 128 * 128, Gu, st);
   gram_mirror_kernel<<<(r * r + 255) / 256, 256, 0, st>>>(Gu, r, G);
   count_launch(2);
 }

@@ -369,6 +369,49 @@ pgd_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r, const double
   }
 }
 
+// lambda_max of the block's Gram G (r x r, symmetric PSD) by power iteration, warm-started from
+// the previous sweep's eigenvector v (r values, kept by the caller; all ones if !warm): thread k
+// owns component k; stop when the Rayleigh quotient changes by <= 1e-15 relative in 3
+// consecutive steps (the Grams change little between sweeps: a few steps) or after max_it.
+// out = 1 / lambda_max (0 if lambda_max <= 0): the fixed step of reading R29.
+__global__ void __launch_bounds__(128) lambda_power_kernel(const double* __restrict__ G, int r,
+                                                           double* v, int warm, int max_it,
+                                                           double* out) {
+  __shared__ double x[128];
+  __shared__ double red[4], red2[4];
+  const int k = threadIdx.x, lane = k & 31, w = k >> 5;
+  x[k] = k < r ? (warm ? v[k] : 1.0) : 0.0;
+  __syncthreads();
+  double rq_prev = 0.0, rq = 0.0;
+  int stable = 0;
+  for (int it = 0; it < max_it && stable < 3; ++it) {
+    double y = 0.0;
+    if (k < r)
+      for (int l = 0; l < r; ++l) y = fma(G[(int64_t)k * r + l], x[l], y);
+    double a = x[k] * y, b = y * y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) { red[w] = a; red2[w] = b; }
+    __syncthreads();
+    const double xy = (red[0] + red[1]) + (red[2] + red[3]);
+    const double yy = (red2[0] + red2[1]) + (red2[2] + red2[3]);
+    double xx = 0.0;
+    for (int l = 0; l < r; ++l) xx = fma(x[l], x[l], xx);
+    rq = xx > 0.0 ? xy / xx : 0.0;
+    stable = fabs(rq - rq_prev) <= 1e-15 * fabs(rq) ? stable + 1 : 0;
+    rq_prev = rq;
+    __syncthreads();
+    if (!(yy > 0.0)) break;
+    x[k] = y / sqrt(yy);
+    __syncthreads();
+  }
+  if (k < r) v[k] = x[k];
+  if (k == 0) *out = rq > 0.0 ? 1.0 / rq : 0.0;
+}
+
 __global__ void recip_first_kernel(const double* s, double* out) {
   if (threadIdx.x == 0) *out = s[0] > 0.0 ? 1.0 / s[0] : 0.0;
 }
@@ -688,6 +731,11 @@ void pgd_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const
   }
   ENMF_CPL_DISPATCH(r, CALL);
 #undef CALL
+  count_launch();
+}
+
+void lambda_power(const double* G, int r, double* v, bool warm, double* out, cudaStream_t st) {
+  lambda_power_kernel<<<1, 128, 0, st>>>(G, r, v, warm ? 1 : 0, 2000, out);
   count_launch();
 }
 

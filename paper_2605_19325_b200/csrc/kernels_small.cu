@@ -193,7 +193,7 @@ __global__ void stage_update_kernel(int* stage, const double* minu, const double
 
 __global__ void objective_finish_kernel(const double* xnorm2, const double* cross,
                                         const double* gu, const double* gv, int r,
-                                        double* fout) {
+                                        double* fout, int* slot) {
   __shared__ double red[256];
   double s = 0.0;
   const int nn = r * r;     // <= 128^2 = 64 x 256
@@ -210,7 +210,11 @@ __global__ void objective_finish_kernel(const double* xnorm2, const double* cros
     for (int q = 0; q < 16; ++q) s += a[q] * b[q];
   }
   s = block_reduce<0>(s, red);
-  if (threadIdx.x == 0) *fout = *xnorm2 - 2.0 * (*cross) + s;
+  if (threadIdx.x == 0) fout[slot ? (*slot)++ : 0] = *xnorm2 - 2.0 * (*cross) + s;
+}
+
+__global__ void append_scalar_kernel(const double* src, double* dst, int* slot) {
+  if (threadIdx.x == 0) dst[(*slot)++] = *src;
 }
 
 // ADMM elementwise part of one step (Alg. 1 lines 171-173 with scaled dual Yh = Y/rho):
@@ -858,8 +862,13 @@ void stage_update(int* stage, const double* minu, const double* minv, int* count
 }
 
 void objective_finish(const double* xnorm2, const double* cross, const double* gu,
-                      const double* gv, int r, double* fout, cudaStream_t st) {
-  objective_finish_kernel<<<1, 256, 0, st>>>(xnorm2, cross, gu, gv, r, fout);
+                      const double* gv, int r, double* fout, cudaStream_t st, int* slot) {
+  objective_finish_kernel<<<1, 256, 0, st>>>(xnorm2, cross, gu, gv, r, fout, slot);
+  count_launch();
+}
+
+void append_scalar(const double* src, double* dst, int* slot, cudaStream_t st) {
+  append_scalar_kernel<<<1, 32, 0, st>>>(src, dst, slot);
   count_launch();
 }
 
