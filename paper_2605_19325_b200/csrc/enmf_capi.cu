@@ -813,6 +813,8 @@ enmf_status_t replay_sweeps(enmf_handle_t h, float* U, int64_t ldu, float* V, in
   const int64_t per = h->launches - l0;
   h->launches = l0;
   if (s != ENMF_OK || e != cudaSuccess) {
+    fprintf(stderr, "enmf: sweep graph capture failed (status %d): %s\n", (int)s,
+            cudaGetErrorString(e));
     if (g) cudaGraphDestroy(g);
     cudaGetLastError();
     return s != ENMF_OK ? s : ENMF_ERR_CUDA;
@@ -852,8 +854,11 @@ enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int
   // sequence every time (stage, k*, the trace slot are device-side), so one of them is
   // captured as a CUDA graph and replayed: the small configurations (C1-C4, ~35 launches per
   // sweep) are bound by launch latency.  ENMF_GRAPH=0 disables it.
-  static const bool graphs = !(getenv("ENMF_GRAPH") && getenv("ENMF_GRAPH")[0] == '0');
-  const bool graph = graphs && !sh && !u_ready && !u_dl_host && !v_dl_host && n_iters >= 3;
+  const char* ge = getenv("ENMF_GRAPH");
+  const bool graphs = !(ge && ge[0] == '0');
+  // (not while the X passes are being timed: enmf_set_profiling brackets every pass with events)
+  const bool graph = graphs && !sh && !u_ready && !u_dl_host && !v_dl_host && n_iters >= 3 &&
+                     !h->prof;
   for (int t = 0; t < n_iters; ++t) {
     SweepHooks hk;
     if (t == 0) hk.u_ready = u_ready;

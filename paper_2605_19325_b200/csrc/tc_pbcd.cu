@@ -20,6 +20,7 @@
 #include <float.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "internal.h"
 #include "tc_ptx.cuh"
@@ -146,17 +147,29 @@ __device__ __forceinline__ void issue_round(uint32_t a0, uint32_t b0, uint32_t t
   tc_commit(bar_d);
 }
 
-__global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
+// NH threads per row (NH = 2: 8 warps, 64 columns each -- round 1; NH = 4: 16 warps, 32
+// columns each -- twice the warps to hide the MMA round trips and the TMEM / shared-memory
+// latencies of the epilogue passes, and half the registers for u).  Warp w reads TMEM lane
+// quadrant w % 4 (tcgen05.ld's rule) and owns columns [CW (w / 4), CW (w / 4 + 1)).
+template <int NH>
+__device__ __forceinline__ void bar_pbcd() {
+  asm volatile("bar.sync 1, %0;" ::"n"(128 * NH) : "memory");
+}
+
+template <int NH>
+__global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
+  constexpr int CW = 128 / NH;               // columns per thread
+  constexpr int NWARP = 4 * NH;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;                  // no-swizzle operands need 16-byte alignment only
   uint8_t* Ad = smem;                        // 4 planes of A digits (128 x KR, K-major)
   uint8_t* Bd = smem + 4 * PLANE_A;          // 4 planes of G digits (rp x KR, K-major)
   __shared__ __align__(8) uint64_t bars[1];
   __shared__ uint32_t tmem_base_s;
-  __shared__ double xch[2][BM];              // row exchange between the two column halves
-  __shared__ int xchi[2][BM];
-  __shared__ double xch2[2][BM];
-  __shared__ double wsum[COMPUTE_WARPS];
+  __shared__ double xch[NH][BM];             // row exchange between the column parts
+  __shared__ int xchi[NH][BM];
+  __shared__ double xch2[NH][BM];
+  __shared__ double wsum[NWARP];
   __shared__ double gsc_s[128];
   if (p.stage != nullptr && *p.stage != 0) return;
   // 2^-21 / t_j: the column scale with comb4's 2^-21 folded in (exact)
@@ -196,15 +209,15 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
     // ===================== compute warps =====================
     const int w = warp;
     const int q = warp & 3;                    // TMEM lane quadrant
-    const int hc = warp >> 2;                  // column half
+    const int hc = warp >> 2;                  // column part
     const int rt = 32 * q + lane;              // row in tile
-    const int c0 = 64 * hc;
-    // my TMEM lane quadrant and column half; class k of the accumulators at column k * KR
+    const int c0 = CW * hc;
+    // my TMEM lane quadrant and columns; class k of the accumulators at column k * KR
     const uint32_t tcol = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
     const double lam = *p.lam;
     const int64_t snap_stride = p.rows * (int64_t)p.r;
     const int g8 = rt >> 3, ri = rt & 7;
-    // my 16-byte digit chunks in the A planes: chunk b of my half at abase + b * 16 * 128
+    // my 16-byte digit chunks in the A planes: chunk b of my part at abase + b * 16 * 128
     uint8_t* const abase = Ad + ((c0 >> 4) * 16 + g8) * 128 + ri * 16;
     uint32_t round = 0;
     const double* gsc = gsc_s + c0;            // 1 / t_j for my columns (shared memory)
@@ -212,10 +225,10 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int64_t row = (int64_t)t * BM + rt;
       const bool rok = row < p.rows;
-      double u[64];
-      uint32_t mlo = 0, mhi = 0;   // M_{U+} bits of my 64 columns
+      double u[CW];
+      uint32_t mlo = 0, mhi = 0;   // M_{U+} bits of my columns
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
+      for (int c = 0; c < CW; ++c) {
         const int col = c0 + c;
         double v = (rok && col < p.r) ? (double)p.F[row * p.ldf + col] : 0.0;
         if (v < 0.0) v += lam;                                     // Eq.(6)/(7) lift
@@ -230,13 +243,16 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
       {
         const double* crow = p.C + row * p.r;
         double cm = 0.0;
-        for (int c = 0; c < 64; ++c)
+        for (int c = 0; c < CW; ++c)
           if (rok && c0 + c < p.r) cm = fmax(cm, fabs(crow[c0 + c]));
         xch2[hc][rt] = cm;
-        bar_compute();
-        const double sc = pow2s(fmax(cm, xch2[1 - hc][rt]));
+        bar_pbcd<NH>();
+        double cmx = 0.0;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) cmx = fmax(cmx, xch2[h][rt]);
+        const double sc = pow2s(cmx);
         cs = 0x1p-21 / sc;
-        for (int c = 0; c < 64; ++c)
+        for (int c = 0; c < CW; ++c)
           Cq[rt * CQ_LD + c0 + c] =
               (rok && c0 + c < p.r) ? __double2int_rn(crow[c0 + c] * sc * 0x1p21) : 0;
       }
@@ -245,13 +261,16 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
         // ---------------- round A: T1 = u G ----------------
         int mh = 0;
 #pragma unroll
-        for (int c = 0; c < 64; ++c) mh = max(mh, hiabs(u[c]));
+        for (int c = 0; c < CW; ++c) mh = max(mh, hiabs(u[c]));
         xchi[hc][rt] = mh;
-        bar_compute();
-        const double su = pow2s_hi(max(mh, xchi[1 - hc][rt]));
+        bar_pbcd<NH>();
+        int mhx = 0;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) mhx = max(mhx, xchi[h][rt]);
+        const double su = pow2s_hi(mhx);
         // digits of u * su into the A planes: chunk (kc, g8, ri), 16 columns each
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
+        for (int ch = 0; ch < CW / 16; ++ch) {
           Pack16 pk;
           pack_clear(pk);
 #pragma unroll
@@ -259,7 +278,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
           pack_store(pk, abase, ch * 16 * 128);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        bar_compute();
+        bar_pbcd<NH>();
         if (threadIdx.x == 0) issue_round(a_s, b_s, tmem_base, rp, p.r, bar_d);
         mbar_wait(bar_d, round & 1);
         ++round;
@@ -270,7 +289,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
         opaque(mlo, mhi);
         const double isu = 1.0 / su;
 #pragma unroll 1
-        for (int b = 0; b < 8; ++b) {       // rolled: keeps the kernel inside the icache
+        for (int b = 0; b < CW / 8; ++b) {  // rolled: keeps the kernel inside the icache
           uint32_t v[4][8];
 #pragma unroll
           for (int cls = 0; cls < 4; ++cls) TMEM_LD8(tcol + cls * KR + 8 * b, v[cls]);
@@ -293,24 +312,30 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
         if (lane == 0) wsum[w] = pg;
         xchi[hc][rt] = gmh;
         xch2[hc][rt] = num;
-        bar_compute();
+        bar_pbcd<NH>();
         if (threadIdx.x == 32) {
           double s = 0.0;
-          for (int k = 0; k < COMPUTE_WARPS; ++k) s += wsum[k];
+          for (int k = 0; k < NWARP; ++k) s += wsum[k];
           pgsm[it] += s;
         }
         if (it == p.max_iter) {
           tc_fence_before();
           // the final round A has no round B; TMEM reads finish before the next tile's MMAs
-          bar_compute();
+          bar_pbcd<NH>();
           break;
         }
-        const double numr = hc == 0 ? num + xch2[1][rt] : xch2[0][rt] + num;
-        const double sg = pow2s_hi(max(gmh, xchi[1 - hc][rt]));
+        double numr = 0.0;
+        int gmx = 0;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          numr += xch2[h][rt];
+          gmx = max(gmx, xchi[h][rt]);
+        }
+        const double sg = pow2s_hi(gmx);
         // pass 2: digits of g * sg (g = M o grad) into the A planes (T1 re-read from TMEM)
         opaque(mlo, mhi);
 #pragma unroll 1
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < CW / 16; ++b) {
           Pack16 pk;
           pack_clear(pk);
           const uint32_t mb = ((b < 2 ? mlo : mhi) >> (16 * (b & 1))) & 65535u;
@@ -333,7 +358,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
         }
         tc_fence_before();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        bar_compute();
+        bar_pbcd<NH>();
         if (threadIdx.x == 0) issue_round(a_s, b_s, tmem_base, rp, p.r, bar_d);
         // ---------------- round B: T2 = g G ----------------
         mbar_wait(bar_d, round & 1);
@@ -344,7 +369,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
         double den = 0.0;
         const double isg = 1.0 / sg;
 #pragma unroll 1
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < CW / 16; ++b) {
           uint4 dq[4];
 #pragma unroll
           for (int pl = 0; pl < 4; ++pl)
@@ -366,13 +391,15 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
         den *= isg * isg;
         tc_fence_before();
         xch[hc][rt] = den;
-        bar_compute();
-        const double denr = hc == 0 ? den + xch[1][rt] : xch[0][rt] + den;
+        bar_pbcd<NH>();
+        double denr = 0.0;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) denr += xch[h][rt];
         // Eq.(10): d_i = ||g_i||^2 / ||g_i V^T||^2 (0 on a zero denominator, R10); Eq.(8)
         const double dstep = denr > 0.0 ? numr / denr : 0.0;
         opaque(mlo, mhi);
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < CW / 16; ++b) {
           uint4 dq[4];
 #pragma unroll
           for (int pl = 0; pl < 4; ++pl)
@@ -389,17 +416,17 @@ __global__ void __launch_bounds__(THREADS, 1) tc_pbcd_kernel(const Params p) {
           const int nt = (int)(p.rows - (int64_t)t * BM < BM ? p.rows - (int64_t)t * BM : BM);
           float* sn = p.snaps + (int64_t)it * snap_stride + (int64_t)t * BM * p.r +
                       (int64_t)c0 * nt + rt;
-          const int ncol = p.r - c0 < 64 ? p.r - c0 : 64;   // columns of my half that exist
+          const int ncol = p.r - c0 < CW ? p.r - c0 : CW;   // columns of my part that exist
 #pragma unroll
-          for (int c = 0; c < 64; ++c) {
+          for (int c = 0; c < CW; ++c) {
             if (c < ncol) *sn = (float)u[c];
             sn += nt;
           }
         }
-        bar_compute();          // everyone has read the g digits before they are overwritten
+        bar_pbcd<NH>();          // everyone has read the g digits before they are overwritten
       }
     }
-    bar_compute();
+    bar_pbcd<NH>();
     if (threadIdx.x == 32)
       for (int it = 0; it <= p.max_iter; ++it)
         p.pgparts[(int64_t)blockIdx.x * (p.max_iter + 1) + it] = pgsm[it];
@@ -943,19 +970,24 @@ int tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double*
   const size_t smem = SMEM_BYTES + sizeof(double) * (max_iter + 1);
   // the dynamic size grows with max_iter; static shared memory (row exchanges) counts against
   // the same 227 KB, so the attribute is the exact dynamic request, raised when it grows
-  static size_t attr = 0;
+  // NH = 4 (16 warps, 32 columns per thread) unless ENMF_TC_PBCD_NH=2 (the round-1 form)
+  const char* nh = getenv("ENMF_TC_PBCD_NH");
+  const bool four = !(nh && nh[0] == '2');
+  static size_t attr2 = 0, attr4 = 0;
+  size_t& attr = four ? attr4 : attr2;
   if (smem > attr) {
-    if (cudaFuncSetAttribute(tc_pbcd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
+    auto k = four ? tc_pbcd_kernel<4> : tc_pbcd_kernel<2>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
       return 1;
-    cudaFuncSetAttribute(tc_pbcd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr = smem;
   }
-  const int tiles = (int)((rows + BM - 1) / BM);
-  const int grid = tiles < kSMs ? tiles : kSMs;
   // unused CTAs of the persistent grid still write their (zero) partials: launch kSMs always
-  tc_pbcd_kernel<<<kSMs, THREADS, smem, st>>>(p);
-  (void)grid;
+  if (four)
+    tc_pbcd_kernel<4><<<kSMs, 512, smem, st>>>(p);
+  else
+    tc_pbcd_kernel<2><<<kSMs, 256, smem, st>>>(p);
   count_launch(2);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

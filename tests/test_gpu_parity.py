@@ -468,3 +468,40 @@ def test_iterate_host_matches_iterate():
     assert np.array_equal(Uh.numpy(), to_np(Ud).astype(np.float32))
     assert np.array_equal(Vh.numpy(), to_np(Vd).astype(np.float32))
     assert i1["ascent_sweeps"] == 10 and h2.get_stage()[0] == 1
+
+
+@pytest.mark.parametrize("prec", [FP64, TC], ids=["fp64", "tc"])
+def test_graph_replay_matches_eager(prec, monkeypatch):
+    """Sweeps 1 .. n-1 of an enmf_iterate call are captured once as a CUDA graph and replayed
+    (enmf_capi.cu replay_sweeps): bitwise the same factors, objective trace, stage counts and
+    k* as the eager launch sequence (ENMF_GRAPH=0), through the ascent -> HALS transition."""
+    cfg = CASES[1]
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("ENMF_GRAPH", mode)
+        h, X, _ = make(cfg, precision=prec)
+        U0, V0, lu, lv = rotated_point(X, cfg.r)
+        U, V = to_dev(U0), to_dev(V0)
+        h.set_stage(0, lu, lv)
+        f, info = h.iterate(U, V, 14)
+        out[mode] = (f, to_np(U), to_np(V), info["ascent_sweeps"], info["pbcd_iters_u"])
+    a, b = out["0"], out["1"]
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    assert a[3:] == b[3:] and a[3] == 10
+
+
+def test_solve_host_matches_device_calls():
+    """enmf_solve_host (X, U, V in host memory: X staged through pinned buffers, init, sweeps,
+    U and V copied back) gives exactly what enmf_init + enmf_iterate give on device copies."""
+    import paper_2605_19325_b200 as E
+    cfg = CASES[0]
+    X = synth.x_full(cfg)
+    h1 = E.Enmf(cfg.m, cfg.n, cfg.r)
+    Uh, Vh, fh, info = h1.solve_host(X, 30)
+    h2 = E.Enmf(cfg.m, cfg.n, cfg.r)
+    U = to_dev(np.zeros((cfg.m, cfg.r)))
+    V = to_dev(np.zeros((cfg.n, cfg.r)))
+    h2.init(to_dev(X), U, V)
+    fd, _ = h2.iterate(U, V, 30)
+    assert np.array_equal(fh, fd)
+    assert np.array_equal(Uh.astype(np.float64), to_np(U)) and np.array_equal(Vh.astype(np.float64), to_np(V))
