@@ -192,19 +192,55 @@ enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
   }
   if (maybe_ascent) {
     if (h->tc_pbcd && !h->opt.step_rule) {
-      if (tc_pbcd_rows(F, ldf, rows, r, C, G, h->dscal + lam_slot, mi, h->snaps, h->parts,
-                       reinterpret_cast<int8_t*>(h->tcpb_ws + 128), h->tcpb_ws, stage, h->st))
+      // Alg. 2 in stages [0,1) [1,2) [2,4) [4,8) ... [.., max_iter): the stopping rule is global
+      // (all rows, all ranks), so each stage runs every row, the partials are reduced and the
+      // rule applied on the device; once it fires the later stages return at once.  Stages
+      // hand the fp64 iterate over through two state buffers (ping-pong), so the iterates are
+      // those of one uninterrupted run (bitwise, test_gpu_pbcd_stages.py).  No per-iteration
+      // snapshots (round 1 wrote max_iter fp32 copies of the block, 5 GB per C5 U block): a
+      // stop inside a stage replays that stage from its start up to k* (the replay launch
+      // returns at once otherwise), and the buffer holding u_k* is committed into F.  A stop
+      // in the first stage (k* = 1: the U block of the first C5 sweep) costs ~1.5 iterations
+      // instead of max_iter + 1.  Staging costs ~3 ms per C5 ascent sweep when the rule never
+      // fires (k* = max_iter: every later C5 sweep, measured), so a block whose previous k*
+      // was max_iter runs its first stage to the end (kprev rule of tc_pbcd_chunk).
+      int8_t* gd = reinterpret_cast<int8_t*>(h->tcpb_ws + 128);
+      int* done = h->dint + I_PBCD_DONE;        // done, then ctl[4] = {replay, it0, src, dst}
+      int* ctl = h->dint + I_PBCD_CTL;
+      double* ust0 = h->pbcd_state;
+      double* ust1 = h->pbcd_state + h->pbcd_state_len;
+      CUDA_TRY(cudaMemsetAsync(done, 0, sizeof(int) * 5, h->st));
+      tc_pbcd_prepare(G, r, gd, h->tcpb_ws, stage, h->st);
+      const char* stg = getenv("ENMF_PBCD_STAGES");   // "0": one stage [0, max_iter) (tests)
+      const bool one = stg && stg[0] == '0';
+      int src = -1, dst = 0;
+      for (int a = 0; a < mi;) {
+        const int b = one ? mi : std::min(mi, a == 0 ? 1 : 2 * a);
+        if (tc_pbcd_chunk(F, ldf, rows, r, C, h->dscal + lam_slot, mi, a, b, src, dst, ust0,
+                          ust1, h->parts, gd, h->tcpb_ws, stage, done, h->dint + kstar_slot,
+                          nullptr, nullptr, h->st))
+          return ENMF_ERR_CUDA;
+        reduce_parts(h->parts, tc_pbcd_parts(), mi + 1, h->pgsum, h->st);
+        if (sharded) ENMF_TRY(ar(h, h->pgsum, (size_t)(mi + 1), CommOp::Sum));
+        pbcd_select_stage(h->pgsum, a, b, src, dst, mi, h->opt.pbcd_eps, h->dint + kstar_slot,
+                          done, ctl, stage, h->st);
+        src = dst;
+        dst ^= 1;
+        a = b;
+      }
+      if (tc_pbcd_chunk(F, ldf, rows, r, C, h->dscal + lam_slot, mi, 0, 1, -1, 0, ust0, ust1,
+                        h->parts, gd, h->tcpb_ws, stage, done, nullptr, ctl,
+                        h->dint + kstar_slot, h->st))
         return ENMF_ERR_CUDA;
-      reduce_parts(h->parts, tc_pbcd_parts(), mi + 1, h->pgsum, h->st);
+      pbcd_commit_state(F, ldf, rows, r, ust0, ust1, ctl, stage, h->minparts, h->st, colmax);
     } else {
       pbcd_rows(F, ldf, rows, r, C, G, h->dscal + lam_slot, mi, h->snaps, h->parts, stage, h->st,
                 h->opt.step_rule ? fstep : nullptr);
       reduce_parts(h->parts, pbcd_parts(), mi + 1, h->pgsum, h->st);
+      if (sharded) ENMF_TRY(ar(h, h->pgsum, (size_t)(mi + 1), CommOp::Sum));
+      pbcd_commit(F, ldf, rows, r, h->snaps, h->pgsum, h->opt.pbcd_eps, mi,
+                  h->dint + kstar_slot, stage, h->minparts, h->st);
     }
-    if (sharded) ENMF_TRY(ar(h, h->pgsum, (size_t)(mi + 1), CommOp::Sum));
-    const bool tiled = h->tc_pbcd && !h->opt.step_rule;
-    pbcd_commit(F, ldf, rows, r, h->snaps, h->pgsum, h->opt.pbcd_eps, mi, h->dint + kstar_slot,
-                stage, h->minparts, tiled, h->st, tiled ? colmax : nullptr);
   }
   if (h->opt.descent) {
     pgd_rows(F, ldf, rows, r, C, G, stage, fstep, h->minparts, h->st, colmax);
@@ -227,8 +263,14 @@ enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
 }
 
 enmf_status_t ensure_snaps(enmf_handle_t h) {
-  if (h->snaps) return ENMF_OK;
+  // the staged tensor-core PBCD keeps two fp64 state buffers; the SIMT PBCD (fp64 path, the
+  // fixed-step ablation, eNMC) max_iter fp32 snapshots
   const size_t rows = (size_t)std::max(h->m_loc, h->n);
+  if (h->tc_pbcd && !h->pbcd_state) {
+    h->pbcd_state_len = (rows + 127) / 128 * 128 * (size_t)h->r;
+    ENMF_TRY(dalloc(&h->pbcd_state, 2 * h->pbcd_state_len));
+  }
+  if (h->snaps || (h->tc_pbcd && !h->opt.step_rule && !h->nmc)) return ENMF_OK;
   return dalloc(&h->snaps, (size_t)h->opt.pbcd_max_iter * rows * (size_t)h->r);
 }
 
@@ -352,7 +394,7 @@ enmf_status_t sweep_nmc(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_
                 h->dscal + S_LAMU, mi, h->snaps, h->parts, st);
   reduce_parts(h->parts, nmc_pbcd_parts(), mi + 1, h->pgsum, st);
   pbcd_commit(U, ldu, h->m_loc, r, h->snaps, h->pgsum, h->opt.pbcd_eps, mi,
-              h->dint + I_KSTAR_U, nullptr, h->minparts, false, st);
+              h->dint + I_KSTAR_U, nullptr, h->minparts, st);
   reduce_min(h->minparts, kRowGrid, h->dscal + S_MINU, st);
   if (hk.u_download) {
     CUDA_TRY(cudaEventRecord(h->ev_a, st));
@@ -364,7 +406,7 @@ enmf_status_t sweep_nmc(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_
                 h->dscal + S_LAMV, mi, h->snaps, h->parts, st);
   reduce_parts(h->parts, nmc_pbcd_parts(), mi + 1, h->pgsum, st);
   pbcd_commit(V, ldv, h->n, r, h->snaps, h->pgsum, h->opt.pbcd_eps, mi, h->dint + I_KSTAR_V,
-              nullptr, h->minparts, false, st);
+              nullptr, h->minparts, st);
   reduce_min(h->minparts, kRowGrid, h->dscal + S_MINV, st);
   if (hk.v_download) {
     CUDA_TRY(cudaEventRecord(h->ev_a, st));
@@ -480,7 +522,7 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
   void* bufs[] = {h->dscal, h->dint, h->P, h->Q, h->GU, h->GV, h->work, h->parts,
                   h->minparts, h->pgsum, h->snaps, h->ftrace, h->x_owned, h->W64,
                   h->tcpb_ws, h->fmax_uv, h->Ud, h->Vd, h->arena, h->Vg, h->Vpad,
-                  h->csc_ptr, h->csc_row, h->csc_val, h->stepws};
+                  h->csc_ptr, h->csc_row, h->csc_val, h->stepws, h->pbcd_state};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (void* b : h->arena_extra) cudaFree(b);

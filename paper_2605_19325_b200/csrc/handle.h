@@ -24,7 +24,9 @@ enum {
 // device int slots
 enum { I_STAGE = 0, I_KSTAR_U, I_KSTAR_V, I_CNT_ASC, I_CNT_HALS, I_BAD, I_HALS_FB, I_HALS_ILL,
        I_FCNT,   // next slot of the objective trace (sweeps append; graph replays share args)
-       I_COUNT = 9 };
+       I_PBCD_DONE,   // staged tensor-core PBCD: the stopping rule has fired in this block
+       I_PBCD_CTL,    // 4 slots: replay?, replay it0, replay src, committed state buffer
+       I_COUNT = I_PBCD_CTL + 4 };
 
 }  // namespace enmf
 
@@ -57,6 +59,8 @@ struct enmf_handle_s {
   int ftrace_cap = 0;
   enmf::TcState* tc = nullptr;
   double* tcpb_ws = nullptr;  // tensor-core PBCD: G digits (64 KB) + 128 column scales
+  double* pbcd_state = nullptr;  // staged tensor-core PBCD: 2 x fp64 u (tile-major, ping-pong)
+  size_t pbcd_state_len = 0;
   double* stepws = nullptr;   // lambda_max workspace of the ablation step rules (R29)
   bool step_warm[2] = {false, false};   // stepws holds a warm start per block (U, V)
   bool tc_pbcd = false;       // ascent PBCD on the tensor cores (precision TC, r <= 128)

@@ -112,13 +112,21 @@ void lambda_power(const double* G, int r, double* v, bool warm, double* out, cud
 // *out = 1 / s[0] (0 if s[0] <= 0): the fixed step 1 / lambda_max from a singular-value list.
 void recip_first(const double* s, double* out, cudaStream_t st);
 int pbcd_parts();
-// Selects k* from the partials (eps rule of Alg. 2), copies snapshot k* into F and
-// writes min partials; records k* into *kstar.  tiled: snapshots in tc_pbcd.cu's tile-major
-// layout (see pbcd_copy_tiled_kernel), else row-major rows x r.
+// Selects k* from the partials (eps rule of Alg. 2), copies snapshot k* (row-major rows x r)
+// into F and writes min partials; records k* into *kstar.
 void pbcd_commit(float* F, int64_t ldf, int64_t rows, int r, const float* snaps,
                  const double* pgparts, double eps, int max_iter, int* kstar,
-                 const int* stage, double* minparts, bool tiled, cudaStream_t st,
-                 unsigned long long* colmax = nullptr);
+                 const int* stage, double* minparts, cudaStream_t st);
+// Staged PBCD (tc_pbcd_chunk): the stopping rule on iterations [it0, it1] of the stage that
+// read state src and wrote dst (sets *kstar, *done and the replay / commit control ctl[4]
+// once it fires, or at it1 == max_iter), and the commit of the fp64 state ust[ctl[3]] into F
+// with min partials / column maxima; both no-ops unless *stage == 0.
+void pbcd_select_stage(const double* pgsum, int it0, int it1, int src, int dst, int max_iter,
+                       double eps, int* kstar, int* done, int* ctl, const int* stage,
+                       cudaStream_t st);
+void pbcd_commit_state(float* F, int64_t ldf, int64_t rows, int r, const double* ust0,
+                       const double* ust1, const int* ctl, const int* stage, double* minparts,
+                       cudaStream_t st, unsigned long long* colmax);
 // eNMC PBCD of one block (App. C; kernels_rows.cu nmc_pbcd_kernel): F (rows x r, ld) with the
 // other factor O (ld ldo) fixed, the block's observed entries as CSR lists (ptr rows + 1,
 // idx, val); lift, mask, all max_iter inner iterations with snapshots and per-iteration

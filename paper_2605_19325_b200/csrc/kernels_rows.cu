@@ -431,14 +431,47 @@ __global__ void pbcd_select_kernel(const double* __restrict__ pgsum, int max_ite
   }
 }
 
-// Same as pbcd_copy_kernel for the tile-major snapshot layout of tc_pbcd.cu: element (i, j)
-// at (i / 128) * 128 * r + j * nt + i % 128, nt = min(128, rows - 128 * (i / 128)) the rows of
-// that tile (so a snapshot still spans exactly rows * r floats).  A (tile, 32-column chunk) unit is transposed
-// through shared memory so that both the snapshot reads and the F writes are coalesced.
-__global__ void pbcd_copy_tiled_kernel(float* __restrict__ F, int64_t ldf, int64_t rows, int r,
-                                       const float* __restrict__ snaps,
-                                       const int* __restrict__ kstar, const int* stage,
-                                       double* minparts, unsigned long long* colmax) {
+// Alg. 2's stopping rule on a stage [it0, it1) of the staged tensor-core PBCD: the first
+// it in [max(1, it0), it1] with ||M o grad_it|| < eps ||M o grad_0|| is k* (as in
+// pbcd_select_kernel); none and it1 == max_iter: k* = max_iter.  Either way *done = 1, which
+// makes the later stages of this block update return at once, and ctl[3] = dst (the state
+// buffer holding the result); a stop before the stage's end (k* < it1) sets
+// ctl[0..2] = {1, it0, src}: replay the stage from its start up to k* (no per-iteration
+// snapshots are kept).  *kstar holds the previous sweep's k* on entry to the first stage:
+// max_iter there means that stage ran to the end (tc_pbcd_chunk's kprev rule).
+__global__ void pbcd_select_stage_kernel(const double* __restrict__ pgsum, int it0, int it1,
+                                         int src, int dst, int max_iter, double eps,
+                                         int* kstar, int* done, int* ctl, const int* stage) {
+  if (stage != nullptr && *stage != 0) return;
+  if (threadIdx.x == 0 && *done == 0) {
+    if (it0 == 0 && *kstar == max_iter) it1 = max_iter;
+    const double pg0 = sqrt(pgsum[0]);
+    int k = -1;
+    for (int it = it0 > 1 ? it0 : 1; it <= it1; ++it)
+      if (sqrt(pgsum[it]) < eps * pg0) {
+        k = it;
+        break;
+      }
+    if (k < 0 && it1 == max_iter) k = max_iter;
+    if (k < 0) return;
+    *kstar = k;
+    *done = 1;
+    ctl[0] = k < it1 ? 1 : 0;
+    ctl[1] = it0;
+    ctl[2] = src;
+    ctl[3] = dst;
+  }
+}
+
+// The committed PBCD result: the fp64 state ust[ctl[3]] of the staged tensor-core PBCD
+// (tile-major, element (i, j) at (i / 128) 128 r + j 128 + i % 128) rounded into F (fp32, the
+// factor state, R26), with min partials and column maxima.  A (tile, 32-column chunk) unit is
+// transposed through shared memory so that both the state reads and the F writes coalesce.
+__global__ void pbcd_commit_state_kernel(float* __restrict__ F, int64_t ldf, int64_t rows,
+                                         int r, const double* __restrict__ ust0,
+                                         const double* __restrict__ ust1,
+                                         const int* __restrict__ ctl, const int* stage,
+                                         double* minparts, unsigned long long* colmax) {
   __shared__ float t[128][33];
   __shared__ double red[256];
   __shared__ unsigned long long cm[128];
@@ -447,18 +480,18 @@ __global__ void pbcd_copy_tiled_kernel(float* __restrict__ F, int64_t ldf, int64
   const bool active = stage == nullptr || *stage == 0;
   double mn = DBL_MAX;
   if (active) {
-    const float* src = snaps + (int64_t)(*kstar - 1) * rows * r;
+    const double* src = ctl[3] ? ust1 : ust0;
     const int64_t tiles = (rows + 127) / 128;
     const int chunks = (r + 31) / 32;
     for (int64_t unit = blockIdx.x; unit < tiles * chunks; unit += gridDim.x) {
       const int64_t tile = unit / chunks;
       const int j0 = (int)(unit - tile * chunks) * 32;
-      const float* ts = src + tile * 128 * (int64_t)r;
+      const double* ts = src + tile * 128 * (int64_t)r;
       const int nt = (int)(rows - tile * 128 < 128 ? rows - tile * 128 : 128);
       __syncthreads();
       for (int e = threadIdx.x; e < 32 * 128; e += blockDim.x) {
         const int jl = e >> 7, il = e & 127;
-        if (j0 + jl < r && il < nt) t[il][jl] = ts[(int64_t)(j0 + jl) * nt + il];
+        if (j0 + jl < r && il < nt) t[il][jl] = (float)ts[(int64_t)(j0 + jl) * 128 + il];
       }
       __syncthreads();
       for (int e = threadIdx.x; e < 128 * 32; e += blockDim.x) {
@@ -790,14 +823,26 @@ void nmc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const int64
 
 void pbcd_commit(float* F, int64_t ldf, int64_t rows, int r, const float* snaps,
                  const double* pgsum, double eps, int max_iter, int* kstar, const int* stage,
-                 double* minparts, bool tiled, cudaStream_t st, unsigned long long* colmax) {
+                 double* minparts, cudaStream_t st) {
   pbcd_select_kernel<<<1, 32, 0, st>>>(pgsum, max_iter, eps, kstar, stage);
-  if (tiled)
-    pbcd_copy_tiled_kernel<<<kRowGrid, 256, 0, st>>>(F, ldf, rows, r, snaps, kstar, stage,
-                                                     minparts, colmax);
-  else
-    pbcd_copy_kernel<<<kRowGrid, 256, 0, st>>>(F, ldf, rows, r, snaps, kstar, stage, minparts);
+  pbcd_copy_kernel<<<kRowGrid, 256, 0, st>>>(F, ldf, rows, r, snaps, kstar, stage, minparts);
   count_launch(2);
+}
+
+void pbcd_select_stage(const double* pgsum, int it0, int it1, int src, int dst, int max_iter,
+                       double eps, int* kstar, int* done, int* ctl, const int* stage,
+                       cudaStream_t st) {
+  pbcd_select_stage_kernel<<<1, 32, 0, st>>>(pgsum, it0, it1, src, dst, max_iter, eps, kstar,
+                                             done, ctl, stage);
+  count_launch();
+}
+
+void pbcd_commit_state(float* F, int64_t ldf, int64_t rows, int r, const double* ust0,
+                       const double* ust1, const int* ctl, const int* stage, double* minparts,
+                       cudaStream_t st, unsigned long long* colmax) {
+  pbcd_commit_state_kernel<<<kRowGrid, 256, 0, st>>>(F, ldf, rows, r, ust0, ust1, ctl, stage,
+                                                     minparts, colmax);
+  count_launch();
 }
 
 int kkt_parts() { return kRowGrid * kRowWarps; }

@@ -43,15 +43,26 @@ int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st,
 int tc_xf(TcState* s, bool transposed, const double* F, int64_t ldf, int ncols, double* out,
           int64_t ldo, cudaStream_t st);
 
-// Alg. 2 PBCD on the tensor cores: same contract as pbcd_rows (kernels_rows.cu); pgparts holds
-// tc_pbcd_parts() x (max_iter + 1) partials; gd_work >= 4*128*128 bytes, gscale_work >= 128.
+// Alg. 2 PBCD on the tensor cores, staged: tc_pbcd_prepare turns G into the B-operand digits
+// (gd_work >= 4*128*128 bytes, gscale_work >= 128), then each tc_pbcd_chunk runs iterations
+// [it0, it1) for every row -- lift + mask of F (src < 0) or resume from the fp64 state
+// ust[src] -- and leaves u_it1 in ust[dst] (each >= ceil(rows / 128) * 128 * r doubles,
+// tile-major), with the partials of ||M o grad||^2 for iterations it0 .. it1 in pgparts
+// (tc_pbcd_parts() x (max_iter + 1)).  No per-iteration snapshots: when the stopping rule
+// fires inside a stage, pbcd_select_stage fills rctl = {1, it0, src, dst} and a launch with
+// rctl (and kst = the k* slot) replays that stage up to k*.  A stage returns at once if
+// *stage != 0 or *done != 0, a replay unless rctl[0] != 0.  kprev (optional): the block's k*
+// of the previous sweep; if it equals max_iter, the first stage (it0 = 0) runs to max_iter.
 // Returns 0, or 1 on a launch / configuration error.
 bool tc_pbcd_supported(int r);
 int tc_pbcd_parts();
-int tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
-                  const double* G, const double* lam, int max_iter, float* snaps,
-                  double* pgparts, int8_t* gd_work, double* gscale_work, const int* stage,
-                  cudaStream_t st);
+void tc_pbcd_prepare(const double* G, int r, int8_t* gd_work, double* gscale_work,
+                     const int* stage, cudaStream_t st);
+int tc_pbcd_chunk(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
+                  const double* lam, int max_iter, int it0, int it1, int src, int dst,
+                  double* ust0, double* ust1, double* pgparts, const int8_t* gd_work,
+                  const double* gscale_work, const int* stage, const int* done,
+                  const int* kprev, const int* rctl, const int* kst, cudaStream_t st);
 // HALS sweep of the rows with t = C - u G from exact int8-digit tcgen05
 // rounds, 32-column Gauss-Seidel blocks in registers (tc_pbcd.cu).  Runs only if *stage == 1.
 // Writes minparts[0, nparts) (nparts >= tc_hals_parts()); colmax (u64[r]) as hals_rows;

@@ -5,18 +5,21 @@
 //   h_i    = g_i G,  g = M o grad   (the Eq.(10) denominator ||g V^T||^2 = g G g^T)
 // i.e. 2 r^2 MACs per row-iteration -- 33 GFMA per U block at C5, 50 iterations.  The SIMT fp64
 // kernel (kernels_rows.cu) is bound by the fp64 pipe; here a CTA holds a 128-row tile and runs
-// all max_iter iterations with both products as exact int8-digit tcgen05 MMAs (same 4-digit,
-// 4-class scheme as tc_gemm.cu: A = digits of u or g with a power-of-two scale per row, B =
-// digits of G with a power-of-two scale per column, 4 exact int32 TMEM accumulators, combined
-// exactly in fp64).  u stays in fp64 registers; g is never stored: it is rebuilt from its digit
-// planes in shared memory, which represent it to 2^-22 of its row maximum.
+// the iterations with both products as exact int8-digit tcgen05 MMAs: A = u or g on the 2^-24
+// grid of a power-of-two row scale (|t| < 64), B = G on the same grid per column, each as FOUR
+// BALANCED BASE-2^8 DIGITS -- the bytes of (n + 0x808080) ^ 0x808080, n the grid integer (bdig;
+// round 2b: the base-2^7 split cost ~30 integer ops per element and encoding, the byte form 2
+// plus a 4 x 4 byte transpose per 4 columns) -- 10 digit products in 4 weight classes, i.e. 4
+// exact int32 TMEM accumulators combined exactly in fp64 (comb8).  Resolution 2^-30 .. 2^-29 of
+// the row maximum; the dropped classes (>= 4) are unbiased.  u stays in fp64 registers; g is
+// never stored: its grid integers are read back from the digit planes in shared memory.
 //
-// Warp roles: 8 warps, thread (row, half) owns 64 columns of one row (TMEM lane quadrant =
-// warp % 4, column half = warp / 4).  Warp 0 allocates TMEM; thread 0 issues each round's MMAs
-// after the named barrier that publishes the A planes (a ninth, issuer-only warp would cap the
-// register file at 168 per thread and spill the 64 fp64 row values).
+// Warp roles: 4 NH warps, NH threads per row, each owning 128 / NH columns (TMEM lane quadrant =
+// warp % 4, column part = warp / 4).  Warp 0 allocates TMEM; thread 0 issues each round's MMAs
+// after the named barrier that publishes the A planes.
 // Everything else follows pbcd_kernel: lift + mask at entry, a snapshot of every iterate, and the
-// per-iteration ||M o grad||^2 partials for the global stopping rule (pbcd_select / pbcd_copy).
+// per-iteration ||M o grad||^2 partials for the global stopping rule (pbcd_select_stage /
+// pbcd_copy_tiled), run in stages (tc_pbcd_chunk).
 #include <float.h>
 #include <math.h>
 #include <stdint.h>
@@ -31,8 +34,6 @@ namespace tpb {
 using namespace tcp;
 
 constexpr int BM = 128;
-constexpr int COMPUTE_WARPS = 8;
-constexpr int THREADS = 32 * COMPUTE_WARPS;   // 8 warps: 255 registers per thread available
 constexpr int KR = 128;                     // K (= r) padded to the MMA depth multiple
 constexpr int PLANE_A = BM * KR;            // 16 KB
 constexpr int PLANE_B = 128 * KR;           // 16 KB (G padded to 128 rows)
@@ -50,9 +51,23 @@ struct Params {
   const double* gscale;      // r: 1 / t_j
   const double* lam;
   int max_iter;
-  float* snaps;
-  double* pgparts;           // gridDim x (max_iter + 1)
+  double* pgparts;           // gridDim x (max_iter + 1); this launch writes [it0, it1]
   const int* stage;
+  // Staged Alg. 2 (tc_pbcd_chunk): this launch runs iterations [it0, it1) -- round A of
+  // it0 .. it1 (the ||M o grad||^2 of u_it0 .. u_it1) and the steps to u_{it0+1} .. u_{it1}
+  // -- starting from the lifted F (src < 0) or from the fp64 state ust[src], and leaves u_it1
+  // in ust[dst] (tile-major: element (row, col) of tile t at t 128 r + col 128 + row % 128).
+  // No per-iteration snapshots: a stop inside a stage is replayed (rctl).  done != 0 (the
+  // stopping rule already fired): nothing to do.  kprev: this block's k* of the previous
+  // sweep; when it was max_iter (Alg. 2 ran to the end) the first stage runs all iterations
+  // at once (it1 := max_iter), as pbcd_select_stage does.  rctl (a replay launch):
+  // rctl = {replay?, it0, src, dst} written by pbcd_select_stage, it1 = *kst.
+  int it0, it1, src, dst;
+  double* ust[2];
+  const int* done;
+  const int* kprev;
+  const int* rctl;
+  const int* kst;
 };
 
 __device__ __forceinline__ double pow2s(double mx) {
@@ -79,10 +94,6 @@ __device__ __forceinline__ double comb4(uint32_t v0, uint32_t v1, uint32_t v2, u
   const int hi = (int)v0 * 128 + (int)v1;
   const int lo = (int)v2 * 128 + (int)v3;
   return fma((double)hi, 16384.0, (double)lo);
-}
-
-__device__ __forceinline__ void bar_compute() {
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * COMPUTE_WARPS) : "memory");
 }
 
 // digits_word(t): tc_ptx.cuh
@@ -115,11 +126,101 @@ __device__ __forceinline__ int digit_at(const uint4& v, int k) {
   const uint32_t w = (k >> 2) == 0 ? v.x : ((k >> 2) == 1 ? v.y : ((k >> 2) == 2 ? v.z : v.w));
   return (int)(int8_t)(uint8_t)(w >> (8 * (k & 3)));
 }
-// the value the digit planes hold for column k of a 16-column chunk (exact)
-__device__ __forceinline__ double rebuild(const uint4 (&dq)[4], int k) {
-  const int n = (digit_at(dq[0], k) << 21) + (digit_at(dq[1], k) << 14) +
-                (digit_at(dq[2], k) << 7) + digit_at(dq[3], k);
-  return (double)n * 0x1p-21;
+
+// ---- byte digits (tc_pbcd_kernel) ----
+// t (|t| < 64) on the 2^-24 grid, n = rint(t 2^24) (|n| < 2^30), as four balanced signed
+// base-2^8 digits n = d0 2^24 + d1 2^16 + d2 2^8 + d3 (d1..d3 in [-128, 127], |d0| <= 64): the
+// bytes of w = (n + 0x808080) ^ 0x808080 (byte 3 = d0 ... byte 0 = d3).  With b the bytes of
+// n + 0x808080, n = b0 2^24 + (b1 - 128) 2^16 + (b2 - 128) 2^8 + (b3 - 128), and b - 128 is
+// the byte b ^ 0x80 read as int8.  2 integer ops instead of the 4-step base-2^7 split; every
+// digit signed and balanced, so the dropped weight classes (>= 4) stay unbiased.
+// Conversions without the XU pipe (quarter rate; ncu: 37 % busy, I2F the top stall after the
+// MMA waits): rint(x) for |x| < 2^31 is the low word of x + 1.5 2^52 (one DFMA, round to
+// nearest even like __double2int_rn), and an int32 k is the double with high word 0x43300000
+// and low word k ^ 2^31 (= 2^52 + 2^31 + k) minus 2^52 + 2^31 (one LOP3 and one DADD).
+__device__ __forceinline__ int rint_lo(double t, double scale) {
+  return __double2loint(fma(t, scale, 0x1.8p52));
+}
+__device__ __forceinline__ double i2d(int k) {
+  return __hiloint2double(0x43300000, k ^ (int)0x80000000) - 4503601774854144.0;
+}
+// bdig(t, s): the digit word of t s 2^24 (s a power of two)
+__device__ __forceinline__ uint32_t bdig(double t, double s24) {
+  return ((uint32_t)rint_lo(t, s24) + 0x00808080u) ^ 0x00808080u;
+}
+__device__ __forceinline__ uint32_t bdig(double t) { return bdig(t, 0x1p24); }
+__device__ __forceinline__ int bdig_n(uint32_t w) {
+  return (int)((w ^ 0x00808080u) - 0x00808080u);
+}
+// 4 x 4 byte transpose (an involution): o[j] byte i = byte j of input i
+__device__ __forceinline__ void bt4(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                    uint32_t (&o)[4]) {
+  const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+  const uint32_t t2 = __byte_perm(c, d, 0x5140), t3 = __byte_perm(c, d, 0x7362);
+  o[0] = __byte_perm(t0, t2, 0x5410);
+  o[1] = __byte_perm(t0, t2, 0x7632);
+  o[2] = __byte_perm(t1, t3, 0x5410);
+  o[3] = __byte_perm(t1, t3, 0x7632);
+}
+// 16 columns' digit words -> the 16-byte chunks of the 4 A planes (plane pl = digit d_pl =
+// byte 3 - pl), one 16-byte store per plane
+__device__ __forceinline__ void bstore16(const uint32_t (&w)[16], uint8_t* Ad, int off) {
+  uint32_t pl[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t o[4];
+    bt4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3], o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pl[3 - j][q] = o[j];
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    *reinterpret_cast<uint4*>(Ad + k * PLANE_A + off) =
+        make_uint4(pl[k][0], pl[k][1], pl[k][2], pl[k][3]);
+}
+// the grid integers n of 16 columns back from the A planes (exact)
+__device__ __forceinline__ void bload16(const uint8_t* Ad, int off, int (&n)[16]) {
+  uint4 v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const uint4*>(Ad + k * PLANE_A + off);
+  const uint32_t pw[4][4] = {{v[0].x, v[0].y, v[0].z, v[0].w}, {v[1].x, v[1].y, v[1].z, v[1].w},
+                             {v[2].x, v[2].y, v[2].z, v[2].w}, {v[3].x, v[3].y, v[3].z, v[3].w}};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t o[4];
+    bt4(pw[3][q], pw[2][q], pw[1][q], pw[0][q], o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) n[4 * q + j] = bdig_n(o[j]);
+  }
+}
+// The 4 weight classes of an accumulator column combined exactly: v0 2^24 + v1 2^16 + v2 2^8
+// + v3; callers fold 2^-24 into their scales.  With K <= 128 and |digits| <= 128 a product
+// sum is < 2^21 in magnitude and class c holds c + 1 products, so v0 2^8 + v1 (< 2^29.1) and
+// v2 2^8 + v3 (< 1.62e9) are exact int32 and hi 2^16 + lo (< 2^46) is exact in int64 and in
+// fp64.  One int64 -> fp64 conversion: the conversions share the quarter-rate XU pipe, which
+// ncu showed 38 % busy in the round-2 kernel (13 conversions per element and iteration).
+__device__ __forceinline__ double comb8(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3) {
+  const int hi = (int)v0 * 256 + (int)v1;
+  const int lo = (int)v2 * 256 + (int)v3;
+  return __longlong_as_double(0x4338000000000000LL + ((long long)hi << 16) + (long long)lo) -
+         0x1p52 * 1.5;
+}
+// 8 doubles of this thread's lanes as two 32-bit TMEM words each (lo words at taddr_lo,
+// hi words at taddr_hi, 8 consecutive columns)
+__device__ __forceinline__ void tmem_st8d(uint32_t taddr_lo, uint32_t taddr_hi,
+                                          const double (&d)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr_lo),
+      "r"(__double2loint(d[0])), "r"(__double2loint(d[1])), "r"(__double2loint(d[2])),
+      "r"(__double2loint(d[3])), "r"(__double2loint(d[4])), "r"(__double2loint(d[5])),
+      "r"(__double2loint(d[6])), "r"(__double2loint(d[7]))
+      : "memory");
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr_hi),
+      "r"(__double2hiint(d[0])), "r"(__double2hiint(d[1])), "r"(__double2hiint(d[2])),
+      "r"(__double2hiint(d[3])), "r"(__double2hiint(d[4])), "r"(__double2hiint(d[5])),
+      "r"(__double2hiint(d[6])), "r"(__double2hiint(d[7]))
+      : "memory");
 }
 
 // The 4-class digit products of one round as 6 MMAs (see tc_gemm.cu MmaList<4>), issued by one
@@ -172,9 +273,20 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
   __shared__ double wsum[NWARP];
   __shared__ double gsc_s[128];
   if (p.stage != nullptr && *p.stage != 0) return;
-  // 2^-21 / t_j: the column scale with comb4's 2^-21 folded in (exact)
+  int it0 = p.it0, it1 = p.it1, src = p.src, dst = p.dst;
+  if (p.rctl != nullptr) {                   // replay of the stage in which the rule fired
+    if (p.rctl[0] == 0) return;
+    it0 = p.rctl[1];
+    it1 = *p.kst;
+    src = p.rctl[2];
+    dst = p.rctl[3];
+  } else {
+    if (p.done != nullptr && *p.done != 0) return;
+    if (it0 == 0 && p.kprev != nullptr && *p.kprev == p.max_iter) it1 = p.max_iter;
+  }
+  // 2^-24 / t_j: the column scale with comb8's 2^-24 folded in (exact)
   for (int j = threadIdx.x; j < 128; j += blockDim.x)
-    gsc_s[j] = j < p.r ? p.gscale[j] * 0x1p-21 : 0.0;
+    gsc_s[j] = j < p.r ? p.gscale[j] * 0x1p-24 : 0.0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_d = smem_u32(&bars[0]);     // MMA -> all warps: accumulators ready
   constexpr int rp = KR;                         // G padded to 128 columns (p.rp == KR)
@@ -188,6 +300,9 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
   for (int e = threadIdx.x; e < 4 * PLANE_A / 16; e += blockDim.x)
     reinterpret_cast<uint4*>(Ad)[e] = make_uint4(0, 0, 0, 0);
   for (int e = threadIdx.x; e <= p.max_iter; e += blockDim.x) pgsm[e] = 0.0;
+  const bool resume = src >= 0;
+  const double* const ust_in = resume ? p.ust[src] : nullptr;
+  double* const ust_out = p.ust[dst];
   if (threadIdx.x == 0) {
     mbar_init(bar_d, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -215,7 +330,6 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
     // my TMEM lane quadrant and columns; class k of the accumulators at column k * KR
     const uint32_t tcol = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
     const double lam = *p.lam;
-    const int64_t snap_stride = p.rows * (int64_t)p.r;
     const int g8 = rt >> 3, ri = rt & 7;
     // my 16-byte digit chunks in the A planes: chunk b of my part at abase + b * 16 * 128
     uint8_t* const abase = Ad + ((c0 >> 4) * 16 + g8) * 128 + ri * 16;
@@ -227,18 +341,27 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
       const bool rok = row < p.rows;
       double u[CW];
       uint32_t mlo = 0, mhi = 0;   // M_{U+} bits of my columns
+      // my state slots: column c0 + c of my row at [c * BM] (coalesced across the warp)
+      const int64_t sto = (int64_t)t * BM * p.r + (int64_t)c0 * BM + rt;
 #pragma unroll
       for (int c = 0; c < CW; ++c) {
         const int col = c0 + c;
-        double v = (rok && col < p.r) ? (double)p.F[row * p.ldf + col] : 0.0;
-        if (v < 0.0) v += lam;                                     // Eq.(6)/(7) lift
+        double v;
+        if (resume) {
+          // u_it0 of an earlier launch: entries outside M_{U+} kept their (negative) lifted
+          // value and the projected ones are >= 0, so the mask is again [u >= 0]
+          v = (rok && col < p.r) ? ust_in[sto + (int64_t)c * BM] : 0.0;
+        } else {
+          v = (rok && col < p.r) ? (double)p.F[row * p.ldf + col] : 0.0;
+          if (v < 0.0) v += lam;                                   // Eq.(6)/(7) lift
+        }
         u[c] = v;
         if (rok && col < p.r && v >= 0.0) {                        // M_{U+} (R14)
           if (c < 32) mlo |= 1u << c; else mhi |= 1u << (c - 32);
         }
       }
       // c_i (row of P or Q) -> shared memory as int32 fixed point with a power-of-two row scale:
-      // c = cq * csc, |error| <= 2^-27 max_j |c_ij| (the same resolution as the u / g digits)
+      // c = cq * csc, |error| <= 2^-30 max_j |c_ij| (the resolution of the u / g digits)
       double cs;
       {
         const double* crow = p.C + row * p.r;
@@ -251,13 +374,13 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
 #pragma unroll
         for (int h = 0; h < NH; ++h) cmx = fmax(cmx, xch2[h][rt]);
         const double sc = pow2s(cmx);
-        cs = 0x1p-21 / sc;
+        cs = 0x1p-24 / sc;
         for (int c = 0; c < CW; ++c)
           Cq[rt * CQ_LD + c0 + c] =
-              (rok && c0 + c < p.r) ? __double2int_rn(crow[c0 + c] * sc * 0x1p21) : 0;
+              (rok && c0 + c < p.r) ? __double2int_rn(crow[c0 + c] * sc * 0x1p24) : 0;
       }
       const int32_t* cqrow = Cq + rt * CQ_LD + c0;
-      for (int it = 0; it <= p.max_iter; ++it) {
+      for (int it = it0; it <= it1; ++it) {
         // ---------------- round A: T1 = u G ----------------
         int mh = 0;
 #pragma unroll
@@ -271,16 +394,15 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
         // digits of u * su into the A planes: chunk (kc, g8, ri), 16 columns each
 #pragma unroll
         for (int ch = 0; ch < CW / 16; ++ch) {
-          Pack16 pk;
-          pack_clear(pk);
+          uint32_t wd[16];
 #pragma unroll
-          for (int k = 0; k < 16; ++k) pack_put(pk, k, digits_word(u[16 * ch + k] * su));
-          pack_store(pk, abase, ch * 16 * 128);
+          for (int k = 0; k < 16; ++k) wd[k] = bdig(u[16 * ch + k], su * 0x1p24);
+          bstore16(wd, abase, ch * 16 * 128);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         bar_pbcd<NH>();
         if (threadIdx.x == 0) issue_round(a_s, b_s, tmem_base, rp, p.r, bar_d);
-        mbar_wait(bar_d, round & 1);
+        mbar_wait_hint(bar_d, round & 1);
         ++round;
         tc_fence_after();
         // pass 1: grad = T1 / su - c ; ||M o grad||^2 (pg of iteration it), num, max|g|
@@ -291,6 +413,7 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
 #pragma unroll 1
         for (int b = 0; b < CW / 8; ++b) {  // rolled: keeps the kernel inside the icache
           uint32_t v[4][8];
+          double gk[8];
 #pragma unroll
           for (int cls = 0; cls < 4; ++cls) TMEM_LD8(tcol + cls * KR + 8 * b, v[cls]);
           const uint32_t mb = ((b < 4 ? mlo : mhi) >> (8 * (b & 3))) & 255u;
@@ -298,13 +421,18 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const int c = 8 * b + k;
-            const double a = comb4(v[0][k], v[1][k], v[2][k], v[3][k]);
-            const double gr = a * isu * gsc[c] - (double)cqrow[c] * cs;
+            const double a = comb8(v[0][k], v[1][k], v[2][k], v[3][k]);
+            const double gr = a * isu * gsc[c] - i2d(cqrow[c]) * cs;
             const double gm = ((mb >> k) & 1u) ? gr : 0.0;     // M o grad
+            gk[k] = gm;
             num = fma(gm, gm, num);
             gmh = max(gmh, hiabs(gm));
           }
+          // M o grad back into the classes-0/1 columns just read (lo / hi words): pass 2
+          // reads it instead of recombining T1 (round B rewrites all four classes)
+          tmem_st8d(tcol + 8 * b, tcol + KR + 8 * b, gk);
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         // per-iteration partial of ||M o grad||^2 (fixed-order block reduction)
         double pg = num;
 #pragma unroll
@@ -318,9 +446,15 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
           for (int k = 0; k < NWARP; ++k) s += wsum[k];
           pgsm[it] += s;
         }
-        if (it == p.max_iter) {
+        if (it == it1) {
           tc_fence_before();
           // the final round A has no round B; TMEM reads finish before the next tile's MMAs
+          if (rok) {               // u_it1: the next stage's start, or the committed result
+            const int ncol = p.r - c0 < CW ? p.r - c0 : CW;
+#pragma unroll
+            for (int c = 0; c < CW; ++c)
+              if (c < ncol) ust_out[sto + (int64_t)c * BM] = u[c];
+          }
           bar_pbcd<NH>();
           break;
         }
@@ -332,48 +466,40 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
           gmx = max(gmx, xchi[h][rt]);
         }
         const double sg = pow2s_hi(gmx);
-        // pass 2: digits of g * sg (g = M o grad) into the A planes (T1 re-read from TMEM)
-        opaque(mlo, mhi);
+        // pass 2: digits of g * sg (g = M o grad, from the TMEM words pass 1 left) into the A
+        // planes
+        const double sg24 = sg * 0x1p24;
 #pragma unroll 1
         for (int b = 0; b < CW / 16; ++b) {
-          Pack16 pk;
-          pack_clear(pk);
-          const uint32_t mb = ((b < 2 ? mlo : mhi) >> (16 * (b & 1))) & 65535u;
+          uint32_t wd[16];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            uint32_t v[4][8];
-#pragma unroll
-            for (int cls = 0; cls < 4; ++cls) TMEM_LD8(tcol + cls * KR + 16 * b + 8 * h, v[cls]);
+            uint32_t lo[8], hi[8];
+            TMEM_LD8(tcol + 16 * b + 8 * h, lo);
+            TMEM_LD8(tcol + KR + 16 * b + 8 * h, hi);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const int c = 16 * b + 8 * h + k;
-              const double a = comb4(v[0][k], v[1][k], v[2][k], v[3][k]);
-              const double gr = a * isu * gsc[c] - (double)cqrow[c] * cs;
-              const double g = ((mb >> (8 * h + k)) & 1u) ? gr : 0.0;
-              pack_put(pk, 8 * h + k, digits_word(g * sg));
-            }
+            for (int k = 0; k < 8; ++k)
+              wd[8 * h + k] = bdig(__hiloint2double((int)hi[k], (int)lo[k]), sg24);
           }
-          pack_store(pk, abase, b * 16 * 128);
+          bstore16(wd, abase, b * 16 * 128);
         }
         tc_fence_before();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         bar_pbcd<NH>();
         if (threadIdx.x == 0) issue_round(a_s, b_s, tmem_base, rp, p.r, bar_d);
         // ---------------- round B: T2 = g G ----------------
-        mbar_wait(bar_d, round & 1);
+        mbar_wait_hint(bar_d, round & 1);
         ++round;
         tc_fence_after();
-        // den = sum_j g_j h_j with g = rebuild / sg, h = T2 gsc / sg: accumulate rebuild * T2 gsc
-        // and apply the exact power-of-two 1 / sg^2 once
+        // den = sum_j g_j h_j with g = n 2^-24 / sg (n: the digits' grid integer), h = T2 gsc / sg:
+        // accumulate n * T2 gsc and apply the exact power of two 2^-24 / sg^2 once
         double den = 0.0;
         const double isg = 1.0 / sg;
 #pragma unroll 1
         for (int b = 0; b < CW / 16; ++b) {
-          uint4 dq[4];
-#pragma unroll
-          for (int pl = 0; pl < 4; ++pl)
-            dq[pl] = *reinterpret_cast<const uint4*>(abase + pl * PLANE_A + b * 16 * 128);
+          int gn[16];
+          bload16(abase, b * 16 * 128, gn);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             uint32_t v[4][8];
@@ -383,12 +509,12 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const int c = 16 * b + 8 * hh + k;
-              const double a = comb4(v[0][k], v[1][k], v[2][k], v[3][k]);
-              den = fma(rebuild(dq, 8 * hh + k), a * gsc[c], den);
+              const double a = comb8(v[0][k], v[1][k], v[2][k], v[3][k]);
+              den = fma(i2d(gn[8 * hh + k]), a * gsc[c], den);
             }
           }
         }
-        den *= isg * isg;
+        den *= 0x1p-24 * isg * isg;
         tc_fence_before();
         xch[hc][rt] = den;
         bar_pbcd<NH>();
@@ -398,29 +524,16 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
         // Eq.(10): d_i = ||g_i||^2 / ||g_i V^T||^2 (0 on a zero denominator, R10); Eq.(8)
         const double dstep = denr > 0.0 ? numr / denr : 0.0;
         opaque(mlo, mhi);
+        const double dsg = dstep * 0x1p-24 * isg;     // step on the grid integers of g
 #pragma unroll
         for (int b = 0; b < CW / 16; ++b) {
-          uint4 dq[4];
-#pragma unroll
-          for (int pl = 0; pl < 4; ++pl)
-            dq[pl] = *reinterpret_cast<const uint4*>(abase + pl * PLANE_A + b * 16 * 128);
+          int gn[16];
+          bload16(abase, b * 16 * 128, gn);
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
             const int c = 16 * b + k;
-            const double un = fmax(0.0, u[c] - dstep * (rebuild(dq, k) * isg));
+            const double un = fmax(0.0, u[c] - dsg * i2d(gn[k]));
             u[c] = mbit(mlo, mhi, c) ? un : u[c];     // entries outside M_{U+} stay fixed
-          }
-        }
-        if (rok) {
-          // snapshot, tile-major (pbcd_copy_tiled_kernel): a warp's 32 rows are contiguous
-          const int nt = (int)(p.rows - (int64_t)t * BM < BM ? p.rows - (int64_t)t * BM : BM);
-          float* sn = p.snaps + (int64_t)it * snap_stride + (int64_t)t * BM * p.r +
-                      (int64_t)c0 * nt + rt;
-          const int ncol = p.r - c0 < CW ? p.r - c0 : CW;   // columns of my part that exist
-#pragma unroll
-          for (int c = 0; c < CW; ++c) {
-            if (c < ncol) *sn = (float)u[c];
-            sn += nt;
           }
         }
         bar_pbcd<NH>();          // everyone has read the g digits before they are overwritten
@@ -428,7 +541,7 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
     }
     bar_pbcd<NH>();
     if (threadIdx.x == 32)
-      for (int it = 0; it <= p.max_iter; ++it)
+      for (int it = it0; it <= it1; ++it)
         p.pgparts[(int64_t)blockIdx.x * (p.max_iter + 1) + it] = pgsm[it];
   }
   tc_fence_before();
@@ -441,6 +554,9 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
 
 // G (r x r fp64, symmetric) -> 4 digit planes of the B operand (row j of B = column j of G,
 // power-of-two scale t_j per column), layout (g * (KR/16) + kc) * 128 + ri * 16 + ki.
+// BYTE8: the byte digits of tc_pbcd_kernel (bdig: 4 balanced base-2^8 digits on the 2^-24
+// grid); else the balanced base-2^7 digits on the 2^-21 grid of tc_hals_kernel.
+template <bool BYTE8>
 __global__ void __launch_bounds__(KR) gdigits_kernel(const double* __restrict__ G, int r, int rp,
                                                      int8_t* gd, double* gscale, const int* stage,
                                                      int want, int* ill) {
@@ -472,11 +588,17 @@ __global__ void __launch_bounds__(KR) gdigits_kernel(const double* __restrict__ 
   }
   const double t = pow2s(mx);
   if (l == 0 && j < r) gscale[j] = 1.0 / t;
-  const Dig4 z = digits4(g * t);
   const int plane = rp * KR;
   const int off = ((j >> 3) * (KR / 16) + (l >> 4)) * 128 + (j & 7) * 16 + (l & 15);
+  if (BYTE8) {
+    const uint32_t w = bdig(g * t);
 #pragma unroll
-  for (int pl = 0; pl < 4; ++pl) gd[pl * plane + off] = z.d[pl];
+    for (int pl = 0; pl < 4; ++pl) gd[pl * plane + off] = (int8_t)(w >> (8 * (3 - pl)));
+  } else {
+    const Dig4 z = digits4(g * t);
+#pragma unroll
+    for (int pl = 0; pl < 4; ++pl) gd[pl * plane + off] = z.d[pl];
+  }
 }
 
 // ------------------------------------------------------------------------------ HALS
@@ -945,38 +1067,58 @@ int tc_pbcd_parts() { return kSMs; }
 
 bool tc_pbcd_supported(int r) { return r >= 1 && r <= 128; }
 
-// Same contract as pbcd_rows (kernels_rows.cu); pgparts holds gridDim x (max_iter + 1).
-int tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
-                  const double* G, const double* lam, int max_iter, float* snaps,
-                  double* pgparts, int8_t* gd_work, double* gscale_work, const int* stage,
-                  cudaStream_t st) {
+// G (r x r) -> the B-operand digits and column scales of tc_pbcd_chunk (ascent stage only).
+void tc_pbcd_prepare(const double* G, int r, int8_t* gd_work, double* gscale_work,
+                     const int* stage, cudaStream_t st) {
   using namespace tpb;
-  const int rp = KR;   // G padded to 128 columns: class k of the accumulators at column k * 128
-  gdigits_kernel<<<rp, KR, 0, st>>>(G, r, rp, gd_work, gscale_work, stage, 0, nullptr);
+  gdigits_kernel<true><<<KR, KR, 0, st>>>(G, r, KR, gd_work, gscale_work, stage, 0, nullptr);
+  count_launch();
+}
+
+// One stage [it0, it1) of Alg. 2 on the tensor cores (see Params), or (rctl != nullptr) the
+// replay of the stage in which the stopping rule fired; pgparts holds gridDim x
+// (max_iter + 1), a launch writes columns it0 .. it1.  The caller reduces the partials and
+// applies the stopping rule between stages (pbcd_select_stage), which sets *done.
+int tc_pbcd_chunk(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
+                  const double* lam, int max_iter, int it0, int it1, int src, int dst,
+                  double* ust0, double* ust1, double* pgparts, const int8_t* gd_work,
+                  const double* gscale_work, const int* stage, const int* done,
+                  const int* kprev, const int* rctl, const int* kst, cudaStream_t st) {
+  using namespace tpb;
   Params p;
   p.F = F;
   p.ldf = ldf;
   p.rows = rows;
   p.r = r;
-  p.rp = rp;
+  p.rp = KR;   // G padded to 128 columns: class k of the accumulators at column k * 128
   p.C = C;
   p.gd = gd_work;
   p.gscale = gscale_work;
   p.lam = lam;
   p.max_iter = max_iter;
-  p.snaps = snaps;
   p.pgparts = pgparts;
   p.stage = stage;
+  p.it0 = it0;
+  p.it1 = it1;
+  p.src = src;
+  p.dst = dst;
+  p.ust[0] = ust0;
+  p.ust[1] = ust1;
+  p.done = done;
+  p.kprev = kprev;
+  p.rctl = rctl;
+  p.kst = kst;
+  if (!ust0 || !ust1 || dst < 0 || dst > 1 || src > 1 ||
+      (!rctl && (it0 < 0 || it1 <= it0 || it1 > max_iter)) || (rctl && !kst))
+    return 1;
   const size_t smem = SMEM_BYTES + sizeof(double) * (max_iter + 1);
   // the dynamic size grows with max_iter; static shared memory (row exchanges) counts against
   // the same 227 KB, so the attribute is the exact dynamic request, raised when it grows
-  // NH = 4 (16 warps, 32 columns per thread) unless ENMF_TC_PBCD_NH=2 (the round-1 form)
-  const char* nh = getenv("ENMF_TC_PBCD_NH");
-  const bool four = !(nh && nh[0] == '2');
-  static size_t attr2 = 0, attr4 = 0;
-  size_t& attr = four ? attr4 : attr2;
+  // NH = 4: 16 warps, 32 columns per thread (round 1's NH = 2, 64 columns per thread, was
+  // 15 % slower: fewer warps to hide the MMA round trips and TMEM / shared-memory latencies)
+  static size_t attr = 0;
   if (smem > attr) {
-    auto k = four ? tc_pbcd_kernel<4> : tc_pbcd_kernel<2>;
+    auto k = tc_pbcd_kernel<4>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return 1;
@@ -984,11 +1126,8 @@ int tc_pbcd_rows(const float* F, int64_t ldf, int64_t rows, int r, const double*
     attr = smem;
   }
   // unused CTAs of the persistent grid still write their (zero) partials: launch kSMs always
-  if (four)
-    tc_pbcd_kernel<4><<<kSMs, 512, smem, st>>>(p);
-  else
-    tc_pbcd_kernel<2><<<kSMs, 256, smem, st>>>(p);
-  count_launch(2);
+  tc_pbcd_kernel<4><<<kSMs, 512, smem, st>>>(p);
+  count_launch();
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -1000,7 +1139,7 @@ int tc_hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, co
                  cudaStream_t st) {
   using namespace tpb;
   if (ill != nullptr && cudaMemsetAsync(ill, 0, sizeof(int), st) != cudaSuccess) return 1;
-  gdigits_kernel<<<KR, KR, 0, st>>>(G, r, KR, gd_work, gscale_work, stage, 1, ill);
+  gdigits_kernel<false><<<KR, KR, 0, st>>>(G, r, KR, gd_work, gscale_work, stage, 1, ill);
   HParams p;
   p.F = F;
   p.ldf = ldf;

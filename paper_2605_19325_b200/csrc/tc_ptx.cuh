@@ -40,6 +40,29 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
   }
 }
+// mbar_wait with a suspend-time hint: a waiting thread may be suspended in try_wait until the
+// phase completes (or ~the hint, in ns) instead of re-polling -- for waits every warp of a CTA
+// takes at once (the MMA rounds of tc_pbcd_kernel), where polling warps only steal issue slots
+// from the thread that issues the MMAs.
+__device__ __forceinline__ void mbar_wait_hint(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  long long t0 = 0;
+  int spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity), "r"(20000)
+        : "memory");
+    if (done) return;
+    if (++spins == 64) t0 = clock64();
+    if (spins > 64 && (spins & 63) == 0 && clock64() - t0 > 40000000000LL) {
+      printf("enmf tc: mbarrier wait timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+      __trap();
+    }
+  }
+}
 // For barriers a peer CTA arrives on.  CTA-scope polling, as CUTLASS's cluster barriers do:
 // try_wait.acquire.cluster invalidates L1 on every poll and a per-stage fence.acq_rel.cluster
 // serialises the issuing thread (both measured: 2x slower pair kernel).  The data that matters
