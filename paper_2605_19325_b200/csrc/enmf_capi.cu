@@ -81,7 +81,8 @@ static enmf_status_t prof_mark(enmf_handle_t h, int kind) {
   return ENMF_OK;
 }
 
-// Accumulate elapsed times of completed event pairs (stream already synchronised).
+// Accumulate elapsed times of completed event pairs (stream already synchronised), plus the
+// X V passes timed by their own kernel timestamps (fused sweeps: see sweep()).
 static void prof_collect(enmf_handle_t h) {
   for (size_t p = 0; p + 1 < h->ev_used; p += 2) {
     float ms = 0.f;
@@ -93,11 +94,26 @@ static void prof_collect(enmf_handle_t h) {
   }
   h->ev_used = 0;
   h->ev_kind.clear();
+  if (h->tc) {
+    double ms = 0.0;
+    int64_t cnt = 0;
+    if (tc_stamp_read(h->tc, &ms, &cnt) == 0) {
+      h->prof_ms[0] += ms;
+      h->prof_cnt[0] += cnt;
+    }
+  }
 }
 
 // P = X V (this rank's rows): the first X pass of a sweep.
+// band_ready (tensor-core path, tc_band_flags): the pass publishes its finished bands for the
+// U-block kernel enqueued right behind it; it is then timed by its own timestamps (an event
+// between the two launches would serialise them).
 enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* P,
-                          const unsigned long long* vmax) {
+                          const unsigned long long* vmax, unsigned* band_ready) {
+  if (band_ready) {
+    return tc_xv(h->tc, V, ldv, P, h->st, vmax, band_ready, h->prof) != 0 ? ENMF_ERR_CUDA
+                                                                         : ENMF_OK;
+  }
   ENMF_TRY(prof_mark(h, 0));
   if (h->sparse) {
     spmm<float>(h->csr_ptr, h->csr_col, h->csr_val, h->m_loc, V, ldv, (int)h->r, P, h->r, h->st);
@@ -169,12 +185,14 @@ namespace {
 
 // One block update (U block: F = U, C = P, G = G_V; V block: F = V, C = Q, G = G_U).
 // In the ascent stage: lift + mask + PBCD (Eqs.(6)-(10), Alg. 2); in HALS: the column sweep.
+// hals_issued: the tensor-core HALS kernel of this block is already enqueued (fused with the
+// X V pass, see sweep()) together with the colmax reset and its G digits.
 enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
                            const double* C, const double* G, int lam_slot, int kstar_slot,
                            int min_slot, bool sharded, bool maybe_ascent,
-                           unsigned long long* colmax = nullptr) {
+                           unsigned long long* colmax = nullptr, bool hals_issued = false) {
   const int r = (int)h->r;
-  if (colmax)
+  if (colmax && !hals_issued)
     CUDA_TRY(cudaMemsetAsync(colmax, 0, sizeof(unsigned long long) * r, h->st));
   int* stage = h->dint + I_STAGE;
   const int mi = h->opt.pbcd_max_iter;
@@ -250,7 +268,8 @@ enmf_status_t block_update(enmf_handle_t h, float* F, int64_t ldf, int64_t rows,
   if (h->tc_hals) {
     // tensor-core HALS; if G has a column too ill-conditioned for the digit coupling the
     // device flag I_HALS_ILL hands the sweep to the SIMT fp64 kernel (no host sync)
-    if (tc_hals_rows(F, ldf, rows, r, C, G, reinterpret_cast<int8_t*>(h->tcpb_ws + 128),
+    if (!hals_issued &&
+        tc_hals_rows(F, ldf, rows, r, C, G, reinterpret_cast<int8_t*>(h->tcpb_ws + 128),
                      h->tcpb_ws, stage, h->minparts, kRowGrid, colmax, h->dint + I_HALS_FB,
                      h->dint + I_HALS_ILL, h->st))
       return ENMF_ERR_CUDA;
@@ -306,15 +325,51 @@ enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ld
   unsigned long long* umax =
       h->fmax_uv && ((h->tc_pbcd && !h->opt.step_rule) || !maybe_ascent) ? h->fmax_uv : nullptr;
   unsigned long long* vmax = umax ? h->fmax_uv + 128 : nullptr;
-  ENMF_TRY(contract_xv(h, V, ldv, h->P, h->vmax_valid ? h->fmax_uv + 128 : nullptr));
-  if (hk.u_ready) {                    // U arrives on the copy stream during the X V pass
-    CUDA_TRY(cudaStreamWaitEvent(st, hk.u_ready, 0));
-    ENMF_TRY(min_factor(h, U, ldu, h->m_loc, S_MINU, sh));
+  const unsigned long long* vmax_in = h->vmax_valid ? h->fmax_uv + 128 : nullptr;
+  // Fused U block (tensor-core path, HALS on the tensor cores, P written without a K split):
+  // the HALS kernel is enqueued right behind the X V pass with programmatic dependent launch
+  // and takes each 128-row band of P as the pass publishes it, so its tiles fill the SMs the
+  // pass's last wave leaves idle (1563 bands on 148 SMs at C5: 65 SMs idle for the last band)
+  // instead of waiting for the whole pass.  Everything it needs from before the pass (the
+  // stage decision, G_V's digits, the colmax reset) is enqueued ahead of the pass.
+  const char* fe = getenv("ENMF_FUSE_HALS");
+  const bool fuse_ok = h->tc && h->tc_hals && !h->sparse && !hk.u_ready && !h->opt.descent &&
+                       !(fe && fe[0] == '0');
+  bool fused = false;
+  if (fuse_ok) {
+    stage_update(h->dint + I_STAGE, h->dscal + S_MINU, h->dscal + S_MINV, h->dint + I_CNT_ASC,
+                 st);
+    if (umax) CUDA_TRY(cudaMemsetAsync(umax, 0, sizeof(unsigned long long) * h->r, st));
+    int8_t* gd = reinterpret_cast<int8_t*>(h->tcpb_ws + 128);
+    if (tc_hals_prepare(h->GV, (int)h->r, gd, h->tcpb_ws, h->dint + I_STAGE,
+                        h->dint + I_HALS_ILL, st))
+      return ENMF_ERR_CUDA;
+    unsigned* bands = tc_band_flags(h->tc, st);
+    if (bands) {
+      ENMF_TRY(contract_xv(h, V, ldv, h->P, vmax_in, bands));
+      if (tc_hals_launch(U, ldu, h->m_loc, (int)h->r, h->P, h->GV, gd, h->tcpb_ws,
+                         h->dint + I_STAGE, h->minparts, kRowGrid, umax, h->dint + I_HALS_FB,
+                         h->dint + I_HALS_ILL, bands, tc_bands(h->tc), st))
+        return ENMF_ERR_CUDA;
+      if (h->prof && tc_stamp_accum(h->tc, st)) return ENMF_ERR_CUDA;
+      fused = true;
+    } else {
+      ENMF_TRY(contract_xv(h, V, ldv, h->P, vmax_in));
+    }
+  } else {
+    ENMF_TRY(contract_xv(h, V, ldv, h->P, vmax_in));
+    if (hk.u_ready) {                    // U arrives on the copy stream during the X V pass
+      CUDA_TRY(cudaStreamWaitEvent(st, hk.u_ready, 0));
+      ENMF_TRY(min_factor(h, U, ldu, h->m_loc, S_MINU, sh));
+    }
+    // stage control: HALS once U >= 0 and V >= 0
+    stage_update(h->dint + I_STAGE, h->dscal + S_MINU, h->dscal + S_MINV, h->dint + I_CNT_ASC,
+                 st);
   }
-  // stage control: HALS once U >= 0 and V >= 0
-  stage_update(h->dint + I_STAGE, h->dscal + S_MINU, h->dscal + S_MINV, h->dint + I_CNT_ASC, st);
+  // (fused but without band flags: tc_hals_prepare already ran, so the kernel is enqueued
+  // by block_update through tc_hals_rows, which repeats the cheap digit preparation)
   ENMF_TRY(block_update(h, U, ldu, h->m_loc, h->P, h->GV, S_LAMU, I_KSTAR_U, S_MINU, sh,
-                        maybe_ascent, umax));
+                        maybe_ascent, umax, fused));
   h->umax_valid = umax != nullptr;
   if (hk.u_download) {                 // U is final: download it behind the V block
     CUDA_TRY(cudaEventRecord(h->ev_a, st));

@@ -143,7 +143,8 @@ enmf_status_t dalloc(T** p, size_t count) {
 }
 enmf_status_t ar(enmf_handle_t h, double* buf, size_t count, CommOp op);
 enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* P,
-                          const unsigned long long* vmax = nullptr);
+                          const unsigned long long* vmax = nullptr,
+                          unsigned* band_ready = nullptr);
 enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q,
                            const unsigned long long* umax = nullptr, bool slice = false);
 enmf_status_t gram_f32(enmf_handle_t h, const float* A, int64_t lda, int64_t rows, double* G,

@@ -34,7 +34,20 @@ void tc_destroy(TcState* s);
 // (optional, device u64[r]): fp64 bits of the factor's column maxima |F| when the kernel that
 // wrote the factor already computed them (hals / pbcd copy); else a scan computes them.
 int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st,
-          const unsigned long long* vmax = nullptr);
+          const unsigned long long* vmax = nullptr, unsigned* band_ready = nullptr,
+          bool stamp = false);
+// stamp: the X V kernel records its own start / end (%globaltimer); tc_stamp_accum (enqueue
+// after the pass, anywhere later in the stream) adds end - start to a device total that
+// tc_stamp_read returns (ms, passes; synchronous) and resets.  For timing the pass when its
+// successor overlaps it (no CUDA event can sit between the two launches).
+int tc_stamp_accum(TcState* s, cudaStream_t st);
+int tc_stamp_read(TcState* s, double* ms, int64_t* count);
+// Band flags for overlapping the U-block update with P = X V (programmatic dependent launch):
+// null unless pass 1 writes P directly (no K split, single-CTA kernel).  Enqueues the epoch
+// increment on st; pass the result to tc_xv (the X pass then publishes each finished
+// 128-row band) and to tc_hals_launch.  tc_bands: the number of 128-row bands (Mt).
+unsigned* tc_band_flags(TcState* s, cudaStream_t st);
+int64_t tc_bands(const TcState* s);
 int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st,
            const unsigned long long* umax = nullptr);
 // Column-block products for the randomised SVD (fp64 factors of any width):
@@ -71,6 +84,16 @@ int tc_pbcd_chunk(const float* F, int64_t ldf, int64_t rows, int r, const double
 // (optional, device int): set nonzero when some column of G is too ill-conditioned for the
 // digit coupling (the kernel then returns at once; run hals_rows gated on *ill).  0 = launched.
 int tc_hals_parts();
+// tc_hals_rows in two steps: the G digits (and the ill flag), then the kernel.  band_ready /
+// bands (optional, tc_band_flags / tc_bands): the kernel takes tiles as the X V pass just
+// enqueued before it publishes their bands, launched with programmatic dependent launch, so
+// it must directly follow that pass in the stream.
+int tc_hals_prepare(const double* G, int r, int8_t* gd_work, double* gscale_work,
+                    const int* stage, int* ill, cudaStream_t st);
+int tc_hals_launch(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
+                   const int8_t* gd_work, const double* gscale_work, const int* stage,
+                   double* minparts, int nparts, unsigned long long* colmax, int* fallbacks,
+                   const int* ill, unsigned* band_ready, int64_t bands, cudaStream_t st);
 int tc_hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
                  int8_t* gd_work, double* gscale_work, const int* stage, double* minparts,
                  int nparts, unsigned long long* colmax, int* fallbacks, int* ill,

@@ -89,7 +89,20 @@ struct Params {
   int r;                     // valid output columns
   int64_t out_rows;          // valid output rows
   int tiles;                 // 128-row output tiles (pair kernel: tile 2 t + rank may not exist)
+  // mode 0, no K split: after a band's output rows are stored each epilogue warp adds 1 to
+  // band_ready[tile] (release), so a consumer launched behind this kernel with programmatic
+  // dependent launch (tc_hals_kernel) can take the band while later bands are still running
+  unsigned* band_ready;
+  // optional: {earliest CTA start, latest CTA end} in %globaltimer ns (atomicMin / atomicMax):
+  // the pass's own device time when its successor overlaps it (no event can sit between them)
+  unsigned long long* tstamp;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 using namespace tcp;
 
@@ -147,6 +160,10 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
   const uint32_t bar_tfull = smem_u32(&bars[2 * NST]);
   const uint32_t bar_tempty = smem_u32(&bars[2 * NST + 1]);
   const uint32_t tile_b = (uint32_t)p.rp * BK;
+  // a dependent grid (programmatic dependent launch) may start as soon as SMs free up: it
+  // synchronises on band_ready, not on this grid's completion
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (p.tstamp != nullptr && threadIdx.x == 0) atomicMin(&p.tstamp[0], gtimer());
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
@@ -294,14 +311,19 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
         }
       }
       zero_acc_slice(tmem_base, q, hcol, p.rp);   // acc2 starts at 0 for the next unit
+      if (p.band_ready != nullptr) __threadfence();  // this lane's rows before the flag
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_tempty);
+      if (lane == 0) {
+        mbar_arrive(bar_tempty);
+        if (p.band_ready != nullptr) atomicAdd(&p.band_ready[tile], 1u);
+      }
       ++nunit;
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (p.tstamp != nullptr && threadIdx.x == 0) atomicMax(&p.tstamp[1], gtimer());
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -814,6 +836,8 @@ struct TcState {
   bool pair = false;           // cta_group::2 kernel (ENMF_TC_PAIR=1 enables)
   int ksplit1p = 1, ksplit2p = 1;
   int sms = kSMs;
+  unsigned* band_flags = nullptr;   // Mt + 2: pass-1 band flags, epoch, consumer tile counter
+  unsigned long long* stamps = nullptr;   // 4: pass-1 kernel timestamps (tc_stamp_*)
 };
 
 bool tc_supported(int64_t rows, int64_t n, int64_t r) {
@@ -826,7 +850,7 @@ void tc_destroy(TcState* s) {
   if (s->xtp[0]) cudaFree(s->xtp[0]);
   if (s->fp[0]) cudaFree(s->fp[0]);
   void* bufs[] = {s->xinv_r, s->xinv_c, s->xbits, s->xq2, s->fmaxbits, s->fscale,
-                  s->colscale, s->partial, s->colbuf};
+                  s->colscale, s->partial, s->colbuf, s->band_flags, s->stamps};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete s;
@@ -1011,8 +1035,11 @@ static void pack_factor(TcState* s, const T* F, int64_t ldf, int64_t K, int64_t 
 
 static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out_ld,
                        int64_t split_stride, int tiles, int ksplit, int stages_total,
-                       int64_t out_rows, int ncols, int rp, cudaStream_t st) {
+                       int64_t out_rows, int ncols, int rp, cudaStream_t st,
+                       unsigned* band_ready = nullptr, unsigned long long* tstamp = nullptr) {
   Params p;
+  p.band_ready = (mode == 0 && ksplit == 1 && !pair) ? band_ready : nullptr;
+  p.tstamp = pair ? nullptr : tstamp;
   for (int q = 0; q < PLANES; ++q) {
     p.xp[q] = s->xp[q];
     p.xtp[q] = s->xtp[q];
@@ -1051,8 +1078,70 @@ static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+// band flags: Mt counters, then the epoch (flagged passes so far) and a tile counter for the
+// consumer's dynamic schedule
+__global__ void band_epoch_kernel(unsigned* flags, int64_t Mt) {
+  flags[Mt] += 1u;
+  flags[Mt + 1] = 0u;
+}
+
+unsigned* tc_band_flags(TcState* s, cudaStream_t st) {
+  if (s->pair || s->ksplit1 != 1) return nullptr;
+  if (!s->band_flags) {
+    if (cudaMalloc(&s->band_flags, sizeof(unsigned) * (s->Mt + 2)) != cudaSuccess) {
+      s->band_flags = nullptr;
+      cudaGetLastError();
+      return nullptr;
+    }
+    if (cudaMemsetAsync(s->band_flags, 0, sizeof(unsigned) * (s->Mt + 2), st) != cudaSuccess)
+      return nullptr;
+  }
+  band_epoch_kernel<<<1, 1, 0, st>>>(s->band_flags, s->Mt);
+  count_launch();
+  return s->band_flags;
+}
+
+int64_t tc_bands(const TcState* s) { return s ? s->Mt : 0; }
+
+// pass-1 device time from the kernel's own timestamps: {start, end, accumulated ns, count}
+__global__ void stamp_accum_kernel(unsigned long long* ts) {
+  if (ts[1] > ts[0]) {
+    ts[2] += ts[1] - ts[0];
+    ts[3] += 1ull;
+  }
+  ts[0] = ~0ull;
+  ts[1] = 0ull;
+}
+
+static int ensure_stamps(TcState* s) {
+  if (s->stamps) return 0;
+  if (cudaMalloc(&s->stamps, 4 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  const unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
+  return cudaMemcpy(s->stamps, init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess ? 0 : 1;
+}
+
+int tc_stamp_accum(TcState* s, cudaStream_t st) {
+  if (!s->stamps) return 0;
+  stamp_accum_kernel<<<1, 1, 0, st>>>(s->stamps);
+  count_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int tc_stamp_read(TcState* s, double* ms, int64_t* count) {
+  *ms = 0.0;
+  *count = 0;
+  if (!s || !s->stamps) return 0;
+  unsigned long long h[4];
+  if (cudaMemcpy(h, s->stamps, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+  *ms = (double)h[2] * 1e-6;
+  *count = (int64_t)h[3];
+  const unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
+  return cudaMemcpy(s->stamps, init, sizeof(init), cudaMemcpyHostToDevice) == cudaSuccess ? 0 : 1;
+}
+
 int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st,
-          const unsigned long long* vmax) {
+          const unsigned long long* vmax, unsigned* band_ready, bool stamp) {
+  if (stamp && ensure_stamps(s)) return 1;
   // B = V (K = n), over all 64-column stages of X
   const int r = (int)s->r;
   pack_factor<float>(s, V, ldv, s->n, s->tiles_per_row, r, s->rp, st, vmax);
@@ -1060,7 +1149,7 @@ int tc_xv(TcState* s, const float* V, int64_t ldv, double* P, cudaStream_t st,
   const int ks = pair ? s->ksplit1p : s->ksplit1;
   if (ks == 1)
     return launch_gemm(s, 0, pair, P, r, 0, (int)s->Mt, 1, (int)s->tiles_per_row, s->rows, r,
-                       s->rp, st);
+                       s->rp, st, band_ready, stamp ? s->stamps : nullptr);
   if (launch_gemm(s, 0, pair, s->partial, r, s->rows * r, (int)s->Mt, ks, (int)s->tiles_per_row,
                   s->rows, r, s->rp, st))
     return 1;

@@ -641,7 +641,41 @@ struct HParams {
   unsigned long long* colmax;                 // optional, u64[r]
   int* fallbacks;                             // optional
   const int* ill;                             // optional: nonzero -> the SIMT kernel runs
+  // optional (tc_band_flags): tiles taken in order from the counter band_ready[bands + 1],
+  // each once its pass-1 band is published (band_ready[t] >= 8 x epoch band_ready[bands]):
+  // this kernel then runs behind the X V pass with programmatic dependent launch
+  unsigned* band_ready;
+  int64_t bands;
 };
+
+// the next tile of a dynamically scheduled launch, once its P rows are published (thread 0
+// polls with acquire loads; the CTA barrier then orders everyone's reads after them)
+__device__ __forceinline__ int next_band_tile(unsigned* band_ready, int64_t bands, int tiles,
+                                              int* tile_s) {
+  if (threadIdx.x == 0) {
+    const int t = (int)atomicAdd(&band_ready[bands + 1], 1u);
+    if (t < tiles) {
+      const unsigned want = 8u * *((volatile unsigned*)&band_ready[bands]);
+      unsigned v;
+      long long t0 = clock64();
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(band_ready + t)
+                     : "memory");
+        if (v >= want) break;
+        __nanosleep(256);
+        if (clock64() - t0 > 40000000000LL) {
+          printf("enmf tc: band %d never published (%u < %u)\n", t, v, want);
+          __trap();
+        }
+      }
+    }
+    *tile_s = t;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(HT) : "memory");
+  const int t = *tile_s;
+  asm volatile("bar.sync 1, %0;" ::"n"(HT) : "memory");   // *tile_s is reused by the next call
+  return t;
+}
 
 // (k, j), j >= k, of a packed upper-triangular 32 x 32 block; (k, k) holds 1 / G_kk (the
 // diagonal itself is never needed: t_k is dead once u_k is updated)
@@ -790,8 +824,13 @@ __global__ void __launch_bounds__(HT, 1) tc_hals_kernel(const HParams p) {
   __shared__ double gsc_s[KR];
   __shared__ unsigned cm_s[KR];                                  // fp32 bits of max |u|
   __shared__ double wmin_s[HT / 32];
-  if (p.stage != nullptr && *p.stage != 1) return;
-  if (p.ill != nullptr && *p.ill != 0) return;
+  // Launched as the programmatic dependent of the X V pass (band_ready), this grid may finish
+  // before that pass does; griddepcontrol.wait (a no-op otherwise) on every exit keeps the
+  // stream order for what follows (the PBCD stages and the SIMT fallback read P).
+  if ((p.stage != nullptr && *p.stage != 1) || (p.ill != nullptr && *p.ill != 0)) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = p.r;
   const int nblk = (r + HB - 1) / HB;
@@ -842,7 +881,11 @@ __global__ void __launch_bounds__(HT, 1) tc_hals_kernel(const HParams p) {
   uint32_t round = 0;
   double wmin = DBL_MAX;
   int nfall = 0;
-  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+  __shared__ int tile_s;
+  const bool dyn = p.band_ready != nullptr;
+  for (int t = dyn ? next_band_tile(p.band_ready, p.bands, tiles, &tile_s) : (int)blockIdx.x;
+       t < tiles;
+       t = dyn ? next_band_tile(p.band_ready, p.bands, tiles, &tile_s) : t + (int)gridDim.x) {
     const int64_t row0 = (int64_t)t * BM;
     const int nt = (int)(p.rows - row0 < BM ? p.rows - row0 : BM);
     const bool rok = rt < nt;
@@ -1059,6 +1102,7 @@ __global__ void __launch_bounds__(HT, 1) tc_hals_kernel(const HParams p) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 }  // namespace tpb
@@ -1133,13 +1177,20 @@ int tc_pbcd_chunk(const float* F, int64_t ldf, int64_t rows, int r, const double
 
 int tc_hals_parts() { return kSMs; }
 
-int tc_hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
-                 int8_t* gd_work, double* gscale_work, const int* stage, double* minparts,
-                 int nparts, unsigned long long* colmax, int* fallbacks, int* ill,
-                 cudaStream_t st) {
+int tc_hals_prepare(const double* G, int r, int8_t* gd_work, double* gscale_work,
+                    const int* stage, int* ill, cudaStream_t st) {
   using namespace tpb;
   if (ill != nullptr && cudaMemsetAsync(ill, 0, sizeof(int), st) != cudaSuccess) return 1;
   gdigits_kernel<false><<<KR, KR, 0, st>>>(G, r, KR, gd_work, gscale_work, stage, 1, ill);
+  count_launch();
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int tc_hals_launch(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
+                   const int8_t* gd_work, const double* gscale_work, const int* stage,
+                   double* minparts, int nparts, unsigned long long* colmax, int* fallbacks,
+                   const int* ill, unsigned* band_ready, int64_t bands, cudaStream_t st) {
+  using namespace tpb;
   HParams p;
   p.F = F;
   p.ldf = ldf;
@@ -1155,6 +1206,9 @@ int tc_hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, co
   p.colmax = colmax;
   p.fallbacks = fallbacks;
   p.ill = ill;
+  p.band_ready = band_ready;
+  p.bands = bands;
+  if (band_ready != nullptr && bands != (rows + BM - 1) / BM) return 1;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(tc_hals_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1162,9 +1216,34 @@ int tc_hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, co
       return 1;
     attr = true;
   }
-  tc_hals_kernel<<<kSMs, HT, H_SMEM, st>>>(p);
-  count_launch(2);
+  if (band_ready == nullptr) {
+    tc_hals_kernel<<<kSMs, HT, H_SMEM, st>>>(p);
+  } else {
+    // programmatic dependent launch behind the X V pass (which triggers at its start): CTAs
+    // take SMs as pass-1 CTAs retire and consume bands as they are published
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kSMs);
+    cfg.blockDim = dim3(HT);
+    cfg.dynamicSmemBytes = H_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, tc_hals_kernel, p) != cudaSuccess) return 1;
+  }
+  count_launch();
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int tc_hals_rows(float* F, int64_t ldf, int64_t rows, int r, const double* C, const double* G,
+                 int8_t* gd_work, double* gscale_work, const int* stage, double* minparts,
+                 int nparts, unsigned long long* colmax, int* fallbacks, int* ill,
+                 cudaStream_t st) {
+  if (tc_hals_prepare(G, r, gd_work, gscale_work, stage, ill, st)) return 1;
+  return tc_hals_launch(F, ldf, rows, r, C, G, gd_work, gscale_work, stage, minparts, nparts,
+                        colmax, fallbacks, ill, nullptr, 0, st);
 }
 
 }  // namespace enmf
