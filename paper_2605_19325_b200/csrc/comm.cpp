@@ -2,7 +2,9 @@
 // NCCL is resolved at run time with dlopen("libnccl.so.2") so the process uses the NCCL
 // already loaded by torch (or the system one when used from plain C).  ncclAllReduce for the
 // r x r Grams, the PBCD stopping partials and scalars; in a sweep the n x r partial X^T U is
-// reduce-scattered (each rank updates its V slice) and the V slices are all-gathered (fp32).
+// reduce-scattered (each rank updates its V slice) -- on the tensor-core path one ncclReduce
+// per slice, each overlapping the pass's next band range -- and the V slices are all-gathered
+// (fp32).
 #include <dlfcn.h>
 #include <nccl.h>
 #include <stdio.h>
@@ -19,6 +21,7 @@ struct Api {
   decltype(&ncclAllReduce) allreduce = nullptr;
   decltype(&ncclReduceScatter) reduce_scatter = nullptr;
   decltype(&ncclAllGather) allgather = nullptr;
+  decltype(&ncclReduce) reduce = nullptr;
   decltype(&ncclCommDestroy) destroy = nullptr;
   decltype(&ncclGetErrorString) errstr = nullptr;
 };
@@ -34,6 +37,7 @@ Api& api() {
       a.allreduce = (decltype(a.allreduce))dlsym(a.so, "ncclAllReduce");
       a.reduce_scatter = (decltype(a.reduce_scatter))dlsym(a.so, "ncclReduceScatter");
       a.allgather = (decltype(a.allgather))dlsym(a.so, "ncclAllGather");
+      a.reduce = (decltype(a.reduce))dlsym(a.so, "ncclReduce");
       a.destroy = (decltype(a.destroy))dlsym(a.so, "ncclCommDestroy");
       a.errstr = (decltype(a.errstr))dlsym(a.so, "ncclGetErrorString");
     }
@@ -51,7 +55,7 @@ struct Comm {
 int comm_init(Comm** out, const void* uid128, int world, int rank) {
   *out = nullptr;
   Api& a = api();
-  if (!a.init || !a.allreduce || !a.reduce_scatter || !a.allgather) return -1;
+  if (!a.init || !a.allreduce || !a.reduce_scatter || !a.allgather || !a.reduce) return -1;
   ncclUniqueId id;
   static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
   memcpy(&id, uid128, sizeof(id));
@@ -84,6 +88,14 @@ int comm_reduce_scatter(Comm* c, void* buf, size_t count, CommType t, cudaStream
   // in place: recvbuff = sendbuff + rank * recvcount (NCCL's in-place convention)
   ncclResult_t rc = api().reduce_scatter(b, b + (size_t)c->rank * count * esz, count, dt, ncclSum,
                                          c->comm, st);
+  return rc == ncclSuccess ? 0 : -1;
+}
+
+int comm_reduce(Comm* c, void* buf, size_t count, CommType t, int root, cudaStream_t st) {
+  if (!c || c->world == 1 || count == 0) return 0;
+  const ncclDataType_t dt = t == CommType::F64 ? ncclFloat64 : ncclFloat32;
+  // in place on the root (sendbuff == recvbuff); the other ranks only send
+  ncclResult_t rc = api().reduce(buf, buf, count, dt, ncclSum, root, c->comm, st);
   return rc == ncclSuccess ? 0 : -1;
 }
 

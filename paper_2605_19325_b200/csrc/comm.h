@@ -17,6 +17,8 @@ int comm_allreduce(Comm* c, void* buf, size_t count, CommType t, CommOp op, cuda
 // or scratch).  In-place all-gather: this rank's block of buf is sent, every block is filled.
 int comm_reduce_scatter(Comm* c, void* buf, size_t count, CommType t, cudaStream_t st);
 int comm_allgather(Comm* c, void* buf, size_t count, CommType t, cudaStream_t st);
+// In-place sum to `root` (buf holds count elements on every rank; the result on root).
+int comm_reduce(Comm* c, void* buf, size_t count, CommType t, int root, cudaStream_t st);
 void comm_destroy(Comm* c);
 // ncclGetUniqueId into 128 bytes (rank 0 of a job); 0 on success.
 int comm_unique_id(void* out128);

@@ -132,8 +132,57 @@ enmf_status_t contract_xv(enmf_handle_t h, const float* V, int64_t ldv, double* 
 // Q = X^T U summed over ranks: the second X pass.  slice: only this rank's V
 // slice of Q is needed (the sweep's sharded V block) -- with NCCL a reduce-scatter (Q holds
 // world x v_pad rows), otherwise the full allreduce (which includes the slice).
+//
+// Tensor-core path, several ranks, 128-row-aligned V slices: the pass runs slice by slice
+// (band range of the owner's rows, tc_xtu_bands) and each slice is summed to its owner
+// (ncclReduce on a communication stream) while the next slice computes -- the pass's
+// reduce-scatter overlapped with its own tail.  Through the
+// host collective (one-GPU multi-rank tests) each slice is allreduced in turn.
+static enmf_status_t contract_xtu_sliced(enmf_handle_t h, const float* U, int64_t ldu,
+                                         double* Q, const unsigned long long* umax) {
+  const int world = h->prob.world_size;
+  const int64_t r = h->r, bands = tc_xtu_band_count(h->tc), per = h->v_pad / 128;
+  if (h->comm) {
+    if (!h->st_comm) CUDA_TRY(cudaStreamCreateWithFlags(&h->st_comm, cudaStreamNonBlocking));
+    while ((int)h->ev_comm.size() < world + 1) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->ev_comm.push_back(e);
+    }
+  }
+  bool first = true;
+  for (int s = 0; s < world; ++s) {
+    const int64_t b0 = s * per, b1 = std::min(bands, (s + 1) * per);
+    if (b0 >= b1) continue;
+    const int rc = tc_xtu_bands(h->tc, U, ldu, Q, b0, b1, h->st, umax, first);
+    if (rc) return rc == 2 ? ENMF_ERR_OOM : ENMF_ERR_CUDA;
+    first = false;
+    const int64_t row0 = s * h->v_pad, rows = std::min(h->n, row0 + h->v_pad) - row0;
+    if (h->comm) {
+      CUDA_TRY(cudaEventRecord(h->ev_comm[s], h->st));
+      CUDA_TRY(cudaStreamWaitEvent(h->st_comm, h->ev_comm[s], 0));
+      if (comm_reduce(h->comm, Q + row0 * r, (size_t)(rows * r), CommType::F64, s,
+                      h->st_comm) != 0)
+        return ENMF_ERR_NCCL;
+    } else {
+      ENMF_TRY(ar(h, Q + row0 * r, (size_t)(rows * r), CommOp::Sum));
+    }
+  }
+  if (h->comm) {
+    CUDA_TRY(cudaEventRecord(h->ev_comm[world], h->st_comm));
+    CUDA_TRY(cudaStreamWaitEvent(h->st, h->ev_comm[world], 0));
+  }
+  return ENMF_OK;
+}
+
 enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q,
                            const unsigned long long* umax, bool slice) {
+  const char* pc = getenv("ENMF_PASS2_SLICED");
+  if (slice && h->tc && h->prob.world_size > 1 && h->v_pad % 128 == 0 && !(pc && pc[0] == '0')) {
+    ENMF_TRY(prof_mark(h, 1));
+    ENMF_TRY(contract_xtu_sliced(h, U, ldu, Q, umax));
+    return prof_mark(h, 1);
+  }
   ENMF_TRY(prof_mark(h, 1));
   if (h->sparse) {
     spmm<float>(h->csc_ptr, h->csc_row, h->csc_val, h->n, U, ldu, (int)h->r, Q, h->r, h->st);
@@ -588,6 +637,11 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
     cudaEventDestroy(h->ev_b);
   }
   if (h->ev_a) cudaEventDestroy(h->ev_a);
+  if (h->st_comm) {
+    cudaStreamSynchronize(h->st_comm);
+    cudaStreamDestroy(h->st_comm);
+  }
+  for (cudaEvent_t e : h->ev_comm) cudaEventDestroy(e);
   if (h->cap_st) cudaStreamDestroy(h->cap_st);
   if (h->tc) tc_destroy(h->tc);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
@@ -633,7 +687,14 @@ enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
   ALLOC(h->P, (size_t)(h->m_loc * r));
   // V slices: ceil(n / world) rows per rank; Q holds world such blocks for the in-place
   // reduce-scatter
+  // V slices (the sharded V block): ceil(n / world) rows each, rounded up to whole 128-row
+  // bands when every rank still gets rows (n >= 128 world), so that the tensor-core pass 2 can
+  // reduce each slice to its owner as soon as that slice's bands are done
   h->v_pad = (n + prob->world_size - 1) / prob->world_size;
+  if (prob->world_size > 1 && n >= 128 * (int64_t)prob->world_size) {
+    const int64_t al = (h->v_pad + 127) / 128 * 128;
+    if ((prob->world_size - 1) * al < n) h->v_pad = al;
+  }
   ALLOC(h->Q, (size_t)(std::max<int64_t>(n, h->v_pad * prob->world_size) * r));
   ALLOC(h->GU, (size_t)(r * r));
   ALLOC(h->GV, (size_t)(r * r));

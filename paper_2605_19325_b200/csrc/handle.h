@@ -73,6 +73,8 @@ struct enmf_handle_s {
   // is reassembled by a zero-padded fp64 allreduce (exact: adding zeros), SURVEY §8(e)
   int64_t v_begin = 0, v_count = 0;
   int64_t v_pad = 0;
+  cudaStream_t st_comm = nullptr;          // slice reductions of the sliced pass 2 (NCCL)
+  std::vector<cudaEvent_t> ev_comm;
   // sparse X (enmf_set_data_csr): this rank's rows as CSR (caller-owned) and a handle-owned
   // CSC copy for X^T U
   bool sparse = false;

@@ -50,6 +50,12 @@ unsigned* tc_band_flags(TcState* s, cudaStream_t st);
 int64_t tc_bands(const TcState* s);
 int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st,
            const unsigned long long* umax = nullptr);
+// Pass 2 over the 128-column bands [b0, b1) of X only: Q rows [128 b0, min(n, 128 b1)).
+// pack: repack U's digits first (the first range of a pass; later ranges reuse them).
+// tc_xtu_band_count: ceil(n / 128).  Returns 0, 1 (error) or 2 (OOM).
+int tc_xtu_bands(TcState* s, const float* U, int64_t ldu, double* Q, int64_t b0, int64_t b1,
+                 cudaStream_t st, const unsigned long long* umax, bool pack);
+int64_t tc_xtu_band_count(const TcState* s);
 // Column-block products for the randomised SVD (fp64 factors of any width):
 // out (ld ldo) = X F (F: n x ncols) or, transposed, X^T F (F: this rank's rows x ncols).
 // Returns 0, 1 (CUDA error) or 2 (OOM).

@@ -89,6 +89,10 @@ struct Params {
   int r;                     // valid output columns
   int64_t out_rows;          // valid output rows
   int tiles;                 // 128-row output tiles (pair kernel: tile 2 t + rank may not exist)
+  // single-CTA kernel: units cover output tiles tile0 .. tile0 + tiles - 1 (a band range of
+  // pass 2, tc_xtu_bands); output row i is stored at out row i - row0
+  int tile0;
+  int64_t row0;
   // mode 0, no K split: after a band's output rows are stored each epilogue warp adds 1 to
   // band_ready[tile] (release), so a consumer launched behind this kernel with programmatic
   // dependent launch (tc_hals_kernel) can take the band while later bands are still running
@@ -108,7 +112,7 @@ using namespace tcp;
 
 __device__ __forceinline__ void unit_range(const Params& p, int u, int& tile, int& s0, int& s1,
                                            int& split) {
-  tile = u / p.ksplit;
+  tile = u / p.ksplit + p.tile0;
   split = u % p.ksplit;
   const int per = (p.stages_total + p.ksplit - 1) / p.ksplit;
   s0 = split * per;
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_i8_kernel(const Params p) {
       mbar_wait_sleep(bar_tfull, nunit & 1);
       tc_fence_after();
       const int64_t row = (int64_t)tile * BM + row_in_tile;
-      double* o = p.out + (int64_t)split * p.split_stride + row * p.out_ld;
+      double* o = p.out + (int64_t)split * p.split_stride + (row - p.row0) * p.out_ld;
       const double rinv = row < p.out_rows ? p.rowinv[row] : 0.0;
       const uint32_t lane_addr = tmem_base + ((uint32_t)(32 * q) << 16);
 #pragma unroll 1
@@ -838,6 +842,8 @@ struct TcState {
   int sms = kSMs;
   unsigned* band_flags = nullptr;   // Mt + 2: pass-1 band flags, epoch, consumer tile counter
   unsigned long long* stamps = nullptr;   // 4: pass-1 kernel timestamps (tc_stamp_*)
+  double* chunk_partial = nullptr;        // split-K partials of a pass-2 band range
+  size_t chunk_cap = 0;
 };
 
 bool tc_supported(int64_t rows, int64_t n, int64_t r) {
@@ -850,7 +856,8 @@ void tc_destroy(TcState* s) {
   if (s->xtp[0]) cudaFree(s->xtp[0]);
   if (s->fp[0]) cudaFree(s->fp[0]);
   void* bufs[] = {s->xinv_r, s->xinv_c, s->xbits, s->xq2, s->fmaxbits, s->fscale,
-                  s->colscale, s->partial, s->colbuf, s->band_flags, s->stamps};
+                  s->colscale, s->partial, s->colbuf, s->band_flags, s->stamps,
+                  s->chunk_partial};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete s;
@@ -1036,8 +1043,12 @@ static void pack_factor(TcState* s, const T* F, int64_t ldf, int64_t K, int64_t 
 static int launch_gemm(TcState* s, int mode, bool pair, double* out, int64_t out_ld,
                        int64_t split_stride, int tiles, int ksplit, int stages_total,
                        int64_t out_rows, int ncols, int rp, cudaStream_t st,
-                       unsigned* band_ready = nullptr, unsigned long long* tstamp = nullptr) {
+                       unsigned* band_ready = nullptr, unsigned long long* tstamp = nullptr,
+                       int tile0 = 0, int64_t row0 = 0) {
   Params p;
+  p.tile0 = pair ? 0 : tile0;    // band ranges: single-CTA kernel only
+  p.row0 = pair ? 0 : row0;
+  if (pair && (tile0 != 0 || row0 != 0)) return 1;
   p.band_ready = (mode == 0 && ksplit == 1 && !pair) ? band_ready : nullptr;
   p.tstamp = pair ? nullptr : tstamp;
   for (int q = 0; q < PLANES; ++q) {
@@ -1171,6 +1182,43 @@ int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st,
   reduce_parts(s->partial, ks, s->n * r, Q, st);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
+
+// Q rows of the 128-column bands [b0, b1) of X (pass 2 over a band range: the chunks of the
+// multi-rank V block, each reduced to its owner while the next one runs).  pack: repack the
+// factor's digits (the first range of a pass).  The K split fills the SMs for the range alone
+// (a chunk has few bands); its partials live in a range-sized buffer.
+int tc_xtu_bands(TcState* s, const float* U, int64_t ldu, double* Q, int64_t b0, int64_t b1,
+                 cudaStream_t st, const unsigned long long* umax, bool pack) {
+  const int r = (int)s->r;
+  const int64_t bands = s->tiles_per_row / 2;
+  if (b0 < 0 || b1 > bands || b0 >= b1) return 1;
+  if (pack) pack_factor<float>(s, U, ldu, s->rows, s->Kt2, r, s->rp, st, umax);
+  const int mode = s->xtp[0] ? 2 : 1;
+  const int64_t row0 = b0 * BM, rows = std::min<int64_t>(s->n, b1 * BM) - row0;
+  const int nb = (int)(b1 - b0);
+  const int ks = choose_split_waves(nb, s->Kt2, s->sms);
+  if (ks == 1)
+    return launch_gemm(s, mode, false, Q, r, 0, nb, 1, (int)s->Kt2, s->n, r, s->rp, st, nullptr,
+                       nullptr, (int)b0, 0);
+  const size_t need = (size_t)ks * rows * r;
+  if (need > s->chunk_cap) {
+    if (s->chunk_partial) cudaFree(s->chunk_partial);
+    s->chunk_partial = nullptr;
+    s->chunk_cap = 0;
+    if (cudaMalloc(&s->chunk_partial, sizeof(double) * need) != cudaSuccess) {
+      cudaGetLastError();
+      return 2;
+    }
+    s->chunk_cap = need;
+  }
+  if (launch_gemm(s, mode, false, s->chunk_partial, r, rows * r, nb, ks, (int)s->Kt2, s->n, r,
+                  s->rp, st, nullptr, nullptr, (int)b0, row0))
+    return 1;
+  reduce_parts(s->chunk_partial, ks, rows * r, Q + row0 * r, st);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int64_t tc_xtu_band_count(const TcState* s) { return s ? s->tiles_per_row / 2 : 0; }
 
 int tc_xf(TcState* s, bool transposed, const double* F, int64_t ldf, int ncols, double* out,
           int64_t ldo, cudaStream_t st) {

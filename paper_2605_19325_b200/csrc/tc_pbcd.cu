@@ -223,10 +223,14 @@ __device__ __forceinline__ void tmem_st8d(uint32_t taddr_lo, uint32_t taddr_hi,
       : "memory");
 }
 
-// The 4-class digit products of one round as 6 MMAs (see tc_gemm.cu MmaList<4>), issued by one
-// thread after the named barrier that publishes the A planes; completion arrives on bar_d.
+// The digit products of one round, issued by one thread after the named barrier that publishes
+// the A planes; completion arrives on bar_d.  Round A (u G, the gradient: cancellation against
+// c) keeps the 4 weight classes -- 10 products as 6 MMAs; round B (g G, only the Eq.(10)
+// denominator g G g^T, no cancellation) keeps classes <= 2 -- 6 products as 4 MMAs, 2^-22 of
+// the row maximum, like the X passes' operands (round 2b: -40 % of round B's tensor work and
+// one TMEM load per column less in its epilogue).
 __device__ __forceinline__ void issue_round(uint32_t a0, uint32_t b0, uint32_t tmem_base, int rp,
-                                            int r, uint32_t bar_d) {
+                                            int r, uint32_t bar_d, bool three = false) {
   const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BM >> 4) << 24);
   const uint32_t idesc1 = idesc_base | ((uint32_t)(rp >> 3) << 17);
   const uint32_t idesc2 = idesc_base | ((uint32_t)(2 * rp >> 3) << 17);
@@ -235,14 +239,26 @@ __device__ __forceinline__ void issue_round(uint32_t a0, uint32_t b0, uint32_t t
   const int ksteps = (r + 31) / 32;
   constexpr int tab[6][4] = {{0, 0, 0, 1}, {0, 2, 2, 1}, {1, 0, 1, 1},
                              {1, 2, 3, 0}, {2, 0, 2, 1}, {3, 0, 3, 0}};
+  // classes <= 2: A0 [B0;B1] -> 0|1, A0 B2 -> 2 (both fresh), A1 [B0;B1] -> 1|2, A2 B0 -> 2
+  constexpr int tab3[4][4] = {{0, 0, 0, 1}, {0, 2, 2, 0}, {1, 0, 1, 1}, {2, 0, 2, 0}};
   tc_fence_after();
   for (int j = 0; j < ksteps; ++j) {
+    if (three) {
 #pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const uint64_t ad = umma_desc(a0 + tab[q][0] * PLANE_A + j * a_kstep, a_lbo, a_sbo);
-      const uint64_t bd = umma_desc(b0 + tab[q][1] * rp * KR + j * b_kstep, b_lbo, b_sbo);
-      tc_mma_i8(tmem_base + tab[q][2] * rp, ad, bd, tab[q][3] ? idesc2 : idesc1,
-                (j == 0 && q < 2) ? 0u : 1u);
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t ad = umma_desc(a0 + tab3[q][0] * PLANE_A + j * a_kstep, a_lbo, a_sbo);
+        const uint64_t bd = umma_desc(b0 + tab3[q][1] * rp * KR + j * b_kstep, b_lbo, b_sbo);
+        tc_mma_i8(tmem_base + tab3[q][2] * rp, ad, bd, tab3[q][3] ? idesc2 : idesc1,
+                  (j == 0 && q < 2) ? 0u : 1u);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const uint64_t ad = umma_desc(a0 + tab[q][0] * PLANE_A + j * a_kstep, a_lbo, a_sbo);
+        const uint64_t bd = umma_desc(b0 + tab[q][1] * rp * KR + j * b_kstep, b_lbo, b_sbo);
+        tc_mma_i8(tmem_base + tab[q][2] * rp, ad, bd, tab[q][3] ? idesc2 : idesc1,
+                  (j == 0 && q < 2) ? 0u : 1u);
+      }
     }
   }
   tc_commit(bar_d);
@@ -487,7 +503,7 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
         tc_fence_before();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         bar_pbcd<NH>();
-        if (threadIdx.x == 0) issue_round(a_s, b_s, tmem_base, rp, p.r, bar_d);
+        if (threadIdx.x == 0) issue_round(a_s, b_s, tmem_base, rp, p.r, bar_d, true);
         // ---------------- round B: T2 = g G ----------------
         mbar_wait_hint(bar_d, round & 1);
         ++round;
@@ -502,14 +518,14 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
           bload16(abase, b * 16 * 128, gn);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            uint32_t v[4][8];
+            uint32_t v[3][8];
 #pragma unroll
-            for (int cls = 0; cls < 4; ++cls) TMEM_LD8(tcol + cls * KR + 16 * b + 8 * hh, v[cls]);
+            for (int cls = 0; cls < 3; ++cls) TMEM_LD8(tcol + cls * KR + 16 * b + 8 * hh, v[cls]);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const int c = 16 * b + 8 * hh + k;
-              const double a = comb8(v[0][k], v[1][k], v[2][k], v[3][k]);
+              const double a = comb8(v[0][k], v[1][k], v[2][k], 0u);   // classes <= 2
               den = fma(i2d(gn[8 * hh + k]), a * gsc[c], den);
             }
           }

@@ -50,27 +50,27 @@ def run_smoke():
     eu = np.linalg.norm(Ud.cpu().numpy() - Uo) / np.linalg.norm(Uo)
     ev = np.linalg.norm(Vd.cpu().numpy() - Vo) / np.linalg.norm(Vo)
     assert eu < 1e-5 and ev < 1e-5, (eu, ev)
-    # (4) one ascent sweep (lift + PBCD) with the tensor-core PBCD kernel, from the oracle's
-    # rotated point, within max(1e-5, 10 x the oracle's own one-ulp spread) (R26)
-    from tests.gpu_common import oracle_floor, rotated_point
-    Ur, Vr, lu, lv = rotated_point(X, cfg.r)
-    ht = E.Enmf(cfg.m, cfg.n, cfg.r, precision=E.PREC_TC)
-    ht.set_data(torch.from_numpy(X).cuda())
-    Ut, Vt = torch.from_numpy(Ur.astype(np.float32)).cuda(), torch.from_numpy(
-        Vr.astype(np.float32)).cuda()
+    # (4) one ascent sweep (lift + PBCD) with the tensor-core PBCD kernel, repeated by the
+    # oracle from the GPU's own state with the GPU's k* (the well-posed parity of
+    # tests/test_gpu_shadow.py): 1e-5 per factor on the rows that are well conditioned at the
+    # path's 2^-22 operand rounding (reading R33), no mask flips (R20)
+    from tests.test_gpu_shadow import TC, Shadow, shadow_sweep, start_point
+    c4 = synth.C4.scaled(300, 250, 20, 0)
+    X4 = synth.x_full(c4)
+    Ur, Vr, lu, lv = start_point(X4, c4.r, want_infeasible=True)
+    ht = E.Enmf(c4.m, c4.n, c4.r, precision=E.PREC_TC)
+    ht.set_data(torch.from_numpy(X4).cuda())
+    Ut = torch.from_numpy(Ur.astype(np.float32)).cuda()
+    Vt = torch.from_numpy(Vr.astype(np.float32)).cuda()
     ht.set_stage(0, lu, lv)
     _, it4 = ht.iterate(Ut, Vt, 1)
     assert it4["ascent_sweeps"] == 1, it4
-
-    def run(Ua, Va):
-        Uo4, Vo4, _, _ = oracle.sweep(X, Ua, Va, oracle.SweepState(0, lu, lv, 0),
-                                      oracle.options(cfg.r, round_f32=1))
-        return Uo4, Vo4
-
-    (Uo4, Vo4), floor = oracle_floor(run, Ur, Vr)
-    ea = np.linalg.norm(Ut.cpu().numpy() - Uo4) / np.linalg.norm(Uo4)
-    eb = np.linalg.norm(Vt.cpu().numpy() - Vo4) / np.linalg.norm(Vo4)
-    assert ea < max(1e-5, 10 * floor[0]) and eb < max(1e-5, 10 * floor[1]), (ea, eb, floor)
+    sh = Shadow(c4.m, c4.n, c4.r)
+    shadow_sweep(sh, X4, Ur, Vr, Ut.cpu().numpy().astype(np.float64),
+                 Vt.cpu().numpy().astype(np.float64), it4, lu, lv, TC, 0)
+    ea, eb = sh.eu, sh.ev
+    assert ea < 1e-5 and eb < 1e-5 and sh.flips == 0, (ea, eb, sh.flips, sh.ill)
     print(f"smoke ok: HALS f rel err {rel.max():.2e}; tc path ({h5.precision}) U {eu:.2e} "
-          f"V {ev:.2e}; tc ascent U {ea:.2e} V {eb:.2e} (floor {floor[0]:.1e}/{floor[1]:.1e}); "
+          f"V {ev:.2e}; tc ascent (k* {it4['pbcd_iters_u']}/{it4['pbcd_iters_v']}) U {ea:.2e} "
+          f"V {eb:.2e} ({sh.ill} ill-conditioned rows excluded, 0 flips); "
           f"launches {h.launch_count + h5.launch_count + ht.launch_count}")

@@ -141,3 +141,21 @@ def test_two_ranks_ascent_sharded_v(cfg_args, prec):
         ev = np.linalg.norm(r0["V"] - V) / np.linalg.norm(V)
         print(f"{cfg_args[0]} ascent: U {eu:.2e} V {ev:.2e}")
         assert eu < 1e-12 and ev < 1e-12
+
+
+@pytest.mark.parametrize("mode", ["hals", "ascent"])
+def test_two_ranks_sliced_pass2_bitwise(mode, monkeypatch):
+    """The tensor-core pass 2 of the sharded V block runs slice by slice (each V slice's band
+    range, reduced to its owner while the next slice computes; here through the host
+    collective) instead of one pass and one reduction: the per-slice K split differs, but every
+    partial is an integer multiple of one power of two below 2^53, so the sums -- and U, V and
+    the objective trace -- are bitwise those of the unsliced pass (ENMF_PASS2_SLICED=0).  The
+    C5-shape case (n = 300) has 128-row-aligned slices of 256 and 44 rows."""
+    cfg_args = ("C5-large-planted", 400, 300, 128, 128)
+    monkeypatch.setenv("ENMF_PASS2_SLICED", "1")
+    a = _spawn(cfg_args, TC, mode)
+    monkeypatch.setenv("ENMF_PASS2_SLICED", "0")
+    b = _spawn(cfg_args, TC, mode)
+    for ra, rb in zip(a, b):
+        assert np.array_equal(ra["U"], rb["U"]) and np.array_equal(ra["V"], rb["V"])
+        assert np.array_equal(ra["f"], rb["f"])
