@@ -124,9 +124,10 @@ void pbcd_commit(float* F, int64_t ldf, int64_t rows, int r, const float* snaps,
 void pbcd_select_stage(const double* pgsum, int it0, int it1, int src, int dst, int max_iter,
                        double eps, int* kstar, int* done, int* ctl, const int* stage,
                        cudaStream_t st);
+// (ctl == nullptr: ust0; want_stage 1: the tensor-core projected-gradient step, R29)
 void pbcd_commit_state(float* F, int64_t ldf, int64_t rows, int r, const double* ust0,
                        const double* ust1, const int* ctl, const int* stage, double* minparts,
-                       cudaStream_t st, unsigned long long* colmax);
+                       cudaStream_t st, unsigned long long* colmax, int want_stage = 0);
 // eNMC PBCD of one block (App. C; kernels_rows.cu nmc_pbcd_kernel): F (rows x r, ld) with the
 // other factor O (ld ldo) fixed, the block's observed entries as CSR lists (ptr rows + 1,
 // idx, val); lift, mask, all max_iter inner iterations with snapshots and per-iteration

@@ -471,16 +471,17 @@ __global__ void pbcd_commit_state_kernel(float* __restrict__ F, int64_t ldf, int
                                          int r, const double* __restrict__ ust0,
                                          const double* __restrict__ ust1,
                                          const int* __restrict__ ctl, const int* stage,
-                                         double* minparts, unsigned long long* colmax) {
+                                         double* minparts, unsigned long long* colmax,
+                                         int want_stage) {
   __shared__ float t[128][33];
   __shared__ double red[256];
   __shared__ unsigned long long cm[128];
   for (int c = threadIdx.x; c < 128; c += blockDim.x) cm[c] = 0ull;
   __syncthreads();
-  const bool active = stage == nullptr || *stage == 0;
+  const bool active = stage == nullptr || *stage == want_stage;
   double mn = DBL_MAX;
   if (active) {
-    const double* src = ctl[3] ? ust1 : ust0;
+    const double* src = (ctl != nullptr && ctl[3]) ? ust1 : ust0;   // no ctl: ust0
     const int64_t tiles = (rows + 127) / 128;
     const int chunks = (r + 31) / 32;
     for (int64_t unit = blockIdx.x; unit < tiles * chunks; unit += gridDim.x) {
@@ -839,9 +840,9 @@ void pbcd_select_stage(const double* pgsum, int it0, int it1, int src, int dst, 
 
 void pbcd_commit_state(float* F, int64_t ldf, int64_t rows, int r, const double* ust0,
                        const double* ust1, const int* ctl, const int* stage, double* minparts,
-                       cudaStream_t st, unsigned long long* colmax) {
+                       cudaStream_t st, unsigned long long* colmax, int want_stage) {
   pbcd_commit_state_kernel<<<kRowGrid, 256, 0, st>>>(F, ldf, rows, r, ust0, ust1, ctl, stage,
-                                                     minparts, colmax);
+                                                     minparts, colmax, want_stage);
   count_launch();
 }
 

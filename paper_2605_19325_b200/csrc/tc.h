@@ -56,6 +56,10 @@ int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st,
 int tc_xtu_bands(TcState* s, const float* U, int64_t ldu, double* Q, int64_t b0, int64_t b1,
                  cudaStream_t st, const unsigned long long* umax, bool pack);
 int64_t tc_xtu_band_count(const TcState* s);
+// G (r x r fp64) = U~^T U~ of the digits the last tc_xtu / tc_xtu_bands packed (the Gram of
+// the quantised U, scales tc_factor_scales), exact on the tensor cores up to the final
+// rounding to fp64.  Returns 0, 1 (error) or 2 (unsupported size: use the SIMT Gram).
+int tc_gram_quantised(TcState* s, double* G, cudaStream_t st);
 // Column-block products for the randomised SVD (fp64 factors of any width):
 // out (ld ldo) = X F (F: n x ncols) or, transposed, X^T F (F: this rank's rows x ncols).
 // Returns 0, 1 (CUDA error) or 2 (OOM).
@@ -75,13 +79,17 @@ int tc_xf(TcState* s, bool transposed, const double* F, int64_t ldf, int ncols, 
 // Returns 0, or 1 on a launch / configuration error.
 bool tc_pbcd_supported(int r);
 int tc_pbcd_parts();
+// fstep (optional, device): the ablation's fixed step 1 / lambda_max(G) instead of Eq.(10)
+// (round B skipped); want_stage = 1 with fstep and [0, 1): one projected-gradient step of the
+// descent stage (runs only if *stage == 1; commit with pbcd_commit_state(..., want_stage 1)).
 void tc_pbcd_prepare(const double* G, int r, int8_t* gd_work, double* gscale_work,
-                     const int* stage, cudaStream_t st);
+                     const int* stage, cudaStream_t st, int want_stage = 0);
 int tc_pbcd_chunk(const float* F, int64_t ldf, int64_t rows, int r, const double* C,
                   const double* lam, int max_iter, int it0, int it1, int src, int dst,
                   double* ust0, double* ust1, double* pgparts, const int8_t* gd_work,
                   const double* gscale_work, const int* stage, const int* done,
-                  const int* kprev, const int* rctl, const int* kst, cudaStream_t st);
+                  const int* kprev, const int* rctl, const int* kst, cudaStream_t st,
+                  const double* fstep = nullptr, int want_stage = 0);
 // HALS sweep of the rows with t = C - u G from exact int8-digit tcgen05
 // rounds, 32-column Gauss-Seidel blocks in registers (tc_pbcd.cu).  Runs only if *stage == 1.
 // Writes minparts[0, nparts) (nparts >= tc_hals_parts()); colmax (u64[r]) as hals_rows;

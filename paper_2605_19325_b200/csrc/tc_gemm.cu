@@ -844,6 +844,7 @@ struct TcState {
   unsigned long long* stamps = nullptr;   // 4: pass-1 kernel timestamps (tc_stamp_*)
   double* chunk_partial = nullptr;        // split-K partials of a pass-2 band range
   size_t chunk_cap = 0;
+  unsigned long long* gram64 = nullptr;   // 128 x 128 int64: the exact quantised Gram
 };
 
 bool tc_supported(int64_t rows, int64_t n, int64_t r) {
@@ -857,7 +858,7 @@ void tc_destroy(TcState* s) {
   if (s->fp[0]) cudaFree(s->fp[0]);
   void* bufs[] = {s->xinv_r, s->xinv_c, s->xbits, s->xq2, s->fmaxbits, s->fscale,
                   s->colscale, s->partial, s->colbuf, s->band_flags, s->stamps,
-                  s->chunk_partial};
+                  s->chunk_partial, s->gram64};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete s;
@@ -1180,6 +1181,181 @@ int tc_xtu(TcState* s, const float* U, int64_t ldu, double* Q, cudaStream_t st,
                   (int)s->Kt2, s->n, r, s->rp, st))
     return 1;
   reduce_parts(s->partial, ks, s->n * r, Q, st);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+// ------------------------------------------------------------------ quantised Gram
+// G = U~^T U~ of the factor digits the last pass packed (the Gram the trace-form objective
+// and the V update use, tc_factor_scales), EXACTLY, on the tensor cores.  A packed K-stage
+// (64 factor rows x rp columns, 3 digit planes, K-major, core matrix (g, kc) at
+// (4 g + kc) 128 B) serves as both operands: A = U~^T (M = rp rows of the Gram) and B = U~
+// (N = rp), so every digit product d_i(u_k) d_j(u_l) of the stage is one kind::i8 MMA.  The
+// digit weights 2^15, 2^7, 1 (mixed radix 8/8/7) give six product weights; TMEM holds four
+// 128-column accumulators, so PHASE 0 accumulates 2^30 | 2^22 | 2^14 | 2^15 (products 00 |
+// 01+10 | 11 | 02+20, the X passes' MMA list) and PHASE 1 2^7 | 1 (12+21 | 22).  Each CTA
+// takes a contiguous K range (<= 65536 rows: |class| < 2^31), combines its classes into one
+// int64 per entry (< 2^62) and adds it to the global int64 Gram with atomics (exact, order
+// independent); gram_finish_kernel scales by 2^-30 / (s_k s_l).  Replaces gram_sym's fp64
+// SIMT accumulation of the quantised factor (0.36 ms at C5, ~0.03 ms here).
+constexpr int GRAM_STAGE = PLANES * 128 * BK;      // 24 KB at rp = 128
+
+template <int PHASE>
+__global__ void __launch_bounds__(128, 1)
+tc_gram_kernel(const int8_t* __restrict__ planes, int64_t Kt, int rp, int per,
+               unsigned long long* __restrict__ G64) {
+  extern __shared__ __align__(1024) uint8_t gsm_raw[];
+  uint8_t* gsm = (uint8_t*)(((uintptr_t)gsm_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t bars[5];
+  __shared__ uint32_t tmem_base_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ks0 = (int64_t)blockIdx.x * per, ks1 = ks0 + per < Kt ? ks0 + per : Kt;
+  const uint32_t bar_full[2] = {smem_u32(&bars[0]), smem_u32(&bars[1])};
+  const uint32_t bar_mma[2] = {smem_u32(&bars[2]), smem_u32(&bars[3])};
+  const uint32_t bar_done = smem_u32(&bars[4]);
+  const uint32_t stage_bytes = (uint32_t)PLANES * rp * BK;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 5; ++b) mbar_init(smem_u32(&bars[b]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+  const uint32_t lane_addr = tmem_base + ((uint32_t)(32 * warp) << 16);
+  if (PHASE == 0) {   // accumulator 2 is only ever accumulated into (wide A1 [B0;B1])
+#pragma unroll 1
+    for (int c0 = 0; c0 < rp; c0 += 16) TMEM_ST16_ZERO(lane_addr + 2 * rp + c0);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0 && ks1 > ks0) {
+    const uint32_t base = smem_u32(gsm);
+    const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BM >> 4) << 24);
+    const uint32_t idesc1 = idesc_base | ((uint32_t)(rp >> 3) << 17);
+    const uint32_t idesc2 = idesc_base | ((uint32_t)(2 * rp >> 3) << 17);
+    const uint32_t plane = (uint32_t)rp * BK;
+    auto load = [&](int64_t ks, int slot) {
+      mbar_expect_tx(bar_full[slot], stage_bytes);
+      bulk_g2s(base + slot * GRAM_STAGE, planes + ks * stage_bytes, stage_bytes, bar_full[slot]);
+    };
+    load(ks0, 0);
+    for (int64_t ks = ks0; ks < ks1; ++ks) {
+      const int i = (int)(ks - ks0), slot = i & 1;
+      if (ks + 1 < ks1) {
+        if (i >= 1) mbar_wait(bar_mma[slot ^ 1], ((i - 1) >> 1) & 1);   // slot free again
+        load(ks + 1, slot ^ 1);
+      }
+      mbar_wait(bar_full[slot], (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t st = base + slot * GRAM_STAGE;
+#pragma unroll
+      for (int j = 0; j < BK / 32; ++j) {
+        const bool first = ks == ks0 && j == 0;
+        auto mma = [&](int pa, int pb, int acc, bool wide, bool fresh) {
+          const uint64_t ad = umma_desc(st + pa * plane + j * 256, 128, 512);
+          const uint64_t bd = umma_desc(st + pb * plane + j * 256, 128, 512);
+          tc_mma_i8(tmem_base + acc * rp, ad, bd, wide ? idesc2 : idesc1, fresh ? 0u : 1u);
+        };
+        if (PHASE == 0) {
+          mma(0, 0, 0, true, first);    // 00 -> acc0, 01 -> acc1
+          mma(0, 2, 3, false, first);   // 02 -> acc3
+          mma(2, 0, 3, false, false);   // 20 -> acc3
+          mma(1, 0, 1, true, false);    // 10 -> acc1, 11 -> acc2 (zeroed above)
+        } else {
+          mma(1, 2, 0, false, first);   // 12 -> acc0
+          mma(2, 1, 0, false, false);   // 21 -> acc0
+          mma(2, 2, 1, false, first);   // 22 -> acc1
+        }
+      }
+      tc_commit(bar_mma[slot]);
+    }
+    tc_commit(bar_done);
+  }
+  __syncwarp();
+  if (ks1 > ks0) {
+    mbar_wait_sleep(bar_done, 0);
+    tc_fence_after();
+    const int k = 32 * warp + lane;            // Gram row (TMEM lane)
+#pragma unroll 1
+    for (int c0 = 0; c0 < rp; c0 += 16) {
+      uint32_t v[4][16];
+      TMEM_LD16(lane_addr + 0 * rp + c0, v[0]);
+      TMEM_LD16(lane_addr + 1 * rp + c0, v[1]);
+      if (PHASE == 0) {
+        TMEM_LD16(lane_addr + 2 * rp + c0, v[2]);
+        TMEM_LD16(lane_addr + 3 * rp + c0, v[3]);
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (k < rp) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          long long val;
+          if (PHASE == 0)
+            val = ((long long)(int)v[0][i] << 30) + ((long long)(int)v[1][i] << 22) +
+                  ((long long)(int)v[2][i] << 14) + ((long long)(int)v[3][i] << 15);
+          else
+            val = ((long long)(int)v[0][i] << 7) + (long long)(int)v[1][i];
+          if (val != 0)
+            atomicAdd(&G64[(int64_t)k * rp + c0 + i], (unsigned long long)val);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+// G (r x r fp64) = G64 2^-30 / (s_k s_l): colscale holds 1 / s of the factor's columns
+__global__ void gram_finish_kernel(const unsigned long long* __restrict__ G64, int r, int rp,
+                                   const double* __restrict__ colscale, double* __restrict__ G) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < r * r; e += gridDim.x * blockDim.x) {
+    const int k = e / r, l = e % r;
+    G[e] = (double)(long long)G64[(int64_t)k * rp + l] * 0x1p-30 * colscale[k] * colscale[l];
+  }
+}
+
+int tc_gram_quantised(TcState* s, double* G, cudaStream_t st) {
+  const int rp = s->rp, r = (int)s->r;
+  if (rp != 128 && rp % 16 != 0) return 1;
+  const int64_t Kt = s->Kt2;
+  // <= 1024 stages (65536 rows) per CTA keeps every class below 2^31; the int64 total below
+  // 2^63 needs rows < 2^63 / (126 2^15)^2, i.e. m < 5.2e5 per rank (else: SIMT path)
+  int grid = (int)std::min<int64_t>(Kt, s->sms);
+  int per = (int)((Kt + grid - 1) / grid);
+  if (per > 1024 || s->rows > 500000) return 2;
+  grid = (int)((Kt + per - 1) / per);
+  if (!s->gram64) {
+    if (cudaMalloc(&s->gram64, sizeof(unsigned long long) * 128 * 128) != cudaSuccess) {
+      cudaGetLastError();
+      return 1;
+    }
+  }
+  static bool attr = false;
+  const int smem = 2 * GRAM_STAGE + 1024;
+  if (!attr) {
+    cudaFuncSetAttribute(tc_gram_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(tc_gram_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  if (cudaMemsetAsync(s->gram64, 0, sizeof(unsigned long long) * 128 * 128, st) != cudaSuccess)
+    return 1;
+  const int8_t* planes = fplane(s, 0, rp);
+  tc_gram_kernel<0><<<grid, 128, smem, st>>>(planes, Kt, rp, per, s->gram64);
+  tc_gram_kernel<1><<<grid, 128, smem, st>>>(planes, Kt, rp, per, s->gram64);
+  gram_finish_kernel<<<(r * r + 255) / 256, 256, 0, st>>>(s->gram64, r, rp, s->colscale, G);
+  count_launch(3);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

@@ -68,6 +68,12 @@ struct Params {
   const int* kprev;
   const int* rctl;
   const int* kst;
+  // ablation variants (R29): fstep (device, optional) -- the fixed step 1 / lambda_max(G)
+  // replaces Eq.(10)'s d_i (round B, the denominator, is skipped); want_stage 1 with fstep
+  // and [0, 1) is one projected-gradient step of the descent stage (no stopping rule, no
+  // final gradient).  want_stage 0: the ascent stage (Alg. 2).
+  const double* fstep;
+  int want_stage;
 };
 
 __device__ __forceinline__ double pow2s(double mx) {
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
   __shared__ double xch2[NH][BM];
   __shared__ double wsum[NWARP];
   __shared__ double gsc_s[128];
-  if (p.stage != nullptr && *p.stage != 0) return;
+  if (p.stage != nullptr && *p.stage != p.want_stage) return;
   int it0 = p.it0, it1 = p.it1, src = p.src, dst = p.dst;
   if (p.rctl != nullptr) {                   // replay of the stage in which the rule fired
     if (p.rctl[0] == 0) return;
@@ -346,6 +352,7 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
     // my TMEM lane quadrant and columns; class k of the accumulators at column k * KR
     const uint32_t tcol = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
     const double lam = *p.lam;
+    const double fstep = p.fstep != nullptr ? *p.fstep : 0.0;
     const int g8 = rt >> 3, ri = rt & 7;
     // my 16-byte digit chunks in the A planes: chunk b of my part at abase + b * 16 * 128
     uint8_t* const abase = Ad + ((c0 >> 4) * 16 + g8) * 128 + ri * 16;
@@ -397,6 +404,15 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
       }
       const int32_t* cqrow = Cq + rt * CQ_LD + c0;
       for (int it = it0; it <= it1; ++it) {
+        if (it == it1 && p.want_stage == 1) {   // projected-gradient step: u_1 is the result
+          if (rok) {
+            const int ncol = p.r - c0 < CW ? p.r - c0 : CW;
+#pragma unroll
+            for (int c = 0; c < CW; ++c)
+              if (c < ncol) ust_out[sto + (int64_t)c * BM] = u[c];
+          }
+          break;
+        }
         // ---------------- round A: T1 = u G ----------------
         int mh = 0;
 #pragma unroll
@@ -473,6 +489,28 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
           }
           bar_pbcd<NH>();
           break;
+        }
+        if (fstep > 0.0) {
+          // fixed step (R29): u <- max(0, u - step M o grad) from the TMEM words of pass 1
+          // (unrolled: u must stay in registers)
+          opaque(mlo, mhi);
+#pragma unroll
+          for (int b = 0; b < CW / 8; ++b) {
+            uint32_t lo[8], hi[8];
+            TMEM_LD8(tcol + 8 * b, lo);
+            TMEM_LD8(tcol + KR + 8 * b, hi);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const uint32_t mb = ((b < 4 ? mlo : mhi) >> (8 * (b & 3))) & 255u;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int c = 8 * b + k;
+              const double un = fmax(0.0, u[c] - fstep * __hiloint2double((int)hi[k], (int)lo[k]));
+              u[c] = ((mb >> k) & 1u) ? un : u[c];
+            }
+          }
+          tc_fence_before();
+          bar_pbcd<NH>();
+          continue;
         }
         double numr = 0.0;
         int gmx = 0;
@@ -1129,9 +1167,10 @@ bool tc_pbcd_supported(int r) { return r >= 1 && r <= 128; }
 
 // G (r x r) -> the B-operand digits and column scales of tc_pbcd_chunk (ascent stage only).
 void tc_pbcd_prepare(const double* G, int r, int8_t* gd_work, double* gscale_work,
-                     const int* stage, cudaStream_t st) {
+                     const int* stage, cudaStream_t st, int want_stage) {
   using namespace tpb;
-  gdigits_kernel<true><<<KR, KR, 0, st>>>(G, r, KR, gd_work, gscale_work, stage, 0, nullptr);
+  gdigits_kernel<true><<<KR, KR, 0, st>>>(G, r, KR, gd_work, gscale_work, stage, want_stage,
+                                          nullptr);
   count_launch();
 }
 
@@ -1143,9 +1182,12 @@ int tc_pbcd_chunk(const float* F, int64_t ldf, int64_t rows, int r, const double
                   const double* lam, int max_iter, int it0, int it1, int src, int dst,
                   double* ust0, double* ust1, double* pgparts, const int8_t* gd_work,
                   const double* gscale_work, const int* stage, const int* done,
-                  const int* kprev, const int* rctl, const int* kst, cudaStream_t st) {
+                  const int* kprev, const int* rctl, const int* kst, cudaStream_t st,
+                  const double* fstep, int want_stage) {
   using namespace tpb;
   Params p;
+  p.fstep = fstep;
+  p.want_stage = want_stage;
   p.F = F;
   p.ldf = ldf;
   p.rows = rows;
