@@ -37,9 +37,11 @@ def _run(cfg, X, U0, V0, tcgram):
         U, V = to_dev(U0), to_dev(V0)
         f_obj = h.objective(U, V, exact=False)
         h.set_stage(1)
+        l0 = h.launch_count
         f, _ = h.iterate(U, V, 3)
+        launches = h.launch_count - l0
         h.close()
-        return to_np(U), to_np(V), np.array(f), f_obj
+        return to_np(U), to_np(V), np.array(f), f_obj, launches
     finally:
         if old is None:
             del os.environ["ENMF_TC_GRAM"]
@@ -53,12 +55,16 @@ def test_tc_gram_matches_simt_gram_of_quantised_u(cfg):
     g = np.random.default_rng(4)
     U0 = (0.5 + g.random((cfg.m, cfg.r))).astype(np.float32).astype(np.float64)
     V0 = (0.5 + g.random((cfg.n, cfg.r))).astype(np.float32).astype(np.float64)
-    Ua, Va, fa, oa = _run(cfg, X, U0, V0, "1")
-    Ub, Vb, fb, ob = _run(cfg, X, U0, V0, "0")
+    Ua, Va, fa, oa, la = _run(cfg, X, U0, V0, "1")
+    Ub, Vb, fb, ob, lb = _run(cfg, X, U0, V0, "0")
+    assert la != lb, "both runs took the same Gram path"
+    # (at these row counts the fp64 SIMT sums of the <= 44-bit digit products stay below 2^53,
+    # so they are exact too and the two agree bitwise; at C5, 2e5 rows, they round)
     eu = np.linalg.norm(Ua - Ub) / np.linalg.norm(Ub)
     ev = np.linalg.norm(Va - Vb) / np.linalg.norm(Vb)
     ef = np.max(np.abs(fa - fb) / fb)
     eo = abs(oa - ob) / ob
-    print(f"{cfg.name}: tc Gram vs SIMT Gram: U {eu:.1e} V {ev:.1e} f {ef:.1e} objective {eo:.1e}")
+    print(f"{cfg.name}: tc Gram vs SIMT Gram: U {eu:.1e} V {ev:.1e} f {ef:.1e} objective {eo:.1e} "
+          f"(launches per 3 sweeps {la} / {lb})")
     assert eo < 1e-13
     assert eu < 1e-8 and ev < 1e-8 and ef < 1e-8
