@@ -83,6 +83,38 @@ __global__ void reduce_parts_kernel(const double* __restrict__ parts, int nparts
   }
 }
 
+// long outputs (the pass-2 split-K partials, n x r): 16-byte loads, 4 independent double2 per
+// thread and iteration so that enough loads are in flight (the scalar loop ran at ~1 TB/s);
+// the same per-element summation order as reduce_parts_kernel (bitwise equal results)
+__global__ void __launch_bounds__(256) reduce_parts_vec_kernel(const double2* __restrict__ parts,
+                                                               int nparts, int64_t len2,
+                                                               double2* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 < len2; e0 += 4 * stride) {
+    double2 s[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = make_double2(0.0, 0.0);
+    for (int p = 0; p < nparts; ++p) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + u * stride;
+        v[u] = e < len2 ? parts[(int64_t)p * len2 + e] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s[u].x += v[u].x;
+        s[u].y += v[u].y;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t e = e0 + u * stride;
+      if (e < len2) out[e] = s[u];
+    }
+  }
+}
+
 // short outputs (len <= 64: scalars, the PBCD stopping vector): one block per element, the
 // parts strided over 256 threads and a fixed-order tree -- deterministic, and no single
 // thread walking hundreds of dependent loads
@@ -202,6 +234,9 @@ void reduce_parts(const double* parts, int nparts, int64_t len, double* out, cud
     reduce_parts_short_kernel<<<(unsigned)len, 256, 0, st>>>(parts, nparts, len, out);
   else if (len < (int64_t)kSMs * 256)   // e.g. the Gram partials (16384 x 296): 64-thread
     reduce_parts_kernel<<<grid_for(len, 64), 64, 0, st>>>(parts, nparts, len, out);   // blocks
+  else if (len % 2 == 0 && ((reinterpret_cast<uintptr_t>(parts) | reinterpret_cast<uintptr_t>(out)) & 15) == 0)
+    reduce_parts_vec_kernel<<<2 * kSMs, 256, 0, st>>>(reinterpret_cast<const double2*>(parts), nparts,
+                                                       len / 2, reinterpret_cast<double2*>(out));
   else
     reduce_parts_kernel<<<grid_for(len), 256, 0, st>>>(parts, nparts, len, out);
   count_launch();
