@@ -155,9 +155,6 @@ __device__ __forceinline__ uint32_t bdig(double t, double s24) {
   return ((uint32_t)rint_lo(t, s24) + 0x00808080u) ^ 0x00808080u;
 }
 __device__ __forceinline__ uint32_t bdig(double t) { return bdig(t, 0x1p24); }
-__device__ __forceinline__ int bdig_n(uint32_t w) {
-  return (int)((w ^ 0x00808080u) - 0x00808080u);
-}
 // 4 x 4 byte transpose (an involution): o[j] byte i = byte j of input i
 __device__ __forceinline__ void bt4(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
                                     uint32_t (&o)[4]) {
@@ -183,21 +180,6 @@ __device__ __forceinline__ void bstore16(const uint32_t (&w)[16], uint8_t* Ad, i
   for (int k = 0; k < 4; ++k)
     *reinterpret_cast<uint4*>(Ad + k * PLANE_A + off) =
         make_uint4(pl[k][0], pl[k][1], pl[k][2], pl[k][3]);
-}
-// the grid integers n of 16 columns back from the A planes (exact)
-__device__ __forceinline__ void bload16(const uint8_t* Ad, int off, int (&n)[16]) {
-  uint4 v[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const uint4*>(Ad + k * PLANE_A + off);
-  const uint32_t pw[4][4] = {{v[0].x, v[0].y, v[0].z, v[0].w}, {v[1].x, v[1].y, v[1].z, v[1].w},
-                             {v[2].x, v[2].y, v[2].z, v[2].w}, {v[3].x, v[3].y, v[3].z, v[3].w}};
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t o[4];
-    bt4(pw[3][q], pw[2][q], pw[1][q], pw[0][q], o);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) n[4 * q + j] = bdig_n(o[j]);
-  }
 }
 // The 4 weight classes of an accumulator column combined exactly: v0 2^24 + v1 2^16 + v2 2^8
 // + v3; callers fold 2^-24 into their scales.  With K <= 128 and |digits| <= 128 a product
@@ -532,12 +514,26 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
             TMEM_LD8(tcol + 16 * b + 8 * h, lo);
             TMEM_LD8(tcol + KR + 16 * b + 8 * h, hi);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            uint32_t nq[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-              wd[8 * h + k] = bdig(__hiloint2double((int)hi[k], (int)lo[k]), sg24);
+            for (int k = 0; k < 8; ++k) {
+              const int n = rint_lo(__hiloint2double((int)hi[k], (int)lo[k]), sg24);
+              nq[k] = (uint32_t)n;
+              wd[8 * h + k] = ((uint32_t)n + 0x00808080u) ^ 0x00808080u;
+            }
+            // the grid integers of g also go to my class-3 TMEM columns, which round B (classes
+            // <= 2) leaves alone: its epilogue and the update read them there instead of
+            // transposing the digit planes back out of shared memory
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                    tcol + 3 * KR + 16 * b + 8 * h),
+                "r"(nq[0]), "r"(nq[1]), "r"(nq[2]), "r"(nq[3]), "r"(nq[4]), "r"(nq[5]),
+                "r"(nq[6]), "r"(nq[7])
+                : "memory");
           }
           bstore16(wd, abase, b * 16 * 128);
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         bar_pbcd<NH>();
@@ -552,19 +548,17 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
         const double isg = 1.0 / sg;
 #pragma unroll 1
         for (int b = 0; b < CW / 16; ++b) {
-          int gn[16];
-          bload16(abase, b * 16 * 128, gn);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            uint32_t v[3][8];
+            uint32_t v[4][8];        // classes 0..2 of T2, and g's grid integers (class 3)
 #pragma unroll
-            for (int cls = 0; cls < 3; ++cls) TMEM_LD8(tcol + cls * KR + 16 * b + 8 * hh, v[cls]);
+            for (int cls = 0; cls < 4; ++cls) TMEM_LD8(tcol + cls * KR + 16 * b + 8 * hh, v[cls]);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const int c = 16 * b + 8 * hh + k;
               const double a = comb8(v[0][k], v[1][k], v[2][k], 0u);   // classes <= 2
-              den = fma(i2d(gn[8 * hh + k]), a * gsc[c], den);
+              den = fma(i2d((int)v[3][k]), a * gsc[c], den);
             }
           }
         }
@@ -581,15 +575,18 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
         const double dsg = dstep * 0x1p-24 * isg;     // step on the grid integers of g
 #pragma unroll
         for (int b = 0; b < CW / 16; ++b) {
-          int gn[16];
-          bload16(abase, b * 16 * 128, gn);
+          uint32_t gn[2][8];
+          TMEM_LD8(tcol + 3 * KR + 16 * b, gn[0]);
+          TMEM_LD8(tcol + 3 * KR + 16 * b + 8, gn[1]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
             const int c = 16 * b + k;
-            const double un = fmax(0.0, u[c] - dsg * i2d(gn[k]));
+            const double un = fmax(0.0, u[c] - dsg * i2d((int)gn[k >> 3][k & 7]));
             u[c] = mbit(mlo, mhi, c) ? un : u[c];     // entries outside M_{U+} stay fixed
           }
         }
+        tc_fence_before();       // TMEM reads done before the next round's MMAs
         bar_pbcd<NH>();          // everyone has read the g digits before they are overwritten
       }
     }

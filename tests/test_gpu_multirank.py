@@ -159,3 +159,19 @@ def test_two_ranks_sliced_pass2_bitwise(mode, monkeypatch):
     for ra, rb in zip(a, b):
         assert np.array_equal(ra["U"], rb["U"]) and np.array_equal(ra["V"], rb["V"])
         assert np.array_equal(ra["f"], rb["f"])
+
+
+def test_three_ranks_sliced_pass2_bitwise(monkeypatch):
+    """Three ranks (host collectives on one GPU): n = 700 gives 128-row-aligned V slices of
+    256, 256 and 188 rows, so the sliced pass 2 has a short last slice and three reductions;
+    U, V and f bitwise equal to the unsliced pass, V and f identical on all ranks."""
+    cfg_args = ("C2-image", 361, 700, 49, 49)
+    monkeypatch.setenv("ENMF_PASS2_SLICED", "1")
+    a = _spawn(cfg_args, TC, "hals", world=3)
+    monkeypatch.setenv("ENMF_PASS2_SLICED", "0")
+    b = _spawn(cfg_args, TC, "hals", world=3)
+    for ra in a[1:]:
+        assert np.array_equal(ra["V"], a[0]["V"]) and np.array_equal(ra["f"], a[0]["f"])
+    for ra, rb in zip(a, b):
+        assert np.array_equal(ra["U"], rb["U"]) and np.array_equal(ra["V"], rb["V"])
+        assert np.array_equal(ra["f"], rb["f"])
