@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
           v = (rok && col < p.r) ? (double)p.F[row * p.ldf + col] : 0.0;
           if (v < 0.0) v += lam;                                   // Eq.(6)/(7) lift
         }
-        u[c] = v;
+        u[c] = v + 0.0;            // -0 -> +0: the update below tells M_{U+} by the sign bit
         if (rok && col < p.r && v >= 0.0) {                        // M_{U+} (R14)
           if (c < 32) mlo |= 1u << c; else mhi |= 1u << (c - 32);
         }
@@ -579,11 +579,14 @@ __global__ void __launch_bounds__(128 * NH, 1) tc_pbcd_kernel(const Params p) {
           TMEM_LD8(tcol + 3 * KR + 16 * b, gn[0]);
           TMEM_LD8(tcol + 3 * KR + 16 * b + 8, gn[1]);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          // Eq.(8) with the projection: entries of M_{U+} are exactly those with a clear sign
+          // bit (>= +0 after the lift, kept there by the projection; the others stay < 0 and
+          // see g = 0, so t = u for them), hence max(0, t) on M_{U+} is "t < 0 <= u -> 0"
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
             const int c = 16 * b + k;
-            const double un = fmax(0.0, u[c] - dsg * i2d((int)gn[k >> 3][k & 7]));
-            u[c] = mbit(mlo, mhi, c) ? un : u[c];     // entries outside M_{U+} stay fixed
+            const double t = fma(-dsg, i2d((int)gn[k >> 3][k & 7]), u[c]);
+            u[c] = (__double2hiint(t) & ~__double2hiint(u[c])) < 0 ? 0.0 : t;
           }
         }
         tc_fence_before();       // TMEM reads done before the next round's MMAs
