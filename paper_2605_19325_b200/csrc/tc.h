@@ -94,7 +94,7 @@ int tc_pbcd_chunk(const float* F, int64_t ldf, int64_t rows, int r, const double
 // rounds, 32-column Gauss-Seidel blocks in registers (tc_pbcd.cu).  Runs only if *stage == 1.
 // Writes minparts[0, nparts) (nparts >= tc_hals_parts()); colmax (u64[r]) as hals_rows;
 // fallbacks (optional) counts rows redone in fp64 because u outgrew its digit scale.
-// gd_work / gscale_work as tc_pbcd_rows (the two never run in the same stage).  ill
+// gd_work / gscale_work as tc_pbcd_prepare (the two never run in the same stage).  ill
 // (optional, device int): set nonzero when some column of G is too ill-conditioned for the
 // digit coupling (the kernel then returns at once; run hals_rows gated on *ill).  0 = launched.
 int tc_hals_parts();

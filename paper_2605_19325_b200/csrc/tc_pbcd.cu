@@ -17,9 +17,10 @@
 // Warp roles: 4 NH warps, NH threads per row, each owning 128 / NH columns (TMEM lane quadrant =
 // warp % 4, column part = warp / 4).  Warp 0 allocates TMEM; thread 0 issues each round's MMAs
 // after the named barrier that publishes the A planes.
-// Everything else follows pbcd_kernel: lift + mask at entry, a snapshot of every iterate, and the
-// per-iteration ||M o grad||^2 partials for the global stopping rule (pbcd_select_stage /
-// pbcd_copy_tiled), run in stages (tc_pbcd_chunk).
+// Everything else follows pbcd_kernel -- lift + mask at entry and the per-iteration
+// ||M o grad||^2 partials for the global stopping rule -- but run in stages (tc_pbcd_chunk,
+// pbcd_select_stage) that hand the fp64 iterate over through two state buffers, with a replay
+// instead of pbcd_kernel's per-iterate snapshots (pbcd_commit_state commits the result).
 #include <float.h>
 #include <math.h>
 #include <stdint.h>
