@@ -256,6 +256,41 @@ def test_shadow_ascent_sweeps(cfg, prec):
     assert all(m[4] < tol_margin for m in sh.kmis), sh.kmis
 
 
+@pytest.mark.parametrize("cfg", CASES[:5] + [CASES[6]], ids=IDS[:5] + [IDS[6]])
+def test_shadow_tc_pbcd_one_iteration_all_rows(cfg):
+    """The tensor-core PBCD kernel against Alg. 2 on EVERY row: with max_iter = 1 (eps = 0, so
+    k* = 1) the inner iteration cannot amplify the X passes' ~6e-9 into the R33 orbits, so one
+    lift + PBCD step per block -- the oracle from the GPU's own start state, on the exact X V
+    and X^T U_new -- must agree per update at 1e-5 over all rows, for 3 ascent sweeps.  This
+    separates the kernel's arithmetic (digit MMAs, byte digits, the Eq.(10) step, the
+    projection) from the method's own ill-conditioning, which removes most rows of the
+    tensor-core cases from test_shadow_ascent_sweeps at 50 iterations.  The rows that
+    test_shadow_ascent_sweeps would exclude (perturbation 2^-22) are counted and printed."""
+    h, X, _ = make(cfg, precision=TC, pbcd_max_iter=1, pbcd_eps=0.0)
+    Ut, Vt, lu, lv = start_point(X, cfg.r, want_infeasible=True)
+    U, V = to_dev(Ut), to_dev(Vt)
+    h.set_stage(0, lu, lv)
+    eu = ev = 0.0
+    flips = ill = 0
+    for t in range(3):
+        _, info = h.iterate(U, V, 1)
+        assert info["ascent_sweeps"] == 1
+        assert info["pbcd_iters_u"] == 1 and info["pbcd_iters_v"] == 1
+        Un, Vn = to_np(U), to_np(V)
+        Uo, _, _, illu = oracle_block(X, Ut, Vt, True, True, lu, 1, DELTA[TC])
+        Vo, _, _, illv = oracle_block(X, Vt, Un, False, True, lv, 1, DELTA[TC])
+        for gpu, ora, il in ((Un, Uo, illu), (Vn, Vo, illv)):
+            e, fl = r20(gpu, ora)
+            flips += fl
+            ill += int(il.sum())
+        eu, ev = max(eu, r20(Un, Uo)[0]), max(ev, r20(Vn, Vo)[0])
+        Ut, Vt = Un, Vn
+    print(f"{cfg.name} tc PBCD x1, all rows: per-update U {eu:.2e} V {ev:.2e}, flips {flips} "
+          f"({ill} rows would count as ill-conditioned at 2^-22)")
+    assert eu < 1e-5 and ev < 1e-5
+    assert flips <= 1e-6 * (cfg.m + cfg.n) * cfg.r * 3
+
+
 # ----------------------------------------------------------------------------- trajectories
 @pytest.mark.parametrize("prec", PRECS, ids=PIDS)
 @pytest.mark.parametrize("cfg", CASES[:4] + [CASES[6]], ids=IDS[:4] + [IDS[6]])
