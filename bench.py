@@ -41,6 +41,10 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-ablation", action="store_true")
     p.add_argument("--cpu-sample-rows", type=int, default=0)
+    p.add_argument("--nccl-single", action="store_true",
+                   help="at one GPU, still run the sharded code path with a one-rank NCCL "
+                        "communicator (exercises the collectives; results are bitwise those "
+                        "of the plain path)")
     p.add_argument("--no-small", action="store_true",
                    help="skip the C1-C4 / eNMC / C6 rates reported in config.small_configs")
     return p.parse_args()
@@ -333,7 +337,7 @@ def run_enmf(args):
     cfg = synth.ALL[args.config]
     m, n, r = cfg.m, cfg.n, cfg.r
     begin, count = E.row_partition(m, world, rank)
-    uid = None
+    uid = E.nccl_unique_id() if (world == 1 and args.nccl_single) else None
     if world > 1:
         obj = [E.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -573,7 +577,10 @@ def run_enmf(args):
             "data": "synthetic",
             "config": {"workload": cfg.name, "m": m, "n": n, "r": r,
                        "global_batch": m, "seq_len": n,
-                       "parallelism": f"row-shard x{world} (NCCL reduce-scatter of X^T U, all-gather of V slices, allreduce of Grams)",
+                       "parallelism": (f"row-shard x{world} (NCCL: per-slice reduce of X^T U "
+                                       "overlapped with pass 2, all-gather of V slices, "
+                                       "allreduce of Grams)" if uid is not None else
+                                       "single GPU, no collectives"),
                        "l2": (f"CSR of X {x_bytes_pass / 1e9:.2f} GB > L2, no flush"
                               if sparse else "inputs larger than L2 (X is 40 GB), no flush"),
                        "nnz": int(nnz_all) if sparse else m * n,

@@ -61,8 +61,12 @@ typedef struct {
   int64_t row_count;       /* X/U rows owned by this rank (m_global when world_size == 1) */
   int world_size;          /* ranks (GPUs) */
   int rank;                /* this rank */
-  const void* nccl_unique_id; /* 128-byte ncclUniqueId from rank 0; NULL if world_size == 1,
-                              or NULL with world_size > 1 to use enmf_set_host_allreduce */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId from rank 0; NULL with world_size > 1
+                              to use enmf_set_host_allreduce.  Non-NULL at world_size == 1:
+                              a one-rank communicator and the sharded code path (V slice,
+                              sliced pass 2, collectives) -- results equal the plain
+                              single-rank path bitwise; NULL at world_size == 1: no
+                              collectives at all */
   void* cuda_stream;       /* cudaStream_t for every call; NULL = legacy default stream */
 } enmf_problem_t;
 
@@ -132,7 +136,7 @@ typedef struct {
 void enmf_default_options(enmf_options_t* opt);
 
 /* Create a handle for one problem shape.  Validates shapes (ENMF_ERR_SHAPE), sets up the
- * NCCL communicator when world_size > 1 (ENMF_ERR_NCCL), allocates workspaces
+ * NCCL communicator when nccl_unique_id is set (ENMF_ERR_NCCL), allocates workspaces
  * (ENMF_ERR_OOM).  *out is NULL on failure. */
 enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
                           enmf_handle_t* out);

@@ -160,7 +160,7 @@ class Enmf:
         self.rows = int(row_count if row_count is not None else m)
         self._stream = stream if stream is not None else torch.cuda.current_stream()
         self._uid = None
-        if world_size > 1 and nccl_id is not None:
+        if nccl_id is not None:
             if len(nccl_id) != 128:
                 raise ValueError("nccl_id must be the 128-byte ncclUniqueId")
             self._uid = ctypes.create_string_buffer(bytes(nccl_id), 128)

@@ -73,7 +73,7 @@ int comm_init(Comm** out, const void* uid128, int world, int rank) {
 }
 
 int comm_allreduce(Comm* c, void* buf, size_t count, CommType t, CommOp op, cudaStream_t st) {
-  if (!c || c->world == 1 || count == 0) return 0;
+  if (!c || count == 0) return 0;
   ncclDataType_t dt = t == CommType::F64 ? ncclFloat64 : ncclFloat32;
   ncclRedOp_t o = op == CommOp::Sum ? ncclSum : (op == CommOp::Min ? ncclMin : ncclMax);
   ncclResult_t rc = api().allreduce(buf, buf, count, dt, o, c->comm, st);
@@ -81,7 +81,7 @@ int comm_allreduce(Comm* c, void* buf, size_t count, CommType t, CommOp op, cuda
 }
 
 int comm_reduce_scatter(Comm* c, void* buf, size_t count, CommType t, cudaStream_t st) {
-  if (!c || c->world == 1 || count == 0) return 0;
+  if (!c || count == 0) return 0;
   const ncclDataType_t dt = t == CommType::F64 ? ncclFloat64 : ncclFloat32;
   const size_t esz = t == CommType::F64 ? 8 : 4;
   char* b = static_cast<char*>(buf);
@@ -92,7 +92,7 @@ int comm_reduce_scatter(Comm* c, void* buf, size_t count, CommType t, cudaStream
 }
 
 int comm_reduce(Comm* c, void* buf, size_t count, CommType t, int root, cudaStream_t st) {
-  if (!c || c->world == 1 || count == 0) return 0;
+  if (!c || count == 0) return 0;
   const ncclDataType_t dt = t == CommType::F64 ? ncclFloat64 : ncclFloat32;
   // in place on the root (sendbuff == recvbuff); the other ranks only send
   ncclResult_t rc = api().reduce(buf, buf, count, dt, ncclSum, root, c->comm, st);
@@ -100,7 +100,7 @@ int comm_reduce(Comm* c, void* buf, size_t count, CommType t, int root, cudaStre
 }
 
 int comm_allgather(Comm* c, void* buf, size_t count, CommType t, cudaStream_t st) {
-  if (!c || c->world == 1 || count == 0) return 0;
+  if (!c || count == 0) return 0;
   const ncclDataType_t dt = t == CommType::F64 ? ncclFloat64 : ncclFloat32;
   const size_t esz = t == CommType::F64 ? 8 : 4;
   char* b = static_cast<char*>(buf);

@@ -37,7 +37,7 @@ enmf_status_t dalloc_bytes(void** p, size_t bytes) {
 }
 
 enmf_status_t ar(enmf_handle_t h, double* buf, size_t count, CommOp op) {
-  if (h->prob.world_size <= 1 || count == 0) return ENMF_OK;
+  if (!h->sharded || count == 0) return ENMF_OK;
   if (h->comm)
     return comm_allreduce(h->comm, buf, count, CommType::F64, op, h->st) == 0 ? ENMF_OK
                                                                              : ENMF_ERR_NCCL;
@@ -178,7 +178,7 @@ static enmf_status_t contract_xtu_sliced(enmf_handle_t h, const float* U, int64_
 enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double* Q,
                            const unsigned long long* umax, bool slice) {
   const char* pc = getenv("ENMF_PASS2_SLICED");
-  if (slice && h->tc && h->prob.world_size > 1 && h->v_pad % 128 == 0 && !(pc && pc[0] == '0')) {
+  if (slice && h->tc && h->sharded && h->v_pad % 128 == 0 && !(pc && pc[0] == '0')) {
     ENMF_TRY(prof_mark(h, 1));
     ENMF_TRY(contract_xtu_sliced(h, U, ldu, Q, umax));
     return prof_mark(h, 1);
@@ -196,7 +196,7 @@ enmf_status_t contract_xtu(enmf_handle_t h, const float* U, int64_t ldu, double*
                        h->work_elems, h->st);
   }
   ENMF_TRY(prof_mark(h, 1));
-  if (slice && h->comm && h->prob.world_size > 1)
+  if (slice && h->comm && h->sharded)
     return comm_reduce_scatter(h->comm, Q, (size_t)(h->v_pad * h->r), CommType::F64, h->st) == 0
                ? ENMF_OK
                : ENMF_ERR_NCCL;
@@ -392,7 +392,7 @@ struct SweepHooks {
 
 enmf_status_t sweep(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv, int t,
                     bool maybe_ascent, const SweepHooks& hk = SweepHooks()) {
-  const bool sh = h->prob.world_size > 1;
+  const bool sh = h->sharded;
   cudaStream_t st = h->st;
   // U block: P = X V, G_V = V^T V (G_V carried over from the previous sweep's end).  The X V
   // pass depends on V only, so it is issued before the stage decision (which reads min U).
@@ -718,8 +718,9 @@ enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
   // V slices (the sharded V block): ceil(n / world) rows each, rounded up to whole 128-row
   // bands when every rank still gets rows (n >= 128 world), so that the tensor-core pass 2 can
   // reduce each slice to its owner as soon as that slice's bands are done
+  h->sharded = prob->world_size > 1 || prob->nccl_unique_id != nullptr;
   h->v_pad = (n + prob->world_size - 1) / prob->world_size;
-  if (prob->world_size > 1 && n >= 128 * (int64_t)prob->world_size) {
+  if (h->sharded && n >= 128 * (int64_t)prob->world_size) {
     const int64_t al = (h->v_pad + 127) / 128 * 128;
     if ((prob->world_size - 1) * al < n) h->v_pad = al;
   }
@@ -738,7 +739,7 @@ enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
   ALLOC(h->minparts, (size_t)kRowGrid);
   ALLOC(h->pgsum, (size_t)(o.pbcd_max_iter + 1));
 #undef ALLOC
-  if (s == ENMF_OK && prob->world_size > 1) {
+  if (s == ENMF_OK && h->sharded) {
     // V slice of this rank: rows [rank v_pad, rank v_pad + v_count), the last one(s) shorter
     h->v_begin = std::min<int64_t>(n, prob->rank * h->v_pad);
     h->v_count = std::min<int64_t>(h->v_pad, n - h->v_begin);
@@ -747,7 +748,7 @@ enmf_status_t enmf_create(const enmf_problem_t* prob, const enmf_options_t* opt,
     else
       s = dalloc(&h->Vg, (size_t)(n * r));
   }
-  if (s == ENMF_OK && prob->world_size > 1 && prob->nccl_unique_id) {
+  if (s == ENMF_OK && h->sharded && prob->nccl_unique_id) {
     if (comm_init(&h->comm, prob->nccl_unique_id, prob->world_size, prob->rank) != 0)
       s = ENMF_ERR_NCCL;
   }
@@ -836,7 +837,7 @@ namespace {
 enmf_status_t bind_csr(enmf_handle_t h, const int64_t* row_ptr, const int32_t* col_idx,
                        const float* vals, int64_t nnz, bool nmc) {
   if (!h || !row_ptr || nnz < 0 || (nnz > 0 && (!col_idx || !vals))) return ENMF_ERR_INVALID_ARG;
-  if (nmc && (h->prob.world_size != 1 || !nmc_supported((int)h->r))) return ENMF_ERR_SHAPE;
+  if (nmc && (h->sharded || !nmc_supported((int)h->r))) return ENMF_ERR_SHAPE;
   if (nnz > INT32_MAX || h->n > INT32_MAX) return ENMF_ERR_SHAPE;
   LaunchScope ls(h);
   h->bound = false;
@@ -1024,7 +1025,7 @@ enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int
                            int n_iters, double* f_trace_host, enmf_iter_info_t* info,
                            cudaEvent_t u_ready, float* u_dl_host, float* v_dl_host) {
   LaunchScope ls(h);
-  const bool sh = h->prob.world_size > 1;
+  const bool sh = h->sharded;
   const bool maybe_ascent = !h->stage_known_hals || h->nmc;
   if (maybe_ascent || h->opt.descent) ENMF_TRY(ensure_snaps(h));
   ENMF_TRY(ensure_ftrace(h, std::max(n_iters, 1)));
@@ -1138,7 +1139,7 @@ enmf_status_t enmf_objective(enmf_handle_t h, const float* U, int64_t ldu, const
   ENMF_TRY(validate_ld(U, ldu, h->r));
   ENMF_TRY(validate_ld(V, ldv, h->r));
   LaunchScope ls(h);
-  const bool sh = h->prob.world_size > 1;
+  const bool sh = h->sharded;
   double* f = h->dscal + S_SCRATCH;
   if (h->nmc) {
     // eNMC: the masked objective over the observed entries
@@ -1190,7 +1191,7 @@ enmf_status_t enmf_kkt_residual(enmf_handle_t h, const float* U, int64_t ldu, co
   ENMF_TRY(validate_ld(U, ldu, h->r));
   ENMF_TRY(validate_ld(V, ldv, h->r));
   LaunchScope ls(h);
-  const bool sh = h->prob.world_size > 1;
+  const bool sh = h->sharded;
   const int r = (int)h->r;
   // grad_U f = U G_V - X V ; grad_V f = V G_U - X^T U
   ENMF_TRY(contract_xv(h, V, ldv, h->P));

@@ -90,7 +90,7 @@ enmf_status_t column_signs(enmf_handle_t h, const double* A, int64_t rows, int r
       }
     }
   sign.assign(r, 1.0);
-  if (h->prob.world_size > 1) {
+  if (h->sharded) {
     double* d = h->work;   // [best | idx | sign]
     std::vector<double> tmp(best);
     CUDA_TRY(cudaMemcpyAsync(d, tmp.data(), sizeof(double) * r, cudaMemcpyHostToDevice, h->st));
@@ -134,7 +134,7 @@ enmf_status_t svd_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t
   int64_t l64 = std::min<int64_t>(std::min(m, n), r + h->opt.oversample);
   l64 = std::min<int64_t>(l64, 512);
   const int l = (int)l64;
-  const bool sh = h->prob.world_size > 1;
+  const bool sh = h->sharded;
   DevBuf db(h);
   double *Om, *Y, *Z, *Qt, *tmp, *G, *R, *Rinv, *Ue, *Ve, *sv, *jw, *Us;
   int* bad;
@@ -252,7 +252,7 @@ enmf_status_t rotate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int6
   const int64_t mr = h->m_loc, n = h->n, rows = mr + n;
   const int r = (int)h->r;
   const int64_t count = rows * r;
-  const bool sh = h->prob.world_size > 1;
+  const bool sh = h->sharded;
   DevBuf db(h);
   double *WR, *Yh, *Z, *B, *R, *M, *Cs, *Ds, *sv, *jw;
   unsigned long long* third;
@@ -678,7 +678,7 @@ enmf_status_t enmf_rotate_rsr(enmf_handle_t h, float* U, int64_t ldu, float* V, 
                               enmf_init_info_t* info, double* lambda_host) {
   if (!h) return ENMF_ERR_INVALID_ARG;
   if (!h->bound) return ENMF_ERR_STATE;
-  if (h->prob.world_size != 1) return ENMF_ERR_STATE;
+  if (h->sharded) return ENMF_ERR_STATE;
   ENMF_TRY(validate_ld(U, ldu, h->r));
   ENMF_TRY(validate_ld(V, ldv, h->r));
   LaunchScope ls(h);
@@ -710,7 +710,7 @@ enmf_status_t enmf_solve_host(enmf_handle_t h, const float* X_host, float* U_hos
                               float* V_host, int n_iters, double* f_trace_host,
                               enmf_init_info_t* info) {
   if (!h || !X_host || !U_host || !V_host || n_iters < 0) return ENMF_ERR_INVALID_ARG;
-  if (h->prob.world_size != 1) return ENMF_ERR_STATE;
+  if (h->sharded) return ENMF_ERR_STATE;
   const int64_t m = h->m_loc, n = h->n, r = h->r;
   if (!h->x_owned) ENMF_TRY(dalloc(&h->x_owned, (size_t)(m * n)));
   // host -> device through two pinned staging buffers, copies overlapped with memcpy

@@ -72,6 +72,9 @@ struct enmf_handle_s {
   // multi-rank V block: this rank updates V rows [v_begin, v_begin + v_count) and the full V
   // is reassembled by a zero-padded fp64 allreduce (exact: adding zeros), SURVEY §8(e)
   int64_t v_begin = 0, v_count = 0;
+  // the collective path runs: world_size > 1, or a communicator was requested at one rank
+  // (enmf_problem_t.nccl_unique_id set) -- the single-rank NCCL path tests and bench run
+  bool sharded = false;
   int64_t v_pad = 0;
   cudaStream_t st_comm = nullptr;          // slice reductions of the sliced pass 2 (NCCL)
   std::vector<cudaEvent_t> ev_comm;
