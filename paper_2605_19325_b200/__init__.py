@@ -406,6 +406,10 @@ class Enmf:
 
 
 def nccl_unique_id():
+    # torch first: its libtorch_cuda.so binds the NCCL it ships (2.28); libenmf.so dlopens
+    # "libnccl.so.2", which then resolves to that already-loaded copy instead of loading the
+    # system one (2.27), which torch's later import would fail to link against
+    import torch  # noqa: F401
     buf = ctypes.create_string_buffer(128)
     _check(_lib.enmf_nccl_unique_id(buf), "enmf_nccl_unique_id")
     return buf.raw

@@ -30,25 +30,6 @@ def rotated_point(X, r, admm_iters=100):
     return U, V, oracle.lift_constant(U), oracle.lift_constant(V)
 
 
-def ulp_perturb(A, seed):
-    """A with every entry moved by about one fp32 ulp (relative 2^-24 N(0,1))."""
-    g = np.random.default_rng(seed)
-    return (A * (1 + 2.0 ** -24 * g.standard_normal(A.shape))).astype(np.float32).astype(np.float64)
-
-
-def oracle_floor(run, U0, V0, trials=3):
-    """The method's own fp32 floor: spread of the oracle's output `run(U, V)` (a tuple of
-    arrays) when its input state is perturbed by one fp32 ulp.  Returns the max
-    relative Frobenius difference per output."""
-    ref = run(U0, V0)
-    worst = [0.0] * len(ref)
-    for t in range(trials):
-        out = run(ulp_perturb(U0, 100 + t), ulp_perturb(V0, 200 + t))
-        for i, (a, b) in enumerate(zip(out, ref)):
-            worst[i] = max(worst[i], rel_fro(a, b))
-    return ref, worst
-
-
 def make(cfg_or_X, r=None, **opts):
     import paper_2605_19325_b200 as E
     X = cfg_or_X if isinstance(cfg_or_X, np.ndarray) else synth.x_full(cfg_or_X)
