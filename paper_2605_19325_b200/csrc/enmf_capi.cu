@@ -654,7 +654,8 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
   void* bufs[] = {h->dscal, h->dint, h->P, h->Q, h->GU, h->GV, h->work, h->parts,
                   h->minparts, h->pgsum, h->snaps, h->ftrace, h->x_owned, h->W64,
                   h->tcpb_ws, h->fmax_uv, h->Ud, h->Vd, h->arena, h->Vg, h->Vpad,
-                  h->csc_ptr, h->csc_row, h->csc_val, h->stepws, h->pbcd_state};
+                  h->csc_ptr, h->csc_row, h->csc_val, h->stepws, h->pbcd_state,
+                  h->small_ws};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (void* b : h->arena_extra) cudaFree(b);
@@ -1043,15 +1044,57 @@ enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int
   // sweep) are bound by launch latency.  ENMF_GRAPH=0 disables it.
   const char* ge = getenv("ENMF_GRAPH");
   const bool graphs = !(ge && ge[0] == '0');
+  // Cache-resident problems on the fp64 path (C1-C4): every HALS sweep runs in the persistent
+  // kernel of small_sweep.cu (one cooperative launch for all remaining sweeps).  Which sweeps
+  // are HALS sweeps must not depend on how the caller chunks its calls, so while the stage is
+  // still the ascent the host reads the stage flag and the factor minima before every sweep
+  // (stage_update's rule; a sync per ascent sweep, ~10 of them) and the ascent
+  // sweeps run as separate launches.  ENMF_SMALL_FUSED=0 disables it.
+  const char* se = getenv("ENMF_SMALL_FUSED");
+  const bool small = !(se && se[0] == '0') && !sh && !h->sparse && !h->nmc && !h->tc &&
+                     !h->opt.descent && !h->prof &&
+                     small_sweeps_supported(h->m_loc, h->n, (int)h->r);
+  if (small && u_ready) {                // tiny transfers: no overlap worth a second code path
+    CUDA_TRY(cudaStreamWaitEvent(h->st, u_ready, 0));
+    ENMF_TRY(min_factor(h, U, ldu, h->m_loc, S_MINU, sh));
+    u_ready = nullptr;
+  }
   // (not while the X passes are being timed: enmf_set_profiling brackets every pass with events)
   const bool graph = graphs && !sh && !u_ready && !u_dl_host && !v_dl_host && n_iters >= 3 &&
-                     !h->prof;
+                     !h->prof && !small;
   for (int t = 0; t < n_iters; ++t) {
     SweepHooks hk;
     if (t == 0) hk.u_ready = u_ready;
     if (t == n_iters - 1) {
       hk.u_download = u_dl_host;
       hk.v_download = v_dl_host;
+    }
+    if (small && !h->stage_known_hals) {
+      int stg = 0;
+      double mn[2];
+      CUDA_TRY(cudaMemcpyAsync(&stg, h->dint + I_STAGE, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+      CUDA_TRY(cudaMemcpyAsync(mn, h->dscal + S_MINU, sizeof(mn), cudaMemcpyDeviceToHost, h->st));
+      CUDA_TRY(cudaStreamSynchronize(h->st));
+      if (stg == 1 || (mn[0] >= 0.0 && mn[1] >= 0.0)) h->stage_known_hals = true;
+    }
+    if (small && h->stage_known_hals) {
+      if (!h->small_ws) {
+        const size_t need = small_sweeps_workspace(h->m_loc, h->n, (int)h->r);
+        if (need == 0) return ENMF_ERR_CUDA;
+        ENMF_TRY(dalloc(&h->small_ws, need));
+      }
+      if (small_sweeps_launch(h->X, h->ldx, h->m_loc, h->n, (int)h->r, U, ldu, V, ldv, h->GV,
+                              h->GU, h->dscal + S_XNORM2, h->ftrace, h->dint + I_FCNT,
+                              h->dscal + S_MINU, h->dscal + S_MINV, h->dint + I_STAGE,
+                              h->dint + I_CNT_HALS, h->small_ws, n_iters - t, h->st))
+        return ENMF_ERR_CUDA;
+      if (u_dl_host)
+        CUDA_TRY(cudaMemcpyAsync(u_dl_host, U, sizeof(float) * h->m_loc * h->r,
+                                 cudaMemcpyDeviceToHost, h->st));
+      if (v_dl_host)
+        CUDA_TRY(cudaMemcpyAsync(v_dl_host, V, sizeof(float) * h->n * h->r,
+                                 cudaMemcpyDeviceToHost, h->st));
+      break;
     }
     if (graph && t == 1) {
       ENMF_TRY(replay_sweeps(h, U, ldu, V, ldv, maybe_ascent, n_iters - 1));

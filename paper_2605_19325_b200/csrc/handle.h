@@ -106,6 +106,7 @@ struct enmf_handle_s {
   cudaStream_t st2 = nullptr;
   cudaStream_t cap_st = nullptr;   // non-blocking stream a sweep is captured on (CUDA graph)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  double* small_ws = nullptr;      // workspace of the persistent small-problem HALS kernel
   float* x_owned = nullptr;  // device copy of X owned by enmf_solve_host
   double* W64 = nullptr;     // (m_loc + n) x r fp64 [U*; V*] kept from enmf_svd for enmf_rotate
   // profiling of the X passes (enmf_set_profiling): CUDA events around every contraction

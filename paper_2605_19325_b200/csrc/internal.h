@@ -177,6 +177,21 @@ void frob_direct(const float* X, int64_t ldx, int64_t rows, int64_t n, const flo
                  int64_t ldu, const float* V, int64_t ldv, int r, double* parts, int* nparts,
                  cudaStream_t st);
 
+// ---------------------------------------------------------------- cache-resident sweeps
+// small_sweep.cu: `count` HALS sweeps of a dense problem whose X
+// stays cache resident (C1-C4) in one cooperative persistent kernel, fp64 on the
+// fp32 state: U, V updated in place; GV in = V^T V of the V passed in, GV / GU out = the Grams
+// of the final factors; one trace-form objective per sweep appended at ftrace[(*fcnt)++];
+// *minu, *minv = the factor minima, *stage = 1, *cnt_hals += count.  ws >=
+// small_sweeps_workspace() doubles.  Returns nonzero if the launch failed.
+bool small_sweeps_supported(int64_t m, int64_t n, int r);
+size_t small_sweeps_workspace(int64_t m, int64_t n, int r);
+int small_sweeps_launch(const float* X, int64_t ldx, int64_t m, int64_t n, int r, float* U,
+                        int64_t ldu, float* V, int64_t ldv, double* GV, double* GU,
+                        const double* xnorm2, double* ftrace, int* fcnt, double* minu,
+                        double* minv, int* stage, int* cnt_hals, double* ws, int count,
+                        cudaStream_t st);
+
 // ---------------------------------------------------------------- small dense (one CTA)
 // Upper Cholesky G = R^T R of a k x k SPD matrix (row-major, ld k) with diagonal shift,
 // and Rinv = R^{-1}.  *bad = number of non-positive pivots (replaced by tiny values).

@@ -1,0 +1,555 @@
+// small_sweep.cu -- HALS sweeps of a cache-resident problem in ONE persistent kernel.
+//
+// the small BASELINE configurations (C1-C4, X <= 90 MB) are bound by launch and
+// synchronisation latency, not by HBM: a HALS sweep issued as separate kernels is ~25 launches
+// of a few microseconds each around ~10 us of arithmetic.  Here a cooperative grid runs
+// `count` whole sweeps (U block with P = X V and G_V, V block with
+// Q = X^T U_new and G_U, then the trace-form objective, BASELINE.json:5) with four grid
+// barriers per sweep and no host involvement:
+//
+//   A   partial products of P = X V over (64-row block) x (K chunk) tiles        | barrier
+//   A'  per row: P = sum of its partials, HALS column sweep, U written (fp32),
+//       per-CTA partial of G_U = U^T U, min U                                    | barrier
+//   B   G_U = fixed-order sum of the partials; partial products of Q = X^T U     | barrier
+//   B'  per row of V: Q, HALS, V written, partials of G_V, <Q, V>, min V         | barrier
+//   (next A: G_V and <Q, V> summed; next A': f = ||X||^2 - 2 <Q, V> + <G_U, G_V>)
+//
+// All arithmetic is fp64 on the fp32 state (the ENMF_PREC_FP64 path); every sum has a fixed
+// order given the grid, so results are deterministic.  The grid is sized to the problem (a
+// barrier over 8 CTAs is cheaper than over 296).  Single rank, dense X, HALS stage only.
+#include <cooperative_groups.h>
+#include <float.h>
+
+#include <algorithm>
+
+#include "internal.h"
+#include "rows_dev.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace enmf {
+namespace {
+
+using namespace rows_dev;
+
+constexpr int kT = 256;     // threads per CTA
+constexpr int kW = kT / 32;
+constexpr int kTM = 64;     // output rows of a product tile
+constexpr int kKS = 16;     // K slab
+constexpr int kXP = kTM + 2;   // padded slab row (doubles; 16-byte aligned rows)
+constexpr int kRB = 4;      // rows per warp in the HALS phases
+
+struct SmallArgs {
+  const float* X;
+  int64_t ldx, m, n;
+  int r;
+  float* U;
+  int64_t ldu;
+  float* V;
+  int64_t ldv;
+  double* GV;        // in: V^T V of the V passed in; out: of the final V
+  double* GU;        // out: U^T U of the final U
+  const double* xnorm2;
+  double* ftrace;
+  int* fcnt;
+  double* minu;
+  double* minv;
+  int* stage;
+  int* cnt_hals;
+  double* pp;        // tile partials: max(ksA m, ksB n) r
+  double* gp;        // Gram partials: gridDim x r^2
+  double* sc;        // scalar partials: cross[grid], min[grid], then 2 reduced scalars
+  int ksA, ksB;
+  int64_t kcA, kcB;  // K chunk of a tile
+  int count;
+};
+
+// ---------------------------------------------------------------------------------------------
+// One product tile: out[(row - r0)][c] = sum_{k in [k0, k1)} op(X)[row][k] F[k][c] for the 64
+// output rows r0.. (rows of X if !TRANS, columns of X if TRANS) and all r columns.  Thread
+// (ty, tx) owns output rows 4 ty .. 4 ty + 3 and columns 2 tx + (b & 1) + 32 (b >> 1)
+// (RC = 1: column tx), so both operands are read from shared memory as 16-byte loads.
+template <int RC, bool TRANS>
+__device__ __forceinline__ void product_tile(const float* __restrict__ X, int64_t ldx, int64_t M,
+                                             int64_t K, const float* F, int64_t ldf, int r,
+                                             int64_t r0, int64_t k0, int64_t k1, double* out,
+                                             double* Xs, double* Fs) {
+  constexpr int RCOLS = 16 * RC;
+  constexpr int XQ = kTM * kKS / kT;       // X elements per thread and slab (4)
+  constexpr int FQ = RCOLS * kKS / kT;     // factor elements per thread and slab (RC)
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  double acc[4][RC];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < RC; ++b) acc[a][b] = 0.0;
+  float xr[XQ], fr[FQ];
+  auto fetch = [&](int64_t ks) {
+#pragma unroll
+    for (int q = 0; q < XQ; ++q) {
+      const int e = t + kT * q;
+      int ii, kk;
+      if (TRANS) { kk = e / kTM; ii = e % kTM; }
+      else { ii = e / kKS; kk = e % kKS; }
+      const int64_t gi = r0 + ii, gk = ks + kk;
+      float v = 0.f;
+      if (gi < M && gk < k1) v = TRANS ? X[gk * ldx + gi] : X[gi * ldx + gk];
+      xr[q] = v;
+    }
+#pragma unroll
+    for (int q = 0; q < FQ; ++q) {
+      const int e = t + kT * q;
+      const int kk = e / RCOLS, c = e % RCOLS;
+      const int64_t gk = ks + kk;
+      fr[q] = (c < r && gk < k1) ? F[gk * ldf + c] : 0.f;
+    }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int q = 0; q < XQ; ++q) {
+      const int e = t + kT * q;
+      int ii, kk;
+      if (TRANS) { kk = e / kTM; ii = e % kTM; }
+      else { ii = e / kKS; kk = e % kKS; }
+      Xs[kk * kXP + ii] = (double)xr[q];
+    }
+#pragma unroll
+    for (int q = 0; q < FQ; ++q) {
+      const int e = t + kT * q;
+      Fs[e] = (double)fr[q];               // Fs[kk][c], kk = e / RCOLS
+    }
+  };
+  fetch(k0);
+  for (int64_t ks = k0; ks < k1; ks += kKS) {
+    __syncthreads();                       // the previous slab's reads are done
+    stash();
+    __syncthreads();
+    if (ks + kKS < k1) fetch(ks + kKS);    // next slab's loads in flight during the FMAs
+#pragma unroll
+    for (int kk = 0; kk < kKS; ++kk) {
+      const double2 x01 = *reinterpret_cast<const double2*>(Xs + kk * kXP + 4 * ty);
+      const double2 x23 = *reinterpret_cast<const double2*>(Xs + kk * kXP + 4 * ty + 2);
+      const double xv[4] = {x01.x, x01.y, x23.x, x23.y};
+      double fv[RC];
+      if (RC == 1) {
+        fv[0] = Fs[kk * RCOLS + tx];
+      } else {
+#pragma unroll
+        for (int b = 0; b < RC; b += 2) {
+          const double2 f2 = *reinterpret_cast<const double2*>(Fs + kk * RCOLS + 2 * tx + 16 * b);
+          fv[b] = f2.x;
+          fv[b + 1] = f2.y;
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < RC; ++b) acc[a][b] = fma(xv[a], fv[b], acc[a][b]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t row = r0 + 4 * ty + a;
+    if (row >= M) continue;
+#pragma unroll
+    for (int b = 0; b < RC; ++b) {
+      const int c = RC == 1 ? tx : 2 * tx + (b & 1) + 32 * (b >> 1);
+      if (c < r) out[row * r + c] = acc[a][b];
+    }
+  }
+}
+
+// All tiles of one pass: tile = (row block, K chunk); partial of chunk q at pp[q M r ...].
+template <int RC, bool TRANS>
+__device__ __forceinline__ void product_pass(const float* __restrict__ X, int64_t ldx, int64_t M,
+                                             int64_t K, const float* F, int64_t ldf, int r,
+                                             int ksplit, int64_t kchunk, double* pp, double* Xs,
+                                             double* Fs) {
+  const int64_t nrb = (M + kTM - 1) / kTM;
+  const int64_t tiles = nrb * ksplit;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t rb = tile % nrb, q = tile / nrb;
+    const int64_t k0 = q * kchunk, k1 = K < k0 + kchunk ? K : k0 + kchunk;
+    product_tile<RC, TRANS>(X, ldx, M, K, F, ldf, r, rb * kTM, k0, k1, pp + q * M * r, Xs, Fs);
+  }
+}
+
+// G (r x r) = sum over the first nparts per-CTA partials, one entry per warp at a time: the
+// lanes take the partials strided, then a fixed xor tree.
+__device__ __forceinline__ void reduce_gram(const double* gp, int nparts, int r, double* G) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * kW + (threadIdx.x >> 5);
+  const int nn = r * r;
+  for (int64_t e = gw; e < nn; e += (int64_t)gridDim.x * kW) {
+    double s = 0.0;
+    for (int p = lane; p < nparts; p += 32) s += gp[(int64_t)p * nn + e];
+    s = warp_sum(s);
+    if (lane == 0) G[e] = s;
+  }
+}
+
+// CTA 0, warp 0: out = sum (or min) of n partials
+__device__ __forceinline__ double reduce_scalar(const double* parts, int n, bool is_min) {
+  const int lane = threadIdx.x & 31;
+  double s = is_min ? DBL_MAX : 0.0;
+  for (int p = lane; p < n; p += 32) s = is_min ? fmin(s, parts[p]) : s + parts[p];
+  return is_min ? warp_min(s) : warp_sum(s);
+}
+
+// HALS on the rows of F (rows x r): C = sum of the ksplit tile partials, t = C - u G, then the
+// Gauss-Seidel column sweep U_ik <- max(0, U_ik + (C_ik - sum_l U_il G_lk) / G_kk)
+// (PAPER.md:322-324), F written in fp32; per-CTA partial Gram of the written rows, optional
+// partial <C, F_new>, partial min.  Gs: the Gram in shared memory; Ss: kW x kRB x RP doubles.
+template <int CPL>
+__device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, int r,
+                                           const double* pp, int ksplit, const double* G,
+                                           double* gpart, double* crosspart, double* minpart,
+                                           double* Gs, double* Ss, double* ginv, double* red) {
+  constexpr int RP = 32 * CPL;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nblk = (rows + kRB - 1) / kRB;
+  const bool cta_active = (int64_t)blockIdx.x * kW < nblk;
+  double wmin = DBL_MAX, wcross = 0.0;
+  if (cta_active) {
+    load_gram<CPL>(G, r, Gs);
+    for (int k = threadIdx.x; k < RP; k += kT) {
+      const double gkk = k < r ? G[k * r + k] : 0.0;
+      ginv[k] = gkk > 0.0 ? 1.0 / gkk : 0.0;
+    }
+    __syncthreads();
+    double* Sw = Ss + warp * kRB * RP;
+    bool first = true;
+    for (int64_t base = (int64_t)blockIdx.x * kW; base < nblk; base += (int64_t)gridDim.x * kW) {
+      const int64_t rb = base + warp;
+      double u[kRB][CPL], t[kRB][CPL], c0[kRB][CPL];
+#pragma unroll
+      for (int b = 0; b < kRB; ++b)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int64_t row = rb * kRB + b;
+          const int col = lane + 32 * c;
+          const bool ok = rb < nblk && row < rows && col < r;
+          u[b][c] = ok ? (double)F[row * ldf + col] : 0.0;
+          double s = 0.0;
+          if (ok)
+            for (int q = 0; q < ksplit; ++q) s += pp[((int64_t)q * rows + row) * r + col];
+          t[b][c] = s;
+          c0[b][c] = s;
+        }
+      row_times_gram<CPL, kRB>(u, Gs, Sw, r, lane, -1.0, t);      // t = C - u G
+#pragma unroll
+      for (int s = 0; s < CPL; ++s) {
+        const int kmax = r - 32 * s < 32 ? r - 32 * s : 32;
+        for (int kk = 0; kk < kmax; ++kk) {
+          const int k = 32 * s + kk;
+          const double ig = ginv[k];
+          if (ig == 0.0) continue;                  // G_kk <= 0: column skipped (warp-uniform)
+          double gk[CPL];
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) gk[c] = Gs[k * RP + lane + 32 * c];
+#pragma unroll
+          for (int b = 0; b < kRB; ++b) {
+            // lane kk owns (u_k, t_k); its change d is broadcast and the residual follows
+            const double uo = u[b][s];
+            const double v = fma(t[b][s], ig, uo);
+            const double nu = v > 0.0 ? v : 0.0;
+            if (lane == kk) u[b][s] = nu;
+            const double d = __shfl_sync(FULL, nu - uo, kk);
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) t[b][c] = fma(-d, gk[c], t[b][c]);
+          }
+        }
+      }
+      // write the rows (fp32: the state), keep their rounded values for the Gram partial
+      __syncwarp();
+#pragma unroll
+      for (int b = 0; b < kRB; ++b)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int64_t row = rb * kRB + b;
+          const int col = lane + 32 * c;
+          double w = 0.0;
+          if (rb < nblk && row < rows && col < r) {
+            const float v = (float)u[b][c];
+            F[row * ldf + col] = v;
+            w = (double)v;
+            wmin = fmin(wmin, w);
+            wcross = fma(c0[b][c], w, wcross);
+          }
+          Sw[b * RP + col] = w;
+        }
+      __syncthreads();
+      // partial Gram of this round's kW * kRB rows: 4 x 4 blocks of the upper block triangle
+      {
+        const int nb4 = (r + 3) / 4;
+        const int npair = nb4 * (nb4 + 1) / 2;
+        for (int p = threadIdx.x; p < npair; p += kT) {
+          // p -> (a, b), a <= b, row-major over the upper triangle
+          int a = 0, rem = p;
+          while (rem >= nb4 - a) { rem -= nb4 - a; ++a; }
+          const int b = a + rem;
+          double g[4][4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) g[i][j] = 0.0;
+          for (int row = 0; row < kW * kRB; ++row) {
+            const double2 a01 = *reinterpret_cast<const double2*>(Ss + row * RP + 4 * a);
+            const double2 a23 = *reinterpret_cast<const double2*>(Ss + row * RP + 4 * a + 2);
+            const double2 b01 = *reinterpret_cast<const double2*>(Ss + row * RP + 4 * b);
+            const double2 b23 = *reinterpret_cast<const double2*>(Ss + row * RP + 4 * b + 2);
+            const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+            const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) g[i][j] = fma(av[i], bv[j], g[i][j]);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int ci = 4 * a + i, cj = 4 * b + j;
+              if (ci < r && cj < r) {
+                const double val = first ? g[i][j] : gpart[ci * r + cj] + g[i][j];
+                gpart[ci * r + cj] = val;
+                if (a != b) gpart[cj * r + ci] = val;
+              }
+            }
+        }
+      }
+      first = false;
+      __syncthreads();
+    }
+  }
+  // per-CTA scalars (every CTA writes: the reductions read all gridDim slots)
+  wmin = warp_min(wmin);
+  wcross = warp_sum(wcross);
+  if (lane == 0) {
+    red[warp] = wmin;
+    red[kW + warp] = wcross;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mn = DBL_MAX, cr = 0.0;
+    for (int w = 0; w < kW; ++w) {
+      mn = fmin(mn, red[w]);
+      cr += red[kW + w];
+    }
+    minpart[blockIdx.x] = mn;
+    if (crosspart) crosspart[blockIdx.x] = cr;
+  }
+  __syncthreads();
+}
+
+// f = ||X||^2 - 2 <Q, V> + <G_U, G_V> (CTA 0), appended to the trace
+__device__ __forceinline__ void objective_append(const SmallArgs& a, double cross, double* red) {
+  const int nn = a.r * a.r;
+  double s = 0.0;
+  for (int e = threadIdx.x; e < nn; e += kT) s = fma(a.GU[e], a.GV[e], s);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double g = 0.0;
+    for (int w = 0; w < kW; ++w) g += red[w];
+    a.ftrace[(*a.fcnt)++] = *a.xnorm2 - 2.0 * cross + g;
+  }
+  __syncthreads();
+}
+
+template <int CPL, int RC>
+__global__ void __launch_bounds__(kT) small_hals_kernel(SmallArgs a) {
+  constexpr int RP = 32 * CPL;
+  extern __shared__ double smem[];
+  // product phases: Xs (kKS x kXP) + Fs (kKS x RCOLS); HALS phases: Gs (RP^2) + Ss + ginv
+  double* Xs = smem;
+  double* Fs = smem + kKS * kXP;
+  double* Gs = smem;
+  double* Ss = smem + RP * RP;
+  double* ginv = Ss + kW * kRB * RP;
+  __shared__ double red[2 * kW];
+  cg::grid_group grid = cg::this_grid();
+  const int G = (int)gridDim.x;
+  const int r = a.r;
+  const int64_t nblkU = (a.m + kRB - 1) / kRB, nblkV = (a.n + kRB - 1) / kRB;
+  const int64_t ctaU = (nblkU + kW - 1) / kW, ctaV = (nblkV + kW - 1) / kW;
+  const int actU = ctaU < G ? (int)ctaU : G;      // CTAs that write a Gram partial
+  const int actV = ctaV < G ? (int)ctaV : G;
+  double* crossp = a.sc;
+  double* minp = a.sc + G;
+  double* scal = a.sc + 2 * G;               // [0] cross, [1] min U, [2] min V
+  for (int t = 0; t < a.count; ++t) {
+    // ---- A: (G_V, <Q, V>, min V of the previous sweep;) partial products of P = X V
+    if (t > 0) {
+      reduce_gram(a.gp, actV, r, a.GV);
+      if (blockIdx.x == 0 && threadIdx.x < 32) {
+        const double cr = reduce_scalar(crossp, G, false);
+        const double mv = reduce_scalar(minp, G, true);
+        if (threadIdx.x == 0) {
+          scal[0] = cr;
+          scal[2] = mv;
+        }
+      }
+    }
+    product_pass<RC, false>(a.X, a.ldx, a.m, a.n, a.V, a.ldv, r, a.ksA, a.kcA, a.pp, Xs, Fs);
+    grid.sync();
+    // ---- A': (objective of the previous sweep;) HALS on U
+    if (t > 0 && blockIdx.x == 0) objective_append(a, scal[0], red);
+    hals_phase<CPL>(a.U, a.ldu, a.m, r, a.pp, a.ksA, a.GV, a.gp + (int64_t)blockIdx.x * r * r,
+                    nullptr, minp, Gs, Ss, ginv, red);
+    grid.sync();
+    // ---- B: G_U, min U; partial products of Q = X^T U
+    reduce_gram(a.gp, actU, r, a.GU);
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+      const double mu = reduce_scalar(minp, G, true);
+      if (threadIdx.x == 0) scal[1] = mu;
+    }
+    product_pass<RC, true>(a.X, a.ldx, a.n, a.m, a.U, a.ldu, r, a.ksB, a.kcB, a.pp, Xs, Fs);
+    grid.sync();
+    // ---- B': HALS on V with the cross-term partial <Q, V_new>
+    hals_phase<CPL>(a.V, a.ldv, a.n, r, a.pp, a.ksB, a.GU, a.gp + (int64_t)blockIdx.x * r * r,
+                    crossp, minp, Gs, Ss, ginv, red);
+    grid.sync();
+  }
+  // ---- tail: G_V, <Q, V>, min V of the last sweep, its objective, the handle's scalars
+  reduce_gram(a.gp, actV, r, a.GV);
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const double cr = reduce_scalar(crossp, G, false);
+    const double mv = reduce_scalar(minp, G, true);
+    if (threadIdx.x == 0) {
+      scal[0] = cr;
+      scal[2] = mv;
+    }
+  }
+  grid.sync();
+  if (blockIdx.x == 0) {
+    objective_append(a, scal[0], red);
+    if (threadIdx.x == 0) {
+      *a.minu = scal[1];
+      *a.minv = scal[2];
+      *a.stage = 1;
+      *a.cnt_hals += a.count;
+    }
+  }
+}
+
+template <int CPL, int RC>
+size_t smem_bytes() {
+  constexpr int RP = 32 * CPL;
+  const size_t prod = (size_t)(kKS * kXP + kKS * 16 * RC);
+  const size_t hals = (size_t)(RP * RP + kW * kRB * RP + RP);
+  return sizeof(double) * std::max(prod, hals);
+}
+
+// K split of a product pass: tiles = row blocks x ksplit on G CTAs; the cost of a pass is
+// (waves of tiles) x (chunk length + a fixed per-tile latency, in K units)
+void choose_split(int64_t M, int64_t K, int G, int* ksplit, int64_t* kchunk) {
+  const int64_t nrb = (M + kTM - 1) / kTM;
+  const int64_t kmax = std::max<int64_t>(1, (K + 63) / 64);
+  double best = 1e300;
+  int64_t bk = 1;
+  for (int64_t ks = 1; ks <= kmax && ks <= 4096; ++ks) {
+    int64_t kc = ((K + ks - 1) / ks + kKS - 1) / kKS * kKS;
+    if (kc < kKS) kc = kKS;
+    const int64_t real = (K + kc - 1) / kc;
+    const int64_t waves = (nrb * real + G - 1) / G;
+    const double cost = (double)waves * ((double)kc + 96.0) + 0.25 * (double)real;
+    if (cost < best) {
+      best = cost;
+      bk = ks;
+    }
+    if (nrb * ks > 8 * (int64_t)G) break;
+  }
+  int64_t kc = ((K + bk - 1) / bk + kKS - 1) / kKS * kKS;
+  if (kc < kKS) kc = kKS;
+  *kchunk = kc;
+  *ksplit = (int)std::max<int64_t>(1, (K + kc - 1) / kc);
+}
+
+struct Plan {
+  int grid = 0, ksA = 1, ksB = 1;
+  int64_t kcA = 0, kcB = 0;
+  size_t smem = 0;
+  const void* fn = nullptr;
+};
+
+template <int CPL, int RC>
+bool make_plan_t(int64_t m, int64_t n, Plan* p) {
+  auto k = small_hals_kernel<CPL, RC>;
+  const size_t sm = smem_bytes<CPL, RC>();
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kT, sm) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  if (occ > 2) occ = 2;
+  int dev = 0, sms = kSMs;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int gmax = occ * sms;
+  choose_split(m, n, gmax, &p->ksA, &p->kcA);
+  choose_split(n, m, gmax, &p->ksB, &p->kcB);
+  const int64_t tilesA = (m + kTM - 1) / kTM * p->ksA, tilesB = (n + kTM - 1) / kTM * p->ksB;
+  const int64_t hu = ((m + kRB - 1) / kRB + kW - 1) / kW, hv = ((n + kRB - 1) / kRB + kW - 1) / kW;
+  const int64_t want = std::max(std::max(tilesA, tilesB), std::max(hu, hv));
+  p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(gmax, want));
+  p->smem = sm;
+  p->fn = reinterpret_cast<const void*>(k);
+  return true;
+}
+
+bool make_plan(int64_t m, int64_t n, int r, Plan* p) {
+  if (r <= 16) return make_plan_t<1, 1>(m, n, p);
+  if (r <= 32) return make_plan_t<1, 2>(m, n, p);
+  if (r <= 64) return make_plan_t<2, 4>(m, n, p);
+  if (r <= 96) return make_plan_t<3, 8>(m, n, p);
+  if (r <= 128) return make_plan_t<4, 8>(m, n, p);
+  return false;
+}
+
+}  // namespace
+
+bool small_sweeps_supported(int64_t m, int64_t n, int r) {
+  // cache-resident problems (C1-C4, X <= 90 MB); larger ones are bound by the X
+  // passes, which have their own kernels
+  return r >= 1 && r <= 128 && m >= 1 && n >= 1 && m * n <= (int64_t)64 * 1024 * 1024;
+}
+
+size_t small_sweeps_workspace(int64_t m, int64_t n, int r) {
+  Plan p;
+  if (!make_plan(m, n, r, &p)) return 0;
+  const size_t pp = (size_t)std::max(p.ksA * m, p.ksB * n) * r;
+  return pp + (size_t)p.grid * r * r + 2 * (size_t)p.grid + 8;
+}
+
+int small_sweeps_launch(const float* X, int64_t ldx, int64_t m, int64_t n, int r, float* U,
+                        int64_t ldu, float* V, int64_t ldv, double* GV, double* GU,
+                        const double* xnorm2, double* ftrace, int* fcnt, double* minu,
+                        double* minv, int* stage, int* cnt_hals, double* ws, int count,
+                        cudaStream_t st) {
+  if (count <= 0) return 0;
+  Plan p;
+  if (!make_plan(m, n, r, &p)) return 1;
+  SmallArgs a;
+  a.X = X; a.ldx = ldx; a.m = m; a.n = n; a.r = r;
+  a.U = U; a.ldu = ldu; a.V = V; a.ldv = ldv;
+  a.GV = GV; a.GU = GU; a.xnorm2 = xnorm2; a.ftrace = ftrace; a.fcnt = fcnt;
+  a.minu = minu; a.minv = minv; a.stage = stage; a.cnt_hals = cnt_hals;
+  a.pp = ws;
+  a.gp = ws + (size_t)std::max(p.ksA * m, p.ksB * n) * r;
+  a.sc = a.gp + (size_t)p.grid * r * r;
+  a.ksA = p.ksA; a.ksB = p.ksB; a.kcA = p.kcA; a.kcB = p.kcB;
+  a.count = count;
+  void* args[] = {&a};
+  if (cudaLaunchCooperativeKernel(p.fn, dim3(p.grid), dim3(kT), args, p.smem, st) != cudaSuccess)
+    return 1;
+  count_launch();
+  return 0;
+}
+
+}  // namespace enmf
