@@ -64,6 +64,7 @@ __device__ __forceinline__ void row_times_gram(const double (&S)[RB][CPL], const
 template <int CPL>
 __device__ __forceinline__ void load_gram(const double* G, int r, double* Gs) {
   constexpr int RP = 32 * CPL;
+#pragma unroll 8                              // eight loads in flight per thread
   for (int e = threadIdx.x; e < RP * RP; e += blockDim.x) {
     const int l = e / RP, j = e % RP;
     Gs[e] = (l < r && j < r) ? G[l * r + j] : 0.0;

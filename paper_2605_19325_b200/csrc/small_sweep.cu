@@ -17,15 +17,14 @@
 // All arithmetic is fp64 on the fp32 state (the ENMF_PREC_FP64 path); every sum has a fixed
 // order given the grid, so results are deterministic.  The grid is sized to the problem (a
 // barrier over 8 CTAs is cheaper than over 296).  Single rank, dense X, HALS stage only.
-#include <cooperative_groups.h>
 #include <float.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
 #include "internal.h"
 #include "rows_dev.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace enmf {
 namespace {
@@ -35,7 +34,7 @@ using namespace rows_dev;
 constexpr int kT = 256;     // threads per CTA
 constexpr int kW = kT / 32;
 constexpr int kTM = 64;     // output rows of a product tile
-constexpr int kKS = 16;     // K slab
+constexpr int kKS = 32;     // K slab
 constexpr int kXP = kTM + 2;   // padded slab row (doubles; 16-byte aligned rows)
 constexpr int kRB = 4;      // rows per warp in the HALS phases
 
@@ -61,117 +60,197 @@ struct SmallArgs {
   double* sc;        // scalar partials: cross[grid], min[grid], then 2 reduced scalars
   int ksA, ksB;
   int64_t kcA, kcB;  // K chunk of a tile
+  unsigned* bar;     // grid barrier counter (zeroed before the launch)
   int count;
+  int debug;         // ENMF_SMALL_DEBUG=1: CTA 0 prints the last sweep's phase times
 };
 
 // ---------------------------------------------------------------------------------------------
-// One product tile: out[(row - r0)][c] = sum_{k in [k0, k1)} op(X)[row][k] F[k][c] for the 64
-// output rows r0.. (rows of X if !TRANS, columns of X if TRANS) and all r columns.  Thread
-// (ty, tx) owns output rows 4 ty .. 4 ty + 3 and columns 2 tx + (b & 1) + 32 (b >> 1)
-// (RC = 1: column tx), so both operands are read from shared memory as 16-byte loads.
-template <int RC, bool TRANS>
+// One product tile: out[row][c] = sum_{k in [k0, k1)} op(X)[row][k] F[k][c] for the 64 output
+// rows r0.. (rows of X if !TRANS, columns of X if TRANS) and all r <= RCOLS columns.
+// The CTA's 256 threads form NG = 64 / RCOLS groups (1 for RCOLS = 128); a group covers the
+// whole 64 x RCOLS tile with a 4 x TC register tile per thread (TC = 4, or 8 at RCOLS = 128:
+// 4 TC DFMA per 2 + TC/2 shared-memory loads of 16 bytes, so the fp64 pipe, not shared memory,
+// is the bound, in few enough registers for two CTAs per SM) and takes every NG-th k of a
+// slab; the groups' sums are added in group order through shared memory at the end.
+// Thread (ty, tx) of a group owns rows 32 (a >> 1) + 2 ty + (a & 1), a < 4, and columns
+// 2 tx + (b & 1) + 2 TXN (b >> 1), b < TC, so that a warp's 16-byte loads are contiguous.
+template <int RCOLS, bool TRANS>
 __device__ __forceinline__ void product_tile(const float* __restrict__ X, int64_t ldx, int64_t M,
-                                             int64_t K, const float* F, int64_t ldf, int r,
-                                             int64_t r0, int64_t k0, int64_t k1, double* out,
-                                             double* Xs, double* Fs) {
-  constexpr int RCOLS = 16 * RC;
-  constexpr int XQ = kTM * kKS / kT;       // X elements per thread and slab (4)
-  constexpr int FQ = RCOLS * kKS / kT;     // factor elements per thread and slab (RC)
-  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
-  double acc[4][RC];
+                                             const float* F, int64_t ldf, int r, int64_t r0,
+                                             int64_t k0, int64_t k1, double* out, double* Xs,
+                                             double* Fs, float* St) {
+  constexpr int TC = RCOLS == 128 ? 8 : 4; // columns per thread
+  constexpr int TXN = RCOLS / TC;          // threads across the columns
+  constexpr int GT = 16 * TXN;             // threads per group
+  constexpr int NG = kT / GT;              // k groups
+  constexpr int XQ = kTM * kKS / kT;       // X elements per thread and slab (8)
+  constexpr int FQ = RCOLS * kKS / kT;     // factor elements per thread and slab (RCOLS / 8)
+  const int t = threadIdx.x;
+  const int g = t / GT, w = t % GT, tx = w % TXN, ty = w / TXN;
+  double acc[4][TC];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < RC; ++b) acc[a][b] = 0.0;
-  float xr[XQ], fr[FQ];
-  auto fetch = [&](int64_t ks) {
+    for (int b = 0; b < TC; ++b) acc[a][b] = 0.0;
+  // Per-thread element maps of a slab (e = t + 256 q):
+  //   X, !TRANS: row t/16 + 16 (q%4), k t%16 + 16 (q/4)  (a warp reads 2 rows x 64 bytes and
+  //              stores 16 k x 2 rows: conflict free);  TRANS: k t/64 + 4 q, row t%64;
+  //   F: k t/RCOLS + (256/RCOLS) q, column t%RCOLS.
+  // Slabs arrive as fp32 through cp.async into a two-deep staging ring (no registers held, two
+  // slabs of FMAs to cover the L2 / HBM latency); every thread converts the elements it
+  // requested itself into the fp64 slab the FMAs read.
+  const int xi = TRANS ? t % kTM : t / 16, xk = TRANS ? t / kTM : t % 16;
+  const float* xp = TRANS ? X + (k0 + xk) * ldx + r0 + xi : X + (r0 + xi) * ldx + k0 + xk;
+  const int64_t xrows = M - r0 - xi;             // rows left from this thread's first row
+  constexpr int FK = kT / RCOLS;
+  const int fc = t % RCOLS, fk = t / RCOLS;
+  const float* fp = F + (k0 + fk) * ldf + fc;
+  const bool fok = fc < r;
+  constexpr int SLAB32 = kTM * kKS + RCOLS * kKS;      // floats per staged slab
+  const unsigned st_base = (unsigned)__cvta_generic_to_shared(St) + 4u * t;
+  auto request = [&](int64_t ks, int buf) {
+    const int64_t kleft = k1 - ks;               // valid k of this slab: kk < kleft
+    const unsigned dst = st_base + 4u * SLAB32 * buf;
 #pragma unroll
     for (int q = 0; q < XQ; ++q) {
-      const int e = t + kT * q;
-      int ii, kk;
-      if (TRANS) { kk = e / kTM; ii = e % kTM; }
-      else { ii = e / kKS; kk = e % kKS; }
-      const int64_t gi = r0 + ii, gk = ks + kk;
-      float v = 0.f;
-      if (gi < M && gk < k1) v = TRANS ? X[gk * ldx + gi] : X[gi * ldx + gk];
-      xr[q] = v;
-    }
-#pragma unroll
-    for (int q = 0; q < FQ; ++q) {
-      const int e = t + kT * q;
-      const int kk = e / RCOLS, c = e % RCOLS;
-      const int64_t gk = ks + kk;
-      fr[q] = (c < r && gk < k1) ? F[gk * ldf + c] : 0.f;
-    }
-  };
-  auto stash = [&]() {
-#pragma unroll
-    for (int q = 0; q < XQ; ++q) {
-      const int e = t + kT * q;
-      int ii, kk;
-      if (TRANS) { kk = e / kTM; ii = e % kTM; }
-      else { ii = e / kKS; kk = e % kKS; }
-      Xs[kk * kXP + ii] = (double)xr[q];
-    }
-#pragma unroll
-    for (int q = 0; q < FQ; ++q) {
-      const int e = t + kT * q;
-      Fs[e] = (double)fr[q];               // Fs[kk][c], kk = e / RCOLS
-    }
-  };
-  fetch(k0);
-  for (int64_t ks = k0; ks < k1; ks += kKS) {
-    __syncthreads();                       // the previous slab's reads are done
-    stash();
-    __syncthreads();
-    if (ks + kKS < k1) fetch(ks + kKS);    // next slab's loads in flight during the FMAs
-#pragma unroll
-    for (int kk = 0; kk < kKS; ++kk) {
-      const double2 x01 = *reinterpret_cast<const double2*>(Xs + kk * kXP + 4 * ty);
-      const double2 x23 = *reinterpret_cast<const double2*>(Xs + kk * kXP + 4 * ty + 2);
-      const double xv[4] = {x01.x, x01.y, x23.x, x23.y};
-      double fv[RC];
-      if (RC == 1) {
-        fv[0] = Fs[kk * RCOLS + tx];
+      bool ok;
+      const float* src;
+      if (TRANS) {
+        ok = xrows > 0 && xk + 4 * q < kleft;
+        src = xp + (int64_t)(4 * q) * ldx;
       } else {
+        ok = 16 * (q % 4) < xrows && xk + 16 * (q / 4) < kleft;
+        src = xp + (int64_t)(16 * (q % 4)) * ldx + 16 * (q / 4);
+      }
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst + 4u * kT * q),
+                   "l"(ok ? src : X), "r"(ok ? 4 : 0));
+    }
 #pragma unroll
-        for (int b = 0; b < RC; b += 2) {
-          const double2 f2 = *reinterpret_cast<const double2*>(Fs + kk * RCOLS + 2 * tx + 16 * b);
-          fv[b] = f2.x;
-          fv[b + 1] = f2.y;
-        }
+    for (int q = 0; q < FQ; ++q) {
+      const bool ok = fok && fk + FK * q < kleft;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst + 4u * kT * (XQ + q)),
+                   "l"(ok ? fp + (int64_t)(FK * q) * ldf : F), "r"(ok ? 4 : 0));
+    }
+    xp += TRANS ? (int64_t)kKS * ldx : kKS;
+    fp += (int64_t)kKS * ldf;
+  };
+  auto convert = [&](int buf) {
+    const float* src = St + SLAB32 * buf + t;
+#pragma unroll
+    for (int q = 0; q < XQ; ++q) {
+      const int kk = TRANS ? xk + 4 * q : xk + 16 * (q / 4);
+      const int ii = TRANS ? xi : xi + 16 * (q % 4);
+      Xs[kk * kXP + ii] = (double)src[kT * q];
+    }
+#pragma unroll
+    for (int q = 0; q < FQ; ++q) Fs[t + kT * q] = (double)src[kT * (XQ + q)];   // Fs[kk][c]
+  };
+  request(k0, 0);
+  asm volatile("cp.async.commit_group;");
+  if (k0 + kKS < k1) request(k0 + kKS, 1);
+  asm volatile("cp.async.commit_group;");
+  int buf = 0;
+  for (int64_t ks = k0; ks < k1; ks += kKS, buf ^= 1) {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");   // this thread's requests of slab ks
+    __syncthreads();                       // the previous slab's FMAs are done with Xs / Fs
+    convert(buf);
+    __syncthreads();
+    if (ks + 2 * kKS < k1) request(ks + 2 * kKS, buf);
+    asm volatile("cp.async.commit_group;");
+#pragma unroll
+    for (int kq = 0; kq < kKS / NG; ++kq) {
+      const int kk = kq * NG + g;
+      double xv[4], fv[TC];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const double2 x2 = *reinterpret_cast<const double2*>(Xs + kk * kXP + 32 * j + 2 * ty);
+        xv[2 * j] = x2.x;
+        xv[2 * j + 1] = x2.y;
+      }
+#pragma unroll
+      for (int j = 0; j < TC / 2; ++j) {
+        const double2 f2 =
+            *reinterpret_cast<const double2*>(Fs + kk * RCOLS + 2 * tx + 2 * TXN * j);
+        fv[2 * j] = f2.x;
+        fv[2 * j + 1] = f2.y;
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < RC; ++b) acc[a][b] = fma(xv[a], fv[b], acc[a][b]);
+        for (int b = 0; b < TC; ++b) acc[a][b] = fma(xv[a], fv[b], acc[a][b]);
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  // groups 1 .. NG-1 hand their sums to group 0 through shared memory (over the slabs)
+  constexpr int NA = 4 * TC;
+  if (NG > 1) {
+    double* red = Xs;                      // (NG - 1) x NA x GT doubles
+    __syncthreads();
+    if (g > 0) {
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int64_t row = r0 + 4 * ty + a;
-    if (row >= M) continue;
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < RC; ++b) {
-      const int c = RC == 1 ? tx : 2 * tx + (b & 1) + 32 * (b >> 1);
-      if (c < r) out[row * r + c] = acc[a][b];
+        for (int b = 0; b < TC; ++b) red[((g - 1) * NA + a * TC + b) * GT + w] = acc[a][b];
+    }
+    __syncthreads();
+    if (g == 0) {
+      for (int gg = 0; gg < NG - 1; ++gg)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < TC; ++b) acc[a][b] += red[(gg * NA + a * TC + b) * GT + w];
     }
   }
+  if (g == 0) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int64_t row = r0 + 32 * (a >> 1) + 2 * ty + (a & 1);
+      if (row >= M) continue;
+#pragma unroll
+      for (int b = 0; b < TC; ++b) {
+        const int c = 2 * tx + (b & 1) + 2 * TXN * (b >> 1);
+        if (c < r) out[row * r + c] = acc[a][b];
+      }
+    }
+  }
+  __syncthreads();                         // the next tile's stash overwrites red
 }
 
 // All tiles of one pass: tile = (row block, K chunk); partial of chunk q at pp[q M r ...].
-template <int RC, bool TRANS>
+template <int RCOLS, bool TRANS>
 __device__ __forceinline__ void product_pass(const float* __restrict__ X, int64_t ldx, int64_t M,
                                              int64_t K, const float* F, int64_t ldf, int r,
                                              int ksplit, int64_t kchunk, double* pp, double* Xs,
-                                             double* Fs) {
+                                             double* Fs, float* St) {
   const int64_t nrb = (M + kTM - 1) / kTM;
   const int64_t tiles = nrb * ksplit;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t rb = tile % nrb, q = tile / nrb;
     const int64_t k0 = q * kchunk, k1 = K < k0 + kchunk ? K : k0 + kchunk;
-    product_tile<RC, TRANS>(X, ldx, M, K, F, ldf, r, rb * kTM, k0, k1, pp + q * M * r, Xs, Fs);
+    product_tile<RCOLS, TRANS>(X, ldx, M, F, ldf, r, rb * kTM, k0, k1, pp + q * M * r, Xs, Fs, St);
   }
+}
+
+// Grid barrier (all CTAs co-resident: cooperative launch).  One thread per CTA arrives on a
+// monotonically increasing counter and polls it with a back-off: with cg::grid_group::sync the
+// ~200 waiting CTAs of a phase that only a dozen CTAs work in poll one L2 line without pause,
+// and the working CTAs' loads queue behind them (measured: ~2 us per dependent L2 round trip).
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    target += gridDim.x;
+    __threadfence();                                   // release this CTA's writes
+    atomicAdd(bar, 1u);
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if ((int)(v - target) >= 0) break;
+      __nanosleep(200);
+    }
+    __threadfence();                                   // acquire; invalidates this SM's L1
+  }
+  __syncthreads();
 }
 
 // G (r x r) = sum over the first nparts per-CTA partials, one entry per warp at a time: the
@@ -188,7 +267,7 @@ __device__ __forceinline__ void reduce_gram(const double* gp, int nparts, int r,
   }
 }
 
-// CTA 0, warp 0: out = sum (or min) of n partials
+// one warp (of the last CTA, the least likely to own HALS rows): sum (or min) of n partials
 __device__ __forceinline__ double reduce_scalar(const double* parts, int n, bool is_min) {
   const int lane = threadIdx.x & 31;
   double s = is_min ? DBL_MAX : 0.0;
@@ -204,8 +283,13 @@ template <int CPL>
 __device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, int r,
                                            const double* pp, int ksplit, const double* G,
                                            double* gpart, double* crosspart, double* minpart,
-                                           double* Gs, double* Ss, double* ginv, double* red) {
+                                           double* Gs, double* Ss, double* ginv, double* red,
+                                           unsigned long long* dbg) {
   constexpr int RP = 32 * CPL;
+  auto hstamp = [&](int i) {               // ENMF_SMALL_DEBUG: phase-internal times of CTA 0
+    if (dbg && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg[i]));
+  };
+  hstamp(0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nblk = (rows + kRB - 1) / kRB;
   const bool cta_active = (int64_t)blockIdx.x * kW < nblk;
@@ -217,11 +301,42 @@ __device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, 
       ginv[k] = gkk > 0.0 ? 1.0 / gkk : 0.0;
     }
     __syncthreads();
+    hstamp(1);
     double* Sw = Ss + warp * kRB * RP;
+    double* Cw = Ss + (kW + warp) * kRB * RP;      // this warp's C rows
     bool first = true;
     for (int64_t base = (int64_t)blockIdx.x * kW; base < nblk; base += (int64_t)gridDim.x * kW) {
       const int64_t rb = base + warp;
-      double u[kRB][CPL], t[kRB][CPL], c0[kRB][CPL];
+      double u[kRB][CPL], t[kRB][CPL];
+      // C rows of this warp: kRB consecutive rows are ONE contiguous span of cnt = rows * r
+      // doubles in every K-chunk partial, so the lanes sum it flat (coalesced, 4 CPL loads in
+      // flight per chunk, chunk order fixed) and scatter the sums into the warp's Cw[b][col]
+      {
+        const int64_t row0 = rb * kRB;
+        const int64_t left = rb < nblk ? rows - row0 : 0;
+        const int cnt = (int)(left < kRB ? left : kRB) * r;
+        const double* src = pp + row0 * r + lane;
+        const int64_t stride = rows * (int64_t)r;
+        double sacc[kRB * CPL];
+#pragma unroll
+        for (int j = 0; j < kRB * CPL; ++j) sacc[j] = 0.0;
+#pragma unroll 4
+        for (int q = 0; q < ksplit; ++q) {
+          double pv[kRB * CPL];
+#pragma unroll
+          for (int j = 0; j < kRB * CPL; ++j)
+            pv[j] = lane + 32 * j < cnt ? __ldcg(src + q * stride + 32 * j) : 0.0;
+#pragma unroll
+          for (int j = 0; j < kRB * CPL; ++j) sacc[j] += pv[j];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kRB * CPL; ++j) {
+          const int idx = lane + 32 * j;
+          if (idx < cnt) Cw[(idx / r) * RP + idx % r] = sacc[j];
+        }
+        __syncwarp();
+      }
 #pragma unroll
       for (int b = 0; b < kRB; ++b)
 #pragma unroll
@@ -230,13 +345,11 @@ __device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, 
           const int col = lane + 32 * c;
           const bool ok = rb < nblk && row < rows && col < r;
           u[b][c] = ok ? (double)F[row * ldf + col] : 0.0;
-          double s = 0.0;
-          if (ok)
-            for (int q = 0; q < ksplit; ++q) s += pp[((int64_t)q * rows + row) * r + col];
-          t[b][c] = s;
-          c0[b][c] = s;
+          t[b][c] = ok ? Cw[b * RP + col] : 0.0;
         }
+      hstamp(2);
       row_times_gram<CPL, kRB>(u, Gs, Sw, r, lane, -1.0, t);      // t = C - u G
+      hstamp(3);
 #pragma unroll
       for (int s = 0; s < CPL; ++s) {
         const int kmax = r - 32 * s < 32 ? r - 32 * s : 32;
@@ -250,16 +363,21 @@ __device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, 
 #pragma unroll
           for (int b = 0; b < kRB; ++b) {
             // lane kk owns (u_k, t_k); its change d is broadcast and the residual follows
+            // (the change d = t / G_kk or -u_k is formed beside v, not from nu - u_k: two
+            // fp64 latencies on the serial chain instead of four)
             const double uo = u[b][s];
+            const double p = t[b][s] * ig;
             const double v = fma(t[b][s], ig, uo);
-            const double nu = v > 0.0 ? v : 0.0;
-            if (lane == kk) u[b][s] = nu;
-            const double d = __shfl_sync(FULL, nu - uo, kk);
+            const bool pos = v > 0.0;
+            if (lane == kk) u[b][s] = pos ? v : 0.0;
+            const double d = __shfl_sync(FULL, pos ? p : -uo, kk);
+            // (integer-pipe selects on the high words were tried: 2.5x slower, measured)
 #pragma unroll
             for (int c = 0; c < CPL; ++c) t[b][c] = fma(-d, gk[c], t[b][c]);
           }
         }
       }
+      hstamp(4);
       // write the rows (fp32: the state), keep their rounded values for the Gram partial
       __syncwarp();
 #pragma unroll
@@ -274,11 +392,12 @@ __device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, 
             F[row * ldf + col] = v;
             w = (double)v;
             wmin = fmin(wmin, w);
-            wcross = fma(c0[b][c], w, wcross);
+            wcross = fma(Cw[b * RP + col], w, wcross);
           }
           Sw[b * RP + col] = w;
         }
       __syncthreads();
+      hstamp(5);
       // partial Gram of this round's kW * kRB rows: 4 x 4 blocks of the upper block triangle
       {
         const int nb4 = (r + 3) / 4;
@@ -320,6 +439,7 @@ __device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, 
       }
       first = false;
       __syncthreads();
+      hstamp(6);
     }
   }
   // per-CTA scalars (every CTA writes: the reductions read all gridDim slots)
@@ -340,9 +460,10 @@ __device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, 
     if (crosspart) crosspart[blockIdx.x] = cr;
   }
   __syncthreads();
+  hstamp(7);
 }
 
-// f = ||X||^2 - 2 <Q, V> + <G_U, G_V> (CTA 0), appended to the trace
+// f = ||X||^2 - 2 <Q, V> + <G_U, G_V> (one CTA: the last), appended to the trace
 __device__ __forceinline__ void objective_append(const SmallArgs& a, double cross, double* red) {
   const int nn = a.r * a.r;
   double s = 0.0;
@@ -358,18 +479,24 @@ __device__ __forceinline__ void objective_append(const SmallArgs& a, double cros
   __syncthreads();
 }
 
-template <int CPL, int RC>
-__global__ void __launch_bounds__(kT) small_hals_kernel(SmallArgs a) {
+template <int CPL, int RCOLS>
+__global__ void __launch_bounds__(kT, CPL <= 2 ? 2 : 1) small_hals_kernel(SmallArgs a) {
   constexpr int RP = 32 * CPL;
   extern __shared__ double smem[];
   // product phases: Xs (kKS x kXP) + Fs (kKS x RCOLS); HALS phases: Gs (RP^2) + Ss + ginv
   double* Xs = smem;
   double* Fs = smem + kKS * kXP;
+  constexpr int NGK = RCOLS == 128 ? 1 : 64 / RCOLS;
+  constexpr int PRODD = (kKS * kXP + kKS * RCOLS) > (NGK - 1) * kTM * RCOLS
+                            ? (kKS * kXP + kKS * RCOLS) : (NGK - 1) * kTM * RCOLS;
+  float* St = reinterpret_cast<float*>(smem + PRODD);   // 2 staged fp32 slabs
   double* Gs = smem;
   double* Ss = smem + RP * RP;
-  double* ginv = Ss + kW * kRB * RP;
+  double* ginv = Ss + 2 * kW * kRB * RP;
   __shared__ double red[2 * kW];
-  cg::grid_group grid = cg::this_grid();
+  unsigned bar_target = 0;
+  unsigned* bar = a.bar;
+  auto grid_sync = [&]() { grid_barrier(bar, bar_target); };
   const int G = (int)gridDim.x;
   const int r = a.r;
   const int64_t nblkU = (a.m + kRB - 1) / kRB, nblkV = (a.n + kRB - 1) / kRB;
@@ -379,11 +506,24 @@ __global__ void __launch_bounds__(kT) small_hals_kernel(SmallArgs a) {
   double* crossp = a.sc;
   double* minp = a.sc + G;
   double* scal = a.sc + 2 * G;               // [0] cross, [1] min U, [2] min V
+  unsigned long long tl[6] = {0, 0, 0, 0, 0, 0}, hu[8] = {0}, hv[8] = {0};
+  const bool dbg0 = a.debug && blockIdx.x == 0;
+  auto stamp = [&](int i) {
+    if (a.debug && blockIdx.x == 0 && threadIdx.x == 0)
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl[i]));
+  };
+  unsigned long long gt0 = 0;
+  long long ck0 = 0;
+  if (dbg0 && threadIdx.x == 0) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+    ck0 = clock64();
+  }
   for (int t = 0; t < a.count; ++t) {
+    stamp(0);
     // ---- A: (G_V, <Q, V>, min V of the previous sweep;) partial products of P = X V
     if (t > 0) {
       reduce_gram(a.gp, actV, r, a.GV);
-      if (blockIdx.x == 0 && threadIdx.x < 32) {
+      if (blockIdx.x == gridDim.x - 1 && threadIdx.x < 32) {
         const double cr = reduce_scalar(crossp, G, false);
         const double mv = reduce_scalar(minp, G, true);
         if (threadIdx.x == 0) {
@@ -392,29 +532,50 @@ __global__ void __launch_bounds__(kT) small_hals_kernel(SmallArgs a) {
         }
       }
     }
-    product_pass<RC, false>(a.X, a.ldx, a.m, a.n, a.V, a.ldv, r, a.ksA, a.kcA, a.pp, Xs, Fs);
-    grid.sync();
+    product_pass<RCOLS, false>(a.X, a.ldx, a.m, a.n, a.V, a.ldv, r, a.ksA, a.kcA, a.pp, Xs, Fs, St);
+    stamp(5);
+    grid_sync();
+    stamp(1);
     // ---- A': (objective of the previous sweep;) HALS on U
-    if (t > 0 && blockIdx.x == 0) objective_append(a, scal[0], red);
+    if (t > 0 && blockIdx.x == gridDim.x - 1) objective_append(a, scal[0], red);
     hals_phase<CPL>(a.U, a.ldu, a.m, r, a.pp, a.ksA, a.GV, a.gp + (int64_t)blockIdx.x * r * r,
-                    nullptr, minp, Gs, Ss, ginv, red);
-    grid.sync();
+                    nullptr, minp, Gs, Ss, ginv, red, dbg0 ? hu : nullptr);
+    grid_sync();
+    stamp(2);
     // ---- B: G_U, min U; partial products of Q = X^T U
     reduce_gram(a.gp, actU, r, a.GU);
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < 32) {
       const double mu = reduce_scalar(minp, G, true);
       if (threadIdx.x == 0) scal[1] = mu;
     }
-    product_pass<RC, true>(a.X, a.ldx, a.n, a.m, a.U, a.ldu, r, a.ksB, a.kcB, a.pp, Xs, Fs);
-    grid.sync();
+    product_pass<RCOLS, true>(a.X, a.ldx, a.n, a.m, a.U, a.ldu, r, a.ksB, a.kcB, a.pp, Xs, Fs, St);
+    grid_sync();
+    stamp(3);
     // ---- B': HALS on V with the cross-term partial <Q, V_new>
     hals_phase<CPL>(a.V, a.ldv, a.n, r, a.pp, a.ksB, a.GU, a.gp + (int64_t)blockIdx.x * r * r,
-                    crossp, minp, Gs, Ss, ginv, red);
-    grid.sync();
+                    crossp, minp, Gs, Ss, ginv, red, dbg0 ? hv : nullptr);
+    grid_sync();
+    stamp(4);
   }
+  if (a.debug && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long gt1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+    printf("  SM clock %.0f MHz over %d sweeps\n", 1e3 * (double)(clock64() - ck0) / (double)(gt1 - gt0),
+           a.count);
+  }
+  if (a.debug && blockIdx.x == 0 && threadIdx.x == 0)
+    printf("small_hals grid %d ksA %d kcA %d ksB %d kcB %d: A %llu (own work %llu) A' %llu B %llu B' %llu ns\n",
+           G, a.ksA, (int)a.kcA, a.ksB, (int)a.kcB, tl[1] - tl[0], tl[5] - tl[0], tl[2] - tl[1],
+           tl[3] - tl[2], tl[4] - tl[3]);
+  if (a.debug && blockIdx.x == 0 && threadIdx.x == 0)
+    printf("  CTA 0 HALS U: gram %llu partials %llu uG %llu sweep %llu write %llu Gpart %llu tail %llu | "
+           "V: gram %llu partials %llu uG %llu sweep %llu write %llu Gpart %llu tail %llu ns\n",
+           hu[1] - hu[0], hu[2] - hu[1], hu[3] - hu[2], hu[4] - hu[3], hu[5] - hu[4], hu[6] - hu[5],
+           hu[7] - hu[6], hv[1] - hv[0], hv[2] - hv[1], hv[3] - hv[2], hv[4] - hv[3], hv[5] - hv[4],
+           hv[6] - hv[5], hv[7] - hv[6]);
   // ---- tail: G_V, <Q, V>, min V of the last sweep, its objective, the handle's scalars
   reduce_gram(a.gp, actV, r, a.GV);
-  if (blockIdx.x == 0 && threadIdx.x < 32) {
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x < 32) {
     const double cr = reduce_scalar(crossp, G, false);
     const double mv = reduce_scalar(minp, G, true);
     if (threadIdx.x == 0) {
@@ -422,8 +583,8 @@ __global__ void __launch_bounds__(kT) small_hals_kernel(SmallArgs a) {
       scal[2] = mv;
     }
   }
-  grid.sync();
-  if (blockIdx.x == 0) {
+  grid_sync();
+  if (blockIdx.x == gridDim.x - 1) {
     objective_append(a, scal[0], red);
     if (threadIdx.x == 0) {
       *a.minu = scal[1];
@@ -434,11 +595,14 @@ __global__ void __launch_bounds__(kT) small_hals_kernel(SmallArgs a) {
   }
 }
 
-template <int CPL, int RC>
+template <int CPL, int RCOLS>
 size_t smem_bytes() {
   constexpr int RP = 32 * CPL;
-  const size_t prod = (size_t)(kKS * kXP + kKS * 16 * RC);
-  const size_t hals = (size_t)(RP * RP + kW * kRB * RP + RP);
+  constexpr int NG = RCOLS == 128 ? 1 : 64 / RCOLS;
+  const size_t slabs = (size_t)(kKS * kXP + kKS * RCOLS);
+  const size_t gred = (size_t)(NG - 1) * kTM * RCOLS;          // group sums (over the slabs)
+  const size_t prod = std::max(slabs, gred) + (size_t)(kTM * kKS + RCOLS * kKS);   // + staging
+  const size_t hals = (size_t)(RP * RP + 2 * kW * kRB * RP + RP);
   return sizeof(double) * std::max(prod, hals);
 }
 
@@ -454,7 +618,8 @@ void choose_split(int64_t M, int64_t K, int G, int* ksplit, int64_t* kchunk) {
     if (kc < kKS) kc = kKS;
     const int64_t real = (K + kc - 1) / kc;
     const int64_t waves = (nrb * real + G - 1) / G;
-    const double cost = (double)waves * ((double)kc + 96.0) + 0.25 * (double)real;
+    // (+ ~0.25 us per chunk in the row phase that sums the chunk partials: ~8 k of FMAs)
+    const double cost = (double)waves * ((double)kc + 96.0) + 8.0 * (double)real;
     if (cost < best) {
       best = cost;
       bk = ks;
@@ -474,10 +639,10 @@ struct Plan {
   const void* fn = nullptr;
 };
 
-template <int CPL, int RC>
+template <int CPL, int RCOLS>
 bool make_plan_t(int64_t m, int64_t n, Plan* p) {
-  auto k = small_hals_kernel<CPL, RC>;
-  const size_t sm = smem_bytes<CPL, RC>();
+  auto k = small_hals_kernel<CPL, RCOLS>;
+  const size_t sm = smem_bytes<CPL, RCOLS>();
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
     cudaGetLastError();
     return false;
@@ -504,11 +669,11 @@ bool make_plan_t(int64_t m, int64_t n, Plan* p) {
 }
 
 bool make_plan(int64_t m, int64_t n, int r, Plan* p) {
-  if (r <= 16) return make_plan_t<1, 1>(m, n, p);
-  if (r <= 32) return make_plan_t<1, 2>(m, n, p);
-  if (r <= 64) return make_plan_t<2, 4>(m, n, p);
-  if (r <= 96) return make_plan_t<3, 8>(m, n, p);
-  if (r <= 128) return make_plan_t<4, 8>(m, n, p);
+  if (r <= 16) return make_plan_t<1, 16>(m, n, p);
+  if (r <= 32) return make_plan_t<1, 32>(m, n, p);
+  if (r <= 64) return make_plan_t<2, 64>(m, n, p);
+  if (r <= 96) return make_plan_t<3, 128>(m, n, p);
+  if (r <= 128) return make_plan_t<4, 128>(m, n, p);
   return false;
 }
 
@@ -524,7 +689,7 @@ size_t small_sweeps_workspace(int64_t m, int64_t n, int r) {
   Plan p;
   if (!make_plan(m, n, r, &p)) return 0;
   const size_t pp = (size_t)std::max(p.ksA * m, p.ksB * n) * r;
-  return pp + (size_t)p.grid * r * r + 2 * (size_t)p.grid + 8;
+  return pp + (size_t)p.grid * r * r + 2 * (size_t)p.grid + 8 + 16;
 }
 
 int small_sweeps_launch(const float* X, int64_t ldx, int64_t m, int64_t n, int r, float* U,
@@ -543,8 +708,12 @@ int small_sweeps_launch(const float* X, int64_t ldx, int64_t m, int64_t n, int r
   a.pp = ws;
   a.gp = ws + (size_t)std::max(p.ksA * m, p.ksB * n) * r;
   a.sc = a.gp + (size_t)p.grid * r * r;
+  a.bar = reinterpret_cast<unsigned*>(a.sc + 2 * (size_t)p.grid + 8);
+  if (cudaMemsetAsync(a.bar, 0, 16 * sizeof(double), st) != cudaSuccess) return 1;
   a.ksA = p.ksA; a.ksB = p.ksB; a.kcA = p.kcA; a.kcB = p.kcB;
   a.count = count;
+  const char* dbg = getenv("ENMF_SMALL_DEBUG");
+  a.debug = dbg && dbg[0] == '1';
   void* args[] = {&a};
   if (cudaLaunchCooperativeKernel(p.fn, dim3(p.grid), dim3(kT), args, p.smem, st) != cudaSuccess)
     return 1;
