@@ -35,7 +35,7 @@ constexpr int kT = 256;     // threads per CTA
 constexpr int kW = kT / 32;
 constexpr int kTM = 64;     // output rows of a product tile
 constexpr int kKS = 32;     // K slab
-constexpr int kXP = kTM + 2;   // padded slab row (doubles; 16-byte aligned rows)
+constexpr int kXP = kTM + 4;   // padded slab row: the DMMA A-fragment loads (4 k x 8 rows) hit 16 banks
 constexpr int kRB = 4;      // rows per warp in the HALS phases
 
 struct SmallArgs {
@@ -66,48 +66,63 @@ struct SmallArgs {
 };
 
 // ---------------------------------------------------------------------------------------------
+// D(8x8) += A(8x4) B(4x8) on the fp64 tensor cores: lane holds A[lane/4][lane%4],
+// B[lane%4][lane/4] and D[lane/4][2 (lane%4) + {0, 1}].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+template <int RCOLS>
+struct TileShape {
+  static constexpr int NB = RCOLS / 8;                 // 8-column B fragments of the tile
+  static constexpr int WNB = NB < 8 ? NB : 8;          // ... of a warp
+  static constexpr int CW = NB / WNB;                  // warps across the columns (1 or 2)
+  static constexpr int NG = kW / (4 * CW);             // k groups (2 or 1)
+  static constexpr int GT = kT / NG;                   // threads per group
+  static constexpr int NA = 4 * WNB;                   // accumulators per thread
+  static constexpr int FP = RCOLS + 4;                 // padded row of the factor slab
+  static constexpr int SLABD = kKS * kXP + kKS * FP;   // doubles of the fp64 slabs
+  static constexpr int REDD = (NG - 1) * NA * GT;      // doubles of the group hand-over
+  static constexpr int PRODD = SLABD > REDD ? SLABD : REDD;
+  static constexpr int SLAB32 = kTM * kKS + RCOLS * kKS;   // floats per staged slab
+};
+
 // One product tile: out[row][c] = sum_{k in [k0, k1)} op(X)[row][k] F[k][c] for the 64 output
-// rows r0.. (rows of X if !TRANS, columns of X if TRANS) and all r <= RCOLS columns.
-// The CTA's 256 threads form NG = 64 / RCOLS groups (1 for RCOLS = 128); a group covers the
-// whole 64 x RCOLS tile with a 4 x TC register tile per thread (TC = 4, or 8 at RCOLS = 128:
-// 4 TC DFMA per 2 + TC/2 shared-memory loads of 16 bytes, so the fp64 pipe, not shared memory,
-// is the bound, in few enough registers for two CTAs per SM) and takes every NG-th k of a
-// slab; the groups' sums are added in group order through shared memory at the end.
-// Thread (ty, tx) of a group owns rows 32 (a >> 1) + 2 ty + (a & 1), a < 4, and columns
-// 2 tx + (b & 1) + 2 TXN (b >> 1), b < TC, so that a warp's 16-byte loads are contiguous.
+// rows r0.. (rows of X if !TRANS, columns of X if TRANS) and all r <= RCOLS columns, fp64 on
+// the tensor cores (DMMA m8n8k4: 256 FMA per instruction from two operand registers per lane,
+// so shared memory carries ~1/5 of the SIMT register-tile traffic; the SIMT 4 x 4 tile ran at
+// 35 % of the fp64 rate, bound by shared-memory wavefronts -- ncu, profiles/r02d notes).
+// Warp (wr, wc) of a k group owns rows 16 wr .. +15 and columns 8 WNB wc .. ; the NG groups take
+// the 4-deep k steps of a slab alternately and their sums are added in group order through
+// shared memory at the end (fixed order).
 template <int RCOLS, bool TRANS>
 __device__ __forceinline__ void product_tile(const float* __restrict__ X, int64_t ldx, int64_t M,
                                              const float* F, int64_t ldf, int r, int64_t r0,
                                              int64_t k0, int64_t k1, double* out, double* Xs,
                                              double* Fs, float* St) {
-  constexpr int TC = RCOLS == 128 ? 8 : 4; // columns per thread
-  constexpr int TXN = RCOLS / TC;          // threads across the columns
-  constexpr int GT = 16 * TXN;             // threads per group
-  constexpr int NG = kT / GT;              // k groups
+  using TS = TileShape<RCOLS>;
+  constexpr int NB = TS::NB, WNB = TS::WNB, CW = TS::CW, NG = TS::NG, GT = TS::GT, NA = TS::NA;
+  constexpr int FP = TS::FP, SLAB32 = TS::SLAB32;
   constexpr int XQ = kTM * kKS / kT;       // X elements per thread and slab (8)
-  constexpr int FQ = RCOLS * kKS / kT;     // factor elements per thread and slab (RCOLS / 8)
-  const int t = threadIdx.x;
-  const int g = t / GT, w = t % GT, tx = w % TXN, ty = w / TXN;
-  double acc[4][TC];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int g = warp / (4 * CW), wr = (warp % (4 * CW)) / CW, wc = warp % CW;
+  double acc[2][WNB][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int b = 0; b < TC; ++b) acc[a][b] = 0.0;
-  // Per-thread element maps of a slab (e = t + 256 q):
-  //   X, !TRANS: row t/16 + 16 (q%4), k t%16 + 16 (q/4)  (a warp reads 2 rows x 64 bytes and
-  //              stores 16 k x 2 rows: conflict free);  TRANS: k t/64 + 4 q, row t%64;
-  //   F: k t/RCOLS + (256/RCOLS) q, column t%RCOLS.
+    for (int j = 0; j < WNB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // Per-thread element maps of a slab:
+  //   X, !TRANS: row t/16 + 16 (q%4), k t%16 + 16 (q/4)  (a warp reads 2 rows x 64 bytes);
+  //      TRANS:  k t/64 + 4 q, row t%64;      F: k t/8, columns t%8 + 8 q, q < NB.
   // Slabs arrive as fp32 through cp.async into a two-deep staging ring (no registers held, two
   // slabs of FMAs to cover the L2 / HBM latency); every thread converts the elements it
-  // requested itself into the fp64 slab the FMAs read.
+  // requested itself into the fp64 slab the tensor cores read.
   const int xi = TRANS ? t % kTM : t / 16, xk = TRANS ? t / kTM : t % 16;
   const float* xp = TRANS ? X + (k0 + xk) * ldx + r0 + xi : X + (r0 + xi) * ldx + k0 + xk;
   const int64_t xrows = M - r0 - xi;             // rows left from this thread's first row
-  constexpr int FK = kT / RCOLS;
-  const int fc = t % RCOLS, fk = t / RCOLS;
+  const int fc = t % 8, fk = t / 8;
   const float* fp = F + (k0 + fk) * ldf + fc;
-  const bool fok = fc < r;
-  constexpr int SLAB32 = kTM * kKS + RCOLS * kKS;      // floats per staged slab
   const unsigned st_base = (unsigned)__cvta_generic_to_shared(St) + 4u * t;
   auto request = [&](int64_t ks, int buf) {
     const int64_t kleft = k1 - ks;               // valid k of this slab: kk < kleft
@@ -127,10 +142,10 @@ __device__ __forceinline__ void product_tile(const float* __restrict__ X, int64_
                    "l"(ok ? src : X), "r"(ok ? 4 : 0));
     }
 #pragma unroll
-    for (int q = 0; q < FQ; ++q) {
-      const bool ok = fok && fk + FK * q < kleft;
+    for (int q = 0; q < NB; ++q) {
+      const bool ok = fc + 8 * q < r && fk < kleft;
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst + 4u * kT * (XQ + q)),
-                   "l"(ok ? fp + (int64_t)(FK * q) * ldf : F), "r"(ok ? 4 : 0));
+                   "l"(ok ? fp + 8 * q : F), "r"(ok ? 4 : 0));
     }
     xp += TRANS ? (int64_t)kKS * ldx : kKS;
     fp += (int64_t)kKS * ldf;
@@ -144,77 +159,78 @@ __device__ __forceinline__ void product_tile(const float* __restrict__ X, int64_
       Xs[kk * kXP + ii] = (double)src[kT * q];
     }
 #pragma unroll
-    for (int q = 0; q < FQ; ++q) Fs[t + kT * q] = (double)src[kT * (XQ + q)];   // Fs[kk][c]
+    for (int q = 0; q < NB; ++q) Fs[fk * FP + fc + 8 * q] = (double)src[kT * (XQ + q)];
   };
   request(k0, 0);
   asm volatile("cp.async.commit_group;");
   if (k0 + kKS < k1) request(k0 + kKS, 1);
   asm volatile("cp.async.commit_group;");
   int buf = 0;
+  const double* xa = Xs + (lane & 3) * kXP + 16 * wr + (lane >> 2);
+  const double* fb = Fs + (lane & 3) * FP + 8 * WNB * wc + (lane >> 2);
   for (int64_t ks = k0; ks < k1; ks += kKS, buf ^= 1) {
     asm volatile("cp.async.wait_group 1;" ::: "memory");   // this thread's requests of slab ks
-    __syncthreads();                       // the previous slab's FMAs are done with Xs / Fs
+    __syncthreads();                       // the previous slab's MMAs are done with Xs / Fs
     convert(buf);
     __syncthreads();
     if (ks + 2 * kKS < k1) request(ks + 2 * kKS, buf);
     asm volatile("cp.async.commit_group;");
 #pragma unroll
-    for (int kq = 0; kq < kKS / NG; ++kq) {
-      const int kk = kq * NG + g;
-      double xv[4], fv[TC];
+    for (int kq = 0; kq < kKS / 4 / NG; ++kq) {
+      const int k4 = 4 * (kq * NG + g);
+      const double a0 = xa[k4 * kXP], a1 = xa[k4 * kXP + 8];
+      double bv[WNB];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const double2 x2 = *reinterpret_cast<const double2*>(Xs + kk * kXP + 32 * j + 2 * ty);
-        xv[2 * j] = x2.x;
-        xv[2 * j + 1] = x2.y;
+      for (int j = 0; j < WNB; ++j) bv[j] = fb[k4 * FP + 8 * j];
+#pragma unroll
+      for (int j = 0; j < WNB; ++j) {
+        dmma884(acc[0][j][0], acc[0][j][1], a0, bv[j]);
+        dmma884(acc[1][j][0], acc[1][j][1], a1, bv[j]);
       }
-#pragma unroll
-      for (int j = 0; j < TC / 2; ++j) {
-        const double2 f2 =
-            *reinterpret_cast<const double2*>(Fs + kk * RCOLS + 2 * tx + 2 * TXN * j);
-        fv[2 * j] = f2.x;
-        fv[2 * j + 1] = f2.y;
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < TC; ++b) acc[a][b] = fma(xv[a], fv[b], acc[a][b]);
     }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   // groups 1 .. NG-1 hand their sums to group 0 through shared memory (over the slabs)
-  constexpr int NA = 4 * TC;
+  const int w = t % GT;
   if (NG > 1) {
     double* red = Xs;                      // (NG - 1) x NA x GT doubles
     __syncthreads();
     if (g > 0) {
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int b = 0; b < TC; ++b) red[((g - 1) * NA + a * TC + b) * GT + w] = acc[a][b];
+        for (int j = 0; j < WNB; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            red[((g - 1) * NA + (i * WNB + j) * 2 + e) * GT + w] = acc[i][j][e];
     }
     __syncthreads();
     if (g == 0) {
       for (int gg = 0; gg < NG - 1; ++gg)
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int b = 0; b < TC; ++b) acc[a][b] += red[(gg * NA + a * TC + b) * GT + w];
+          for (int j = 0; j < WNB; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              acc[i][j][e] += red[(gg * NA + (i * WNB + j) * 2 + e) * GT + w];
     }
   }
   if (g == 0) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int64_t row = r0 + 32 * (a >> 1) + 2 * ty + (a & 1);
+    for (int i = 0; i < 2; ++i) {
+      const int64_t row = r0 + 16 * wr + 8 * i + (lane >> 2);
       if (row >= M) continue;
 #pragma unroll
-      for (int b = 0; b < TC; ++b) {
-        const int c = 2 * tx + (b & 1) + 2 * TXN * (b >> 1);
-        if (c < r) out[row * r + c] = acc[a][b];
-      }
+      for (int j = 0; j < WNB; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 8 * WNB * wc + 8 * j + 2 * (lane & 3) + e;
+          if (c < r) out[row * r + c] = acc[i][j][e];
+        }
     }
   }
-  __syncthreads();                         // the next tile's stash overwrites red
+  __syncthreads();                         // the next tile's slabs overwrite red
 }
 
 // All tiles of one pass: tile = (row block, K chunk); partial of chunk q at pp[q M r ...].
@@ -483,16 +499,14 @@ template <int CPL, int RCOLS>
 __global__ void __launch_bounds__(kT, CPL <= 2 ? 2 : 1) small_hals_kernel(SmallArgs a) {
   constexpr int RP = 32 * CPL;
   extern __shared__ double smem[];
-  // product phases: Xs (kKS x kXP) + Fs (kKS x RCOLS); HALS phases: Gs (RP^2) + Ss + ginv
+  // product phases: Xs (kKS x kXP) + Fs (kKS x FP) [+ staging]; HALS phases: Gs + Ss + ginv
   double* Xs = smem;
   double* Fs = smem + kKS * kXP;
-  constexpr int NGK = RCOLS == 128 ? 1 : 64 / RCOLS;
-  constexpr int PRODD = (kKS * kXP + kKS * RCOLS) > (NGK - 1) * kTM * RCOLS
-                            ? (kKS * kXP + kKS * RCOLS) : (NGK - 1) * kTM * RCOLS;
-  float* St = reinterpret_cast<float*>(smem + PRODD);   // 2 staged fp32 slabs
   double* Gs = smem;
   double* Ss = smem + RP * RP;
   double* ginv = Ss + 2 * kW * kRB * RP;
+  constexpr int PRODD = TileShape<RCOLS>::PRODD;
+  float* St = reinterpret_cast<float*>(smem + PRODD);   // 2 staged fp32 slabs
   __shared__ double red[2 * kW];
   unsigned bar_target = 0;
   unsigned* bar = a.bar;
@@ -598,10 +612,8 @@ __global__ void __launch_bounds__(kT, CPL <= 2 ? 2 : 1) small_hals_kernel(SmallA
 template <int CPL, int RCOLS>
 size_t smem_bytes() {
   constexpr int RP = 32 * CPL;
-  constexpr int NG = RCOLS == 128 ? 1 : 64 / RCOLS;
-  const size_t slabs = (size_t)(kKS * kXP + kKS * RCOLS);
-  const size_t gred = (size_t)(NG - 1) * kTM * RCOLS;          // group sums (over the slabs)
-  const size_t prod = std::max(slabs, gred) + (size_t)(kTM * kKS + RCOLS * kKS);   // + staging
+  using TS = TileShape<RCOLS>;
+  const size_t prod = (size_t)TS::PRODD + (size_t)TS::SLAB32;     // fp64 slabs + 2 staged fp32
   const size_t hals = (size_t)(RP * RP + 2 * kW * kRB * RP + RP);
   return sizeof(double) * std::max(prod, hals);
 }
@@ -670,6 +682,7 @@ bool make_plan_t(int64_t m, int64_t n, Plan* p) {
 
 bool make_plan(int64_t m, int64_t n, int r, Plan* p) {
   if (r <= 16) return make_plan_t<1, 16>(m, n, p);
+  if (r <= 24) return make_plan_t<1, 24>(m, n, p);
   if (r <= 32) return make_plan_t<1, 32>(m, n, p);
   if (r <= 64) return make_plan_t<2, 64>(m, n, p);
   if (r <= 96) return make_plan_t<3, 128>(m, n, p);
