@@ -722,15 +722,19 @@ int small_sweeps_launch(const float* X, int64_t ldx, int64_t m, int64_t n, int r
   a.gp = ws + (size_t)std::max(p.ksA * m, p.ksB * n) * r;
   a.sc = a.gp + (size_t)p.grid * r * r;
   a.bar = reinterpret_cast<unsigned*>(a.sc + 2 * (size_t)p.grid + 8);
-  if (cudaMemsetAsync(a.bar, 0, 16 * sizeof(double), st) != cudaSuccess) return 1;
   a.ksA = p.ksA; a.ksB = p.ksB; a.kcA = p.kcA; a.kcB = p.kcB;
   a.count = count;
   const char* dbg = getenv("ENMF_SMALL_DEBUG");
   a.debug = dbg && dbg[0] == '1';
-  void* args[] = {&a};
-  if (cudaLaunchCooperativeKernel(p.fn, dim3(p.grid), dim3(kT), args, p.smem, st) != cudaSuccess)
-    return 1;
-  count_launch();
+  // (the barrier counter advances by 4 grid sizes per sweep: launches of <= 2^18 sweeps)
+  for (int done = 0; done < count; done += 1 << 18) {
+    a.count = count - done < (1 << 18) ? count - done : 1 << 18;
+    if (cudaMemsetAsync(a.bar, 0, 16 * sizeof(double), st) != cudaSuccess) return 1;
+    void* args[] = {&a};
+    if (cudaLaunchCooperativeKernel(p.fn, dim3(p.grid), dim3(kT), args, p.smem, st) != cudaSuccess)
+      return 1;
+    count_launch();
+  }
   return 0;
 }
 

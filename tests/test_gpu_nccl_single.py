@@ -41,9 +41,13 @@ def _handle(cfg, prec, uid, X, **opts):
 @pytest.mark.parametrize("cfg", [synth.C1, synth.C5.scaled(700, 650, 128, 128, name="C5-700x650"),
                                  synth.C3.scaled(300, 1100, 32, 32, name="C3-300x1100")],
                          ids=["C1", "C5-700x650", "C3-300x1100"])
-def test_single_rank_nccl_path_bitwise(cfg, prec):
+def test_single_rank_nccl_path_bitwise(cfg, prec, monkeypatch):
     import torch
     import paper_2605_19325_b200 as E
+    # the plain handle's HALS sweeps on the separate-launch path, which is the one the
+    # collective path runs (the persistent small-problem kernel, small_sweep.cu, is a
+    # single-rank specialisation with its own fixed summation order: test_gpu_small_fused.py)
+    monkeypatch.setenv("ENMF_SMALL_FUSED", "0")
     uid = E.nccl_unique_id()
     assert len(uid) == 128
     X = to_dev(synth.x_full(cfg))
