@@ -370,8 +370,15 @@ enmf_status_t ensure_snaps(enmf_handle_t h) {
   return dalloc(&h->snaps, (size_t)h->opt.pbcd_max_iter * rows * (size_t)h->r);
 }
 
+// The cached sweep graph bakes in the handle's buffers and options: dropped when any changes.
+void drop_sweep_graph(enmf_handle_t h) {
+  if (h->sw_exec) cudaGraphExecDestroy(h->sw_exec);
+  h->sw_exec = nullptr;
+}
+
 enmf_status_t ensure_ftrace(enmf_handle_t h, int n) {
   if (h->ftrace_cap >= n) return ENMF_OK;
+  drop_sweep_graph(h);
   if (h->ftrace) cudaFree(h->ftrace);
   h->ftrace = nullptr;
   h->ftrace_cap = 0;
@@ -671,6 +678,7 @@ enmf_status_t enmf_destroy(enmf_handle_t h) {
     cudaStreamDestroy(h->st_comm);
   }
   for (cudaEvent_t e : h->ev_comm) cudaEventDestroy(e);
+  if (h->sw_exec) cudaGraphExecDestroy(h->sw_exec);
   if (h->cap_st) cudaStreamDestroy(h->cap_st);
   if (h->tc) tc_destroy(h->tc);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
@@ -770,6 +778,7 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
   if (!h) return ENMF_ERR_INVALID_ARG;
   ENMF_TRY(validate_ld(X, ldx, h->n));
   LaunchScope ls(h);
+  drop_sweep_graph(h);
   h->X = X;
   h->ldx = ldx;
   h->bound = false;
@@ -841,6 +850,7 @@ enmf_status_t bind_csr(enmf_handle_t h, const int64_t* row_ptr, const int32_t* c
   if (nmc && (h->sharded || !nmc_supported((int)h->r))) return ENMF_ERR_SHAPE;
   if (nnz > INT32_MAX || h->n > INT32_MAX) return ENMF_ERR_SHAPE;
   LaunchScope ls(h);
+  drop_sweep_graph(h);
   h->bound = false;
   h->X = nullptr;
   h->ldx = 0;
@@ -956,6 +966,7 @@ enmf_status_t enmf_project(enmf_handle_t h, float* U, int64_t ldu, float* V, int
 enmf_status_t enmf_set_ablation(enmf_handle_t h, int step_rule, int descent) {
   if (!h || (step_rule != 0 && step_rule != 1) || (descent != 0 && descent != 1))
     return ENMF_ERR_INVALID_ARG;
+  drop_sweep_graph(h);
   h->opt.step_rule = step_rule;
   h->opt.descent = descent;
   h->umax_valid = h->vmax_valid = false;
@@ -1017,6 +1028,51 @@ enmf_status_t replay_sweeps(enmf_handle_t h, float* U, int64_t ldu, float* V, in
   }
   cudaGraphExecDestroy(ge);
   CUDA_TRY(e);
+  return ENMF_OK;
+}
+
+// One ascent-capable sweep as a cached CUDA graph (the small-problem path steps the ascent
+// stage one sweep at a time with a host check of the stage in between; ~50 launches per sweep
+// otherwise).  The graph is keyed on the factor pointers and leading dimensions.
+enmf_status_t graph_sweep_once(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv) {
+  if (h->sw_exec && (h->sw_key[0] != U || h->sw_key[1] != V || h->sw_ld[0] != ldu ||
+                     h->sw_ld[1] != ldv)) {
+    cudaGraphExecDestroy(h->sw_exec);
+    h->sw_exec = nullptr;
+  }
+  if (!h->sw_exec) {
+    if (!h->cap_st) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking));
+      if (!h->ev_a) CUDA_TRY(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
+    }
+    cudaStream_t user = h->st;
+    h->st = h->cap_st;
+    const int64_t l0 = h->launches;
+    cudaGraph_t g = nullptr;
+    enmf_status_t s = ENMF_OK;
+    cudaError_t e = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeRelaxed);
+    if (e == cudaSuccess) {
+      s = sweep(h, U, ldu, V, ldv, 1, true, SweepHooks());
+      e = cudaStreamEndCapture(h->st, &g);
+    }
+    h->st = user;
+    h->sw_launches = h->launches - l0;
+    h->launches = l0;
+    if (s != ENMF_OK || e != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      return s != ENMF_OK ? s : ENMF_ERR_CUDA;
+    }
+    e = cudaGraphInstantiate(&h->sw_exec, g, 0);
+    cudaGraphDestroy(g);
+    CUDA_TRY(e);
+    h->sw_key[0] = U;
+    h->sw_key[1] = V;
+    h->sw_ld[0] = ldu;
+    h->sw_ld[1] = ldv;
+  }
+  CUDA_TRY(cudaGraphLaunch(h->sw_exec, h->st));
+  h->launches += h->sw_launches;
   return ENMF_OK;
 }
 
@@ -1100,10 +1156,19 @@ enmf_status_t iterate_core(enmf_handle_t h, float* U, int64_t ldu, float* V, int
       ENMF_TRY(replay_sweeps(h, U, ldu, V, ldv, maybe_ascent, n_iters - 1));
       break;
     }
-    if (h->nmc)
+    if (h->nmc) {
       ENMF_TRY(sweep_nmc(h, U, ldu, V, ldv, t, hk));
-    else
+    } else if (small && graphs && maybe_ascent && !hk.u_ready && !h->opt.step_rule) {
+      ENMF_TRY(graph_sweep_once(h, U, ldu, V, ldv));   // an ascent sweep of the small path
+      if (hk.u_download)
+        CUDA_TRY(cudaMemcpyAsync(hk.u_download, U, sizeof(float) * h->m_loc * h->r,
+                                 cudaMemcpyDeviceToHost, h->st));
+      if (hk.v_download)
+        CUDA_TRY(cudaMemcpyAsync(hk.v_download, V, sizeof(float) * h->n * h->r,
+                                 cudaMemcpyDeviceToHost, h->st));
+    } else {
       ENMF_TRY(sweep(h, U, ldu, V, ldv, t, maybe_ascent, hk));
+    }
   }
   if (u_ready && n_iters == 0) CUDA_TRY(cudaStreamWaitEvent(h->st, u_ready, 0));
   h->umax_valid = h->vmax_valid = false;

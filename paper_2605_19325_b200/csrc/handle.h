@@ -107,6 +107,10 @@ struct enmf_handle_s {
   cudaStream_t cap_st = nullptr;   // non-blocking stream a sweep is captured on (CUDA graph)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   double* small_ws = nullptr;      // workspace of the persistent small-problem HALS kernel
+  cudaGraphExec_t sw_exec = nullptr;   // cached graph of one ascent-capable sweep (small path)
+  const void* sw_key[2] = {nullptr, nullptr};
+  int64_t sw_ld[2] = {0, 0};
+  int64_t sw_launches = 0;
   float* x_owned = nullptr;  // device copy of X owned by enmf_solve_host
   double* W64 = nullptr;     // (m_loc + n) x r fp64 [U*; V*] kept from enmf_svd for enmf_rotate
   // profiling of the X passes (enmf_set_profiling): CUDA events around every contraction

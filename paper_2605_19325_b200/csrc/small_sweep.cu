@@ -291,6 +291,10 @@ __device__ __forceinline__ double reduce_scalar(const double* parts, int n, bool
   return is_min ? warp_min(s) : warp_sum(s);
 }
 
+// (A lane-per-row form -- 32 rows per warp, rows k-major in shared memory, the column sweep
+// blocked left-looking with 16 residuals in registers -- was built and measured: the sweep part
+// took 14.7 / 6.5 / 4.7 us at C2 / C3 / C4 against 9.5 / 5.6 / 3.6 us here, one warp bound by
+// the shared-memory wavefronts of the broadcast G rows; rejected, profiles/r02d_small_notes.md.)
 // HALS on the rows of F (rows x r): C = sum of the ksplit tile partials, t = C - u G, then the
 // Gauss-Seidel column sweep U_ik <- max(0, U_ik + (C_ik - sum_l U_il G_lk) / G_kk)
 // (PAPER.md:322-324), F written in fp32; per-CTA partial Gram of the written rows, optional
