@@ -250,11 +250,19 @@ def small_config_rates(stream):
         torch.cuda.synchronize()
         ms = a.elapsed_time(b)
         lps = (h.launch_count - l0) / cfg.sweeps
+        # steady state of the HALS stage: 100 more sweeps (one persistent-kernel launch on
+        # these cache-resident problems, csrc/small_sweep.cu)
+        a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a2.record(stream)
+        _, info2 = h.iterate(U, V, 100)
+        b2.record(stream)
+        torch.cuda.synchronize()
+        hals_us = 1e3 * a2.elapsed_time(b2) / 100 if info2["hals_sweeps"] == 100 else None
         out[cfg.name] = {"sweeps": cfg.sweeps, "ms": ms, "sweeps_per_s": cfg.sweeps / (ms / 1e3),
                          "effective_gbs_over_x": 2.0 * cfg.m * cfg.n * 4 * cfg.sweeps / (ms / 1e3) / 1e9,
                          "ascent_sweeps": info["ascent_sweeps"], "precision_path": h.precision,
                          "init_s": init_s, "f_last": float(f[-1]),
-                         "kernel_launches_per_sweep": lps,
+                         "kernel_launches_per_sweep": lps, "hals_sweep_us": hals_us,
                          "x": "effective rate: X (<= 90 MB) stays cache resident"}
         h.close()
         del X, U, V

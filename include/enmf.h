@@ -248,7 +248,14 @@ enmf_status_t enmf_get_stage(enmf_handle_t h, int* stage, double* lambda_u, doub
  * sweep in trace form ||X||^2 - 2<X^T U, V> + <U^T U, V^T V> (fp64 terms); on the
  * tensor-core path the terms are those of the quantised operands the X pass multiplied,
  * ||X~||^2 - 2<X~^T U~, V> + <U~^T U~, V^T V> = ||X~ - U~ V^T||^2 up to the dropped digit
- * products, which keeps the ||X||^2 / f conditioning of the trace form out of f. */
+ * products, which keeps the ||X||^2 / f conditioning of the trace form out of f.
+ * Cache-resident problems (single rank, dense X, fp64 path, m n <= 2^26: the small
+ * BASELINE configurations): every HALS sweep runs in one persistent
+ * cooperative kernel (all remaining sweeps of the call in one launch), the ascent sweeps as
+ * a CUDA graph each with a host check of the stage in between; the result does not depend
+ * on how the caller chunks its calls.  The first such call allocates that kernel's
+ * workspace (ENMF_ERR_OOM if it does not fit).  ENMF_SMALL_FUSED=0 in the environment keeps
+ * the separate launches (the path the multi-rank handle runs). */
 enmf_status_t enmf_iterate(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
                            int n_iters, double* f_trace_host, enmf_iter_info_t* info_host);
 

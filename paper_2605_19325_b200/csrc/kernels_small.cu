@@ -3,6 +3,7 @@
 // SVD, Procrustes) used at init.
 #include <float.h>
 
+#include "grid_barrier.cuh"
 #include "internal.h"
 
 namespace enmf {
@@ -689,7 +690,9 @@ polar_newton_kernel(const double* __restrict__ M, int k, double* R, int* fail, i
 // returns at once), else writes X (1.5 I - 0.5 Y) to the other buffer.  state = {done, fail}.
 constexpr int kNsTile = 16;              // 16 x 16 output tiles: 64 CTAs at k = 128
 
-__global__ void ns_init_kernel(const double* __restrict__ M, int k, double* X, int* state) {
+__global__ void ns_init_kernel(const double* __restrict__ M, int k, double* X, int* state,
+                               unsigned* bar) {
+  if (threadIdx.x == 0) *bar = 0u;
   __shared__ double red[256];
   double s = 0.0;
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) s += M[e] * M[e];
@@ -703,12 +706,10 @@ __global__ void ns_init_kernel(const double* __restrict__ M, int k, double* X, i
 }
 
 // Y[I, J] tile = sum_l X[l][I] X[l][J]; partial |Y - I|^2 of the tile
-__global__ void __launch_bounds__(256) ns_gram_kernel(const double* __restrict__ X, int k,
-                                                      double* Y, double* part,
-                                                      const int* state) {
-  if (state[0]) return;
-  __shared__ double Xi[128][kNsTile + 1], Xj[128][kNsTile + 1];
-  __shared__ double red[256];
+__device__ __forceinline__ void ns_gram_tile(const double* X, int k, double* Y, double* part,
+                                             double* buf, double* red) {
+  double (*Xi)[kNsTile + 1] = reinterpret_cast<double (*)[kNsTile + 1]>(buf);
+  double (*Xj)[kNsTile + 1] = reinterpret_cast<double (*)[kNsTile + 1]>(buf + 128 * (kNsTile + 1));
   const int nt = (k + kNsTile - 1) / kNsTile;
   const int ti = blockIdx.x / nt, tj = blockIdx.x % nt;
   for (int e = threadIdx.x; e < k * kNsTile; e += blockDim.x) {
@@ -734,14 +735,13 @@ __global__ void __launch_bounds__(256) ns_gram_kernel(const double* __restrict__
   if (threadIdx.x == 0) part[blockIdx.x] = dev;
 }
 
-// X_out[I, J] = sum_l X[I][l] (1.5 delta_lJ - 0.5 Y[l][J]), or R = X when converged
-__global__ void __launch_bounds__(256) ns_step_kernel(const double* __restrict__ X, int k,
-                                                      const double* __restrict__ Y,
-                                                      const double* __restrict__ part,
-                                                      int nparts, double tol2, double* Xout,
-                                                      double* R, int* state) {
-  if (state[0]) return;
-  __shared__ double Xr[kNsTile][128 + 1], Yc[128][kNsTile + 1];
+// X_out[I, J] = sum_l X[I][l] (1.5 delta_lJ - 0.5 Y[l][J]), or R = X when converged (returns
+// true: the same decision on every CTA, the partials are summed in one fixed order)
+__device__ __forceinline__ bool ns_step_tile(const double* X, int k, const double* Y,
+                                             const double* part, int nparts, double tol2,
+                                             double* Xout, double* R, int* state, double* buf) {
+  double (*Xr)[128 + 1] = reinterpret_cast<double (*)[128 + 1]>(buf);
+  double (*Yc)[kNsTile + 1] = reinterpret_cast<double (*)[kNsTile + 1]>(buf + kNsTile * 129);
   double dev = 0.0;
   for (int q = 0; q < nparts; ++q) dev += part[q];          // fixed order: same on every CTA
   if (dev <= tol2) {
@@ -749,10 +749,10 @@ __global__ void __launch_bounds__(256) ns_step_kernel(const double* __restrict__
       R[e] = X[e];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       state[1] = 0;
+      state[0] = 1;
       __threadfence();
     }
-    // state[0] (done) is raised by ns_done_kernel after this grid: no CTA may skip the copy
-    return;
+    return true;
   }
   const int nt = (k + kNsTile - 1) / kNsTile;
   const int ti = blockIdx.x / nt, tj = blockIdx.x % nt;
@@ -774,11 +774,31 @@ __global__ void __launch_bounds__(256) ns_step_kernel(const double* __restrict__
     const int i = ti * kNsTile + a, j = tj * kNsTile + b;
     if (i < k && j < k) Xout[i * k + j] = acc;
   }
+  return false;
 }
 
-// done flag after a converged step (separate launch: every CTA of the step saw done = 0)
-__global__ void ns_done_kernel(int* state) {
-  if (threadIdx.x == 0 && state[0] == 0 && state[1] == 0) state[0] = 1;
+// The whole iteration in one cooperative launch (one CTA per 16 x 16 output tile, <= 64 CTAs):
+// Gram phase | grid barrier | step phase | grid barrier, until |X^T X - I|_F <= tol or max_iter.
+// (Round 1-2c issued 3 launches per iteration, 121 per ADMM step whether or not the iteration
+// had converged: 12000 launches = 40 ms of a 100-step rotation, most of the init of the small
+// configurations; profiles/r02e_small_C3_launches_summary.txt.)
+__global__ void __launch_bounds__(256) ns_polar_kernel(int k, double* X0, double* X1, double* Y,
+                                                       double* part, int nparts, double tol2,
+                                                       double* R, int* state, unsigned* bar,
+                                                       int max_iter) {
+  // one buffer for both phases: (Xi, Xj) of the Gram tile, (Xr, Yc) of the step tile
+  __shared__ double buf[2 * 128 * (kNsTile + 1)];
+  __shared__ double red[256];
+  if (state[0]) return;                        // M = 0: left to the fallback (uniform)
+  unsigned target = 0;
+  for (int it = 0; it < max_iter; ++it) {
+    const double* Xc = (it & 1) ? X1 : X0;
+    double* Xn = (it & 1) ? X0 : X1;
+    ns_gram_tile(Xc, k, Y, part, buf, red);
+    grid_barrier(bar, target);
+    if (ns_step_tile(Xc, k, Y, part, nparts, tol2, Xn, R, state, buf)) return;
+    grid_barrier(bar, target);
+  }
 }
 
 // Columns of C with s = 0 are completed to an orthonormal basis (rank-deficient M only).
@@ -950,15 +970,14 @@ void polar_ns(const double* M, int k, double* R, int* state, double* work, int m
   double* Y = work + (size_t)2 * k * k;
   double* part = work + (size_t)3 * k * k;
   const double tol2 = 1e-26 * k;          // |X^T X - I|_F <= 1e-13 sqrt(k)
-  ns_init_kernel<<<1, 256, 0, st>>>(M, k, X0, state);
-  for (int it = 0; it < max_iter; ++it) {
-    const double* Xc = (it & 1) ? X1 : X0;
-    double* Xn = (it & 1) ? X0 : X1;
-    ns_gram_kernel<<<nt * nt, 256, 0, st>>>(Xc, k, Y, part, state);
-    ns_step_kernel<<<nt * nt, 256, 0, st>>>(Xc, k, Y, part, nt * nt, tol2, Xn, R, state);
-    ns_done_kernel<<<1, 32, 0, st>>>(state);
-  }
-  count_launch(1 + 3 * max_iter);
+  unsigned* bar = reinterpret_cast<unsigned*>(work + (size_t)3 * k * k + 128);
+  ns_init_kernel<<<1, 256, 0, st>>>(M, k, X0, state, bar);
+  int nparts = nt * nt;
+  void* args[] = {&k, &X0, &X1, &Y, &part, &nparts, const_cast<double*>(&tol2), &R, &state, &bar,
+                  &max_iter};
+  cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(ns_polar_kernel), dim3(nt * nt),
+                              dim3(256), args, 0, st);
+  count_launch(2);
 }
 
 void polar_newton(const double* M, int k, double* R, int* fail, cudaStream_t st, int* iters,

@@ -23,6 +23,7 @@
 
 #include <algorithm>
 
+#include "grid_barrier.cuh"
 #include "internal.h"
 #include "rows_dev.cuh"
 
@@ -248,27 +249,6 @@ __device__ __forceinline__ void product_pass(const float* __restrict__ X, int64_
   }
 }
 
-// Grid barrier (all CTAs co-resident: cooperative launch).  One thread per CTA arrives on a
-// monotonically increasing counter and polls it with a back-off: with cg::grid_group::sync the
-// ~200 waiting CTAs of a phase that only a dozen CTAs work in poll one L2 line without pause,
-// and the working CTAs' loads queue behind them (measured: ~2 us per dependent L2 round trip).
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    target += gridDim.x;
-    __threadfence();                                   // release this CTA's writes
-    atomicAdd(bar, 1u);
-    unsigned v;
-    for (;;) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-      if ((int)(v - target) >= 0) break;
-      __nanosleep(200);
-    }
-    __threadfence();                                   // acquire; invalidates this SM's L1
-  }
-  __syncthreads();
-}
-
 // G (r x r) = sum over the first nparts per-CTA partials, one entry per warp at a time: the
 // lanes take the partials strided, then a fixed xor tree.
 __device__ __forceinline__ void reduce_gram(const double* gp, int nparts, int r, double* G) {
@@ -383,15 +363,15 @@ __device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, 
 #pragma unroll
           for (int b = 0; b < kRB; ++b) {
             // lane kk owns (u_k, t_k); its change d is broadcast and the residual follows
-            // (the change d = t / G_kk or -u_k is formed beside v, not from nu - u_k: two
-            // fp64 latencies on the serial chain instead of four)
+            // u_k <- max(0, u_k + t_k / G_kk) as the change d = max(-u_k, t_k / G_kk) and
+            // u_k + d: a multiply, a max and an add per row (the loop is bound by its
+            // instruction count; forming v = fma(t, 1/G_kk, u), testing v > 0 and selecting
+            // took ~25 instructions per row and step).  u_k + d is 0 exactly when the bound
+            // is active; otherwise it differs from the fused form by <= 1/2 ulp of fp64.
             const double uo = u[b][s];
-            const double p = t[b][s] * ig;
-            const double v = fma(t[b][s], ig, uo);
-            const bool pos = v > 0.0;
-            if (lane == kk) u[b][s] = pos ? v : 0.0;
-            const double d = __shfl_sync(FULL, pos ? p : -uo, kk);
-            // (integer-pipe selects on the high words were tried: 2.5x slower, measured)
+            const double dn = fmax(t[b][s] * ig, -uo);
+            if (lane == kk) u[b][s] = uo + dn;
+            const double d = __shfl_sync(FULL, dn, kk);
 #pragma unroll
             for (int c = 0; c < CPL; ++c) t[b][c] = fma(-d, gk[c], t[b][c]);
           }
