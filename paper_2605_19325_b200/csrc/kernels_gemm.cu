@@ -4,32 +4,47 @@
 // Used for the cross terms X V and X^T U, the Grams U^T U, V^T V, the
 // range-finder products X Omega, X^T Q and the ADMM products W R,
 // W^T B.  64x64 output tiles, 16-deep K slabs staged in shared memory
-// as fp64, 4x4 register tile per thread (rows ty+16a, cols tx+16b so both operand reads
-// are conflict-free / broadcast), split-K layers reduced in a fixed order.
+// as fp64, 16 x 32 warp tiles on the fp64 tensor cores (DMMA m8n8k4), split-K layers reduced
+// in a fixed order.
 #include "internal.h"
 
 namespace enmf {
 namespace {
 
 constexpr int BM = 64, BN = 64, BK = 16;
+constexpr int LDS = BM + 4;   // padded slab rows: the DMMA fragment loads (4 k x 8 rows) hit 16 banks
 
+// D(8x8) += A(8x4) B(4x8) on the fp64 tensor cores: lane holds A[lane/4][lane%4],
+// B[lane%4][lane/4] and D[lane/4][2 (lane%4) + {0, 1}].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// 64 x 64 output tile, 16-deep K slabs staged in shared memory as fp64 (k-major), next slab
+// prefetched into registers; the 8 warps are a 4 x 2 grid of 16 x 32 warp tiles on the fp64
+// tensor cores (DMMA m8n8k4: 8 per 4-deep k step from 6 operand loads per lane).  Round 1-2c
+// used 4 x 4 SIMT register tiles: 35 % of the fp64 rate, bound by shared-memory wavefronts
+// (profiles/r02d_small_notes.md); DMMA has the same peak and ~1/5 of the operand traffic.
 template <typename TA, typename TB, bool TRANS>
 __global__ void __launch_bounds__(256)
 gemm_kernel(const TA* __restrict__ A, int64_t lda, const TB* __restrict__ B, int64_t ldb,
             int64_t M, int64_t N, int64_t K, int64_t kchunk, double* __restrict__ out,
             int64_t ldo, int64_t split_stride) {
-  __shared__ double As[BK][BM + 1];
-  __shared__ double Bs[BK][BN];
-  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  __shared__ double As[BK][LDS];
+  __shared__ double Bs[BK][LDS];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int wr = warp >> 1, wc = warp & 1;
   const int64_t i0 = (int64_t)blockIdx.y * BM, j0 = (int64_t)blockIdx.x * BN;
   const int64_t kb = (int64_t)blockIdx.z * kchunk;
   const int64_t ke = K < kb + kchunk ? K : kb + kchunk;
-  double acc[4][4];
+  double acc[2][4][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  double ar[4], br[4];
+  auto fetch = [&](int64_t k0) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int e = t + 256 * q;
@@ -37,38 +52,53 @@ gemm_kernel(const TA* __restrict__ A, int64_t lda, const TB* __restrict__ B, int
       if (TRANS) { kk = e / BM; ii = e % BM; }
       else { ii = e / BK; kk = e % BK; }
       const int64_t gi = i0 + ii, gk = k0 + kk;
-      double v = 0.0;
-      if (gi < M && gk < ke) v = (double)(TRANS ? A[gk * lda + gi] : A[gi * lda + gk]);
-      As[kk][ii] = v;
+      ar[q] = (gi < M && gk < ke) ? (double)(TRANS ? A[gk * lda + gi] : A[gi * lda + gk]) : 0.0;
       const int kb2 = e / BN, jj = e % BN;
       const int64_t gj = j0 + jj, gk2 = k0 + kb2;
-      Bs[kb2][jj] = (gj < N && gk2 < ke) ? (double)B[gk2 * ldb + gj] : 0.0;
+      br[q] = (gj < N && gk2 < ke) ? (double)B[gk2 * ldb + gj] : 0.0;
+    }
+  };
+  fetch(kb);
+  const double* xa = &As[lane & 3][16 * wr + (lane >> 2)];
+  const double* xb = &Bs[lane & 3][32 * wc + (lane >> 2)];
+  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+    __syncthreads();                       // the previous slab's MMAs are done
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = t + 256 * q;
+      int ii, kk;
+      if (TRANS) { kk = e / BM; ii = e % BM; }
+      else { ii = e / BK; kk = e % BK; }
+      As[kk][ii] = ar[q];
+      Bs[e / BN][e % BN] = br[q];
     }
     __syncthreads();
+    if (k0 + BK < ke) fetch(k0 + BK);      // next slab's loads in flight during the MMAs
 #pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      double av[4], bv[4];
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      const double a0 = xa[k4 * LDS], a1 = xa[k4 * LDS + 8];
+      double bv[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) av[a] = As[kk][ty + 16 * a];
+      for (int j = 0; j < 4; ++j) bv[j] = xb[k4 * LDS + 8 * j];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][tx + 16 * b];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+      for (int j = 0; j < 4; ++j) {
+        dmma884(acc[0][j][0], acc[0][j][1], a0, bv[j]);
+        dmma884(acc[1][j][0], acc[1][j][1], a1, bv[j]);
+      }
     }
-    __syncthreads();
   }
   double* o = out + (int64_t)blockIdx.z * split_stride;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int64_t gi = i0 + ty + 16 * a;
+  for (int a = 0; a < 2; ++a) {
+    const int64_t gi = i0 + 16 * wr + 8 * a + (lane >> 2);
     if (gi >= M) continue;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int64_t gj = j0 + tx + 16 * b;
-      if (gj < N) o[gi * ldo + gj] = acc[a][b];
-    }
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t gj = j0 + 32 * wc + 8 * b + 2 * (lane & 3) + e;
+        if (gj < N) o[gi * ldo + gj] = acc[a][b][e];
+      }
   }
 }
 
