@@ -271,6 +271,10 @@ __device__ __forceinline__ double reduce_scalar(const double* parts, int n, bool
   return is_min ? warp_min(s) : warp_sum(s);
 }
 
+// (Dealing the 4-row blocks over the CTAs first -- one working warp per SM in a phase with few
+// rows -- made the column sweep faster (C3 U 5.5 -> 3.8 us) but the partial sums slower
+// (C2 U 6.3 -> 18.4 us, one warp per SM exposes every L2 round trip): 89 -> 107 us per C2 sweep,
+// rejected.  Warps without rows now skip the sweep instead of running it on zeros.)
 // (A lane-per-row form -- 32 rows per warp, rows k-major in shared memory, the column sweep
 // blocked left-looking with 16 residuals in registers -- was built and measured: the sweep part
 // took 14.7 / 6.5 / 4.7 us at C2 / C3 / C4 against 9.5 / 5.6 / 3.6 us here, one warp bound by
@@ -279,7 +283,7 @@ __device__ __forceinline__ double reduce_scalar(const double* parts, int n, bool
 // Gauss-Seidel column sweep U_ik <- max(0, U_ik + (C_ik - sum_l U_il G_lk) / G_kk)
 // (PAPER.md:322-324), F written in fp32; per-CTA partial Gram of the written rows, optional
 // partial <C, F_new>, partial min.  Gs: the Gram in shared memory; Ss: kW x kRB x RP doubles.
-template <int CPL>
+template <int CPL, bool DBG>
 __device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, int r,
                                            const double* pp, int ksplit, const double* G,
                                            double* gpart, double* crosspart, double* minpart,
@@ -287,7 +291,9 @@ __device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, 
                                            unsigned long long* dbg) {
   constexpr int RP = 32 * CPL;
   auto hstamp = [&](int i) {               // ENMF_SMALL_DEBUG: phase-internal times of CTA 0
-    if (dbg && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg[i]));
+    if constexpr (DBG) {
+      if (dbg && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg[i]));
+    }
   };
   hstamp(0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -308,6 +314,7 @@ __device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, 
     for (int64_t base = (int64_t)blockIdx.x * kW; base < nblk; base += (int64_t)gridDim.x * kW) {
       const int64_t rb = base + warp;
       double u[kRB][CPL], t[kRB][CPL];
+      if (rb < nblk) {                              // (a warp without rows only zeroes its slot)
       // C rows of this warp: kRB consecutive rows are ONE contiguous span of cnt = rows * r
       // doubles in every K-chunk partial, so the lanes sum it flat (coalesced, 4 CPL loads in
       // flight per chunk, chunk order fixed) and scatter the sums into the warp's Cw[b][col]
@@ -376,6 +383,7 @@ __device__ __forceinline__ void hals_phase(float* F, int64_t ldf, int64_t rows, 
             for (int c = 0; c < CPL; ++c) t[b][c] = fma(-d, gk[c], t[b][c]);
           }
         }
+      }
       }
       hstamp(4);
       // write the rows (fp32: the state), keep their rounded values for the Gram partial
@@ -479,7 +487,7 @@ __device__ __forceinline__ void objective_append(const SmallArgs& a, double cros
   __syncthreads();
 }
 
-template <int CPL, int RCOLS>
+template <int CPL, int RCOLS, bool DBG>
 __global__ void __launch_bounds__(kT, CPL <= 2 ? 2 : 1) small_hals_kernel(SmallArgs a) {
   constexpr int RP = 32 * CPL;
   extern __shared__ double smem[];
@@ -505,14 +513,16 @@ __global__ void __launch_bounds__(kT, CPL <= 2 ? 2 : 1) small_hals_kernel(SmallA
   double* minp = a.sc + G;
   double* scal = a.sc + 2 * G;               // [0] cross, [1] min U, [2] min V
   unsigned long long tl[6] = {0, 0, 0, 0, 0, 0}, hu[8] = {0}, hv[8] = {0};
-  const bool dbg0 = a.debug && blockIdx.x == 0;
+  const bool dbg0 = DBG && a.debug && blockIdx.x == 0;
   auto stamp = [&](int i) {
-    if (a.debug && blockIdx.x == 0 && threadIdx.x == 0)
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl[i]));
+    if constexpr (DBG) {
+      if (a.debug && blockIdx.x == 0 && threadIdx.x == 0)
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl[i]));
+    }
   };
   unsigned long long gt0 = 0;
   long long ck0 = 0;
-  if (dbg0 && threadIdx.x == 0) {
+  if (DBG && dbg0 && threadIdx.x == 0) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
     ck0 = clock64();
   }
@@ -536,7 +546,7 @@ __global__ void __launch_bounds__(kT, CPL <= 2 ? 2 : 1) small_hals_kernel(SmallA
     stamp(1);
     // ---- A': (objective of the previous sweep;) HALS on U
     if (t > 0 && blockIdx.x == gridDim.x - 1) objective_append(a, scal[0], red);
-    hals_phase<CPL>(a.U, a.ldu, a.m, r, a.pp, a.ksA, a.GV, a.gp + (int64_t)blockIdx.x * r * r,
+    hals_phase<CPL, DBG>(a.U, a.ldu, a.m, r, a.pp, a.ksA, a.GV, a.gp + (int64_t)blockIdx.x * r * r,
                     nullptr, minp, Gs, Ss, ginv, red, dbg0 ? hu : nullptr);
     grid_sync();
     stamp(2);
@@ -550,22 +560,22 @@ __global__ void __launch_bounds__(kT, CPL <= 2 ? 2 : 1) small_hals_kernel(SmallA
     grid_sync();
     stamp(3);
     // ---- B': HALS on V with the cross-term partial <Q, V_new>
-    hals_phase<CPL>(a.V, a.ldv, a.n, r, a.pp, a.ksB, a.GU, a.gp + (int64_t)blockIdx.x * r * r,
+    hals_phase<CPL, DBG>(a.V, a.ldv, a.n, r, a.pp, a.ksB, a.GU, a.gp + (int64_t)blockIdx.x * r * r,
                     crossp, minp, Gs, Ss, ginv, red, dbg0 ? hv : nullptr);
     grid_sync();
     stamp(4);
   }
-  if (a.debug && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (DBG && a.debug && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long gt1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
     printf("  SM clock %.0f MHz over %d sweeps\n", 1e3 * (double)(clock64() - ck0) / (double)(gt1 - gt0),
            a.count);
   }
-  if (a.debug && blockIdx.x == 0 && threadIdx.x == 0)
+  if (DBG && a.debug && blockIdx.x == 0 && threadIdx.x == 0)
     printf("small_hals grid %d ksA %d kcA %d ksB %d kcB %d: A %llu (own work %llu) A' %llu B %llu B' %llu ns\n",
            G, a.ksA, (int)a.kcA, a.ksB, (int)a.kcB, tl[1] - tl[0], tl[5] - tl[0], tl[2] - tl[1],
            tl[3] - tl[2], tl[4] - tl[3]);
-  if (a.debug && blockIdx.x == 0 && threadIdx.x == 0)
+  if (DBG && a.debug && blockIdx.x == 0 && threadIdx.x == 0)
     printf("  CTA 0 HALS U: gram %llu partials %llu uG %llu sweep %llu write %llu Gpart %llu tail %llu | "
            "V: gram %llu partials %llu uG %llu sweep %llu write %llu Gpart %llu tail %llu ns\n",
            hu[1] - hu[0], hu[2] - hu[1], hu[3] - hu[2], hu[4] - hu[3], hu[5] - hu[4], hu[6] - hu[5],
@@ -635,9 +645,15 @@ struct Plan {
   const void* fn = nullptr;
 };
 
+bool timeline_requested() {                 // ENMF_SMALL_DEBUG=1: the instrumented instantiation
+  const char* dbg = getenv("ENMF_SMALL_DEBUG");
+  return dbg && dbg[0] == '1';
+}
+
 template <int CPL, int RCOLS>
 bool make_plan_t(int64_t m, int64_t n, Plan* p) {
-  auto k = small_hals_kernel<CPL, RCOLS>;
+  auto k = timeline_requested() ? small_hals_kernel<CPL, RCOLS, true>
+                                : small_hals_kernel<CPL, RCOLS, false>;
   const size_t sm = smem_bytes<CPL, RCOLS>();
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
     cudaGetLastError();
@@ -708,8 +724,7 @@ int small_sweeps_launch(const float* X, int64_t ldx, int64_t m, int64_t n, int r
   a.bar = reinterpret_cast<unsigned*>(a.sc + 2 * (size_t)p.grid + 8);
   a.ksA = p.ksA; a.ksB = p.ksB; a.kcA = p.kcA; a.kcB = p.kcB;
   a.count = count;
-  const char* dbg = getenv("ENMF_SMALL_DEBUG");
-  a.debug = dbg && dbg[0] == '1';
+  a.debug = timeline_requested() ? 1 : 0;
   // (the barrier counter advances by 4 grid sizes per sweep: launches of <= 2^18 sweeps)
   for (int done = 0; done < count; done += 1 << 18) {
     a.count = count - done < (1 << 18) ? count - done : 1 << 18;
