@@ -25,7 +25,8 @@
  *   - Errors: every call returns an enmf_status_t; nothing throws across the ABI.  After
  *     ENMF_ERR_CUDA / ENMF_ERR_NCCL the handle must be destroyed.
  *   - The handle owns every workspace (allocated in enmf_create / enmf_set_data), so
- *     enmf_iterate performs no allocation.
+ *     enmf_iterate performs no allocation -- except, once per handle, the workspace of the
+ *     stage it first runs (PBCD state, the cache-resident HALS kernel; see enmf_iterate).
  */
 #ifndef ENMF_H
 #define ENMF_H
