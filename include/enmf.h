@@ -25,8 +25,8 @@
  *   - Errors: every call returns an enmf_status_t; nothing throws across the ABI.  After
  *     ENMF_ERR_CUDA / ENMF_ERR_NCCL the handle must be destroyed.
  *   - The handle owns every workspace (allocated in enmf_create / enmf_set_data), so
- *     enmf_iterate performs no allocation -- except, once per handle, the workspace of the
- *     stage it first runs (PBCD state, the cache-resident HALS kernel; see enmf_iterate).
+ *     enmf_iterate performs no allocation -- except, once per handle, the PBCD state of the
+ *     ascent stage it first runs.
  */
 #ifndef ENMF_H
 #define ENMF_H
@@ -254,8 +254,8 @@ enmf_status_t enmf_get_stage(enmf_handle_t h, int* stage, double* lambda_u, doub
  * BASELINE configurations): every HALS sweep runs in one persistent
  * cooperative kernel (all remaining sweeps of the call in one launch), the ascent sweeps as
  * a CUDA graph each with a host check of the stage in between; the result does not depend
- * on how the caller chunks its calls.  The first such call allocates that kernel's
- * workspace (ENMF_ERR_OOM if it does not fit).  ENMF_SMALL_FUSED=0 in the environment keeps
+ * on how the caller chunks its calls.  That kernel's workspace is allocated when X is bound
+ * (enmf_set_data / enmf_init).  ENMF_SMALL_FUSED=0 in the environment keeps
  * the separate launches (the path the multi-rank handle runs). */
 enmf_status_t enmf_iterate(enmf_handle_t h, float* U, int64_t ldu, float* V, int64_t ldv,
                            int n_iters, double* f_trace_host, enmf_iter_info_t* info_host);

@@ -831,6 +831,14 @@ enmf_status_t enmf_set_data(enmf_handle_t h, const float* X, int64_t ldx) {
   h->umax_valid = h->vmax_valid = false;
   h->step_warm[0] = h->step_warm[1] = false;
   h->precision = prec;
+  // cache-resident problems: the persistent HALS kernel's plan (module load, occupancy) and
+  // workspace now, not inside the first enmf_iterate
+  const char* se = getenv("ENMF_SMALL_FUSED");
+  if (prec == ENMF_PREC_FP64 && !h->sharded && !(se && se[0] == '0') && !h->small_ws &&
+      small_sweeps_supported(h->m_loc, h->n, (int)h->r)) {
+    const size_t need = small_sweeps_workspace(h->m_loc, h->n, (int)h->r);
+    if (need) ENMF_TRY(dalloc(&h->small_ws, need));
+  }
   int zero[I_COUNT] = {0};
   CUDA_TRY(cudaMemcpyAsync(h->dint, zero, sizeof(zero), cudaMemcpyHostToDevice, h->st));
   CUDA_TRY(cudaStreamSynchronize(h->st));
